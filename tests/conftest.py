@@ -1,0 +1,68 @@
+"""Shared fixtures: golden-vector loading, the oracle, and the gpu marker."""
+
+from __future__ import annotations
+
+import glob
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+
+
+def golden_names(prefix: str) -> list[str]:
+    return sorted(os.path.basename(p)[len(prefix) + 1:-4] for p in glob.glob(os.path.join(GOLDEN, f"{prefix}_*.npz")))
+
+
+def load_golden(prefix: str, name: str):
+    return np.load(os.path.join(GOLDEN, f"{prefix}_{name}.npz"), allow_pickle=False)
+
+
+def slices_of(task_id: np.ndarray, order: np.ndarray) -> list[np.ndarray]:
+    """Task slices in task order, each in the order the reference received them."""
+    T = int(task_id.max()) + 1
+    return [order[task_id[order] == t].astype(np.int64) for t in range(T)]
+
+
+def search_case(name: str) -> dict:
+    g = load_golden("search", name)
+    return {
+        "values": g["values"], "y": g["y"], "slices": slices_of(g["task_id"], g["order"]),
+        "n": int(g["n"]), "keep": int(g["keep"]), "precision": str(g["precision"]),
+        "exp_indices": g["exp_indices"], "exp_score": g["exp_score"], "exp_coef": g["exp_coef"],
+        "exp_rmse": g["exp_rmse"], "all_scores": g["all_scores"] if "all_scores" in g else None,
+    }
+
+
+def bits_equal(a, b) -> bool:
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+    if a.shape != b.shape:
+        return False
+    # NaN payloads may differ; compare NaN-ness, then exact bits elsewhere
+    na, nb = np.isnan(a), np.isnan(b)
+    if not np.array_equal(na, nb):
+        return False
+    return np.array_equal(a[~na].view(np.int64), b[~nb].view(np.int64))
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    from oracle import oracle as orc
+
+    orc.build()
+    return orc
+
+
+@pytest.fixture()
+def rng():
+    return np.random.default_rng(20260822)
