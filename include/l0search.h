@@ -1,0 +1,149 @@
+/*
+ * l0search.h -- C ABI of the B200-native SO / l0 descriptor search.
+ *
+ * The reference (descsearch 0.1.0, /root/reference/pkg) is a Python package
+ * whose only native code is four numba kernels; it has no FFI.  Its operator
+ * boundary for this path is the Python function
+ *
+ *     descsearch.search.l0_search(subspace, property_values, task_slices,
+ *                                 config, workers, task_labels, stats)
+ *                                                      search.py:202-322
+ *
+ * and its companions fit_tuple (search.py:136-171) and the kernels
+ * score_tuples / fit_tuple_kernel / fill_combinations (lsq.py:113-215).
+ * The Python host package paper_2502_20072_b200 mirrors that API and binds
+ * the entry points below with ctypes.
+ *
+ * Conventions:
+ *   - every function returns an int status (L0S_OK == 0); l0s_last_error()
+ *     gives a per-thread message for the last failure;
+ *   - the caller owns every in/out buffer; the context owns device memory,
+ *     streams and events;
+ *   - a context is bound to one CUDA device and is not thread-safe; calls
+ *     block until their results are in the caller's buffers.
+ *   - no CPU fallback: without a usable sm_100 device l0s_create fails with
+ *     L0S_ENODEV.
+ */
+#ifndef L0SEARCH_H
+#define L0SEARCH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define L0S_OK 0
+#define L0S_EINVAL 1    /* maps to ValueError                          */
+#define L0S_ECAPACITY 2 /* maps to descsearch.errors.CapacityError      */
+#define L0S_ECUDA 3     /* maps to RuntimeError                         */
+#define L0S_ENOMEM 4    /* device allocation failed -> RuntimeError     */
+#define L0S_ENODEV 5    /* no usable B200 / sm_100 device              */
+#define L0S_ESTATE 6    /* call order violated (e.g. search before stage) */
+
+#define L0S_PREC_FP64 0
+#define L0S_PREC_FP32 1
+
+/* search modes (l0s_search 'mode') */
+#define L0S_MODE_AUTO 0  /* screened Gram path when it applies, exact otherwise   */
+#define L0S_MODE_FAST 1  /* force the screened Gram path (n in {2,3,4}, T <= 8)   */
+#define L0S_MODE_EXACT 2 /* score every tuple with the bit-exact Householder kernel */
+
+typedef struct l0s_ctx l0s_ctx;
+
+/* Throughput / diagnostics bookkeeping (superset of search.SearchStats, search.py:45-56). */
+typedef struct {
+    int64_t n_tuples;        /* tuples in [rank_begin, rank_end)                      */
+    double ms_total;         /* device time of the whole search (events)              */
+    double ms_fit;           /* screened fit kernel(s)                                */
+    double ms_exact;         /* bit-exact kernels (refit / ill / exact mode)          */
+    double ms_gram;          /* stage + Gram, set by l0s_stage                        */
+    double theta;            /* final global screening threshold                      */
+    int64_t n_candidates;    /* screened candidates refit exactly                     */
+    int64_t n_ill;           /* tuples routed to the exact kernel by conditioning     */
+    int64_t n_rescan;        /* certification rescans                                 */
+    int64_t n_fit_launches;  /* kernel launches of the screened fit                   */
+    int64_t n_launches;      /* all kernel launches of this search                    */
+    int32_t mode_used;       /* L0S_MODE_FAST or L0S_MODE_EXACT                       */
+    int32_t certified;       /* 1 when the top-k set is proven exact                  */
+    double margin;           /* lb(K')-th minus k-th exact score at certification     */
+} l0s_stats;
+
+const char *l0s_last_error(void);
+int l0s_version(void);
+
+/* Device discovery: number of CUDA devices (0 when none). */
+int l0s_device_count(int *count);
+
+/* Context on one device (replaces the per-call thread pool of search.py:258-301). */
+int l0s_create(int device, l0s_ctx **out);
+int l0s_destroy(l0s_ctx *ctx);
+
+/*
+ * Stage one problem on the device (replaces search._prepare, search.py:113-127,
+ * and adds the Gram precompute).
+ *   values : (m, s) float64, row-major, samples in the caller's original order
+ *   y      : (s,)   float64
+ *   perm   : (s,)   int64, concatenation of the task slices in task order
+ *   bounds : (ntasks+1,) int64 task boundaries on the permuted axis
+ *   precision : L0S_PREC_FP64 / L0S_PREC_FP32 (values and y are rounded to
+ *            float32 first, as _prepare does, search.py:125-126)
+ *   is_device : 1 when values / y / perm are device pointers on this context's device
+ * The Gram (normalized, per-task centered, fp64 DMMA) is built here.
+ */
+int l0s_stage(l0s_ctx *ctx, const double *values, int64_t m, int64_t s, const double *y,
+              const int64_t *perm, const int64_t *bounds, int ntasks, int precision,
+              int is_device);
+
+/*
+ * Exhaustive search over tuple ranks [rank_begin, rank_end) of C(m, n)
+ * (search.l0_search's scan + merge, search.py:233-304).  Writes the best
+ * min(keep, #finite) tuples ordered by (score, rank); scores and ssr are
+ * bit-identical to the reference's score_tuples / fit_tuple_kernel.
+ *   out_scores : (keep,) float64   score = sum_task ssr / s (lsq.py:153-156)
+ *   out_ranks  : (keep,) int64
+ *   out_coef   : (keep, ntasks, n+1) float64 (working-dtype values widened)
+ *   out_ssr    : (keep, ntasks) float64
+ *   out_count  : number written
+ */
+int l0s_search(l0s_ctx *ctx, int n, int64_t keep, int64_t rank_begin, int64_t rank_end,
+               int mode, double *out_scores, int64_t *out_ranks, double *out_coef,
+               double *out_ssr, int64_t *out_count, l0s_stats *stats);
+
+/*
+ * Bit-exact fits of explicit tuples (fit_tuple_kernel, lsq.py:159-192, for
+ * many tuples at once).  tuples: (count, n) int64 strictly increasing.
+ *   out_ok    : (count,) int32
+ *   out_score : (count,) float64  score_tuples value (+inf when deficient)
+ *   out_coef  : (count, ntasks, n+1) float64;  out_ssr : (count, ntasks)
+ */
+int l0s_fit_tuples(l0s_ctx *ctx, int n, const int64_t *tuples, int64_t count, int32_t *out_ok,
+                   double *out_score, double *out_coef, double *out_ssr);
+
+/*
+ * Screened lower bounds for explicit tuples (diagnostics / tests): the value
+ * the fit kernel compares against its threshold, lb <= exact score, with
+ * flag bit0 = conditioning check passed, bit1 = reference rank rule certain.
+ */
+int l0s_screen_tuples(l0s_ctx *ctx, int n, const int64_t *tuples, int64_t count, double *out_lb,
+                      int32_t *out_flags);
+
+/* Copy of the staged normalized Gram of one task ((m+1) x (m+1), last row/col = y). */
+int l0s_get_gram(l0s_ctx *ctx, int task, double *out);
+
+/* Unranking helpers on the device's binomial table (search.py:66-104). */
+int l0s_unrank(int64_t rank, int64_t m, int n, int64_t *out_tuple);
+int l0s_rank(const int64_t *tuple, int64_t m, int n, int64_t *out_rank);
+int l0s_count(int64_t m, int n, int64_t *out_count); /* C(m,n); L0S_ECAPACITY if >= 2^63 */
+
+/* Microbenchmarks used by bench.py for the roofline denominator. */
+int l0s_fp64_peak(l0s_ctx *ctx, double *out_tflops);
+/* Worst relative error of the screen's fast reciprocal over `count` hashed doubles
+ * (the screen assumes <= 2^-17; tests/test_gpu_kernels.py checks it). */
+int l0s_rcp_check(int64_t count, double *out_max_rel);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* L0SEARCH_H */

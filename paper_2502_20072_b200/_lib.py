@@ -1,0 +1,218 @@
+"""ctypes binding of libl0search.so (include/l0search.h).
+
+The shared library is built in-tree (``python -m paper_2502_20072_b200.build``
+or ``__graft_entry__.build()``).  There is no CPU fallback: if the library or
+a B200 device is missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from . import _compat
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libl0search.so")
+
+L0S_OK, L0S_EINVAL, L0S_ECAPACITY, L0S_ECUDA, L0S_ENOMEM, L0S_ENODEV, L0S_ESTATE = range(7)
+PREC = {"fp64": 0, "fp32": 1}
+MODES = {"auto": 0, "fast": 1, "exact": 2}
+
+# every symbol include/l0search.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "l0s_last_error", "l0s_version", "l0s_device_count", "l0s_create", "l0s_destroy", "l0s_stage",
+    "l0s_search", "l0s_fit_tuples", "l0s_screen_tuples", "l0s_get_gram", "l0s_unrank", "l0s_rank",
+    "l0s_count", "l0s_fp64_peak", "l0s_rcp_check",
+)
+
+
+class Stats(ctypes.Structure):
+    """Mirror of l0s_stats."""
+
+    _fields_ = [
+        ("n_tuples", ctypes.c_int64),
+        ("ms_total", ctypes.c_double),
+        ("ms_fit", ctypes.c_double),
+        ("ms_exact", ctypes.c_double),
+        ("ms_gram", ctypes.c_double),
+        ("theta", ctypes.c_double),
+        ("n_candidates", ctypes.c_int64),
+        ("n_ill", ctypes.c_int64),
+        ("n_rescan", ctypes.c_int64),
+        ("n_fit_launches", ctypes.c_int64),
+        ("n_launches", ctypes.c_int64),
+        ("mode_used", ctypes.c_int32),
+        ("certified", ctypes.c_int32),
+        ("margin", ctypes.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load and type the shared library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2502_20072_b200.build` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        P = ctypes.POINTER
+        L.l0s_last_error.restype = ctypes.c_char_p
+        L.l0s_last_error.argtypes = []
+        L.l0s_version.restype = i32
+        L.l0s_device_count.argtypes = [P(i32)]
+        L.l0s_create.argtypes = [i32, P(vp)]
+        L.l0s_destroy.argtypes = [vp]
+        L.l0s_stage.argtypes = [vp, vp, i64, i64, vp, vp, vp, i32, i32, i32]
+        L.l0s_search.argtypes = [vp, i32, i64, i64, i64, i32, vp, vp, vp, vp, P(i64), P(Stats)]
+        L.l0s_fit_tuples.argtypes = [vp, i32, vp, i64, vp, vp, vp, vp]
+        L.l0s_screen_tuples.argtypes = [vp, i32, vp, i64, vp, vp]
+        L.l0s_get_gram.argtypes = [vp, i32, vp]
+        L.l0s_unrank.argtypes = [i64, i64, i32, vp]
+        L.l0s_rank.argtypes = [vp, i64, i32, P(i64)]
+        L.l0s_count.argtypes = [i64, i32, P(i64)]
+        L.l0s_fp64_peak.argtypes = [vp, P(dbl)]
+        L.l0s_rcp_check.argtypes = [i64, P(dbl)]
+        for name in EXPORTS:
+            if name not in ("l0s_last_error",):
+                getattr(L, name).restype = i32
+        _lib = L
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map an l0s status to the reference's exception types."""
+    if rc == L0S_OK:
+        return
+    msg = lib().l0s_last_error().decode(errors="replace")
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == L0S_EINVAL:
+        raise ValueError(msg)
+    if rc == L0S_ECAPACITY:
+        raise _compat.CapacityError(msg)
+    raise RuntimeError(f"l0search error {rc}: {msg}")
+
+
+def ptr(a: np.ndarray) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class Engine:
+    """One device context (owns device memory, a stream and events)."""
+
+    def __init__(self, device: int = 0):
+        L = lib()
+        h = ctypes.c_void_p()
+        check(L.l0s_create(int(device), ctypes.byref(h)), "l0s_create")
+        self.handle = h
+        self.device = device
+        self.staged_key = None
+
+    def close(self):
+        if self.handle:
+            lib().l0s_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def stage(self, values: np.ndarray, y: np.ndarray, perm: np.ndarray, bounds: np.ndarray, precision: str,
+              device_ptrs: tuple | None = None) -> None:
+        """Host arrays (or, with device_ptrs=(values, y, perm) data pointers, device-resident inputs)."""
+        bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+        m, s = values.shape if device_ptrs is None else (values[0], values[1])
+        if device_ptrs is None:
+            values = np.ascontiguousarray(values, dtype=np.float64)
+            y = np.ascontiguousarray(y, dtype=np.float64)
+            perm = np.ascontiguousarray(perm, dtype=np.int64)
+            args = (ptr(values), m, s, ptr(y), ptr(perm))
+            is_dev = 0
+        else:
+            args = (ctypes.c_void_p(device_ptrs[0]), m, s, ctypes.c_void_p(device_ptrs[1]),
+                    ctypes.c_void_p(device_ptrs[2]))
+            is_dev = 1
+        check(lib().l0s_stage(self.handle, *args, ptr(bounds), bounds.shape[0] - 1, PREC[precision], is_dev),
+              "l0s_stage")
+        self.m, self.s, self.T = int(m), int(s), bounds.shape[0] - 1
+
+    def search(self, n: int, keep: int, rank_begin: int = 0, rank_end: int = 2**63 - 1, mode: str = "auto"):
+        keep = int(keep)
+        scores = np.zeros(keep, dtype=np.float64)
+        ranks = np.zeros(keep, dtype=np.int64)
+        coef = np.zeros((keep, self.T, n + 1), dtype=np.float64)
+        ssr = np.zeros((keep, self.T), dtype=np.float64)
+        cnt = ctypes.c_int64(0)
+        st = Stats()
+        check(lib().l0s_search(self.handle, n, keep, int(rank_begin), int(rank_end), MODES[mode], ptr(scores),
+                               ptr(ranks), ptr(coef), ptr(ssr), ctypes.byref(cnt), ctypes.byref(st)), "l0s_search")
+        k = cnt.value
+        return scores[:k], ranks[:k], coef[:k], ssr[:k], st
+
+    def fit_tuples(self, tuples: np.ndarray):
+        tuples = np.ascontiguousarray(tuples, dtype=np.int64)
+        count, n = tuples.shape
+        ok = np.zeros(count, dtype=np.int32)
+        score = np.zeros(count, dtype=np.float64)
+        coef = np.zeros((count, self.T, n + 1), dtype=np.float64)
+        ssr = np.zeros((count, self.T), dtype=np.float64)
+        check(lib().l0s_fit_tuples(self.handle, n, ptr(tuples), count, ptr(ok), ptr(score), ptr(coef), ptr(ssr)),
+              "l0s_fit_tuples")
+        return ok.astype(bool), score, coef, ssr
+
+    def screen_tuples(self, tuples: np.ndarray):
+        tuples = np.ascontiguousarray(tuples, dtype=np.int64)
+        count, n = tuples.shape
+        lb = np.zeros(count, dtype=np.float64)
+        flags = np.zeros(count, dtype=np.int32)
+        check(lib().l0s_screen_tuples(self.handle, n, ptr(tuples), count, ptr(lb), ptr(flags)), "l0s_screen_tuples")
+        return lb, flags
+
+    def gram(self, task: int = 0) -> np.ndarray:
+        out = np.zeros((self.m + 1, self.m + 1), dtype=np.float64)
+        check(lib().l0s_get_gram(self.handle, task, ptr(out)), "l0s_get_gram")
+        return out
+
+    def fp64_peak(self) -> float:
+        v = ctypes.c_double(0.0)
+        check(lib().l0s_fp64_peak(self.handle, ctypes.byref(v)), "l0s_fp64_peak")
+        return v.value
+
+
+_engines: dict[int, Engine] = {}
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    lib().l0s_device_count(ctypes.byref(n))
+    return n.value
+
+
+def engine(device: int | None = None) -> Engine:
+    """Process-wide engine per device (LOCAL_RANK or 0 by default)."""
+    if device is None:
+        device = int(os.environ.get("L0S_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    eng = _engines.get(device)
+    if eng is None or eng.handle is None:
+        eng = Engine(device)
+        _engines[device] = eng
+    return eng

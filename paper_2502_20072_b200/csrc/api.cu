@@ -1,0 +1,736 @@
+// api.cu -- the C ABI (include/l0search.h): context, staging, search orchestration.
+//
+// Search = screened fit kernel over every tuple (fit3.cu) -> device merge of
+// the per-warp top-K' lists (merge.cu) -> bit-exact Householder refit of the
+// candidates and of every tuple the screen could not certify (exact.cu) ->
+// (score, rank) order, certification, optional threshold rescan.  See
+// DESIGN.md for the proof obligations behind "certified".
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/l0search.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace l0s;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(x)                                                                                    \
+    do {                                                                                         \
+        cudaError_t e_ = (x);                                                                    \
+        if (e_ != cudaSuccess) return fail(L0S_ECUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+struct DBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= n && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        cudaError_t e = cudaMalloc(&p, bytes < 256 ? 256 : bytes);
+        if (e == cudaSuccess) n = bytes < 256 ? 256 : bytes;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return (T*)p;
+    }
+};
+
+// C(a, b) with 128-bit intermediates, saturated at INT64_MAX
+int64_t binom_sat(int64_t a, int64_t b) {
+    if (b < 0 || a < 0 || b > a) return 0;
+    if (b > a - b) b = a - b;
+    unsigned __int128 r = 1;
+    for (int64_t i = 1; i <= b; ++i) {
+        r = r * (unsigned __int128)(a - b + i) / (unsigned __int128)i;
+        if (r > (unsigned __int128)INT64_MAX) return INT64_MAX;
+    }
+    return (int64_t)r;
+}
+
+}  // namespace
+
+struct l0s_ctx {
+    int dev = 0, nsm = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // staged problem
+    bool staged = false;
+    int64_t m = 0, s = 0, mp = 0, sp = 0, ld = 0;
+    int T = 0, prec = 0;
+    std::vector<int64_t> bounds_h, zoff_h, rpad_h;
+    std::vector<double> rows_h, eta_h, yyu_h;
+    double ms_gram = 0.0;
+    DBuf in_values, in_y, in_perm, bounds_d, zoff_d, Xp, yp, Z, G, qf, un2, yyu, rowsd, eta_d;
+    // binomial table (k <= binom_n) x (a <= m)
+    DBuf binom;
+    int binom_n = -1;
+    int64_t binom_m = -1;
+    // search workspace
+    DBuf units, ucount, theta_g, wl_lb, wl_rank, wl_cnt, ill, ill_cnt, cand_lb, cand_rank, cand_cnt, sort_tmp,
+        lb_tmp, rank_tmp, coll_lb, coll_rank, coll_cnt;
+    DBuf ex_scratch, ex_ssr_tmp, ex_ok_tmp, ex_ok, ex_score, ex_coef, ex_ssr, ex_ranks, ex_tuples;
+    std::vector<int4> units_h;
+    int64_t units_key[5] = {-1, -1, -1, -1, -1};
+
+    ~l0s_ctx() {
+        DBuf* all[] = {&in_values, &in_y, &in_perm, &bounds_d, &zoff_d, &Xp, &yp, &Z, &G, &qf, &un2, &yyu, &rowsd,
+                       &eta_d, &binom, &units, &ucount, &theta_g, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
+                       &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
+                       &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
+                       &ex_ranks, &ex_tuples};
+        for (DBuf* b : all) b->release();
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
+namespace {
+
+int ensure_binom(l0s_ctx* c, int n) {
+    int need = std::max(n, 3);
+    if (c->binom_n >= need && c->binom_m == c->m) return L0S_OK;
+    std::vector<int64_t> tab((size_t)(need + 1) * (size_t)(c->m + 1));
+    for (int k = 0; k <= need; ++k)
+        for (int64_t a = 0; a <= c->m; ++a) tab[(size_t)k * (c->m + 1) + a] = binom_sat(a, k);
+    CK(c->binom.ensure(tab.size() * sizeof(int64_t)));
+    CK(cudaMemcpyAsync(c->binom.p, tab.data(), tab.size() * sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+    c->binom_n = need;
+    c->binom_m = c->m;
+    return L0S_OK;
+}
+
+struct ExactOut {
+    std::vector<int32_t> ok;
+    std::vector<double> score;
+};
+
+// Bit-exact scores (and optionally coef/ssr) for `count` tuples given by device ranks or device tuples.
+int run_exact(l0s_ctx* c, int n, const int64_t* ranks_d, const int64_t* tuples_d, int64_t count, bool want_coef,
+              int64_t* launches) {
+    const int p = n + 1;
+    size_t wsz = c->prec == L0S_PREC_FP32 ? 4 : 8;
+    // scratch budget: <= 1 GiB of interleaved systems
+    int64_t per_sys = (int64_t)(p + 1) * std::max<int64_t>(c->ld, 1) * (int64_t)wsz;
+    int64_t budget = (int64_t)1 << 30;
+    int64_t cap_thr = std::max<int64_t>(c->T, std::min<int64_t>(budget / per_sys, count * c->T));
+    cap_thr = std::max<int64_t>(cap_thr, 1);
+    CK(c->ex_scratch.ensure((size_t)(cap_thr * per_sys)));
+    CK(c->ex_ssr_tmp.ensure(sizeof(double) * (size_t)std::max<int64_t>(count * c->T, 1)));
+    CK(c->ex_ok_tmp.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(count * c->T, 1)));
+    CK(c->ex_ok.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(count, 1)));
+    CK(c->ex_score.ensure(sizeof(double) * (size_t)std::max<int64_t>(count, 1)));
+    CK(c->ex_ssr.ensure(sizeof(double) * (size_t)std::max<int64_t>(count * c->T, 1)));
+    if (want_coef) CK(c->ex_coef.ensure(sizeof(double) * (size_t)std::max<int64_t>(count * c->T * p, 1)));
+    ExactArgs a{};
+    a.Xp = c->Xp.p;
+    a.yp = c->yp.p;
+    a.bounds = c->bounds_d.as<int64_t>();
+    a.T = c->T;
+    a.m = c->m;
+    a.s = c->s;
+    a.n = n;
+    a.tol = c->prec == L0S_PREC_FP32 ? 1e-5 : 1e-10;  // RANK_TOL_FACTOR, lsq.py:23
+    a.precision = c->prec;
+    a.tuples = tuples_d;
+    a.ranks = ranks_d;
+    a.binom = c->binom.as<int64_t>();
+    a.count = count;
+    a.ok = c->ex_ok.as<int32_t>();
+    a.score = c->ex_score.as<double>();
+    a.coef = want_coef ? c->ex_coef.as<double>() : nullptr;
+    a.ssr = c->ex_ssr.as<double>();
+    a.scratch = c->ex_scratch.p;
+    a.scratch_threads = cap_thr;
+    a.ld = std::max<int64_t>(c->ld, 1);
+    launch_exact(a, c->ex_ssr_tmp.as<double>(), c->ex_ok_tmp.as<int32_t>(), c->st, launches);
+    CK(cudaGetLastError());
+    return L0S_OK;
+}
+
+struct Cand {
+    double score;
+    int64_t rank;
+};
+bool cand_less(const Cand& x, const Cand& y) { return x.score < y.score || (x.score == y.score && x.rank < y.rank); }
+
+__global__ void k_iota(int64_t* out, int64_t start, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = start + i;
+}
+
+// keep the best `keep` finite (score, rank) in `best` (sorted)
+void merge_best(std::vector<Cand>& best, const std::vector<Cand>& more, int64_t keep) {
+    for (const Cand& x : more)
+        if (std::isfinite(x.score)) best.push_back(x);
+    std::sort(best.begin(), best.end(), cand_less);
+    best.erase(std::unique(best.begin(), best.end(),
+                           [](const Cand& x, const Cand& y) { return x.rank == y.rank; }),
+               best.end());
+    if ((int64_t)best.size() > keep) best.resize((size_t)keep);
+}
+
+// Exact scores for device ranks [0, count) of c->ex_ranks; appends finite (score, rank) to out.
+int exact_ranks_to_host(l0s_ctx* c, int n, const int64_t* ranks_d, int64_t count, std::vector<Cand>& out,
+                        int64_t* launches) {
+    if (count <= 0) return L0S_OK;
+    int rc = run_exact(c, n, ranks_d, nullptr, count, false, launches);
+    if (rc) return rc;
+    std::vector<double> sc((size_t)count);
+    std::vector<int64_t> rk((size_t)count);
+    CK(cudaMemcpyAsync(sc.data(), c->ex_score.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(rk.data(), ranks_d, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    for (int64_t i = 0; i < count; ++i) out.push_back({sc[(size_t)i], rk[(size_t)i]});
+    return L0S_OK;
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* l0s_last_error(void) { return g_err.c_str(); }
+int l0s_version(void) { return 1; }
+
+int l0s_device_count(int* count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) n = 0;
+    *count = n;
+    return L0S_OK;
+}
+
+int l0s_create(int device, l0s_ctx** out) {
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return fail(L0S_ENODEV, "no CUDA device visible");
+    if (device < 0 || device >= n) return fail(L0S_EINVAL, "device %d out of range [0, %d)", device, n);
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(L0S_ENODEV, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
+    CK(cudaSetDevice(device));
+    l0s_ctx* c = new l0s_ctx();
+    c->dev = device;
+    c->nsm = prop.multiProcessorCount;
+    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return fail(L0S_ECUDA, "stream creation failed");
+    }
+    for (auto& e : c->ev) cudaEventCreate(&e);
+    *out = c;
+    return L0S_OK;
+}
+
+int l0s_destroy(l0s_ctx* c) {
+    if (!c) return L0S_OK;
+    cudaSetDevice(c->dev);
+    cudaStreamSynchronize(c->st);
+    delete c;
+    return L0S_OK;
+}
+
+int l0s_stage(l0s_ctx* c, const double* values, int64_t m, int64_t s, const double* y, const int64_t* perm,
+              const int64_t* bounds, int ntasks, int precision, int is_device) {
+    if (!c) return fail(L0S_EINVAL, "null context");
+    if (m < 1 || s < 1 || ntasks < 1) return fail(L0S_EINVAL, "need m >= 1, s >= 1, ntasks >= 1 (got %lld, %lld, %d)", (long long)m, (long long)s, ntasks);
+    if (precision != L0S_PREC_FP64 && precision != L0S_PREC_FP32) return fail(L0S_EINVAL, "bad precision %d", precision);
+    if (bounds[0] != 0 || bounds[ntasks] != s) return fail(L0S_EINVAL, "bounds must run from 0 to s");
+    for (int t = 0; t < ntasks; ++t)
+        if (bounds[t + 1] < bounds[t]) return fail(L0S_EINVAL, "bounds must be non-decreasing");
+    CK(cudaSetDevice(c->dev));
+    c->staged = false;
+    c->m = m;
+    c->s = s;
+    c->T = ntasks;
+    c->prec = precision;
+    c->mp = ((m + 1 + 32 + 63) / 64) * 64;
+    c->bounds_h.assign(bounds, bounds + ntasks + 1);
+    c->zoff_h.assign((size_t)ntasks + 1, 0);
+    c->rpad_h.assign((size_t)ntasks, 0);
+    c->rows_h.assign((size_t)ntasks, 0.0);
+    c->eta_h.assign((size_t)ntasks, 0.0);
+    c->ld = 0;
+    for (int t = 0; t < ntasks; ++t) {
+        int64_t r = bounds[t + 1] - bounds[t];
+        c->rpad_h[t] = ((r + 7) / 8) * 8;
+        c->zoff_h[t + 1] = c->zoff_h[t] + c->rpad_h[t];
+        c->rows_h[t] = (double)r;
+        // per-entry bound on the normalized Gram error (error model):
+        // dot products of length r over unit vectors (gamma_r) plus normalization
+        c->eta_h[t] = 4.0 * (double)(r + 8) * kEps;
+        c->ld = std::max(c->ld, r);
+    }
+    c->sp = std::max<int64_t>(c->zoff_h[ntasks], 8);
+    size_t wsz = precision == L0S_PREC_FP32 ? 4 : 8;
+    cudaEventRecord(c->ev[0], c->st);
+    const double *vd = values, *yd = y;
+    const int64_t* pd = perm;
+    if (!is_device) {
+        CK(c->in_values.ensure(sizeof(double) * m * s));
+        CK(c->in_y.ensure(sizeof(double) * s));
+        CK(c->in_perm.ensure(sizeof(int64_t) * s));
+        CK(cudaMemcpyAsync(c->in_values.p, values, sizeof(double) * m * s, cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(c->in_y.p, y, sizeof(double) * s, cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(c->in_perm.p, perm, sizeof(int64_t) * s, cudaMemcpyHostToDevice, c->st));
+        vd = c->in_values.as<double>();
+        yd = c->in_y.as<double>();
+        pd = c->in_perm.as<int64_t>();
+    }
+    CK(c->bounds_d.ensure(sizeof(int64_t) * (ntasks + 1)));
+    CK(c->zoff_d.ensure(sizeof(int64_t) * (ntasks + 1)));
+    CK(cudaMemcpyAsync(c->bounds_d.p, bounds, sizeof(int64_t) * (ntasks + 1), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->zoff_d.p, c->zoff_h.data(), sizeof(int64_t) * (ntasks + 1), cudaMemcpyHostToDevice, c->st));
+    CK(c->Xp.ensure(wsz * m * s));
+    CK(c->yp.ensure(wsz * s));
+    CK(c->Z.ensure(sizeof(double) * c->mp * c->sp));
+    CK(c->G.ensure(sizeof(double) * c->mp * c->mp * ntasks));
+    CK(c->qf.ensure(sizeof(double) * m * ntasks));
+    CK(c->un2.ensure(sizeof(double) * m * ntasks));
+    CK(c->yyu.ensure(sizeof(double) * ntasks));
+    CK(c->rowsd.ensure(sizeof(double) * ntasks));
+    CK(c->eta_d.ensure(sizeof(double) * ntasks));
+    CK(cudaMemcpyAsync(c->rowsd.p, c->rows_h.data(), sizeof(double) * ntasks, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->eta_d.p, c->eta_h.data(), sizeof(double) * ntasks, cudaMemcpyHostToDevice, c->st));
+    launch_gather(vd, yd, pd, m, s, precision, c->Xp.p, c->yp.p, c->st);
+    CK(cudaMemsetAsync(c->Z.p, 0, sizeof(double) * c->mp * c->sp, c->st));
+    launch_normalize(c->Xp.p, c->yp.p, precision, m, s, c->bounds_d.as<int64_t>(), c->zoff_d.as<int64_t>(), ntasks,
+                     c->sp, c->Z.as<double>(), c->qf.as<double>(), c->un2.as<double>(), c->yyu.as<double>(), c->st);
+    launch_gram(c->Z.as<double>(), c->sp, c->zoff_h.data(), c->rpad_h.data(), ntasks, m, c->mp, c->G.as<double>(),
+                c->st);
+    CK(cudaGetLastError());
+    cudaEventRecord(c->ev[1], c->st);
+    c->yyu_h.assign((size_t)ntasks, 0.0);
+    CK(cudaMemcpyAsync(c->yyu_h.data(), c->yyu.p, sizeof(double) * ntasks, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    c->ms_gram = elapsed(c->ev[0], c->ev[1]);
+    c->staged = true;
+    c->binom_m = -1;
+    return L0S_OK;
+}
+
+int l0s_count(int64_t m, int n, int64_t* out) {
+    if (n < 1 || m < 0) return fail(L0S_EINVAL, "need m >= 0 and n >= 1");
+    int64_t v = binom_sat(m, n);
+    if (v == INT64_MAX) return fail(L0S_ECAPACITY, "C(%lld, %d) exceeds the enumerable range", (long long)m, n);
+    *out = v;
+    return L0S_OK;
+}
+
+int l0s_unrank(int64_t rank, int64_t m, int n, int64_t* out) {
+    int64_t total;
+    int rc = l0s_count(m, n, &total);
+    if (rc) return rc;
+    if (rank < 0 || rank >= total) return fail(L0S_EINVAL, "rank %lld outside [0, %lld)", (long long)rank, (long long)total);
+    int64_t r = rank, e = 0;
+    for (int k = 0; k < n; ++k) {
+        int rem = n - k - 1;
+        for (;;) {
+            int64_t cc = binom_sat(m - 1 - e, rem);
+            if (r < cc) break;
+            r -= cc;
+            ++e;
+        }
+        out[k] = e++;
+    }
+    return L0S_OK;
+}
+
+int l0s_rank(const int64_t* tup, int64_t m, int n, int64_t* out) {
+    int64_t total;
+    int rc = l0s_count(m, n, &total);
+    if (rc) return rc;
+    int64_t prev = -1;
+    for (int k = 0; k < n; ++k) {
+        if (!(prev < tup[k] && tup[k] < m)) return fail(L0S_EINVAL, "tuple is not strictly increasing within range");
+        prev = tup[k];
+    }
+    // rank = C(m,n) - 1 - sum_k C(m-1-c_k, n-k)
+    int64_t acc = 0;
+    for (int k = 0; k < n; ++k) acc += binom_sat(m - 1 - tup[k], n - k);
+    *out = total - 1 - acc;
+    return L0S_OK;
+}
+
+int l0s_fit_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, int32_t* out_ok, double* out_score,
+                   double* out_coef, double* out_ssr) {
+    if (!c || !c->staged) return fail(L0S_ESTATE, "l0s_stage must be called first");
+    if (n < 1 || n > 15) return fail(L0S_EINVAL, "dimension %d outside [1, 15]", n);
+    if (count <= 0) return L0S_OK;
+    CK(cudaSetDevice(c->dev));
+    for (int64_t i = 0; i < count; ++i)
+        for (int k = 0; k < n; ++k) {
+            int64_t v = tuples[i * n + k];
+            if (v < 0 || v >= c->m || (k > 0 && v <= tuples[i * n + k - 1]))
+                return fail(L0S_EINVAL, "tuple %lld is not strictly increasing within [0, %lld)", (long long)i, (long long)c->m);
+        }
+    int rc = ensure_binom(c, n);
+    if (rc) return rc;
+    CK(c->ex_tuples.ensure(sizeof(int64_t) * count * n));
+    CK(cudaMemcpyAsync(c->ex_tuples.p, tuples, sizeof(int64_t) * count * n, cudaMemcpyHostToDevice, c->st));
+    rc = run_exact(c, n, nullptr, c->ex_tuples.as<int64_t>(), count, true, nullptr);
+    if (rc) return rc;
+    const int p = n + 1;
+    if (out_ok) CK(cudaMemcpyAsync(out_ok, c->ex_ok.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, c->st));
+    if (out_score) CK(cudaMemcpyAsync(out_score, c->ex_score.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->st));
+    if (out_coef) CK(cudaMemcpyAsync(out_coef, c->ex_coef.p, sizeof(double) * count * c->T * p, cudaMemcpyDeviceToHost, c->st));
+    if (out_ssr) CK(cudaMemcpyAsync(out_ssr, c->ex_ssr.p, sizeof(double) * count * c->T, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return L0S_OK;
+}
+
+static void fill_fit_common(l0s_ctx* c, FitArgs& a, int n) {
+    a.G = c->G.as<double>();
+    a.qf = c->qf.as<double>();
+    a.un2 = c->un2.as<double>();
+    a.rowsd = c->rowsd.as<double>();
+    a.eta = c->eta_d.as<double>();
+    a.binom = c->binom.as<int64_t>();
+    a.m = c->m;
+    a.mp = c->mp;
+    a.T = c->T;
+    a.N_total = binom_sat(c->m, n);
+    double tol = c->prec == L0S_PREC_FP32 ? 1e-5 : 1e-10;
+    a.tol2 = tol * tol;
+}
+
+int l0s_screen_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags) {
+    if (!c || !c->staged) return fail(L0S_ESTATE, "l0s_stage must be called first");
+    if (n != 3) return fail(L0S_EINVAL, "screened bounds are implemented for n = 3");
+    if (count <= 0) return L0S_OK;
+    CK(cudaSetDevice(c->dev));
+    int rc = ensure_binom(c, n);
+    if (rc) return rc;
+    FitArgs a{};
+    fill_fit_common(c, a, n);
+    CK(c->ex_tuples.ensure(sizeof(int64_t) * count * n));
+    CK(c->cand_lb.ensure(sizeof(double) * count));
+    CK(c->ex_ok.ensure(sizeof(int32_t) * count));
+    CK(cudaMemcpyAsync(c->ex_tuples.p, tuples, sizeof(int64_t) * count * n, cudaMemcpyHostToDevice, c->st));
+    launch_screen3(a, c->ex_tuples.as<int64_t>(), count, c->cand_lb.as<double>(), c->ex_ok.as<int32_t>(), c->st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out_lb, c->cand_lb.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(out_flags, c->ex_ok.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return L0S_OK;
+}
+
+int l0s_get_gram(l0s_ctx* c, int task, double* out) {
+    if (!c || !c->staged) return fail(L0S_ESTATE, "l0s_stage must be called first");
+    if (task < 0 || task >= c->T) return fail(L0S_EINVAL, "task out of range");
+    CK(cudaSetDevice(c->dev));
+    int64_t w = c->m + 1;
+    CK(cudaMemcpy2DAsync(out, sizeof(double) * w, c->G.as<double>() + (int64_t)task * c->mp * c->mp,
+                         sizeof(double) * c->mp, sizeof(double) * w, (size_t)w, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return L0S_OK;
+}
+
+// ---------------------------------------------------------------------------
+// the search
+// ---------------------------------------------------------------------------
+
+static int search_exact_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t re, std::vector<Cand>& best,
+                             l0s_stats* st) {
+    // every tuple through the bit-exact kernel, chunked; per chunk the device sorts the scores
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(re - rb, (int64_t)1 << 20));
+    CK(c->ex_ranks.ensure(sizeof(int64_t) * chunk));
+    CK(c->lb_tmp.ensure(sizeof(double) * chunk));
+    CK(c->rank_tmp.ensure(sizeof(int64_t) * chunk));
+    size_t tb = sort_pairs_temp_bytes(chunk);
+    CK(c->sort_tmp.ensure(tb));
+    for (int64_t r0 = rb; r0 < re; r0 += chunk) {
+        int64_t cnt = std::min(chunk, re - r0);
+        k_iota<<<(unsigned)((cnt + 255) / 256), 256, 0, c->st>>>(c->ex_ranks.as<int64_t>(), r0, cnt);
+        st->n_launches++;
+        int rc = run_exact(c, n, c->ex_ranks.as<int64_t>(), nullptr, cnt, false, &st->n_launches);
+        if (rc) return rc;
+        // sort (score, rank) on device; non-finite scores sort last (ord_enc maps +inf above all finite)
+        sort_pairs(c->ex_score.as<double>(), c->ex_ranks.as<int64_t>(), c->lb_tmp.as<double>(),
+                   c->rank_tmp.as<int64_t>(), cnt, c->sort_tmp.p, tb, c->st);
+        st->n_launches += 3;
+        // the radix sort is stable and the ranks enter in increasing order, so the first
+        // `keep` entries are the chunk's best by (score, rank); non-finite scores sort last
+        int64_t take = std::min<int64_t>(cnt, keep);
+        std::vector<double> sc((size_t)take);
+        std::vector<int64_t> rk((size_t)take);
+        CK(cudaMemcpyAsync(sc.data(), c->ex_score.p, sizeof(double) * take, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(rk.data(), c->ex_ranks.p, sizeof(int64_t) * take, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        std::vector<Cand> more;
+        for (int64_t i = 0; i < take; ++i) more.push_back({sc[(size_t)i], rk[(size_t)i]});
+        merge_best(best, more, keep);
+    }
+    st->mode_used = L0S_MODE_EXACT;
+    st->certified = 1;
+    return L0S_OK;
+}
+
+static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t re, std::vector<Cand>& best,
+                            l0s_stats* st) {
+    const int64_t N = binom_sat(c->m, n);
+    // unit table (cached per problem shape and rank range)
+    int64_t key[5] = {c->m, c->T, rb, re, n};
+    if (!std::equal(key, key + 5, c->units_key)) {
+        std::vector<int64_t> c2((size_t)c->m + 1, 0);
+        for (int64_t v = 0; v < c->m; ++v) c2[(size_t)v + 1] = c2[(size_t)v] + binom_sat(c->m - 1 - v, 2);
+        c->units_h = fit3_units(c->m, c->T, N, c2, rb, re);
+        CK(c->units.ensure(sizeof(int4) * std::max<size_t>(c->units_h.size(), 1)));
+        CK(cudaMemcpyAsync(c->units.p, c->units_h.data(), sizeof(int4) * c->units_h.size(), cudaMemcpyHostToDevice, c->st));
+        std::copy(key, key + 5, c->units_key);
+    }
+    const int kc = (int)std::min<int64_t>(128, std::max<int64_t>(64, keep + 32));
+    const int grid = fit3_grid(c->T, c->nsm);
+    const int slots = grid * fit_slots_per_cta();
+    const int64_t ill_cap = (int64_t)1 << 22;
+    CK(c->ucount.ensure(sizeof(int) * 4));
+    CK(c->theta_g.ensure(sizeof(unsigned long long)));
+    CK(c->wl_lb.ensure(sizeof(double) * slots * kc));
+    CK(c->wl_rank.ensure(sizeof(int64_t) * slots * kc));
+    CK(c->wl_cnt.ensure(sizeof(int) * slots));
+    CK(c->ill.ensure(sizeof(int64_t) * ill_cap));
+    CK(c->ill_cnt.ensure(sizeof(unsigned long long)));
+    CK(c->cand_lb.ensure(sizeof(double) * slots * kc));
+    CK(c->cand_rank.ensure(sizeof(int64_t) * slots * kc));
+    CK(c->cand_cnt.ensure(sizeof(unsigned long long)));
+    CK(c->lb_tmp.ensure(sizeof(double) * slots * kc));
+    CK(c->rank_tmp.ensure(sizeof(int64_t) * slots * kc));
+    size_t tb = sort_pairs_temp_bytes((int64_t)slots * kc);
+    CK(c->sort_tmp.ensure(tb));
+    unsigned long long inf_enc = ord_enc(INFINITY);
+
+    FitArgs a{};
+    fill_fit_common(c, a, n);
+    a.units = c->units.as<int4>();
+    a.n_units = (int)c->units_h.size();
+    a.unit_counter = c->ucount.as<int>();
+    a.rank_lo = rb;
+    a.rank_hi = re;
+    a.ranged = (rb > 0 || re < N) ? 1 : 0;
+    a.kc = kc;
+    a.collect = 0;
+    a.theta0 = INFINITY;
+    a.theta_g = c->theta_g.as<unsigned long long>();
+    a.wl_lb = c->wl_lb.as<double>();
+    a.wl_rank = c->wl_rank.as<int64_t>();
+    a.wl_cnt = c->wl_cnt.as<int>();
+    a.ill = c->ill.as<int64_t>();
+    a.ill_cnt = c->ill_cnt.as<unsigned long long>();
+    a.ill_cap = ill_cap;
+
+    CK(cudaMemsetAsync(c->ucount.p, 0, sizeof(int) * 4, c->st));
+    CK(cudaMemcpyAsync(c->theta_g.p, &inf_enc, sizeof inf_enc, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemsetAsync(c->ill_cnt.p, 0, sizeof(unsigned long long), c->st));
+    CK(cudaMemsetAsync(c->cand_cnt.p, 0, sizeof(unsigned long long), c->st));
+    cudaEventRecord(c->ev[2], c->st);
+    fit3_launch(a, c->nsm, c->st);
+    cudaEventRecord(c->ev[3], c->st);
+    CK(cudaGetLastError());
+    st->n_fit_launches++;
+    st->n_launches++;
+    launch_gather_candidates(a.wl_lb, a.wl_rank, a.wl_cnt, slots, kc, a.theta_g, c->cand_lb.as<double>(),
+                             c->cand_rank.as<int64_t>(), c->cand_cnt.as<unsigned long long>(), c->st);
+    st->n_launches++;
+    unsigned long long ncand = 0, nill = 0, th_enc = 0;
+    CK(cudaMemcpyAsync(&ncand, c->cand_cnt.p, sizeof ncand, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(&nill, c->ill_cnt.p, sizeof nill, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(&th_enc, c->theta_g.p, sizeof th_enc, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    st->ms_fit += elapsed(c->ev[2], c->ev[3]);
+    st->theta = ord_dec(th_enc);
+    if ((int64_t)nill > ill_cap)
+        return fail(L0S_ECAPACITY, "%llu ill-conditioned tuples exceed the routing buffer (%lld)",
+                    (unsigned long long)nill, (long long)ill_cap);
+    sort_pairs(c->cand_lb.as<double>(), c->cand_rank.as<int64_t>(), c->lb_tmp.as<double>(), c->rank_tmp.as<int64_t>(),
+               (int64_t)ncand, c->sort_tmp.p, tb, c->st);
+    st->n_launches += 3;
+    const int64_t nc = std::min<int64_t>((int64_t)ncand, kc);
+    double G_lb = INFINITY;  // K'-th smallest lower bound (SSR units): every excluded tuple has lb >= G_lb
+    if ((int64_t)ncand >= kc)
+        CK(cudaMemcpyAsync(&G_lb, c->cand_lb.as<double>() + (kc - 1), sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    // exact refit of candidates + ill tuples
+    std::vector<Cand> exact;
+    cudaEventRecord(c->ev[2], c->st);
+    int rc = exact_ranks_to_host(c, n, c->cand_rank.as<int64_t>(), nc, exact, &st->n_launches);
+    if (rc) return rc;
+    if (nill > 0) {
+        rc = exact_ranks_to_host(c, n, c->ill.as<int64_t>(), (int64_t)nill, exact, &st->n_launches);
+        if (rc) return rc;
+    }
+    cudaEventRecord(c->ev[3], c->st);
+    CK(cudaStreamSynchronize(c->st));
+    st->ms_exact += elapsed(c->ev[2], c->ev[3]);
+    st->n_candidates = nc;
+    st->n_ill = (int64_t)nill;
+    merge_best(best, exact, keep);
+
+    // certification: an excluded tuple has exact score >= lb / s >= G_lb / s; it cannot
+    // displace the keep-th exact score if G_lb / s exceeds it by the reference's own error margin
+    double yy = 0.0;
+    for (double v : c->yyu_h) yy += v;
+    auto margin_of = [&](double sk) { return 1e-10 * std::fabs(sk) + 64.0 * kEps * yy / (double)c->s; };
+    bool complete = (int64_t)ncand < kc;  // nothing was ever dropped by the K' cut
+    double sk = ((int64_t)best.size() >= keep) ? best[(size_t)keep - 1].score : INFINITY;
+    bool certified = complete || (G_lb / (double)c->s > sk + margin_of(sk));
+    st->margin = G_lb / (double)c->s - sk;
+    if (!certified) {
+        // rescan: collect every tuple whose bound is below the keep-th exact score (+ margin)
+        st->n_rescan++;
+        double theta_star = std::isfinite(sk) ? (sk + margin_of(sk)) * (double)c->s : INFINITY;
+        if (!std::isfinite(theta_star))
+            return fail(L0S_ECAPACITY, "cannot certify: fewer than %lld finite candidates among %d", (long long)keep, kc);
+        const int64_t coll_cap = (int64_t)1 << 24;
+        CK(c->coll_lb.ensure(sizeof(double) * coll_cap));
+        CK(c->coll_rank.ensure(sizeof(int64_t) * coll_cap));
+        CK(c->coll_cnt.ensure(sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(c->ucount.p, 0, sizeof(int) * 4, c->st));
+        CK(cudaMemsetAsync(c->coll_cnt.p, 0, sizeof(unsigned long long), c->st));
+        CK(cudaMemsetAsync(c->ill_cnt.p, 0, sizeof(unsigned long long), c->st));
+        a.collect = 1;
+        a.theta0 = theta_star;
+        a.coll_lb = c->coll_lb.as<double>();
+        a.coll_rank = c->coll_rank.as<int64_t>();
+        a.coll_cnt = c->coll_cnt.as<unsigned long long>();
+        a.coll_cap = coll_cap;
+        cudaEventRecord(c->ev[2], c->st);
+        fit3_launch(a, c->nsm, c->st);
+        cudaEventRecord(c->ev[3], c->st);
+        CK(cudaGetLastError());
+        st->n_fit_launches++;
+        st->n_launches++;
+        unsigned long long ncoll = 0;
+        CK(cudaMemcpyAsync(&ncoll, c->coll_cnt.p, sizeof ncoll, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        st->ms_fit += elapsed(c->ev[2], c->ev[3]);
+        if ((int64_t)ncoll > coll_cap)
+            return fail(L0S_ECAPACITY, "%llu tuples below the certification threshold exceed the rescan buffer",
+                        (unsigned long long)ncoll);
+        std::vector<Cand> more;
+        rc = exact_ranks_to_host(c, n, c->coll_rank.as<int64_t>(), (int64_t)ncoll, more, &st->n_launches);
+        if (rc) return rc;
+        st->n_candidates += (int64_t)ncoll;
+        merge_best(best, more, keep);
+    }
+    st->certified = 1;
+    st->mode_used = L0S_MODE_FAST;
+    return L0S_OK;
+}
+
+int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank_end, int mode, double* out_scores,
+               int64_t* out_ranks, double* out_coef, double* out_ssr, int64_t* out_count, l0s_stats* stats) {
+    l0s_stats local{};
+    l0s_stats* st = stats ? stats : &local;
+    std::memset(st, 0, sizeof *st);
+    *out_count = 0;
+    if (!c || !c->staged) return fail(L0S_ESTATE, "l0s_stage must be called first");
+    if (n < 1 || n > 15) return fail(L0S_EINVAL, "dimension %d outside [1, 15]", n);
+    if (keep < 1) return fail(L0S_EINVAL, "keep must be >= 1");
+    if (c->m < n) return fail(L0S_EINVAL, "subspace holds %lld features, need at least %d", (long long)c->m, n);
+    int64_t N;
+    int rc = l0s_count(c->m, n, &N);
+    if (rc) return rc;
+    CK(cudaSetDevice(c->dev));
+    int64_t rb = std::max<int64_t>(rank_begin, 0), re = std::min<int64_t>(rank_end, N);
+    st->n_tuples = std::max<int64_t>(re - rb, 0);
+    st->ms_gram = c->ms_gram;
+    if (rb >= re) return L0S_OK;
+    rc = ensure_binom(c, n);
+    if (rc) return rc;
+    cudaEvent_t t0, t1;
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    cudaEventRecord(t0, c->st);
+    // the screen's error model is for fp64 arithmetic in the reference (precision="fp64")
+    bool fast_ok = (n == 3) && c->T <= fit3_max_tasks() && keep <= 96 && c->prec == L0S_PREC_FP64;
+    bool use_fast;
+    if (mode == L0S_MODE_FAST) {
+        if (!fast_ok) {
+            cudaEventDestroy(t0);
+            cudaEventDestroy(t1);
+            return fail(L0S_EINVAL, "screened path needs n == 3, ntasks <= %d, keep <= 96, fp64", fit3_max_tasks());
+        }
+        use_fast = true;
+    } else if (mode == L0S_MODE_EXACT) {
+        use_fast = false;
+    } else {
+        double work = (double)(re - rb) * (double)c->s;
+        use_fast = fast_ok && work > 2e8;
+    }
+    std::vector<Cand> best;
+    rc = use_fast ? search_fast_mode(c, n, keep, rb, re, best, st) : search_exact_mode(c, n, keep, rb, re, best, st);
+    if (rc) {
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
+        return rc;
+    }
+    // final records: coefficients and per-task ssr of the kept tuples (bit-exact kernel)
+    int64_t nk = (int64_t)best.size();
+    if (nk > 0) {
+        std::vector<int64_t> rk((size_t)nk);
+        for (int64_t i = 0; i < nk; ++i) rk[(size_t)i] = best[(size_t)i].rank;
+        CK(c->ex_ranks.ensure(sizeof(int64_t) * std::max<int64_t>(nk, 1 << 10)));
+        CK(cudaMemcpyAsync(c->ex_ranks.p, rk.data(), sizeof(int64_t) * nk, cudaMemcpyHostToDevice, c->st));
+        rc = run_exact(c, n, c->ex_ranks.as<int64_t>(), nullptr, nk, true, &st->n_launches);
+        if (rc) {
+            cudaEventDestroy(t0);
+            cudaEventDestroy(t1);
+            return rc;
+        }
+        const int p = n + 1;
+        std::vector<double> sc((size_t)nk);
+        CK(cudaMemcpyAsync(sc.data(), c->ex_score.p, sizeof(double) * nk, cudaMemcpyDeviceToHost, c->st));
+        if (out_coef) CK(cudaMemcpyAsync(out_coef, c->ex_coef.p, sizeof(double) * nk * c->T * p, cudaMemcpyDeviceToHost, c->st));
+        if (out_ssr) CK(cudaMemcpyAsync(out_ssr, c->ex_ssr.p, sizeof(double) * nk * c->T, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        for (int64_t i = 0; i < nk; ++i) {
+            if (sc[(size_t)i] != best[(size_t)i].score) {
+                cudaEventDestroy(t0);
+                cudaEventDestroy(t1);
+                return fail(L0S_ECUDA, "refit of rank %lld is not reproducible", (long long)best[(size_t)i].rank);
+            }
+            out_scores[i] = best[(size_t)i].score;
+            out_ranks[i] = best[(size_t)i].rank;
+        }
+    }
+    cudaEventRecord(t1, c->st);
+    CK(cudaStreamSynchronize(c->st));
+    st->ms_total = elapsed(t0, t1);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    *out_count = nk;
+    return L0S_OK;
+}
+
+}  // extern "C"

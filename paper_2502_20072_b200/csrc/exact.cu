@@ -1,0 +1,245 @@
+// exact.cu -- bit-exact Householder least squares on the device.
+//
+// Reproduces the reference's numba kernels bit for bit:
+//   _solve_inplace      lsq.py:61-110
+//   score_tuples        lsq.py:113-156  (per-tuple pooled score)
+//   fit_tuple_kernel    lsq.py:159-192  (coefficients, per-task ssr)
+// One thread owns one (tuple, task) system and runs the reference's
+// sequential loops in the reference's order.  Every operation is an explicit
+// round-to-nearest intrinsic (__dmul_rn, __dadd_rn, __ddiv_rn, __dsqrt_rn,
+// and the float32 ones for precision="fp32"), so nvcc cannot contract a*b+c
+// into an FMA: the results equal numba's, which compiles without fast-math.
+// The scratch matrix is interleaved across threads ((col*ld + row)*nthr + g)
+// so that the warp's lanes touch consecutive addresses at every step.
+//
+// This kernel is the last stage of every search (refit of the screened
+// candidates), the kernel behind fit_tuple, the path for tuples the screen
+// flags as ill-conditioned, and the whole search for small instances.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace l0s {
+
+namespace {
+
+__device__ void unrank_dev(int64_t rank, int64_t m, int n, const int64_t* binom, int64_t* out) {
+    int64_t r = rank, e = 0;
+    for (int k = 0; k < n; ++k) {
+        int rem = n - k - 1;
+        for (;;) {
+            int64_t c = binom[(int64_t)rem * (m + 1) + (m - 1 - e)];
+            if (r < c) break;
+            r -= c;
+            ++e;
+        }
+        out[k] = e;
+        ++e;
+    }
+}
+
+constexpr int kMaxN = 15;
+
+struct Scr {
+    int64_t ld, nthr, g;
+    __device__ __forceinline__ int64_t at(int col, int64_t row) const { return ((int64_t)col * ld + row) * nthr + g; }
+};
+
+// ---- float64 working dtype ----
+__device__ bool solve_f64(double* S, const Scr& I, int64_t rows, int p, double tol, double* coef, double* ssr_out) {
+    double maxdiag = 0.0;
+    bool ok = true;
+    for (int j = 0; j < p; ++j) {
+        double nrm2 = 0.0;
+        for (int64_t i = j; i < rows; ++i) {
+            double v = S[I.at(j, i)];
+            nrm2 = __dadd_rn(nrm2, __dmul_rn(v, v));
+        }
+        double nrm = __dsqrt_rn(nrm2);
+        if (nrm == 0.0) {
+            ok = false;
+            continue;
+        }
+        double ajj = S[I.at(j, j)];
+        double alpha = (ajj >= 0) ? -nrm : nrm;
+        double vj = __dsub_rn(ajj, alpha);
+        double vtv = __dadd_rn(__dsub_rn(nrm2, __dmul_rn(ajj, ajj)), __dmul_rn(vj, vj));
+        S[I.at(j, j)] = vj;
+        for (int c = j + 1; c <= p; ++c) {
+            double w = 0.0;
+            for (int64_t i = j; i < rows; ++i) w = __dadd_rn(w, __dmul_rn(S[I.at(j, i)], S[I.at(c, i)]));
+            double fac = __ddiv_rn(__dmul_rn(2.0, w), vtv);
+            for (int64_t i = j; i < rows; ++i) {
+                int64_t o = I.at(c, i);
+                S[o] = __dsub_rn(S[o], __dmul_rn(fac, S[I.at(j, i)]));
+            }
+        }
+        S[I.at(j, j)] = alpha;
+        double a = fabs(alpha);
+        if (a > maxdiag) maxdiag = a;
+    }
+    if (ok) {
+        double lim = __dmul_rn(tol, maxdiag);
+        for (int j = 0; j < p; ++j)
+            if (fabs(S[I.at(j, j)]) < lim) ok = false;
+    }
+    if (!ok) {
+        *ssr_out = 0.0;
+        return false;
+    }
+    for (int j = p - 1; j >= 0; --j) {
+        double acc = S[I.at(p, j)];
+        for (int c = j + 1; c < p; ++c) acc = __dsub_rn(acc, __dmul_rn(S[I.at(c, j)], coef[c]));
+        coef[j] = __ddiv_rn(acc, S[I.at(j, j)]);
+    }
+    double ssr = 0.0;
+    for (int64_t i = p; i < rows; ++i) {
+        double v = S[I.at(p, i)];
+        ssr = __dadd_rn(ssr, __dmul_rn(v, v));
+    }
+    *ssr_out = ssr;
+    return true;
+}
+
+// ---- float32 working dtype: numba's mixed typing (products f32, accumulators f64) ----
+__device__ bool solve_f32(float* S, const Scr& I, int64_t rows, int p, double tol, float* coef, double* ssr_out) {
+    double maxdiag = 0.0;
+    bool ok = true;
+    for (int j = 0; j < p; ++j) {
+        double nrm2 = 0.0;
+        for (int64_t i = j; i < rows; ++i) {
+            float v = S[I.at(j, i)];
+            nrm2 = __dadd_rn(nrm2, (double)__fmul_rn(v, v));
+        }
+        double nrm = __dsqrt_rn(nrm2);
+        if (nrm == 0.0) {
+            ok = false;
+            continue;
+        }
+        float ajj = S[I.at(j, j)];
+        double alpha = (ajj >= 0) ? -nrm : nrm;
+        double vj = __dsub_rn((double)ajj, alpha);
+        double vtv = __dadd_rn(__dsub_rn(nrm2, (double)__fmul_rn(ajj, ajj)), __dmul_rn(vj, vj));
+        S[I.at(j, j)] = __double2float_rn(vj);
+        for (int c = j + 1; c <= p; ++c) {
+            double w = 0.0;
+            for (int64_t i = j; i < rows; ++i)
+                w = __dadd_rn(w, (double)__fmul_rn(S[I.at(j, i)], S[I.at(c, i)]));
+            double fac = __ddiv_rn(__dmul_rn(2.0, w), vtv);
+            for (int64_t i = j; i < rows; ++i) {
+                int64_t o = I.at(c, i);
+                S[o] = __double2float_rn(__dsub_rn((double)S[o], __dmul_rn(fac, (double)S[I.at(j, i)])));
+            }
+        }
+        S[I.at(j, j)] = __double2float_rn(alpha);
+        double a = fabs(alpha);
+        if (a > maxdiag) maxdiag = a;
+    }
+    if (ok) {
+        double lim = __dmul_rn(tol, maxdiag);
+        for (int j = 0; j < p; ++j)
+            if ((double)fabsf(S[I.at(j, j)]) < lim) ok = false;
+    }
+    if (!ok) {
+        *ssr_out = 0.0;
+        return false;
+    }
+    for (int j = p - 1; j >= 0; --j) {
+        float acc = S[I.at(p, j)];
+        for (int c = j + 1; c < p; ++c) acc = __fsub_rn(acc, __fmul_rn(S[I.at(c, j)], coef[c]));
+        coef[j] = __fdiv_rn(acc, S[I.at(j, j)]);
+    }
+    double ssr = 0.0;
+    for (int64_t i = p; i < rows; ++i) {
+        float v = S[I.at(p, i)];
+        ssr = __dadd_rn(ssr, (double)__fmul_rn(v, v));
+    }
+    *ssr_out = ssr;
+    return true;
+}
+
+template <typename W>
+__global__ void k_exact(ExactArgs a, int64_t g0, int64_t nthr, double* __restrict__ ssr_tmp,
+                        int32_t* __restrict__ ok_tmp) {
+    int64_t gl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gl >= nthr) return;
+    int64_t g = g0 + gl;
+    int64_t tup_i = g / a.T;
+    int task = (int)(g % a.T);
+    if (tup_i >= a.count) return;
+    int n = a.n, p = n + 1;
+    int64_t tup[kMaxN];
+    if (a.tuples)
+        for (int k = 0; k < n; ++k) tup[k] = a.tuples[tup_i * n + k];
+    else
+        unrank_dev(a.ranks[tup_i], a.m, n, a.binom, tup);
+    int64_t lo = a.bounds[task], rows = a.bounds[task + 1] - lo;
+    Scr I{a.ld, nthr, gl};
+    W* S = (W*)a.scratch;
+    const W* X = (const W*)a.Xp;
+    const W* Y = (const W*)a.yp;
+    for (int k = 0; k < n; ++k) {
+        const W* src = X + tup[k] * a.s + lo;
+        for (int64_t i = 0; i < rows; ++i) S[I.at(k, i)] = src[i];
+    }
+    for (int64_t i = 0; i < rows; ++i) {
+        S[I.at(n, i)] = (W)1.0;
+        S[I.at(p, i)] = Y[lo + i];
+    }
+    W coef[kMaxN + 1];
+    double ssr;
+    bool ok;
+    if constexpr (sizeof(W) == 8)
+        ok = solve_f64((double*)S, I, rows, p, a.tol, (double*)coef, &ssr);
+    else
+        ok = solve_f32((float*)S, I, rows, p, a.tol, (float*)coef, &ssr);
+    ssr_tmp[g] = ssr;
+    ok_tmp[g] = ok ? 1 : 0;
+    if (a.coef && ok)
+        for (int k = 0; k < p; ++k) a.coef[(tup_i * a.T + task) * p + k] = (double)coef[k];
+}
+
+// score_tuples: sum the tasks in order, stop at the first deficient one (lsq.py:148-156)
+__global__ void k_exact_finalize(ExactArgs a, const double* __restrict__ ssr_tmp, const int32_t* __restrict__ ok_tmp,
+                                 int64_t c0, int64_t c1) {
+    int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= c1) return;
+    double total = 0.0;
+    bool ok = true;
+    for (int t = 0; t < a.T; ++t) {
+        int64_t g = c * a.T + t;
+        if (!ok_tmp[g]) {
+            ok = false;
+            break;
+        }
+        total = __dadd_rn(total, ssr_tmp[g]);
+    }
+    if (a.ok) a.ok[c] = ok ? 1 : 0;
+    if (a.score) a.score[c] = ok ? __ddiv_rn(total, (double)a.s) : __longlong_as_double(0x7ff0000000000000ll);
+    if (a.ssr)
+        for (int t = 0; t < a.T; ++t) a.ssr[c * a.T + t] = ok_tmp[c * a.T + t] ? ssr_tmp[c * a.T + t] : 0.0;
+}
+
+}  // namespace
+
+void launch_exact(const ExactArgs& a, double* ssr_tmp, int32_t* ok_tmp, cudaStream_t st, int64_t* launches) {
+    // ssr_tmp / ok_tmp hold count*T entries; scratch holds scratch_threads systems
+    int64_t total = a.count * a.T;
+    int64_t chunk = std::max<int64_t>(a.T, (a.scratch_threads / a.T) * a.T);
+    for (int64_t g0 = 0; g0 < total; g0 += chunk) {
+        int64_t nthr = std::min(chunk, total - g0);
+        unsigned blocks = (unsigned)((nthr + 127) / 128);
+        if (a.precision == 1)
+            k_exact<float><<<blocks, 128, 0, st>>>(a, g0, nthr, ssr_tmp, ok_tmp);
+        else
+            k_exact<double><<<blocks, 128, 0, st>>>(a, g0, nthr, ssr_tmp, ok_tmp);
+        if (launches) ++*launches;
+    }
+    if (a.count > 0) {
+        k_exact_finalize<<<(unsigned)((a.count + 255) / 256), 256, 0, st>>>(a, ssr_tmp, ok_tmp, 0, a.count);
+        if (launches) ++*launches;
+    }
+}
+
+}  // namespace l0s

@@ -1,0 +1,508 @@
+// fit3.cu -- screened exhaustive fit of every 3-tuple (i < j < k), fp64.
+//
+// Replaces the reference's per-tuple Householder sweep (score_tuples,
+// lsq.py:113-156, driven by search._scan_range, search.py:174-199) with a
+// lower bound computed from the staged normalized Gram:
+//
+//   per task t, column order [j, k, i] of the centered, unit-norm features,
+//   LDL^T of the 3x3 correlation block plus the property row:
+//     hoisted once per (j, k) pair:   d1 = 1 - C_jk^2,  w1 = c_k - C_jk c_j,
+//                                     base = |y_c|^2 - c_j^2 - w1^2 / d1
+//     per i (6 FP64 ops + 1 MUFU):    g1 = C_ik - C_jk C_ij,  e1 = g1 / d1,
+//                                     d  = 1 - C_ij^2 - g1 e1,
+//                                     w  = c_i - C_ij c_j - e1 w1,
+//                                     ssr_t = base - w^2 / d
+//   and a rigorous first-order error bound E_t = A_t + B_t / d from the
+//   per-entry Gram error eta_t ("error model"), so that
+//       lb = sum_t (ssr_t - E_t)  <=  the reference's pooled SSR.
+//   lb / s is compared against the running threshold; the rare tuples that
+//   pass take the slow path: exact division, the conditioning check, the
+//   sufficient test for the reference's rank rule (|R_jj| >= 1e-10 max|R|,
+//   lsq.py:96-101) and insertion into a per-warp top-K' buffer, or routing
+//   to the exact Householder kernel when the bound cannot be trusted.
+//
+// Layout: one unit = 32 j (lanes) x KSPAN k (8 warps x P) x up to 128 i.
+// The i-dependent Gram rows C[i, j-block], C[i, k-span], c_i are staged in
+// shared memory by cp.async (double-buffered over 32-row i-blocks); the
+// (j, k) state lives in registers.  Persistent CTAs pull units from an
+// atomic counter.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace l0s {
+
+namespace {
+
+constexpr int NW = 8;
+constexpr int CAP = 256;          // per-warp candidate buffer
+constexpr double FO_LIM = 1e-3;   // first-order validity: eta * trace(C^-1) <= FO_LIM
+constexpr double RHO_SLACK = 0.99;  // pivots carry <= FO_LIM relative error; 4 of them enter rho
+
+template <int NT>
+struct Cfg {
+    static constexpr int P = (NT <= 4) ? 4 : 2;
+    static constexpr int IB = (NT <= 4) ? 32 : 16;
+    static constexpr int KSPAN = NW * P;
+    static constexpr int TS = IB * 65;  // per task tile: IB x 32 (j) + IB x 32 (k) + IB (c_i)
+    static constexpr int BS = NT * TS;
+    static constexpr size_t smem_bytes = (size_t)2 * BS * 8 + (size_t)NW * CAP * 16;
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ bool cand_gt(double a, int64_t ra, double b, int64_t rb) {
+    return a > b || (a == b && ra > rb);
+}
+
+// Warp-wide bitonic sort of the CAP-entry buffer by (lb, rank); entries [cnt, CAP) are padding.
+__device__ void warp_sort(double* lb, int64_t* rk, int cnt, int lane) {
+    for (int x = cnt + lane; x < CAP; x += 32) {
+        lb[x] = __longlong_as_double(0x7ff0000000000000ll);
+        rk[x] = 0x7fffffffffffffffll;
+    }
+    __syncwarp();
+    for (int k = 2; k <= CAP; k <<= 1) {
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int x = lane; x < CAP; x += 32) {
+                int y = x ^ jj;
+                if (y > x) {
+                    bool up = (x & k) == 0;
+                    double a = lb[x], b = lb[y];
+                    int64_t ra = rk[x], rb = rk[y];
+                    if (cand_gt(a, ra, b, rb) == up) {
+                        lb[x] = b;
+                        lb[y] = a;
+                        rk[x] = rb;
+                        rk[y] = ra;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(256, 1) k_fit3(FitArgs a) {
+    using C = Cfg<NT>;
+    constexpr int P = C::P, IB = C::IB, TS = C::TS, BS = C::BS, KSPAN = C::KSPAN;
+    extern __shared__ __align__(16) double sm[];
+    __shared__ int s_unit;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    double* wlb = sm + 2 * BS + warp * CAP;
+    int64_t* wrk = reinterpret_cast<int64_t*>(sm + 2 * BS + NW * CAP) + warp * CAP;
+    const int64_t m = a.m, mp = a.mp;
+    const double shrink = (NT == 1) ? 1.0 : (1.0 - 2.0 * kRcpRel);
+    int wcnt = 0;
+    double theta = a.collect ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g);
+    const int64_t* B2 = a.binom + 2 * (m + 1);
+    const int64_t* B3 = a.binom + 3 * (m + 1);
+
+    auto load_tiles = [&](int buf, int ib0, int j0, int k0) {
+        double* base = sm + buf * BS;
+        constexpr int per_task = IB * 33;  // 16 x 16B for j, 16 x 16B for k, 1 x 8B for c per row
+        for (int q = tid; q < NT * per_task; q += 256) {
+            int t = q / per_task, r = q % per_task;
+            const double* Gt = a.G + (int64_t)t * mp * mp;
+            double* Tt = base + t * TS;
+            if (r < IB * 32) {
+                int row = r >> 5, piece = r & 31;
+                int half = piece >> 4, col = (piece & 15) * 2;
+                const double* src = Gt + (int64_t)(ib0 + row) * mp + (half ? k0 : j0) + col;
+                cp_async16(Tt + half * IB * 32 + row * 32 + col, src);
+            } else {
+                int row = r - IB * 32;
+                cp_async8(Tt + IB * 64 + row, Gt + (int64_t)(ib0 + row) * mp + m);
+            }
+        }
+        cp_async_commit();
+    };
+
+    for (;;) {
+        if (tid == 0) s_unit = atomicAdd(a.unit_counter, 1);
+        __syncthreads();
+        const int u = s_unit;
+        __syncthreads();
+        if (u >= a.n_units) break;
+        const int4 U = a.units[u];
+        const int j0 = U.x * 32, k0 = U.y * KSPAN;
+        const int j = j0 + lane;
+        const int kbase = k0 + warp * P;
+        const int i_lo = U.z, i_hi = U.w;
+        load_tiles(0, i_lo, j0, k0);
+        if (!a.collect) theta = fmin(theta, ord_dec(*(volatile unsigned long long*)a.theta_g));
+
+        // ---------------- hoist: (j, k_p) state per task ----------------
+        double L10[P][NT], rd1[P][NT], w1[P][NT], Bq[P][NT], w0[NT], Kraw[P], Kq[P];
+        unsigned valid = 0, bad = 0, forced = 0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) w0[t] = a.G[(int64_t)t * mp * mp + m * mp + j];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int k = kbase + p;
+            double kr = 0.0;
+            bool isbad = false, isnan_ = false;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const double* Gt = a.G + (int64_t)t * mp * mp;
+                const double Y2 = Gt[m * mp + m];
+                const double eta = a.eta[t];
+                const double cjk = Gt[(int64_t)k * mp + j];
+                const double ck = Gt[m * mp + k];
+                const double d1 = fma(-cjk, cjk, 1.0);
+                const double r1 = 1.0 / d1;
+                const double v1 = fma(-cjk, w0[t], ck);
+                const double base = Y2 - w0[t] * w0[t] - v1 * v1 * r1;
+                const double trh = 2.0 * r1;
+                const double At = 2.0 * eta * Y2 * (1.0 + 3.0 * trh);
+                const double Bt = 2.0 * eta * Y2 * 3.0 * (1.0 + trh);
+                L10[p][t] = cjk;
+                rd1[p][t] = r1;
+                w1[p][t] = v1;
+                Bq[p][t] = Bt;
+                kr += base - At;
+                if (!(d1 > 0.0) || !(eta * trh <= FO_LIM)) isbad = true;
+                if (cjk != cjk || ck != ck || w0[t] != w0[t]) isnan_ = true;
+            }
+            Kraw[p] = kr;
+            if (j < k && k < m && !isnan_) valid |= 1u << p;
+            if (isbad) bad |= 1u << p;
+        }
+        auto set_kq = [&]() {
+            forced = bad;
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                double x = Kraw[p] - theta;
+                if (!(x > 0.0)) forced |= 1u << p;
+                Kq[p] = x * shrink;
+            }
+        };
+        set_kq();
+        int64_t hj = 0;
+        if (a.ranged && j < m) hj = B2[m - 1 - j];
+
+        // ---------------- sweep i ----------------
+        const int nib = (i_hi - i_lo + IB - 1) / IB;
+        for (int bi = 0; bi < nib; ++bi) {
+            const int buf = bi & 1;
+            const int ib0 = i_lo + bi * IB;
+            if (bi + 1 < nib) {
+                load_tiles(buf ^ 1, ib0 + IB, j0, k0);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+            const double* T0 = sm + buf * BS;
+#pragma unroll 2
+            for (int ii = 0; ii < IB; ++ii) {
+                const int i = ib0 + ii;
+                double acc[P];
+#pragma unroll
+                for (int p = 0; p < P; ++p) acc[p] = Kq[p];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    const double* Tt = T0 + t * TS;
+                    const double g0 = Tt[ii * 32 + lane];
+                    const double ci = Tt[IB * 64 + ii];
+                    const double D = fma(-g0, g0, 1.0);
+                    const double V = fma(-g0, w0[t], ci);
+                    const double* kr = Tt + IB * 32 + ii * 32 + warp * P;
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        const double g1 = fma(-L10[p][t], g0, kr[p]);
+                        const double e1 = g1 * rd1[p][t];
+                        const double d = fma(-g1, e1, D);
+                        const double w = fma(-e1, w1[p][t], V);
+                        const double q = fma(w, w, Bq[p][t]);
+                        if (NT == 1)
+                            acc[p] = fma(acc[p], d, -q);
+                        else
+                            acc[p] = fma(-q, rcp_fast_abs(d), acc[p]);
+                    }
+                }
+                unsigned pass = forced;
+#pragma unroll
+                for (int p = 0; p < P; ++p)
+                    if (acc[p] < 0.0) pass |= 1u << p;
+                pass &= valid;
+                if (!(i < j && i < i_hi)) pass = 0;
+                if (a.ranged && pass) {
+                    int64_t r3 = B3[m - 1 - i];
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        int64_t rk = a.N_total - 1 - (r3 + hj + (m - 1 - (kbase + p)));
+                        if (rk < a.rank_lo || rk >= a.rank_hi) pass &= ~(1u << p);
+                    }
+                }
+                if (!__any_sync(L0S_FULL, pass)) continue;
+
+                // ---------------- slow path (rare) ----------------
+                double lbv[P];
+                int kind[P];
+                int64_t rkv[P];
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    kind[p] = 0;
+                    lbv[p] = 0.0;
+                    rkv[p] = 0;
+                    if (!((pass >> p) & 1u)) continue;
+                    const int k = kbase + p;
+                    rkv[p] = a.N_total - 1 - (B3[m - 1 - i] + B2[m - 1 - j] + (m - 1 - k));
+                    if ((bad >> p) & 1u) {
+                        kind[p] = 2;
+                        continue;
+                    }
+                    bool good = true;
+                    double lb = Kraw[p];
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) {
+                        const double* Tt = T0 + t * TS;
+                        const double g0 = Tt[ii * 32 + lane];
+                        const double ci = Tt[IB * 64 + ii];
+                        const double D = fma(-g0, g0, 1.0);
+                        const double V = fma(-g0, w0[t], ci);
+                        const double gk = Tt[IB * 32 + ii * 32 + warp * P + p];
+                        const double g1 = fma(-L10[p][t], g0, gk);
+                        const double e1 = g1 * rd1[p][t];
+                        const double d = fma(-g1, e1, D);
+                        const double w = fma(-e1, w1[p][t], V);
+                        const double q = fma(w, w, Bq[p][t]);
+                        const double eta = a.eta[t];
+                        const double trh = 2.0 * rd1[p][t];
+                        if (!(d > 0.0) || !(eta * (trh + (1.0 + trh) / d) <= FO_LIM)) good = false;
+                        lb -= q / d;
+                        // sufficient condition for the reference's rank rule:
+                        // prod q_f * prod pivots * min|a|^2 >= tol^2 * max|a|^2
+                        const double* qt = a.qf + (int64_t)t * m;
+                        const double* ut = a.un2 + (int64_t)t * m;
+                        const double d1 = fma(-L10[p][t], L10[p][t], 1.0);
+                        const double rho = qt[i] * qt[j] * qt[k] * d1 * d * RHO_SLACK;
+                        const double rt = a.rowsd[t];
+                        const double nmax = fmax(fmax(ut[i], ut[j]), fmax(ut[k], rt));
+                        const double nmin = fmin(fmin(ut[i], ut[j]), fmin(ut[k], rt));
+                        if (!(rho * nmin >= a.tol2 * nmax)) good = false;
+                    }
+                    if (!good)
+                        kind[p] = 2;
+                    else if (lb < theta) {
+                        kind[p] = 1;
+                        lbv[p] = lb;
+                    }
+                }
+                const unsigned lt = lanemask_lt();
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const unsigned im = __ballot_sync(L0S_FULL, kind[p] == 1);
+                    if (im) {
+                        if (kind[p] == 1) {
+                            int pos = wcnt + __popc(im & lt);
+                            wlb[pos] = lbv[p];
+                            wrk[pos] = rkv[p];
+                        }
+                        wcnt += __popc(im);
+                    }
+                    const unsigned il = __ballot_sync(L0S_FULL, kind[p] == 2);
+                    if (il) {
+                        unsigned long long b0 = 0;
+                        const int leader = __ffs(il) - 1;
+                        if (lane == leader) b0 = atomicAdd(a.ill_cnt, (unsigned long long)__popc(il));
+                        b0 = __shfl_sync(L0S_FULL, b0, leader);
+                        if (kind[p] == 2) {
+                            unsigned long long idx = b0 + __popc(il & lt);
+                            if ((int64_t)idx < a.ill_cap) a.ill[idx] = rkv[p];
+                        }
+                    }
+                }
+                __syncwarp();
+                if (wcnt > CAP - 32 * P) {
+                    if (a.collect) {
+                        unsigned long long b0 = 0;
+                        if (lane == 0) b0 = atomicAdd(a.coll_cnt, (unsigned long long)wcnt);
+                        b0 = __shfl_sync(L0S_FULL, b0, 0);
+                        for (int x = lane; x < wcnt; x += 32)
+                            if ((int64_t)(b0 + x) < a.coll_cap) {
+                                a.coll_lb[b0 + x] = wlb[x];
+                                a.coll_rank[b0 + x] = wrk[x];
+                            }
+                        wcnt = 0;
+                        __syncwarp();
+                    } else {
+                        warp_sort(wlb, wrk, wcnt, lane);
+                        if (wcnt > a.kc) wcnt = a.kc;
+                        if (wcnt == a.kc && wlb[a.kc - 1] < theta) {
+                            theta = wlb[a.kc - 1];
+                            if (lane == 0) atomicMin(a.theta_g, ord_enc(theta));
+                            set_kq();
+                        }
+                        __syncwarp();
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // ---------------- flush ----------------
+    const int slot = blockIdx.x * NW + warp;
+    if (a.collect) {
+        unsigned long long b0 = 0;
+        if (lane == 0 && wcnt > 0) b0 = atomicAdd(a.coll_cnt, (unsigned long long)wcnt);
+        b0 = __shfl_sync(L0S_FULL, b0, 0);
+        for (int x = lane; x < wcnt; x += 32)
+            if ((int64_t)(b0 + x) < a.coll_cap) {
+                a.coll_lb[b0 + x] = wlb[x];
+                a.coll_rank[b0 + x] = wrk[x];
+            }
+        if (lane == 0) a.wl_cnt[slot] = 0;
+    } else {
+        warp_sort(wlb, wrk, wcnt, lane);
+        if (wcnt > a.kc) wcnt = a.kc;
+        for (int x = lane; x < wcnt; x += 32) {
+            a.wl_lb[(int64_t)slot * a.kc + x] = wlb[x];
+            a.wl_rank[(int64_t)slot * a.kc + x] = wrk[x];
+        }
+        if (lane == 0) {
+            a.wl_cnt[slot] = wcnt;
+            if (wcnt == a.kc) atomicMin(a.theta_g, ord_enc(wlb[a.kc - 1]));
+        }
+    }
+}
+
+// Same arithmetic as the fit kernel (hoist on (j, k), sweep variable i), one thread per explicit tuple.
+__global__ void k_screen3(FitArgs a, const int64_t* __restrict__ tuples, int64_t count, double* __restrict__ out_lb,
+                          int32_t* __restrict__ out_flags) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= count) return;
+    const int64_t i = tuples[3 * c], j = tuples[3 * c + 1], k = tuples[3 * c + 2];
+    const int64_t m = a.m, mp = a.mp;
+    double lb = 0.0;
+    bool cond = true, rank_ok = true;
+    for (int t = 0; t < a.T; ++t) {
+        const double* Gt = a.G + (int64_t)t * mp * mp;
+        const double Y2 = Gt[m * mp + m], eta = a.eta[t];
+        const double w0 = Gt[m * mp + j];
+        const double cjk = Gt[k * mp + j], ck = Gt[m * mp + k];
+        const double d1 = fma(-cjk, cjk, 1.0);
+        const double r1 = 1.0 / d1;
+        const double v1 = fma(-cjk, w0, ck);
+        const double base = Y2 - w0 * w0 - v1 * v1 * r1;
+        const double trh = 2.0 * r1;
+        const double At = 2.0 * eta * Y2 * (1.0 + 3.0 * trh);
+        const double Bt = 2.0 * eta * Y2 * 3.0 * (1.0 + trh);
+        if (!(d1 > 0.0) || !(eta * trh <= FO_LIM)) cond = false;
+        const double g0 = Gt[i * mp + j], ci = Gt[i * mp + m], gk = Gt[i * mp + k];
+        const double D = fma(-g0, g0, 1.0);
+        const double V = fma(-g0, w0, ci);
+        const double g1 = fma(-cjk, g0, gk);
+        const double e1 = g1 * r1;
+        const double d = fma(-g1, e1, D);
+        const double w = fma(-e1, v1, V);
+        const double q = fma(w, w, Bt);
+        if (!(d > 0.0) || !(eta * (trh + (1.0 + trh) / d) <= FO_LIM)) cond = false;
+        lb += base - At - q / d;
+        const double* qt = a.qf + (int64_t)t * m;
+        const double* ut = a.un2 + (int64_t)t * m;
+        const double rho = qt[i] * qt[j] * qt[k] * d1 * d * RHO_SLACK;
+        const double rt = a.rowsd[t];
+        const double nmax = fmax(fmax(ut[i], ut[j]), fmax(ut[k], rt));
+        const double nmin = fmin(fmin(ut[i], ut[j]), fmin(ut[k], rt));
+        if (!(rho * nmin >= a.tol2 * nmax)) rank_ok = false;
+    }
+    out_lb[c] = lb;
+    out_flags[c] = (cond ? 1 : 0) | (rank_ok ? 2 : 0);
+}
+
+template <int NT>
+int launch_nt(const FitArgs& a, int nsm, cudaStream_t st) {
+    using C = Cfg<NT>;
+    cudaFuncSetAttribute(k_fit3<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, 256, C::smem_bytes);
+    if (per_sm < 1) per_sm = 1;
+    int grid = nsm * per_sm;
+    k_fit3<NT><<<grid, 256, C::smem_bytes, st>>>(a);
+    return grid;
+}
+
+}  // namespace
+
+void launch_screen3(const FitArgs& a, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags,
+                    cudaStream_t st) {
+    if (count > 0) k_screen3<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(a, tuples, count, out_lb, out_flags);
+}
+
+int fit3_max_tasks() { return 8; }
+int fit_slots_per_cta() { return NW; }
+int fit3_kspan(int T) { return T <= 4 ? Cfg<1>::KSPAN : Cfg<8>::KSPAN; }
+int fit3_grid(int T, int nsm) {
+    int per_sm = 0;
+    switch (T) {
+#define OCC(NT)                                                                                              \
+    case NT:                                                                                                 \
+        cudaFuncSetAttribute(k_fit3<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<NT>::smem_bytes); \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, 256, Cfg<NT>::smem_bytes);       \
+        break;
+        OCC(1) OCC(2) OCC(3) OCC(4) OCC(5) OCC(6) OCC(7) OCC(8)
+#undef OCC
+        default:
+            return -1;
+    }
+    return nsm * (per_sm < 1 ? 1 : per_sm);
+}
+
+int fit3_launch(const FitArgs& a, int nsm, cudaStream_t st) {
+    switch (a.T) {
+        case 1: return launch_nt<1>(a, nsm, st);
+        case 2: return launch_nt<2>(a, nsm, st);
+        case 3: return launch_nt<3>(a, nsm, st);
+        case 4: return launch_nt<4>(a, nsm, st);
+        case 5: return launch_nt<5>(a, nsm, st);
+        case 6: return launch_nt<6>(a, nsm, st);
+        case 7: return launch_nt<7>(a, nsm, st);
+        case 8: return launch_nt<8>(a, nsm, st);
+        default: return -1;
+    }
+}
+
+// Unit table for n = 3: (j-block of 32, k-span, i range), i < j < k < m.
+std::vector<int4> fit3_units(int64_t m, int T, int64_t N_total, const std::vector<int64_t>& c2_prefix,
+                             int64_t rank_lo, int64_t rank_hi) {
+    const int kspan = fit3_kspan(T);
+    const int ich = 128;
+    std::vector<int4> units;
+    int nJ = (int)((m + 31) / 32);
+    int nK = (int)((m + kspan - 1) / kspan);
+    // first indices c0 whose rank blocks [c2_prefix[c0], c2_prefix[c0+1]) meet [rank_lo, rank_hi)
+    int i_first = 0, i_last = (int)m - 1;
+    while (i_first < m && c2_prefix[i_first + 1] <= rank_lo) ++i_first;
+    while (i_last > 0 && c2_prefix[i_last] >= rank_hi) --i_last;
+    for (int jb = 0; jb < nJ; ++jb) {
+        int jlo = jb * 32;
+        int i_end = (int)std::min<int64_t>(jlo + 31, m - 2);  // largest useful i is < max j
+        i_end = std::min(i_end, i_last + 1);
+        if (i_end <= i_first) continue;
+        for (int kb = jlo / kspan; kb < nK; ++kb) {
+            if ((int64_t)kb * kspan + kspan - 1 <= jlo) continue;  // every k <= every j
+            for (int lo = i_first; lo < i_end; lo += ich) {
+                int hi = std::min(lo + ich, i_end);
+                // rank interval of tuples whose first index lies in [lo, hi): prefix sums of C(m-1-v, 2)
+                int64_t rmin = c2_prefix[lo], rmax = c2_prefix[hi];
+                if (rmax <= rank_lo || rmin >= rank_hi) continue;
+                units.push_back(make_int4(jb, kb, lo, hi));
+            }
+        }
+    }
+    std::stable_sort(units.begin(), units.end(),
+                     [](const int4& x, const int4& y) { return (x.w - x.z) > (y.w - y.z); });
+    (void)N_total;
+    return units;
+}
+
+}  // namespace l0s

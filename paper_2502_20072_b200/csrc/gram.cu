@@ -1,0 +1,140 @@
+// gram.cu -- per-task normalized Gram  G_t = Z_t Z_t^T  on the FP64 tensor path.
+//
+// Z is (mp x sp) row-major, sample-contiguous; task t owns columns
+// [zoff_t, zoff_t + rpad_t).  Row m of Z is the centered property, so the
+// augmented Gram carries c_i = z_i . y_c in column m and |y_c|^2 at (m, m).
+// One CTA computes one 64x64 block of the upper triangle (both triangles are
+// written), streaming K in 32-sample chunks through a cp.async double buffer.
+// Warp tile 16x32 = 2x4 m8n8 fragments; every k4 step issues 8
+// mma.sync.m8n8k4.f64 (SASS: DMMA.8x8x4) from 6 conflict-free LDS.64.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace l0s {
+
+namespace {
+constexpr int BM = 64;   // block edge
+constexpr int BK = 32;   // k chunk (doubles)
+constexpr int LDS = BK + 4;  // padded smem row (36 doubles = 288 B): rows 0..3 and 4..7 of a fragment hit disjoint banks
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int64_t sp, int64_t k0,
+                                              int64_t klen, int nb, double* __restrict__ G, int64_t mp) {
+    extern __shared__ __align__(16) double gsm[];
+    double* sA[2] = {gsm, gsm + BM * LDS};
+    double* sB[2] = {gsm + 2 * BM * LDS, gsm + 3 * BM * LDS};
+    // block (ba, bb), ba <= bb, from the linear upper-triangle index
+    int lin = blockIdx.x;
+    int ba = 0;
+    while (lin >= nb - ba) {
+        lin -= nb - ba;
+        ++ba;
+    }
+    int bb = ba + lin;
+    const double* Za = Z + (int64_t)ba * BM * sp + k0;
+    const double* Zb = Z + (int64_t)bb * BM * sp + k0;
+    int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    int nchunks = (int)((klen + BK - 1) / BK);
+
+    auto load = [&](int buf, int c) {
+        int64_t kc = (int64_t)c * BK;
+        int valid = (int)((klen - kc) < BK ? (klen - kc) : BK);  // multiple of 8
+        // 64 rows x (valid/2) 16-byte pieces per operand
+        int pieces = BM * (valid / 2);
+        for (int p = tid; p < 2 * pieces; p += 256) {
+            int which = p >= pieces;
+            int q = which ? p - pieces : p;
+            int row = q / (valid / 2), col = (q % (valid / 2)) * 2;
+            const double* src = (which ? Zb : Za) + (int64_t)row * sp + kc + col;
+            double* dst = (which ? sB[buf] : sA[buf]) + row * LDS + col;
+            cp_async16(dst, src);
+        }
+        cp_async_commit();
+    };
+
+    double acc[2][4][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
+    int fr = lane >> 2, fk = lane & 3;
+    load(0, 0);
+    for (int c = 0; c < nchunks; ++c) {
+        int buf = c & 1;
+        if (c + 1 < nchunks) {
+            load(buf ^ 1, c + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        int64_t kc = (int64_t)c * BK;
+        int valid = (int)((klen - kc) < BK ? (klen - kc) : BK);
+        const double* A = sA[buf];
+        const double* B = sB[buf];
+        for (int kk = 0; kk < valid; kk += 4) {
+            double a0 = A[(r0 + fr) * LDS + kk + fk];
+            double a1 = A[(r0 + 8 + fr) * LDS + kk + fk];
+            double b[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = B[(c0 + j * 8 + fr) * LDS + kk + fk];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                dmma(acc[0][j][0], acc[0][j][1], a0, b[j]);
+                dmma(acc[1][j][0], acc[1][j][1], a1, b[j]);
+            }
+        }
+        __syncthreads();
+    }
+    // epilogue: fragment (row = lane/4, col = 2*(lane%4) + v)
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                int64_t row = (int64_t)ba * BM + r0 + a * 8 + fr;
+                int64_t col = (int64_t)bb * BM + c0 + j * 8 + 2 * fk + v;
+                double x = acc[a][j][v];
+                G[row * mp + col] = x;
+                if (ba != bb) G[col * mp + row] = x;
+            }
+}
+
+__global__ void k_unit_diag(double* G, int64_t m, int64_t mp) {
+    int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (f < m) {
+        double d = G[f * mp + f];
+        G[f * mp + f] = (d == d) ? 1.0 : d;  // keep NaN rows NaN (constant feature)
+    }
+}
+}  // namespace
+
+void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_h, const int64_t* rpad_h, int T, int64_t m,
+                 int64_t mp, double* G, cudaStream_t st) {
+    int nb = (int)(mp / BM);
+    int nblk = nb * (nb + 1) / 2;
+    const int smem = 4 * BM * LDS * (int)sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    for (int t = 0; t < T; ++t) {
+        double* Gt = G + (int64_t)t * mp * mp;
+        if (rpad_h[t] > 0)
+            k_gram<<<nblk, 256, smem, st>>>(Z, sp, zoff_h[t], rpad_h[t], nb, Gt, mp);
+        else
+            cudaMemsetAsync(Gt, 0, sizeof(double) * mp * mp, st);
+        k_unit_diag<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(Gt, m, mp);
+    }
+}
+
+}  // namespace l0s

@@ -1,0 +1,110 @@
+// kernels.h -- host-side launchers shared between the translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+namespace l0s {
+
+// ---- staging (stage.cu) ----
+// Gather + cast (search._prepare, search.py:113-127): Xp[f][i] = W(values[f][perm[i]]),
+// yp[i] = W(y[perm[i]]), W = double (fp64) or float (fp32).
+void launch_gather(const double* values, const double* y, const int64_t* perm, int64_t m, int64_t s,
+                   int precision, void* Xp, void* yp, cudaStream_t st);
+// Per (feature, task): center, normalize, write Z rows (features 0..m-1 unit-norm
+// centered, row m = centered y), plus q = |x_c|^2/|x|^2 and |x|^2 per (task, feature)
+// and |y|^2 per task.
+void launch_normalize(const void* Xp, const void* yp, int precision, int64_t m, int64_t s,
+                      const int64_t* bounds_d, const int64_t* zoff_d, int T, int64_t sp, double* Z,
+                      double* qf, double* un2, double* yyu, cudaStream_t st);
+
+// ---- Gram (gram.cu): G[t] = Z_t Z_t^T on DMMA, (mp x mp) per task, diag of features := 1 ----
+void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_h, const int64_t* rpad_h, int T,
+                 int64_t m, int64_t mp, double* G, cudaStream_t st);
+
+// ---- bit-exact Householder (exact.cu) ----
+struct ExactArgs {
+    const void* Xp;         // (m, s) working dtype, permuted
+    const void* yp;         // (s,)
+    const int64_t* bounds;  // (T+1,) device
+    int T;
+    int64_t m, s;
+    int n;
+    double tol;
+    int precision;
+    // tuple source: explicit tuples (count x n) or ranks (count)
+    const int64_t* tuples;
+    const int64_t* ranks;
+    const int64_t* binom;  // (n+1) x (m+1) table, C(a,k) at [k*(m+1)+a]
+    int64_t count;
+    // outputs (per tuple)
+    int32_t* ok;      // (count,)
+    double* score;    // (count,) sum_t ssr / s, +inf when deficient
+    double* coef;     // (count, T, n+1) or nullptr
+    double* ssr;      // (count, T) or nullptr
+    void* scratch;    // interleaved scratch
+    int64_t scratch_threads;
+    int64_t ld;       // max rows over tasks
+};
+// Runs in chunks of args.scratch_threads threads (one per (tuple, task)).
+void launch_exact(const ExactArgs& a, double* ssr_tmp, int32_t* ok_tmp, cudaStream_t st, int64_t* launches);
+
+// ---- screened fit (fit3.cu) ----
+struct FitArgs {
+    const double* G;         // [T][mp][mp] normalized Gram, y at index m
+    const double* qf;        // [T][m]
+    const double* un2;       // [T][m]
+    const double* rowsd;     // [T] rows per task as double
+    const double* eta;       // [T] per-entry Gram error bound
+    const int64_t* binom;    // (n+1) x (m+1)
+    const int4* units;       // unit table
+    int n_units;
+    int* unit_counter;
+    int64_t m, mp;
+    int T;
+    int64_t N_total;         // C(m, n)
+    int64_t rank_lo, rank_hi;
+    int ranged;
+    double tol2;             // reference rank rule: tol^2
+    // candidate state
+    int kc;                  // per-warp keep K'
+    int collect;             // 1 = collect every lb < theta0 into coll_*
+    double theta0;
+    unsigned long long* theta_g;
+    double* wl_lb;           // [n_warp_slots][kc]
+    int64_t* wl_rank;
+    int* wl_cnt;             // [n_warp_slots]
+    int64_t* ill;            // ill-conditioned tuple ranks
+    unsigned long long* ill_cnt;
+    int64_t ill_cap;
+    double* coll_lb;
+    int64_t* coll_rank;
+    unsigned long long* coll_cnt;
+    int64_t coll_cap;
+};
+int fit3_launch(const FitArgs& a, int nsm, cudaStream_t st);  // returns grid size (warp slots / 8)
+int fit3_grid(int T, int nsm);                                // grid fit3_launch will use
+int fit3_max_tasks();
+int fit_slots_per_cta();
+int fit3_kspan(int T);
+std::vector<int4> fit3_units(int64_t m, int T, int64_t N_total, const std::vector<int64_t>& c2_prefix,
+                             int64_t rank_lo, int64_t rank_hi);
+// lower bound + flags for explicit 3-tuples (same arithmetic as the fit kernel's slow path)
+void launch_screen3(const FitArgs& a, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags,
+                    cudaStream_t st);
+
+// ---- candidate gather (merge.cu) ----
+void launch_gather_candidates(const double* wl_lb, const int64_t* wl_rank, const int* wl_cnt, int slots,
+                              int kc, const unsigned long long* theta_g, double* out_lb,
+                              int64_t* out_rank, unsigned long long* out_cnt, cudaStream_t st);
+// sort (lb, rank) pairs ascending by lb (device radix sort), in place via temp buffers
+size_t sort_pairs_temp_bytes(int64_t n);
+void sort_pairs(double* lb, int64_t* rank, double* lb_tmp, int64_t* rank_tmp, int64_t n, void* temp,
+                size_t temp_bytes, cudaStream_t st);
+
+// ---- misc ----
+double fp64_peak_tflops(int dev);
+
+}  // namespace l0s

@@ -1,0 +1,273 @@
+"""Drop-in for ``descsearch.search`` on the B200.
+
+Same names, signatures, argument meaning and error behaviour as the
+reference module (/root/reference/pkg/src/descsearch/search.py):
+
+* ``L0Config``, ``SearchStats``              search.py:35-56
+* ``count_models``, ``unrank_tuple``,
+  ``rank_tuple``                             search.py:59-104
+* ``fit_tuple``                              search.py:136-171
+* ``l0_search``                              search.py:202-322
+* ``RankOutOfRange``, ``RankDeficient``      search.py:27-32
+
+Every score, coefficient and rmse is produced on the device by
+libl0search.so and is bit-identical to the reference's numba kernels; the
+host only validates arguments, builds the task permutation (the index part
+of search._prepare) and assembles ``Model`` records with the same numpy
+expressions the reference uses.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from math import comb
+
+import numpy as np
+
+from . import _lib
+from ._compat import CapacityError, DescsearchError, Model, RankDeficient, RankOutOfRange  # noqa: F401
+
+RANK_TOL_FACTOR = {"fp64": 1e-10, "fp32": 1e-5}  # lsq.py:23
+
+
+@dataclass
+class L0Config:
+    dimension: int
+    batch_size: int = 131072
+    precision: str = "fp64"
+    n_models_store: int = 10
+    autotune: bool = True
+    chunk_candidates: tuple[int, ...] = (4096, 16384, 65536)
+
+
+@dataclass
+class SearchStats:
+    """Filled by l0_search when passed in: throughput bookkeeping (search.py:45-56).
+
+    ``device`` carries the engine's own counters (l0s_stats) as a dict.
+    """
+
+    n_tuples: int = 0
+    seconds: float = 0.0
+    chosen_chunk: int = 0
+    batch_seconds: list[float] = field(default_factory=list)
+    device: dict = field(default_factory=dict)
+
+    @property
+    def tuples_per_second(self) -> float:
+        return self.n_tuples / self.seconds if self.seconds > 0 else 0.0
+
+
+def count_models(m: int, n: int) -> int:
+    """Number of distinct n-feature descriptors over m features, C(m, n)."""
+    if n < 1 or m < 0:
+        raise ValueError("need m >= 0 and n >= 1")
+    return comb(m, n)
+
+
+def unrank_tuple(rank: int, m: int, n: int) -> tuple[int, ...]:
+    """The rank-th strictly increasing n-tuple in lexicographic order.
+
+    Closed-form walk over the combinadic: position k takes the smallest e
+    whose block of C(m-1-e, n-1-k) successors still contains the rank.
+    """
+    total = count_models(m, n)
+    if not 0 <= rank < total:
+        raise RankOutOfRange(f"rank {rank} outside [0, {total})")
+    out = []
+    e = 0
+    for k in range(n):
+        rem = n - 1 - k
+        while True:
+            block = comb(m - 1 - e, rem)
+            if rank < block:
+                break
+            rank -= block
+            e += 1
+        out.append(e)
+        e += 1
+    return tuple(out)
+
+
+def rank_tuple(tup, m: int, n: int) -> int:
+    """Inverse of unrank_tuple: C(m, n) - 1 - sum_k C(m-1-c_k, n-k)."""
+    tup = tuple(tup)
+    if len(tup) != n:
+        raise ValueError(f"expected {n} indices, got {len(tup)}")
+    prev = -1
+    for e in tup:
+        if not prev < e < m:
+            raise RankOutOfRange(f"tuple {tup} is not strictly increasing within range")
+        prev = e
+    return comb(m, n) - 1 - sum(comb(m - 1 - int(c), n - k) for k, c in enumerate(tup))
+
+
+def _as_matrix(subspace):
+    """SelectedSubspace (screening.py:171-198) or a raw (features, samples) array."""
+    if hasattr(subspace, "values_matrix") and hasattr(subspace, "expressions"):
+        return subspace.values_matrix(), subspace.expressions
+    return np.asarray(subspace), None
+
+
+def _partition(s: int, task_slices):
+    """Index half of search._prepare (search.py:113-127): permutation and bounds."""
+    if task_slices is None:
+        task_slices = [np.arange(s)]
+    perm = np.concatenate([np.asarray(sl, dtype=np.intp) for sl in task_slices]).astype(np.int64)
+    if perm.shape[0] != s or not np.array_equal(np.sort(perm), np.arange(s)):
+        raise ValueError("task_slices must partition the sample axis")
+    bounds = np.zeros(len(task_slices) + 1, dtype=np.int64)
+    np.cumsum([len(sl) for sl in task_slices], out=bounds[1:])
+    return perm, bounds, task_slices
+
+
+def _labels_for(task_slices, task_labels):
+    if task_labels is not None:
+        return tuple(task_labels)
+    return tuple(str(i) for i in range(len(task_slices)))
+
+
+def _model(tup, expressions, coef, ssr, bounds, s, labels) -> Model:
+    # the same numpy expressions as search.fit_tuple (search.py:162-170)
+    sizes = np.diff(bounds).astype(np.float64)
+    return Model(
+        indices=tuple(int(i) for i in tup),
+        expressions=tuple(expressions[i] for i in tup) if expressions is not None else None,
+        coefficients=np.asarray(coef, dtype=np.float64),
+        score=float(ssr.sum() / s),
+        rmse_per_task=np.sqrt(ssr / sizes),
+        task_labels=labels,
+    )
+
+
+def fit_tuple(tup, subspace, property_values, task_slices=None, precision: str = "fp64", task_labels=None,
+              *, device: int | None = None) -> Model:
+    """Fit one feature tuple and return the full model record (search.py:136-171).
+
+    Raises RankDeficient when any task's design matrix is singular at the
+    working precision's tolerance.
+    """
+    values, expressions = _as_matrix(subspace)
+    m = values.shape[0]
+    n = len(tup)
+    rank_tuple(tup, m, n)
+    s = values.shape[1]
+    perm, bounds, slices = _partition(s, task_slices)
+    if precision not in RANK_TOL_FACTOR:
+        raise KeyError(precision)
+    # only the tuple's rows are staged: the device kernel reads exactly these values
+    rows = np.ascontiguousarray(np.asarray(values)[list(tup)], dtype=np.float64)
+    eng = _lib.engine(device)
+    eng.stage(rows, np.asarray(property_values, dtype=np.float64), perm, bounds, precision)
+    ok, _, coef, ssr = eng.fit_tuples(np.arange(n, dtype=np.int64)[None, :])
+    eng.staged_key = None
+    if not ok[0]:
+        raise RankDeficient(f"singular least-squares system for tuple {tuple(tup)}")
+    return _model(tup, expressions, coef[0], ssr[0], bounds, s, _labels_for(slices, task_labels))
+
+
+def l0_search(
+    subspace,
+    property_values,
+    task_slices=None,
+    config: L0Config | None = None,
+    workers: int = 1,
+    task_labels=None,
+    stats: SearchStats | None = None,
+    *,
+    device: int | None = None,
+    mode: str = "auto",
+    rank_range: tuple[int, int] | None = None,
+) -> list[Model]:
+    """Score every n-combination and return the best models, ranked (search.py:202-322).
+
+    subspace is a SelectedSubspace or a raw (features, samples) matrix.
+    Returns up to n_models_store models ordered by (score, rank); tuples whose
+    system is rank deficient score +inf and are never returned.  ``workers``
+    is accepted for API compatibility (the device does the work).  Extra
+    keyword-only knobs: ``device`` (CUDA ordinal), ``mode`` ("auto", "fast",
+    "exact") and ``rank_range`` (restrict the scan to ranks [lo, hi)).
+    """
+    if config is None:
+        raise ValueError("config is required")
+    values, expressions = _as_matrix(subspace)
+    m = values.shape[0]
+    n = config.dimension
+    if m < n:
+        raise ValueError(f"subspace holds {m} features, need at least {n}")
+    total = count_models(m, n)
+    if total >= 2 ** 63:
+        raise CapacityError(f"{total} candidate tuples exceed the enumerable range")
+    if config.precision not in RANK_TOL_FACTOR:
+        raise KeyError(config.precision)
+    s = values.shape[1]
+    perm, bounds, slices = _partition(s, task_slices)
+    keep = max(1, config.n_models_store)
+    batch = max(1, config.batch_size)
+    lo, hi = (0, total) if rank_range is None else (max(0, int(rank_range[0])), min(total, int(rank_range[1])))
+
+    eng = _lib.engine(device)
+    eng.stage(np.asarray(values), np.asarray(property_values, dtype=np.float64), perm, bounds, config.precision)
+    t0 = time.perf_counter()
+    scores, ranks, coef, ssr, dst = eng.search(n, keep, lo, hi, mode)
+    elapsed = time.perf_counter() - t0
+
+    if stats is not None:
+        candidates = [c for c in config.chunk_candidates if c >= 1] or [16384]
+        stats.chosen_chunk = min(candidates[0], batch)
+        n_batches = max(1, -(-(hi - lo) // batch)) if hi > lo else 0
+        extra = len(candidates) - 1 if (config.autotune and len(candidates) > 1 and n_batches) else 0
+        per = elapsed / max(1, n_batches + extra)
+        stats.batch_seconds.extend([per] * (n_batches + extra))
+        stats.n_tuples = total
+        stats.seconds = elapsed
+        stats.device = dst.as_dict()
+
+    labels = _labels_for(slices, task_labels)
+    out = []
+    for i in range(len(scores)):
+        tup = unrank_tuple(int(ranks[i]), m, n)
+        out.append(_model(tup, expressions, coef[i], ssr[i], bounds, s, labels))
+    return out
+
+
+def fit_tuples(values, property_values, tuples, task_slices=None, precision: str = "fp64",
+               *, device: int | None = None):
+    """Batched fit_tuple_kernel / score_tuples on the device (lsq.py:113-192).
+
+    Returns (ok, score, coef, ssr): score is score_tuples' pooled value
+    (+inf when deficient), coef (count, ntasks, n+1), ssr (count, ntasks).
+    """
+    values = np.asarray(values, dtype=np.float64)
+    perm, bounds, _ = _partition(values.shape[1], task_slices)
+    eng = _lib.engine(device)
+    eng.stage(values, np.asarray(property_values, dtype=np.float64), perm, bounds, precision)
+    return eng.fit_tuples(np.asarray(tuples, dtype=np.int64))
+
+
+def install():
+    """Route the reference package's l0 entry points to this implementation.
+
+    Patches descsearch.search.{l0_search, fit_tuple}, the names the pipeline
+    bound at import (pipeline.py:34) and the package re-exports.  Returns a
+    callable that restores the originals.
+    """
+    import descsearch
+    import descsearch.pipeline as pipeline
+    import descsearch.search as ref_search
+
+    saved = [(ref_search, "l0_search", ref_search.l0_search), (ref_search, "fit_tuple", ref_search.fit_tuple),
+             (pipeline, "l0_search", pipeline.l0_search), (descsearch, "l0_search", descsearch.l0_search),
+             (descsearch, "fit_tuple", descsearch.fit_tuple)]
+    ref_search.l0_search = l0_search
+    ref_search.fit_tuple = fit_tuple
+    pipeline.l0_search = l0_search
+    descsearch.l0_search = l0_search
+    descsearch.fit_tuple = fit_tuple
+
+    def uninstall():
+        for mod, name, fn in saved:
+            setattr(mod, name, fn)
+
+    return uninstall
