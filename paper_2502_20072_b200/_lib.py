@@ -16,7 +16,8 @@ import numpy as np
 from . import _compat
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libl0search.so")
+# L0S_LIB selects a tuning variant built by tools/tune_fit.py (same ABI, in-tree .so)
+LIB_PATH = os.environ.get("L0S_LIB") or os.path.join(HERE, "libl0search.so")
 
 L0S_OK, L0S_EINVAL, L0S_ECAPACITY, L0S_ECUDA, L0S_ENOMEM, L0S_ENODEV, L0S_ESTATE = range(7)
 PREC = {"fp64": 0, "fp32": 1}

@@ -45,37 +45,42 @@ def _deps_mtime() -> float:
     return max(os.path.getmtime(p) for p in paths)
 
 
-def _compile(src: str) -> tuple[str, str]:
-    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+def _compile(src: str, objdir: str = OBJ, defines: tuple = ()) -> tuple[str, str]:
+    obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
     return obj, r.stderr
 
 
-def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _deps_mtime():
-        return LIB
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False, defines: tuple = (),
+          out: str | None = None) -> str:
+    """Build the library; `defines`/`out` produce a tuning variant (e.g. L0S_CFG34=...)."""
+    lib_path = out or LIB
+    if not force and os.path.exists(lib_path) and os.path.getmtime(lib_path) >= _deps_mtime():
+        return lib_path
+    objdir = OBJ if not defines else OBJ + "_" + str(abs(hash(defines)) % 10**8)
+    os.makedirs(objdir, exist_ok=True)
     srcs = sources()
     jobs = jobs or min(len(srcs), os.cpu_count() or 4)
     with cf.ThreadPoolExecutor(jobs) as ex:
-        results = list(ex.map(_compile, srcs))
+        results = list(ex.map(lambda s: _compile(s, objdir, defines), srcs))
     if verbose:
         for _, log in results:
             sys.stderr.write(log)
     objs = [o for o, _ in results]
-    tmp = LIB + ".tmp"
+    LIB_OUT = lib_path
+    tmp = LIB_OUT + ".tmp"
     r = subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-lpthread", "-ldl"],
                        capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    with open(os.path.join(OBJ, "ptxas.log"), "w") as fh:
+    os.replace(tmp, LIB_OUT)
+    with open(os.path.join(objdir, "ptxas.log"), "w") as fh:
         for _, log in results:
             fh.write(log)
-    return LIB
+    return LIB_OUT
 
 
 def main() -> None:

@@ -88,6 +88,8 @@ struct l0s_ctx {
     std::vector<double> rows_h, eta_h, yyu_h;
     double ms_gram = 0.0;
     DBuf in_values, in_y, in_perm, bounds_d, zoff_d, Xp, yp, Z, G, qf, un2, yyu, rowsd, eta_d;
+    DBuf rho, rho_cap, ynorm, iforce, dead;
+    int64_t n_dead = 0, n_iforce = 0;
     // binomial table (k <= binom_n) x (a <= m)
     DBuf binom;
     int binom_n = -1;
@@ -101,7 +103,7 @@ struct l0s_ctx {
 
     ~l0s_ctx() {
         DBuf* all[] = {&in_values, &in_y, &in_perm, &bounds_d, &zoff_d, &Xp, &yp, &Z, &G, &qf, &un2, &yyu, &rowsd,
-                       &eta_d, &binom, &units, &ucount, &theta_g, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
+                       &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &binom, &units, &ucount, &theta_g, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
                        &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
                        &ex_ranks, &ex_tuples};
@@ -142,7 +144,9 @@ int run_exact(l0s_ctx* c, int n, const int64_t* ranks_d, const int64_t* tuples_d
     int64_t budget = (int64_t)1 << 30;
     int64_t cap_thr = std::max<int64_t>(c->T, std::min<int64_t>(budget / per_sys, count * c->T));
     cap_thr = std::max<int64_t>(cap_thr, 1);
-    CK(c->ex_scratch.ensure((size_t)(cap_thr * per_sys)));
+    // systems that fit in shared memory never touch the interleaved scratch (exact.cu)
+    const bool smem_path = per_sys <= (int64_t)200 * 1024 && n <= 15;
+    if (!smem_path) CK(c->ex_scratch.ensure((size_t)(cap_thr * per_sys)));
     CK(c->ex_ssr_tmp.ensure(sizeof(double) * (size_t)std::max<int64_t>(count * c->T, 1)));
     CK(c->ex_ok_tmp.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(count * c->T, 1)));
     CK(c->ex_ok.ensure(sizeof(int32_t) * (size_t)std::max<int64_t>(count, 1)));
@@ -333,7 +337,62 @@ int l0s_stage(l0s_ctx* c, const double* values, int64_t m, int64_t s, const doub
     CK(cudaGetLastError());
     cudaEventRecord(c->ev[1], c->st);
     c->yyu_h.assign((size_t)ntasks, 0.0);
+    std::vector<double> qh((size_t)(m * ntasks)), uh((size_t)(m * ntasks));
     CK(cudaMemcpyAsync(c->yyu_h.data(), c->yyu.p, sizeof(double) * ntasks, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(qh.data(), c->qf.p, sizeof(double) * m * ntasks, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(uh.data(), c->un2.p, sizeof(double) * m * ntasks, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    // Per-feature conditioning of the reference's uncentered QR (error model):
+    //   rho = |f| / |f_c| enters the bound on the reference's own error;
+    //   a feature is dead when the reference's rank rule rejects every tuple holding it:
+    //   |R_nn| <= sqrt(r q) (distance of the intercept column to the feature) while
+    //   max|R| >= min_f |f|, so sqrt(q) + 4 gam < tol/2 * sqrt(min|f|^2 / r) is certain rejection.
+    std::vector<double> rho_h((size_t)(m * ntasks)), cap_h((size_t)ntasks), yn_h((size_t)ntasks);
+    std::vector<unsigned char> iforce_h((size_t)m, 0);
+    std::vector<int32_t> dead_h;
+    std::vector<unsigned char> dead_f((size_t)m, 0);
+    for (int t = 0; t < ntasks; ++t) {
+        const double r = c->rows_h[t];
+        const double gam = 2.0 * (r + 1.0) * (15 + 2) * kEps;
+        double umin = INFINITY;
+        for (int64_t f = 0; f < m; ++f) umin = std::min(umin, uh[(size_t)(t * m + f)]);
+        const double lim = 0.5 * 1e-10 * std::sqrt(umin / std::max(r, 1.0)) - 4.0 * gam;
+        double rmax = 1.0;
+        for (int64_t f = 0; f < m; ++f) {
+            const double q = qh[(size_t)(t * m + f)];
+            const double rf = 1.0 / std::sqrt(q);
+            rho_h[(size_t)(t * m + f)] = std::isfinite(rf) ? rf : INFINITY;
+            if (lim > 0.0 && std::sqrt(q) < lim) dead_f[(size_t)f] = 1;
+            else if (std::isfinite(rf)) rmax = std::max(rmax, rf);
+        }
+        cap_h[(size_t)t] = std::min(32.0, rmax);
+        yn_h[(size_t)t] = std::sqrt(c->yyu_h[(size_t)t]);
+    }
+    for (int64_t f = 0; f < m; ++f) {
+        if (dead_f[(size_t)f]) {
+            dead_h.push_back((int32_t)f);
+            continue;
+        }
+        for (int t = 0; t < ntasks; ++t)
+            if (rho_h[(size_t)(t * m + f)] > cap_h[(size_t)t]) iforce_h[(size_t)f] = 1;
+    }
+    CK(c->rho.ensure(sizeof(double) * m * ntasks));
+    CK(c->rho_cap.ensure(sizeof(double) * ntasks));
+    CK(c->ynorm.ensure(sizeof(double) * ntasks));
+    CK(c->iforce.ensure((size_t)m));
+    CK(cudaMemcpyAsync(c->rho.p, rho_h.data(), sizeof(double) * m * ntasks, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->rho_cap.p, cap_h.data(), sizeof(double) * ntasks, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->ynorm.p, yn_h.data(), sizeof(double) * ntasks, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->iforce.p, iforce_h.data(), (size_t)m, cudaMemcpyHostToDevice, c->st));
+    if (!dead_h.empty()) {
+        CK(c->dead.ensure(sizeof(int32_t) * dead_h.size()));
+        CK(cudaMemcpyAsync(c->dead.p, dead_h.data(), sizeof(int32_t) * dead_h.size(), cudaMemcpyHostToDevice, c->st));
+        launch_mark_dead(c->G.as<double>(), c->dead.as<int32_t>(), (int)dead_h.size(), ntasks, c->mp, c->st);
+        CK(cudaGetLastError());
+    }
+    c->n_dead = (int64_t)dead_h.size();
+    c->n_iforce = 0;
+    for (unsigned char x : iforce_h) c->n_iforce += x;
     CK(cudaStreamSynchronize(c->st));
     c->ms_gram = elapsed(c->ev[0], c->ev[1]);
     c->staged = true;
@@ -417,6 +476,11 @@ static void fill_fit_common(l0s_ctx* c, FitArgs& a, int n) {
     a.un2 = c->un2.as<double>();
     a.rowsd = c->rowsd.as<double>();
     a.eta = c->eta_d.as<double>();
+    a.rho = c->rho.as<double>();
+    a.rho_cap = c->rho_cap.as<double>();
+    a.ynorm = c->ynorm.as<double>();
+    a.iforce = c->iforce.as<unsigned char>();
+    a.n = n;
     a.binom = c->binom.as<int64_t>();
     a.m = c->m;
     a.mp = c->mp;

@@ -46,6 +46,13 @@ __device__ __forceinline__ double rcp_fast_abs(double d) {
     return r;
 }
 
+// Same for d known to be positive: MUFU.RCP64H straight on the high word.
+__device__ __forceinline__ double rcp_fast_pos(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    return r;
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));

@@ -200,6 +200,169 @@ __global__ void k_exact(ExactArgs a, int64_t g0, int64_t nthr, double* __restric
         for (int k = 0; k < p; ++k) a.coef[(tup_i * a.T + task) * p + k] = (double)coef[k];
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory variant: one CTA per (tuple, task) system.  The reference's
+// sequential reductions stay sequential (one thread each, products and sums
+// in the reference's order), but the independent ones run concurrently on
+// different lanes -- the p-j dot products of step j -- and the reflection
+// updates are spread over all threads.  The system lives in shared memory,
+// so each sequential chain is bound by DADD latency instead of L2 latency.
+// ---------------------------------------------------------------------------
+template <typename W>
+struct Ops;
+template <>
+struct Ops<double> {
+    // one term of a sum of products: acc + fl(a*b)
+    static __device__ __forceinline__ double term(double acc, double a, double b) {
+        return __dadd_rn(acc, __dmul_rn(a, b));
+    }
+    static __device__ __forceinline__ double upd(double x, double fac, double v) {
+        return __dsub_rn(x, __dmul_rn(fac, v));
+    }
+    static __device__ __forceinline__ double widen(double x) { return x; }
+    static __device__ __forceinline__ double store(double x) { return x; }
+};
+template <>
+struct Ops<float> {
+    static __device__ __forceinline__ double term(double acc, float a, float b) {
+        return __dadd_rn(acc, (double)__fmul_rn(a, b));
+    }
+    static __device__ __forceinline__ float upd(float x, double fac, float v) {
+        return __double2float_rn(__dsub_rn((double)x, __dmul_rn(fac, (double)v)));
+    }
+    static __device__ __forceinline__ double widen(float x) { return (double)x; }
+    static __device__ __forceinline__ float store(double x) { return __double2float_rn(x); }
+};
+
+// sequential sum_{i=from}^{to-1} fl(x_i*y_i) in index order; loads batched ahead of the adds
+template <typename W>
+__device__ __forceinline__ double seq_dot(const W* __restrict__ x, const W* __restrict__ y, int from, int to) {
+    double acc = 0.0;
+    int i = from;
+    for (; i + 8 <= to; i += 8) {
+        W px[8], py[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            px[u] = x[i + u];
+            py[u] = y[i + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = Ops<W>::term(acc, px[u], py[u]);
+    }
+    for (; i < to; ++i) acc = Ops<W>::term(acc, x[i], y[i]);
+    return acc;
+}
+
+template <typename W>
+__global__ void __launch_bounds__(128) k_exact_smem(ExactArgs a, int64_t g0, double* __restrict__ ssr_tmp,
+                                                    int32_t* __restrict__ ok_tmp) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    W* S = reinterpret_cast<W*>(smraw);
+    __shared__ double s_fac[kMaxN + 2];
+    __shared__ double s_vtv, s_alpha;
+    __shared__ int s_skip;
+    __shared__ int64_t s_tup[kMaxN];
+    const int tid = threadIdx.x;
+    const int64_t g = g0 + blockIdx.x;
+    const int64_t tup_i = g / a.T;
+    const int task = (int)(g % a.T);
+    const int n = a.n, p = n + 1;
+    if (tid == 0) {
+        if (a.tuples)
+            for (int k = 0; k < n; ++k) s_tup[k] = a.tuples[tup_i * n + k];
+        else
+            unrank_dev(a.ranks[tup_i], a.m, n, a.binom, s_tup);
+    }
+    __syncthreads();
+    const int64_t lo = a.bounds[task];
+    const int rows = (int)(a.bounds[task + 1] - lo);
+    const int ld = rows;
+    const W* X = (const W*)a.Xp;
+    const W* Y = (const W*)a.yp;
+    for (int k = 0; k < n; ++k) {
+        const W* src = X + s_tup[k] * a.s + lo;
+        for (int i = tid; i < rows; i += blockDim.x) S[k * ld + i] = src[i];
+    }
+    for (int i = tid; i < rows; i += blockDim.x) {
+        S[n * ld + i] = (W)1.0;
+        S[p * ld + i] = Y[lo + i];
+    }
+    __syncthreads();
+    double maxdiag = 0.0;  // meaningful in thread 0
+    bool ok = true;
+    for (int j = 0; j < p; ++j) {
+        W* cj = S + j * ld;
+        if (tid == 0) {
+            double nrm2 = seq_dot<W>(cj, cj, j, rows);
+            double nrm = __dsqrt_rn(nrm2);
+            if (nrm == 0.0) {
+                ok = false;
+                s_skip = 1;
+            } else {
+                W ajj = cj[j];
+                double alpha = (ajj >= 0) ? -nrm : nrm;
+                double vj = __dsub_rn(Ops<W>::widen(ajj), alpha);
+                double sq = (sizeof(W) == 8) ? __dmul_rn(Ops<W>::widen(ajj), Ops<W>::widen(ajj))
+                                             : (double)__fmul_rn((float)ajj, (float)ajj);
+                s_vtv = __dadd_rn(__dsub_rn(nrm2, sq), __dmul_rn(vj, vj));
+                s_alpha = alpha;
+                cj[j] = Ops<W>::store(vj);
+                s_skip = 0;
+            }
+        }
+        __syncthreads();
+        const int skip = s_skip;
+        __syncthreads();  // every thread has read s_skip before thread 0 may rewrite it
+        if (skip) continue;
+        // w_c for c = j+1..p: independent sequential chains on lanes 0..p-j-1
+        if (tid < p - j) {
+            int c = j + 1 + tid;
+            double w = seq_dot<W>(cj, S + c * ld, j, rows);
+            s_fac[c] = __ddiv_rn(__dmul_rn(2.0, w), s_vtv);
+        }
+        __syncthreads();
+        for (int c = j + 1; c <= p; ++c) {
+            const double fac = s_fac[c];
+            W* cc = S + c * ld;
+            for (int i = j + tid; i < rows; i += blockDim.x) cc[i] = Ops<W>::upd(cc[i], fac, cj[i]);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            cj[j] = Ops<W>::store(s_alpha);
+            double aa = fabs(s_alpha);
+            if (aa > maxdiag) maxdiag = aa;
+        }
+    }
+    if (tid != 0) return;
+    if (ok) {
+        double lim = __dmul_rn(a.tol, maxdiag);
+        for (int j = 0; j < p; ++j)
+            if (fabs(Ops<W>::widen(S[j * ld + j])) < lim) ok = false;
+    }
+    double ssr = 0.0;
+    if (ok) {
+        W coef[kMaxN + 1];
+        for (int j = p - 1; j >= 0; --j) {
+            W acc = S[p * ld + j];
+            for (int c = j + 1; c < p; ++c) {
+                if constexpr (sizeof(W) == 8)
+                    acc = __dsub_rn(acc, __dmul_rn(S[c * ld + j], coef[c]));
+                else
+                    acc = __fsub_rn(acc, __fmul_rn(S[c * ld + j], coef[c]));
+            }
+            if constexpr (sizeof(W) == 8)
+                coef[j] = __ddiv_rn(acc, S[j * ld + j]);
+            else
+                coef[j] = __fdiv_rn(acc, S[j * ld + j]);
+        }
+        ssr = seq_dot<W>(S + p * ld, S + p * ld, p, rows);
+        if (a.coef)
+            for (int k = 0; k < p; ++k) a.coef[(tup_i * a.T + task) * p + k] = (double)coef[k];
+    }
+    ssr_tmp[g] = ssr;
+    ok_tmp[g] = ok ? 1 : 0;
+}
+
 // score_tuples: sum the tasks in order, stop at the first deficient one (lsq.py:148-156)
 __global__ void k_exact_finalize(ExactArgs a, const double* __restrict__ ssr_tmp, const int32_t* __restrict__ ok_tmp,
                                  int64_t c0, int64_t c1) {
@@ -226,6 +389,26 @@ __global__ void k_exact_finalize(ExactArgs a, const double* __restrict__ ssr_tmp
 void launch_exact(const ExactArgs& a, double* ssr_tmp, int32_t* ok_tmp, cudaStream_t st, int64_t* launches) {
     // ssr_tmp / ok_tmp hold count*T entries; scratch holds scratch_threads systems
     int64_t total = a.count * a.T;
+    const size_t wsz = a.precision == 1 ? 4 : 8;
+    const size_t smem = (size_t)a.ld * (size_t)(a.n + 2) * wsz;
+    if (smem <= (size_t)200 * 1024 && a.n <= kMaxN) {
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(k_exact_smem<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(k_exact_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            attr_set = true;
+        }
+        const int64_t max_grid = (int64_t)1 << 30;
+        for (int64_t g0 = 0; g0 < total; g0 += max_grid) {
+            unsigned blocks = (unsigned)std::min(max_grid, total - g0);
+            if (a.precision == 1)
+                k_exact_smem<float><<<blocks, 128, smem, st>>>(a, g0, ssr_tmp, ok_tmp);
+            else
+                k_exact_smem<double><<<blocks, 128, smem, st>>>(a, g0, ssr_tmp, ok_tmp);
+            if (launches) ++*launches;
+        }
+        total = 0;  // done
+    }
     int64_t chunk = std::max<int64_t>(a.T, (a.scratch_threads / a.T) * a.T);
     for (int64_t g0 = 0; g0 < total; g0 += chunk) {
         int64_t nthr = std::min(chunk, total - g0);

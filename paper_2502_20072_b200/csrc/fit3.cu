@@ -39,17 +39,133 @@ namespace {
 constexpr int NW = 8;
 constexpr int CAP = 256;          // per-warp candidate buffer
 constexpr double FO_LIM = 1e-3;   // first-order validity: eta * trace(C^-1) <= FO_LIM
-constexpr double RHO_SLACK = 0.99;  // pivots carry <= FO_LIM relative error; 4 of them enter rho
+constexpr double RANK_SLACK = 1.01;  // safety factor on the rank-rule certificate
 
+// Pivots below D_MIN (a power of two: its low word is zero, so the test is one
+// integer compare on the high word) send the tuple to the slow path; above it
+// the bound's B/d term is at most B/D_MIN and is folded into the per-pair constant.
+constexpr double D_MIN = 1.0 / 1024.0;
+constexpr int HI_DMIN = 0x3F500000;  // high word of 2^-10
+
+// Per task count: P = (j,k) pairs per thread, IB = rows per i-tile, MINB = CTAs per SM.
+// (P, IB, MINB, UNROLL) for 3-4 tasks; overridable (-DL0S_C34_P=... etc.) for tuning builds
+#ifndef L0S_C34_P
+#define L0S_C34_P 4
+#endif
+#ifndef L0S_C34_IB
+#define L0S_C34_IB 32
+#endif
+#ifndef L0S_C34_MINB
+#define L0S_C34_MINB 1
+#endif
+#ifndef L0S_C34_UNROLL
+#define L0S_C34_UNROLL 1
+#endif
+struct CfgT {
+    int P, IB, MINB, UNROLL;
+};
+constexpr CfgT kCfg34{L0S_C34_P, L0S_C34_IB, L0S_C34_MINB, L0S_C34_UNROLL};
+constexpr CfgT kCfg12{4, 32, 2, 2};
+constexpr CfgT kCfg58{2, 16, 1, 1};
 template <int NT>
 struct Cfg {
-    static constexpr int P = (NT <= 4) ? 4 : 2;
-    static constexpr int IB = (NT <= 4) ? 32 : 16;
+    static constexpr CfgT c = (NT <= 2) ? kCfg12 : (NT <= 4 ? kCfg34 : kCfg58);
+    static constexpr int P = c.P;
+    static constexpr int IB = c.IB;
     static constexpr int KSPAN = NW * P;
-    static constexpr int TS = IB * 65;  // per task tile: IB x 32 (j) + IB x 32 (k) + IB (c_i)
+    static constexpr int TS = IB * (32 + KSPAN + 1);  // C[i, j-block] | C[i, k-span] | c_i
     static constexpr int BS = NT * TS;
-    static constexpr size_t smem_bytes = (size_t)2 * BS * 8 + (size_t)NW * CAP * 16;
+    static constexpr int MINB = c.MINB;
+    static constexpr int UNROLL = c.UNROLL;  // rows of the i sweep in flight per thread
+    static constexpr size_t smem_bytes = (size_t)2 * BS * 8 + (size_t)NW * CAP * 16 + (size_t)256 * P * 8;
 };
+
+// Error model: for one task, with tr = trace of the inverse of the
+// normalized 3x3 block (tr <= trh + (1 + trh)/d, trh = hoisted 2x2 trace),
+//   |ssr_gram - ssr_true| <= 2 eta Y2 (1 + 3 tr)                (Gram entries, |dC| <= eta)
+//   |ssr_ref  - ssr_true| <= 4 gam |y_c| |y| + 2 gam rho Y2 (1 + 3 tr)
+//                           (reference Householder QR, columnwise backward error gam,
+//                            rho = max |f|/|f_c| over the tuple's features)
+// so ssr_ref >= ssr_gram - A - B/d with
+//   A = 4 gam |y_c||y| + K Y2 (1 + 3 trh),  B = 3 K Y2 (1 + trh),  K = 2 (eta + gam rho),
+// valid while (eta + gam rho)(1 + 3 tr) <= FO_LIM (first-order terms dominate).
+__device__ __forceinline__ void task_bound(double eta, double gam, double rho, double Y2, double yn, double trh,
+                                           double& A, double& B, double& vk) {
+    vk = eta + gam * rho;
+    const double K = 2.0 * vk;
+    // 4 gam |y_c| |y| <= 2 gam (|y_c|^2 + |y|^2): no square root on the device
+    A = 2.0 * gam * (Y2 + yn * yn) + K * Y2 * (1.0 + 3.0 * trh);
+    B = 3.0 * K * Y2 * (1.0 + trh);
+}
+// 1/d without the IEEE-division subroutine call: MUFU seed + two Newton steps
+// (a few ulp; the error model's eta slack covers it).  Garbage for d <= 0, which
+// every caller rejects separately.
+__device__ __forceinline__ double rcp_newton(double d) {
+    double r = rcp_fast_pos(d);
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+__device__ __forceinline__ double ref_gamma(double rows, int n) { return 2.0 * (rows + 1.0) * (n + 2) * kEps; }
+constexpr double LOOSE = 1e-6;  // bounds looser than this fraction of |y_c|^2 go to the exact kernel
+
+// Exact lower bound of one tuple (i < j < k) read straight from the Gram, with the
+// arithmetic of the sweep (hoist on (j, k), i appended last).  Returns
+// bit0 = bound trustworthy (conditioning, first-order validity, tightness),
+// bit1 = the reference's rank rule certainly accepts the tuple; *lb in SSR units.
+// Shared by the fit kernel's slow path and k_screen3 (so the tests exercise
+// exactly the kernel's decision).  Kept out of line: the sweep's hot loop then
+// carries only its (j, k) state in registers.
+__device__ __noinline__ int eval_tuple3(const FitArgs& a, int64_t i, int64_t j, int64_t k, double* lb_out) {
+    const int64_t m = a.m, mp = a.mp;
+    double lb = 0.0;
+    bool cond = true, rank_ok = true;
+    for (int t = 0; t < a.T; ++t) {
+        const double* Gt = a.G + (int64_t)t * mp * mp;
+        const double Y2 = Gt[m * mp + m];
+        const double w0 = Gt[m * mp + j];
+        const double cjk = Gt[k * mp + j], ck = Gt[m * mp + k];
+        const double d1 = fma(-cjk, cjk, 1.0);
+        const double r1 = rcp_newton(d1);
+        const double v1 = fma(-cjk, w0, ck);
+        const double base = Y2 - w0 * w0 - v1 * v1 * r1;
+        const double trh = 2.0 * r1;
+        const double* rt_ = a.rho + (int64_t)t * m;
+        const double rx = fmax(rt_[i], fmax(rt_[j], rt_[k]));
+        double At, Bt, vk;
+        task_bound(a.eta[t], ref_gamma(a.rowsd[t], 3), rx, Y2, a.ynorm[t], trh, At, Bt, vk);
+        if (!(d1 > 0.0) || !(vk * (1.0 + 3.0 * trh) <= FO_LIM)) cond = false;
+        const double g0 = Gt[i * mp + j], ci = Gt[i * mp + m], gk = Gt[i * mp + k];
+        const double D = fma(-g0, g0, 1.0);
+        const double V = fma(-g0, w0, ci);
+        const double g1 = fma(-cjk, g0, gk);
+        const double e1 = g1 * r1;
+        const double d = fma(-g1, e1, D);
+        const double w = fma(-e1, v1, V);
+        const double tr = trh + (1.0 + trh) / d;
+        if (!(d > 0.0) || !(vk * (1.0 + 3.0 * tr) <= FO_LIM) || !(At + Bt / d <= LOOSE * Y2)) cond = false;
+        lb += base - At - fma(w, w, Bt) / d;
+        // Sufficient condition for the reference's rank rule |R_jj| >= tol max|R_jj|
+        // (lsq.py:96-101), columns [f_c0, f_c1, f_c2, 1] uncentered:
+        //   every R_jj^2 >= sigma_min([F, 1])^2 >= min(min_f |f_c|^2 / tr, r) / (1 + |mu|)^2,
+        //   max R_jj^2 <= max(max_f |f|^2, r),  (1 + |mu|)^2 <= 2 (1 + sum_f mean_f^2),
+        // with tr = trace(C^-1) >= 1 / lambda_min(C); tr carries <= FO_LIM relative error.
+        const double* qt = a.qf + (int64_t)t * m;
+        const double* ut = a.un2 + (int64_t)t * m;
+        const double rt = a.rowsd[t];
+        const double trs = tr * (1.0 + 4.0 * FO_LIM);
+        const double fc_min = fmin(fmin(ut[i] * qt[i], ut[j] * qt[j]), ut[k] * qt[k]);
+        const double mu2 = (ut[i] * (1.0 - qt[i]) + ut[j] * (1.0 - qt[j]) + ut[k] * (1.0 - qt[k])) / rt;
+        const double lo = fmin(fc_min / trs, rt) / (2.0 * (1.0 + mu2));
+        const double hi = fmax(fmax(ut[i], ut[j]), fmax(ut[k], rt));
+        const double gam = ref_gamma(rt, 3);
+        const double tl = sqrt(a.tol2) + 4.0 * gam;  // slack for the reference's rounding of R
+        if (!(lo >= tl * tl * hi * RANK_SLACK)) rank_ok = false;
+    }
+    *lb_out = lb;
+    return (cond ? 1 : 0) | (rank_ok ? 2 : 0);
+}
 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned r;
@@ -90,7 +206,7 @@ __device__ void warp_sort(double* lb, int64_t* rk, int cnt, int lane) {
 }
 
 template <int NT>
-__global__ void __launch_bounds__(256, 1) k_fit3(FitArgs a) {
+__global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_constant__ FitArgs a) {
     using C = Cfg<NT>;
     constexpr int P = C::P, IB = C::IB, TS = C::TS, BS = C::BS, KSPAN = C::KSPAN;
     extern __shared__ __align__(16) double sm[];
@@ -98,6 +214,7 @@ __global__ void __launch_bounds__(256, 1) k_fit3(FitArgs a) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     double* wlb = sm + 2 * BS + warp * CAP;
     int64_t* wrk = reinterpret_cast<int64_t*>(sm + 2 * BS + NW * CAP) + warp * CAP;
+    double* sKraw = sm + 2 * BS + 2 * NW * CAP + tid * P;  // per-thread, slow path / threshold updates only
     const int64_t m = a.m, mp = a.mp;
     const double shrink = (NT == 1) ? 1.0 : (1.0 - 2.0 * kRcpRel);
     int wcnt = 0;
@@ -105,22 +222,21 @@ __global__ void __launch_bounds__(256, 1) k_fit3(FitArgs a) {
     const int64_t* B2 = a.binom + 2 * (m + 1);
     const int64_t* B3 = a.binom + 3 * (m + 1);
 
+    // tiles per task: C[i, j-block] (IB x 32), C[i, k-span] (IB x KSPAN), c_i (IB)
     auto load_tiles = [&](int buf, int ib0, int j0, int k0) {
         double* base = sm + buf * BS;
-        constexpr int per_task = IB * 33;  // 16 x 16B for j, 16 x 16B for k, 1 x 8B for c per row
-        for (int q = tid; q < NT * per_task; q += 256) {
-            int t = q / per_task, r = q % per_task;
-            const double* Gt = a.G + (int64_t)t * mp * mp;
+        constexpr int pr = 16 + KSPAN / 2 + 1;  // 16-byte pieces per row (+ one 8-byte c_i)
+        for (int q = tid; q < NT * IB * pr; q += 256) {
+            const int t = q / (IB * pr), r = q % (IB * pr);
+            const int row = r / pr, piece = r % pr;
+            const double* Grow = a.G + (int64_t)t * mp * mp + (int64_t)(ib0 + row) * mp;
             double* Tt = base + t * TS;
-            if (r < IB * 32) {
-                int row = r >> 5, piece = r & 31;
-                int half = piece >> 4, col = (piece & 15) * 2;
-                const double* src = Gt + (int64_t)(ib0 + row) * mp + (half ? k0 : j0) + col;
-                cp_async16(Tt + half * IB * 32 + row * 32 + col, src);
-            } else {
-                int row = r - IB * 32;
-                cp_async8(Tt + IB * 64 + row, Gt + (int64_t)(ib0 + row) * mp + m);
-            }
+            if (piece < 16)
+                cp_async16(Tt + row * 32 + piece * 2, Grow + j0 + piece * 2);
+            else if (piece < 16 + KSPAN / 2)
+                cp_async16(Tt + IB * 32 + row * KSPAN + (piece - 16) * 2, Grow + k0 + (piece - 16) * 2);
+            else
+                cp_async8(Tt + IB * (32 + KSPAN) + row, Grow + m);
         }
         cp_async_commit();
     };
@@ -140,38 +256,40 @@ __global__ void __launch_bounds__(256, 1) k_fit3(FitArgs a) {
         if (!a.collect) theta = fmin(theta, ord_dec(*(volatile unsigned long long*)a.theta_g));
 
         // ---------------- hoist: (j, k_p) state per task ----------------
-        double L10[P][NT], rd1[P][NT], w1[P][NT], Bq[P][NT], w0[NT], Kraw[P], Kq[P];
+        // L10 = C_jk, rd1 = 1/(1 - C_jk^2), w1 = c_k - C_jk c_j; the bound's B/d term is
+        // folded into the constant for d >= D_MIN (tuples with a smaller pivot take the slow path)
+        double L10[P][NT], rd1[P][NT], w1[P][NT], w0[NT], Kq[P];
         unsigned valid = 0, bad = 0, forced = 0;
 #pragma unroll
         for (int t = 0; t < NT; ++t) w0[t] = a.G[(int64_t)t * mp * mp + m * mp + j];
+        const int jj = j < m ? j : (int)m - 1;
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             const int k = kbase + p;
+            const int kk = k < m ? k : (int)m - 1;
             double kr = 0.0;
-            bool isbad = false, isnan_ = false;
+            bool isbad = (a.iforce[jj] | a.iforce[kk]) != 0, isnan_ = false;
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
                 const double* Gt = a.G + (int64_t)t * mp * mp;
                 const double Y2 = Gt[m * mp + m];
-                const double eta = a.eta[t];
                 const double cjk = Gt[(int64_t)k * mp + j];
                 const double ck = Gt[m * mp + k];
                 const double d1 = fma(-cjk, cjk, 1.0);
-                const double r1 = 1.0 / d1;
+                const double r1 = rcp_newton(d1);
                 const double v1 = fma(-cjk, w0[t], ck);
                 const double base = Y2 - w0[t] * w0[t] - v1 * v1 * r1;
                 const double trh = 2.0 * r1;
-                const double At = 2.0 * eta * Y2 * (1.0 + 3.0 * trh);
-                const double Bt = 2.0 * eta * Y2 * 3.0 * (1.0 + trh);
+                double At, Bt, vk;
+                task_bound(a.eta[t], ref_gamma(a.rowsd[t], 3), a.rho_cap[t], Y2, a.ynorm[t], trh, At, Bt, vk);
                 L10[p][t] = cjk;
                 rd1[p][t] = r1;
                 w1[p][t] = v1;
-                Bq[p][t] = Bt;
-                kr += base - At;
-                if (!(d1 > 0.0) || !(eta * trh <= FO_LIM)) isbad = true;
+                kr += base - At - Bt * (1.0 / D_MIN);
+                if (!(d1 > 0.0) || !(vk * (1.0 + 3.0 * trh) <= FO_LIM)) isbad = true;
                 if (cjk != cjk || ck != ck || w0[t] != w0[t]) isnan_ = true;
             }
-            Kraw[p] = kr;
+            sKraw[p] = kr;
             if (j < k && k < m && !isnan_) valid |= 1u << p;
             if (isbad) bad |= 1u << p;
         }
@@ -179,7 +297,7 @@ __global__ void __launch_bounds__(256, 1) k_fit3(FitArgs a) {
             forced = bad;
 #pragma unroll
             for (int p = 0; p < P; ++p) {
-                double x = Kraw[p] - theta;
+                const double x = sKraw[p] - theta;
                 if (!(x > 0.0)) forced |= 1u << p;
                 Kq[p] = x * shrink;
             }
@@ -201,128 +319,123 @@ __global__ void __launch_bounds__(256, 1) k_fit3(FitArgs a) {
             }
             __syncthreads();
             const double* T0 = sm + buf * BS;
-#pragma unroll 2
-            for (int ii = 0; ii < IB; ++ii) {
+            // pending slow-path tuples of this tile: bit (ii * P + p)
+            constexpr int NPW = (IB * P + 31) / 32;  // pending-bit words
+            constexpr int IPW = 32 / P;              // rows per word
+            unsigned pend[NPW];
+#pragma unroll
+            for (int pw = 0; pw < NPW; ++pw) {
+            unsigned word = 0u;
+#pragma unroll(C::UNROLL)
+            for (int iw = 0; iw < IPW; ++iw) {
+                const int ii = pw * IPW + iw;
                 const int i = ib0 + ii;
                 double acc[P];
+                int hmin[P];
 #pragma unroll
-                for (int p = 0; p < P; ++p) acc[p] = Kq[p];
+                for (int p = 0; p < P; ++p) {
+                    acc[p] = Kq[p];
+                    hmin[p] = 0x7fffffff;
+                }
 #pragma unroll
                 for (int t = 0; t < NT; ++t) {
                     const double* Tt = T0 + t * TS;
                     const double g0 = Tt[ii * 32 + lane];
-                    const double ci = Tt[IB * 64 + ii];
+                    const double ci = Tt[IB * (32 + KSPAN) + ii];
                     const double D = fma(-g0, g0, 1.0);
                     const double V = fma(-g0, w0[t], ci);
-                    const double* kr = Tt + IB * 32 + ii * 32 + warp * P;
+                    double gk[P];
+                    if constexpr (P == 1) {
+                        gk[0] = Tt[IB * 32 + ii * KSPAN + warp];
+                    } else {
+#pragma unroll
+                        for (int p = 0; p < P; p += 2) {
+                            const double2 v =
+                                *reinterpret_cast<const double2*>(Tt + IB * 32 + ii * KSPAN + warp * P + p);
+                            gk[p] = v.x;
+                            gk[p + 1] = v.y;
+                        }
+                    }
 #pragma unroll
                     for (int p = 0; p < P; ++p) {
-                        const double g1 = fma(-L10[p][t], g0, kr[p]);
+                        const double g1 = fma(-L10[p][t], g0, gk[p]);
                         const double e1 = g1 * rd1[p][t];
                         const double d = fma(-g1, e1, D);
                         const double w = fma(-e1, w1[p][t], V);
-                        const double q = fma(w, w, Bq[p][t]);
+                        hmin[p] = min(hmin[p], __double2hiint(d));
                         if (NT == 1)
-                            acc[p] = fma(acc[p], d, -q);
+                            acc[p] = fma(acc[p], d, -(w * w));
                         else
-                            acc[p] = fma(-q, rcp_fast_abs(d), acc[p]);
+                            acc[p] = fma(-(w * w), rcp_fast_pos(d), acc[p]);
                     }
                 }
                 unsigned pass = forced;
 #pragma unroll
                 for (int p = 0; p < P; ++p)
-                    if (acc[p] < 0.0) pass |= 1u << p;
+                    if (acc[p] < 0.0 || hmin[p] < HI_DMIN) pass |= 1u << p;
+                if (i < m && a.iforce[i]) pass |= (1u << P) - 1;  // rho_i above rho_cap: bound needs the actual rho
                 pass &= valid;
                 if (!(i < j && i < i_hi)) pass = 0;
-                if (a.ranged && pass) {
-                    int64_t r3 = B3[m - 1 - i];
-#pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        int64_t rk = a.N_total - 1 - (r3 + hj + (m - 1 - (kbase + p)));
-                        if (rk < a.rank_lo || rk >= a.rank_hi) pass &= ~(1u << p);
-                    }
-                }
-                if (!__any_sync(L0S_FULL, pass)) continue;
+                word |= pass << (iw * P);
+            }
+            pend[pw] = word;
+            }
 
-                // ---------------- slow path (rare) ----------------
-                double lbv[P];
-                int kind[P];
-                int64_t rkv[P];
+            // ---------------- slow path (rare): one pending tuple per lane per round ----------------
+            const unsigned lt = lanemask_lt();
+            for (;;) {
+                int b = -1;
 #pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    kind[p] = 0;
-                    lbv[p] = 0.0;
-                    rkv[p] = 0;
-                    if (!((pass >> p) & 1u)) continue;
-                    const int k = kbase + p;
-                    rkv[p] = a.N_total - 1 - (B3[m - 1 - i] + B2[m - 1 - j] + (m - 1 - k));
-                    if ((bad >> p) & 1u) {
-                        kind[p] = 2;
-                        continue;
+                for (int w = 0; w < NPW; ++w)
+                    if (b < 0 && pend[w]) {
+                        b = w * 32 + __ffs(pend[w]) - 1;
+                        pend[w] &= pend[w] - 1u;
                     }
-                    bool good = true;
-                    double lb = Kraw[p];
-#pragma unroll
-                    for (int t = 0; t < NT; ++t) {
-                        const double* Tt = T0 + t * TS;
-                        const double g0 = Tt[ii * 32 + lane];
-                        const double ci = Tt[IB * 64 + ii];
-                        const double D = fma(-g0, g0, 1.0);
-                        const double V = fma(-g0, w0[t], ci);
-                        const double gk = Tt[IB * 32 + ii * 32 + warp * P + p];
-                        const double g1 = fma(-L10[p][t], g0, gk);
-                        const double e1 = g1 * rd1[p][t];
-                        const double d = fma(-g1, e1, D);
-                        const double w = fma(-e1, w1[p][t], V);
-                        const double q = fma(w, w, Bq[p][t]);
-                        const double eta = a.eta[t];
-                        const double trh = 2.0 * rd1[p][t];
-                        if (!(d > 0.0) || !(eta * (trh + (1.0 + trh) / d) <= FO_LIM)) good = false;
-                        lb -= q / d;
-                        // sufficient condition for the reference's rank rule:
-                        // prod q_f * prod pivots * min|a|^2 >= tol^2 * max|a|^2
-                        const double* qt = a.qf + (int64_t)t * m;
-                        const double* ut = a.un2 + (int64_t)t * m;
-                        const double d1 = fma(-L10[p][t], L10[p][t], 1.0);
-                        const double rho = qt[i] * qt[j] * qt[k] * d1 * d * RHO_SLACK;
-                        const double rt = a.rowsd[t];
-                        const double nmax = fmax(fmax(ut[i], ut[j]), fmax(ut[k], rt));
-                        const double nmin = fmin(fmin(ut[i], ut[j]), fmin(ut[k], rt));
-                        if (!(rho * nmin >= a.tol2 * nmax)) good = false;
-                    }
-                    if (!good)
-                        kind[p] = 2;
-                    else if (lb < theta) {
-                        kind[p] = 1;
-                        lbv[p] = lb;
+                if (!__any_sync(L0S_FULL, b >= 0)) break;
+                int kind = 0;
+                double lbv = 0.0;
+                int64_t rkv = 0;
+                if (b >= 0) {
+                    const int ii = b / P, p = b % P;
+                    const int i = ib0 + ii, k = kbase + p;
+                    rkv = a.N_total - 1 - (B3[m - 1 - i] + B2[m - 1 - j] + (m - 1 - k));
+                    if (a.ranged && (rkv < a.rank_lo || rkv >= a.rank_hi)) {
+                        kind = 0;
+                    } else if ((bad >> p) & 1u) {
+                        kind = 2;
+                    } else {
+                        double lb;
+                        const int fl = eval_tuple3(a, i, j, k, &lb);
+                        if (fl != 3)
+                            kind = 2;
+                        else if (lb < theta) {
+                            kind = 1;
+                            lbv = lb;
+                        }
                     }
                 }
-                const unsigned lt = lanemask_lt();
-#pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    const unsigned im = __ballot_sync(L0S_FULL, kind[p] == 1);
-                    if (im) {
-                        if (kind[p] == 1) {
-                            int pos = wcnt + __popc(im & lt);
-                            wlb[pos] = lbv[p];
-                            wrk[pos] = rkv[p];
-                        }
-                        wcnt += __popc(im);
+                const unsigned im = __ballot_sync(L0S_FULL, kind == 1);
+                if (im) {
+                    if (kind == 1) {
+                        int pos = wcnt + __popc(im & lt);
+                        wlb[pos] = lbv;
+                        wrk[pos] = rkv;
                     }
-                    const unsigned il = __ballot_sync(L0S_FULL, kind[p] == 2);
-                    if (il) {
-                        unsigned long long b0 = 0;
-                        const int leader = __ffs(il) - 1;
-                        if (lane == leader) b0 = atomicAdd(a.ill_cnt, (unsigned long long)__popc(il));
-                        b0 = __shfl_sync(L0S_FULL, b0, leader);
-                        if (kind[p] == 2) {
-                            unsigned long long idx = b0 + __popc(il & lt);
-                            if ((int64_t)idx < a.ill_cap) a.ill[idx] = rkv[p];
-                        }
+                    wcnt += __popc(im);
+                }
+                const unsigned il = __ballot_sync(L0S_FULL, kind == 2);
+                if (il) {
+                    unsigned long long b0 = 0;
+                    const int leader = __ffs(il) - 1;
+                    if (lane == leader) b0 = atomicAdd(a.ill_cnt, (unsigned long long)__popc(il));
+                    b0 = __shfl_sync(L0S_FULL, b0, leader);
+                    if (kind == 2) {
+                        unsigned long long idx = b0 + __popc(il & lt);
+                        if ((int64_t)idx < a.ill_cap) a.ill[idx] = rkv;
                     }
                 }
                 __syncwarp();
-                if (wcnt > CAP - 32 * P) {
+                if (wcnt > CAP - 32) {
                     if (a.collect) {
                         unsigned long long b0 = 0;
                         if (lane == 0) b0 = atomicAdd(a.coll_cnt, (unsigned long long)wcnt);
@@ -375,48 +488,15 @@ __global__ void __launch_bounds__(256, 1) k_fit3(FitArgs a) {
     }
 }
 
+
 // Same arithmetic as the fit kernel (hoist on (j, k), sweep variable i), one thread per explicit tuple.
-__global__ void k_screen3(FitArgs a, const int64_t* __restrict__ tuples, int64_t count, double* __restrict__ out_lb,
-                          int32_t* __restrict__ out_flags) {
+__global__ void k_screen3(const __grid_constant__ FitArgs a, const int64_t* __restrict__ tuples, int64_t count,
+                          double* __restrict__ out_lb, int32_t* __restrict__ out_flags) {
     int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= count) return;
-    const int64_t i = tuples[3 * c], j = tuples[3 * c + 1], k = tuples[3 * c + 2];
-    const int64_t m = a.m, mp = a.mp;
-    double lb = 0.0;
-    bool cond = true, rank_ok = true;
-    for (int t = 0; t < a.T; ++t) {
-        const double* Gt = a.G + (int64_t)t * mp * mp;
-        const double Y2 = Gt[m * mp + m], eta = a.eta[t];
-        const double w0 = Gt[m * mp + j];
-        const double cjk = Gt[k * mp + j], ck = Gt[m * mp + k];
-        const double d1 = fma(-cjk, cjk, 1.0);
-        const double r1 = 1.0 / d1;
-        const double v1 = fma(-cjk, w0, ck);
-        const double base = Y2 - w0 * w0 - v1 * v1 * r1;
-        const double trh = 2.0 * r1;
-        const double At = 2.0 * eta * Y2 * (1.0 + 3.0 * trh);
-        const double Bt = 2.0 * eta * Y2 * 3.0 * (1.0 + trh);
-        if (!(d1 > 0.0) || !(eta * trh <= FO_LIM)) cond = false;
-        const double g0 = Gt[i * mp + j], ci = Gt[i * mp + m], gk = Gt[i * mp + k];
-        const double D = fma(-g0, g0, 1.0);
-        const double V = fma(-g0, w0, ci);
-        const double g1 = fma(-cjk, g0, gk);
-        const double e1 = g1 * r1;
-        const double d = fma(-g1, e1, D);
-        const double w = fma(-e1, v1, V);
-        const double q = fma(w, w, Bt);
-        if (!(d > 0.0) || !(eta * (trh + (1.0 + trh) / d) <= FO_LIM)) cond = false;
-        lb += base - At - q / d;
-        const double* qt = a.qf + (int64_t)t * m;
-        const double* ut = a.un2 + (int64_t)t * m;
-        const double rho = qt[i] * qt[j] * qt[k] * d1 * d * RHO_SLACK;
-        const double rt = a.rowsd[t];
-        const double nmax = fmax(fmax(ut[i], ut[j]), fmax(ut[k], rt));
-        const double nmin = fmin(fmin(ut[i], ut[j]), fmin(ut[k], rt));
-        if (!(rho * nmin >= a.tol2 * nmax)) rank_ok = false;
-    }
+    double lb;
+    out_flags[c] = eval_tuple3(a, tuples[3 * c], tuples[3 * c + 1], tuples[3 * c + 2], &lb);
     out_lb[c] = lb;
-    out_flags[c] = (cond ? 1 : 0) | (rank_ok ? 2 : 0);
 }
 
 template <int NT>
@@ -440,7 +520,15 @@ void launch_screen3(const FitArgs& a, const int64_t* tuples, int64_t count, doub
 
 int fit3_max_tasks() { return 8; }
 int fit_slots_per_cta() { return NW; }
-int fit3_kspan(int T) { return T <= 4 ? Cfg<1>::KSPAN : Cfg<8>::KSPAN; }
+int fit3_kspan(int T) {
+    switch (T) {
+        case 1: return Cfg<1>::KSPAN;
+        case 2: return Cfg<2>::KSPAN;
+        case 3: return Cfg<3>::KSPAN;
+        case 4: return Cfg<4>::KSPAN;
+        default: return Cfg<8>::KSPAN;
+    }
+}
 int fit3_grid(int T, int nsm) {
     int per_sm = 0;
     switch (T) {

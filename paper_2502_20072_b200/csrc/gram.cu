@@ -115,7 +115,23 @@ __global__ void k_unit_diag(double* G, int64_t m, int64_t mp) {
         G[f * mp + f] = (d == d) ? 1.0 : d;  // keep NaN rows NaN (constant feature)
     }
 }
+__global__ void k_mark_dead(double* G, const int32_t* dead, int ndead, int T, int64_t mp) {
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)ndead * T * mp;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t x = e % mp;
+        int t = (int)((e / mp) % T);
+        int64_t f = dead[e / (mp * T)];
+        double* Gt = G + (int64_t)t * mp * mp;
+        Gt[f * mp + x] = nan;
+        Gt[x * mp + f] = nan;
+    }
+}
 }  // namespace
+
+void launch_mark_dead(double* G, const int32_t* dead, int ndead, int T, int64_t mp, cudaStream_t st) {
+    if (ndead > 0) k_mark_dead<<<256, 256, 0, st>>>(G, dead, ndead, T, mp);
+}
 
 void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_h, const int64_t* rpad_h, int T, int64_t m,
                  int64_t mp, double* G, cudaStream_t st) {

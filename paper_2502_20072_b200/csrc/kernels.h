@@ -23,6 +23,8 @@ void launch_normalize(const void* Xp, const void* yp, int precision, int64_t m, 
 // ---- Gram (gram.cu): G[t] = Z_t Z_t^T on DMMA, (mp x mp) per task, diag of features := 1 ----
 void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_h, const int64_t* rpad_h, int T,
                  int64_t m, int64_t mp, double* G, cudaStream_t st);
+// Features the reference's rank rule rejects in every tuple: NaN their Gram row and column (all tasks).
+void launch_mark_dead(double* G, const int32_t* dead, int ndead, int T, int64_t mp, cudaStream_t st);
 
 // ---- bit-exact Householder (exact.cu) ----
 struct ExactArgs {
@@ -58,6 +60,11 @@ struct FitArgs {
     const double* un2;       // [T][m]
     const double* rowsd;     // [T] rows per task as double
     const double* eta;       // [T] per-entry Gram error bound
+    const double* rho;       // [T][m] 1/sqrt(q): uncentered / centered norm ratio per feature
+    const double* rho_cap;   // [T] rho assumed for the sweep feature i unless it is flagged in iforce
+    const double* ynorm;     // [T] |y_t| (uncentered)
+    const unsigned char* iforce;  // [m] 1 = rho_i exceeds rho_cap: tuples with this i take the slow path
+    int n;                   // tuple dimension (for the reference's backward-error constant)
     const int64_t* binom;    // (n+1) x (m+1)
     const int4* units;       // unit table
     int n_units;

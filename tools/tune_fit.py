@@ -1,0 +1,83 @@
+"""Tuning sweep for the dim-3 fit kernel's (P, IB, CTAs/SM, unroll) choice.
+
+    python tools/tune_fit.py build            # here: compile the variants
+    python tools/tune_fit.py run [--m 2000]   # GPU box: time each variant on C3
+
+Each variant is a full libl0search.so built with a different L0S_CFG34 /
+L0S_CFG12 define; `run` loads each in its own process (L0S_LIB=...) and
+times the screened fit on the bench workload, checking that every variant
+returns the same models.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
+
+VARIANTS = {
+    "p2_ib16_b2_u1": ("L0S_C34_P=2", "L0S_C34_IB=16", "L0S_C34_MINB=2", "L0S_C34_UNROLL=1"),
+    "p2_ib16_b1_u1": ("L0S_C34_P=2", "L0S_C34_IB=16", "L0S_C34_MINB=1", "L0S_C34_UNROLL=1"),
+    "p1_ib16_b2_u1": ("L0S_C34_P=1", "L0S_C34_IB=16", "L0S_C34_MINB=2", "L0S_C34_UNROLL=1"),
+    "p1_ib32_b1_u2": ("L0S_C34_P=1", "L0S_C34_IB=32", "L0S_C34_MINB=1", "L0S_C34_UNROLL=2"),
+    "p4_ib32_b1_u1": ("L0S_C34_P=4", "L0S_C34_IB=32", "L0S_C34_MINB=1", "L0S_C34_UNROLL=1"),
+    "p2_ib32_b1_u2": ("L0S_C34_P=2", "L0S_C34_IB=32", "L0S_C34_MINB=1", "L0S_C34_UNROLL=2"),
+    "p1_ib16_b2_u2": ("L0S_C34_P=1", "L0S_C34_IB=16", "L0S_C34_MINB=2", "L0S_C34_UNROLL=2"),
+}
+
+
+def build_all():
+    from paper_2502_20072_b200 import build as b
+
+    os.makedirs(VDIR, exist_ok=True)
+    for name, defs in VARIANTS.items():
+        out = os.path.join(VDIR, f"lib_{name}.so")
+        b.build(force=True, defines=defs, out=out)
+        log = open(os.path.join(os.path.dirname(b.OBJ), "_obj_" + str(abs(hash(defs)) % 10**8), "ptxas.log")).read()
+        print(name, out)
+
+
+def time_one(steps: int = 5):
+    import numpy as np
+
+    import bench
+    from paper_2502_20072_b200 import _lib
+    from paper_2502_20072_b200.search import _partition
+
+    v, y, slices = bench.make_c3()
+    perm, bounds, _ = _partition(bench.S, slices)
+    eng = _lib.engine(0)
+    eng.stage(v, y, perm, bounds, "fp64")
+    res = []
+    for _ in range(steps + 2):
+        sc, rk, coef, ssr, st = eng.search(3, 10, 0, 2**62, "fast")
+        res.append((st.ms_fit, st.ms_total, st.n_candidates))
+    fit = sorted(r[0] for r in res[2:])
+    print(json.dumps({"fit_ms_min": fit[0], "fit_ms_med": fit[len(fit) // 2], "total_ms": res[-1][1],
+                      "ranks": rk.tolist(), "scores": [float(x) for x in sc]}))
+
+
+def run_all():
+    out = {}
+    for name in VARIANTS:
+        path = os.path.join(VDIR, f"lib_{name}.so")
+        env = dict(os.environ, L0S_LIB=path)
+        r = subprocess.run([sys.executable, __file__, "one"], env=env, capture_output=True, text=True, timeout=600)
+        line = [x for x in r.stdout.splitlines() if x.startswith("{")]
+        out[name] = json.loads(line[-1]) if line else {"error": r.stderr[-400:]}
+        print(name, {k: v for k, v in out[name].items() if k not in ("ranks", "scores")}, flush=True)
+    ref = next((o for o in out.values() if "ranks" in o), None)
+    for name, o in out.items():
+        if "ranks" in o:
+            assert o["ranks"] == ref["ranks"] and o["scores"] == ref["scores"], name
+    print("all variants agree")
+
+
+if __name__ == "__main__":
+    cmd = sys.argv[1] if len(sys.argv) > 1 else "run"
+    {"build": build_all, "run": run_all, "one": time_one}[cmd]()
