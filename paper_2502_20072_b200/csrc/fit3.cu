@@ -41,12 +41,6 @@ constexpr int CAP = 256;          // per-warp candidate buffer
 constexpr double FO_LIM = 1e-3;   // first-order validity: eta * trace(C^-1) <= FO_LIM
 constexpr double RANK_SLACK = 1.01;  // safety factor on the rank-rule certificate
 
-// Pivots below D_MIN (a power of two: its low word is zero, so the test is one
-// integer compare on the high word) send the tuple to the slow path; above it
-// the bound's B/d term is at most B/D_MIN and is folded into the per-pair constant.
-constexpr double D_MIN = 1.0 / 1024.0;
-constexpr int HI_DMIN = 0x3F500000;  // high word of 2^-10
-
 // Per task count: P = (j,k) pairs per thread, IB = rows per i-tile, MINB = CTAs per SM.
 // (P, IB, MINB, UNROLL) for 3-4 tasks; overridable (-DL0S_C34_P=... etc.) for tuning builds
 #ifndef L0S_C34_P
@@ -211,6 +205,7 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
     constexpr int P = C::P, IB = C::IB, TS = C::TS, BS = C::BS, KSPAN = C::KSPAN;
     extern __shared__ __align__(16) double sm[];
     __shared__ int s_unit;
+    __shared__ unsigned char s_force[2][IB];  // iforce flags of the staged rows
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     double* wlb = sm + 2 * BS + warp * CAP;
     int64_t* wrk = reinterpret_cast<int64_t*>(sm + 2 * BS + NW * CAP) + warp * CAP;
@@ -225,6 +220,7 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
     // tiles per task: C[i, j-block] (IB x 32), C[i, k-span] (IB x KSPAN), c_i (IB)
     auto load_tiles = [&](int buf, int ib0, int j0, int k0) {
         double* base = sm + buf * BS;
+        if (tid < IB) s_force[buf][tid] = (ib0 + tid < m) ? a.iforce[ib0 + tid] : 0;
         constexpr int pr = 16 + KSPAN / 2 + 1;  // 16-byte pieces per row (+ one 8-byte c_i)
         for (int q = tid; q < NT * IB * pr; q += 256) {
             const int t = q / (IB * pr), r = q % (IB * pr);
@@ -256,9 +252,9 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
         if (!a.collect) theta = fmin(theta, ord_dec(*(volatile unsigned long long*)a.theta_g));
 
         // ---------------- hoist: (j, k_p) state per task ----------------
-        // L10 = C_jk, rd1 = 1/(1 - C_jk^2), w1 = c_k - C_jk c_j; the bound's B/d term is
-        // folded into the constant for d >= D_MIN (tuples with a smaller pivot take the slow path)
-        double L10[P][NT], rd1[P][NT], w1[P][NT], w0[NT], Kq[P];
+        // L10 = C_jk, rd1 = 1/(1 - C_jk^2), s1 = rd1 (c_k - C_jk c_j); the bound's B_t/d term
+        // uses Bm = max_t B_t per pair, so the sweep needs one extra register per pair only
+        double L10[P][NT], rd1[P][NT], s1[P][NT], w0[NT], Kq[P], Bm[P];
         unsigned valid = 0, bad = 0, forced = 0;
 #pragma unroll
         for (int t = 0; t < NT; ++t) w0[t] = a.G[(int64_t)t * mp * mp + m * mp + j];
@@ -267,7 +263,7 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
         for (int p = 0; p < P; ++p) {
             const int k = kbase + p;
             const int kk = k < m ? k : (int)m - 1;
-            double kr = 0.0;
+            double kr = 0.0, bm = 0.0;
             bool isbad = (a.iforce[jj] | a.iforce[kk]) != 0, isnan_ = false;
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
@@ -284,12 +280,14 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
                 task_bound(a.eta[t], ref_gamma(a.rowsd[t], 3), a.rho_cap[t], Y2, a.ynorm[t], trh, At, Bt, vk);
                 L10[p][t] = cjk;
                 rd1[p][t] = r1;
-                w1[p][t] = v1;
-                kr += base - At - Bt * (1.0 / D_MIN);
+                s1[p][t] = v1 * r1;
+                kr += base - At;
+                bm = fmax(bm, Bt);
                 if (!(d1 > 0.0) || !(vk * (1.0 + 3.0 * trh) <= FO_LIM)) isbad = true;
                 if (cjk != cjk || ck != ck || w0[t] != w0[t]) isnan_ = true;
             }
             sKraw[p] = kr;
+            Bm[p] = bm;
             if (j < k && k < m && !isnan_) valid |= 1u << p;
             if (isbad) bad |= 1u << p;
         }
@@ -331,12 +329,8 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
                 const int ii = pw * IPW + iw;
                 const int i = ib0 + ii;
                 double acc[P];
-                int hmin[P];
 #pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    acc[p] = Kq[p];
-                    hmin[p] = 0x7fffffff;
-                }
+                for (int p = 0; p < P; ++p) acc[p] = Kq[p];
 #pragma unroll
                 for (int t = 0; t < NT; ++t) {
                     const double* Tt = T0 + t * TS;
@@ -358,22 +352,23 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
                     }
 #pragma unroll
                     for (int p = 0; p < P; ++p) {
+                        // lb_t = base_t - A_t - (w^2 + B_t)/d >= base_t - A_t - (w^2 + Bm)/d
                         const double g1 = fma(-L10[p][t], g0, gk[p]);
                         const double e1 = g1 * rd1[p][t];
+                        const double w = fma(-g1, s1[p][t], V);
                         const double d = fma(-g1, e1, D);
-                        const double w = fma(-e1, w1[p][t], V);
-                        hmin[p] = min(hmin[p], __double2hiint(d));
+                        const double q = fma(w, w, Bm[p]);
                         if (NT == 1)
-                            acc[p] = fma(acc[p], d, -(w * w));
+                            acc[p] = fma(acc[p], d, -q);  // (K - theta) d - q; d <= 0 also passes
                         else
-                            acc[p] = fma(-(w * w), rcp_fast_pos(d), acc[p]);
+                            acc[p] = fma(-q, rcp_fast_abs(d), acc[p]);  // 1/|d|: d <= 0 drives acc down
                     }
                 }
                 unsigned pass = forced;
 #pragma unroll
                 for (int p = 0; p < P; ++p)
-                    if (acc[p] < 0.0 || hmin[p] < HI_DMIN) pass |= 1u << p;
-                if (i < m && a.iforce[i]) pass |= (1u << P) - 1;  // rho_i above rho_cap: bound needs the actual rho
+                    if (acc[p] < 0.0) pass |= 1u << p;
+                if (s_force[buf][ii]) pass |= (1u << P) - 1;  // rho_i above rho_cap: bound needs the actual rho
                 pass &= valid;
                 if (!(i < j && i < i_hi)) pass = 0;
                 word |= pass << (iw * P);

