@@ -253,13 +253,23 @@ def install():
     bound at import (pipeline.py:34) and the package re-exports.  Returns a
     callable that restores the originals.
     """
+    import sys
+
     import descsearch
+    import descsearch.errors as ref_errors
+    import descsearch.models as ref_models
     import descsearch.pipeline as pipeline
     import descsearch.search as ref_search
 
+    me = sys.modules[__name__]
     saved = [(ref_search, "l0_search", ref_search.l0_search), (ref_search, "fit_tuple", ref_search.fit_tuple),
              (pipeline, "l0_search", pipeline.l0_search), (descsearch, "l0_search", descsearch.l0_search),
              (descsearch, "fit_tuple", descsearch.fit_tuple)]
+    # records and exceptions become the reference's own classes
+    for name, obj in (("Model", ref_models.Model), ("CapacityError", ref_errors.CapacityError),
+                      ("RankDeficient", ref_search.RankDeficient), ("RankOutOfRange", ref_search.RankOutOfRange)):
+        saved.append((me, name, getattr(me, name)))
+        setattr(me, name, obj)
     ref_search.l0_search = l0_search
     ref_search.fit_tuple = fit_tuple
     pipeline.l0_search = l0_search
