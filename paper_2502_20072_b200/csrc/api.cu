@@ -492,7 +492,7 @@ static void fill_fit_common(l0s_ctx* c, FitArgs& a, int n) {
 
 int l0s_screen_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags) {
     if (!c || !c->staged) return fail(L0S_ESTATE, "l0s_stage must be called first");
-    if (n != 3) return fail(L0S_EINVAL, "screened bounds are implemented for n = 3");
+    if (n != 3 && n != 4) return fail(L0S_EINVAL, "screened bounds are implemented for n = 3 and 4");
     if (count <= 0) return L0S_OK;
     CK(cudaSetDevice(c->dev));
     int rc = ensure_binom(c, n);
@@ -503,7 +503,10 @@ int l0s_screen_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, d
     CK(c->cand_lb.ensure(sizeof(double) * count));
     CK(c->ex_ok.ensure(sizeof(int32_t) * count));
     CK(cudaMemcpyAsync(c->ex_tuples.p, tuples, sizeof(int64_t) * count * n, cudaMemcpyHostToDevice, c->st));
-    launch_screen3(a, c->ex_tuples.as<int64_t>(), count, c->cand_lb.as<double>(), c->ex_ok.as<int32_t>(), c->st);
+    if (n == 3)
+        launch_screen3(a, c->ex_tuples.as<int64_t>(), count, c->cand_lb.as<double>(), c->ex_ok.as<int32_t>(), c->st);
+    else
+        launch_screen4(a, c->ex_tuples.as<int64_t>(), count, c->cand_lb.as<double>(), c->ex_ok.as<int32_t>(), c->st);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out_lb, c->cand_lb.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(out_flags, c->ex_ok.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, c->st));
@@ -568,15 +571,17 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     // unit table (cached per problem shape and rank range)
     int64_t key[5] = {c->m, c->T, rb, re, n};
     if (!std::equal(key, key + 5, c->units_key)) {
-        std::vector<int64_t> c2((size_t)c->m + 1, 0);
-        for (int64_t v = 0; v < c->m; ++v) c2[(size_t)v + 1] = c2[(size_t)v] + binom_sat(c->m - 1 - v, 2);
-        c->units_h = fit3_units(c->m, c->T, N, c2, rb, re);
+        // prefix[v] = rank of the first tuple whose smallest index is v
+        std::vector<int64_t> pre((size_t)c->m + 1, 0);
+        for (int64_t v = 0; v < c->m; ++v) pre[(size_t)v + 1] = pre[(size_t)v] + binom_sat(c->m - 1 - v, n - 1);
+        c->units_h = n == 3 ? fit3_units(c->m, c->T, N, pre, rb, re) : fit4_units(c->m, c->T, pre, rb, re);
         CK(c->units.ensure(sizeof(int4) * std::max<size_t>(c->units_h.size(), 1)));
         CK(cudaMemcpyAsync(c->units.p, c->units_h.data(), sizeof(int4) * c->units_h.size(), cudaMemcpyHostToDevice, c->st));
         std::copy(key, key + 5, c->units_key);
     }
     const int kc = (int)std::min<int64_t>(128, std::max<int64_t>(64, keep + 32));
-    const int grid = fit3_grid(c->T, c->nsm);
+    const int grid = n == 3 ? fit3_grid(c->T, c->nsm) : fit4_grid(c->T, c->nsm);
+    auto launch_fit = [&](const FitArgs& fa) { return n == 3 ? fit3_launch(fa, c->nsm, c->st) : fit4_launch(fa, c->nsm, c->st); };
     const int slots = grid * fit_slots_per_cta();
     const int64_t ill_cap = (int64_t)1 << 22;
     CK(c->ucount.ensure(sizeof(int) * 4));
@@ -619,7 +624,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     CK(cudaMemsetAsync(c->ill_cnt.p, 0, sizeof(unsigned long long), c->st));
     CK(cudaMemsetAsync(c->cand_cnt.p, 0, sizeof(unsigned long long), c->st));
     cudaEventRecord(c->ev[2], c->st);
-    fit3_launch(a, c->nsm, c->st);
+    launch_fit(a);
     cudaEventRecord(c->ev[3], c->st);
     CK(cudaGetLastError());
     st->n_fit_launches++;
@@ -689,7 +694,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
         a.coll_cnt = c->coll_cnt.as<unsigned long long>();
         a.coll_cap = coll_cap;
         cudaEventRecord(c->ev[2], c->st);
-        fit3_launch(a, c->nsm, c->st);
+        launch_fit(a);
         cudaEventRecord(c->ev[3], c->st);
         CK(cudaGetLastError());
         st->n_fit_launches++;
@@ -737,13 +742,14 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
     cudaEventCreate(&t1);
     cudaEventRecord(t0, c->st);
     // the screen's error model is for fp64 arithmetic in the reference (precision="fp64")
-    bool fast_ok = (n == 3) && c->T <= fit3_max_tasks() && keep <= 96 && c->prec == L0S_PREC_FP64;
+    bool fast_ok = (n == 3 || n == 4) && c->T <= fit3_max_tasks() && keep <= 96 && c->prec == L0S_PREC_FP64;
     bool use_fast;
     if (mode == L0S_MODE_FAST) {
         if (!fast_ok) {
             cudaEventDestroy(t0);
             cudaEventDestroy(t1);
-            return fail(L0S_EINVAL, "screened path needs n == 3, ntasks <= %d, keep <= 96, fp64", fit3_max_tasks());
+            return fail(L0S_EINVAL, "screened path needs n in {3, 4}, ntasks <= %d, keep <= 96, fp64",
+                        fit3_max_tasks());
         }
         use_fast = true;
     } else if (mode == L0S_MODE_EXACT) {

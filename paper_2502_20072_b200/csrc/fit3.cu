@@ -6,42 +6,34 @@
 //
 //   per task t, column order [j, k, i] of the centered, unit-norm features,
 //   LDL^T of the 3x3 correlation block plus the property row:
-//     hoisted once per (j, k) pair:   d1 = 1 - C_jk^2,  w1 = c_k - C_jk c_j,
-//                                     base = |y_c|^2 - c_j^2 - w1^2 / d1
+//     hoisted once per (j, k) pair:   d1 = 1 - C_jk^2,  s1 = (c_k - C_jk c_j) / d1,
+//                                     base = |y_c|^2 - c_j^2 - (c_k - C_jk c_j)^2 / d1
 //     per i (6 FP64 ops + 1 MUFU):    g1 = C_ik - C_jk C_ij,  e1 = g1 / d1,
 //                                     d  = 1 - C_ij^2 - g1 e1,
-//                                     w  = c_i - C_ij c_j - e1 w1,
+//                                     w  = c_i - C_ij c_j - g1 s1,
 //                                     ssr_t = base - w^2 / d
-//   and a rigorous first-order error bound E_t = A_t + B_t / d from the
-//   per-entry Gram error eta_t ("error model"), so that
-//       lb = sum_t (ssr_t - E_t)  <=  the reference's pooled SSR.
-//   lb / s is compared against the running threshold; the rare tuples that
-//   pass take the slow path: exact division, the conditioning check, the
-//   sufficient test for the reference's rank rule (|R_jj| >= 1e-10 max|R|,
-//   lsq.py:96-101) and insertion into a per-warp top-K' buffer, or routing
-//   to the exact Householder kernel when the bound cannot be trusted.
+//   with the rigorous bound of fitcommon.cuh so that
+//       lb = sum_t (ssr_t - A_t - B_t / d_t)  <=  the reference's pooled SSR.
+//   lb is compared against the running threshold; the rare tuples that pass
+//   are evaluated after the i-tile by the out-of-line slow path (exact bound,
+//   conditioning, rank-rule certificate) and inserted into the warp's top-K'
+//   list, or routed to the bit-exact kernel.
 //
 // Layout: one unit = 32 j (lanes) x KSPAN k (8 warps x P) x up to 128 i.
 // The i-dependent Gram rows C[i, j-block], C[i, k-span], c_i are staged in
-// shared memory by cp.async (double-buffered over 32-row i-blocks); the
-// (j, k) state lives in registers.  Persistent CTAs pull units from an
-// atomic counter.
+// shared memory by cp.async (double-buffered over IB-row tiles); the (j, k)
+// state lives in registers.  Persistent CTAs pull units from an atomic counter.
 #include <algorithm>
 #include <vector>
 
-#include "common.cuh"
-#include "kernels.h"
+#include "fitcommon.cuh"
 
 namespace l0s {
 
+using namespace fit;
+
 namespace {
 
-constexpr int NW = 8;
-constexpr int CAP = 256;          // per-warp candidate buffer
-constexpr double FO_LIM = 1e-3;   // first-order validity: eta * trace(C^-1) <= FO_LIM
-constexpr double RANK_SLACK = 1.01;  // safety factor on the rank-rule certificate
-
-// Per task count: P = (j,k) pairs per thread, IB = rows per i-tile, MINB = CTAs per SM.
 // (P, IB, MINB, UNROLL) for 3-4 tasks; overridable (-DL0S_C34_P=... etc.) for tuning builds
 #ifndef L0S_C34_P
 #define L0S_C34_P 4
@@ -61,6 +53,7 @@ struct CfgT {
 constexpr CfgT kCfg34{L0S_C34_P, L0S_C34_IB, L0S_C34_MINB, L0S_C34_UNROLL};
 constexpr CfgT kCfg12{4, 32, 2, 2};
 constexpr CfgT kCfg58{2, 16, 1, 1};
+// Per task count: P = (j,k) pairs per thread, IB = rows per i-tile, MINB = CTAs per SM.
 template <int NT>
 struct Cfg {
     static constexpr CfgT c = (NT <= 2) ? kCfg12 : (NT <= 4 ? kCfg34 : kCfg58);
@@ -73,36 +66,6 @@ struct Cfg {
     static constexpr int UNROLL = c.UNROLL;  // rows of the i sweep in flight per thread
     static constexpr size_t smem_bytes = (size_t)2 * BS * 8 + (size_t)NW * CAP * 16 + (size_t)256 * P * 8;
 };
-
-// Error model: for one task, with tr = trace of the inverse of the
-// normalized 3x3 block (tr <= trh + (1 + trh)/d, trh = hoisted 2x2 trace),
-//   |ssr_gram - ssr_true| <= 2 eta Y2 (1 + 3 tr)                (Gram entries, |dC| <= eta)
-//   |ssr_ref  - ssr_true| <= 4 gam |y_c| |y| + 2 gam rho Y2 (1 + 3 tr)
-//                           (reference Householder QR, columnwise backward error gam,
-//                            rho = max |f|/|f_c| over the tuple's features)
-// so ssr_ref >= ssr_gram - A - B/d with
-//   A = 4 gam |y_c||y| + K Y2 (1 + 3 trh),  B = 3 K Y2 (1 + trh),  K = 2 (eta + gam rho),
-// valid while (eta + gam rho)(1 + 3 tr) <= FO_LIM (first-order terms dominate).
-__device__ __forceinline__ void task_bound(double eta, double gam, double rho, double Y2, double yn, double trh,
-                                           double& A, double& B, double& vk) {
-    vk = eta + gam * rho;
-    const double K = 2.0 * vk;
-    // 4 gam |y_c| |y| <= 2 gam (|y_c|^2 + |y|^2): no square root on the device
-    A = 2.0 * gam * (Y2 + yn * yn) + K * Y2 * (1.0 + 3.0 * trh);
-    B = 3.0 * K * Y2 * (1.0 + trh);
-}
-// 1/d without the IEEE-division subroutine call: MUFU seed + two Newton steps
-// (a few ulp; the error model's eta slack covers it).  Garbage for d <= 0, which
-// every caller rejects separately.
-__device__ __forceinline__ double rcp_newton(double d) {
-    double r = rcp_fast_pos(d);
-    double e = fma(-d, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-d, r, 1.0);
-    return fma(r, e, r);
-}
-__device__ __forceinline__ double ref_gamma(double rows, int n) { return 2.0 * (rows + 1.0) * (n + 2) * kEps; }
-constexpr double LOOSE = 1e-6;  // bounds looser than this fraction of |y_c|^2 go to the exact kernel
 
 // Exact lower bound of one tuple (i < j < k) read straight from the Gram, with the
 // arithmetic of the sweep (hoist on (j, k), i appended last).  Returns
@@ -128,7 +91,7 @@ __device__ __noinline__ int eval_tuple3(const FitArgs& a, int64_t i, int64_t j, 
         const double* rt_ = a.rho + (int64_t)t * m;
         const double rx = fmax(rt_[i], fmax(rt_[j], rt_[k]));
         double At, Bt, vk;
-        task_bound(a.eta[t], ref_gamma(a.rowsd[t], 3), rx, Y2, a.ynorm[t], trh, At, Bt, vk);
+        task_bound(3, a.eta[t], ref_gamma(a.rowsd[t], 3), rx, Y2, a.ynorm[t], trh, At, Bt, vk);
         if (!(d1 > 0.0) || !(vk * (1.0 + 3.0 * trh) <= FO_LIM)) cond = false;
         const double g0 = Gt[i * mp + j], ci = Gt[i * mp + m], gk = Gt[i * mp + k];
         const double D = fma(-g0, g0, 1.0);
@@ -140,63 +103,11 @@ __device__ __noinline__ int eval_tuple3(const FitArgs& a, int64_t i, int64_t j, 
         const double tr = trh + (1.0 + trh) / d;
         if (!(d > 0.0) || !(vk * (1.0 + 3.0 * tr) <= FO_LIM) || !(At + Bt / d <= LOOSE * Y2)) cond = false;
         lb += base - At - fma(w, w, Bt) / d;
-        // Sufficient condition for the reference's rank rule |R_jj| >= tol max|R_jj|
-        // (lsq.py:96-101), columns [f_c0, f_c1, f_c2, 1] uncentered:
-        //   every R_jj^2 >= sigma_min([F, 1])^2 >= min(min_f |f_c|^2 / tr, r) / (1 + |mu|)^2,
-        //   max R_jj^2 <= max(max_f |f|^2, r),  (1 + |mu|)^2 <= 2 (1 + sum_f mean_f^2),
-        // with tr = trace(C^-1) >= 1 / lambda_min(C); tr carries <= FO_LIM relative error.
-        const double* qt = a.qf + (int64_t)t * m;
-        const double* ut = a.un2 + (int64_t)t * m;
-        const double rt = a.rowsd[t];
-        const double trs = tr * (1.0 + 4.0 * FO_LIM);
-        const double fc_min = fmin(fmin(ut[i] * qt[i], ut[j] * qt[j]), ut[k] * qt[k]);
-        const double mu2 = (ut[i] * (1.0 - qt[i]) + ut[j] * (1.0 - qt[j]) + ut[k] * (1.0 - qt[k])) / rt;
-        const double lo = fmin(fc_min / trs, rt) / (2.0 * (1.0 + mu2));
-        const double hi = fmax(fmax(ut[i], ut[j]), fmax(ut[k], rt));
-        const double gam = ref_gamma(rt, 3);
-        const double tl = sqrt(a.tol2) + 4.0 * gam;  // slack for the reference's rounding of R
-        if (!(lo >= tl * tl * hi * RANK_SLACK)) rank_ok = false;
+        const int64_t f[3] = {i, j, k};
+        if (!rank_certain<3>(a, t, f, tr)) rank_ok = false;
     }
     *lb_out = lb;
     return (cond ? 1 : 0) | (rank_ok ? 2 : 0);
-}
-
-__device__ __forceinline__ unsigned lanemask_lt() {
-    unsigned r;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
-    return r;
-}
-
-__device__ __forceinline__ bool cand_gt(double a, int64_t ra, double b, int64_t rb) {
-    return a > b || (a == b && ra > rb);
-}
-
-// Warp-wide bitonic sort of the CAP-entry buffer by (lb, rank); entries [cnt, CAP) are padding.
-__device__ void warp_sort(double* lb, int64_t* rk, int cnt, int lane) {
-    for (int x = cnt + lane; x < CAP; x += 32) {
-        lb[x] = __longlong_as_double(0x7ff0000000000000ll);
-        rk[x] = 0x7fffffffffffffffll;
-    }
-    __syncwarp();
-    for (int k = 2; k <= CAP; k <<= 1) {
-        for (int jj = k >> 1; jj > 0; jj >>= 1) {
-            for (int x = lane; x < CAP; x += 32) {
-                int y = x ^ jj;
-                if (y > x) {
-                    bool up = (x & k) == 0;
-                    double a = lb[x], b = lb[y];
-                    int64_t ra = rk[x], rb = rk[y];
-                    if (cand_gt(a, ra, b, rb) == up) {
-                        lb[x] = b;
-                        lb[y] = a;
-                        rk[x] = rb;
-                        rk[y] = ra;
-                    }
-                }
-            }
-            __syncwarp();
-        }
-    }
 }
 
 template <int NT>
@@ -207,13 +118,11 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
     __shared__ int s_unit;
     __shared__ unsigned char s_force[2][IB];  // iforce flags of the staged rows
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    double* wlb = sm + 2 * BS + warp * CAP;
-    int64_t* wrk = reinterpret_cast<int64_t*>(sm + 2 * BS + NW * CAP) + warp * CAP;
     double* sKraw = sm + 2 * BS + 2 * NW * CAP + tid * P;  // per-thread, slow path / threshold updates only
     const int64_t m = a.m, mp = a.mp;
     const double shrink = (NT == 1) ? 1.0 : (1.0 - 2.0 * kRcpRel);
-    int wcnt = 0;
-    double theta = a.collect ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g);
+    WarpCands wc{sm + 2 * BS + warp * CAP, reinterpret_cast<int64_t*>(sm + 2 * BS + NW * CAP) + warp * CAP, 0,
+                 a.collect ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g)};
     const int64_t* B2 = a.binom + 2 * (m + 1);
     const int64_t* B3 = a.binom + 3 * (m + 1);
 
@@ -249,7 +158,7 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
         const int kbase = k0 + warp * P;
         const int i_lo = U.z, i_hi = U.w;
         load_tiles(0, i_lo, j0, k0);
-        if (!a.collect) theta = fmin(theta, ord_dec(*(volatile unsigned long long*)a.theta_g));
+        if (!a.collect) wc.theta = fmin(wc.theta, ord_dec(*(volatile unsigned long long*)a.theta_g));
 
         // ---------------- hoist: (j, k_p) state per task ----------------
         // L10 = C_jk, rd1 = 1/(1 - C_jk^2), s1 = rd1 (c_k - C_jk c_j); the bound's B_t/d term
@@ -277,7 +186,7 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
                 const double base = Y2 - w0[t] * w0[t] - v1 * v1 * r1;
                 const double trh = 2.0 * r1;
                 double At, Bt, vk;
-                task_bound(a.eta[t], ref_gamma(a.rowsd[t], 3), a.rho_cap[t], Y2, a.ynorm[t], trh, At, Bt, vk);
+                task_bound(3, a.eta[t], ref_gamma(a.rowsd[t], 3), a.rho_cap[t], Y2, a.ynorm[t], trh, At, Bt, vk);
                 L10[p][t] = cjk;
                 rd1[p][t] = r1;
                 s1[p][t] = v1 * r1;
@@ -295,14 +204,12 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
             forced = bad;
 #pragma unroll
             for (int p = 0; p < P; ++p) {
-                const double x = sKraw[p] - theta;
+                const double x = sKraw[p] - wc.theta;
                 if (!(x > 0.0)) forced |= 1u << p;
                 Kq[p] = x * shrink;
             }
         };
         set_kq();
-        int64_t hj = 0;
-        if (a.ranged && j < m) hj = B2[m - 1 - j];
 
         // ---------------- sweep i ----------------
         const int nib = (i_hi - i_lo + IB - 1) / IB;
@@ -323,166 +230,76 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
             unsigned pend[NPW];
 #pragma unroll
             for (int pw = 0; pw < NPW; ++pw) {
-            unsigned word = 0u;
+                unsigned word = 0u;
 #pragma unroll(C::UNROLL)
-            for (int iw = 0; iw < IPW; ++iw) {
-                const int ii = pw * IPW + iw;
-                const int i = ib0 + ii;
-                double acc[P];
+                for (int iw = 0; iw < IPW; ++iw) {
+                    const int ii = pw * IPW + iw;
+                    const int i = ib0 + ii;
+                    double acc[P];
 #pragma unroll
-                for (int p = 0; p < P; ++p) acc[p] = Kq[p];
+                    for (int p = 0; p < P; ++p) acc[p] = Kq[p];
 #pragma unroll
-                for (int t = 0; t < NT; ++t) {
-                    const double* Tt = T0 + t * TS;
-                    const double g0 = Tt[ii * 32 + lane];
-                    const double ci = Tt[IB * (32 + KSPAN) + ii];
-                    const double D = fma(-g0, g0, 1.0);
-                    const double V = fma(-g0, w0[t], ci);
-                    double gk[P];
-                    if constexpr (P == 1) {
-                        gk[0] = Tt[IB * 32 + ii * KSPAN + warp];
-                    } else {
+                    for (int t = 0; t < NT; ++t) {
+                        const double* Tt = T0 + t * TS;
+                        const double g0 = Tt[ii * 32 + lane];
+                        const double ci = Tt[IB * (32 + KSPAN) + ii];
+                        const double D = fma(-g0, g0, 1.0);
+                        const double V = fma(-g0, w0[t], ci);
+                        double gk[P];
+                        if constexpr (P == 1) {
+                            gk[0] = Tt[IB * 32 + ii * KSPAN + warp];
+                        } else {
 #pragma unroll
-                        for (int p = 0; p < P; p += 2) {
-                            const double2 v =
-                                *reinterpret_cast<const double2*>(Tt + IB * 32 + ii * KSPAN + warp * P + p);
-                            gk[p] = v.x;
-                            gk[p + 1] = v.y;
+                            for (int p = 0; p < P; p += 2) {
+                                const double2 v =
+                                    *reinterpret_cast<const double2*>(Tt + IB * 32 + ii * KSPAN + warp * P + p);
+                                gk[p] = v.x;
+                                gk[p + 1] = v.y;
+                            }
+                        }
+#pragma unroll
+                        for (int p = 0; p < P; ++p) {
+                            // lb_t = base_t - A_t - (w^2 + B_t)/d >= base_t - A_t - (w^2 + Bm)/d
+                            const double g1 = fma(-L10[p][t], g0, gk[p]);
+                            const double e1 = g1 * rd1[p][t];
+                            const double w = fma(-g1, s1[p][t], V);
+                            const double d = fma(-g1, e1, D);
+                            const double q = fma(w, w, Bm[p]);
+                            if (NT == 1)
+                                acc[p] = fma(acc[p], d, -q);  // (K - theta) d - q; d <= 0 also passes
+                            else
+                                acc[p] = fma(-q, rcp_fast_abs(d), acc[p]);  // 1/|d|: d <= 0 drives acc down
                         }
                     }
+                    unsigned pass = forced;
 #pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        // lb_t = base_t - A_t - (w^2 + B_t)/d >= base_t - A_t - (w^2 + Bm)/d
-                        const double g1 = fma(-L10[p][t], g0, gk[p]);
-                        const double e1 = g1 * rd1[p][t];
-                        const double w = fma(-g1, s1[p][t], V);
-                        const double d = fma(-g1, e1, D);
-                        const double q = fma(w, w, Bm[p]);
-                        if (NT == 1)
-                            acc[p] = fma(acc[p], d, -q);  // (K - theta) d - q; d <= 0 also passes
-                        else
-                            acc[p] = fma(-q, rcp_fast_abs(d), acc[p]);  // 1/|d|: d <= 0 drives acc down
-                    }
+                    for (int p = 0; p < P; ++p)
+                        if (acc[p] < 0.0) pass |= 1u << p;
+                    if (s_force[buf][ii]) pass |= (1u << P) - 1;  // rho_i above rho_cap: needs the actual rho
+                    pass &= valid;
+                    if (!(i < j && i < i_hi)) pass = 0;
+                    word |= pass << (iw * P);
                 }
-                unsigned pass = forced;
-#pragma unroll
-                for (int p = 0; p < P; ++p)
-                    if (acc[p] < 0.0) pass |= 1u << p;
-                if (s_force[buf][ii]) pass |= (1u << P) - 1;  // rho_i above rho_cap: bound needs the actual rho
-                pass &= valid;
-                if (!(i < j && i < i_hi)) pass = 0;
-                word |= pass << (iw * P);
-            }
-            pend[pw] = word;
+                pend[pw] = word;
             }
 
-            // ---------------- slow path (rare): one pending tuple per lane per round ----------------
-            const unsigned lt = lanemask_lt();
-            for (;;) {
-                int b = -1;
-#pragma unroll
-                for (int w = 0; w < NPW; ++w)
-                    if (b < 0 && pend[w]) {
-                        b = w * 32 + __ffs(pend[w]) - 1;
-                        pend[w] &= pend[w] - 1u;
-                    }
-                if (!__any_sync(L0S_FULL, b >= 0)) break;
-                int kind = 0;
-                double lbv = 0.0;
-                int64_t rkv = 0;
-                if (b >= 0) {
+            // ---------------- slow path (rare), after the tile ----------------
+            drain_pending<NPW>(
+                a, pend, wc, lane,
+                [&](int b, double* lbv, int64_t* rkv) -> int {
                     const int ii = b / P, p = b % P;
                     const int i = ib0 + ii, k = kbase + p;
-                    rkv = a.N_total - 1 - (B3[m - 1 - i] + B2[m - 1 - j] + (m - 1 - k));
-                    if (a.ranged && (rkv < a.rank_lo || rkv >= a.rank_hi)) {
-                        kind = 0;
-                    } else if ((bad >> p) & 1u) {
-                        kind = 2;
-                    } else {
-                        double lb;
-                        const int fl = eval_tuple3(a, i, j, k, &lb);
-                        if (fl != 3)
-                            kind = 2;
-                        else if (lb < theta) {
-                            kind = 1;
-                            lbv = lb;
-                        }
-                    }
-                }
-                const unsigned im = __ballot_sync(L0S_FULL, kind == 1);
-                if (im) {
-                    if (kind == 1) {
-                        int pos = wcnt + __popc(im & lt);
-                        wlb[pos] = lbv;
-                        wrk[pos] = rkv;
-                    }
-                    wcnt += __popc(im);
-                }
-                const unsigned il = __ballot_sync(L0S_FULL, kind == 2);
-                if (il) {
-                    unsigned long long b0 = 0;
-                    const int leader = __ffs(il) - 1;
-                    if (lane == leader) b0 = atomicAdd(a.ill_cnt, (unsigned long long)__popc(il));
-                    b0 = __shfl_sync(L0S_FULL, b0, leader);
-                    if (kind == 2) {
-                        unsigned long long idx = b0 + __popc(il & lt);
-                        if ((int64_t)idx < a.ill_cap) a.ill[idx] = rkv;
-                    }
-                }
-                __syncwarp();
-                if (wcnt > CAP - 32) {
-                    if (a.collect) {
-                        unsigned long long b0 = 0;
-                        if (lane == 0) b0 = atomicAdd(a.coll_cnt, (unsigned long long)wcnt);
-                        b0 = __shfl_sync(L0S_FULL, b0, 0);
-                        for (int x = lane; x < wcnt; x += 32)
-                            if ((int64_t)(b0 + x) < a.coll_cap) {
-                                a.coll_lb[b0 + x] = wlb[x];
-                                a.coll_rank[b0 + x] = wrk[x];
-                            }
-                        wcnt = 0;
-                        __syncwarp();
-                    } else {
-                        warp_sort(wlb, wrk, wcnt, lane);
-                        if (wcnt > a.kc) wcnt = a.kc;
-                        if (wcnt == a.kc && wlb[a.kc - 1] < theta) {
-                            theta = wlb[a.kc - 1];
-                            if (lane == 0) atomicMin(a.theta_g, ord_enc(theta));
-                            set_kq();
-                        }
-                        __syncwarp();
-                    }
-                }
-            }
+                    *rkv = a.N_total - 1 - (B3[m - 1 - i] + B2[m - 1 - j] + (m - 1 - k));
+                    if (a.ranged && (*rkv < a.rank_lo || *rkv >= a.rank_hi)) return 0;
+                    if ((bad >> p) & 1u) return 2;
+                    return eval_tuple3(a, i, j, k, lbv) == 3 ? 1 : 2;
+                },
+                set_kq);
             __syncthreads();
         }
     }
-    // ---------------- flush ----------------
-    const int slot = blockIdx.x * NW + warp;
-    if (a.collect) {
-        unsigned long long b0 = 0;
-        if (lane == 0 && wcnt > 0) b0 = atomicAdd(a.coll_cnt, (unsigned long long)wcnt);
-        b0 = __shfl_sync(L0S_FULL, b0, 0);
-        for (int x = lane; x < wcnt; x += 32)
-            if ((int64_t)(b0 + x) < a.coll_cap) {
-                a.coll_lb[b0 + x] = wlb[x];
-                a.coll_rank[b0 + x] = wrk[x];
-            }
-        if (lane == 0) a.wl_cnt[slot] = 0;
-    } else {
-        warp_sort(wlb, wrk, wcnt, lane);
-        if (wcnt > a.kc) wcnt = a.kc;
-        for (int x = lane; x < wcnt; x += 32) {
-            a.wl_lb[(int64_t)slot * a.kc + x] = wlb[x];
-            a.wl_rank[(int64_t)slot * a.kc + x] = wrk[x];
-        }
-        if (lane == 0) {
-            a.wl_cnt[slot] = wcnt;
-            if (wcnt == a.kc) atomicMin(a.theta_g, ord_enc(wlb[a.kc - 1]));
-        }
-    }
+    flush_warp(a, wc, blockIdx.x * NW + warp, lane);
 }
-
 
 // Same arithmetic as the fit kernel (hoist on (j, k), sweep variable i), one thread per explicit tuple.
 __global__ void k_screen3(const __grid_constant__ FitArgs a, const int64_t* __restrict__ tuples, int64_t count,

@@ -1,0 +1,381 @@
+// fit4.cu -- screened exhaustive fit of every 4-tuple (i < j < k < l), fp64.
+//
+// Same scheme as fit3.cu with one more hoisted column.  Column order of the
+// centered, unit-norm LDL^T is [j, k, l, i]:
+//   hoisted per (j, k) (shared by the thread's P tuples) and per (j, k, l_p),
+//   per i and task: g0 = C_ij, g1 = C_ik - C_jk g0 (shared across l_p),
+//                   g2 = C_il - L20 g0 - L21 g1,
+//                   d  = 1 - g0^2 - g1^2/d1 - g2^2/d2,  w = c_i - g0 c_j - g1 s1 - g2 s2,
+//                   ssr_t = base - w^2/d   (7 FP64 ops per tuple-task + 6 shared per row)
+// with the bound and certificates of fitcommon.cuh (n = 4).
+//
+// Unit = (32 j in lanes) x one k x (8 warps x P l's) x up to 128 i; the unit
+// table stores (j-block | l-block << 16, k, i_lo, i_hi).
+#include <algorithm>
+#include <vector>
+
+#include "fitcommon.cuh"
+
+namespace l0s {
+
+using namespace fit;
+
+namespace {
+
+template <int NT>
+struct Cfg4 {
+    static constexpr int P = (NT <= 2) ? 4 : 2;
+    static constexpr int IB = (NT <= 2) ? 32 : 16;
+    static constexpr int LSPAN = NW * P;
+    static constexpr int TS = IB * (32 + LSPAN + 2);  // C[i, j-block] | C[i, l-span] | C[i, k] | c_i
+    static constexpr int BS = NT * TS;
+    static constexpr size_t smem_bytes = (size_t)2 * BS * 8 + (size_t)NW * CAP * 16 + (size_t)256 * P * 8;
+};
+
+// Hoisted LDL^T of (j, k, l) for one task (normalized, centered), plus the bound's trace term.
+struct Hoist3 {
+    double L10, rd1, s1, w0;   // (j, k) part
+    double L20, L21, rd2, s2;  // l part
+    double base, tr3, d1, d2;
+};
+__device__ __forceinline__ Hoist3 hoist3(const double* Gt, int64_t mp, int64_t m, int64_t j, int64_t k, int64_t l) {
+    Hoist3 h;
+    const double Y2 = Gt[m * mp + m];
+    h.w0 = Gt[m * mp + j];
+    h.L10 = Gt[k * mp + j];
+    h.d1 = fma(-h.L10, h.L10, 1.0);
+    h.rd1 = rcp_newton(h.d1);
+    const double w1 = fma(-h.L10, h.w0, Gt[m * mp + k]);
+    h.s1 = w1 * h.rd1;
+    h.L20 = Gt[l * mp + j];
+    const double a21 = fma(-h.L20, h.L10, Gt[l * mp + k]);
+    h.L21 = a21 * h.rd1;
+    h.d2 = fma(-a21, h.L21, fma(-h.L20, h.L20, 1.0));
+    h.rd2 = rcp_newton(h.d2);
+    const double w2 = fma(-h.L21, w1, fma(-h.L20, h.w0, Gt[m * mp + l]));
+    h.s2 = w2 * h.rd2;
+    h.base = Y2 - h.w0 * h.w0 - w1 * h.s1 - w2 * h.s2;
+    const double tr2 = 2.0 * h.rd1;
+    h.tr3 = tr2 + (1.0 + tr2) * h.rd2;
+    return h;
+}
+
+// Exact lower bound + certificates of one 4-tuple (i < j < k < l); see eval_tuple3.
+__device__ __noinline__ int eval_tuple4(const FitArgs& a, int64_t i, int64_t j, int64_t k, int64_t l,
+                                        double* lb_out) {
+    const int64_t m = a.m, mp = a.mp;
+    double lb = 0.0;
+    bool cond = true, rank_ok = true;
+    for (int t = 0; t < a.T; ++t) {
+        const double* Gt = a.G + (int64_t)t * mp * mp;
+        const double Y2 = Gt[m * mp + m];
+        const Hoist3 h = hoist3(Gt, mp, m, j, k, l);
+        const double* rt_ = a.rho + (int64_t)t * m;
+        const double rx = fmax(fmax(rt_[i], rt_[j]), fmax(rt_[k], rt_[l]));
+        double At, Bt, vk;
+        task_bound(4, a.eta[t], ref_gamma(a.rowsd[t], 4), rx, Y2, a.ynorm[t], h.tr3, At, Bt, vk);
+        if (!(h.d1 > 0.0) || !(h.d2 > 0.0) || !(vk * (1.0 + 4.0 * h.tr3) <= FO_LIM)) cond = false;
+        const double g0 = Gt[i * mp + j], ci = Gt[i * mp + m];
+        const double D = fma(-g0, g0, 1.0);
+        const double V = fma(-g0, h.w0, ci);
+        const double g1 = fma(-h.L10, g0, Gt[i * mp + k]);
+        const double t1 = g1 * h.rd1;
+        const double D1 = fma(-t1, g1, D);
+        const double V1 = fma(-g1, h.s1, V);
+        const double g2 = fma(-h.L21, g1, fma(-h.L20, g0, Gt[i * mp + l]));
+        const double t2 = g2 * h.rd2;
+        const double d = fma(-t2, g2, D1);
+        const double w = fma(-g2, h.s2, V1);
+        const double tr = h.tr3 + (1.0 + h.tr3) / d;
+        if (!(d > 0.0) || !(vk * (1.0 + 4.0 * tr) <= FO_LIM) || !(At + Bt / d <= LOOSE * Y2)) cond = false;
+        lb += h.base - At - fma(w, w, Bt) / d;
+        const int64_t f[4] = {i, j, k, l};
+        if (!rank_certain<4>(a, t, f, tr)) rank_ok = false;
+    }
+    *lb_out = lb;
+    return (cond ? 1 : 0) | (rank_ok ? 2 : 0);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs a) {
+    using C = Cfg4<NT>;
+    constexpr int P = C::P, IB = C::IB, TS = C::TS, BS = C::BS, LSPAN = C::LSPAN;
+    extern __shared__ __align__(16) double sm[];
+    __shared__ int s_unit;
+    __shared__ unsigned char s_force[2][IB];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    double* sKraw = sm + 2 * BS + 2 * NW * CAP + tid * P;
+    const int64_t m = a.m, mp = a.mp;
+    const double shrink = (NT == 1) ? 1.0 : (1.0 - 2.0 * kRcpRel);
+    WarpCands wc{sm + 2 * BS + warp * CAP, reinterpret_cast<int64_t*>(sm + 2 * BS + NW * CAP) + warp * CAP, 0,
+                 a.collect ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g)};
+    const int64_t* B2 = a.binom + 2 * (m + 1);
+    const int64_t* B3 = a.binom + 3 * (m + 1);
+    const int64_t* B4 = a.binom + 4 * (m + 1);
+
+    auto load_tiles = [&](int buf, int ib0, int j0, int k, int l0) {
+        double* base = sm + buf * BS;
+        if (tid < IB) s_force[buf][tid] = (ib0 + tid < m) ? a.iforce[ib0 + tid] : 0;
+        constexpr int pr = 16 + LSPAN / 2 + 2;  // 16-byte pieces for j and l, then C[i,k] and c_i
+        for (int q = tid; q < NT * IB * pr; q += 256) {
+            const int t = q / (IB * pr), r = q % (IB * pr);
+            const int row = r / pr, piece = r % pr;
+            const double* Grow = a.G + (int64_t)t * mp * mp + (int64_t)(ib0 + row) * mp;
+            double* Tt = base + t * TS;
+            if (piece < 16)
+                cp_async16(Tt + row * 32 + piece * 2, Grow + j0 + piece * 2);
+            else if (piece < 16 + LSPAN / 2)
+                cp_async16(Tt + IB * 32 + row * LSPAN + (piece - 16) * 2, Grow + l0 + (piece - 16) * 2);
+            else if (piece == 16 + LSPAN / 2)
+                cp_async8(Tt + IB * (32 + LSPAN) + row, Grow + k);
+            else
+                cp_async8(Tt + IB * (33 + LSPAN) + row, Grow + m);
+        }
+        cp_async_commit();
+    };
+
+    for (;;) {
+        if (tid == 0) s_unit = atomicAdd(a.unit_counter, 1);
+        __syncthreads();
+        const int u = s_unit;
+        __syncthreads();
+        if (u >= a.n_units) break;
+        const int4 U = a.units[u];
+        const int j0 = (U.x & 0xffff) * 32, l0 = (U.x >> 16) * LSPAN;
+        const int k = U.y;
+        const int j = j0 + lane;
+        const int lbase = l0 + warp * P;
+        const int i_lo = U.z, i_hi = U.w;
+        load_tiles(0, i_lo, j0, k, l0);
+        if (!a.collect) wc.theta = fmin(wc.theta, ord_dec(*(volatile unsigned long long*)a.theta_g));
+
+        // ---------------- hoist ----------------
+        double L10[NT], rd1[NT], s1[NT], w0[NT];
+        double L20[P][NT], L21[P][NT], rd2[P][NT], s2[P][NT], Kq[P], Bm[P];
+        unsigned valid = 0, bad = 0, forced = 0;
+        const int jj = j < m ? j : (int)m - 1;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int l = lbase + p;
+            const int ll = l < m ? l : (int)m - 1;
+            double kr = 0.0, bm = 0.0;
+            bool isbad = (a.iforce[jj] | a.iforce[k] | a.iforce[ll]) != 0, isnan_ = false;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const double* Gt = a.G + (int64_t)t * mp * mp;
+                const double Y2 = Gt[m * mp + m];
+                const Hoist3 h = hoist3(Gt, mp, m, j, k, l);
+                double At, Bt, vk;
+                task_bound(4, a.eta[t], ref_gamma(a.rowsd[t], 4), a.rho_cap[t], Y2, a.ynorm[t], h.tr3, At, Bt, vk);
+                L10[t] = h.L10;
+                rd1[t] = h.rd1;
+                s1[t] = h.s1;
+                w0[t] = h.w0;
+                L20[p][t] = h.L20;
+                L21[p][t] = h.L21;
+                rd2[p][t] = h.rd2;
+                s2[p][t] = h.s2;
+                kr += h.base - At;
+                bm = fmax(bm, Bt);
+                if (!(h.d1 > 0.0) || !(h.d2 > 0.0) || !(vk * (1.0 + 4.0 * h.tr3) <= FO_LIM)) isbad = true;
+                if (!(h.base == h.base) || !(h.L21 == h.L21)) isnan_ = true;
+            }
+            sKraw[p] = kr;
+            Bm[p] = bm;
+            if (j < k && k < l && l < m && !isnan_) valid |= 1u << p;
+            if (isbad) bad |= 1u << p;
+        }
+        auto set_kq = [&]() {
+            forced = bad;
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const double x = sKraw[p] - wc.theta;
+                if (!(x > 0.0)) forced |= 1u << p;
+                Kq[p] = x * shrink;
+            }
+        };
+        set_kq();
+
+        // ---------------- sweep i ----------------
+        const int nib = (i_hi - i_lo + IB - 1) / IB;
+        for (int bi = 0; bi < nib; ++bi) {
+            const int buf = bi & 1;
+            const int ib0 = i_lo + bi * IB;
+            if (bi + 1 < nib) {
+                load_tiles(buf ^ 1, ib0 + IB, j0, k, l0);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+            const double* T0 = sm + buf * BS;
+            constexpr int NPW = (IB * P + 31) / 32;
+            constexpr int IPW = 32 / P;
+            unsigned pend[NPW];
+#pragma unroll
+            for (int pw = 0; pw < NPW; ++pw) {
+                unsigned word = 0u;
+#pragma unroll 1
+                for (int iw = 0; iw < IPW; ++iw) {
+                    const int ii = pw * IPW + iw;
+                    const int i = ib0 + ii;
+                    double acc[P];
+#pragma unroll
+                    for (int p = 0; p < P; ++p) acc[p] = Kq[p];
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) {
+                        const double* Tt = T0 + t * TS;
+                        const double g0 = Tt[ii * 32 + lane];
+                        const double gkk = Tt[IB * (32 + LSPAN) + ii];
+                        const double ci = Tt[IB * (33 + LSPAN) + ii];
+                        const double D = fma(-g0, g0, 1.0);
+                        const double V = fma(-g0, w0[t], ci);
+                        const double g1 = fma(-L10[t], g0, gkk);
+                        const double t1 = g1 * rd1[t];
+                        const double D1 = fma(-t1, g1, D);
+                        const double V1 = fma(-g1, s1[t], V);
+                        double gl[P];
+#pragma unroll
+                        for (int p = 0; p < P; p += 2) {
+                            const double2 v =
+                                *reinterpret_cast<const double2*>(Tt + IB * 32 + ii * LSPAN + warp * P + p);
+                            gl[p] = v.x;
+                            gl[p + 1] = v.y;
+                        }
+#pragma unroll
+                        for (int p = 0; p < P; ++p) {
+                            const double g2 = fma(-L21[p][t], g1, fma(-L20[p][t], g0, gl[p]));
+                            const double t2 = g2 * rd2[p][t];
+                            const double w = fma(-g2, s2[p][t], V1);
+                            const double d = fma(-t2, g2, D1);
+                            const double q = fma(w, w, Bm[p]);
+                            if (NT == 1)
+                                acc[p] = fma(acc[p], d, -q);
+                            else
+                                acc[p] = fma(-q, rcp_fast_abs(d), acc[p]);
+                        }
+                    }
+                    unsigned pass = forced;
+#pragma unroll
+                    for (int p = 0; p < P; ++p)
+                        if (acc[p] < 0.0) pass |= 1u << p;
+                    if (s_force[buf][ii]) pass |= (1u << P) - 1;
+                    pass &= valid;
+                    if (!(i < j && i < i_hi)) pass = 0;
+                    word |= pass << (iw * P);
+                }
+                pend[pw] = word;
+            }
+            drain_pending<NPW>(
+                a, pend, wc, lane,
+                [&](int b, double* lbv, int64_t* rkv) -> int {
+                    const int ii = b / P, p = b % P;
+                    const int i = ib0 + ii, l = lbase + p;
+                    *rkv = a.N_total - 1 - (B4[m - 1 - i] + B3[m - 1 - j] + B2[m - 1 - k] + (m - 1 - l));
+                    if (a.ranged && (*rkv < a.rank_lo || *rkv >= a.rank_hi)) return 0;
+                    if ((bad >> p) & 1u) return 2;
+                    return eval_tuple4(a, i, j, k, l, lbv) == 3 ? 1 : 2;
+                },
+                set_kq);
+            __syncthreads();
+        }
+    }
+    flush_warp(a, wc, blockIdx.x * NW + warp, lane);
+}
+
+__global__ void k_screen4(const __grid_constant__ FitArgs a, const int64_t* __restrict__ tuples, int64_t count,
+                          double* __restrict__ out_lb, int32_t* __restrict__ out_flags) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= count) return;
+    double lb;
+    out_flags[c] = eval_tuple4(a, tuples[4 * c], tuples[4 * c + 1], tuples[4 * c + 2], tuples[4 * c + 3], &lb);
+    out_lb[c] = lb;
+}
+
+template <int NT>
+int occupancy4(int nsm) {
+    using C = Cfg4<NT>;
+    cudaFuncSetAttribute(k_fit4<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit4<NT>, 256, C::smem_bytes);
+    return nsm * (per_sm < 1 ? 1 : per_sm);
+}
+
+template <int NT>
+int launch4(const FitArgs& a, int nsm, cudaStream_t st) {
+    const int grid = occupancy4<NT>(nsm);
+    k_fit4<NT><<<grid, 256, Cfg4<NT>::smem_bytes, st>>>(a);
+    return grid;
+}
+
+}  // namespace
+
+void launch_screen4(const FitArgs& a, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags,
+                    cudaStream_t st) {
+    if (count > 0) k_screen4<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(a, tuples, count, out_lb, out_flags);
+}
+
+int fit4_lspan(int T) { return T <= 2 ? Cfg4<1>::LSPAN : Cfg4<8>::LSPAN; }
+
+int fit4_grid(int T, int nsm) {
+    switch (T) {
+        case 1: return occupancy4<1>(nsm);
+        case 2: return occupancy4<2>(nsm);
+        case 3: return occupancy4<3>(nsm);
+        case 4: return occupancy4<4>(nsm);
+        case 5: return occupancy4<5>(nsm);
+        case 6: return occupancy4<6>(nsm);
+        case 7: return occupancy4<7>(nsm);
+        case 8: return occupancy4<8>(nsm);
+        default: return -1;
+    }
+}
+
+int fit4_launch(const FitArgs& a, int nsm, cudaStream_t st) {
+    switch (a.T) {
+        case 1: return launch4<1>(a, nsm, st);
+        case 2: return launch4<2>(a, nsm, st);
+        case 3: return launch4<3>(a, nsm, st);
+        case 4: return launch4<4>(a, nsm, st);
+        case 5: return launch4<5>(a, nsm, st);
+        case 6: return launch4<6>(a, nsm, st);
+        case 7: return launch4<7>(a, nsm, st);
+        case 8: return launch4<8>(a, nsm, st);
+        default: return -1;
+    }
+}
+
+// Unit table for n = 4: (j-block | l-block << 16, k, i_lo, i_hi) with i < j < k < l < m.
+// c3_prefix[v] = rank of the first tuple whose smallest index is v.
+std::vector<int4> fit4_units(int64_t m, int T, const std::vector<int64_t>& c3_prefix, int64_t rank_lo,
+                             int64_t rank_hi) {
+    const int lspan = fit4_lspan(T);
+    const int ich = 128;
+    std::vector<int4> units;
+    const int nJ = (int)((m + 31) / 32);
+    const int nL = (int)((m + lspan - 1) / lspan);
+    int i_first = 0, i_last = (int)m - 1;
+    while (i_first < m && c3_prefix[i_first + 1] <= rank_lo) ++i_first;
+    while (i_last > 0 && c3_prefix[i_last] >= rank_hi) --i_last;
+    for (int jb = 0; jb < nJ; ++jb) {
+        const int jlo = jb * 32;
+        int i_end = (int)std::min<int64_t>(jlo + 31, m - 3);
+        i_end = std::min(i_end, i_last + 1);
+        if (i_end <= i_first) continue;
+        for (int k = jlo + 1; k <= m - 2; ++k) {
+            for (int lb = (k + 1) / lspan; lb < nL; ++lb) {
+                if ((int64_t)lb * lspan + lspan - 1 <= k) continue;
+                for (int lo = i_first; lo < i_end; lo += ich) {
+                    const int hi = std::min(lo + ich, i_end);
+                    if (c3_prefix[hi] <= rank_lo || c3_prefix[lo] >= rank_hi) continue;
+                    units.push_back(make_int4(jb | (lb << 16), k, lo, hi));
+                }
+            }
+        }
+    }
+    std::stable_sort(units.begin(), units.end(),
+                     [](const int4& x, const int4& y) { return (x.w - x.z) > (y.w - y.z); });
+    return units;
+}
+
+}  // namespace l0s

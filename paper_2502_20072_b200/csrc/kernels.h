@@ -102,6 +102,14 @@ std::vector<int4> fit3_units(int64_t m, int T, int64_t N_total, const std::vecto
 void launch_screen3(const FitArgs& a, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags,
                     cudaStream_t st);
 
+// ---- screened fit, n = 4 (fit4.cu) ----
+int fit4_launch(const FitArgs& a, int nsm, cudaStream_t st);
+int fit4_grid(int T, int nsm);
+std::vector<int4> fit4_units(int64_t m, int T, const std::vector<int64_t>& c3_prefix, int64_t rank_lo,
+                             int64_t rank_hi);
+void launch_screen4(const FitArgs& a, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags,
+                    cudaStream_t st);
+
 // ---- candidate gather (merge.cu) ----
 void launch_gather_candidates(const double* wl_lb, const int64_t* wl_rank, const int* wl_cnt, int slots,
                               int kc, const unsigned long long* theta_g, double* out_lb,

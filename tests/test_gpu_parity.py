@@ -75,8 +75,8 @@ def test_l0_search_matches_reference(name, mode):
     from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
 
     c = search_case(name)
-    if mode == "fast" and (c["n"] != 3 or len(c["slices"]) > 8 or c["precision"] != "fp64"):
-        pytest.skip("screened path covers n=3, <= 8 tasks, fp64")
+    if mode == "fast" and (c["n"] not in (3, 4) or len(c["slices"]) > 8 or c["precision"] != "fp64"):
+        pytest.skip("screened path covers n in {3, 4}, <= 8 tasks, fp64")
     cfg = L0Config(dimension=c["n"], n_models_store=c["keep"], precision=c["precision"], autotune=False)
     st = SearchStats()
     models = l0_search(c["values"], c["y"], c["slices"], cfg, stats=st, mode=mode)
@@ -172,6 +172,39 @@ def test_rcp_fast_bound():
     worst = ctypes.c_double()
     assert _lib.lib().l0s_rcp_check(1 << 26, ctypes.byref(worst)) == 0
     assert worst.value <= 2.0 ** -17, worst.value
+
+
+@pytest.mark.parametrize("T", [1, 3])
+def test_fast_n4_matches_oracle(oracle, rng, T):
+    """Screened dimension-4 search == exhaustive CPU oracle (C(36,4) = 58905 tuples)."""
+    from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
+
+    m, s = 36, 180
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    y = 1.5 * v[2] - v[9] + 0.5 * v[20] + 0.25 * v[33] + 0.02 * rng.standard_normal(s)
+    v[30] = v[2] + 1e-7 * rng.standard_normal(s)  # a near-copy of a planted feature
+    slices = [np.arange(t, s, T) for t in range(T)]
+    want = oracle.l0_search(v, y, slices, 4, 10, "fp64", threads=os.cpu_count() or 1)
+    st = SearchStats()
+    got = l0_search(v, y, slices, L0Config(dimension=4), mode="fast", stats=st)
+    assert st.device["mode_used"] == 1 and st.device["certified"] == 1
+    assert [md.indices for md in got] == [w["indices"] for w in want]
+    assert bits_equal([md.score for md in got], [w["score"] for w in want])
+
+
+def test_screen_n4_lower_bound(eng, rng):
+    m, s = 18, 70
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    v[5] = v[1] + 1e-9 * rng.standard_normal(s)
+    y = v[0] - 2 * v[3] + 0.3 * v[7] + 0.1 * v[11] + 1e-3 * rng.standard_normal(s)
+    eng.stage(v, y, np.arange(s), np.array([0, s]), "fp64")
+    tup = np.array(list(itertools.combinations(range(m), 4)), dtype=np.int64)
+    ok, score, _, _ = eng.fit_tuples(tup)
+    lb, flags = eng.screen_tuples(tup)
+    sel = (flags == 3) & np.isfinite(score)
+    assert sel.sum() > 0.5 * len(tup)
+    assert not (lb[sel] > score[sel] * s).any()
+    assert np.all(ok[flags == 3])
 
 
 def test_fast_matches_oracle_random(oracle, rng):
