@@ -624,7 +624,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     CK(cudaMemsetAsync(c->ill_cnt.p, 0, sizeof(unsigned long long), c->st));
     CK(cudaMemsetAsync(c->cand_cnt.p, 0, sizeof(unsigned long long), c->st));
     cudaEventRecord(c->ev[2], c->st);
-    launch_fit(a);
+    if (launch_fit(a) < 0) return fail(L0S_ECUDA, "screened fit launch failed (TMA descriptor)");
     cudaEventRecord(c->ev[3], c->st);
     CK(cudaGetLastError());
     st->n_fit_launches++;
@@ -694,7 +694,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
         a.coll_cnt = c->coll_cnt.as<unsigned long long>();
         a.coll_cap = coll_cap;
         cudaEventRecord(c->ev[2], c->st);
-        launch_fit(a);
+        if (launch_fit(a) < 0) return fail(L0S_ECUDA, "screened fit launch failed (TMA descriptor)");
         cudaEventRecord(c->ev[3], c->st);
         CK(cudaGetLastError());
         st->n_fit_launches++;

@@ -60,7 +60,7 @@ struct Cfg {
     static constexpr int P = c.P;
     static constexpr int IB = c.IB;
     static constexpr int KSPAN = NW * P;
-    static constexpr int TS = IB * (32 + KSPAN + 1);  // C[i, j-block] | C[i, k-span] | c_i
+    static constexpr int TS = IB * (32 + KSPAN + 2);  // C[i, j-block] | C[i, k-span] | (c_i, pad)
     static constexpr int BS = NT * TS;
     static constexpr int MINB = c.MINB;
     static constexpr int UNROLL = c.UNROLL;  // rows of the i sweep in flight per thread
@@ -114,10 +114,18 @@ template <int NT>
 __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_constant__ FitArgs a) {
     using C = Cfg<NT>;
     constexpr int P = C::P, IB = C::IB, TS = C::TS, BS = C::BS, KSPAN = C::KSPAN;
-    extern __shared__ __align__(16) double sm[];
+    extern __shared__ __align__(128) double sm[];
     __shared__ int s_unit;
     __shared__ unsigned char s_force[2][IB];  // iforce flags of the staged rows
+    __shared__ __align__(8) unsigned long long s_bar[2];  // TMA completion, one per tile buffer
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    unsigned parity[2] = {0u, 0u};
     double* sKraw = sm + 2 * BS + 2 * NW * CAP + tid * P;  // per-thread, slow path / threshold updates only
     const int64_t m = a.m, mp = a.mp;
     const double shrink = (NT == 1) ? 1.0 : (1.0 - 2.0 * kRcpRel);
@@ -126,24 +134,27 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
     const int64_t* B2 = a.binom + 2 * (m + 1);
     const int64_t* B3 = a.binom + 3 * (m + 1);
 
-    // tiles per task: C[i, j-block] (IB x 32), C[i, k-span] (IB x KSPAN), c_i (IB)
+    // tiles per task, staged by TMA (one elected thread, completion on s_bar[buf]):
+    // C[i, j-block] (IB x 32), C[i, k-span] (IB x KSPAN), (c_i, pad) (IB x 2)
     auto load_tiles = [&](int buf, int ib0, int j0, int k0) {
-        double* base = sm + buf * BS;
         if (tid < IB) s_force[buf][tid] = (ib0 + tid < m) ? a.iforce[ib0 + tid] : 0;
-        constexpr int pr = 16 + KSPAN / 2 + 1;  // 16-byte pieces per row (+ one 8-byte c_i)
-        for (int q = tid; q < NT * IB * pr; q += 256) {
-            const int t = q / (IB * pr), r = q % (IB * pr);
-            const int row = r / pr, piece = r % pr;
-            const double* Grow = a.G + (int64_t)t * mp * mp + (int64_t)(ib0 + row) * mp;
-            double* Tt = base + t * TS;
-            if (piece < 16)
-                cp_async16(Tt + row * 32 + piece * 2, Grow + j0 + piece * 2);
-            else if (piece < 16 + KSPAN / 2)
-                cp_async16(Tt + IB * 32 + row * KSPAN + (piece - 16) * 2, Grow + k0 + (piece - 16) * 2);
-            else
-                cp_async8(Tt + IB * (32 + KSPAN) + row, Grow + m);
+        if (tid == 0) {
+            double* base = sm + buf * BS;
+            fence_proxy_async();
+            mbar_expect_tx(&s_bar[buf], (unsigned)(BS * sizeof(double)));
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int row = (int)(t * mp) + ib0;
+                double* Tt = base + t * TS;
+                tma_load_2d(Tt, &a.tmJ, j0, row, &s_bar[buf]);
+                tma_load_2d(Tt + IB * 32, &a.tmK, k0, row, &s_bar[buf]);
+                tma_load_2d(Tt + IB * (32 + KSPAN), &a.tmC, (int)m, row, &s_bar[buf]);
+            }
         }
-        cp_async_commit();
+    };
+    auto wait_tiles = [&](int buf) {
+        mbar_wait(&s_bar[buf], parity[buf]);
+        parity[buf] ^= 1u;
     };
 
     for (;;) {
@@ -216,13 +227,9 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
         for (int bi = 0; bi < nib; ++bi) {
             const int buf = bi & 1;
             const int ib0 = i_lo + bi * IB;
-            if (bi + 1 < nib) {
-                load_tiles(buf ^ 1, ib0 + IB, j0, k0);
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
-            __syncthreads();
+            if (bi + 1 < nib) load_tiles(buf ^ 1, ib0 + IB, j0, k0);
+            wait_tiles(buf);
+            __syncthreads();  // s_force of this tile
             const double* T0 = sm + buf * BS;
             // pending slow-path tuples of this tile: bit (ii * P + p)
             constexpr int NPW = (IB * P + 31) / 32;  // pending-bit words
@@ -242,7 +249,7 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
                     for (int t = 0; t < NT; ++t) {
                         const double* Tt = T0 + t * TS;
                         const double g0 = Tt[ii * 32 + lane];
-                        const double ci = Tt[IB * (32 + KSPAN) + ii];
+                        const double ci = Tt[IB * (32 + KSPAN) + 2 * ii];
                         const double D = fma(-g0, g0, 1.0);
                         const double V = fma(-g0, w0[t], ci);
                         double gk[P];
@@ -312,8 +319,13 @@ __global__ void k_screen3(const __grid_constant__ FitArgs a, const int64_t* __re
 }
 
 template <int NT>
-int launch_nt(const FitArgs& a, int nsm, cudaStream_t st) {
+int launch_nt(const FitArgs& a0, int nsm, cudaStream_t st) {
     using C = Cfg<NT>;
+    FitArgs a = a0;
+    const unsigned long long rows = (unsigned long long)a.T * a.mp, cols = (unsigned long long)a.mp;
+    if (!make_tma_2d(&a.tmJ, a.G, cols, rows, 32, C::IB) || !make_tma_2d(&a.tmK, a.G, cols, rows, C::KSPAN, C::IB) ||
+        !make_tma_2d(&a.tmC, a.G, cols, rows, 2, C::IB))
+        return -1;
     cudaFuncSetAttribute(k_fit3<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, 256, C::smem_bytes);
@@ -375,7 +387,7 @@ int fit3_launch(const FitArgs& a, int nsm, cudaStream_t st) {
 std::vector<int4> fit3_units(int64_t m, int T, int64_t N_total, const std::vector<int64_t>& c2_prefix,
                              int64_t rank_lo, int64_t rank_hi) {
     const int kspan = fit3_kspan(T);
-    const int ich = 128;
+    const int ich = 256;  // i rows per unit: amortizes the (j, k) hoist
     std::vector<int4> units;
     int nJ = (int)((m + 31) / 32);
     int nK = (int)((m + kspan - 1) / kspan);

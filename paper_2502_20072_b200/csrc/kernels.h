@@ -54,7 +54,15 @@ struct ExactArgs {
 void launch_exact(const ExactArgs& a, double* ssr_tmp, int32_t* ok_tmp, cudaStream_t st, int64_t* launches);
 
 // ---- screened fit (fit3.cu) ----
+// TMA descriptors for the Gram viewed as a 2-D (T*mp rows x mp columns) f64 tensor;
+// one per box shape the kernel stages (built by the launcher, which knows the tile shape).
+struct alignas(64) TmaDesc {
+    unsigned long long opaque[16];
+};
 struct FitArgs {
+    TmaDesc tmJ;  // box: 32 columns (j-block) x IB rows
+    TmaDesc tmK;  // box: KSPAN columns (k- or l-span) x IB rows
+    TmaDesc tmC;  // box: 2 columns (one Gram column + its neighbour) x IB rows
     const double* G;         // [T][mp][mp] normalized Gram, y at index m
     const double* qf;        // [T][m]
     const double* un2;       // [T][m]
@@ -109,6 +117,10 @@ std::vector<int4> fit4_units(int64_t m, int T, const std::vector<int64_t>& c3_pr
                              int64_t rank_hi);
 void launch_screen4(const FitArgs& a, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags,
                     cudaStream_t st);
+
+// Encode a 2-D f64 tiled TMA descriptor over G ([rows x cols], row stride = cols) with box (bx, by).
+bool make_tma_2d(TmaDesc* out, const double* G, unsigned long long cols, unsigned long long rows, unsigned bx,
+                 unsigned by);
 
 // ---- candidate gather (merge.cu) ----
 void launch_gather_candidates(const double* wl_lb, const int64_t* wl_rank, const int* wl_cnt, int slots,

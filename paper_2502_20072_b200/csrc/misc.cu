@@ -3,9 +3,39 @@
 // MEASURED_PEAKS.json carries HBM and bf16 figures only, so the fp64 peak is
 // measured here: 8 independent DFMA chains per thread, enough warps to cover
 // the pipe latency on every SM, timed with CUDA events.
+#include <cuda.h>
+
 #include "../../include/l0search.h"
 #include "common.cuh"
 #include "kernels.h"
+
+namespace l0s {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link).
+bool make_tma_2d(TmaDesc* out, const double* G, unsigned long long cols, unsigned long long rows, unsigned bx,
+                 unsigned by) {
+    using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                            const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                            CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p)
+            return false;
+        fn = (Fn)p;
+    }
+    static_assert(sizeof(TmaDesc) == sizeof(CUtensorMap), "descriptor size");
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * sizeof(double)};
+    const cuuint32_t box[2] = {bx, by};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)G, dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+}  // namespace l0s
 
 namespace l0s {
 namespace {
