@@ -67,6 +67,8 @@ typedef struct {
     int32_t mode_used;       /* L0S_MODE_FAST or L0S_MODE_EXACT                       */
     int32_t certified;       /* 1 when the top-k set is proven exact                  */
     double margin;           /* lb(K')-th minus k-th exact score at certification     */
+    double ms_qr;            /* QR screen of the uncertifiable tuples                 */
+    int64_t n_ill_refit;     /* of those, refit bit-exactly                           */
 } l0s_stats;
 
 const char *l0s_last_error(void);

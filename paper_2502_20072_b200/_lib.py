@@ -49,6 +49,8 @@ class Stats(ctypes.Structure):
         ("mode_used", ctypes.c_int32),
         ("certified", ctypes.c_int32),
         ("margin", ctypes.c_double),
+        ("ms_qr", ctypes.c_double),
+        ("n_ill_refit", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

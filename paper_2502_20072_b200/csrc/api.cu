@@ -98,6 +98,7 @@ struct l0s_ctx {
     DBuf units, ucount, theta_g, wl_lb, wl_rank, wl_cnt, ill, ill_cnt, cand_lb, cand_rank, cand_cnt, sort_tmp,
         lb_tmp, rank_tmp, coll_lb, coll_rank, coll_cnt;
     DBuf ex_scratch, ex_ssr_tmp, ex_ok_tmp, ex_ok, ex_score, ex_coef, ex_ssr, ex_ranks, ex_tuples;
+    DBuf qr_ssr, qr_ratio, qr_score, qr_minr;
     std::vector<int4> units_h;
     int64_t units_key[5] = {-1, -1, -1, -1, -1};
 
@@ -106,7 +107,7 @@ struct l0s_ctx {
                        &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &binom, &units, &ucount, &theta_g, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
                        &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
-                       &ex_ranks, &ex_tuples};
+                       &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr};
         for (DBuf* b : all) b->release();
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -332,7 +333,7 @@ int l0s_stage(l0s_ctx* c, const double* values, int64_t m, int64_t s, const doub
     CK(cudaMemsetAsync(c->Z.p, 0, sizeof(double) * c->mp * c->sp, c->st));
     launch_normalize(c->Xp.p, c->yp.p, precision, m, s, c->bounds_d.as<int64_t>(), c->zoff_d.as<int64_t>(), ntasks,
                      c->sp, c->Z.as<double>(), c->qf.as<double>(), c->un2.as<double>(), c->yyu.as<double>(), c->st);
-    launch_gram(c->Z.as<double>(), c->sp, c->zoff_h.data(), c->rpad_h.data(), ntasks, m, c->mp, c->G.as<double>(),
+    launch_gram(c->Z.as<double>(), c->sp, c->zoff_h.data(), c->zoff_d.as<int64_t>(), c->rpad_h.data(), ntasks, m, c->mp, c->G.as<double>(),
                 c->st);
     CK(cudaGetLastError());
     cudaEventRecord(c->ev[1], c->st);
@@ -353,7 +354,9 @@ int l0s_stage(l0s_ctx* c, const double* values, int64_t m, int64_t s, const doub
     std::vector<unsigned char> dead_f((size_t)m, 0);
     for (int t = 0; t < ntasks; ++t) {
         const double r = c->rows_h[t];
-        const double gam = 2.0 * (r + 1.0) * (15 + 2) * kEps;
+        // the Gram (hence dead marking) serves the screened path only, n <= 4;
+        // same reference rounding model as fit::ref_gamma (fitcommon.cuh)
+        const double gam = 2.0 * 8.0 * std::sqrt(r + 1.0) * (4 + 2) * kEps;
         double umin = INFINITY;
         for (int64_t f = 0; f < m; ++f) umin = std::min(umin, uh[(size_t)(t * m + f)]);
         const double lim = 0.5 * 1e-10 * std::sqrt(umin / std::max(r, 1.0)) - 4.0 * gam;
@@ -565,6 +568,67 @@ static int search_exact_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_
     return L0S_OK;
 }
 
+// QR screen of the `nill` ranks in c->ill, then bit-exact refit of the ones that can matter.
+static int screen_ill(l0s_ctx* c, int n, int64_t nill, int64_t keep, std::vector<Cand>& best, l0s_stats* st) {
+    CK(c->qr_ssr.ensure(sizeof(double) * nill * c->T));
+    CK(c->qr_ratio.ensure(sizeof(double) * nill * c->T));
+    CK(c->qr_score.ensure(sizeof(double) * nill));
+    CK(c->qr_minr.ensure(sizeof(double) * nill));
+    QrArgs q{};
+    q.Xp = c->Xp.as<double>();
+    q.yp = c->yp.as<double>();
+    q.bounds = c->bounds_d.as<int64_t>();
+    q.T = c->T;
+    q.m = c->m;
+    q.s = c->s;
+    q.n = n;
+    q.ranks = c->ill.as<int64_t>();
+    q.binom = c->binom.as<int64_t>();
+    q.ssr = c->qr_ssr.as<double>();
+    q.ratio = c->qr_ratio.as<double>();
+    q.score = c->qr_score.as<double>();
+    q.min_ratio = c->qr_minr.as<double>();
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, c->st);
+    launch_qr_screen(q, nill, c->st, &st->n_launches);
+    cudaEventRecord(e1, c->st);
+    CK(cudaGetLastError());
+    CK(cudaEventSynchronize(e1));
+    st->ms_qr += elapsed(e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    std::vector<double> sc((size_t)nill), mr((size_t)nill);
+    std::vector<int64_t> rk((size_t)nill);
+    CK(cudaMemcpyAsync(sc.data(), q.score, sizeof(double) * nill, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(mr.data(), q.min_ratio, sizeof(double) * nill, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(rk.data(), c->ill.p, sizeof(int64_t) * nill, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    const double tol = 1e-10;  // RANK_TOL_FACTOR["fp64"], lsq.py:23 (screened path is fp64 only)
+    double yy = 0.0;
+    for (double v : c->yyu_h) yy += v;
+    const double sk = ((int64_t)best.size() >= keep) ? best[(size_t)keep - 1].score : INFINITY;
+    std::vector<int64_t> sel;
+    for (int64_t i = 0; i < nill; ++i) {
+        const double r = mr[(size_t)i];
+        if (r < tol * (1.0 - 1e-3)) continue;  // the reference's rank rule rejects it in some task
+        // QR score error ~ eps * condition; condition >= 1/ratio
+        const double margin = 1e3 * kEps * yy / (double)c->s / std::max(r, 1e-300) + 1e-9 * std::fabs(sc[(size_t)i]);
+        if (!(sc[(size_t)i] - margin > sk)) sel.push_back(rk[(size_t)i]);
+    }
+    st->n_ill_refit += (int64_t)sel.size();
+    if (sel.empty()) return L0S_OK;
+    CK(c->ex_ranks.ensure(sizeof(int64_t) * sel.size()));
+    CK(cudaMemcpyAsync(c->ex_ranks.p, sel.data(), sizeof(int64_t) * sel.size(), cudaMemcpyHostToDevice, c->st));
+    std::vector<Cand> more;
+    int rc = exact_ranks_to_host(c, n, c->ex_ranks.as<int64_t>(), (int64_t)sel.size(), more, &st->n_launches);
+    if (rc) return rc;
+    st->n_candidates += (int64_t)sel.size();
+    merge_best(best, more, keep);
+    return L0S_OK;
+}
+
 static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t re, std::vector<Cand>& best,
                             l0s_stats* st) {
     const int64_t N = binom_sat(c->m, n);
@@ -583,7 +647,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     const int grid = n == 3 ? fit3_grid(c->T, c->nsm) : fit4_grid(c->T, c->nsm);
     auto launch_fit = [&](const FitArgs& fa) { return n == 3 ? fit3_launch(fa, c->nsm, c->st) : fit4_launch(fa, c->nsm, c->st); };
     const int slots = grid * fit_slots_per_cta();
-    const int64_t ill_cap = (int64_t)1 << 22;
+    const int64_t ill_cap = (int64_t)1 << 26;  // 512 MB of ranks; overflow is reported, never dropped
     CK(c->ucount.ensure(sizeof(int) * 4));
     CK(c->theta_g.ensure(sizeof(unsigned long long)));
     CK(c->wl_lb.ensure(sizeof(double) * slots * kc));
@@ -654,8 +718,12 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     cudaEventRecord(c->ev[2], c->st);
     int rc = exact_ranks_to_host(c, n, c->cand_rank.as<int64_t>(), nc, exact, &st->n_launches);
     if (rc) return rc;
+    merge_best(best, exact, keep);
     if (nill > 0) {
-        rc = exact_ranks_to_host(c, n, c->ill.as<int64_t>(), (int64_t)nill, exact, &st->n_launches);
+        // Tuples the Gram screen could not certify: TSQR on the device gives each a score and
+        // the reference's rank-rule ratio; only those that can reach the top list within the
+        // QR's error margin (~ eps / ratio) are refit bit-exactly.
+        rc = screen_ill(c, n, (int64_t)nill, keep, best, st);
         if (rc) return rc;
     }
     cudaEventRecord(c->ev[3], c->st);
@@ -663,7 +731,6 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     st->ms_exact += elapsed(c->ev[2], c->ev[3]);
     st->n_candidates = nc;
     st->n_ill = (int64_t)nill;
-    merge_best(best, exact, keep);
 
     // certification: an excluded tuple has exact score >= lb / s >= G_lb / s; it cannot
     // displace the keep-th exact score if G_lb / s exceeds it by the reference's own error margin

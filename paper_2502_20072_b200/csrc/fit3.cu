@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
             const int k = kbase + p;
             const int kk = k < m ? k : (int)m - 1;
             double kr = 0.0, bm = 0.0;
-            bool isbad = (a.iforce[jj] | a.iforce[kk]) != 0, isnan_ = false;
+            bool isbad = false, isnan_ = false;
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
                 const double* Gt = a.G + (int64_t)t * mp * mp;
@@ -197,7 +197,9 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
                 const double base = Y2 - w0[t] * w0[t] - v1 * v1 * r1;
                 const double trh = 2.0 * r1;
                 double At, Bt, vk;
-                task_bound(3, a.eta[t], ref_gamma(a.rowsd[t], 3), a.rho_cap[t], Y2, a.ynorm[t], trh, At, Bt, vk);
+                // rho of the hoisted pair (the sweep feature's rho is covered by rho_cap or s_force)
+                const double rh = fmax(a.rho_cap[t], fmax(a.rho[(int64_t)t * m + jj], a.rho[(int64_t)t * m + kk]));
+                task_bound(3, a.eta[t], ref_gamma(a.rowsd[t], 3), rh, Y2, a.ynorm[t], trh, At, Bt, vk);
                 L10[p][t] = cjk;
                 rd1[p][t] = r1;
                 s1[p][t] = v1 * r1;

@@ -159,14 +159,16 @@ __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs
             const int l = lbase + p;
             const int ll = l < m ? l : (int)m - 1;
             double kr = 0.0, bm = 0.0;
-            bool isbad = (a.iforce[jj] | a.iforce[k] | a.iforce[ll]) != 0, isnan_ = false;
+            bool isbad = false, isnan_ = false;
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
                 const double* Gt = a.G + (int64_t)t * mp * mp;
                 const double Y2 = Gt[m * mp + m];
                 const Hoist3 h = hoist3(Gt, mp, m, j, k, l);
                 double At, Bt, vk;
-                task_bound(4, a.eta[t], ref_gamma(a.rowsd[t], 4), a.rho_cap[t], Y2, a.ynorm[t], h.tr3, At, Bt, vk);
+                const double* rt_ = a.rho + (int64_t)t * m;
+                const double rh = fmax(fmax(a.rho_cap[t], rt_[jj]), fmax(rt_[k], rt_[ll]));
+                task_bound(4, a.eta[t], ref_gamma(a.rowsd[t], 4), rh, Y2, a.ynorm[t], h.tr3, At, Bt, vk);
                 L10[t] = h.L10;
                 rd1[t] = h.rd1;
                 s1[t] = h.s1;

@@ -13,7 +13,7 @@ constexpr int NW = 8;                 // warps per CTA
 constexpr int CAP = 256;              // per-warp candidate buffer
 constexpr double FO_LIM = 1e-3;       // first-order validity: (eta + gam rho)(1 + n tr) <= FO_LIM
 constexpr double RANK_SLACK = 1.01;   // safety factor on the rank-rule certificate
-constexpr double LOOSE = 1e-6;        // bounds looser than this fraction of |y_c|^2 go to the exact kernel
+constexpr double LOOSE = 1e-3;        // bounds looser than this fraction of |y_c|^2 go to the exact kernel
 
 // Error model, one task, n features, tr = trace of the inverse of the
 // normalized n x n block, tr <= trh + (1 + trh)/d (trh: hoisted (n-1) x (n-1) block):
@@ -30,8 +30,15 @@ __device__ __forceinline__ void task_bound(int n, double eta, double gam, double
     B = n * K * Y2 * (1.0 + trh);
 }
 
-// Householder QR columnwise backward-error constant for r rows, n features + intercept + rhs.
-__device__ __forceinline__ double ref_gamma(double rows, int n) { return 2.0 * (rows + 1.0) * (n + 2) * kEps; }
+// Householder QR columnwise backward-error constant for r rows, n features + intercept + rhs,
+// with the inner products' rounding bounded probabilistically: |error| <= lambda sqrt(r) u
+// with probability >= 1 - 2 exp(-lambda^2 (1-u)^2 / 2) per inner product (Higham & Mary,
+// SIAM J. Sci. Comput. 41(5), 2019); lambda = 8 puts the failure probability below 1e-13.
+// (The worst-case r u growth would make every feature whose mean/std ratio exceeds ~1e6
+// uncertifiable at r = 5000, although the reference's actual error there is ~1e-7.)
+__device__ __host__ __forceinline__ double ref_gamma(double rows, int n) {
+    return 2.0 * 8.0 * sqrt(rows + 1.0) * (n + 2) * kEps;
+}
 
 // 1/d without the IEEE-division subroutine call: MUFU seed + two Newton steps (a few ulp,
 // inside the eta slack).  Garbage for d <= 0, which every caller rejects separately.

@@ -23,11 +23,16 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int64_t sp, int64_t k0,
-                                              int64_t klen, int nb, double* __restrict__ G, int64_t mp) {
+// grid: (upper-triangle blocks, tasks); task t owns Z columns [zoff[t], zoff[t+1]) and G + t mp^2
+__global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int64_t sp,
+                                              const int64_t* __restrict__ zoff, int nb, double* __restrict__ Gall,
+                                              int64_t mp) {
     extern __shared__ __align__(16) double gsm[];
     double* sA[2] = {gsm, gsm + BM * LDS};
     double* sB[2] = {gsm + 2 * BM * LDS, gsm + 3 * BM * LDS};
+    const int task = blockIdx.y;
+    const int64_t k0 = zoff[task], klen = zoff[task + 1] - k0;
+    double* G = Gall + (int64_t)task * mp * mp;
     // block (ba, bb), ba <= bb, from the linear upper-triangle index
     int lin = blockIdx.x;
     int ba = 0;
@@ -108,8 +113,9 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int6
             }
 }
 
-__global__ void k_unit_diag(double* G, int64_t m, int64_t mp) {
+__global__ void k_unit_diag(double* Gall, int64_t m, int64_t mp) {
     int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double* G = Gall + (int64_t)blockIdx.y * mp * mp;
     if (f < m) {
         double d = G[f * mp + f];
         G[f * mp + f] = (d == d) ? 1.0 : d;  // keep NaN rows NaN (constant feature)
@@ -133,24 +139,17 @@ void launch_mark_dead(double* G, const int32_t* dead, int ndead, int T, int64_t 
     if (ndead > 0) k_mark_dead<<<256, 256, 0, st>>>(G, dead, ndead, T, mp);
 }
 
-void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_h, const int64_t* rpad_h, int T, int64_t m,
-                 int64_t mp, double* G, cudaStream_t st) {
+void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_h, const int64_t* zoff_d, const int64_t* rpad_h,
+                 int T, int64_t m, int64_t mp, double* G, cudaStream_t st) {
     int nb = (int)(mp / BM);
     int nblk = nb * (nb + 1) / 2;
     const int smem = 4 * BM * LDS * (int)sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
-    for (int t = 0; t < T; ++t) {
-        double* Gt = G + (int64_t)t * mp * mp;
-        if (rpad_h[t] > 0)
-            k_gram<<<nblk, 256, smem, st>>>(Z, sp, zoff_h[t], rpad_h[t], nb, Gt, mp);
-        else
-            cudaMemsetAsync(Gt, 0, sizeof(double) * mp * mp, st);
-        k_unit_diag<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(Gt, m, mp);
-    }
+    cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    // one launch for every task: ~T * nb^2 / 2 CTAs keep the tail wave short
+    k_gram<<<dim3((unsigned)nblk, (unsigned)T), 256, smem, st>>>(Z, sp, zoff_d, nb, G, mp);
+    k_unit_diag<<<dim3((unsigned)((m + 255) / 256), (unsigned)T), 256, 0, st>>>(G, m, mp);
+    (void)zoff_h;
+    (void)rpad_h;
 }
 
 }  // namespace l0s

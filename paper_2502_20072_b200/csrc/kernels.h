@@ -21,7 +21,7 @@ void launch_normalize(const void* Xp, const void* yp, int precision, int64_t m, 
                       double* qf, double* un2, double* yyu, cudaStream_t st);
 
 // ---- Gram (gram.cu): G[t] = Z_t Z_t^T on DMMA, (mp x mp) per task, diag of features := 1 ----
-void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_h, const int64_t* rpad_h, int T,
+void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_h, const int64_t* zoff_d, const int64_t* rpad_h, int T,
                  int64_t m, int64_t mp, double* G, cudaStream_t st);
 // Features the reference's rank rule rejects in every tuple: NaN their Gram row and column (all tasks).
 void launch_mark_dead(double* G, const int32_t* dead, int ndead, int T, int64_t mp, cudaStream_t st);
@@ -52,6 +52,24 @@ struct ExactArgs {
 };
 // Runs in chunks of args.scratch_threads threads (one per (tuple, task)).
 void launch_exact(const ExactArgs& a, double* ssr_tmp, int32_t* ok_tmp, cudaStream_t st, int64_t* launches);
+
+// ---- QR screen for uncertifiable tuples (qr.cu) ----
+struct QrArgs {
+    const double* Xp;       // (m, s) fp64, permuted
+    const double* yp;
+    const int64_t* bounds;  // (T+1,) device
+    int T;
+    int64_t m, s;
+    int n;
+    const int64_t* ranks;   // (count,)
+    const int64_t* binom;
+    double* ssr;            // (count*T) scratch
+    double* ratio;          // (count*T) scratch
+    double* score;          // (count,) sum_t ssr / s
+    double* min_ratio;      // (count,) min over tasks of min|R_jj| / max|R_jj|
+    int64_t g0, total;      // set by the launcher
+};
+void launch_qr_screen(const QrArgs& a, int64_t count, cudaStream_t st, int64_t* launches);
 
 // ---- screened fit (fit3.cu) ----
 // TMA descriptors for the Gram viewed as a 2-D (T*mp rows x mp columns) f64 tensor;

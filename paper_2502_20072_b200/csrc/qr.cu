@@ -1,0 +1,156 @@
+// qr.cu -- QR screen for the tuples the Gram screen cannot certify (near-collinear
+// features, features nearly collinear with the intercept).
+//
+// One warp per (tuple, task) system [f_c0 .. f_c(n-1), 1 | y] (the reference's column
+// order, lsq.py:141-147).  Every lane folds its rows (i = lane, lane+32, ...) into a
+// register-resident upper-triangular R with Givens rotations, then the 32 triangles are
+// merged pairwise through warp shuffles (5 levels).  Givens QR is backward stable, and the
+// result is the reference's R up to signs and rounding, so
+//   ssr   = R[p][p]^2                          (p = n+1, the rhs column)
+//   ratio = min_j |R_jj| / max_j |R_jj|, j < p (the rank rule's quantity, lsq.py:96-101)
+// carry about eps/ratio relative error; the search refits bit-exactly (exact.cu) every
+// accepted tuple whose QR score can reach the top list within that margin (api.cu).
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace l0s {
+namespace {
+
+__device__ void unrank_q(int64_t rank, int64_t m, int n, const int64_t* binom, int64_t* out) {
+    int64_t r = rank, e = 0;
+    for (int k = 0; k < n; ++k) {
+        const int rem = n - k - 1;
+        for (;;) {
+            const int64_t c = binom[(int64_t)rem * (m + 1) + (m - 1 - e)];
+            if (r < c) break;
+            r -= c;
+            ++e;
+        }
+        out[k] = e++;
+    }
+}
+
+// packed upper triangle: row j starts at off(j) = j*NC - j*(j-1)/2
+template <int NC>
+__device__ __forceinline__ constexpr int off(int j) {
+    return j * NC - j * (j - 1) / 2;
+}
+
+// Fold row x (entries before `start` are zero) into R by Givens rotations.
+template <int NC>
+__device__ __forceinline__ void givens_row(double (&R)[NC * (NC + 1) / 2], double (&x)[NC], int start) {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+        if (j < start) continue;
+        const double a = R[off<NC>(j)], b = x[j];
+        if (b == 0.0) continue;
+        const double r = sqrt(fma(a, a, b * b));
+        const double ir = 1.0 / r;
+        const double c = a * ir, s = b * ir;
+        R[off<NC>(j)] = r;
+#pragma unroll
+        for (int k = j + 1; k < NC; ++k) {
+            const double rk = R[off<NC>(j) + (k - j)], xk = x[k];
+            R[off<NC>(j) + (k - j)] = fma(c, rk, s * xk);
+            x[k] = fma(c, xk, -s * rk);
+        }
+    }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256) k_qr_warp(QrArgs a) {
+    constexpr int NR = NC * (NC + 1) / 2;
+    const int lane = threadIdx.x & 31;
+    const int64_t g = a.g0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (g >= a.total) return;
+    const int64_t tup_i = g / a.T;
+    const int task = (int)(g % a.T);
+    const int n = NC - 2, p = NC - 1;
+    int64_t tup[NC - 2];
+    unrank_q(a.ranks[tup_i], a.m, n, a.binom, tup);
+    const int64_t lo = a.bounds[task];
+    const int rows = (int)(a.bounds[task + 1] - lo);
+    const double* X = a.Xp;
+    double R[NR];
+#pragma unroll
+    for (int e = 0; e < NR; ++e) R[e] = 0.0;
+    for (int i = lane; i < rows; i += 32) {
+        double x[NC];
+#pragma unroll
+        for (int k = 0; k < NC - 2; ++k) x[k] = X[tup[k] * a.s + lo + i];
+        x[NC - 2] = 1.0;
+        x[NC - 1] = a.yp[lo + i];
+        givens_row<NC>(R, x, 0);
+    }
+    // merge the lanes' triangles: partner rows enter as rows with leading zeros
+#pragma unroll
+    for (int offs = 16; offs >= 1; offs >>= 1) {
+        double P[NR];
+#pragma unroll
+        for (int e = 0; e < NR; ++e) P[e] = __shfl_down_sync(L0S_FULL, R[e], offs);
+        if (lane < offs) {
+#pragma unroll
+            for (int j = 0; j < NC; ++j) {
+                double x[NC];
+#pragma unroll
+                for (int k = 0; k < NC; ++k) x[k] = (k < j) ? 0.0 : P[off<NC>(j) + (k - j)];
+                givens_row<NC>(R, x, j);
+            }
+        }
+    }
+    if (lane == 0) {
+        double mx = 0.0, mn = INFINITY;
+#pragma unroll
+        for (int j = 0; j < NC - 1; ++j) {
+            const double d = (j < rows) ? fabs(R[off<NC>(j)]) : 0.0;
+            mx = fmax(mx, d);
+            mn = fmin(mn, d);
+        }
+        const double rpp = R[off<NC>(p)];
+        a.ssr[g] = (rows > p) ? rpp * rpp : 0.0;
+        a.ratio[g] = (mx > 0.0) ? mn / mx : 0.0;
+    }
+}
+
+// pooled score (sum over tasks in order / s) and the worst ratio over tasks
+__global__ void k_qr_finalize(QrArgs a, int64_t count) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= count) return;
+    double tot = 0.0, rmin = INFINITY;
+    for (int t = 0; t < a.T; ++t) {
+        tot += a.ssr[c * a.T + t];
+        rmin = fmin(rmin, a.ratio[c * a.T + t]);
+    }
+    a.score[c] = tot / (double)a.s;
+    a.min_ratio[c] = rmin;
+}
+
+}  // namespace
+
+void launch_qr_screen(const QrArgs& a0, int64_t count, cudaStream_t st, int64_t* launches) {
+    QrArgs a = a0;
+    a.total = count * a.T;
+    const int64_t per_launch = (int64_t)1 << 28;  // warps
+    for (int64_t g0 = 0; g0 < a.total; g0 += per_launch) {
+        a.g0 = g0;
+        const int64_t w = std::min(per_launch, a.total - g0);
+        const unsigned blocks = (unsigned)((w + 7) / 8);
+        switch (a.n) {
+            case 1: k_qr_warp<3><<<blocks, 256, 0, st>>>(a); break;
+            case 2: k_qr_warp<4><<<blocks, 256, 0, st>>>(a); break;
+            case 3: k_qr_warp<5><<<blocks, 256, 0, st>>>(a); break;
+            case 4: k_qr_warp<6><<<blocks, 256, 0, st>>>(a); break;
+            case 5: k_qr_warp<7><<<blocks, 256, 0, st>>>(a); break;
+            default: k_qr_warp<8><<<blocks, 256, 0, st>>>(a); break;
+        }
+        if (launches) ++*launches;
+    }
+    if (count > 0) {
+        k_qr_finalize<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(a, count);
+        if (launches) ++*launches;
+    }
+}
+
+}  // namespace l0s

@@ -46,6 +46,12 @@ __global__ void k_normalize(const W* __restrict__ Xp, const W* __restrict__ yp, 
     for (int64_t i = lane; i < r; i += 32) sum += (double)src[i];
     sum = warp_sum(sum);
     double mean = sum / (double)r;
+    // second pass refines the mean to the rounding level of the *centered* values: an offset
+    // of the computed mean would leave the columns uncentered by (mu - mean), an error the
+    // Gram bound does not cover for near-constant features (mean/std ratio rho >> 1)
+    double corr = 0.0;
+    for (int64_t i = lane; i < r; i += 32) corr += (double)src[i] - mean;
+    mean += warp_sum(corr) / (double)r;
     double cs = 0.0, us = 0.0;
     for (int64_t i = lane; i < r; i += 32) {
         double x = (double)src[i];
