@@ -46,16 +46,61 @@ __device__ __forceinline__ void givens_row(double (&R)[NC * (NC + 1) / 2], doubl
         if (j < start) continue;
         const double a = R[off<NC>(j)], b = x[j];
         if (b == 0.0) continue;
-        const double r = sqrt(fma(a, a, b * b));
-        const double ir = 1.0 / r;
+        // 1/sqrt(a^2 + b^2): MUFU seed + two Newton steps (full precision, no divide)
+        const double q = fma(a, a, b * b);
+        double ir;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(ir) : "d"(q));
+        ir = ir * fma(-0.5 * q * ir, ir, 1.5);
+        ir = ir * fma(-0.5 * q * ir, ir, 1.5);
         const double c = a * ir, s = b * ir;
-        R[off<NC>(j)] = r;
+        R[off<NC>(j)] = q * ir;
 #pragma unroll
         for (int k = j + 1; k < NC; ++k) {
             const double rk = R[off<NC>(j) + (k - j)], xk = x[k];
             R[off<NC>(j) + (k - j)] = fma(c, rk, s * xk);
             x[k] = fma(c, xk, -s * rk);
         }
+    }
+}
+
+// Fold a block of B rows X[b][.] (entries before `start` zero) into R by one structured
+// Householder reflection per column: the reflector touches R's row j and the block only.
+// B rows share each square root and reciprocal; the dot products are short trees.
+template <int NC, int B>
+__device__ __forceinline__ void householder_block(double (&R)[NC * (NC + 1) / 2], double (&X)[B][NC], int start) {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+        if (j < start) continue;
+        const double rjj = R[off<NC>(j)];
+        double nb = 0.0;
+#pragma unroll
+        for (int b = 0; b < B; ++b) nb = fma(X[b][j], X[b][j], nb);
+        if (nb == 0.0) continue;  // the block is already zero in this column
+        const double nrm2 = fma(rjj, rjj, nb);
+        double ir;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(ir) : "d"(nrm2));
+        ir = ir * fma(-0.5 * nrm2 * ir, ir, 1.5);
+        ir = ir * fma(-0.5 * nrm2 * ir, ir, 1.5);
+        const double nrm = nrm2 * ir;
+        const double alpha = rjj >= 0.0 ? -nrm : nrm;
+        const double v0 = rjj - alpha;
+        const double vtv = fma(v0, v0, nb);  // = 2 nrm (nrm + |rjj|)
+        double iv;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(iv) : "d"(vtv));
+        iv = iv * fma(-vtv, iv, 2.0);
+        iv = iv * fma(-vtv, iv, 2.0);
+        const double f2 = 2.0 * iv;
+#pragma unroll
+        for (int c = j + 1; c < NC; ++c) {
+            double w = v0 * R[off<NC>(j) + (c - j)];
+#pragma unroll
+            for (int b = 0; b < B; ++b) w = fma(X[b][j], X[b][c], w);
+            const double f = w * f2;
+            R[off<NC>(j) + (c - j)] = fma(-f, v0, R[off<NC>(j) + (c - j)]);
+#pragma unroll
+            for (int b = 0; b < B; ++b) X[b][c] = fma(-f, X[b][j], X[b][c]);
+        }
+        R[off<NC>(j)] = alpha;
     }
 }
 
@@ -73,16 +118,23 @@ __global__ void __launch_bounds__(256) k_qr_warp(QrArgs a) {
     const int64_t lo = a.bounds[task];
     const int rows = (int)(a.bounds[task + 1] - lo);
     const double* X = a.Xp;
+    // lane-local TSQR: blocks of QB rows (rows lane, lane+32, ...) folded into R
+    constexpr int QB = 4;
     double R[NR];
 #pragma unroll
     for (int e = 0; e < NR; ++e) R[e] = 0.0;
-    for (int i = lane; i < rows; i += 32) {
-        double x[NC];
+    for (int i0 = lane; i0 < rows; i0 += 32 * QB) {
+        double Xb[QB][NC];
 #pragma unroll
-        for (int k = 0; k < NC - 2; ++k) x[k] = X[tup[k] * a.s + lo + i];
-        x[NC - 2] = 1.0;
-        x[NC - 1] = a.yp[lo + i];
-        givens_row<NC>(R, x, 0);
+        for (int b = 0; b < QB; ++b) {
+            const int i = i0 + 32 * b;
+            const bool in = i < rows;
+#pragma unroll
+            for (int k = 0; k < NC - 2; ++k) Xb[b][k] = in ? X[tup[k] * a.s + lo + i] : 0.0;
+            Xb[b][NC - 2] = in ? 1.0 : 0.0;
+            Xb[b][NC - 1] = in ? a.yp[lo + i] : 0.0;
+        }
+        householder_block<NC, QB>(R, Xb, 0);
     }
     // merge the lanes' triangles: partner rows enter as rows with leading zeros
 #pragma unroll
