@@ -10,7 +10,10 @@ namespace l0s {
 namespace fit {
 
 constexpr int NW = 8;                 // warps per CTA
-constexpr int CAP = 256;              // per-warp candidate buffer
+#ifndef L0S_CAP
+#define L0S_CAP 256
+#endif
+constexpr int CAP = L0S_CAP;          // per-warp candidate buffer (K' <= CAP - 32)
 constexpr double FO_LIM = 1e-3;       // first-order validity: (eta + gam rho)(1 + n tr) <= FO_LIM
 constexpr double RANK_SLACK = 1.01;   // safety factor on the rank-rule certificate
 constexpr double LOOSE = 1e-3;        // bounds looser than this fraction of |y_c|^2 go to the exact kernel
