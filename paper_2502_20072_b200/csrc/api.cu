@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/l0search.h"
@@ -74,6 +75,11 @@ int64_t binom_sat(int64_t a, int64_t b) {
     return (int64_t)r;
 }
 
+struct Rec {  // bit-exact record of one refit tuple
+    double score;
+    std::vector<double> coef, ssr;
+};
+
 }  // namespace
 
 struct l0s_ctx {
@@ -88,7 +94,7 @@ struct l0s_ctx {
     std::vector<double> rows_h, eta_h, yyu_h;
     double ms_gram = 0.0;
     DBuf in_values, in_y, in_perm, bounds_d, zoff_d, Xp, yp, Z, G, qf, un2, yyu, rowsd, eta_d;
-    DBuf rho, rho_cap, ynorm, iforce, dead;
+    DBuf rho, rho_cap, ynorm, iforce, dead, umin;
     int64_t n_dead = 0, n_iforce = 0;
     // binomial table (k <= binom_n) x (a <= m)
     DBuf binom;
@@ -99,12 +105,13 @@ struct l0s_ctx {
         lb_tmp, rank_tmp, coll_lb, coll_rank, coll_cnt;
     DBuf ex_scratch, ex_ssr_tmp, ex_ok_tmp, ex_ok, ex_score, ex_coef, ex_ssr, ex_ranks, ex_tuples;
     DBuf qr_ssr, qr_ratio, qr_score, qr_minr;
+    std::unordered_map<int64_t, Rec> recs;  // records of this search's refit candidates
     std::vector<int4> units_h;
     int64_t units_key[5] = {-1, -1, -1, -1, -1};
 
     ~l0s_ctx() {
         DBuf* all[] = {&in_values, &in_y, &in_perm, &bounds_d, &zoff_d, &Xp, &yp, &Z, &G, &qf, &un2, &yyu, &rowsd,
-                       &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &binom, &units, &ucount, &theta_g, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
+                       &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &umin, &binom, &units, &ucount, &theta_g, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
                        &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
                        &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr};
@@ -203,17 +210,36 @@ void merge_best(std::vector<Cand>& best, const std::vector<Cand>& more, int64_t 
 }
 
 // Exact scores for device ranks [0, count) of c->ex_ranks; appends finite (score, rank) to out.
+// Exact scores for `count` device ranks; with `recs`, also keep each tuple's coefficients and
+// per-task ssr (small candidate sets), so the final records need no second launch.
 int exact_ranks_to_host(l0s_ctx* c, int n, const int64_t* ranks_d, int64_t count, std::vector<Cand>& out,
-                        int64_t* launches) {
+                        int64_t* launches, std::unordered_map<int64_t, Rec>* recs = nullptr) {
     if (count <= 0) return L0S_OK;
-    int rc = run_exact(c, n, ranks_d, nullptr, count, false, launches);
+    const bool keep_rec = recs != nullptr && count <= 4096;
+    int rc = run_exact(c, n, ranks_d, nullptr, count, keep_rec, launches);
     if (rc) return rc;
     std::vector<double> sc((size_t)count);
     std::vector<int64_t> rk((size_t)count);
+    std::vector<double> cf, ss;
+    const int p = n + 1;
     CK(cudaMemcpyAsync(sc.data(), c->ex_score.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(rk.data(), ranks_d, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, c->st));
+    if (keep_rec) {
+        cf.resize((size_t)(count * c->T * p));
+        ss.resize((size_t)(count * c->T));
+        CK(cudaMemcpyAsync(cf.data(), c->ex_coef.p, sizeof(double) * cf.size(), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(ss.data(), c->ex_ssr.p, sizeof(double) * ss.size(), cudaMemcpyDeviceToHost, c->st));
+    }
     CK(cudaStreamSynchronize(c->st));
-    for (int64_t i = 0; i < count; ++i) out.push_back({sc[(size_t)i], rk[(size_t)i]});
+    for (int64_t i = 0; i < count; ++i) {
+        out.push_back({sc[(size_t)i], rk[(size_t)i]});
+        if (keep_rec && std::isfinite(sc[(size_t)i])) {
+            Rec& r = (*recs)[rk[(size_t)i]];
+            r.score = sc[(size_t)i];
+            r.coef.assign(cf.begin() + i * c->T * p, cf.begin() + (i + 1) * c->T * p);
+            r.ssr.assign(ss.begin() + i * c->T, ss.begin() + (i + 1) * c->T);
+        }
+    }
     return L0S_OK;
 }
 
@@ -336,66 +362,21 @@ int l0s_stage(l0s_ctx* c, const double* values, int64_t m, int64_t s, const doub
     launch_gram(c->Z.as<double>(), c->sp, c->zoff_h.data(), c->zoff_d.as<int64_t>(), c->rpad_h.data(), ntasks, m, c->mp, c->G.as<double>(),
                 c->st);
     CK(cudaGetLastError());
-    cudaEventRecord(c->ev[1], c->st);
-    c->yyu_h.assign((size_t)ntasks, 0.0);
-    std::vector<double> qh((size_t)(m * ntasks)), uh((size_t)(m * ntasks));
-    CK(cudaMemcpyAsync(c->yyu_h.data(), c->yyu.p, sizeof(double) * ntasks, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(qh.data(), c->qf.p, sizeof(double) * m * ntasks, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(uh.data(), c->un2.p, sizeof(double) * m * ntasks, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    // Per-feature conditioning of the reference's uncentered QR (error model):
-    //   rho = |f| / |f_c| enters the bound on the reference's own error;
-    //   a feature is dead when the reference's rank rule rejects every tuple holding it:
-    //   |R_nn| <= sqrt(r q) (distance of the intercept column to the feature) while
-    //   max|R| >= min_f |f|, so sqrt(q) + 4 gam < tol/2 * sqrt(min|f|^2 / r) is certain rejection.
-    std::vector<double> rho_h((size_t)(m * ntasks)), cap_h((size_t)ntasks), yn_h((size_t)ntasks);
-    std::vector<unsigned char> iforce_h((size_t)m, 0);
-    std::vector<int32_t> dead_h;
-    std::vector<unsigned char> dead_f((size_t)m, 0);
-    for (int t = 0; t < ntasks; ++t) {
-        const double r = c->rows_h[t];
-        // the Gram (hence dead marking) serves the screened path only, n <= 4;
-        // same reference rounding model as fit::ref_gamma (fitcommon.cuh)
-        const double gam = 2.0 * 8.0 * std::sqrt(r + 1.0) * (4 + 2) * kEps;
-        double umin = INFINITY;
-        for (int64_t f = 0; f < m; ++f) umin = std::min(umin, uh[(size_t)(t * m + f)]);
-        const double lim = 0.5 * 1e-10 * std::sqrt(umin / std::max(r, 1.0)) - 4.0 * gam;
-        double rmax = 1.0;
-        for (int64_t f = 0; f < m; ++f) {
-            const double q = qh[(size_t)(t * m + f)];
-            const double rf = 1.0 / std::sqrt(q);
-            rho_h[(size_t)(t * m + f)] = std::isfinite(rf) ? rf : INFINITY;
-            if (lim > 0.0 && std::sqrt(q) < lim) dead_f[(size_t)f] = 1;
-            else if (std::isfinite(rf)) rmax = std::max(rmax, rf);
-        }
-        cap_h[(size_t)t] = std::min(32.0, rmax);
-        yn_h[(size_t)t] = std::sqrt(c->yyu_h[(size_t)t]);
-    }
-    for (int64_t f = 0; f < m; ++f) {
-        if (dead_f[(size_t)f]) {
-            dead_h.push_back((int32_t)f);
-            continue;
-        }
-        for (int t = 0; t < ntasks; ++t)
-            if (rho_h[(size_t)(t * m + f)] > cap_h[(size_t)t]) iforce_h[(size_t)f] = 1;
-    }
+    // per-feature conditioning flags on the device (stage.cu: launch_feature_flags)
     CK(c->rho.ensure(sizeof(double) * m * ntasks));
     CK(c->rho_cap.ensure(sizeof(double) * ntasks));
     CK(c->ynorm.ensure(sizeof(double) * ntasks));
+    CK(c->umin.ensure(sizeof(double) * ntasks));
     CK(c->iforce.ensure((size_t)m));
-    CK(cudaMemcpyAsync(c->rho.p, rho_h.data(), sizeof(double) * m * ntasks, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->rho_cap.p, cap_h.data(), sizeof(double) * ntasks, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->ynorm.p, yn_h.data(), sizeof(double) * ntasks, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->iforce.p, iforce_h.data(), (size_t)m, cudaMemcpyHostToDevice, c->st));
-    if (!dead_h.empty()) {
-        CK(c->dead.ensure(sizeof(int32_t) * dead_h.size()));
-        CK(cudaMemcpyAsync(c->dead.p, dead_h.data(), sizeof(int32_t) * dead_h.size(), cudaMemcpyHostToDevice, c->st));
-        launch_mark_dead(c->G.as<double>(), c->dead.as<int32_t>(), (int)dead_h.size(), ntasks, c->mp, c->st);
-        CK(cudaGetLastError());
-    }
-    c->n_dead = (int64_t)dead_h.size();
-    c->n_iforce = 0;
-    for (unsigned char x : iforce_h) c->n_iforce += x;
+    CK(c->dead.ensure((size_t)m));
+    launch_feature_flags(c->qf.as<double>(), c->un2.as<double>(), c->rowsd.as<double>(), m, c->mp, ntasks,
+                         c->umin.as<double>(), c->rho.as<double>(), c->rho_cap.as<double>(),
+                         c->dead.as<unsigned char>(), c->iforce.as<unsigned char>(), c->G.as<double>(),
+                         c->yyu.as<double>(), c->ynorm.as<double>(), c->st);
+    CK(cudaGetLastError());
+    cudaEventRecord(c->ev[1], c->st);
+    c->yyu_h.assign((size_t)ntasks, 0.0);
+    CK(cudaMemcpyAsync(c->yyu_h.data(), c->yyu.p, sizeof(double) * ntasks, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     c->ms_gram = elapsed(c->ev[0], c->ev[1]);
     c->staged = true;
@@ -622,7 +603,7 @@ static int screen_ill(l0s_ctx* c, int n, int64_t nill, int64_t keep, std::vector
     CK(c->ex_ranks.ensure(sizeof(int64_t) * sel.size()));
     CK(cudaMemcpyAsync(c->ex_ranks.p, sel.data(), sizeof(int64_t) * sel.size(), cudaMemcpyHostToDevice, c->st));
     std::vector<Cand> more;
-    int rc = exact_ranks_to_host(c, n, c->ex_ranks.as<int64_t>(), (int64_t)sel.size(), more, &st->n_launches);
+    int rc = exact_ranks_to_host(c, n, c->ex_ranks.as<int64_t>(), (int64_t)sel.size(), more, &st->n_launches, &c->recs);
     if (rc) return rc;
     st->n_candidates += (int64_t)sel.size();
     merge_best(best, more, keep);
@@ -716,7 +697,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     // exact refit of candidates + ill tuples
     std::vector<Cand> exact;
     cudaEventRecord(c->ev[2], c->st);
-    int rc = exact_ranks_to_host(c, n, c->cand_rank.as<int64_t>(), nc, exact, &st->n_launches);
+    int rc = exact_ranks_to_host(c, n, c->cand_rank.as<int64_t>(), nc, exact, &st->n_launches, &c->recs);
     if (rc) return rc;
     merge_best(best, exact, keep);
     if (nill > 0) {
@@ -774,7 +755,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
             return fail(L0S_ECAPACITY, "%llu tuples below the certification threshold exceed the rescan buffer",
                         (unsigned long long)ncoll);
         std::vector<Cand> more;
-        rc = exact_ranks_to_host(c, n, c->coll_rank.as<int64_t>(), (int64_t)ncoll, more, &st->n_launches);
+        rc = exact_ranks_to_host(c, n, c->coll_rank.as<int64_t>(), (int64_t)ncoll, more, &st->n_launches, &c->recs);
         if (rc) return rc;
         st->n_candidates += (int64_t)ncoll;
         merge_best(best, more, keep);
@@ -803,6 +784,7 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
     st->ms_gram = c->ms_gram;
     if (rb >= re) return L0S_OK;
     rc = ensure_binom(c, n);
+    c->recs.clear();
     if (rc) return rc;
     cudaEvent_t t0, t1;
     cudaEventCreate(&t0);
@@ -832,9 +814,21 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
         cudaEventDestroy(t1);
         return rc;
     }
-    // final records: coefficients and per-task ssr of the kept tuples (bit-exact kernel)
+    // final records: coefficients and per-task ssr of the kept tuples (bit-exact kernel); the
+    // screened path already holds them from the candidate refit
     int64_t nk = (int64_t)best.size();
-    if (nk > 0) {
+    bool have_all = nk > 0;
+    for (int64_t i = 0; i < nk && have_all; ++i) have_all = c->recs.count(best[(size_t)i].rank) != 0;
+    if (have_all) {
+        const int p = n + 1;
+        for (int64_t i = 0; i < nk; ++i) {
+            const Rec& r = c->recs[best[(size_t)i].rank];
+            if (out_coef) std::copy(r.coef.begin(), r.coef.end(), out_coef + i * c->T * p);
+            if (out_ssr) std::copy(r.ssr.begin(), r.ssr.end(), out_ssr + i * c->T);
+            out_scores[i] = best[(size_t)i].score;
+            out_ranks[i] = best[(size_t)i].rank;
+        }
+    } else if (nk > 0) {
         std::vector<int64_t> rk((size_t)nk);
         for (int64_t i = 0; i < nk; ++i) rk[(size_t)i] = best[(size_t)i].rank;
         CK(c->ex_ranks.ensure(sizeof(int64_t) * std::max<int64_t>(nk, 1 << 10)));

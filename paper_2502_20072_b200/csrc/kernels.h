@@ -20,6 +20,11 @@ void launch_normalize(const void* Xp, const void* yp, int precision, int64_t m, 
                       const int64_t* bounds_d, const int64_t* zoff_d, int T, int64_t sp, double* Z,
                       double* qf, double* un2, double* yyu, cudaStream_t st);
 
+// rho, dead, rho_cap, iforce from qf / un2 (stage.cu), and NaN rows/cols of dead features in G
+void launch_feature_flags(const double* qf, const double* un2, const double* rows, int64_t m, int64_t mp, int T,
+                          double* umin, double* rho, double* rho_cap, unsigned char* dead, unsigned char* iforce,
+                          double* G, const double* yyu, double* ynorm, cudaStream_t st);
+
 // ---- Gram (gram.cu): G[t] = Z_t Z_t^T on DMMA, (mp x mp) per task, diag of features := 1 ----
 void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_h, const int64_t* zoff_d, const int64_t* rpad_h, int T,
                  int64_t m, int64_t mp, double* G, cudaStream_t st);

@@ -77,6 +77,112 @@ __global__ void k_normalize(const W* __restrict__ Xp, const W* __restrict__ yp, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Per-feature conditioning flags for the screened path, on the device:
+//   rho[t][f] = |f| / |f_c| = q^-1/2,  dead[f]: the reference's rank rule rejects every
+//   tuple holding f,  rho_cap[t] = min(32, max rho over live features),  iforce[f]: some
+//   task's rho exceeds its cap (the sweep then takes the slow path for that feature).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double block_reduce(double v, bool is_max, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) {
+        double w = __shfl_xor_sync(L0S_FULL, v, o);
+        v = is_max ? fmax(v, w) : fmin(v, w);
+    }
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r = sh[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = is_max ? fmax(r, sh[w]) : fmin(r, sh[w]);
+        sh[0] = r;
+    }
+    __syncthreads();
+    double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+__global__ void k_task_umin(const double* __restrict__ un2, int64_t m, double* __restrict__ umin,
+                            const double* __restrict__ yyu, double* __restrict__ ynorm) {
+    __shared__ double sh[32];
+    const int t = blockIdx.x;
+    if (threadIdx.x == 0) ynorm[t] = sqrt(yyu[t]);
+    double v = INFINITY;
+    for (int64_t f = threadIdx.x; f < m; f += blockDim.x) v = fmin(v, un2[(int64_t)t * m + f]);
+    v = block_reduce(v, false, sh);
+    if (threadIdx.x == 0) umin[t] = v;
+}
+
+__global__ void k_feature_flags(const double* __restrict__ qf, const double* __restrict__ umin,
+                                const double* __restrict__ rows, int64_t m, int T, double* __restrict__ rho,
+                                unsigned char* __restrict__ dead) {
+    const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= m) return;
+    bool d = false;
+    for (int t = 0; t < T; ++t) {
+        const double q = qf[(int64_t)t * m + f];
+        const double rf = 1.0 / sqrt(q);
+        rho[(int64_t)t * m + f] = (rf == rf && rf < INFINITY) ? rf : INFINITY;
+        // |R_nn| <= sqrt(r q) and max|R| >= min_f |f|: certain rejection (n <= 4 rounding model)
+        const double r = rows[t];
+        const double gam = 2.0 * 8.0 * sqrt(r + 1.0) * 6.0 * kEps;
+        const double lim = 0.5 * 1e-10 * sqrt(umin[t] / fmax(r, 1.0)) - 4.0 * gam;
+        if (lim > 0.0 && sqrt(q) < lim) d = true;
+    }
+    dead[f] = d ? 1 : 0;
+}
+
+__global__ void k_task_rhocap(const double* __restrict__ rho, const unsigned char* __restrict__ dead, int64_t m,
+                              double* __restrict__ cap) {
+    __shared__ double sh[32];
+    const int t = blockIdx.x;
+    double v = 1.0;
+    for (int64_t f = threadIdx.x; f < m; f += blockDim.x) {
+        const double r = rho[(int64_t)t * m + f];
+        if (!dead[f] && r < INFINITY) v = fmax(v, r);
+    }
+    v = block_reduce(v, true, sh);
+    if (threadIdx.x == 0) cap[t] = fmin(32.0, v);
+}
+
+__global__ void k_feature_iforce(const double* __restrict__ rho, const double* __restrict__ cap,
+                                 const unsigned char* __restrict__ dead, int64_t m, int T,
+                                 unsigned char* __restrict__ iforce) {
+    const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= m) return;
+    bool fo = false;
+    if (!dead[f])
+        for (int t = 0; t < T; ++t)
+            if (rho[(int64_t)t * m + f] > cap[t]) fo = true;
+    iforce[f] = fo ? 1 : 0;
+}
+
+// NaN the Gram row and column of every dead feature (all tasks): its tuples then never pass the screen.
+__global__ void k_mark_dead_rows(double* __restrict__ G, const unsigned char* __restrict__ dead, int64_t m, int64_t mp,
+                                 int T) {
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    const int64_t f = blockIdx.y;
+    if (f >= m || !dead[f]) return;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)T * mp;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int t = (int)(e / mp);
+        const int64_t x = e % mp;
+        double* Gt = G + (int64_t)t * mp * mp;
+        Gt[f * mp + x] = nan;
+        Gt[x * mp + f] = nan;
+    }
+}
+
+void launch_feature_flags(const double* qf, const double* un2, const double* rows, int64_t m, int64_t mp, int T,
+                          double* umin, double* rho, double* rho_cap, unsigned char* dead, unsigned char* iforce,
+                          double* G, const double* yyu, double* ynorm, cudaStream_t st) {
+    const unsigned fb = (unsigned)((m + 255) / 256);
+    k_task_umin<<<T, 256, 0, st>>>(un2, m, umin, yyu, ynorm);
+    k_feature_flags<<<fb, 256, 0, st>>>(qf, umin, rows, m, T, rho, dead);
+    k_task_rhocap<<<T, 256, 0, st>>>(rho, dead, m, rho_cap);
+    k_feature_iforce<<<fb, 256, 0, st>>>(rho, rho_cap, dead, m, T, iforce);
+    k_mark_dead_rows<<<dim3(4, (unsigned)m), 256, 0, st>>>(G, dead, m, mp, T);
+}
+
 void launch_gather(const double* values, const double* y, const int64_t* perm, int64_t m, int64_t s,
                    int precision, void* Xp, void* yp, cudaStream_t st) {
     dim3 grid((unsigned)((s + 255) / 256 < 64 ? (s + 255) / 256 : 64), (unsigned)(m + 1));
