@@ -24,3 +24,6 @@ timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/${tag}_bench.json
 echo "bench rc=$?"
 kill $smi 2>/dev/null
 tail -1 gpurun_out/${tag}_bench.json
+python tools/summarize_launches.py gpurun_out/${tag}_launches.csv "${tag} launch list (ncu gpu__time_duration + dram bytes, --clock-control none; bench.py --steps 2 --warmup 1; cold-cache, serialised)" > gpurun_out/${tag}_launches_summary.txt
+timeout 300 python tools/e2e_probe.py > gpurun_out/${tag}_e2e_probe.txt 2>&1
+echo "e2e probe rc=$?"
