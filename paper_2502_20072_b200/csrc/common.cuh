@@ -38,12 +38,23 @@ __host__ __device__ inline double ord_dec(unsigned long long u) {
 // bounded by kRcpRel (measured exhaustively over mantissas by
 // tests/test_gpu_kernels.py::test_rcp_fast_bound); the screen absorbs it by
 // shrinking its threshold, so a tuple is never dropped because of it.
-constexpr double kRcpRel = 1.0 / 131072.0;  // 2^-17, conservative
+constexpr double kRcpRel = 1.0 / 65536.0;  // 2^-16, conservative (measured < 2^-17)
 __device__ __forceinline__ double rcp_fast_abs(double d) {
     int hi = __double2hiint(d) & 0x7fffffff;
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(__hiloint2double(hi, 0)));
     return r;
+}
+
+// The sweep's form of the same: MUFU.RCP64H on d's high word, with d's own low word kept
+// as the result's low word (a < 2^-20 relative perturbation, inside kRcpRel), so ptxas
+// writes the result in place -- no zeroing move.  The sign is d's: callers take fabs() of
+// the result inside their FMA, a free DFMA operand modifier (one MUFU per reciprocal, no
+// integer op).
+__device__ __forceinline__ double rcp_sweep(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    return __hiloint2double(__double2hiint(r), __double2loint(d));
 }
 
 // Same for d known to be positive: MUFU.RCP64H straight on the high word.

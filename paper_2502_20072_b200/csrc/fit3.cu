@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
                             if (NT == 1)
                                 acc[p] = fma(acc[p], d, -q);  // (K - theta) d - q; d <= 0 also passes
                             else
-                                acc[p] = fma(-q, rcp_fast_abs(d), acc[p]);  // 1/|d|: d <= 0 drives acc down
+                                acc[p] = fma(-q, fabs(rcp_sweep(d)), acc[p]);  // 1/|d|: d <= 0 drives acc down
                         }
                     }
                     unsigned pass = forced;

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs
                             if (NT == 1)
                                 acc[p] = fma(acc[p], d, -q);
                             else
-                                acc[p] = fma(-q, rcp_fast_abs(d), acc[p]);
+                                acc[p] = fma(-q, fabs(rcp_sweep(d)), acc[p]);
                         }
                     }
                     unsigned pass = forced;

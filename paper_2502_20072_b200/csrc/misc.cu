@@ -113,6 +113,9 @@ __global__ void k_rcp_check(int64_t count, double* out) {
         double r = rcp_fast_abs(d);
         double err = fabs(fma(r, fabs(d), -1.0));
         worst = fmax(worst, err);
+        r = fabs(rcp_sweep(d));
+        err = fabs(fma(r, fabs(d), -1.0));
+        worst = fmax(worst, err);
     }
     for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(L0S_FULL, worst, o));
     if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long*)out, (unsigned long long)__double_as_longlong(worst));

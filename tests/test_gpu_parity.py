@@ -171,7 +171,7 @@ def test_rcp_fast_bound():
 
     worst = ctypes.c_double()
     assert _lib.lib().l0s_rcp_check(1 << 26, ctypes.byref(worst)) == 0
-    assert worst.value <= 2.0 ** -17, worst.value
+    assert worst.value <= 2.0 ** -16, worst.value
 
 
 @pytest.mark.parametrize("T", [1, 3])
