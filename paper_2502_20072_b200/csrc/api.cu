@@ -101,7 +101,7 @@ struct l0s_ctx {
     int binom_n = -1;
     int64_t binom_m = -1;
     // search workspace
-    DBuf units, ucount, theta_g, wl_lb, wl_rank, wl_cnt, ill, ill_cnt, cand_lb, cand_rank, cand_cnt, sort_tmp,
+    DBuf units, ucount, theta_g, hist, wl_lb, wl_rank, wl_cnt, ill, ill_cnt, cand_lb, cand_rank, cand_cnt, sort_tmp,
         lb_tmp, rank_tmp, coll_lb, coll_rank, coll_cnt;
     DBuf ex_scratch, ex_ssr_tmp, ex_ok_tmp, ex_ok, ex_score, ex_coef, ex_ssr, ex_ranks, ex_tuples;
     DBuf qr_ssr, qr_ratio, qr_score, qr_minr;
@@ -111,7 +111,7 @@ struct l0s_ctx {
 
     ~l0s_ctx() {
         DBuf* all[] = {&in_values, &in_y, &in_perm, &bounds_d, &zoff_d, &Xp, &yp, &Z, &G, &qf, &un2, &yyu, &rowsd,
-                       &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &umin, &binom, &units, &ucount, &theta_g, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
+                       &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &umin, &binom, &units, &ucount, &theta_g, &hist, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
                        &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
                        &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr};
@@ -631,6 +631,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     const int64_t ill_cap = (int64_t)1 << 26;  // 512 MB of ranks; overflow is reported, never dropped
     CK(c->ucount.ensure(sizeof(int) * 4));
     CK(c->theta_g.ensure(sizeof(unsigned long long)));
+    CK(c->hist.ensure(sizeof(unsigned) * HIST_BINS));
     CK(c->wl_lb.ensure(sizeof(double) * slots * kc));
     CK(c->wl_rank.ensure(sizeof(int64_t) * slots * kc));
     CK(c->wl_cnt.ensure(sizeof(int) * slots));
@@ -657,6 +658,12 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     a.collect = 0;
     a.theta0 = INFINITY;
     a.theta_g = c->theta_g.as<unsigned long long>();
+    a.hist = c->hist.as<unsigned>();
+    {
+        double yy_top = 0.0;  // uncentered total |y|^2 >= every pooled bound
+        for (double v : c->yyu_h) yy_top += v;
+        a.hist_base = hist_base_for(yy_top > 0.0 ? yy_top : 1.0);
+    }
     a.wl_lb = c->wl_lb.as<double>();
     a.wl_rank = c->wl_rank.as<int64_t>();
     a.wl_cnt = c->wl_cnt.as<int>();
@@ -666,6 +673,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
 
     CK(cudaMemsetAsync(c->ucount.p, 0, sizeof(int) * 4, c->st));
     CK(cudaMemcpyAsync(c->theta_g.p, &inf_enc, sizeof inf_enc, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemsetAsync(c->hist.p, 0, sizeof(unsigned) * HIST_BINS, c->st));
     CK(cudaMemsetAsync(c->ill_cnt.p, 0, sizeof(unsigned long long), c->st));
     CK(cudaMemsetAsync(c->cand_cnt.p, 0, sizeof(unsigned long long), c->st));
     cudaEventRecord(c->ev[2], c->st);
@@ -673,7 +681,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     cudaEventRecord(c->ev[3], c->st);
     CK(cudaGetLastError());
     st->n_fit_launches++;
-    st->n_launches++;
+    st->n_launches += 2;  // threshold seed + sweep
     launch_gather_candidates(a.wl_lb, a.wl_rank, a.wl_cnt, slots, kc, a.theta_g, c->cand_lb.as<double>(),
                              c->cand_rank.as<int64_t>(), c->cand_cnt.as<unsigned long long>(), c->st);
     st->n_launches++;
@@ -691,9 +699,14 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
                (int64_t)ncand, c->sort_tmp.p, tb, c->st);
     st->n_launches += 3;
     const int64_t nc = std::min<int64_t>((int64_t)ncand, kc);
-    double G_lb = INFINITY;  // K'-th smallest lower bound (SSR units): every excluded tuple has lb >= G_lb
-    if ((int64_t)ncand >= kc)
+    // every excluded tuple has lb >= G_lb (SSR units): the K'-th smallest gathered bound, or
+    // -- fewer gathered -- the final shared threshold (+inf: nothing was ever dropped)
+    double G_lb = st->theta;
+    if ((int64_t)ncand >= kc) {
         CK(cudaMemcpyAsync(&G_lb, c->cand_lb.as<double>() + (kc - 1), sizeof(double), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        G_lb = std::min(G_lb, st->theta);
+    }
     // exact refit of candidates + ill tuples
     std::vector<Cand> exact;
     cudaEventRecord(c->ev[2], c->st);
@@ -718,7 +731,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     double yy = 0.0;
     for (double v : c->yyu_h) yy += v;
     auto margin_of = [&](double sk) { return 1e-10 * std::fabs(sk) + 64.0 * kEps * yy / (double)c->s; };
-    bool complete = (int64_t)ncand < kc;  // nothing was ever dropped by the K' cut
+    bool complete = !std::isfinite(G_lb);  // nothing was ever dropped
     double sk = ((int64_t)best.size() >= keep) ? best[(size_t)keep - 1].score : INFINITY;
     bool certified = complete || (G_lb / (double)c->s > sk + margin_of(sk));
     st->margin = G_lb / (double)c->s - sk;

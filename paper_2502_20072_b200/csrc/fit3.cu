@@ -24,6 +24,7 @@
 // shared memory by cp.async (double-buffered over IB-row tiles); the (j, k)
 // state lives in registers.  Persistent CTAs pull units from an atomic counter.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "fitcommon.cuh"
@@ -47,6 +48,9 @@ namespace {
 #ifndef L0S_C34_UNROLL
 #define L0S_C34_UNROLL 1
 #endif
+#ifndef L0S_PRUNE_ROWS
+#define L0S_PRUNE_ROWS 2
+#endif
 struct CfgT {
     int P, IB, MINB, UNROLL;
 };
@@ -64,7 +68,11 @@ struct Cfg {
     static constexpr int BS = NT * TS;
     static constexpr int MINB = c.MINB;
     static constexpr int UNROLL = c.UNROLL;  // rows of the i sweep in flight per thread
-    static constexpr size_t smem_bytes = (size_t)2 * BS * 8 + (size_t)NW * CAP * 16 + (size_t)256 * P * 8;
+    // task pruning (NT > 1): rows per vote group, and per-thread smem slots for the
+    // per-task constants (P x KS doubles: the total, then tasks 1..NT-1 for NT >= 3)
+    static constexpr int R = (NT == 1) ? 1 : L0S_PRUNE_ROWS;
+    static constexpr int KS = (NT >= 3) ? NT : 1;
+    static constexpr size_t smem_bytes = (size_t)2 * BS * 8 + (size_t)NW * CAP * 16 + (size_t)256 * P * KS * 8;
 };
 
 // Exact lower bound of one tuple (i < j < k) read straight from the Gram, with the
@@ -74,9 +82,11 @@ struct Cfg {
 // Shared by the fit kernel's slow path and k_screen3 (so the tests exercise
 // exactly the kernel's decision).  Kept out of line: the sweep's hot loop then
 // carries only its (j, k) state in registers.
-__device__ __noinline__ int eval_tuple3(const FitArgs& a, int64_t i, int64_t j, int64_t k, double* lb_out) {
+// *ub_out (optional) is the matching upper bound ssr_gram + A + B/d on the reference's SSR.
+__device__ __noinline__ int eval_tuple3(const FitArgs& a, int64_t i, int64_t j, int64_t k, double* lb_out,
+                                        double* ub_out = nullptr) {
     const int64_t m = a.m, mp = a.mp;
-    double lb = 0.0;
+    double lb = 0.0, ub = 0.0;
     bool cond = true, rank_ok = true;
     for (int t = 0; t < a.T; ++t) {
         const double* Gt = a.G + (int64_t)t * mp * mp;
@@ -103,39 +113,60 @@ __device__ __noinline__ int eval_tuple3(const FitArgs& a, int64_t i, int64_t j, 
         const double tr = trh + (1.0 + trh) / d;
         if (!(d > 0.0) || !(vk * (1.0 + 3.0 * tr) <= FO_LIM) || !(At + Bt / d <= LOOSE * Y2)) cond = false;
         lb += base - At - fma(w, w, Bt) / d;
+        ub += base + At - fma(w, w, -Bt) / d;
         const int64_t f[3] = {i, j, k};
         if (!rank_certain<3>(a, t, f, tr)) rank_ok = false;
     }
     *lb_out = lb;
+    if (ub_out) *ub_out = ub;
     return (cond ? 1 : 0) | (rank_ok ? 2 : 0);
 }
 
 template <int NT>
 __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_constant__ FitArgs a) {
     using C = Cfg<NT>;
-    constexpr int P = C::P, IB = C::IB, TS = C::TS, BS = C::BS, KSPAN = C::KSPAN;
+    constexpr int P = C::P, IB = C::IB, TS = C::TS, BS = C::BS, KSPAN = C::KSPAN, R = C::R, KS = C::KS;
     extern __shared__ __align__(128) double sm[];
     __shared__ int s_unit;
+    __shared__ int s_tord[NT];
     __shared__ unsigned char s_force[2][IB];  // iforce flags of the staged rows
     __shared__ __align__(8) unsigned long long s_bar[2];  // TMA completion, one per tile buffer
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t m = a.m, mp = a.mp;
     if (tid == 0) {
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
         mbar_fence_init();
+        // sweep order of the tasks: largest |y_c|^2 first, so that the first task's share of the
+        // bound alone already exceeds the threshold for almost every row (task pruning below)
+        double y2[NT];
+        for (int t = 0; t < NT; ++t) {
+            y2[t] = a.G[(int64_t)t * mp * mp + m * mp + m];
+            s_tord[t] = t;
+        }
+        for (int x = 1; x < NT; ++x)
+            for (int z = x; z > 0 && y2[s_tord[z]] > y2[s_tord[z - 1]]; --z) {
+                const int q = s_tord[z];
+                s_tord[z] = s_tord[z - 1];
+                s_tord[z - 1] = q;
+            }
     }
     __syncthreads();
+    const int* tord = s_tord;  // read where the hoist / tile loads need it (rare)
     unsigned parity[2] = {0u, 0u};
-    double* sKraw = sm + 2 * BS + 2 * NW * CAP + tid * P;  // per-thread, slow path / threshold updates only
-    const int64_t m = a.m, mp = a.mp;
+    // per-thread constants, touched by the hoist, threshold updates and pruned rows:
+    // sK[0][p] = sum_t (base_t - A_t) (NT >= 3: sK[t][p] = (base_t - A_t) * shrink, t >= 1)
+    // (slot-major, thread-minor: conflict-free per-thread accesses)
+    double* sKb = sm + 2 * BS + 2 * NW * CAP + tid;
+    auto sK = [&](int idx) -> double& { return sKb[idx * 256]; };
     const double shrink = (NT == 1) ? 1.0 : (1.0 - 2.0 * kRcpRel);
     WarpCands wc{sm + 2 * BS + warp * CAP, reinterpret_cast<int64_t*>(sm + 2 * BS + NW * CAP) + warp * CAP, 0,
-                 a.collect ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g)};
+                 a.collect ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g), 0};
     const int64_t* B2 = a.binom + 2 * (m + 1);
     const int64_t* B3 = a.binom + 3 * (m + 1);
 
-    // tiles per task, staged by TMA (one elected thread, completion on s_bar[buf]):
-    // C[i, j-block] (IB x 32), C[i, k-span] (IB x KSPAN), (c_i, pad) (IB x 2)
+    // tiles per task (slot t holds task tord[t]), staged by TMA (one elected thread,
+    // completion on s_bar[buf]): C[i, j-block] (IB x 32), C[i, k-span] (IB x KSPAN), (c_i, pad) (IB x 2)
     auto load_tiles = [&](int buf, int ib0, int j0, int k0) {
         if (tid < IB) s_force[buf][tid] = (ib0 + tid < m) ? a.iforce[ib0 + tid] : 0;
         if (tid == 0) {
@@ -144,7 +175,7 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
             mbar_expect_tx(&s_bar[buf], (unsigned)(BS * sizeof(double)));
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-                const int row = (int)(t * mp) + ib0;
+                const int row = (int)(tord[t] * mp) + ib0;
                 double* Tt = base + t * TS;
                 tma_load_2d(Tt, &a.tmJ, j0, row, &s_bar[buf]);
                 tma_load_2d(Tt + IB * 32, &a.tmK, k0, row, &s_bar[buf]);
@@ -169,16 +200,36 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
         const int kbase = k0 + warp * P;
         const int i_lo = U.z, i_hi = U.w;
         load_tiles(0, i_lo, j0, k0);
-        if (!a.collect) wc.theta = fmin(wc.theta, ord_dec(*(volatile unsigned long long*)a.theta_g));
+        if (!a.collect) {
+            // shared threshold: the global bound histogram and the other warps' lists
+            double th = fmin(hist_theta(a, lane), ord_dec(*(volatile unsigned long long*)a.theta_g));
+            if (th < wc.theta) {
+                wc.theta = th;
+                if (lane == 0) atomicMin(a.theta_g, ord_enc(th));
+            }
+        }
 
-        // ---------------- hoist: (j, k_p) state per task ----------------
+        // ---------------- hoist: (j, k_p) state per task (slot order) ----------------
         // L10 = C_jk, rd1 = 1/(1 - C_jk^2), s1 = rd1 (c_k - C_jk c_j); the bound's B_t/d term
         // uses Bm = max_t B_t per pair, so the sweep needs one extra register per pair only
         double L10[P][NT], rd1[P][NT], s1[P][NT], w0[NT], Kq[P], Bm[P];
+        double K1r[P];  // NT == 2: task slot 1's (base - A) * shrink in registers
         unsigned valid = 0, bad = 0, forced = 0;
-#pragma unroll
-        for (int t = 0; t < NT; ++t) w0[t] = a.G[(int64_t)t * mp * mp + m * mp + j];
         const int jj = j < m ? j : (int)m - 1;
+        // per-task scalars of this unit, loaded once (live during the hoist only)
+        double Y2v[NT], gamv[NT], etav[NT], ynv[NT], rjv[NT];
+        const double* Gs[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const int tk = tord[t];
+            Gs[t] = a.G + (int64_t)tk * mp * mp;
+            w0[t] = Gs[t][m * mp + j];
+            Y2v[t] = Gs[t][m * mp + m];
+            gamv[t] = ref_gamma(a.rowsd[tk], 3);
+            etav[t] = a.eta[tk];
+            ynv[t] = a.ynorm[tk];
+            rjv[t] = fmax(a.rho_cap[tk], a.rho[(int64_t)tk * m + jj]);
+        }
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             const int k = kbase + p;
@@ -187,8 +238,9 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
             bool isbad = false, isnan_ = false;
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-                const double* Gt = a.G + (int64_t)t * mp * mp;
-                const double Y2 = Gt[m * mp + m];
+                const int tk = tord[t];
+                const double* Gt = Gs[t];
+                const double Y2 = Y2v[t];
                 const double cjk = Gt[(int64_t)k * mp + j];
                 const double ck = Gt[m * mp + k];
                 const double d1 = fma(-cjk, cjk, 1.0);
@@ -198,28 +250,39 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
                 const double trh = 2.0 * r1;
                 double At, Bt, vk;
                 // rho of the hoisted pair (the sweep feature's rho is covered by rho_cap or s_force)
-                const double rh = fmax(a.rho_cap[t], fmax(a.rho[(int64_t)t * m + jj], a.rho[(int64_t)t * m + kk]));
-                task_bound(3, a.eta[t], ref_gamma(a.rowsd[t], 3), rh, Y2, a.ynorm[t], trh, At, Bt, vk);
+                const double rh = fmax(rjv[t], a.rho[(int64_t)tk * m + kk]);
+                task_bound(3, etav[t], gamv[t], rh, Y2, ynv[t], trh, At, Bt, vk);
                 L10[p][t] = cjk;
                 rd1[p][t] = r1;
                 s1[p][t] = v1 * r1;
                 kr += base - At;
+                if (t == 0) Kq[p] = base - At;  // slot 0's share (the sweep's first partial bound)
+                if constexpr (NT == 2) {
+                    if (t == 1) K1r[p] = (base - At) * shrink;
+                } else if constexpr (NT >= 3) {
+                    if (t >= 1) sK(t * P + p) = (base - At) * shrink;
+                }
                 bm = fmax(bm, Bt);
                 if (!(d1 > 0.0) || !(vk * (1.0 + 3.0 * trh) <= FO_LIM)) isbad = true;
                 if (cjk != cjk || ck != ck || w0[t] != w0[t]) isnan_ = true;
             }
-            sKraw[p] = kr;
+            sK(p) = kr;
             Bm[p] = bm;
             if (j < k && k < m && !isnan_) valid |= 1u << p;
             if (isbad) bad |= 1u << p;
         }
+        // Kq = (first slot's share - theta) * shrink for NT > 1 (the remaining slots are added as the
+        // rows survive), (total - theta) for NT == 1; forced = pairs whose whole bound is below theta
+        double K0[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) K0[p] = Kq[p];
         auto set_kq = [&]() {
             forced = bad;
 #pragma unroll
             for (int p = 0; p < P; ++p) {
-                const double x = sKraw[p] - wc.theta;
+                const double x = sK(p) - wc.theta;
                 if (!(x > 0.0)) forced |= 1u << p;
-                Kq[p] = x * shrink;
+                Kq[p] = (NT == 1) ? x : (K0[p] - wc.theta) * shrink;
             }
         };
         set_kq();
@@ -236,58 +299,98 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
             // pending slow-path tuples of this tile: bit (ii * P + p)
             constexpr int NPW = (IB * P + 31) / 32;  // pending-bit words
             constexpr int IPW = 32 / P;              // rows per word
+            static_assert(IPW % R == 0, "vote groups must not straddle pending words");
             unsigned pend[NPW];
+            // one task slot of one row: acc[p] -= (w^2 + Bm) / d  (NT == 1: acc = acc d - q)
+            // lb_t = base_t - A_t - (w^2 + B_t)/d >= base_t - A_t - (w^2 + Bm)/d
+            auto task_row = [&](double (&acc)[P], int t, int ii) {
+                const double* Tt = T0 + t * TS;
+                const double g0 = Tt[ii * 32 + lane];
+                const double ci = Tt[IB * (32 + KSPAN) + 2 * ii];
+                const double D = fma(-g0, g0, 1.0);
+                const double V = fma(-g0, w0[t], ci);
+                double gk[P];
+                if constexpr (P == 1) {
+                    gk[0] = Tt[IB * 32 + ii * KSPAN + warp];
+                } else {
+#pragma unroll
+                    for (int p = 0; p < P; p += 2) {
+                        const double2 v = *reinterpret_cast<const double2*>(Tt + IB * 32 + ii * KSPAN + warp * P + p);
+                        gk[p] = v.x;
+                        gk[p + 1] = v.y;
+                    }
+                }
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const double g1 = fma(-L10[p][t], g0, gk[p]);
+                    const double e1 = g1 * rd1[p][t];
+                    const double w = fma(-g1, s1[p][t], V);
+                    const double d = fma(-g1, e1, D);
+                    const double q = fma(w, w, Bm[p]);
+                    if (NT == 1)
+                        acc[p] = fma(acc[p], d, -q);  // (K - theta) d - q; d <= 0 also passes
+                    else
+                        acc[p] = fma(-q, fabs(rcp_sweep(d)), acc[p]);  // 1/|d|: d <= 0 drives acc down
+                }
+            };
 #pragma unroll
             for (int pw = 0; pw < NPW; ++pw) {
                 unsigned word = 0u;
 #pragma unroll(C::UNROLL)
-                for (int iw = 0; iw < IPW; ++iw) {
-                    const int ii = pw * IPW + iw;
-                    const int i = ib0 + ii;
-                    double acc[P];
+                for (int ig = 0; ig < IPW; ig += R) {
+                    double acc[R][P];
 #pragma unroll
-                    for (int p = 0; p < P; ++p) acc[p] = Kq[p];
+                    for (int r = 0; r < R; ++r) {
 #pragma unroll
-                    for (int t = 0; t < NT; ++t) {
-                        const double* Tt = T0 + t * TS;
-                        const double g0 = Tt[ii * 32 + lane];
-                        const double ci = Tt[IB * (32 + KSPAN) + 2 * ii];
-                        const double D = fma(-g0, g0, 1.0);
-                        const double V = fma(-g0, w0[t], ci);
-                        double gk[P];
-                        if constexpr (P == 1) {
-                            gk[0] = Tt[IB * 32 + ii * KSPAN + warp];
-                        } else {
+                        for (int p = 0; p < P; ++p) acc[r][p] = Kq[p];
+                        task_row(acc[r], 0, pw * IPW + ig + r);
+                    }
+                    // Task pruning: every task's reference SSR is >= 0, so the slots swept so far
+                    // already bound the pooled SSR from below.  Once no (row, lane, pair) of the
+                    // group is below theta on them, the group is done (warp-uniform exit).
+                    bool live = true;
 #pragma unroll
-                            for (int p = 0; p < P; p += 2) {
-                                const double2 v =
-                                    *reinterpret_cast<const double2*>(Tt + IB * 32 + ii * KSPAN + warp * P + p);
-                                gk[p] = v.x;
-                                gk[p + 1] = v.y;
-                            }
+                    for (int t = 1; t < NT; ++t) {
+                        // sign bits OR-ed as integers (acc < 0 or -0: still alive; cheaper than
+                        // predicate chains, which the compiler turns into an fmin reduction)
+                        unsigned sgn = 0u;
+#pragma unroll
+                        for (int r = 0; r < R; ++r)
+#pragma unroll
+                            for (int p = 0; p < P; ++p) sgn |= (unsigned)__double2hiint(acc[r][p]);
+                        if (!__any_sync(L0S_FULL, (int)sgn < 0)) {
+                            live = false;
+                            break;
                         }
+                        double kt[P];
 #pragma unroll
                         for (int p = 0; p < P; ++p) {
-                            // lb_t = base_t - A_t - (w^2 + B_t)/d >= base_t - A_t - (w^2 + Bm)/d
-                            const double g1 = fma(-L10[p][t], g0, gk[p]);
-                            const double e1 = g1 * rd1[p][t];
-                            const double w = fma(-g1, s1[p][t], V);
-                            const double d = fma(-g1, e1, D);
-                            const double q = fma(w, w, Bm[p]);
-                            if (NT == 1)
-                                acc[p] = fma(acc[p], d, -q);  // (K - theta) d - q; d <= 0 also passes
+                            if constexpr (NT == 2)
+                                kt[p] = K1r[p];
                             else
-                                acc[p] = fma(-q, fabs(rcp_sweep(d)), acc[p]);  // 1/|d|: d <= 0 drives acc down
+                                kt[p] = sK(t * P + p);
+                        }
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+#pragma unroll
+                            for (int p = 0; p < P; ++p) acc[r][p] += kt[p];
+                            task_row(acc[r], t, pw * IPW + ig + r);
                         }
                     }
-                    unsigned pass = forced;
 #pragma unroll
-                    for (int p = 0; p < P; ++p)
-                        if (acc[p] < 0.0) pass |= 1u << p;
-                    if (s_force[buf][ii]) pass |= (1u << P) - 1;  // rho_i above rho_cap: needs the actual rho
-                    pass &= valid;
-                    if (!(i < j && i < i_hi)) pass = 0;
-                    word |= pass << (iw * P);
+                    for (int r = 0; r < R; ++r) {
+                        const int ii = pw * IPW + ig + r;
+                        const int i = ib0 + ii;
+                        unsigned pass = forced;
+                        if (live) {
+#pragma unroll
+                            for (int p = 0; p < P; ++p) pass |= ((unsigned)__double2hiint(acc[r][p]) >> 31) << p;
+                        }
+                        if (s_force[buf][ii]) pass |= (1u << P) - 1;  // rho_i above rho_cap: needs the actual rho
+                        pass &= valid;
+                        if (!(i < j && i < i_hi)) pass = 0;
+                        word |= pass << ((ig + r) * P);
+                    }
                 }
                 pend[pw] = word;
             }
@@ -320,6 +423,18 @@ __global__ void k_screen3(const __grid_constant__ FitArgs a, const int64_t* __re
     out_lb[c] = lb;
 }
 
+__global__ void __launch_bounds__(256, 1) k_seed3(const __grid_constant__ FitArgs a) {
+    __shared__ SeedSmem S;
+    const int ns = seed_subsets<3, 16>(a, S);
+    for (int c = threadIdx.x; c < ns; c += blockDim.x) {
+        int64_t f[3];
+        double lb = 0.0, ub = INFINITY;
+        const int fl = seed_tuple<3>(a, S, c, f) ? eval_tuple3(a, f[0], f[1], f[2], &lb, &ub) : 0;
+        S.ub[c] = (fl == 3 && ub == ub) ? ub : INFINITY;
+    }
+    seed_commit(a, S, ns);
+}
+
 template <int NT>
 int launch_nt(const FitArgs& a0, int nsm, cudaStream_t st) {
     using C = Cfg<NT>;
@@ -333,6 +448,7 @@ int launch_nt(const FitArgs& a0, int nsm, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, 256, C::smem_bytes);
     if (per_sm < 1) per_sm = 1;
     int grid = nsm * per_sm;
+    if (!a.collect) k_seed3<<<1, 256, 0, st>>>(a);
     k_fit3<NT><<<grid, 256, C::smem_bytes, st>>>(a);
     return grid;
 }
@@ -389,7 +505,12 @@ int fit3_launch(const FitArgs& a, int nsm, cudaStream_t st) {
 std::vector<int4> fit3_units(int64_t m, int T, int64_t N_total, const std::vector<int64_t>& c2_prefix,
                              int64_t rank_lo, int64_t rank_hi) {
     const int kspan = fit3_kspan(T);
-    const int ich = 256;  // i rows per unit: amortizes the (j, k) hoist
+    // i rows per unit: amortizes the (j, k) hoist; L0S_ICH overrides (tuning)
+    static const int ich = [] {
+        const char* e = getenv("L0S_ICH");
+        const int v = e ? atoi(e) : 0;
+        return v > 0 ? v : 4096;
+    }();
     std::vector<int4> units;
     int nJ = (int)((m + 31) / 32);
     int nK = (int)((m + kspan - 1) / kspan);

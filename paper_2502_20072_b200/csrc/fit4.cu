@@ -62,9 +62,9 @@ __device__ __forceinline__ Hoist3 hoist3(const double* Gt, int64_t mp, int64_t m
 
 // Exact lower bound + certificates of one 4-tuple (i < j < k < l); see eval_tuple3.
 __device__ __noinline__ int eval_tuple4(const FitArgs& a, int64_t i, int64_t j, int64_t k, int64_t l,
-                                        double* lb_out) {
+                                        double* lb_out, double* ub_out = nullptr) {
     const int64_t m = a.m, mp = a.mp;
-    double lb = 0.0;
+    double lb = 0.0, ub = 0.0;
     bool cond = true, rank_ok = true;
     for (int t = 0; t < a.T; ++t) {
         const double* Gt = a.G + (int64_t)t * mp * mp;
@@ -89,10 +89,12 @@ __device__ __noinline__ int eval_tuple4(const FitArgs& a, int64_t i, int64_t j, 
         const double tr = h.tr3 + (1.0 + h.tr3) / d;
         if (!(d > 0.0) || !(vk * (1.0 + 4.0 * tr) <= FO_LIM) || !(At + Bt / d <= LOOSE * Y2)) cond = false;
         lb += h.base - At - fma(w, w, Bt) / d;
+        ub += h.base + At - fma(w, w, -Bt) / d;
         const int64_t f[4] = {i, j, k, l};
         if (!rank_certain<4>(a, t, f, tr)) rank_ok = false;
     }
     *lb_out = lb;
+    if (ub_out) *ub_out = ub;
     return (cond ? 1 : 0) | (rank_ok ? 2 : 0);
 }
 
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs
     const int64_t m = a.m, mp = a.mp;
     const double shrink = (NT == 1) ? 1.0 : (1.0 - 2.0 * kRcpRel);
     WarpCands wc{sm + 2 * BS + warp * CAP, reinterpret_cast<int64_t*>(sm + 2 * BS + NW * CAP) + warp * CAP, 0,
-                 a.collect ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g)};
+                 a.collect ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g), 0};
     const int64_t* B2 = a.binom + 2 * (m + 1);
     const int64_t* B3 = a.binom + 3 * (m + 1);
     const int64_t* B4 = a.binom + 4 * (m + 1);
@@ -147,7 +149,14 @@ __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs
         const int lbase = l0 + warp * P;
         const int i_lo = U.z, i_hi = U.w;
         load_tiles(0, i_lo, j0, k, l0);
-        if (!a.collect) wc.theta = fmin(wc.theta, ord_dec(*(volatile unsigned long long*)a.theta_g));
+        if (!a.collect) {
+            // shared threshold: the global bound histogram and the other warps' lists
+            double th = fmin(hist_theta(a, lane), ord_dec(*(volatile unsigned long long*)a.theta_g));
+            if (th < wc.theta) {
+                wc.theta = th;
+                if (lane == 0) atomicMin(a.theta_g, ord_enc(th));
+            }
+        }
 
         // ---------------- hoist ----------------
         double L10[NT], rd1[NT], s1[NT], w0[NT];
@@ -303,9 +312,22 @@ int occupancy4(int nsm) {
     return nsm * (per_sm < 1 ? 1 : per_sm);
 }
 
+__global__ void __launch_bounds__(256, 1) k_seed4(const __grid_constant__ FitArgs a) {
+    __shared__ SeedSmem S;
+    const int ns = seed_subsets<4, 12>(a, S);
+    for (int c = threadIdx.x; c < ns; c += blockDim.x) {
+        int64_t f[4];
+        double lb = 0.0, ub = INFINITY;
+        const int fl = seed_tuple<4>(a, S, c, f) ? eval_tuple4(a, f[0], f[1], f[2], f[3], &lb, &ub) : 0;
+        S.ub[c] = (fl == 3 && ub == ub) ? ub : INFINITY;
+    }
+    seed_commit(a, S, ns);
+}
+
 template <int NT>
 int launch4(const FitArgs& a, int nsm, cudaStream_t st) {
     const int grid = occupancy4<NT>(nsm);
+    if (!a.collect) k_seed4<<<1, 256, 0, st>>>(a);
     k_fit4<NT><<<grid, 256, Cfg4<NT>::smem_bytes, st>>>(a);
     return grid;
 }

@@ -121,7 +121,68 @@ struct WarpCands {
     int64_t* rk;
     int cnt;
     double theta;
+    int counted;  // entries [0, counted) are already in the global histogram
 };
+
+// ---- global lower-bound histogram (the shared threshold) ----
+// A warp sees ~1/1000 of the tuples, so its own K'-th bound is far looser than the global
+// K'-th.  Every tuple a warp keeps (lb below its threshold) is counted once in a global
+// histogram of lb (HIST_SUB sub-bins per binary exponent, HIST_EXP exponents below the
+// total |y|^2); the upper edge of the first bin at which the cumulative count reaches K' is
+// a valid shared threshold: at least K' distinct tuples have smaller bounds, and every tuple
+// below it was kept somewhere (all thresholds stay above it).
+
+// bin of a bound (-1: above the histogram's range, not counted -- undercounting is safe)
+__device__ __forceinline__ int hist_bin(double lb, int base) {
+    if (!(lb > 0.0)) return 0;
+    const int b = (int)((unsigned long long)__double_as_longlong(lb) >> (52 - HIST_SUB_BITS)) - base;
+    return b < 0 ? 0 : (b >= HIST_BINS ? -1 : b);
+}
+__device__ __forceinline__ double hist_upper(int b, int base) {
+    return __longlong_as_double((long long)((unsigned long long)(base + b + 1) << (52 - HIST_SUB_BITS)));
+}
+
+// Count the warp's entries [counted, cnt) (one aggregated atomic per distinct bin per round).
+__device__ __forceinline__ void hist_count(const FitArgs& a, WarpCands& wc, int lane) {
+    for (int x0 = wc.counted; x0 < wc.cnt; x0 += 32) {
+        const int x = x0 + lane;
+        const bool on = x < wc.cnt;
+        int b = on ? hist_bin(wc.lb[x], a.hist_base) : -1;
+        if (b < 0) b = -1 - lane;  // not counted: a key no other lane shares
+        const unsigned peers = __match_any_sync(L0S_FULL, b);
+        if (b >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(a.hist + b, (unsigned)__popc(peers));
+    }
+    wc.counted = wc.cnt;
+}
+
+// Smallest histogram edge with >= kc counted bounds below it (+inf when fewer).
+__device__ __forceinline__ double hist_theta(const FitArgs& a, int lane) {
+    constexpr int PER = HIST_BINS / 32;
+    const unsigned* h = a.hist + lane * PER;
+    unsigned sum = 0;
+    for (int x = 0; x < PER; ++x) sum += __ldcg(h + x);
+    unsigned inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(L0S_FULL, inc, o);
+        if (lane >= o) inc += v;
+    }
+    const unsigned hit = __ballot_sync(L0S_FULL, inc >= (unsigned)a.kc);
+    if (!hit) return INFINITY;
+    const int L = __ffs(hit) - 1;
+    double th = INFINITY;
+    if (lane == L) {
+        unsigned c = inc - sum;
+        for (int x = 0; x < PER; ++x) {
+            c += __ldcg(h + x);
+            if (c >= (unsigned)a.kc) {
+                th = hist_upper(lane * PER + x, a.hist_base);
+                break;
+            }
+        }
+    }
+    return __shfl_sync(L0S_FULL, th, L);
+}
 
 // Deferred slow path: drain the pending bits (one tuple per lane per round).
 //   eval(b, &lb, &rank) -> 0 drop, 1 insert (lb < theta checked here), 2 exact kernel
@@ -154,6 +215,15 @@ __device__ __forceinline__ void drain_pending(const FitArgs& a, unsigned (&pend)
                 wc.rk[pos] = rkv;
             }
             wc.cnt += __popc(im);
+            if (!a.collect) {
+                // count the new entries in the global histogram right away (the shared
+                // threshold must not wait for this warp's buffer to fill)
+                int hb = (kind == 1) ? hist_bin(lbv, a.hist_base) : -1;
+                if (hb < 0) hb = -1 - lane;
+                const unsigned peers = __match_any_sync(L0S_FULL, hb);
+                if (hb >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(a.hist + hb, (unsigned)__popc(peers));
+                wc.counted = wc.cnt;
+            }
         }
         const unsigned il = __ballot_sync(L0S_FULL, kind == 2);
         if (il) {
@@ -180,15 +250,138 @@ __device__ __forceinline__ void drain_pending(const FitArgs& a, unsigned (&pend)
                 wc.cnt = 0;
                 __syncwarp();
             } else {
+                hist_count(a, wc, lane);
                 warp_sort(wc.lb, wc.rk, wc.cnt, lane);
                 if (wc.cnt > a.kc) wc.cnt = a.kc;
-                if (wc.cnt == a.kc && wc.lb[a.kc - 1] < wc.theta) {
-                    wc.theta = wc.lb[a.kc - 1];
+                wc.counted = wc.cnt;
+                double th = hist_theta(a, lane);
+                if (wc.cnt == a.kc) th = fmin(th, wc.lb[a.kc - 1]);
+                th = fmin(th, ord_dec(*(volatile unsigned long long*)a.theta_g));
+                if (th < wc.theta) {
+                    wc.theta = th;
                     if (lane == 0) atomicMin(a.theta_g, ord_enc(wc.theta));
                     on_theta();
                 }
                 __syncwarp();
             }
+        }
+    }
+}
+
+// Seed of the shared threshold (one CTA of 256 threads, launched before the sweep): the F
+// features with the largest pooled single-feature explained variance sum_t c_f^2, and every
+// N-subset of them inside the rank range is evaluated with the Gram bound pair (lb, ub).  The
+// kc-th smallest upper bound among the certified subsets is >= the kc-th smallest lower bound
+// over all tuples, so it is a valid starting threshold: the sweep's first tiles then drop the
+// hopeless tuples instead of sending every one of them through the slow path.
+constexpr int SEED_MAX = 1024;
+struct SeedSmem {
+    double ub[SEED_MAX];
+    short sub[SEED_MAX][4];
+    int top[16];
+    double rv[8];
+    int ri[8];
+    int nsub;
+};
+
+// Phase 1: top-F features and their N-subsets (ascending feature order); returns the count
+// (0 when fewer than F live features or fewer than kc subsets).
+template <int N, int F>
+__device__ int seed_subsets(const FitArgs& a, SeedSmem& S) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t m = a.m, mp = a.mp;
+    if (m < F) return 0;
+    for (int r = 0; r < F; ++r) {
+        double best = -1.0;
+        int bi = -1;
+        for (int f = tid; f < m; f += blockDim.x) {
+            bool taken = false;
+            for (int q = 0; q < r; ++q) taken |= S.top[q] == f;
+            if (taken) continue;
+            double sc = 0.0;
+            for (int t = 0; t < a.T; ++t) {
+                const double c = a.G[(int64_t)t * mp * mp + m * mp + f];
+                sc = fma(c, c, sc);
+            }
+            if (sc > best) {  // NaN (dead feature) never wins
+                best = sc;
+                bi = f;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_down_sync(L0S_FULL, best, o);
+            const int oi = __shfl_down_sync(L0S_FULL, bi, o);
+            if (ov > best) {
+                best = ov;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            S.rv[warp] = best;
+            S.ri[warp] = bi;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+                if (S.rv[w] > S.rv[0]) {
+                    S.rv[0] = S.rv[w];
+                    S.ri[0] = S.ri[w];
+                }
+            S.top[r] = S.ri[0];
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        bool ok = true;
+        for (int r = 0; r < F; ++r) ok &= S.top[r] >= 0;  // fewer than F live features: no seed
+        for (int x = 1; ok && x < F; ++x)
+            for (int z = x; z > 0 && S.top[z] < S.top[z - 1]; --z) {
+                const int q = S.top[z];
+                S.top[z] = S.top[z - 1];
+                S.top[z - 1] = q;
+            }
+        int c[N], cnt = 0;
+        for (int x = 0; x < N; ++x) c[x] = x;
+        while (ok && cnt < SEED_MAX) {
+            for (int x = 0; x < N; ++x) S.sub[cnt][x] = (short)c[x];
+            ++cnt;
+            int x = N - 1;
+            while (x >= 0 && c[x] == F - N + x) --x;
+            if (x < 0) break;
+            ++c[x];
+            for (int z = x + 1; z < N; ++z) c[z] = c[z - 1] + 1;
+        }
+        S.nsub = cnt >= a.kc ? cnt : 0;
+    }
+    __syncthreads();
+    return S.nsub;
+}
+
+// Subset c's features and whether its rank lies in the searched range.
+template <int N>
+__device__ __forceinline__ bool seed_tuple(const FitArgs& a, const SeedSmem& S, int c, int64_t (&f)[N]) {
+    const int64_t m = a.m;
+    int64_t rk = a.N_total - 1;
+    for (int x = 0; x < N; ++x) {
+        f[x] = S.top[S.sub[c][x]];
+        rk -= a.binom[(int64_t)(N - x) * (m + 1) + (m - 1 - f[x])];
+    }
+    return !a.ranged || (rk >= a.rank_lo && rk < a.rank_hi);
+}
+
+// Phase 3: the kc-th smallest upper bound becomes the starting threshold.
+__device__ __forceinline__ void seed_commit(const FitArgs& a, SeedSmem& S, int ns) {
+    __syncthreads();
+    for (int c = threadIdx.x; c < ns; c += blockDim.x) {
+        const double v = S.ub[c];
+        int pos = 0;
+        for (int x = 0; x < ns; ++x) {
+            const double u = S.ub[x];
+            pos += (u < v || (u == v && x < c)) ? 1 : 0;
+        }
+        if (pos == a.kc - 1 && v < INFINITY) {
+            const double th = v + fabs(v) * 1e-9 + 1e-300;  // strictly above kc certified bounds
+            atomicMin(a.theta_g, ord_enc(th));
         }
     }
 }

@@ -77,6 +77,17 @@ struct QrArgs {
 void launch_qr_screen(const QrArgs& a, int64_t count, cudaStream_t st, int64_t* launches);
 
 // ---- screened fit (fit3.cu) ----
+// global lower-bound histogram behind the shared threshold (fitcommon.cuh): HIST_SUB sub-bins
+// per binary exponent, HIST_EXP exponents below the top (the total |y|^2)
+constexpr int HIST_SUB_BITS = 5;
+constexpr int HIST_EXP = 44;
+constexpr int HIST_BINS = HIST_EXP << HIST_SUB_BITS;
+inline int hist_base_for(double top) {
+    unsigned long long u;
+    __builtin_memcpy(&u, &top, 8);
+    const int e = (int)((u >> 52) & 0x7ff);
+    return (e + 1 - HIST_EXP) << HIST_SUB_BITS;
+}
 // TMA descriptors for the Gram viewed as a 2-D (T*mp rows x mp columns) f64 tensor;
 // one per box shape the kernel stages (built by the launcher, which knows the tile shape).
 struct alignas(64) TmaDesc {
@@ -111,6 +122,8 @@ struct FitArgs {
     int collect;             // 1 = collect every lb < theta0 into coll_*
     double theta0;
     unsigned long long* theta_g;
+    unsigned* hist;          // [HIST_BINS] global lower-bound histogram (fitcommon.cuh)
+    int hist_base;           // bin offset: (biased exponent of the top) - HIST_EXP, times HIST_SUB
     double* wl_lb;           // [n_warp_slots][kc]
     int64_t* wl_rank;
     int* wl_cnt;             // [n_warp_slots]

@@ -5,8 +5,8 @@ for what in "$@"; do
 case $what in
 tests)
   timeout 300 python __graft_entry__.py > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke.log
-  timeout 1200 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?"
-  grep -E "passed|failed|Error|FAILED" gpurun_out/gpu_tests.log | tail -15 ;;
+  timeout 1200 python -m pytest tests -m gpu -q --timeout 900 --durations=8 > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?"
+  grep -E "passed|failed|Error|FAILED|s call|s setup" gpurun_out/gpu_tests.log | tail -15 ;;
 bench)
   timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -3 gpurun_out/bench.log ;;
 ncu)
