@@ -33,6 +33,45 @@ __host__ __device__ inline double ord_dec(unsigned long long u) {
 }
 
 #ifdef __CUDACC__
+// Lexicographic unranking (search.unrank_tuple, search.py:66-85) on the device's binomial
+// table (C(a, k) at binom[k * (m + 1) + a]).  Position k takes the largest e with
+// sum_{e0 <= e' < e} C(m-1-e', rem) <= r; by the hockey-stick identity that sum is
+// C(m-e0, rem+1) - C(m-e, rem+1), so e is found by binary search: O(n log m) dependent
+// loads instead of a scan over e.  (A saturated table entry falls back to the scan.)
+__device__ __forceinline__ void unrank_lex(int64_t rank, int64_t m, int n, const int64_t* __restrict__ binom,
+                                          int64_t* out) {
+    int64_t r = rank, e0 = 0;
+    for (int k = 0; k < n; ++k) {
+        const int rem = n - k - 1;
+        const int64_t* B = binom + (int64_t)(rem + 1) * (m + 1);
+        const int64_t top = B[m - e0];
+        int64_t e;
+        if (top == INT64_MAX) {
+            e = e0;
+            for (;;) {
+                const int64_t c = binom[(int64_t)rem * (m + 1) + (m - 1 - e)];
+                if (r < c) break;
+                r -= c;
+                ++e;
+            }
+        } else {
+            const int64_t target = top - r;
+            int64_t lo = e0, hi = m - 1 - rem;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (B[m - mid] >= target)
+                    lo = mid;
+                else
+                    hi = mid - 1;
+            }
+            e = lo;
+            r -= top - B[m - e];
+        }
+        out[k] = e;
+        e0 = e + 1;
+    }
+}
+
 // 1/|d| from the MUFU.RCP64H unit: one integer LOP (sign clear, low word
 // dropped) and one MUFU op, no FP64-pipe instruction.  Relative error is
 // bounded by kRcpRel (measured exhaustively over mantissas by

@@ -24,20 +24,6 @@ namespace l0s {
 
 namespace {
 
-__device__ void unrank_dev(int64_t rank, int64_t m, int n, const int64_t* binom, int64_t* out) {
-    int64_t r = rank, e = 0;
-    for (int k = 0; k < n; ++k) {
-        int rem = n - k - 1;
-        for (;;) {
-            int64_t c = binom[(int64_t)rem * (m + 1) + (m - 1 - e)];
-            if (r < c) break;
-            r -= c;
-            ++e;
-        }
-        out[k] = e;
-        ++e;
-    }
-}
 
 constexpr int kMaxN = 15;
 
@@ -173,7 +159,7 @@ __global__ void k_exact(ExactArgs a, int64_t g0, int64_t nthr, double* __restric
     if (a.tuples)
         for (int k = 0; k < n; ++k) tup[k] = a.tuples[tup_i * n + k];
     else
-        unrank_dev(a.ranks[tup_i], a.m, n, a.binom, tup);
+        unrank_lex(a.ranks[tup_i], a.m, n, a.binom, tup);
     int64_t lo = a.bounds[task], rows = a.bounds[task + 1] - lo;
     Scr I{a.ld, nthr, gl};
     W* S = (W*)a.scratch;
@@ -234,23 +220,49 @@ struct Ops<float> {
     static __device__ __forceinline__ float store(double x) { return __double2float_rn(x); }
 };
 
-// sequential sum_{i=from}^{to-1} fl(x_i*y_i) in index order; loads batched ahead of the adds
+// sequential sum_{i=from}^{to-1} fl(x_i*y_i) in index order.  The loads of the next batch
+// are issued before the current batch's adds, so the chain runs at DADD latency.
 template <typename W>
 __device__ __forceinline__ double seq_dot(const W* __restrict__ x, const W* __restrict__ y, int from, int to) {
     double acc = 0.0;
     int i = from;
-    for (; i + 8 <= to; i += 8) {
+    if (i + 8 <= to) {
         W px[8], py[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             px[u] = x[i + u];
             py[u] = y[i + u];
         }
+        for (; i + 16 <= to; i += 8) {
+            W nx[8], ny[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                nx[u] = x[i + 8 + u];
+                ny[u] = y[i + 8 + u];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = Ops<W>::term(acc, px[u], py[u]);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                px[u] = nx[u];
+                py[u] = ny[u];
+            }
+        }
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc = Ops<W>::term(acc, px[u], py[u]);
+        i += 8;
     }
     for (; i < to; ++i) acc = Ops<W>::term(acc, x[i], y[i]);
     return acc;
+}
+
+template <typename W>
+__device__ __forceinline__ void cp_async_w(W* dst, const W* src) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    if constexpr (sizeof(W) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src));
 }
 
 template <typename W>
@@ -271,7 +283,7 @@ __global__ void __launch_bounds__(128) k_exact_smem(ExactArgs a, int64_t g0, dou
         if (a.tuples)
             for (int k = 0; k < n; ++k) s_tup[k] = a.tuples[tup_i * n + k];
         else
-            unrank_dev(a.ranks[tup_i], a.m, n, a.binom, s_tup);
+            unrank_lex(a.ranks[tup_i], a.m, n, a.binom, s_tup);
     }
     __syncthreads();
     const int64_t lo = a.bounds[task];
@@ -279,21 +291,27 @@ __global__ void __launch_bounds__(128) k_exact_smem(ExactArgs a, int64_t g0, dou
     const int ld = rows;
     const W* X = (const W*)a.Xp;
     const W* Y = (const W*)a.yp;
+    // the system [f_1 .. f_n | 1 | y] (lsq.py:141-147), every element in flight at once
     for (int k = 0; k < n; ++k) {
         const W* src = X + s_tup[k] * a.s + lo;
-        for (int i = tid; i < rows; i += blockDim.x) S[k * ld + i] = src[i];
+        for (int i = tid; i < rows; i += blockDim.x) cp_async_w<W>(S + k * ld + i, src + i);
     }
     for (int i = tid; i < rows; i += blockDim.x) {
         S[n * ld + i] = (W)1.0;
-        S[p * ld + i] = Y[lo + i];
+        cp_async_w<W>(S + p * ld + i, Y + lo + i);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     double maxdiag = 0.0;  // meaningful in thread 0
-    bool ok = true;
+    double nrm2 = 0.0;     // thread 0: norm^2 of the next column, when produced by the fused pass
+    double ssr = 0.0;      // thread 0: the fused final sum of squares
+    bool have = false, ok = true;
     for (int j = 0; j < p; ++j) {
         W* cj = S + j * ld;
         if (tid == 0) {
-            double nrm2 = seq_dot<W>(cj, cj, j, rows);
+            if (!have) nrm2 = seq_dot<W>(cj, cj, j, rows);
+            have = false;
             double nrm = __dsqrt_rn(nrm2);
             if (nrm == 0.0) {
                 ok = false;
@@ -321,10 +339,28 @@ __global__ void __launch_bounds__(128) k_exact_smem(ExactArgs a, int64_t g0, dou
             s_fac[c] = __ddiv_rn(__dmul_rn(2.0, w), s_vtv);
         }
         __syncthreads();
-        for (int c = j + 1; c <= p; ++c) {
-            const double fac = s_fac[c];
-            W* cc = S + c * ld;
-            for (int i = j + tid; i < rows; i += blockDim.x) cc[i] = Ops<W>::upd(cc[i], fac, cj[i]);
+        {
+            // column j+1 first, on every thread; then its sequential sum of squares (the next
+            // norm, or the ssr when j+1 == p) on thread 0 while the other warps update the rest
+            W* c1 = S + (j + 1) * ld;
+            const double fac = s_fac[j + 1];
+            for (int i = j + tid; i < rows; i += blockDim.x) c1[i] = Ops<W>::upd(c1[i], fac, cj[i]);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            W* c1 = S + (j + 1) * ld;
+            if (j + 1 < p) {
+                nrm2 = seq_dot<W>(c1, c1, j + 1, rows);
+                have = true;
+            } else {
+                ssr = seq_dot<W>(c1, c1, p, rows);
+            }
+        } else if (tid >= 32) {
+            for (int c = j + 2; c <= p; ++c) {
+                const double fac = s_fac[c];
+                W* cc = S + c * ld;
+                for (int i = j + tid - 32; i < rows; i += blockDim.x - 32) cc[i] = Ops<W>::upd(cc[i], fac, cj[i]);
+            }
         }
         __syncthreads();
         if (tid == 0) {
@@ -339,7 +375,6 @@ __global__ void __launch_bounds__(128) k_exact_smem(ExactArgs a, int64_t g0, dou
         for (int j = 0; j < p; ++j)
             if (fabs(Ops<W>::widen(S[j * ld + j])) < lim) ok = false;
     }
-    double ssr = 0.0;
     if (ok) {
         W coef[kMaxN + 1];
         for (int j = p - 1; j >= 0; --j) {
@@ -355,9 +390,10 @@ __global__ void __launch_bounds__(128) k_exact_smem(ExactArgs a, int64_t g0, dou
             else
                 coef[j] = __fdiv_rn(acc, S[j * ld + j]);
         }
-        ssr = seq_dot<W>(S + p * ld, S + p * ld, p, rows);
         if (a.coef)
             for (int k = 0; k < p; ++k) a.coef[(tup_i * a.T + task) * p + k] = (double)coef[k];
+    } else {
+        ssr = 0.0;
     }
     ssr_tmp[g] = ssr;
     ok_tmp[g] = ok ? 1 : 0;

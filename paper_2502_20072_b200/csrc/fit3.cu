@@ -49,7 +49,7 @@ namespace {
 #define L0S_C34_UNROLL 1
 #endif
 #ifndef L0S_PRUNE_ROWS
-#define L0S_PRUNE_ROWS 2
+#define L0S_PRUNE_ROWS 4
 #endif
 struct CfgT {
     int P, IB, MINB, UNROLL;

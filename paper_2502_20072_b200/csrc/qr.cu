@@ -18,19 +18,6 @@
 namespace l0s {
 namespace {
 
-__device__ void unrank_q(int64_t rank, int64_t m, int n, const int64_t* binom, int64_t* out) {
-    int64_t r = rank, e = 0;
-    for (int k = 0; k < n; ++k) {
-        const int rem = n - k - 1;
-        for (;;) {
-            const int64_t c = binom[(int64_t)rem * (m + 1) + (m - 1 - e)];
-            if (r < c) break;
-            r -= c;
-            ++e;
-        }
-        out[k] = e++;
-    }
-}
 
 // packed upper triangle: row j starts at off(j) = j*NC - j*(j-1)/2
 template <int NC>
@@ -114,7 +101,7 @@ __global__ void __launch_bounds__(256) k_qr_warp(QrArgs a) {
     const int task = (int)(g % a.T);
     const int n = NC - 2, p = NC - 1;
     int64_t tup[NC - 2];
-    unrank_q(a.ranks[tup_i], a.m, n, a.binom, tup);
+    unrank_lex(a.ranks[tup_i], a.m, n, a.binom, tup);
     const int64_t lo = a.bounds[task];
     const int rows = (int)(a.bounds[task + 1] - lo);
     const double* X = a.Xp;
