@@ -206,8 +206,11 @@ def main():
     pd = torch.from_numpy(perm).to(f"cuda:{local}")
     torch.cuda.synchronize()
 
+    from paper_2502_20072_b200.dist import sharded_stage
+
     def device_step():
-        eng.stage((M, S), None, None, bounds, "fp64", device_ptrs=(vd.data_ptr(), yd.data_ptr(), pd.data_ptr()))
+        # N > 1: each rank computes 1/N of the Gram, NCCL all-gathers the shards (dist.sharded_stage)
+        sharded_stage(eng, (M, S), bounds, "fp64", (vd.data_ptr(), yd.data_ptr(), pd.data_ptr()))
         sc, rk, coef, ssr, st = eng.search(N_DIM, 10, lo, hi, "fast")
         return st, sc, rk
 
@@ -222,7 +225,8 @@ def main():
         device_step()
     barrier()
     ms_steps, fit_ms, launches = [], [], 0
-    stage_launches = 2 + 2 * T  # gather, normalize, (gram + unit_diag) per task
+    # gather, normalize, gram, unit_diag, 5 feature-flag kernels (+ the shard unpack for N > 1)
+    stage_launches = 9 + (1 if world > 1 else 0)
     with ClockSampler(local) as clk:
         t_wall = time.perf_counter()
         for _ in range(args.steps):

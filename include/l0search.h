@@ -98,6 +98,21 @@ int l0s_stage(l0s_ctx *ctx, const double *values, int64_t m, int64_t s, const do
               int is_device);
 
 /*
+ * Multi-GPU staging (one process per GPU): every rank stages the whole problem but computes
+ * only its shard of the Gram -- a contiguous range of the T x (upper-triangle 64 x 64 block)
+ * order -- into `pack` (device buffer of l0s_gram_shard_size doubles).  The caller all-gathers
+ * the packs in rank order (NCCL over NVLink) and hands the gathered buffer (nshards x pack
+ * doubles, device memory) to l0s_stage_finish, which scatters it into the full Gram and
+ * completes the stage.  nshards == 1 is l0s_stage.  (search.py:113-127 + the Gram precompute,
+ * split across GPUs; no reference counterpart -- the reference is single-process.)
+ */
+int l0s_gram_shard_size(int64_t m, int ntasks, int nshards, int64_t *out_doubles);
+int l0s_stage_shard(l0s_ctx *ctx, const double *values, int64_t m, int64_t s, const double *y,
+                    const int64_t *perm, const int64_t *bounds, int ntasks, int precision,
+                    int is_device, int shard, int nshards, double *pack);
+int l0s_stage_finish(l0s_ctx *ctx, const double *gathered);
+
+/*
  * Exhaustive search over tuple ranks [rank_begin, rank_end) of C(m, n)
  * (search.l0_search's scan + merge, search.py:233-304).  Writes the best
  * min(keep, #finite) tuples ordered by (score, rank); scores and ssr are

@@ -27,7 +27,8 @@ MODES = {"auto": 0, "fast": 1, "exact": 2}
 EXPORTS = (
     "l0s_last_error", "l0s_version", "l0s_device_count", "l0s_create", "l0s_destroy", "l0s_stage",
     "l0s_search", "l0s_fit_tuples", "l0s_screen_tuples", "l0s_get_gram", "l0s_unrank", "l0s_rank",
-    "l0s_count", "l0s_fp64_peak", "l0s_rcp_check",
+    "l0s_count", "l0s_fp64_peak", "l0s_rcp_check", "l0s_gram_shard_size", "l0s_stage_shard",
+    "l0s_stage_finish",
 )
 
 
@@ -83,6 +84,9 @@ def lib():
         L.l0s_create.argtypes = [i32, P(vp)]
         L.l0s_destroy.argtypes = [vp]
         L.l0s_stage.argtypes = [vp, vp, i64, i64, vp, vp, vp, i32, i32, i32]
+        L.l0s_gram_shard_size.argtypes = [i64, i32, i32, P(i64)]
+        L.l0s_stage_shard.argtypes = [vp, vp, i64, i64, vp, vp, vp, i32, i32, i32, i32, i32, vp]
+        L.l0s_stage_finish.argtypes = [vp, vp]
         L.l0s_search.argtypes = [vp, i32, i64, i64, i64, i32, vp, vp, vp, vp, P(i64), P(Stats)]
         L.l0s_fit_tuples.argtypes = [vp, i32, vp, i64, vp, vp, vp, vp]
         L.l0s_screen_tuples.argtypes = [vp, i32, vp, i64, vp, vp]
@@ -157,6 +161,28 @@ class Engine:
         check(lib().l0s_stage(self.handle, *args, ptr(bounds), bounds.shape[0] - 1, PREC[precision], is_dev),
               "l0s_stage")
         self.m, self.s, self.T = int(m), int(s), bounds.shape[0] - 1
+
+    @staticmethod
+    def gram_shard_size(m: int, ntasks: int, nshards: int) -> int:
+        """Doubles in one rank's Gram pack (l0s_gram_shard_size)."""
+        out = ctypes.c_int64(0)
+        check(lib().l0s_gram_shard_size(int(m), int(ntasks), int(nshards), ctypes.byref(out)), "l0s_gram_shard_size")
+        return out.value
+
+    def stage_shard(self, shape: tuple, bounds: np.ndarray, precision: str, device_ptrs: tuple, shard: int,
+                    nshards: int, pack_ptr: int) -> None:
+        """Stage device-resident inputs and compute this rank's Gram shard into pack_ptr (device)."""
+        bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+        m, s = shape
+        check(lib().l0s_stage_shard(self.handle, ctypes.c_void_p(device_ptrs[0]), m, s, ctypes.c_void_p(device_ptrs[1]),
+                                    ctypes.c_void_p(device_ptrs[2]), ptr(bounds), bounds.shape[0] - 1,
+                                    PREC[precision], 1, int(shard), int(nshards), ctypes.c_void_p(pack_ptr)),
+              "l0s_stage_shard")
+        self.m, self.s, self.T = int(m), int(s), bounds.shape[0] - 1
+
+    def stage_finish(self, gathered_ptr: int) -> None:
+        """Scatter the all-gathered packs (device pointer, nshards x pack doubles) into the Gram."""
+        check(lib().l0s_stage_finish(self.handle, ctypes.c_void_p(gathered_ptr)), "l0s_stage_finish")
 
     def search(self, n: int, keep: int, rank_begin: int = 0, rank_end: int = 2**63 - 1, mode: str = "auto"):
         keep = int(keep)

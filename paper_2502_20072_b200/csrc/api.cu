@@ -96,6 +96,7 @@ struct l0s_ctx {
     DBuf in_values, in_y, in_perm, bounds_d, zoff_d, Xp, yp, Z, G, qf, un2, yyu, rowsd, eta_d;
     DBuf rho, rho_cap, ynorm, iforce, dead, umin;
     int64_t n_dead = 0, n_iforce = 0;
+    bool shard_pending = false;  // l0s_stage_shard done, l0s_stage_finish due
     // binomial table (k <= binom_n) x (a <= m)
     DBuf binom;
     int binom_n = -1;
@@ -293,8 +294,9 @@ int l0s_destroy(l0s_ctx* c) {
     return L0S_OK;
 }
 
-int l0s_stage(l0s_ctx* c, const double* values, int64_t m, int64_t s, const double* y, const int64_t* perm,
-              const int64_t* bounds, int ntasks, int precision, int is_device) {
+// stage up to (not including) the Gram: validation, layout, H2D, gather + normalize into Z
+static int stage_prepare(l0s_ctx* c, const double* values, int64_t m, int64_t s, const double* y, const int64_t* perm,
+                         const int64_t* bounds, int ntasks, int precision, int is_device) {
     if (!c) return fail(L0S_EINVAL, "null context");
     if (m < 1 || s < 1 || ntasks < 1) return fail(L0S_EINVAL, "need m >= 1, s >= 1, ntasks >= 1 (got %lld, %lld, %d)", (long long)m, (long long)s, ntasks);
     if (precision != L0S_PREC_FP64 && precision != L0S_PREC_FP32) return fail(L0S_EINVAL, "bad precision %d", precision);
@@ -359,8 +361,14 @@ int l0s_stage(l0s_ctx* c, const double* values, int64_t m, int64_t s, const doub
     CK(cudaMemsetAsync(c->Z.p, 0, sizeof(double) * c->mp * c->sp, c->st));
     launch_normalize(c->Xp.p, c->yp.p, precision, m, s, c->bounds_d.as<int64_t>(), c->zoff_d.as<int64_t>(), ntasks,
                      c->sp, c->Z.as<double>(), c->qf.as<double>(), c->un2.as<double>(), c->yyu.as<double>(), c->st);
-    launch_gram(c->Z.as<double>(), c->sp, c->zoff_h.data(), c->zoff_d.as<int64_t>(), c->rpad_h.data(), ntasks, m, c->mp, c->G.as<double>(),
-                c->st);
+    return L0S_OK;
+}
+
+// stage after the Gram: unit diagonal, per-feature conditioning flags, host copies
+static int stage_post(l0s_ctx* c) {
+    const int64_t m = c->m;
+    const int ntasks = c->T;
+    launch_unit_diag(c->G.as<double>(), ntasks, m, c->mp, c->st);
     CK(cudaGetLastError());
     // per-feature conditioning flags on the device (stage.cu: launch_feature_flags)
     CK(c->rho.ensure(sizeof(double) * m * ntasks));
@@ -382,6 +390,48 @@ int l0s_stage(l0s_ctx* c, const double* values, int64_t m, int64_t s, const doub
     c->staged = true;
     c->binom_m = -1;
     return L0S_OK;
+}
+
+int l0s_stage(l0s_ctx* c, const double* values, int64_t m, int64_t s, const double* y, const int64_t* perm,
+              const int64_t* bounds, int ntasks, int precision, int is_device) {
+    int rc = stage_prepare(c, values, m, s, y, perm, bounds, ntasks, precision, is_device);
+    if (rc) return rc;
+    launch_gram(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), ntasks, c->mp, c->G.as<double>(), 0, 1, nullptr,
+                c->st);
+    return stage_post(c);
+}
+
+int l0s_gram_shard_size(int64_t m, int ntasks, int nshards, int64_t* out_doubles) {
+    if (m < 1 || ntasks < 1 || nshards < 1) return fail(L0S_EINVAL, "need m, ntasks, nshards >= 1");
+    const int64_t mp = ((m + 1 + 32 + 63) / 64) * 64;
+    *out_doubles = gram_shard_blocks(mp, ntasks, nshards) * 64 * 64;
+    return L0S_OK;
+}
+
+int l0s_stage_shard(l0s_ctx* c, const double* values, int64_t m, int64_t s, const double* y, const int64_t* perm,
+                    const int64_t* bounds, int ntasks, int precision, int is_device, int shard, int nshards,
+                    double* pack) {
+    if (nshards < 1 || shard < 0 || shard >= nshards) return fail(L0S_EINVAL, "shard %d of %d", shard, nshards);
+    if (nshards > 1 && !pack) return fail(L0S_EINVAL, "pack buffer required for nshards > 1");
+    int rc = stage_prepare(c, values, m, s, y, perm, bounds, ntasks, precision, is_device);
+    if (rc) return rc;
+    launch_gram(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), ntasks, c->mp, c->G.as<double>(), shard, nshards,
+                pack, c->st);
+    CK(cudaGetLastError());
+    if (nshards == 1) return stage_post(c);
+    CK(cudaStreamSynchronize(c->st));  // the pack is complete for the caller's all-gather
+    c->shard_pending = true;
+    return L0S_OK;
+}
+
+int l0s_stage_finish(l0s_ctx* c, const double* gathered) {
+    if (!c || !c->shard_pending) return fail(L0S_ESTATE, "l0s_stage_shard (nshards > 1) must come first");
+    if (!gathered) return fail(L0S_EINVAL, "null gathered buffer");
+    CK(cudaSetDevice(c->dev));
+    launch_gram_unpack(gathered, c->T, c->mp, c->G.as<double>(), c->st);
+    CK(cudaGetLastError());
+    c->shard_pending = false;
+    return stage_post(c);
 }
 
 int l0s_count(int64_t m, int n, int64_t* out) {

@@ -7,6 +7,8 @@
 // written), streaming K in 32-sample chunks through a cp.async double buffer.
 // Warp tile 16x32 = 2x4 m8n8 fragments; every k4 step issues 8
 // mma.sync.m8n8k4.f64 (SASS: DMMA.8x8x4) from 6 conflict-free LDS.64.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -23,24 +25,33 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-// grid: (upper-triangle blocks, tasks); task t owns Z columns [zoff[t], zoff[t+1]) and G + t mp^2
-__global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int64_t sp,
-                                              const int64_t* __restrict__ zoff, int nb, double* __restrict__ Gall,
-                                              int64_t mp) {
-    extern __shared__ __align__(16) double gsm[];
-    double* sA[2] = {gsm, gsm + BM * LDS};
-    double* sB[2] = {gsm + 2 * BM * LDS, gsm + 3 * BM * LDS};
-    const int task = blockIdx.y;
-    const int64_t k0 = zoff[task], klen = zoff[task + 1] - k0;
-    double* G = Gall + (int64_t)task * mp * mp;
-    // block (ba, bb), ba <= bb, from the linear upper-triangle index
-    int lin = blockIdx.x;
-    int ba = 0;
+// Block (task, ba, bb), ba <= bb, of the linear index g over T x (upper-triangle blocks).
+__device__ __forceinline__ void gram_block(int64_t g, int nb, int& task, int& ba, int& bb) {
+    const int nblk = nb * (nb + 1) / 2;
+    task = (int)(g / nblk);
+    int lin = (int)(g % nblk);
+    ba = 0;
     while (lin >= nb - ba) {
         lin -= nb - ba;
         ++ba;
     }
-    int bb = ba + lin;
+    bb = ba + lin;
+}
+
+// grid: blocks [g0, g0 + gridDim.x) of the linear (task, upper-triangle block) order; task t owns
+// Z columns [zoff[t], zoff[t+1]) and G + t mp^2.  pack == nullptr: write G (both triangles);
+// otherwise write block g - g0 as a row-major 64 x 64 tile at pack + (g - g0) * 4096 (a shard
+// of the multi-GPU Gram, exchanged by all-gather and scattered by k_gram_unpack).
+__global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int64_t sp,
+                                              const int64_t* __restrict__ zoff, int nb, double* __restrict__ Gall,
+                                              int64_t mp, int64_t g0, double* __restrict__ pack) {
+    extern __shared__ __align__(16) double gsm[];
+    double* sA[2] = {gsm, gsm + BM * LDS};
+    double* sB[2] = {gsm + 2 * BM * LDS, gsm + 3 * BM * LDS};
+    int task, ba, bb;
+    gram_block(g0 + blockIdx.x, nb, task, ba, bb);
+    const int64_t k0 = zoff[task], klen = zoff[task + 1] - k0;
+    double* G = Gall + (int64_t)task * mp * mp;
     const double* Za = Z + (int64_t)ba * BM * sp + k0;
     const double* Zb = Z + (int64_t)bb * BM * sp + k0;
     int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -99,18 +110,49 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int6
         __syncthreads();
     }
     // epilogue: fragment (row = lane/4, col = 2*(lane%4) + v)
+    double* P = pack ? pack + (int64_t)blockIdx.x * (BM * BM) : nullptr;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
-                int64_t row = (int64_t)ba * BM + r0 + a * 8 + fr;
-                int64_t col = (int64_t)bb * BM + c0 + j * 8 + 2 * fk + v;
-                double x = acc[a][j][v];
-                G[row * mp + col] = x;
-                if (ba != bb) G[col * mp + row] = x;
+                const int lr = r0 + a * 8 + fr, lc = c0 + j * 8 + 2 * fk + v;
+                const double x = acc[a][j][v];
+                if (P) {
+                    P[lr * BM + lc] = x;
+                } else {
+                    const int64_t row = (int64_t)ba * BM + lr, col = (int64_t)bb * BM + lc;
+                    G[row * mp + col] = x;
+                    if (ba != bb) G[col * mp + row] = x;
+                }
             }
+}
+
+// Scatter all shards' packed tiles into G (both triangles; the mirror goes through shared
+// memory so both stores are coalesced).  recv = nshards x per_shard tiles, shard r holding
+// blocks [r * per_shard, ...) of the linear order, total blocks overall.
+__global__ void __launch_bounds__(256) k_gram_unpack(const double* __restrict__ recv, int64_t total, int nb,
+                                                     double* __restrict__ Gall, int64_t mp) {
+    __shared__ double t[BM][BM + 1];
+    const int64_t g = blockIdx.x;
+    if (g >= total) return;
+    int task, ba, bb;
+    gram_block(g, nb, task, ba, bb);
+    double* G = Gall + (int64_t)task * mp * mp;
+    const double* P = recv + g * (BM * BM);
+    for (int e = threadIdx.x; e < BM * BM; e += blockDim.x) {
+        const int r = e / BM, c = e % BM;
+        const double x = P[e];
+        G[((int64_t)ba * BM + r) * mp + (int64_t)bb * BM + c] = x;
+        t[r][c] = x;
+    }
+    if (ba == bb) return;
+    __syncthreads();
+    for (int e = threadIdx.x; e < BM * BM; e += blockDim.x) {
+        const int r = e / BM, c = e % BM;
+        G[((int64_t)bb * BM + r) * mp + (int64_t)ba * BM + c] = t[c][r];
+    }
 }
 
 __global__ void k_unit_diag(double* Gall, int64_t m, int64_t mp) {
@@ -139,17 +181,37 @@ void launch_mark_dead(double* G, const int32_t* dead, int ndead, int T, int64_t 
     if (ndead > 0) k_mark_dead<<<256, 256, 0, st>>>(G, dead, ndead, T, mp);
 }
 
-void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_h, const int64_t* zoff_d, const int64_t* rpad_h,
-                 int T, int64_t m, int64_t mp, double* G, cudaStream_t st) {
-    int nb = (int)(mp / BM);
-    int nblk = nb * (nb + 1) / 2;
+int64_t gram_blocks(int64_t mp, int T) {
+    const int64_t nb = mp / BM;
+    return (int64_t)T * (nb * (nb + 1) / 2);
+}
+int64_t gram_shard_blocks(int64_t mp, int T, int nshards) {
+    return (gram_blocks(mp, T) + nshards - 1) / nshards;
+}
+
+void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_d, int T, int64_t mp, double* G, int shard,
+                 int nshards, double* pack, cudaStream_t st) {
+    const int nb = (int)(mp / BM);
+    const int64_t total = gram_blocks(mp, T);
     const int smem = 4 * BM * LDS * (int)sizeof(double);
     cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     // one launch for every task: ~T * nb^2 / 2 CTAs keep the tail wave short
-    k_gram<<<dim3((unsigned)nblk, (unsigned)T), 256, smem, st>>>(Z, sp, zoff_d, nb, G, mp);
+    int64_t g0 = 0, cnt = total;
+    if (nshards > 1) {
+        const int64_t per = gram_shard_blocks(mp, T, nshards);
+        g0 = std::min<int64_t>(total, per * shard);
+        cnt = std::min<int64_t>(total, g0 + per) - g0;
+    }
+    if (cnt > 0) k_gram<<<(unsigned)cnt, 256, smem, st>>>(Z, sp, zoff_d, nb, G, mp, g0, nshards > 1 ? pack : nullptr);
+}
+
+void launch_gram_unpack(const double* recv, int T, int64_t mp, double* G, cudaStream_t st) {
+    const int64_t total = gram_blocks(mp, T);
+    k_gram_unpack<<<(unsigned)total, 256, 0, st>>>(recv, total, (int)(mp / BM), G, mp);
+}
+
+void launch_unit_diag(double* G, int T, int64_t m, int64_t mp, cudaStream_t st) {
     k_unit_diag<<<dim3((unsigned)((m + 255) / 256), (unsigned)T), 256, 0, st>>>(G, m, mp);
-    (void)zoff_h;
-    (void)rpad_h;
 }
 
 }  // namespace l0s

@@ -25,9 +25,18 @@ void launch_feature_flags(const double* qf, const double* un2, const double* row
                           double* umin, double* rho, double* rho_cap, unsigned char* dead, unsigned char* iforce,
                           double* G, const double* yyu, double* ynorm, cudaStream_t st);
 
-// ---- Gram (gram.cu): G[t] = Z_t Z_t^T on DMMA, (mp x mp) per task, diag of features := 1 ----
-void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_h, const int64_t* zoff_d, const int64_t* rpad_h, int T,
-                 int64_t m, int64_t mp, double* G, cudaStream_t st);
+// ---- Gram (gram.cu): G[t] = Z_t Z_t^T on DMMA, (mp x mp) per task ----
+// The T x (upper-triangle 64 x 64 blocks) are numbered linearly; nshards == 1 computes all of
+// them into G, otherwise shard `shard` computes its contiguous range of gram_shard_blocks()
+// into `pack` (row-major 64 x 64 tiles), exchanged by an all-gather and scattered by
+// launch_gram_unpack (recv = nshards x per-shard tiles, in shard order).
+int64_t gram_blocks(int64_t mp, int T);
+int64_t gram_shard_blocks(int64_t mp, int T, int nshards);
+void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_d, int T, int64_t mp, double* G, int shard,
+                 int nshards, double* pack, cudaStream_t st);
+void launch_gram_unpack(const double* recv, int T, int64_t mp, double* G, cudaStream_t st);
+// diagonal of the feature rows := 1 (unit-norm columns; NaN rows stay NaN)
+void launch_unit_diag(double* G, int T, int64_t m, int64_t mp, cudaStream_t st);
 // Features the reference's rank rule rejects in every tuple: NaN their Gram row and column (all tasks).
 void launch_mark_dead(double* G, const int32_t* dead, int ndead, int T, int64_t mp, cudaStream_t st);
 

@@ -39,6 +39,38 @@ def merge_candidates(parts, keep: int):
     return out
 
 
+def sharded_stage(eng, shape, bounds, precision, device_ptrs, group=None, all_gather=None):
+    """Collective stage: every rank stages the whole problem, computes 1/world of the Gram
+    (l0s_stage_shard) and the shards are all-gathered over NCCL straight into the buffer
+    l0s_stage_finish scatters from.  world == 1 is a plain stage.
+
+    ``all_gather(out, inp)`` defaults to ``torch.distributed.all_gather_into_tensor``.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from ._lib import Engine
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    me = dist.get_rank(group) if dist.is_initialized() else 0
+    if world == 1:
+        eng.stage(shape, None, None, bounds, precision, device_ptrs=device_ptrs)
+        return
+    m, ntasks = int(shape[0]), len(bounds) - 1
+    per = Engine.gram_shard_size(m, ntasks, world)
+    key = (per, world)
+    if getattr(eng, "_xbuf_key", None) != key:
+        dev = torch.device("cuda", eng.device)
+        eng._xbuf = (torch.empty(per, dtype=torch.float64, device=dev),
+                     torch.empty(world * per, dtype=torch.float64, device=dev))
+        eng._xbuf_key = key
+    send, recv = eng._xbuf
+    eng.stage_shard(shape, bounds, precision, device_ptrs, me, world, send.data_ptr())
+    (all_gather or (lambda o, i: dist.all_gather_into_tensor(o, i, group=group)))(recv, send)
+    torch.cuda.current_stream(send.device).synchronize()  # the engine runs on its own stream
+    eng.stage_finish(recv.data_ptr())
+
+
 def sharded_l0_search(values, property_values, task_slices=None, config=None, task_labels=None,
                       group=None, local_search=None):
     """Collective l0_search: every rank must call it with the same inputs; every rank
@@ -66,4 +98,4 @@ def sharded_l0_search(values, property_values, task_slices=None, config=None, ta
     return [c[2] for c in merge_candidates(parts, keep)]
 
 
-__all__ = ["rank_range", "merge_candidates", "sharded_l0_search", "comb"]
+__all__ = ["rank_range", "merge_candidates", "sharded_stage", "sharded_l0_search", "comb"]

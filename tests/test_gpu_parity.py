@@ -305,3 +305,40 @@ def test_pipeline_drop_in_model_files(tmp_path, name):
             assert got.split(b"model: 10")[0] == want.split(b"model: 10")[0]
         else:
             assert got == want
+
+
+@pytest.mark.parametrize("W", [2, 3, 8])
+def test_sharded_gram_equals_single_gpu(rng, W):
+    """Multi-GPU staging emulated on one device: W engines each compute their Gram shard into
+    their slice of one buffer (what the NCCL all-gather assembles), the last finishes the stage;
+    its Gram and its search equal the single-GPU stage bit for bit."""
+    import torch
+
+    from paper_2502_20072_b200 import _lib
+
+    m, T = 150, 3
+    s = 3 * 200
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    y = 1.5 * v[4] - 0.5 * v[77] + v[140] + 0.01 * rng.standard_normal(s)
+    slices = [np.arange(t, s, T) for t in range(T)]
+    perm = np.concatenate(slices).astype(np.int64)
+    bounds = np.array([0, 200, 400, 600], dtype=np.int64)
+    ref = _lib.Engine(0)
+    ref.stage(v, y, perm, bounds, "fp64")
+    per = _lib.Engine.gram_shard_size(m, T, W)
+    vd, yd, pd = (torch.from_numpy(a).cuda() for a in (v, y, perm))
+    ptrs = (vd.data_ptr(), yd.data_ptr(), pd.data_ptr())
+    recv = torch.full((W * per,), float("nan"), dtype=torch.float64, device="cuda")
+    engs = [_lib.Engine(0) for _ in range(W)]
+    for r, e in enumerate(engs):
+        e.stage_shard((m, s), bounds, "fp64", ptrs, r, W, recv[r * per:].data_ptr())
+    torch.cuda.synchronize()
+    last = engs[-1]
+    last.stage_finish(recv.data_ptr())
+    for t in range(T):
+        assert bits_equal(last.gram(t), ref.gram(t))
+    a = ref.search(3, 10, 0, 2**62, "fast")
+    b = last.search(3, 10, 0, 2**62, "fast")
+    assert np.array_equal(a[1], b[1]) and bits_equal(a[0], b[0])
+    with pytest.raises(RuntimeError):
+        engs[0].search(3, 10, 0, 2**62, "fast")  # shard staged but never finished
