@@ -116,6 +116,8 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("L0S_BENCH_ONE_DEVICE"):  # exercise the N > 1 code path on a 1-GPU box (gloo)
+        local = 0
     return world, rank, local
 
 
@@ -190,9 +192,12 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("L0S_BENCH_ONE_DEVICE"):
+            dist.init_process_group("gloo")  # ranks share one GPU: NCCL needs distinct devices
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2502_20072_b200 import L0Config, SearchStats, _lib, l0_search
-    from paper_2502_20072_b200.search import _partition
+    from paper_2502_20072_b200.search import _partition, unrank_tuple
 
     v, y, slices = make_c3()
     total = comb(M, N_DIM)
@@ -240,15 +245,22 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([dev_ms], device=f"cuda:{local}", dtype=torch.float64)
+        cdev = "cpu" if dist.get_backend() == "gloo" else f"cuda:{local}"
+        t = torch.tensor([dev_ms], device=cdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms = float(t.item())
         # merge the per-rank certified top lists (NCCL all-gather of (score, rank))
-        buf = torch.full((2, 10), float("inf"), dtype=torch.float64, device=f"cuda:{local}")
+        buf = torch.full((2, 10), float("inf"), dtype=torch.float64, device=cdev)
         buf[0, : len(sc)] = torch.from_numpy(sc)
         buf[1, : len(rk)] = torch.from_numpy(rk.astype(np.float64))
         parts = [torch.empty_like(buf) for _ in range(world)]
         dist.all_gather(parts, buf)
+        from paper_2502_20072_b200.dist import merge_candidates
+
+        merged = merge_candidates([[(float(p[0, i]), int(p[1, i]), None) for i in range(10)] for p in parts], 10)
+        best_rank = merged[0][1] if merged else None
+    else:
+        best_rank = int(rk[0]) if len(rk) else None
     value = total * args.steps / (dev_ms * 1e-3)
 
     # ---- end to end through the public API on pinned host buffers ----
@@ -256,20 +268,29 @@ def main():
     yh = torch.from_numpy(y).pin_memory().numpy()
     cfg = L0Config(dimension=N_DIM)
     e2e_ms = []
+    if world > 1:
+        from paper_2502_20072_b200.dist import sharded_l0_search
+
+        def public_call():  # the multi-GPU public API: collective stage, rank ranges, merge
+            return sharded_l0_search(vh, yh, slices, cfg)
+    else:
+        def public_call():
+            return l0_search(vh, yh, slices, cfg, stats=SearchStats())
     for _ in range(args.warmup):
-        l0_search(vh, yh, slices, cfg, rank_range=(lo, hi))
+        public_call()
     barrier()
     clk.__enter__()
     for _ in range(args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        models = l0_search(vh, yh, slices, cfg, rank_range=(lo, hi), stats=SearchStats())
+        models = public_call()
         torch.cuda.synchronize()
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
     clk.__exit__()
     e2e_total = sum(e2e_ms)
     if world > 1:
-        t = torch.tensor([e2e_total], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([e2e_total], device="cpu" if dist.get_backend() == "gloo" else f"cuda:{local}",
+                         dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
     e2e_value = total * args.steps / (e2e_total * 1e-3)
@@ -315,7 +336,8 @@ def main():
         "detail": {"fit_ms": fit_avg, "stage_gram_ms": st.ms_gram, "search_ms": st.ms_total,
                    "exact_ms": st.ms_exact, "n_candidates": st.n_candidates, "n_ill": st.n_ill,
                    "n_rescan": st.n_rescan, "certified": st.certified, "wall_s": wall,
-                   "best": [list(models[0].indices), models[0].score] if models else None},
+                   "best": [list(models[0].indices), models[0].score] if models else None,
+                   "best_device_step": list(unrank_tuple(best_rank, M, N_DIM)) if best_rank is not None else None},
     }
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(v, y, slices, args.cpu_seconds)

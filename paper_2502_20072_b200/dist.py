@@ -66,35 +66,70 @@ def sharded_stage(eng, shape, bounds, precision, device_ptrs, group=None, all_ga
         eng._xbuf_key = key
     send, recv = eng._xbuf
     eng.stage_shard(shape, bounds, precision, device_ptrs, me, world, send.data_ptr())
-    (all_gather or (lambda o, i: dist.all_gather_into_tensor(o, i, group=group)))(recv, send)
+    if all_gather is None:
+        if dist.get_backend(group) == "gloo":  # CPU transport (tests / ranks sharing one GPU)
+            def all_gather(o, i):
+                oc = o.new_empty(o.shape, device="cpu")
+                dist.all_gather_into_tensor(oc, i.cpu(), group=group)
+                o.copy_(oc)
+        else:
+            def all_gather(o, i):
+                dist.all_gather_into_tensor(o, i, group=group)
+    torch.cuda.synchronize(send.device)  # shard written on the engine's stream
+    all_gather(recv, send)
     torch.cuda.current_stream(send.device).synchronize()  # the engine runs on its own stream
     eng.stage_finish(recv.data_ptr())
 
 
 def sharded_l0_search(values, property_values, task_slices=None, config=None, task_labels=None,
-                      group=None, local_search=None):
+                      group=None, local_search=None, device=None):
     """Collective l0_search: every rank must call it with the same inputs; every rank
     receives the same merged list of ``Model`` records.
 
-    local_search(values, y, task_slices, config, task_labels, rank_range) -> list of models
-    (default: this package's device search).
+    Default path (one process per GPU): the inputs go to this rank's device, the stage is
+    collective (``sharded_stage``: 1/world of the Gram per rank, NCCL all-gather), the rank
+    searches its contiguous rank range and certifies its own top list exactly, and the lists
+    are merged by (score, rank).  ``local_search(values, y, task_slices, config, task_labels,
+    rank_range) -> list of models`` replaces the device part (the CPU tests inject the oracle).
     """
     import torch.distributed as dist
 
-    from .search import count_models, l0_search, rank_tuple
+    from . import _lib
+    from .search import _as_matrix, _labels_for, _model, _partition, count_models, l0_search, rank_tuple, unrank_tuple
 
     world = dist.get_world_size(group)
     me = dist.get_rank(group)
-    m = np.asarray(values).shape[0] if not hasattr(values, "values_matrix") else len(values.expressions)
-    total = count_models(m, config.dimension)
+    vals, expressions = _as_matrix(values)
+    m = vals.shape[0]
+    n = config.dimension
+    total = count_models(m, n)
     lo, hi = rank_range(total, me, world)
-    search = local_search or (lambda v, y, sl, cfg, lab, rr: l0_search(v, y, sl, cfg, task_labels=lab,
-                                                                          rank_range=rr))
-    models = search(values, property_values, task_slices, config, task_labels, (lo, hi)) if hi > lo else []
-    mine = [(float(md.score), rank_tuple(md.indices, m, config.dimension), md) for md in models]
+    keep = max(1, config.n_models_store)
+    if local_search is not None:
+        models = local_search(values, property_values, task_slices, config, task_labels, (lo, hi)) if hi > lo else []
+    elif m < n:
+        models = l0_search(values, property_values, task_slices, config, task_labels=task_labels)  # raises
+    else:
+        import torch
+
+        s = vals.shape[1]
+        perm, bounds, slices = _partition(s, task_slices)
+        dev = torch.cuda.current_device() if device is None else int(device)
+        eng = _lib.engine(dev)
+        vd = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.float64)).to(dev)
+        yd = torch.from_numpy(np.ascontiguousarray(property_values, dtype=np.float64)).to(dev)
+        pd = torch.from_numpy(perm).to(dev)
+        torch.cuda.synchronize(dev)
+        sharded_stage(eng, (m, s), bounds, config.precision, (vd.data_ptr(), yd.data_ptr(), pd.data_ptr()), group)
+        models = []
+        if hi > lo:
+            sc, rk, coef, ssr, _ = eng.search(n, keep, lo, hi, "auto")
+            labels = _labels_for(slices, task_labels)
+            models = [_model(unrank_tuple(int(rk[i]), m, n), expressions, coef[i], ssr[i], bounds, s, labels)
+                      for i in range(len(sc))]
+    mine = [(float(md.score), rank_tuple(md.indices, m, n), md) for md in models]
     parts = [None] * world
     dist.all_gather_object(parts, mine, group=group)
-    keep = max(1, config.n_models_store)
     return [c[2] for c in merge_candidates(parts, keep)]
 
 
