@@ -526,7 +526,7 @@ static void fill_fit_common(l0s_ctx* c, FitArgs& a, int n) {
 
 int l0s_screen_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags) {
     if (!c || !c->staged) return fail(L0S_ESTATE, "l0s_stage must be called first");
-    if (n != 3 && n != 4) return fail(L0S_EINVAL, "screened bounds are implemented for n = 3 and 4");
+    if (n < 2 || n > 4) return fail(L0S_EINVAL, "screened bounds are implemented for n = 2, 3 and 4");
     if (count <= 0) return L0S_OK;
     CK(cudaSetDevice(c->dev));
     int rc = ensure_binom(c, n);
@@ -537,7 +537,9 @@ int l0s_screen_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, d
     CK(c->cand_lb.ensure(sizeof(double) * count));
     CK(c->ex_ok.ensure(sizeof(int32_t) * count));
     CK(cudaMemcpyAsync(c->ex_tuples.p, tuples, sizeof(int64_t) * count * n, cudaMemcpyHostToDevice, c->st));
-    if (n == 3)
+    if (n == 2)
+        launch_screen2(a, c->ex_tuples.as<int64_t>(), count, c->cand_lb.as<double>(), c->ex_ok.as<int32_t>(), c->st);
+    else if (n == 3)
         launch_screen3(a, c->ex_tuples.as<int64_t>(), count, c->cand_lb.as<double>(), c->ex_ok.as<int32_t>(), c->st);
     else
         launch_screen4(a, c->ex_tuples.as<int64_t>(), count, c->cand_lb.as<double>(), c->ex_ok.as<int32_t>(), c->st);
@@ -669,14 +671,20 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
         // prefix[v] = rank of the first tuple whose smallest index is v
         std::vector<int64_t> pre((size_t)c->m + 1, 0);
         for (int64_t v = 0; v < c->m; ++v) pre[(size_t)v + 1] = pre[(size_t)v] + binom_sat(c->m - 1 - v, n - 1);
-        c->units_h = n == 3 ? fit3_units(c->m, c->T, N, pre, rb, re) : fit4_units(c->m, c->T, pre, rb, re);
+        c->units_h = n == 2 ? fit2_units(c->m, pre, rb, re)
+                     : n == 3 ? fit3_units(c->m, c->T, N, pre, rb, re)
+                              : fit4_units(c->m, c->T, pre, rb, re);
         CK(c->units.ensure(sizeof(int4) * std::max<size_t>(c->units_h.size(), 1)));
         CK(cudaMemcpyAsync(c->units.p, c->units_h.data(), sizeof(int4) * c->units_h.size(), cudaMemcpyHostToDevice, c->st));
         std::copy(key, key + 5, c->units_key);
     }
     const int kc = (int)std::min<int64_t>(128, std::max<int64_t>(64, keep + 32));
-    const int grid = n == 3 ? fit3_grid(c->T, c->nsm) : fit4_grid(c->T, c->nsm);
-    auto launch_fit = [&](const FitArgs& fa) { return n == 3 ? fit3_launch(fa, c->nsm, c->st) : fit4_launch(fa, c->nsm, c->st); };
+    const int grid = n == 2 ? fit2_grid(c->T, c->nsm) : n == 3 ? fit3_grid(c->T, c->nsm) : fit4_grid(c->T, c->nsm);
+    auto launch_fit = [&](const FitArgs& fa) {
+        return n == 2 ? fit2_launch(fa, c->nsm, c->st)
+               : n == 3 ? fit3_launch(fa, c->nsm, c->st)
+                        : fit4_launch(fa, c->nsm, c->st);
+    };
     const int slots = grid * fit_slots_per_cta();
     const int64_t ill_cap = (int64_t)1 << 26;  // 512 MB of ranks; overflow is reported, never dropped
     CK(c->ucount.ensure(sizeof(int) * 4));
@@ -854,13 +862,13 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
     cudaEventCreate(&t1);
     cudaEventRecord(t0, c->st);
     // the screen's error model is for fp64 arithmetic in the reference (precision="fp64")
-    bool fast_ok = (n == 3 || n == 4) && c->T <= fit3_max_tasks() && keep <= 96 && c->prec == L0S_PREC_FP64;
+    bool fast_ok = (n >= 2 && n <= 4) && c->T <= fit3_max_tasks() && keep <= 96 && c->prec == L0S_PREC_FP64;
     bool use_fast;
     if (mode == L0S_MODE_FAST) {
         if (!fast_ok) {
             cudaEventDestroy(t0);
             cudaEventDestroy(t1);
-            return fail(L0S_EINVAL, "screened path needs n in {3, 4}, ntasks <= %d, keep <= 96, fp64",
+            return fail(L0S_EINVAL, "screened path needs n in {2, 3, 4}, ntasks <= %d, keep <= 96, fp64",
                         fit3_max_tasks());
         }
         use_fast = true;

@@ -155,6 +155,13 @@ std::vector<int4> fit3_units(int64_t m, int T, int64_t N_total, const std::vecto
 void launch_screen3(const FitArgs& a, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags,
                     cudaStream_t st);
 
+// ---- screened fit, n = 2 (fit2.cu) ----
+int fit2_launch(const FitArgs& a, int nsm, cudaStream_t st);
+int fit2_grid(int T, int nsm);
+std::vector<int4> fit2_units(int64_t m, const std::vector<int64_t>& c1_prefix, int64_t rank_lo, int64_t rank_hi);
+void launch_screen2(const FitArgs& a, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags,
+                    cudaStream_t st);
+
 // ---- screened fit, n = 4 (fit4.cu) ----
 int fit4_launch(const FitArgs& a, int nsm, cudaStream_t st);
 int fit4_grid(int T, int nsm);

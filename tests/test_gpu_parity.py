@@ -342,3 +342,56 @@ def test_sharded_gram_equals_single_gpu(rng, W):
     assert np.array_equal(a[1], b[1]) and bits_equal(a[0], b[0])
     with pytest.raises(RuntimeError):
         engs[0].search(3, 10, 0, 2**62, "fast")  # shard staged but never finished
+
+
+@pytest.mark.parametrize("T", [1, 2, 5])
+def test_fast_n2_matches_oracle(oracle, rng, T):
+    """Screened dimension-2 search == exhaustive CPU oracle, single and multi-task."""
+    from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
+
+    m, s = 300, 250
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    y = 1.5 * v[12] - v[240] + 0.05 * rng.standard_normal(s)
+    v[100] = v[12] + 1e-9 * rng.standard_normal(s)  # near-copy: rank rule territory
+    slices = [np.arange(t, s, T) for t in range(T)]
+    want = oracle.l0_search(v, y, slices, 2, 10, "fp64", threads=os.cpu_count() or 1)
+    st = SearchStats()
+    got = l0_search(v, y, slices, L0Config(dimension=2), mode="fast", stats=st)
+    assert st.device["mode_used"] == 1 and st.device["certified"] == 1
+    assert [md.indices for md in got] == [w["indices"] for w in want]
+    assert bits_equal([md.score for md in got], [w["score"] for w in want])
+    assert bits_equal(np.array([md.coefficients for md in got]), np.array([w["coefficients"] for w in want]))
+
+
+def test_screen_n2_lower_bound(eng, rng):
+    m, s = 40, 90
+    v = rng.uniform(0.5, 2.0, size=(m, s)) * np.logspace(-2, 2, m)[:, None]
+    v[7] = v[3] + 1e-8 * rng.standard_normal(s)
+    y = v[0] - 2 * v[9] + 1e-3 * rng.standard_normal(s)
+    eng.stage(v, y, np.arange(s), np.array([0, s]), "fp64")
+    tup = np.array(list(itertools.combinations(range(m), 2)), dtype=np.int64)
+    ok, score, _, _ = eng.fit_tuples(tup)
+    lb, flags = eng.screen_tuples(tup)
+    sel = (flags == 3) & np.isfinite(score)
+    assert sel.sum() > 0.5 * len(tup)
+    assert not (lb[sel] > score[sel] * s).any()
+    assert np.all(ok[flags == 3])
+
+
+def test_criterion9_shape_prefix(oracle):
+    """The reference's criterion-9 shape (m=4500, s=200, n=2; test_acceptance.py:304-326) on a
+    rank prefix, GPU screened path vs CPU oracle, then the full search's best model."""
+    from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
+
+    rng = np.random.default_rng(9)
+    m, s = 4500, 200
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    y = 2.0 * v[10] * 0.5 + v[3000] + 0.01 * rng.standard_normal(s)
+    hi = 400_000
+    want = oracle.l0_search(v, y, None, 2, 10, "fp64", threads=os.cpu_count() or 1, rank_range=(0, hi))
+    got = l0_search(v, y, None, L0Config(dimension=2), mode="fast", rank_range=(0, hi))
+    assert [md.indices for md in got] == [w["indices"] for w in want]
+    assert bits_equal([md.score for md in got], [w["score"] for w in want])
+    st = SearchStats()
+    full = l0_search(v, y, None, L0Config(dimension=2), stats=st)
+    assert st.device["mode_used"] == 1 and full[0].indices == (10, 3000)
