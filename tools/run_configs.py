@@ -46,10 +46,18 @@ def make_c4(seed=3):
     return v, y, None, 4
 
 
+def make_crit9(seed=9):
+    """The reference's criterion-9 shape (test_acceptance.py:304-326): m=4500, s=200, n=2."""
+    rng = np.random.default_rng(seed)
+    v = rng.uniform(0.5, 2.0, size=(4500, 200))
+    y = v[10] + v[3000] + 0.01 * rng.standard_normal(200)
+    return v, y, None, 2
+
+
 def run(name, check=False, steps=3):
     from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
 
-    v, y, slices, n = {"c2": make_c2, "c4": make_c4}[name]()
+    v, y, slices, n = {"c2": make_c2, "c4": make_c4, "crit9": make_crit9}[name]()
     total = comb(v.shape[0], n)
     cfg = L0Config(dimension=n)
     l0_search(v, y, slices, cfg)  # warm-up (also stages)
@@ -68,7 +76,7 @@ def run(name, check=False, steps=3):
     if check:
         from oracle import oracle as orc
 
-        hi = min(total, 200_000 if name == "c2" else 20_000)
+        hi = min(total, {"c2": 200_000, "crit9": 2_000_000}.get(name, 20_000))
         want = orc.l0_search(v, y, slices, n, 10, "fp64", threads=os.cpu_count() or 1, rank_range=(0, hi))
         got = l0_search(v, y, slices, cfg, rank_range=(0, hi))
         ok = [g.indices for g in got] == [w["indices"] for w in want] and all(
