@@ -85,7 +85,10 @@ struct Rec {  // bit-exact record of one refit tuple
 struct l0s_ctx {
     int dev = 0, nsm = 0;
     cudaStream_t st = nullptr;
+    cudaStream_t cst = nullptr;  // H2D copies of the overlapped stage
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    static constexpr int kChunks = 8;
+    cudaEvent_t cev[kChunks + 1] = {};
     // staged problem
     bool staged = false;
     int64_t m = 0, s = 0, mp = 0, sp = 0, ld = 0;
@@ -119,7 +122,10 @@ struct l0s_ctx {
         for (DBuf* b : all) b->release();
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
+        for (auto& e : cev)
+            if (e) cudaEventDestroy(e);
         if (st) cudaStreamDestroy(st);
+        if (cst) cudaStreamDestroy(cst);
     }
 };
 
@@ -281,7 +287,13 @@ int l0s_create(int device, l0s_ctx** out) {
         delete c;
         return fail(L0S_ECUDA, "stream creation failed");
     }
+    if (cudaStreamCreateWithFlags(&c->cst, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamDestroy(c->st);
+        delete c;
+        return fail(L0S_ECUDA, "stream creation failed");
+    }
     for (auto& e : c->ev) cudaEventCreate(&e);
+    for (auto& e : c->cev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     *out = c;
     return L0S_OK;
 }
@@ -329,19 +341,6 @@ static int stage_prepare(l0s_ctx* c, const double* values, int64_t m, int64_t s,
     c->sp = std::max<int64_t>(c->zoff_h[ntasks], 8);
     size_t wsz = precision == L0S_PREC_FP32 ? 4 : 8;
     cudaEventRecord(c->ev[0], c->st);
-    const double *vd = values, *yd = y;
-    const int64_t* pd = perm;
-    if (!is_device) {
-        CK(c->in_values.ensure(sizeof(double) * m * s));
-        CK(c->in_y.ensure(sizeof(double) * s));
-        CK(c->in_perm.ensure(sizeof(int64_t) * s));
-        CK(cudaMemcpyAsync(c->in_values.p, values, sizeof(double) * m * s, cudaMemcpyHostToDevice, c->st));
-        CK(cudaMemcpyAsync(c->in_y.p, y, sizeof(double) * s, cudaMemcpyHostToDevice, c->st));
-        CK(cudaMemcpyAsync(c->in_perm.p, perm, sizeof(int64_t) * s, cudaMemcpyHostToDevice, c->st));
-        vd = c->in_values.as<double>();
-        yd = c->in_y.as<double>();
-        pd = c->in_perm.as<int64_t>();
-    }
     CK(c->bounds_d.ensure(sizeof(int64_t) * (ntasks + 1)));
     CK(c->zoff_d.ensure(sizeof(int64_t) * (ntasks + 1)));
     CK(cudaMemcpyAsync(c->bounds_d.p, bounds, sizeof(int64_t) * (ntasks + 1), cudaMemcpyHostToDevice, c->st));
@@ -357,10 +356,9 @@ static int stage_prepare(l0s_ctx* c, const double* values, int64_t m, int64_t s,
     CK(c->eta_d.ensure(sizeof(double) * ntasks));
     CK(cudaMemcpyAsync(c->rowsd.p, c->rows_h.data(), sizeof(double) * ntasks, cudaMemcpyHostToDevice, c->st));
     CK(cudaMemcpyAsync(c->eta_d.p, c->eta_h.data(), sizeof(double) * ntasks, cudaMemcpyHostToDevice, c->st));
-    launch_gather(vd, yd, pd, m, s, precision, c->Xp.p, c->yp.p, c->st);
-    CK(cudaMemsetAsync(c->Z.p, 0, sizeof(double) * c->mp * c->sp, c->st));
-    launch_normalize(c->Xp.p, c->yp.p, precision, m, s, c->bounds_d.as<int64_t>(), c->zoff_d.as<int64_t>(), ntasks,
-                     c->sp, c->Z.as<double>(), c->qf.as<double>(), c->un2.as<double>(), c->yyu.as<double>(), c->st);
+    // rows past the property (m+1 .. mp-1) are Gram padding: zero; every other row of Z is
+    // written whole (task padding included) by the normalize kernel
+    CK(cudaMemsetAsync(c->Z.as<double>() + (m + 1) * c->sp, 0, sizeof(double) * (c->mp - m - 1) * c->sp, c->st));
     return L0S_OK;
 }
 
@@ -392,12 +390,76 @@ static int stage_post(l0s_ctx* c) {
     return L0S_OK;
 }
 
+// Inputs -> Z (the reference's _prepare plus centering / normalization), and -- with
+// gram_cols -- the Gram, overlapped with the transfer: host inputs travel in kChunks row
+// chunks (multiples of the Gram's 64-row blocks) on the copy stream while the compute stream
+// gathers and normalizes each chunk as it lands and computes every Gram block whose later
+// block-row it completes.  Only the last chunk's blocks remain after the copy.
+static int stage_fill(l0s_ctx* c, const double* values, const double* y, const int64_t* perm, int is_device,
+                      bool gram_cols) {
+    const int64_t m = c->m, s = c->s;
+    const int ntasks = c->T, precision = c->prec;
+    const double *vd = values, *yd = y;
+    const int64_t* pd = perm;
+    if (!is_device) {
+        CK(c->in_values.ensure(sizeof(double) * m * s));
+        CK(c->in_y.ensure(sizeof(double) * s));
+        CK(c->in_perm.ensure(sizeof(int64_t) * s));
+        CK(cudaMemcpyAsync(c->in_y.p, y, sizeof(double) * s, cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(c->in_perm.p, perm, sizeof(int64_t) * s, cudaMemcpyHostToDevice, c->st));
+        vd = c->in_values.as<double>();
+        yd = c->in_y.as<double>();
+        pd = c->in_perm.as<int64_t>();
+    }
+    auto rows_to_z = [&](int64_t f0, int64_t f1) {
+        launch_gather(vd, yd, pd, m, s, precision, c->Xp.p, c->yp.p, f0, f1, c->st);
+        launch_normalize(c->Xp.p, c->yp.p, precision, m, s, c->bounds_d.as<int64_t>(), c->zoff_d.as<int64_t>(),
+                         ntasks, c->sp, c->Z.as<double>(), c->qf.as<double>(), c->un2.as<double>(),
+                         c->yyu.as<double>(), f0, f1, c->st);
+    };
+    const int nb = (int)(c->mp / 64);
+    const bool chunked = !is_device && (double)m * (double)s * 8.0 >= 32.0 * (1 << 20) && m >= 2 * 64;
+    rows_to_z(m, m + 1);  // the property first: every Gram column block needs it
+    if (!chunked) {
+        if (!is_device)
+            CK(cudaMemcpyAsync(c->in_values.p, values, sizeof(double) * m * s, cudaMemcpyHostToDevice, c->st));
+        rows_to_z(0, m);
+        if (gram_cols) launch_gram_cols(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), ntasks, c->mp,
+                                        c->G.as<double>(), 0, nb, c->st);
+        return L0S_OK;
+    }
+    const int64_t R = (((m + l0s_ctx::kChunks - 1) / l0s_ctx::kChunks) + 63) / 64 * 64;
+    // the copy stream starts after everything queued so far (buffers may be in use by a search)
+    cudaEventRecord(c->cev[l0s_ctx::kChunks], c->st);
+    cudaStreamWaitEvent(c->cst, c->cev[l0s_ctx::kChunks], 0);
+    int k = 0;
+    for (int64_t r0 = 0; r0 < m; r0 += R, ++k) {
+        const int64_t r1 = std::min(m, r0 + R);
+        CK(cudaMemcpyAsync(c->in_values.as<double>() + r0 * s, values + r0 * s, sizeof(double) * (r1 - r0) * s,
+                           cudaMemcpyHostToDevice, c->cst));
+        cudaEventRecord(c->cev[k], c->cst);
+    }
+    k = 0;
+    for (int64_t r0 = 0; r0 < m; r0 += R, ++k) {
+        const int64_t r1 = std::min(m, r0 + R);
+        cudaStreamWaitEvent(c->st, c->cev[k], 0);
+        rows_to_z(r0, r1);
+        if (gram_cols) {
+            const int B0 = (int)(r0 / 64), B1 = r1 >= m ? nb : (int)(r1 / 64);
+            launch_gram_cols(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), ntasks, c->mp, c->G.as<double>(),
+                             B0, B1, c->st);
+        }
+    }
+    return L0S_OK;
+}
+
 int l0s_stage(l0s_ctx* c, const double* values, int64_t m, int64_t s, const double* y, const int64_t* perm,
               const int64_t* bounds, int ntasks, int precision, int is_device) {
     int rc = stage_prepare(c, values, m, s, y, perm, bounds, ntasks, precision, is_device);
     if (rc) return rc;
-    launch_gram(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), ntasks, c->mp, c->G.as<double>(), 0, 1, nullptr,
-                c->st);
+    rc = stage_fill(c, values, y, perm, is_device, true);
+    if (rc) return rc;
+    CK(cudaGetLastError());
     return stage_post(c);
 }
 
@@ -415,8 +477,11 @@ int l0s_stage_shard(l0s_ctx* c, const double* values, int64_t m, int64_t s, cons
     if (nshards > 1 && !pack) return fail(L0S_EINVAL, "pack buffer required for nshards > 1");
     int rc = stage_prepare(c, values, m, s, y, perm, bounds, ntasks, precision, is_device);
     if (rc) return rc;
-    launch_gram(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), ntasks, c->mp, c->G.as<double>(), shard, nshards,
-                pack, c->st);
+    rc = stage_fill(c, values, y, perm, is_device, nshards == 1);
+    if (rc) return rc;
+    if (nshards > 1)
+        launch_gram(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), ntasks, c->mp, c->G.as<double>(), shard,
+                    nshards, pack, c->st);
     CK(cudaGetLastError());
     if (nshards == 1) return stage_post(c);
     CK(cudaStreamSynchronize(c->st));  // the pack is complete for the caller's all-gather

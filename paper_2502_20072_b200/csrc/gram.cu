@@ -42,14 +42,26 @@ __device__ __forceinline__ void gram_block(int64_t g, int nb, int& task, int& ba
 // Z columns [zoff[t], zoff[t+1]) and G + t mp^2.  pack == nullptr: write G (both triangles);
 // otherwise write block g - g0 as a row-major 64 x 64 tile at pack + (g - g0) * 4096 (a shard
 // of the multi-GPU Gram, exchanged by all-gather and scattered by k_gram_unpack).
+// colmajor != 0: blockIdx.y is the task and g0 + blockIdx.x indexes that task's upper-triangle
+// blocks column by column (bb outer, ba = 0..bb inner), so a range of column block-rows is a
+// contiguous range of blocks.
 __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int64_t sp,
                                               const int64_t* __restrict__ zoff, int nb, double* __restrict__ Gall,
-                                              int64_t mp, int64_t g0, double* __restrict__ pack) {
+                                              int64_t mp, int64_t g0, double* __restrict__ pack, int colmajor) {
     extern __shared__ __align__(16) double gsm[];
     double* sA[2] = {gsm, gsm + BM * LDS};
     double* sB[2] = {gsm + 2 * BM * LDS, gsm + 3 * BM * LDS};
     int task, ba, bb;
-    gram_block(g0 + blockIdx.x, nb, task, ba, bb);
+    if (colmajor) {
+        task = blockIdx.y;
+        const int64_t g = g0 + blockIdx.x;
+        bb = (int)((sqrt(8.0 * (double)g + 1.0) - 1.0) * 0.5);
+        while ((int64_t)(bb + 1) * (bb + 2) / 2 <= g) ++bb;
+        while ((int64_t)bb * (bb + 1) / 2 > g) --bb;
+        ba = (int)(g - (int64_t)bb * (bb + 1) / 2);
+    } else {
+        gram_block(g0 + blockIdx.x, nb, task, ba, bb);
+    }
     const int64_t k0 = zoff[task], klen = zoff[task + 1] - k0;
     double* G = Gall + (int64_t)task * mp * mp;
     const double* Za = Z + (int64_t)ba * BM * sp + k0;
@@ -202,7 +214,19 @@ void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_d, int T, int6
         g0 = std::min<int64_t>(total, per * shard);
         cnt = std::min<int64_t>(total, g0 + per) - g0;
     }
-    if (cnt > 0) k_gram<<<(unsigned)cnt, 256, smem, st>>>(Z, sp, zoff_d, nb, G, mp, g0, nshards > 1 ? pack : nullptr);
+    if (cnt > 0)
+        k_gram<<<(unsigned)cnt, 256, smem, st>>>(Z, sp, zoff_d, nb, G, mp, g0, nshards > 1 ? pack : nullptr, 0);
+}
+
+void launch_gram_cols(const double* Z, int64_t sp, const int64_t* zoff_d, int T, int64_t mp, double* G, int B0,
+                      int B1, cudaStream_t st) {
+    const int nb = (int)(mp / BM);
+    if (B1 > nb) B1 = nb;
+    if (B1 <= B0) return;
+    const int64_t g0 = (int64_t)B0 * (B0 + 1) / 2, g1 = (int64_t)B1 * (B1 + 1) / 2;
+    const int smem = 4 * BM * LDS * (int)sizeof(double);
+    cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_gram<<<dim3((unsigned)(g1 - g0), (unsigned)T), 256, smem, st>>>(Z, sp, zoff_d, nb, G, mp, g0, nullptr, 1);
 }
 
 void launch_gram_unpack(const double* recv, int T, int64_t mp, double* G, cudaStream_t st) {

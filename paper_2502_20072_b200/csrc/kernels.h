@@ -11,14 +11,15 @@ namespace l0s {
 // ---- staging (stage.cu) ----
 // Gather + cast (search._prepare, search.py:113-127): Xp[f][i] = W(values[f][perm[i]]),
 // yp[i] = W(y[perm[i]]), W = double (fp64) or float (fp32).
+// rows [f0, f1) of [0, m] (row m = the property)
 void launch_gather(const double* values, const double* y, const int64_t* perm, int64_t m, int64_t s,
-                   int precision, void* Xp, void* yp, cudaStream_t st);
+                   int precision, void* Xp, void* yp, int64_t f0, int64_t f1, cudaStream_t st);
 // Per (feature, task): center, normalize, write Z rows (features 0..m-1 unit-norm
 // centered, row m = centered y), plus q = |x_c|^2/|x|^2 and |x|^2 per (task, feature)
 // and |y|^2 per task.
 void launch_normalize(const void* Xp, const void* yp, int precision, int64_t m, int64_t s,
                       const int64_t* bounds_d, const int64_t* zoff_d, int T, int64_t sp, double* Z,
-                      double* qf, double* un2, double* yyu, cudaStream_t st);
+                      double* qf, double* un2, double* yyu, int64_t f0, int64_t f1, cudaStream_t st);
 
 // rho, dead, rho_cap, iforce from qf / un2 (stage.cu), and NaN rows/cols of dead features in G
 void launch_feature_flags(const double* qf, const double* un2, const double* rows, int64_t m, int64_t mp, int T,
@@ -35,6 +36,10 @@ int64_t gram_shard_blocks(int64_t mp, int T, int nshards);
 void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_d, int T, int64_t mp, double* G, int shard,
                  int nshards, double* pack, cudaStream_t st);
 void launch_gram_unpack(const double* recv, int T, int64_t mp, double* G, cudaStream_t st);
+// Blocks of every task whose column block-row bb lies in [B0, B1) (bb >= ba): the part of the
+// Gram that becomes computable once Z's block-rows < B1 are staged (overlapped stage).
+void launch_gram_cols(const double* Z, int64_t sp, const int64_t* zoff_d, int T, int64_t mp, double* G, int B0,
+                      int B1, cudaStream_t st);
 // diagonal of the feature rows := 1 (unit-norm columns; NaN rows stay NaN)
 void launch_unit_diag(double* G, int T, int64_t m, int64_t mp, cudaStream_t st);
 // Features the reference's rank rule rejects in every tuple: NaN their Gram row and column (all tasks).

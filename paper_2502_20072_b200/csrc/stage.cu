@@ -9,11 +9,12 @@
 
 namespace l0s {
 
+// rows f0 + blockIdx.y (row m is the property)
 template <typename W>
 __global__ void k_gather(const double* __restrict__ values, const double* __restrict__ y,
                          const int64_t* __restrict__ perm, int64_t m, int64_t s, W* __restrict__ Xp,
-                         W* __restrict__ yp) {
-    int64_t f = blockIdx.y;
+                         W* __restrict__ yp, int64_t f0) {
+    int64_t f = f0 + blockIdx.y;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t src = perm[i];
         if (f < m)
@@ -29,17 +30,17 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// One warp per (row, task); row m is the property.
+// One warp per (row, task) of rows [f0, f1); row m is the property.
 template <typename W>
 __global__ void k_normalize(const W* __restrict__ Xp, const W* __restrict__ yp, int64_t m, int64_t s,
                             const int64_t* __restrict__ bounds, const int64_t* __restrict__ zoff, int T,
                             int64_t sp, double* __restrict__ Z, double* __restrict__ qf,
-                            double* __restrict__ un2, double* __restrict__ yyu) {
+                            double* __restrict__ un2, double* __restrict__ yyu, int64_t f0, int64_t f1) {
     int lane = threadIdx.x & 31;
     int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (wid >= (m + 1) * T) return;
+    if (wid >= (f1 - f0) * T) return;
     int t = (int)(wid % T);
-    int64_t f = wid / T;
+    int64_t f = f0 + wid / T;
     int64_t lo = bounds[t], r = bounds[t + 1] - lo;
     const W* src = (f < m) ? Xp + f * s + lo : yp + lo;
     double sum = 0.0;
@@ -184,25 +185,27 @@ void launch_feature_flags(const double* qf, const double* un2, const double* row
 }
 
 void launch_gather(const double* values, const double* y, const int64_t* perm, int64_t m, int64_t s,
-                   int precision, void* Xp, void* yp, cudaStream_t st) {
-    dim3 grid((unsigned)((s + 255) / 256 < 64 ? (s + 255) / 256 : 64), (unsigned)(m + 1));
+                   int precision, void* Xp, void* yp, int64_t f0, int64_t f1, cudaStream_t st) {
+    if (f1 <= f0) return;
+    dim3 grid((unsigned)((s + 255) / 256 < 64 ? (s + 255) / 256 : 64), (unsigned)(f1 - f0));
     if (precision == 1)
-        k_gather<float><<<grid, 256, 0, st>>>(values, y, perm, m, s, (float*)Xp, (float*)yp);
+        k_gather<float><<<grid, 256, 0, st>>>(values, y, perm, m, s, (float*)Xp, (float*)yp, f0);
     else
-        k_gather<double><<<grid, 256, 0, st>>>(values, y, perm, m, s, (double*)Xp, (double*)yp);
+        k_gather<double><<<grid, 256, 0, st>>>(values, y, perm, m, s, (double*)Xp, (double*)yp, f0);
 }
 
 void launch_normalize(const void* Xp, const void* yp, int precision, int64_t m, int64_t s,
                       const int64_t* bounds_d, const int64_t* zoff_d, int T, int64_t sp, double* Z,
-                      double* qf, double* un2, double* yyu, cudaStream_t st) {
-    int64_t warps = (m + 1) * T;
+                      double* qf, double* un2, double* yyu, int64_t f0, int64_t f1, cudaStream_t st) {
+    if (f1 <= f0) return;
+    int64_t warps = (f1 - f0) * T;
     unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
     if (precision == 1)
         k_normalize<float><<<blocks, 256, 0, st>>>((const float*)Xp, (const float*)yp, m, s, bounds_d, zoff_d, T,
-                                                   sp, Z, qf, un2, yyu);
+                                                   sp, Z, qf, un2, yyu, f0, f1);
     else
         k_normalize<double><<<blocks, 256, 0, st>>>((const double*)Xp, (const double*)yp, m, s, bounds_d, zoff_d,
-                                                    T, sp, Z, qf, un2, yyu);
+                                                    T, sp, Z, qf, un2, yyu, f0, f1);
 }
 
 }  // namespace l0s
