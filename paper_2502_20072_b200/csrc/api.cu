@@ -105,7 +105,7 @@ struct l0s_ctx {
     int binom_n = -1;
     int64_t binom_m = -1;
     // search workspace
-    DBuf units, ucount, theta_g, hist, wl_lb, wl_rank, wl_cnt, ill, ill_cnt, cand_lb, cand_rank, cand_cnt, sort_tmp,
+    DBuf units, ucount, theta_g, hist, seedbuf, wl_lb, wl_rank, wl_cnt, ill, ill_cnt, cand_lb, cand_rank, cand_cnt, sort_tmp,
         lb_tmp, rank_tmp, coll_lb, coll_rank, coll_cnt;
     DBuf ex_scratch, ex_ssr_tmp, ex_ok_tmp, ex_ok, ex_score, ex_coef, ex_ssr, ex_ranks, ex_tuples;
     DBuf qr_ssr, qr_ratio, qr_score, qr_minr;
@@ -115,7 +115,7 @@ struct l0s_ctx {
 
     ~l0s_ctx() {
         DBuf* all[] = {&in_values, &in_y, &in_perm, &bounds_d, &zoff_d, &Xp, &yp, &Z, &G, &qf, &un2, &yyu, &rowsd,
-                       &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &umin, &binom, &units, &ucount, &theta_g, &hist, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
+                       &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &umin, &binom, &units, &ucount, &theta_g, &hist, &seedbuf, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
                        &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
                        &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr};
@@ -755,6 +755,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     CK(c->ucount.ensure(sizeof(int) * 4));
     CK(c->theta_g.ensure(sizeof(unsigned long long)));
     CK(c->hist.ensure(sizeof(unsigned) * HIST_BINS));
+    CK(c->seedbuf.ensure(sizeof(int64_t) * 1024 * 5 + 64));
     CK(c->wl_lb.ensure(sizeof(double) * slots * kc));
     CK(c->wl_rank.ensure(sizeof(int64_t) * slots * kc));
     CK(c->wl_cnt.ensure(sizeof(int) * slots));
@@ -782,6 +783,9 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     a.theta0 = INFINITY;
     a.theta_g = c->theta_g.as<unsigned long long>();
     a.hist = c->hist.as<unsigned>();
+    a.seed_tup = c->seedbuf.as<int64_t>();
+    a.seed_ub = c->seedbuf.as<double>() + 1024 * 4;
+    a.seed_n = reinterpret_cast<int*>(c->seedbuf.as<double>() + 1024 * 5);
     {
         double yy_top = 0.0;  // uncentered total |y|^2 >= every pooled bound
         for (double v : c->yyu_h) yy_top += v;
@@ -804,7 +808,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     cudaEventRecord(c->ev[3], c->st);
     CK(cudaGetLastError());
     st->n_fit_launches++;
-    st->n_launches += 2;  // threshold seed + sweep
+    st->n_launches += 4;  // threshold seed (select, eval, commit) + sweep
     launch_gather_candidates(a.wl_lb, a.wl_rank, a.wl_cnt, slots, kc, a.theta_g, c->cand_lb.as<double>(),
                              c->cand_rank.as<int64_t>(), c->cand_cnt.as<unsigned long long>(), c->st);
     st->n_launches++;

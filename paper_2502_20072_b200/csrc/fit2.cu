@@ -150,16 +150,12 @@ __global__ void __launch_bounds__(256, 2) k_fit2(const __grid_constant__ FitArgs
     flush_warp(a, wc, blockIdx.x * NW + warp, lane);
 }
 
-__global__ void __launch_bounds__(256, 1) k_seed2(const __grid_constant__ FitArgs a) {
-    __shared__ SeedSmem S;
-    const int ns = seed_subsets<2, 16>(a, S);
-    for (int c = threadIdx.x; c < ns; c += blockDim.x) {
-        int64_t f[2];
-        double lb = 0.0, ub = INFINITY;
-        const int fl = seed_tuple<2>(a, S, c, f) ? eval_tuple2(a, f[0], f[1], &lb, &ub) : 0;
-        S.ub[c] = (fl == 3 && ub == ub) ? ub : INFINITY;
-    }
-    seed_commit(a, S, ns);
+__global__ void __launch_bounds__(128) k_seed_eval2(const __grid_constant__ FitArgs a) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= *a.seed_n) return;
+    double lb = 0.0, ub = INFINITY;
+    const int fl = a.seed_tup[c * 4] >= 0 ? eval_tuple2(a, a.seed_tup[c * 4 + 0], a.seed_tup[c * 4 + 1], &lb, &ub) : 0;
+    a.seed_ub[c] = (fl == 3 && ub == ub) ? ub : INFINITY;
 }
 
 __global__ void k_screen2(const __grid_constant__ FitArgs a, const int64_t* __restrict__ tuples, int64_t count,
@@ -179,7 +175,7 @@ int launch2(const FitArgs& a, int nsm, cudaStream_t st) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit2<NT>, 256, kSmem2);
     const int grid = nsm * (per_sm < 1 ? 1 : per_sm);
-    if (!a.collect) k_seed2<<<1, 256, 0, st>>>(a);
+    if (!a.collect) seed_launch<2, 24>(k_seed_eval2, a, st);
     k_fit2<NT><<<grid, 256, kSmem2, st>>>(a);
     return grid;
 }

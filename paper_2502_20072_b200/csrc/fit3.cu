@@ -423,16 +423,12 @@ __global__ void k_screen3(const __grid_constant__ FitArgs a, const int64_t* __re
     out_lb[c] = lb;
 }
 
-__global__ void __launch_bounds__(256, 1) k_seed3(const __grid_constant__ FitArgs a) {
-    __shared__ SeedSmem S;
-    const int ns = seed_subsets<3, 16>(a, S);
-    for (int c = threadIdx.x; c < ns; c += blockDim.x) {
-        int64_t f[3];
-        double lb = 0.0, ub = INFINITY;
-        const int fl = seed_tuple<3>(a, S, c, f) ? eval_tuple3(a, f[0], f[1], f[2], &lb, &ub) : 0;
-        S.ub[c] = (fl == 3 && ub == ub) ? ub : INFINITY;
-    }
-    seed_commit(a, S, ns);
+__global__ void __launch_bounds__(128) k_seed_eval3(const __grid_constant__ FitArgs a) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= *a.seed_n) return;
+    double lb = 0.0, ub = INFINITY;
+    const int fl = a.seed_tup[c * 4] >= 0 ? eval_tuple3(a, a.seed_tup[c * 4 + 0], a.seed_tup[c * 4 + 1], a.seed_tup[c * 4 + 2], &lb, &ub) : 0;
+    a.seed_ub[c] = (fl == 3 && ub == ub) ? ub : INFINITY;
 }
 
 template <int NT>
@@ -448,7 +444,7 @@ int launch_nt(const FitArgs& a0, int nsm, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, 256, C::smem_bytes);
     if (per_sm < 1) per_sm = 1;
     int grid = nsm * per_sm;
-    if (!a.collect) k_seed3<<<1, 256, 0, st>>>(a);
+    if (!a.collect) seed_launch<3, 18>(k_seed_eval3, a, st);
     k_fit3<NT><<<grid, 256, C::smem_bytes, st>>>(a);
     return grid;
 }

@@ -312,22 +312,18 @@ int occupancy4(int nsm) {
     return nsm * (per_sm < 1 ? 1 : per_sm);
 }
 
-__global__ void __launch_bounds__(256, 1) k_seed4(const __grid_constant__ FitArgs a) {
-    __shared__ SeedSmem S;
-    const int ns = seed_subsets<4, 12>(a, S);
-    for (int c = threadIdx.x; c < ns; c += blockDim.x) {
-        int64_t f[4];
-        double lb = 0.0, ub = INFINITY;
-        const int fl = seed_tuple<4>(a, S, c, f) ? eval_tuple4(a, f[0], f[1], f[2], f[3], &lb, &ub) : 0;
-        S.ub[c] = (fl == 3 && ub == ub) ? ub : INFINITY;
-    }
-    seed_commit(a, S, ns);
+__global__ void __launch_bounds__(128) k_seed_eval4(const __grid_constant__ FitArgs a) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= *a.seed_n) return;
+    double lb = 0.0, ub = INFINITY;
+    const int fl = a.seed_tup[c * 4] >= 0 ? eval_tuple4(a, a.seed_tup[c * 4 + 0], a.seed_tup[c * 4 + 1], a.seed_tup[c * 4 + 2], a.seed_tup[c * 4 + 3], &lb, &ub) : 0;
+    a.seed_ub[c] = (fl == 3 && ub == ub) ? ub : INFINITY;
 }
 
 template <int NT>
 int launch4(const FitArgs& a, int nsm, cudaStream_t st) {
     const int grid = occupancy4<NT>(nsm);
-    if (!a.collect) k_seed4<<<1, 256, 0, st>>>(a);
+    if (!a.collect) seed_launch<4, 12>(k_seed_eval4, a, st);
     k_fit4<NT><<<grid, 256, Cfg4<NT>::smem_bytes, st>>>(a);
     return grid;
 }

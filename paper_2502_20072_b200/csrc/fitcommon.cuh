@@ -275,12 +275,13 @@ __device__ __forceinline__ void drain_pending(const FitArgs& a, unsigned (&pend)
 // over all tuples, so it is a valid starting threshold: the sweep's first tiles then drop the
 // hopeless tuples instead of sending every one of them through the slow path.
 constexpr int SEED_MAX = 1024;
+constexpr int SEED_POOL = 16384;  // candidate features of the seed (dynamic smem doubles)
 struct SeedSmem {
     double ub[SEED_MAX];
     short sub[SEED_MAX][4];
-    int top[16];
-    double rv[8];
-    int ri[8];
+    int top[32];
+    double rv[32];
+    int ri[32];
     int nsub;
 };
 
@@ -291,23 +292,27 @@ __device__ int seed_subsets(const FitArgs& a, SeedSmem& S) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t m = a.m, mp = a.mp;
     if (m < F) return 0;
+    // pooled single-feature scores of the first SEED_POOL features, once, into shared memory
+    // (dynamic, SEED_POOL doubles); the F selection rounds then only scan shared memory
+    extern __shared__ double s_score[];
+    const int pool = (int)(m < SEED_POOL ? m : SEED_POOL);
+    for (int f = tid; f < pool; f += blockDim.x) {
+        double sc = 0.0;
+        for (int t = 0; t < a.T; ++t) {
+            const double c = a.G[(int64_t)t * mp * mp + m * mp + f];
+            sc = fma(c, c, sc);
+        }
+        s_score[f] = sc;  // NaN (dead feature) never wins a comparison
+    }
+    __syncthreads();
     for (int r = 0; r < F; ++r) {
         double best = -1.0;
         int bi = -1;
-        for (int f = tid; f < m; f += blockDim.x) {
-            bool taken = false;
-            for (int q = 0; q < r; ++q) taken |= S.top[q] == f;
-            if (taken) continue;
-            double sc = 0.0;
-            for (int t = 0; t < a.T; ++t) {
-                const double c = a.G[(int64_t)t * mp * mp + m * mp + f];
-                sc = fma(c, c, sc);
-            }
-            if (sc > best) {  // NaN (dead feature) never wins
-                best = sc;
+        for (int f = tid; f < pool; f += blockDim.x)
+            if (s_score[f] > best) {
+                best = s_score[f];
                 bi = f;
             }
-        }
         for (int o = 16; o > 0; o >>= 1) {
             const double ov = __shfl_down_sync(L0S_FULL, best, o);
             const int oi = __shfl_down_sync(L0S_FULL, bi, o);
@@ -328,6 +333,7 @@ __device__ int seed_subsets(const FitArgs& a, SeedSmem& S) {
                     S.ri[0] = S.ri[w];
                 }
             S.top[r] = S.ri[0];
+            if (S.ri[0] >= 0) s_score[S.ri[0]] = -1.0;  // taken
         }
         __syncthreads();
     }
@@ -369,14 +375,31 @@ __device__ __forceinline__ bool seed_tuple(const FitArgs& a, const SeedSmem& S, 
     return !a.ranged || (rk >= a.rank_lo && rk < a.rank_hi);
 }
 
-// Phase 3: the kc-th smallest upper bound becomes the starting threshold.
-__device__ __forceinline__ void seed_commit(const FitArgs& a, SeedSmem& S, int ns) {
+namespace {
+// Seed phase 1 (one CTA of 512): the subsets, written to a.seed_tup (-1: outside the rank range).
+template <int N, int F>
+__global__ void __launch_bounds__(512, 1) k_seed_select(const __grid_constant__ FitArgs a) {
+    __shared__ SeedSmem S;
+    const int ns = seed_subsets<N, F>(a, S);
+    for (int c = threadIdx.x; c < ns; c += blockDim.x) {
+        int64_t f[N];
+        const bool in = seed_tuple<N>(a, S, c, f);
+        for (int x = 0; x < N; ++x) a.seed_tup[c * 4 + x] = in ? f[x] : -1;
+    }
+    if (threadIdx.x == 0) *a.seed_n = ns;
+}
+
+// Seed phase 3 (one CTA of 512): the kc-th smallest upper bound becomes the starting threshold.
+__global__ void __launch_bounds__(512, 1) k_seed_commit(const __grid_constant__ FitArgs a) {
+    __shared__ double ub[SEED_MAX];
+    const int ns = *a.seed_n;
+    for (int c = threadIdx.x; c < ns; c += blockDim.x) ub[c] = a.seed_ub[c];
     __syncthreads();
     for (int c = threadIdx.x; c < ns; c += blockDim.x) {
-        const double v = S.ub[c];
+        const double v = ub[c];
         int pos = 0;
         for (int x = 0; x < ns; ++x) {
-            const double u = S.ub[x];
+            const double u = ub[x];
             pos += (u < v || (u == v && x < c)) ? 1 : 0;
         }
         if (pos == a.kc - 1 && v < INFINITY) {
@@ -384,6 +407,18 @@ __device__ __forceinline__ void seed_commit(const FitArgs& a, SeedSmem& S, int n
             atomicMin(a.theta_g, ord_enc(th));
         }
     }
+}
+}  // namespace
+
+// Phase 2 is the dimension's own eval kernel (one thread per subset, grid over SEED_MAX):
+//   k_seed_evalN: a.seed_ub[c] = upper bound of subset c if certified, else +inf.
+template <int N, int F, typename E>
+inline void seed_launch(E eval_kernel, const FitArgs& a, cudaStream_t st) {
+    const int bytes = (int)(sizeof(double) * (a.m < SEED_POOL ? a.m : SEED_POOL));
+    cudaFuncSetAttribute(k_seed_select<N, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    k_seed_select<N, F><<<1, 512, bytes, st>>>(a);
+    eval_kernel<<<SEED_MAX / 128, 128, 0, st>>>(a);
+    k_seed_commit<<<1, 512, 0, st>>>(a);
 }
 
 // End of the persistent loop: write the warp's list (or flush the collect buffer).

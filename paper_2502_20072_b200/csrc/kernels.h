@@ -137,6 +137,9 @@ struct FitArgs {
     double theta0;
     unsigned long long* theta_g;
     unsigned* hist;          // [HIST_BINS] global lower-bound histogram (fitcommon.cuh)
+    int64_t* seed_tup;       // [SEED_MAX][4] threshold-seed subsets (fitcommon.cuh)
+    double* seed_ub;         // [SEED_MAX] their upper bounds
+    int* seed_n;             // subset count
     int hist_base;           // bin offset: (biased exponent of the top) - HIST_EXP, times HIST_SUB
     double* wl_lb;           // [n_warp_slots][kc]
     int64_t* wl_rank;
