@@ -229,7 +229,7 @@ def main():
     for _ in range(args.warmup):
         device_step()
     barrier()
-    ms_steps, fit_ms, launches = [], [], 0
+    ms_steps, fit_ms, gram_ms, launches = [], [], [], 0
     # gather, normalize, gram, unit_diag, 5 feature-flag kernels (+ the shard unpack for N > 1)
     stage_launches = 9 + (1 if world > 1 else 0)
     with ClockSampler(local) as clk:
@@ -237,6 +237,7 @@ def main():
         for _ in range(args.steps):
             st, sc, rk = device_step()
             ms_steps.append(st.ms_gram + st.ms_total)
+            gram_ms.append(st.ms_gram_kernel)
             fit_ms.append(st.ms_fit / max(1, st.n_fit_launches))
             launches += int(st.n_launches) + stage_launches
         barrier()
@@ -305,6 +306,9 @@ def main():
     flops_per_launch = (hi - lo) * T * F_TASK[N_DIM]
     fit_avg = statistics.mean(fit_ms)
     achieved = flops_per_launch / (fit_avg * 1e-3) / 1e12
+    # secondary roofline: the Gram on the FP64 tensor path (DMMA), F_gram = m (m + 3) s
+    gram_avg = statistics.mean(gram_ms) if gram_ms and min(gram_ms) > 0 else None
+    gram_tf = (M * (M + 3) * S) / (gram_avg * 1e-3) / 1e12 if gram_avg else None
     prof = os.path.join(ROOT, "profiles", "fit3_traffic.json")
     traffic, pipe = None, None
     if os.path.exists(prof):
@@ -325,9 +329,15 @@ def main():
                      "kernel": "k_fit3<4>", "flops_per_tuple": T * F_TASK[N_DIM],
                      "peak_source": "measured DFMA microbenchmark (l0s_fp64_peak); datasheet 37 TF/s",
                      "physical_fp64_pipe_frac": pipe,
-                     "note": "achieved counts SURVEY 8(d)'s normal-equations flops per tuple; the kernel hoists the "
-                             "(j,k) LDL^T out of the i sweep and does ~8 FP64 ops per task-tuple, so the algorithmic "
-                             "frac exceeds 1 while the FP64 pipe is physical_fp64_pipe_frac busy (ncu)"},
+                     "note": "achieved counts SURVEY 8(d)'s normal-equations flops per tuple (216 at T=4) for every "
+                             "tuple; the kernel hoists the (j,k) LDL^T out of the i sweep (~6.5 FP64 ops per "
+                             "task-tuple) and prunes a row group after its first task once that task alone bounds "
+                             "the pooled SSR above the threshold, so the algorithmic frac exceeds 1; the FP64 pipe "
+                             "is physical_fp64_pipe_frac busy (ncu, profiles/)"},
+        "roofline_gram": {"bound": "fp64 tensor (DMMA.8x8x4)", "kernel": "k_gram",
+                          "achieved": gram_tf, "peak": peak, "unit": "TFLOP/s",
+                          "frac": (gram_tf / peak) if gram_tf else None, "ms": gram_avg,
+                          "flops": M * (M + 3) * S},
         "e2e": {"value": e2e_value, "unit": "tuples/s", "h2d_bytes_per_step": int(v.nbytes + y.nbytes + perm.nbytes
                                                                                   + bounds.nbytes),
                 "d2h_bytes_per_step": int(10 * (8 + 8 + T * (N_DIM + 1) * 8 + T * 8))},

@@ -69,6 +69,7 @@ typedef struct {
     double margin;           /* lb(K')-th minus k-th exact score at certification     */
     double ms_qr;            /* QR screen of the uncertifiable tuples                 */
     int64_t n_ill_refit;     /* of those, refit bit-exactly                           */
+    double ms_gram_kernel;   /* the Gram kernel alone (device-resident, unchunked stage) */
 } l0s_stats;
 
 const char *l0s_last_error(void);

@@ -52,6 +52,7 @@ class Stats(ctypes.Structure):
         ("margin", ctypes.c_double),
         ("ms_qr", ctypes.c_double),
         ("n_ill_refit", ctypes.c_int64),
+        ("ms_gram_kernel", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -96,10 +96,12 @@ struct l0s_ctx {
     std::vector<int64_t> bounds_h, zoff_h, rpad_h;
     std::vector<double> rows_h, eta_h, yyu_h;
     double ms_gram = 0.0;
+    double ms_gram_k = 0.0;  // the Gram kernel alone (unchunked stage)
     DBuf in_values, in_y, in_perm, bounds_d, zoff_d, Xp, yp, Z, G, qf, un2, yyu, rowsd, eta_d;
     DBuf rho, rho_cap, ynorm, iforce, dead, umin;
     int64_t n_dead = 0, n_iforce = 0;
     bool shard_pending = false;  // l0s_stage_shard done, l0s_stage_finish due
+    bool gram_timed = false;     // ev[2..3] bracket the Gram kernel of this stage
     // binomial table (k <= binom_n) x (a <= m)
     DBuf binom;
     int binom_n = -1;
@@ -385,6 +387,8 @@ static int stage_post(l0s_ctx* c) {
     CK(cudaMemcpyAsync(c->yyu_h.data(), c->yyu.p, sizeof(double) * ntasks, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     c->ms_gram = elapsed(c->ev[0], c->ev[1]);
+    c->ms_gram_k = c->gram_timed ? elapsed(c->ev[2], c->ev[3]) : 0.0;
+    c->gram_timed = false;
     c->staged = true;
     c->binom_m = -1;
     return L0S_OK;
@@ -424,8 +428,13 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
         if (!is_device)
             CK(cudaMemcpyAsync(c->in_values.p, values, sizeof(double) * m * s, cudaMemcpyHostToDevice, c->st));
         rows_to_z(0, m);
-        if (gram_cols) launch_gram_cols(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), ntasks, c->mp,
-                                        c->G.as<double>(), 0, nb, c->st);
+        if (gram_cols) {
+            cudaEventRecord(c->ev[2], c->st);
+            launch_gram_cols(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), ntasks, c->mp, c->G.as<double>(), 0,
+                             nb, c->st);
+            cudaEventRecord(c->ev[3], c->st);
+            c->gram_timed = true;
+        }
         return L0S_OK;
     }
     const int64_t R = (((m + l0s_ctx::kChunks - 1) / l0s_ctx::kChunks) + 63) / 64 * 64;
@@ -922,6 +931,7 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
     int64_t rb = std::max<int64_t>(rank_begin, 0), re = std::min<int64_t>(rank_end, N);
     st->n_tuples = std::max<int64_t>(re - rb, 0);
     st->ms_gram = c->ms_gram;
+    st->ms_gram_kernel = c->ms_gram_k;
     if (rb >= re) return L0S_OK;
     rc = ensure_binom(c, n);
     c->recs.clear();
