@@ -8,6 +8,7 @@
 // Warp tile 16x32 = 2x4 m8n8 fragments; every k4 step issues 8
 // mma.sync.m8n8k4.f64 (SASS: DMMA.8x8x4) from 6 conflict-free LDS.64.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -45,9 +46,12 @@ __device__ __forceinline__ void gram_block(int64_t g, int nb, int& task, int& ba
 // colmajor != 0: blockIdx.y is the task and g0 + blockIdx.x indexes that task's upper-triangle
 // blocks column by column (bb outer, ba = 0..bb inner), so a range of column block-rows is a
 // contiguous range of blocks.
-__global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int64_t sp,
-                                              const int64_t* __restrict__ zoff, int nb, double* __restrict__ Gall,
-                                              int64_t mp, int64_t g0, double* __restrict__ pack, int colmajor) {
+// NW warps (8: warp tile 16 x 32, 4: warp tile 32 x 32 with twice the accumulators per warp)
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_gram(const double* __restrict__ Z, int64_t sp,
+                                                  const int64_t* __restrict__ zoff, int nb, double* __restrict__ Gall,
+                                                  int64_t mp, int64_t g0, double* __restrict__ pack, int colmajor) {
+    constexpr int FA = 64 / (NW / 2) / 8;  // row fragments per warp
     extern __shared__ __align__(16) double gsm[];
     double* sA[2] = {gsm, gsm + BM * LDS};
     double* sB[2] = {gsm + 2 * BM * LDS, gsm + 3 * BM * LDS};
@@ -74,7 +78,7 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int6
         int valid = (int)((klen - kc) < BK ? (klen - kc) : BK);  // multiple of 8
         // 64 rows x (valid/2) 16-byte pieces per operand
         int pieces = BM * (valid / 2);
-        for (int p = tid; p < 2 * pieces; p += 256) {
+        for (int p = tid; p < 2 * pieces; p += NW * 32) {
             int which = p >= pieces;
             int q = which ? p - pieces : p;
             int row = q / (valid / 2), col = (q % (valid / 2)) * 2;
@@ -85,13 +89,13 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int6
         cp_async_commit();
     };
 
-    double acc[2][4][2];
+    double acc[FA][4][2];
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+    for (int a = 0; a < FA; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-    int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
+    int r0 = (warp >> 1) * (8 * FA), c0 = (warp & 1) * 32;
     int fr = lane >> 2, fk = lane & 3;
     load(0, 0);
     for (int c = 0; c < nchunks; ++c) {
@@ -108,23 +112,22 @@ __global__ void __launch_bounds__(256) k_gram(const double* __restrict__ Z, int6
         const double* A = sA[buf];
         const double* B = sB[buf];
         for (int kk = 0; kk < valid; kk += 4) {
-            double a0 = A[(r0 + fr) * LDS + kk + fk];
-            double a1 = A[(r0 + 8 + fr) * LDS + kk + fk];
-            double b[4];
+            double av[FA], b[4];
+#pragma unroll
+            for (int a = 0; a < FA; ++a) av[a] = A[(r0 + a * 8 + fr) * LDS + kk + fk];
 #pragma unroll
             for (int j = 0; j < 4; ++j) b[j] = B[(c0 + j * 8 + fr) * LDS + kk + fk];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                dmma(acc[0][j][0], acc[0][j][1], a0, b[j]);
-                dmma(acc[1][j][0], acc[1][j][1], a1, b[j]);
-            }
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int a = 0; a < FA; ++a) dmma(acc[a][j][0], acc[a][j][1], av[a], b[j]);
         }
         __syncthreads();
     }
     // epilogue: fragment (row = lane/4, col = 2*(lane%4) + v)
     double* P = pack ? pack + (int64_t)blockIdx.x * (BM * BM) : nullptr;
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+    for (int a = 0; a < FA; ++a)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -193,6 +196,22 @@ void launch_mark_dead(double* G, const int32_t* dead, int ndead, int T, int64_t 
     if (ndead > 0) k_mark_dead<<<256, 256, 0, st>>>(G, dead, ndead, T, mp);
 }
 
+static void gram_launch(dim3 grid, const double* Z, int64_t sp, const int64_t* zoff_d, int nb, double* G, int64_t mp,
+                        int64_t g0, double* pack, int colmajor, cudaStream_t st) {
+    static const int nw = [] {
+        const char* e = getenv("L0S_GRAM_W");
+        return (e && atoi(e) == 4) ? 4 : 8;
+    }();
+    const int smem = 4 * BM * LDS * (int)sizeof(double);
+    if (nw == 4) {
+        cudaFuncSetAttribute(k_gram<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_gram<4><<<grid, 128, smem, st>>>(Z, sp, zoff_d, nb, G, mp, g0, pack, colmajor);
+    } else {
+        cudaFuncSetAttribute(k_gram<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_gram<8><<<grid, 256, smem, st>>>(Z, sp, zoff_d, nb, G, mp, g0, pack, colmajor);
+    }
+}
+
 int64_t gram_blocks(int64_t mp, int T) {
     const int64_t nb = mp / BM;
     return (int64_t)T * (nb * (nb + 1) / 2);
@@ -205,8 +224,6 @@ void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_d, int T, int6
                  int nshards, double* pack, cudaStream_t st) {
     const int nb = (int)(mp / BM);
     const int64_t total = gram_blocks(mp, T);
-    const int smem = 4 * BM * LDS * (int)sizeof(double);
-    cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     // one launch for every task: ~T * nb^2 / 2 CTAs keep the tail wave short
     int64_t g0 = 0, cnt = total;
     if (nshards > 1) {
@@ -214,8 +231,7 @@ void launch_gram(const double* Z, int64_t sp, const int64_t* zoff_d, int T, int6
         g0 = std::min<int64_t>(total, per * shard);
         cnt = std::min<int64_t>(total, g0 + per) - g0;
     }
-    if (cnt > 0)
-        k_gram<<<(unsigned)cnt, 256, smem, st>>>(Z, sp, zoff_d, nb, G, mp, g0, nshards > 1 ? pack : nullptr, 0);
+    if (cnt > 0) gram_launch(dim3((unsigned)cnt), Z, sp, zoff_d, nb, G, mp, g0, nshards > 1 ? pack : nullptr, 0, st);
 }
 
 void launch_gram_cols(const double* Z, int64_t sp, const int64_t* zoff_d, int T, int64_t mp, double* G, int B0,
@@ -224,9 +240,7 @@ void launch_gram_cols(const double* Z, int64_t sp, const int64_t* zoff_d, int T,
     if (B1 > nb) B1 = nb;
     if (B1 <= B0) return;
     const int64_t g0 = (int64_t)B0 * (B0 + 1) / 2, g1 = (int64_t)B1 * (B1 + 1) / 2;
-    const int smem = 4 * BM * LDS * (int)sizeof(double);
-    cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_gram<<<dim3((unsigned)(g1 - g0), (unsigned)T), 256, smem, st>>>(Z, sp, zoff_d, nb, G, mp, g0, nullptr, 1);
+    gram_launch(dim3((unsigned)(g1 - g0), (unsigned)T), Z, sp, zoff_d, nb, G, mp, g0, nullptr, 1, st);
 }
 
 void launch_gram_unpack(const double* recv, int T, int64_t mp, double* G, cudaStream_t st) {
