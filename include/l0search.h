@@ -146,6 +146,18 @@ int l0s_fit_tuples(l0s_ctx *ctx, int n, const int64_t *tuples, int64_t count, in
 int l0s_screen_tuples(l0s_ctx *ctx, int n, const int64_t *tuples, int64_t count, double *out_lb,
                       int32_t *out_flags);
 
+/*
+ * SIS projection scores (screening._chunk_scores, screening.py:126-155),
+ * bit-identical to the reference's fixed-shape pairwise sums.
+ *   l0s_sis_prepare: targets (R x s) float64 in dataset sample order (R <= 8), the task
+ *                    slices as perm (concatenated, int64) + bounds (ntasks+1)
+ *   l0s_sis_scores : F (k x s) float64 feature rows (host, or device with is_device=1)
+ *                    -> out (k) float64 host: clip(max_r sum_t w_t |pearson_t|, 0, 1)
+ */
+int l0s_sis_prepare(l0s_ctx *ctx, const double *targets, int R, int64_t s, const int64_t *perm,
+                    const int64_t *bounds, int ntasks);
+int l0s_sis_scores(l0s_ctx *ctx, const double *F, int64_t k, int is_device, double *out);
+
 /* Copy of the staged normalized Gram of one task ((m+1) x (m+1), last row/col = y). */
 int l0s_get_gram(l0s_ctx *ctx, int task, double *out);
 

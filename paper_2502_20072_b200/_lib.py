@@ -28,7 +28,7 @@ EXPORTS = (
     "l0s_last_error", "l0s_version", "l0s_device_count", "l0s_create", "l0s_destroy", "l0s_stage",
     "l0s_search", "l0s_fit_tuples", "l0s_screen_tuples", "l0s_get_gram", "l0s_unrank", "l0s_rank",
     "l0s_count", "l0s_fp64_peak", "l0s_rcp_check", "l0s_gram_shard_size", "l0s_stage_shard",
-    "l0s_stage_finish",
+    "l0s_stage_finish", "l0s_sis_prepare", "l0s_sis_scores",
 )
 
 
@@ -88,6 +88,8 @@ def lib():
         L.l0s_gram_shard_size.argtypes = [i64, i32, i32, P(i64)]
         L.l0s_stage_shard.argtypes = [vp, vp, i64, i64, vp, vp, vp, i32, i32, i32, i32, i32, vp]
         L.l0s_stage_finish.argtypes = [vp, vp]
+        L.l0s_sis_prepare.argtypes = [vp, vp, i32, i64, vp, vp, i32]
+        L.l0s_sis_scores.argtypes = [vp, vp, i64, i32, vp]
         L.l0s_search.argtypes = [vp, i32, i64, i64, i64, i32, vp, vp, vp, vp, P(i64), P(Stats)]
         L.l0s_fit_tuples.argtypes = [vp, i32, vp, i64, vp, vp, vp, vp]
         L.l0s_screen_tuples.argtypes = [vp, i32, vp, i64, vp, vp]
@@ -184,6 +186,25 @@ class Engine:
     def stage_finish(self, gathered_ptr: int) -> None:
         """Scatter the all-gathered packs (device pointer, nshards x pack doubles) into the Gram."""
         check(lib().l0s_stage_finish(self.handle, ctypes.c_void_p(gathered_ptr)), "l0s_stage_finish")
+
+    def sis_prepare(self, targets: np.ndarray, perm: np.ndarray, bounds: np.ndarray) -> None:
+        targets = np.ascontiguousarray(np.atleast_2d(targets), dtype=np.float64)
+        perm = np.ascontiguousarray(perm, dtype=np.int64)
+        bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+        check(lib().l0s_sis_prepare(self.handle, ptr(targets), targets.shape[0], targets.shape[1], ptr(perm),
+                                    ptr(bounds), bounds.shape[0] - 1), "l0s_sis_prepare")
+
+    def sis_scores(self, F, device_ptr: int | None = None, k: int | None = None) -> np.ndarray:
+        """Scores of the rows of F (host array), or of k device rows at device_ptr."""
+        if device_ptr is None:
+            F = np.ascontiguousarray(F, dtype=np.float64)
+            k = F.shape[0]
+            src, is_dev = ptr(F), 0
+        else:
+            src, is_dev = ctypes.c_void_p(device_ptr), 1
+        out = np.empty(int(k), dtype=np.float64)
+        check(lib().l0s_sis_scores(self.handle, src, int(k), is_dev, ptr(out)), "l0s_sis_scores")
+        return out
 
     def search(self, n: int, keep: int, rank_begin: int = 0, rank_end: int = 2**63 - 1, mode: str = "auto"):
         keep = int(keep)

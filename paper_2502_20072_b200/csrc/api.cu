@@ -111,6 +111,10 @@ struct l0s_ctx {
         lb_tmp, rank_tmp, coll_lb, coll_rank, coll_cnt;
     DBuf ex_scratch, ex_ssr_tmp, ex_ok_tmp, ex_ok, ex_score, ex_coef, ex_ssr, ex_ranks, ex_tuples;
     DBuf qr_ssr, qr_ratio, qr_score, qr_minr;
+    // SIS projection scores
+    DBuf sis_y, sis_yc, sis_sy, sis_perm, sis_bounds, sis_F, sis_out;
+    int sis_R = 0, sis_T = 0;
+    int64_t sis_s = 0;
     std::unordered_map<int64_t, Rec> recs;  // records of this search's refit candidates
     std::vector<int4> units_h;
     int64_t units_key[5] = {-1, -1, -1, -1, -1};
@@ -120,7 +124,8 @@ struct l0s_ctx {
                        &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &umin, &binom, &units, &ucount, &theta_g, &hist, &seedbuf, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
                        &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
-                       &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr};
+                       &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr, &sis_y, &sis_yc, &sis_sy, &sis_perm,
+                       &sis_bounds, &sis_F, &sis_out};
         for (DBuf* b : all) b->release();
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -1015,3 +1020,56 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// SIS projection scores (screening._chunk_scores, screening.py:126-155)
+// ---------------------------------------------------------------------------
+
+int l0s_sis_prepare(l0s_ctx* c, const double* targets, int R, int64_t s, const int64_t* perm, const int64_t* bounds,
+                    int ntasks) {
+    if (!c) return fail(L0S_EINVAL, "null context");
+    if (R < 1 || R > sis_max_targets()) return fail(L0S_EINVAL, "1 <= targets <= %d (got %d)", sis_max_targets(), R);
+    if (s < 1 || ntasks < 1) return fail(L0S_EINVAL, "need s >= 1 and ntasks >= 1");
+    if (bounds[0] != 0 || bounds[ntasks] != s) return fail(L0S_EINVAL, "bounds must run from 0 to s");
+    for (int t = 0; t < ntasks; ++t)
+        if (bounds[t + 1] < bounds[t]) return fail(L0S_EINVAL, "bounds must be non-decreasing");
+    CK(cudaSetDevice(c->dev));
+    CK(c->sis_y.ensure(sizeof(double) * R * s));
+    CK(c->sis_yc.ensure(sizeof(double) * R * s));
+    CK(c->sis_sy.ensure(sizeof(double) * R * ntasks));
+    CK(c->sis_perm.ensure(sizeof(int64_t) * s));
+    CK(c->sis_bounds.ensure(sizeof(int64_t) * (ntasks + 1)));
+    CK(cudaMemcpyAsync(c->sis_y.p, targets, sizeof(double) * R * s, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->sis_perm.p, perm, sizeof(int64_t) * s, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->sis_bounds.p, bounds, sizeof(int64_t) * (ntasks + 1), cudaMemcpyHostToDevice, c->st));
+    launch_sis_targets(c->sis_y.as<double>(), R, s, c->sis_perm.as<int64_t>(), c->sis_bounds.as<int64_t>(), ntasks,
+                       c->sis_yc.as<double>(), c->sis_sy.as<double>(), c->st);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->st));
+    c->sis_R = R;
+    c->sis_T = ntasks;
+    c->sis_s = s;
+    return L0S_OK;
+}
+
+int l0s_sis_scores(l0s_ctx* c, const double* F, int64_t k, int is_device, double* out) {
+    if (!c || c->sis_R < 1) return fail(L0S_ESTATE, "l0s_sis_prepare must be called first");
+    if (k < 0) return fail(L0S_EINVAL, "negative feature count");
+    if (k == 0) return L0S_OK;
+    CK(cudaSetDevice(c->dev));
+    const int64_t s = c->sis_s;
+    const double* Fd = F;
+    if (!is_device) {
+        CK(c->sis_F.ensure(sizeof(double) * k * s));
+        CK(cudaMemcpyAsync(c->sis_F.p, F, sizeof(double) * k * s, cudaMemcpyHostToDevice, c->st));
+        Fd = c->sis_F.as<double>();
+    }
+    CK(c->sis_out.ensure(sizeof(double) * k));
+    if (launch_sis_scores(Fd, k, s, c->sis_perm.as<int64_t>(), c->sis_bounds.as<int64_t>(), c->sis_T,
+                          c->sis_yc.as<double>(), c->sis_sy.as<double>(), c->sis_R, c->sis_out.as<double>(), c->st))
+        return fail(L0S_EINVAL, "%lld samples exceed the SIS kernel's shared-memory row (max 6400)", (long long)s);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, c->sis_out.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return L0S_OK;
+}

@@ -191,6 +191,13 @@ size_t sort_pairs_temp_bytes(int64_t n);
 void sort_pairs(double* lb, int64_t* rank, double* lb_tmp, int64_t* rank_tmp, int64_t n, void* temp,
                 size_t temp_bytes, cudaStream_t st);
 
+// ---- SIS projection scores (sis.cu), bit-identical to screening._chunk_scores ----
+int sis_max_targets();
+void launch_sis_targets(const double* y, int R, int64_t s, const int64_t* perm, const int64_t* bounds, int T,
+                        double* yc, double* sy, cudaStream_t st);
+int launch_sis_scores(const double* F, int64_t k, int64_t s, const int64_t* perm, const int64_t* bounds, int T,
+                      const double* yc, const double* sy, int R, double* out, cudaStream_t st);
+
 // ---- misc ----
 double fp64_peak_tflops(int dev);
 

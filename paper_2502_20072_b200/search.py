@@ -246,12 +246,13 @@ def fit_tuples(values, property_values, tuples, task_slices=None, precision: str
     return eng.fit_tuples(np.asarray(tuples, dtype=np.int64))
 
 
-def install():
+def install(sis: bool = True):
     """Route the reference package's l0 entry points to this implementation.
 
     Patches descsearch.search.{l0_search, fit_tuple}, the names the pipeline
-    bound at import (pipeline.py:34) and the package re-exports.  Returns a
-    callable that restores the originals.
+    bound at import (pipeline.py:34) and the package re-exports; with ``sis``
+    also the SIS projection scores (screening._chunk_scores, screening.py:126).
+    Returns a callable that restores the originals.
     """
     import sys
 
@@ -259,7 +260,10 @@ def install():
     import descsearch.errors as ref_errors
     import descsearch.models as ref_models
     import descsearch.pipeline as pipeline
+    import descsearch.screening as ref_screening
     import descsearch.search as ref_search
+
+    from . import screening as gpu_screening
 
     me = sys.modules[__name__]
     saved = [(ref_search, "l0_search", ref_search.l0_search), (ref_search, "fit_tuple", ref_search.fit_tuple),
@@ -270,6 +274,9 @@ def install():
                       ("RankDeficient", ref_search.RankDeficient), ("RankOutOfRange", ref_search.RankOutOfRange)):
         saved.append((me, name, getattr(me, name)))
         setattr(me, name, obj)
+    if sis:  # SIS projection scores (screening._chunk_scores, looked up by sis_select at call time)
+        saved.append((ref_screening, "_chunk_scores", ref_screening._chunk_scores))
+        ref_screening._chunk_scores = lambda matrix, target: gpu_screening.chunk_scores(matrix, target)
     ref_search.l0_search = l0_search
     ref_search.fit_tuple = fit_tuple
     pipeline.l0_search = l0_search

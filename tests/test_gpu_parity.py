@@ -395,3 +395,39 @@ def test_criterion9_shape_prefix(oracle):
     st = SearchStats()
     full = l0_search(v, y, None, L0Config(dimension=2), stats=st)
     assert st.device["mode_used"] == 1 and full[0].indices == (10, 3000)
+
+
+class _Target:  # the attributes of descsearch.screening.ScreeningTarget that the scores read
+    def __init__(self, targets, slices, s):
+        self.targets = [np.ascontiguousarray(t, dtype=np.float64) for t in targets]
+        self.task_slices = [np.asarray(sl, dtype=np.intp) for sl in slices]
+        self.n_samples = s
+
+
+@pytest.mark.parametrize("name", golden_names("sis"))
+def test_sis_scores_match_reference_golden(name):
+    """csrc/sis.cu == the reference's screening._chunk_scores, bit for bit (incl. NaN/inf rows,
+    ragged and constant-target tasks, several targets)."""
+    from paper_2502_20072_b200.screening import chunk_scores
+
+    g = load_golden("sis", name)
+    F = g["F"]
+    tgt = _Target(list(g["targets"]), slices_of(g["task_id"], g["order"]), F.shape[1])
+    got = chunk_scores(F, tgt)
+    assert bits_equal(got, g["scores"])
+    # chunking invariance: the reference's scores do not depend on the chunk height
+    parts = np.concatenate([chunk_scores(F[i:i + 3], tgt) for i in range(0, F.shape[0], 3)])
+    assert bits_equal(parts, g["scores"])
+
+
+def test_sis_scores_match_oracle_large(oracle, rng):
+    """C5-shaped chunk (2048 features x 2000 samples, 4 round-robin tasks, 10 targets)."""
+    from oracle import sis
+    from paper_2502_20072_b200.screening import chunk_scores
+
+    s, T = 2000, 4
+    F = rng.uniform(0.5, 2.0, size=(2048, s)) * rng.uniform(0.1, 10.0, size=(2048, 1))
+    targets = [rng.standard_normal(s) + 0.3 * F[i] for i in range(10)]
+    slices = [np.arange(t, s, T) for t in range(T)]
+    got = chunk_scores(F, _Target(targets, slices, s))
+    assert bits_equal(got, sis.chunk_scores(F, targets, slices))

@@ -13,7 +13,7 @@ import itertools
 import numpy as np
 import pytest
 
-from conftest import bits_equal, golden_names, load_golden, search_case
+from conftest import bits_equal, golden_names, load_golden, search_case, slices_of
 
 
 @pytest.mark.parametrize("name", golden_names("lsq"))
@@ -116,3 +116,14 @@ def test_threaded_scan_is_thread_invariant(oracle, rng):
     one = oracle.scan(vals, yy, bounds, 25, 3, 1e-10, 0, 2300, 10, threads=1)
     four = oracle.scan(vals, yy, bounds, 25, 3, 1e-10, 0, 2300, 10, threads=4)
     assert one == four
+
+
+@pytest.mark.parametrize("name", golden_names("sis"))
+def test_sis_oracle_matches_reference_golden(name):
+    """oracle/sis.py == the reference's _chunk_scores, bit for bit."""
+    from oracle import sis
+
+    g = load_golden("sis", name)
+    slices = slices_of(g["task_id"], g["order"])
+    got = sis.chunk_scores(g["F"], list(g["targets"]), slices)
+    assert bits_equal(got, g["scores"])
