@@ -112,8 +112,8 @@ struct l0s_ctx {
     DBuf ex_scratch, ex_ssr_tmp, ex_ok_tmp, ex_ok, ex_score, ex_coef, ex_ssr, ex_ranks, ex_tuples;
     DBuf qr_ssr, qr_ratio, qr_score, qr_minr;
     // SIS projection scores
-    DBuf sis_y, sis_yc, sis_sy, sis_perm, sis_bounds, sis_F, sis_out;
-    int sis_R = 0, sis_T = 0;
+    DBuf sis_y, sis_yc, sis_sy, sis_perm, sis_bounds, sis_F, sis_out, sis_dest, sis_tE, sis_tpoff;
+    int sis_R = 0, sis_T = 0, sis_rowlen = 0;
     int64_t sis_s = 0;
     std::unordered_map<int64_t, Rec> recs;  // records of this search's refit candidates
     std::vector<int4> units_h;
@@ -125,7 +125,7 @@ struct l0s_ctx {
                        &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
                        &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr, &sis_y, &sis_yc, &sis_sy, &sis_perm,
-                       &sis_bounds, &sis_F, &sis_out};
+                       &sis_bounds, &sis_F, &sis_out, &sis_dest, &sis_tE, &sis_tpoff};
         for (DBuf* b : all) b->release();
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -1044,6 +1044,31 @@ int l0s_sis_prepare(l0s_ctx* c, const double* targets, int R, int64_t s, const i
     CK(cudaMemcpyAsync(c->sis_bounds.p, bounds, sizeof(int64_t) * (ntasks + 1), cudaMemcpyHostToDevice, c->st));
     launch_sis_targets(c->sis_y.as<double>(), R, s, c->sis_perm.as<int64_t>(), c->sis_bounds.as<int64_t>(), ntasks,
                        c->sis_yc.as<double>(), c->sis_sy.as<double>(), c->st);
+    // the scores kernel's shared-memory row layout (k_sis_scores): per task, lane l's contiguous
+    // range of E_t samples at l * (E_t + 1)
+    std::vector<int> tE((size_t)ntasks), tpoff((size_t)ntasks), dest((size_t)s);
+    int off = 0;
+    for (int t = 0; t < ntasks; ++t) {
+        const int64_t ns = bounds[t + 1] - bounds[t];
+        int64_t W = 1;
+        while (W < ns) W <<= 1;
+        const int E = (int)std::min<int64_t>(16, std::max<int64_t>(1, W / 32));  // lane range per super-block
+        const int64_t nsb = std::max<int64_t>(1, W / (32 * E));
+        tE[(size_t)t] = E;
+        tpoff[(size_t)t] = off;
+        for (int64_t i = 0; i < ns; ++i) {
+            const int64_t q = i / (32 * E), r = i % (32 * E);
+            dest[(size_t)(bounds[t] + i)] = off + (int)((q * 32 + r / E) * (E + 1) + r % E);
+        }
+        off += (int)(nsb * 32 * (E + 1));
+    }
+    c->sis_rowlen = off;
+    CK(c->sis_dest.ensure(sizeof(int) * s));
+    CK(c->sis_tE.ensure(sizeof(int) * ntasks));
+    CK(c->sis_tpoff.ensure(sizeof(int) * ntasks));
+    CK(cudaMemcpyAsync(c->sis_dest.p, dest.data(), sizeof(int) * s, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->sis_tE.p, tE.data(), sizeof(int) * ntasks, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->sis_tpoff.p, tpoff.data(), sizeof(int) * ntasks, cudaMemcpyHostToDevice, c->st));
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->st));
     c->sis_R = R;
@@ -1065,9 +1090,10 @@ int l0s_sis_scores(l0s_ctx* c, const double* F, int64_t k, int is_device, double
         Fd = c->sis_F.as<double>();
     }
     CK(c->sis_out.ensure(sizeof(double) * k));
-    if (launch_sis_scores(Fd, k, s, c->sis_perm.as<int64_t>(), c->sis_bounds.as<int64_t>(), c->sis_T,
-                          c->sis_yc.as<double>(), c->sis_sy.as<double>(), c->sis_R, c->sis_out.as<double>(), c->st))
-        return fail(L0S_EINVAL, "%lld samples exceed the SIS kernel's shared-memory row (max 6400)", (long long)s);
+    if (launch_sis_scores(Fd, k, s, c->sis_perm.as<int64_t>(), c->sis_dest.as<int>(), c->sis_bounds.as<int64_t>(),
+                          c->sis_tE.as<int>(), c->sis_tpoff.as<int>(), c->sis_rowlen, c->sis_T, c->sis_yc.as<double>(),
+                          c->sis_sy.as<double>(), c->sis_R, c->sis_out.as<double>(), c->nsm, c->st))
+        return fail(L0S_EINVAL, "%lld samples exceed the SIS kernel's shared-memory row", (long long)s);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out, c->sis_out.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
