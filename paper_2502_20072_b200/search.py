@@ -69,24 +69,29 @@ def count_models(m: int, n: int) -> int:
 def unrank_tuple(rank: int, m: int, n: int) -> tuple[int, ...]:
     """The rank-th strictly increasing n-tuple in lexicographic order.
 
-    Closed-form walk over the combinadic: position k takes the smallest e
-    whose block of C(m-1-e, n-1-k) successors still contains the rank.
+    Walk over the combinadic: position k takes the largest e whose preceding
+    blocks sum_{e0 <= e' < e} C(m-1-e', n-1-k) = C(m-e0, n-k) - C(m-e, n-k)
+    (hockey stick) do not exceed the remaining rank -- found by binary search,
+    O(n log m) exact binomials instead of a scan over e.
     """
     total = count_models(m, n)
     if not 0 <= rank < total:
         raise RankOutOfRange(f"rank {rank} outside [0, {total})")
     out = []
-    e = 0
+    e0 = 0
     for k in range(n):
-        rem = n - 1 - k
-        while True:
-            block = comb(m - 1 - e, rem)
-            if rank < block:
-                break
-            rank -= block
-            e += 1
-        out.append(e)
-        e += 1
+        top = comb(m - e0, n - k)
+        target = top - rank
+        lo, hi = e0, m - n + k  # largest e with C(m - e, n - k) >= target
+        while lo < hi:
+            mid = (lo + hi + 1) // 2
+            if comb(m - mid, n - k) >= target:
+                lo = mid
+            else:
+                hi = mid - 1
+        rank -= top - comb(m - lo, n - k)
+        out.append(lo)
+        e0 = lo + 1
     return tuple(out)
 
 
