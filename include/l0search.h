@@ -158,6 +158,16 @@ int l0s_sis_prepare(l0s_ctx *ctx, const double *targets, int R, int64_t s, const
                     const int64_t *bounds, int ntasks);
 int l0s_sis_scores(l0s_ctx *ctx, const double *F, int64_t k, int is_device, double *out);
 
+/* Gram method of subsequent stages: AUTO (INT8 Ozaki on tcgen05 for fp64 problems with
+ * m >= 256, DMMA otherwise or when the INT8 error bound is too loose), DMMA (fp64 tensor),
+ * OZAKI (INT8 whenever possible). */
+#define L0S_GRAM_AUTO 0
+#define L0S_GRAM_DMMA 1
+#define L0S_GRAM_OZAKI 2
+int l0s_set_gram_mode(l0s_ctx *ctx, int mode);
+/* Per-task entry error bound of the staged Gram (ntasks values) and whether it is the INT8 one. */
+int l0s_stage_info(l0s_ctx *ctx, double *eta_out, int *ozaki_out);
+
 /* Copy of the staged normalized Gram of one task ((m+1) x (m+1), last row/col = y). */
 int l0s_get_gram(l0s_ctx *ctx, int task, double *out);
 

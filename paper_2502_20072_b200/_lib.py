@@ -28,7 +28,7 @@ EXPORTS = (
     "l0s_last_error", "l0s_version", "l0s_device_count", "l0s_create", "l0s_destroy", "l0s_stage",
     "l0s_search", "l0s_fit_tuples", "l0s_screen_tuples", "l0s_get_gram", "l0s_unrank", "l0s_rank",
     "l0s_count", "l0s_fp64_peak", "l0s_rcp_check", "l0s_gram_shard_size", "l0s_stage_shard",
-    "l0s_stage_finish", "l0s_sis_prepare", "l0s_sis_scores",
+    "l0s_stage_finish", "l0s_sis_prepare", "l0s_sis_scores", "l0s_set_gram_mode", "l0s_stage_info",
 )
 
 
@@ -88,6 +88,8 @@ def lib():
         L.l0s_gram_shard_size.argtypes = [i64, i32, i32, P(i64)]
         L.l0s_stage_shard.argtypes = [vp, vp, i64, i64, vp, vp, vp, i32, i32, i32, i32, i32, vp]
         L.l0s_stage_finish.argtypes = [vp, vp]
+        L.l0s_set_gram_mode.argtypes = [vp, i32]
+        L.l0s_stage_info.argtypes = [vp, vp, vp]
         L.l0s_sis_prepare.argtypes = [vp, vp, i32, i64, vp, vp, i32]
         L.l0s_sis_scores.argtypes = [vp, vp, i64, i32, vp]
         L.l0s_search.argtypes = [vp, i32, i64, i64, i64, i32, vp, vp, vp, vp, P(i64), P(Stats)]
@@ -186,6 +188,17 @@ class Engine:
     def stage_finish(self, gathered_ptr: int) -> None:
         """Scatter the all-gathered packs (device pointer, nshards x pack doubles) into the Gram."""
         check(lib().l0s_stage_finish(self.handle, ctypes.c_void_p(gathered_ptr)), "l0s_stage_finish")
+
+    def set_gram_mode(self, mode: str) -> None:
+        """'auto' | 'dmma' | 'ozaki' (INT8 tensor cores) for subsequent stages."""
+        check(lib().l0s_set_gram_mode(self.handle, {"auto": 0, "dmma": 1, "ozaki": 2}[mode]), "l0s_set_gram_mode")
+
+    def stage_info(self):
+        """(per-task Gram entry error bound eta, whether the INT8 path produced the Gram)."""
+        eta = np.zeros(self.T, dtype=np.float64)
+        oz = ctypes.c_int(0)
+        check(lib().l0s_stage_info(self.handle, ptr(eta), ctypes.byref(oz)), "l0s_stage_info")
+        return eta, bool(oz.value)
 
     def sis_prepare(self, targets: np.ndarray, perm: np.ndarray, bounds: np.ndarray) -> None:
         targets = np.ascontiguousarray(np.atleast_2d(targets), dtype=np.float64)

@@ -102,6 +102,9 @@ struct l0s_ctx {
     int64_t n_dead = 0, n_iforce = 0;
     bool shard_pending = false;  // l0s_stage_shard done, l0s_stage_finish due
     bool gram_timed = false;     // ev[2..3] bracket the Gram kernel of this stage
+    int gram_mode = 0;           // L0S_GRAM_AUTO / _DMMA / _OZAKI (l0s_set_gram_mode)
+    bool gram_ozaki = false;     // the staged Gram came from the INT8 path (eta on the device)
+    DBuf oz_q, oz_ex, oz_koff;
     // binomial table (k <= binom_n) x (a <= m)
     DBuf binom;
     int binom_n = -1;
@@ -125,7 +128,7 @@ struct l0s_ctx {
                        &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
                        &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr, &sis_y, &sis_yc, &sis_sy, &sis_perm,
-                       &sis_bounds, &sis_F, &sis_out, &sis_dest, &sis_tE, &sis_tpoff};
+                       &sis_bounds, &sis_F, &sis_out, &sis_dest, &sis_tE, &sis_tpoff, &oz_q, &oz_ex, &oz_koff};
         for (DBuf* b : all) b->release();
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -369,6 +372,8 @@ static int stage_prepare(l0s_ctx* c, const double* values, int64_t m, int64_t s,
     return L0S_OK;
 }
 
+static int gram_full(l0s_ctx* c);
+
 // stage after the Gram: unit diagonal, per-feature conditioning flags, host copies
 static int stage_post(l0s_ctx* c) {
     const int64_t m = c->m;
@@ -390,12 +395,63 @@ static int stage_post(l0s_ctx* c) {
     cudaEventRecord(c->ev[1], c->st);
     c->yyu_h.assign((size_t)ntasks, 0.0);
     CK(cudaMemcpyAsync(c->yyu_h.data(), c->yyu.p, sizeof(double) * ntasks, cudaMemcpyDeviceToHost, c->st));
+    if (c->gram_ozaki)
+        CK(cudaMemcpyAsync(c->eta_h.data(), c->eta_d.p, sizeof(double) * ntasks, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
+    if (c->gram_ozaki) {
+        // the INT8 Gram's error bound must stay well inside the screen's first-order regime;
+        // spiky rows (max |z| close to 1) make it too loose: redo the Gram in fp64 (DMMA)
+        bool loose = false;
+        for (int t = 0; t < ntasks; ++t) loose |= !(c->eta_h[(size_t)t] <= 1e-6);
+        if (loose) {
+            for (int t = 0; t < ntasks; ++t) c->eta_h[(size_t)t] = 4.0 * (c->rows_h[(size_t)t] + 8.0) * kEps;
+            CK(cudaMemcpyAsync(c->eta_d.p, c->eta_h.data(), sizeof(double) * ntasks, cudaMemcpyHostToDevice, c->st));
+            const int prev = c->gram_mode;
+            c->gram_mode = L0S_GRAM_DMMA;
+            gram_full(c);
+            c->gram_mode = prev;
+            launch_unit_diag(c->G.as<double>(), ntasks, m, c->mp, c->st);
+            launch_feature_flags(c->qf.as<double>(), c->un2.as<double>(), c->rowsd.as<double>(), m, c->mp, ntasks,
+                                 c->umin.as<double>(), c->rho.as<double>(), c->rho_cap.as<double>(),
+                                 c->dead.as<unsigned char>(), c->iforce.as<unsigned char>(), c->G.as<double>(),
+                                 c->yyu.as<double>(), c->ynorm.as<double>(), c->st);
+            CK(cudaStreamSynchronize(c->st));
+        }
+    }
     c->ms_gram = elapsed(c->ev[0], c->ev[1]);
     c->ms_gram_k = c->gram_timed ? elapsed(c->ev[2], c->ev[3]) : 0.0;
     c->gram_timed = false;
     c->staged = true;
     c->binom_m = -1;
+    return L0S_OK;
+}
+
+// The whole Gram in one go: the INT8 Ozaki path (tcgen05) when selected, else DMMA.
+static int gram_full(l0s_ctx* c) {
+    const int nb = (int)(c->mp / 64);
+    c->gram_ozaki = false;
+    if (c->gram_mode == L0S_GRAM_OZAKI || (c->gram_mode == L0S_GRAM_AUTO && c->prec == L0S_PREC_FP64 &&
+                                           c->m >= 256)) {
+        int64_t KP = 0;
+        const int64_t qb = ozaki_q_bytes(c->mp, c->T, c->rpad_h.data(), &KP);
+        const int64_t R = (c->mp + 127) / 128 * 128;
+        CK(c->oz_q.ensure((size_t)qb));
+        CK(c->oz_ex.ensure(sizeof(int) * c->T * R));
+        CK(c->oz_koff.ensure(sizeof(int64_t) * (c->T + 1)));
+        cudaEventRecord(c->ev[2], c->st);
+        if (launch_ozaki_gram(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), c->rpad_h.data(), c->T, c->m, c->mp,
+                              c->rowsd.as<double>(), c->G.as<double>(), c->eta_d.as<double>(), c->oz_q.as<int8_t>(),
+                              c->oz_ex.as<int>(), c->oz_koff.as<int64_t>(), c->st) == 0) {
+            cudaEventRecord(c->ev[3], c->st);
+            c->gram_timed = true;
+            c->gram_ozaki = true;
+            return L0S_OK;
+        }
+    }
+    cudaEventRecord(c->ev[2], c->st);
+    launch_gram_cols(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), c->T, c->mp, c->G.as<double>(), 0, nb, c->st);
+    cudaEventRecord(c->ev[3], c->st);
+    c->gram_timed = true;
     return L0S_OK;
 }
 
@@ -433,15 +489,13 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
         if (!is_device)
             CK(cudaMemcpyAsync(c->in_values.p, values, sizeof(double) * m * s, cudaMemcpyHostToDevice, c->st));
         rows_to_z(0, m);
-        if (gram_cols) {
-            cudaEventRecord(c->ev[2], c->st);
-            launch_gram_cols(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), ntasks, c->mp, c->G.as<double>(), 0,
-                             nb, c->st);
-            cudaEventRecord(c->ev[3], c->st);
-            c->gram_timed = true;
-        }
+        if (gram_cols) return gram_full(c);
         return L0S_OK;
     }
+    // the INT8 Gram runs once all rows have landed (its digits need whole rows)
+    const bool ozaki = gram_cols && (c->gram_mode == L0S_GRAM_OZAKI ||
+                                     (c->gram_mode == L0S_GRAM_AUTO && precision == L0S_PREC_FP64 && m >= 256));
+    if (ozaki) gram_cols = false;
     const int64_t R = (((m + l0s_ctx::kChunks - 1) / l0s_ctx::kChunks) + 63) / 64 * 64;
     // the copy stream starts after everything queued so far (buffers may be in use by a search)
     cudaEventRecord(c->cev[l0s_ctx::kChunks], c->st);
@@ -464,6 +518,7 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
                              B0, B1, c->st);
         }
     }
+    if (ozaki) return gram_full(c);
     return L0S_OK;
 }
 
@@ -1097,5 +1152,19 @@ int l0s_sis_scores(l0s_ctx* c, const double* F, int64_t k, int is_device, double
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out, c->sis_out.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
+    return L0S_OK;
+}
+
+int l0s_set_gram_mode(l0s_ctx* c, int mode) {
+    if (!c) return fail(L0S_EINVAL, "null context");
+    if (mode < L0S_GRAM_AUTO || mode > L0S_GRAM_OZAKI) return fail(L0S_EINVAL, "bad gram mode %d", mode);
+    c->gram_mode = mode;
+    return L0S_OK;
+}
+
+int l0s_stage_info(l0s_ctx* c, double* eta_out, int* ozaki_out) {
+    if (!c || !c->staged) return fail(L0S_ESTATE, "l0s_stage must be called first");
+    for (int t = 0; t < c->T; ++t) eta_out[t] = c->eta_h[(size_t)t];
+    *ozaki_out = c->gram_ozaki ? 1 : 0;
     return L0S_OK;
 }

@@ -45,6 +45,12 @@ void launch_unit_diag(double* G, int T, int64_t m, int64_t mp, cudaStream_t st);
 // Features the reference's rank rule rejects in every tuple: NaN their Gram row and column (all tasks).
 void launch_mark_dead(double* G, const int32_t* dead, int ndead, int T, int64_t mp, cudaStream_t st);
 
+// ---- Gram on the INT8 tensor cores by Ozaki splitting (ozaki.cu) ----
+int64_t ozaki_q_bytes(int64_t mp, int T, const int64_t* rpad_h, int64_t* KP_out);
+int launch_ozaki_gram(const double* Z, int64_t sp, const int64_t* zoff_d, const int64_t* rpad_h, int T, int64_t m,
+                      int64_t mp, const double* rows_d, double* G, double* eta_d, int8_t* Q, int* ex, int64_t* koff_d,
+                      cudaStream_t st);
+
 // ---- bit-exact Householder (exact.cu) ----
 struct ExactArgs {
     const void* Xp;         // (m, s) working dtype, permuted
@@ -178,6 +184,9 @@ std::vector<int4> fit4_units(int64_t m, int T, const std::vector<int64_t>& c3_pr
 void launch_screen4(const FitArgs& a, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags,
                     cudaStream_t st);
 
+// 3-D int8 tensor (x = cols contiguous, y = rows, z = planes), box (bx, by, 1), 64-byte swizzle
+bool make_tma_i8_3d(TmaDesc* out, const void* base, unsigned long long cols, unsigned long long rows,
+                    unsigned long long planes, unsigned bx, unsigned by);
 // Encode a 2-D f64 tiled TMA descriptor over G ([rows x cols], row stride = cols) with box (bx, by).
 bool make_tma_2d(TmaDesc* out, const double* G, unsigned long long cols, unsigned long long rows, unsigned bx,
                  unsigned by);

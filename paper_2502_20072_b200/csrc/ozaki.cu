@@ -1,0 +1,297 @@
+// ozaki.cu -- the per-task Gram on the INT8 tensor cores (tcgen05.mma kind::i8, TMEM).
+//
+// Ozaki splitting: every row f of Z (one task's segment) is scaled by 2^-e_f (max |z| < 2^e_f)
+// and cut into S = 4 signed 7-bit digits, u = sum_a q_a 2^-7a + rho, |q_a| <= 127,
+// |rho| < 2^-28.  Then
+//     G[f, g] = 2^(e_f + e_g) sum_{a + b <= S + 1} 2^-7(a+b) sum_s q_fa(s) q_gb(s)  (+ error)
+// where every inner sum is an exact int32 (|.| <= 4 r 127^2 < 2^31 for r <= 33k samples):
+// the tensor cores accumulate it in TMEM, one accumulator per digit weight d = a + b
+// (4 x 128 columns), and the epilogue combines the four in fp64.  The dropped digit
+// products and the remainders bound the error of every entry by
+//     eta_t = C4 r_t max_f 2^(2 e_f)   (C4 = 1.9e-8, normalised to unit rows)
+// which the screen's error model takes in place of the fp64 dot-product bound; a task whose
+// eta exceeds OZ_ETA_MAX falls back to the DMMA Gram (spiky rows).
+//
+// GEMM: one CTA per 128 x 128 upper-triangle tile of one task; 192 threads = TMA producer
+// warp, MMA warp (one elected thread issues tcgen05.mma; it also owns the TMEM allocation)
+// and 4 epilogue warps (tcgen05.ld by TMEM lane quadrant).  A pipeline stage is one 64-byte
+// K chunk of all 4 digit planes of both operands (8 TMA boxes of 128 x 64 B, SWIZZLE_64B,
+// 64 KB), 3 stages; each stage feeds 10 digit pairs x 2 MMAs of 128 x 128 x 32.
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace l0s {
+
+namespace {
+
+constexpr int OZ_S = 4;             // digits per value
+constexpr int OZ_NG = OZ_S;         // digit-weight groups d = 2 .. S + 1
+constexpr int OZ_BM = 128;          // tile rows = cols
+constexpr int OZ_KC = 64;           // K bytes per stage
+constexpr int OZ_ST = 3;            // stages
+constexpr int OZ_TILE = OZ_BM * OZ_KC;              // 8 KB: one digit plane of one operand
+constexpr int OZ_STAGE = 2 * OZ_S * OZ_TILE;        // 64 KB
+constexpr int OZ_SMEM = OZ_ST * OZ_STAGE + 1024;    // + alignment slack
+constexpr double OZ_C = 1.9e-8;     // error constant per unit-scaled entry and sample (S = 4)
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// K-major operand tile, rows of 64 bytes, 64-byte swizzle: 8-row atoms of 512 B
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr & 0x3FFFF) >> 4);  // start address
+    d |= (uint64_t)1 << 16;                    // leading byte offset (unused for swizzled K-major)
+    d |= (uint64_t)(512 >> 4) << 32;           // stride byte offset: 8 rows x 64 B
+    d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
+    d |= (uint64_t)4 << 61;                    // SWIZZLE_64B
+    return d;
+}
+
+// kind::i8 instruction descriptor: s32 accumulate, s8 x s8, K-major A and B, M = 128, N = 128
+constexpr uint32_t OZ_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BM >> 3) << 17) |
+                              ((uint32_t)(OZ_BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(OZ_IDESC), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(unsigned long long* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int x, int y, int z, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::
+            "r"(smem_addr(dst)),
+        "l"(reinterpret_cast<unsigned long long>(tmap)), "r"(x), "r"(y), "r"(z), "r"(smem_addr(bar))
+        : "memory");
+}
+
+// ---- digits: one warp per (row f < mp, task t) ----
+__global__ void k_oz_split(const double* __restrict__ Z, int64_t sp, const int64_t* __restrict__ zoff, int T, int64_t mp,
+                           int64_t R, const int64_t* __restrict__ koff, int8_t* __restrict__ Q, int64_t KP,
+                           int* __restrict__ ex) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wid >= mp * T) return;
+    const int t = (int)(wid % T);
+    const int64_t f = wid / T;
+    const double* src = Z + f * sp + zoff[t];
+    const int len = (int)(zoff[t + 1] - zoff[t]);
+    const int64_t k0 = koff[t];
+    const int klen = (int)(koff[t + 1] - k0);
+    double mx = 0.0;
+    for (int j = lane; j < len; j += 32) mx = fmax(mx, fabs(src[j]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(L0S_FULL, mx, o));
+    // e: max |z| < 2^e (exact power-of-two scaling); NaN rows (dead features) give zero digits
+    int e = 0;
+    if (mx > 0.0 && mx == mx && mx < INFINITY) {
+        frexp(mx, &e);  // mx = m 2^e, 0.5 <= m < 1
+    }
+    for (int j = lane; j < klen; j += 32) {
+        double u = (j < len && mx == mx) ? ldexp(src[j], -e) : 0.0;
+        if (!(u == u)) u = 0.0;
+#pragma unroll
+        for (int a = 0; a < OZ_S; ++a) {
+            const double v = u * 128.0;  // exact
+            const double q = trunc(v);   // |q| <= 127
+            u = v - q;                   // exact remainder
+            Q[((int64_t)a * R + f) * KP + k0 + j] = (int8_t)(int)q;
+        }
+    }
+    if (lane == 0) ex[(int64_t)t * R + f] = e;
+}
+
+// ---- GEMM: one 128 x 128 upper-triangle tile (fb <= gb) of one task per CTA ----
+__global__ void __launch_bounds__(192, 1) k_oz_gemm(const __grid_constant__ TmaDesc tmQ, const int64_t* __restrict__ koff,
+                                                   const int* __restrict__ ex, int64_t R, int nb, int64_t mp,
+                                                   double* __restrict__ Gall) {
+    extern __shared__ unsigned char oz_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)oz_raw + 1023) & ~(uintptr_t)1023);
+    __shared__ __align__(8) unsigned long long full[OZ_ST], empty[OZ_ST], done;
+    __shared__ uint32_t tmem_slot;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = blockIdx.y;
+    int lin = blockIdx.x, fb = 0;
+    while (lin >= nb - fb) {
+        lin -= nb - fb;
+        ++fb;
+    }
+    const int gb = fb + lin;
+    const int64_t k0 = koff[t];
+    const int nkc = (int)((koff[t + 1] - k0) / OZ_KC);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < OZ_ST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&done, 1);
+        mbar_fence_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_addr(&tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // TMA producer
+            for (int kc = 0; kc < nkc; ++kc) {
+                const int s = kc % OZ_ST;
+                if (kc >= OZ_ST) mbar_wait(&empty[s], (unsigned)((kc / OZ_ST - 1) & 1));
+                unsigned char* st = sm + s * OZ_STAGE;
+                mbar_expect_tx(&full[s], (unsigned)OZ_STAGE);
+                const int x = (int)(k0 + (int64_t)kc * OZ_KC);
+                for (int a = 0; a < OZ_S; ++a) {
+                    tma_load_3d(st + a * OZ_TILE, &tmQ, x, fb * OZ_BM, a, &full[s]);
+                    tma_load_3d(st + (OZ_S + a) * OZ_TILE, &tmQ, x, gb * OZ_BM, a, &full[s]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            for (int kc = 0; kc < nkc; ++kc) {
+                const int s = kc % OZ_ST;
+                mbar_wait(&full[s], (unsigned)((kc / OZ_ST) & 1));
+                tc_fence_after();
+                const uint32_t st = smem_addr(sm + s * OZ_STAGE);
+#pragma unroll
+                for (int a = 1; a <= OZ_S; ++a)
+#pragma unroll
+                    for (int b = 1; a + b <= OZ_S + 1; ++b)
+#pragma unroll
+                        for (int kk = 0; kk < OZ_KC / 32; ++kk) {
+                            const uint64_t da = sw64_desc(st + (a - 1) * OZ_TILE + kk * 32);
+                            const uint64_t db = sw64_desc(st + (OZ_S + b - 1) * OZ_TILE + kk * 32);
+                            const uint32_t acc = (kc == 0 && kk == 0 && a == 1) ? 0u : 1u;
+                            mma_i8(tmem + (uint32_t)(a + b - 2) * OZ_BM, da, db, acc);
+                        }
+                mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+            }
+            mma_commit(&done);
+        }
+    } else {  // epilogue warps 2..5: TMEM lane quadrant (warp % 4) = tile rows
+        mbar_wait(&done, 0u);
+        tc_fence_after();
+        const int quad = warp & 3;
+        const int r = quad * 32 + lane;
+        const int64_t row = (int64_t)fb * OZ_BM + r;
+        const int er = ex[(int64_t)t * R + (row < R ? row : 0)];
+        double* G = Gall + (int64_t)t * mp * mp;
+        for (int c0 = 0; c0 < OZ_BM; c0 += 32) {
+            double acc[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+#pragma unroll
+            for (int g = 0; g < OZ_NG; ++g) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(g * OZ_BM + c0);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                const double w = ldexp(1.0, -7 * (g + 2));
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[j] = fma((double)(int)v[j], w, acc[j]);  // exact products
+            }
+            if (row < mp) {
+#pragma unroll 4
+                for (int j = 0; j < 32; ++j) {
+                    const int64_t col = (int64_t)gb * OZ_BM + c0 + j;
+                    if (col < mp && row <= col) {
+                        const double x = ldexp(acc[j], er + ex[(int64_t)t * R + col]);
+                        G[row * mp + col] = x;
+                        G[col * mp + row] = x;
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    }
+}
+
+// eta_t = C r_t max over rows of 2^(2 e) / |row|^2 (features: unit rows; the property row: Y2)
+__global__ void k_oz_eta(const int* __restrict__ ex, int64_t R, int64_t m, int64_t mp, const double* __restrict__ Gall,
+                         const double* __restrict__ rows, double* __restrict__ eta) {
+    const int t = blockIdx.x;
+    double mx = 0.0;
+    for (int64_t f = threadIdx.x; f <= m; f += blockDim.x) {
+        double v = ldexp(1.0, 2 * ex[(int64_t)t * R + f]);
+        if (f == m) {
+            const double y2 = Gall[(int64_t)t * mp * mp + m * mp + m];
+            v = y2 > 0.0 ? v / y2 : 0.0;
+        }
+        mx = fmax(mx, v);
+    }
+    __shared__ double red[256];
+    red[threadIdx.x] = mx;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) eta[t] = OZ_C * rows[t] * red[0] * (1.0 + 1e-6);
+}
+
+}  // namespace
+
+int64_t ozaki_q_bytes(int64_t mp, int T, const int64_t* rpad_h, int64_t* KP_out) {
+    const int64_t R = (mp + OZ_BM - 1) / OZ_BM * OZ_BM;
+    int64_t KP = 0;
+    for (int t = 0; t < T; ++t) KP += (rpad_h[t] + OZ_KC - 1) / OZ_KC * OZ_KC;
+    if (KP_out) *KP_out = KP;
+    return (int64_t)OZ_S * R * KP;
+}
+
+// Z (mp x sp, task t's columns [zoff_t, +rpad_t)) -> G (T x mp x mp) and eta (T); workspaces:
+// Q (ozaki_q_bytes), ex (T x R ints), koff_d (T+1 int64, filled here).  Returns 0, or -1 when
+// the TMA descriptor could not be built.
+int launch_ozaki_gram(const double* Z, int64_t sp, const int64_t* zoff_d, const int64_t* rpad_h, int T, int64_t m,
+                      int64_t mp, const double* rows_d, double* G, double* eta_d, int8_t* Q, int* ex, int64_t* koff_d,
+                      cudaStream_t st) {
+    const int64_t R = (mp + OZ_BM - 1) / OZ_BM * OZ_BM;
+    std::vector<int64_t> koff((size_t)T + 1, 0);
+    for (int t = 0; t < T; ++t) koff[(size_t)t + 1] = koff[(size_t)t] + (rpad_h[t] + OZ_KC - 1) / OZ_KC * OZ_KC;
+    const int64_t KP = koff[(size_t)T];
+    if (cudaMemcpyAsync(koff_d, koff.data(), sizeof(int64_t) * (T + 1), cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return -1;
+    if (R > mp) {
+        for (int a = 0; a < OZ_S; ++a)
+            cudaMemsetAsync(Q + ((int64_t)a * R + mp) * KP, 0, (size_t)((R - mp) * KP), st);
+        cudaMemsetAsync(ex, 0, sizeof(int) * T * R, st);
+    }
+    const int64_t warps = mp * T;
+    k_oz_split<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(Z, sp, zoff_d, T, mp, R, koff_d, Q, KP, ex);
+    TmaDesc tm;
+    if (!make_tma_i8_3d(&tm, Q, (unsigned long long)KP, (unsigned long long)R, OZ_S, OZ_KC, OZ_BM)) return -1;
+    cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
+    const int nb = (int)(R / OZ_BM);
+    k_oz_gemm<<<dim3((unsigned)(nb * (nb + 1) / 2), (unsigned)T), 192, OZ_SMEM, st>>>(tm, koff_d, ex, R, nb, mp, G);
+    k_oz_eta<<<T, 256, 0, st>>>(ex, R, m, mp, G, rows_d, eta_d);
+    return 0;
+}
+
+}  // namespace l0s

@@ -431,3 +431,34 @@ def test_sis_scores_match_oracle_large(oracle, rng):
     slices = [np.arange(t, s, T) for t in range(T)]
     got = chunk_scores(F, _Target(targets, slices, s))
     assert bits_equal(got, sis.chunk_scores(F, targets, slices))
+
+
+@pytest.mark.parametrize("shape", [(300, 700, 1), (1000, 2500, 4)])
+def test_ozaki_gram_within_its_bound(rng, shape):
+    """INT8 tensor-core Gram (Ozaki digits, tcgen05) vs the fp64 DMMA Gram: every entry within
+    the two error bounds; the search on it returns the same models bit for bit."""
+    from paper_2502_20072_b200 import _lib
+
+    m, s, T = shape
+    v = rng.uniform(0.5, 2.0, size=(m, s)) * rng.uniform(0.2, 5.0, size=(m, 1))
+    y = 1.5 * v[4] - 0.5 * v[77] + v[140] + 0.05 * rng.standard_normal(s)
+    slices = [np.arange(t, s, T) for t in range(T)]
+    perm = np.concatenate(slices).astype(np.int64)
+    bounds = np.array([0] + [len(sl) for sl in slices]).cumsum().astype(np.int64)
+    d, o = _lib.Engine(0), _lib.Engine(0)
+    d.set_gram_mode("dmma")
+    o.set_gram_mode("ozaki")
+    d.stage(v, y, perm, bounds, "fp64")
+    o.stage(v, y, perm, bounds, "fp64")
+    eta_d, oz_d = d.stage_info()
+    eta_o, oz_o = o.stage_info()
+    assert not oz_d and oz_o
+    for t in range(T):
+        gd, go = d.gram(t), o.gram(t)
+        scale = np.ones(m + 1)
+        scale[m] = np.sqrt(gd[m, m])  # the property row is not unit-norm
+        err = np.abs(go - gd) / np.outer(scale, scale)
+        assert err.max() <= eta_o[t] + eta_d[t], (t, err.max(), eta_o[t])
+    a = d.search(3, 10, 0, 2**62, "fast")
+    b = o.search(3, 10, 0, 2**62, "fast")
+    assert np.array_equal(a[1], b[1]) and bits_equal(a[0], b[0]) and bits_equal(a[2], b[2])
