@@ -12,11 +12,13 @@
 // which the screen's error model takes in place of the fp64 dot-product bound; a task whose
 // eta exceeds OZ_ETA_MAX falls back to the DMMA Gram (spiky rows).
 //
-// GEMM: one CTA per 128 x 128 upper-triangle tile of one task; 192 threads = TMA producer
-// warp, MMA warp (one elected thread issues tcgen05.mma; it also owns the TMEM allocation)
-// and 4 epilogue warps (tcgen05.ld by TMEM lane quadrant).  A pipeline stage is one 64-byte
-// K chunk of all 4 digit planes of both operands (8 TMA boxes of 128 x 64 B, SWIZZLE_64B,
-// 64 KB), 3 stages; each stage feeds 10 digit pairs x 2 MMAs of 128 x 128 x 32.
+// GEMM: one CTA per 128 x 64 upper-triangle tile of one task, two CTAs per SM (256 TMEM
+// columns and 97 KB of shared memory each, so one CTA's epilogue overlaps the other's main
+// loop); 192 threads = TMA producer warp, MMA warp (one elected thread issues tcgen05.mma; it
+// also owns the TMEM allocation) and 4 epilogue warps (tcgen05.ld by TMEM lane quadrant,
+// stores staged through shared memory so both G[r][c] and its mirror G[c][r] are coalesced).
+// A pipeline stage is one 64-byte K chunk of all 4 digit planes of both operands (8 TMA boxes,
+// SWIZZLE_64B, 48 KB), 2 stages; each stage feeds 10 digit pairs x 2 MMAs of 128 x 64 x 32.
 #include <algorithm>
 #include <cstdlib>
 
@@ -29,12 +31,15 @@ namespace {
 
 constexpr int OZ_S = 4;             // digits per value
 constexpr int OZ_NG = OZ_S;         // digit-weight groups d = 2 .. S + 1
-constexpr int OZ_BM = 128;          // tile rows = cols
+constexpr int OZ_BM = 128;          // tile rows (TMEM lanes)
+constexpr int OZ_BN = 64;           // tile cols: 4 groups x 64 = 256 TMEM columns -> 2 CTAs per SM
 constexpr int OZ_KC = 64;           // K bytes per stage
-constexpr int OZ_ST = 3;            // stages
-constexpr int OZ_TILE = OZ_BM * OZ_KC;              // 8 KB: one digit plane of one operand
-constexpr int OZ_STAGE = 2 * OZ_S * OZ_TILE;        // 64 KB
+constexpr int OZ_ST = 2;            // stages (per CTA; two CTAs per SM overlap)
+constexpr int OZ_TA = OZ_BM * OZ_KC;                // 8 KB: one digit plane of A
+constexpr int OZ_TB = OZ_BN * OZ_KC;                // 4 KB: one digit plane of B
+constexpr int OZ_STAGE = OZ_S * (OZ_TA + OZ_TB);    // 48 KB
 constexpr int OZ_SMEM = OZ_ST * OZ_STAGE + 1024;    // + alignment slack
+constexpr int OZ_TMEM_COLS = OZ_NG * OZ_BN;         // 256
 constexpr double OZ_C = 1.9e-8;     // error constant per unit-scaled entry and sample (S = 4)
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -50,8 +55,8 @@ __device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
     return d;
 }
 
-// kind::i8 instruction descriptor: s32 accumulate, s8 x s8, K-major A and B, M = 128, N = 128
-constexpr uint32_t OZ_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BM >> 3) << 17) |
+// kind::i8 instruction descriptor: s32 accumulate, s8 x s8, K-major A and B, M = 128, N = 64
+constexpr uint32_t OZ_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
                               ((uint32_t)(OZ_BM >> 4) << 24);
 
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
@@ -111,9 +116,11 @@ __global__ void k_oz_split(const double* __restrict__ Z, int64_t sp, const int64
     if (lane == 0) ex[(int64_t)t * R + f] = e;
 }
 
-// ---- GEMM: one 128 x 128 upper-triangle tile (fb <= gb) of one task per CTA ----
-__global__ void __launch_bounds__(192, 1) k_oz_gemm(const __grid_constant__ TmaDesc tmQ, const int64_t* __restrict__ koff,
-                                                   const int* __restrict__ ex, int64_t R, int nb, int64_t mp,
+// ---- GEMM: one 128 x 64 tile (rows fb, cols gb, gb >= 2 fb: every entry with row <= col
+// lies in exactly one such tile) of one task per CTA ----
+__global__ void __launch_bounds__(192, 2) k_oz_gemm(const __grid_constant__ TmaDesc tmA,
+                                                   const __grid_constant__ TmaDesc tmB, const int64_t* __restrict__ koff,
+                                                   const int* __restrict__ ex, int64_t R, int nbc, int64_t mp,
                                                    double* __restrict__ Gall) {
     extern __shared__ unsigned char oz_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)oz_raw + 1023) & ~(uintptr_t)1023);
@@ -122,11 +129,11 @@ __global__ void __launch_bounds__(192, 1) k_oz_gemm(const __grid_constant__ TmaD
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int t = blockIdx.y;
     int lin = blockIdx.x, fb = 0;
-    while (lin >= nb - fb) {
-        lin -= nb - fb;
+    while (lin >= nbc - 2 * fb) {
+        lin -= nbc - 2 * fb;
         ++fb;
     }
-    const int gb = fb + lin;
+    const int gb = 2 * fb + lin;
     const int64_t k0 = koff[t];
     const int nkc = (int)((koff[t + 1] - k0) / OZ_KC);
     if (threadIdx.x == 0) {
@@ -138,7 +145,8 @@ __global__ void __launch_bounds__(192, 1) k_oz_gemm(const __grid_constant__ TmaD
         mbar_fence_init();
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_addr(&tmem_slot)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_addr(&tmem_slot)),
+                     "r"(OZ_TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     tc_fence_before();
@@ -155,8 +163,8 @@ __global__ void __launch_bounds__(192, 1) k_oz_gemm(const __grid_constant__ TmaD
                 mbar_expect_tx(&full[s], (unsigned)OZ_STAGE);
                 const int x = (int)(k0 + (int64_t)kc * OZ_KC);
                 for (int a = 0; a < OZ_S; ++a) {
-                    tma_load_3d(st + a * OZ_TILE, &tmQ, x, fb * OZ_BM, a, &full[s]);
-                    tma_load_3d(st + (OZ_S + a) * OZ_TILE, &tmQ, x, gb * OZ_BM, a, &full[s]);
+                    tma_load_3d(st + a * OZ_TA, &tmA, x, fb * OZ_BM, a, &full[s]);
+                    tma_load_3d(st + OZ_S * OZ_TA + a * OZ_TB, &tmB, x, gb * OZ_BN, a, &full[s]);
                 }
             }
         }
@@ -173,31 +181,34 @@ __global__ void __launch_bounds__(192, 1) k_oz_gemm(const __grid_constant__ TmaD
                     for (int b = 1; a + b <= OZ_S + 1; ++b)
 #pragma unroll
                         for (int kk = 0; kk < OZ_KC / 32; ++kk) {
-                            const uint64_t da = sw64_desc(st + (a - 1) * OZ_TILE + kk * 32);
-                            const uint64_t db = sw64_desc(st + (OZ_S + b - 1) * OZ_TILE + kk * 32);
+                            const uint64_t da = sw64_desc(st + (a - 1) * OZ_TA + kk * 32);
+                            const uint64_t db = sw64_desc(st + OZ_S * OZ_TA + (b - 1) * OZ_TB + kk * 32);
                             const uint32_t acc = (kc == 0 && kk == 0 && a == 1) ? 0u : 1u;
-                            mma_i8(tmem + (uint32_t)(a + b - 2) * OZ_BM, da, db, acc);
+                            mma_i8(tmem + (uint32_t)(a + b - 2) * OZ_BN, da, db, acc);
                         }
                 mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
             }
             mma_commit(&done);
         }
-    } else {  // epilogue warps 2..5: TMEM lane quadrant (warp % 4) = tile rows
+    } else {  // epilogue warps 2..5: TMEM lane quadrant (warp % 4) = 32 tile rows
         mbar_wait(&done, 0u);
         tc_fence_after();
         const int quad = warp & 3;
         const int r = quad * 32 + lane;
-        const int64_t row = (int64_t)fb * OZ_BM + r;
-        const int er = ex[(int64_t)t * R + (row < R ? row : 0)];
+        const int64_t row0 = (int64_t)fb * OZ_BM + quad * 32;
+        const int64_t row = row0 + lane;
+        const int er = ex[(int64_t)t * R + row];
         double* G = Gall + (int64_t)t * mp * mp;
-        for (int c0 = 0; c0 < OZ_BM; c0 += 32) {
+        // staging for coalesced row stores: this warp's 32 rows x 32 cols (stage buffers are idle now)
+        double* stg = reinterpret_cast<double*>(sm) + quad * 32 * 33;
+        for (int c0 = 0; c0 < OZ_BN; c0 += 32) {
             double acc[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) acc[j] = 0.0;
 #pragma unroll
             for (int g = 0; g < OZ_NG; ++g) {
                 uint32_t v[32];
-                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(g * OZ_BM + c0);
+                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(g * OZ_BN + c0);
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
                     "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
@@ -212,24 +223,30 @@ __global__ void __launch_bounds__(192, 1) k_oz_gemm(const __grid_constant__ TmaD
 #pragma unroll
                 for (int j = 0; j < 32; ++j) acc[j] = fma((double)(int)v[j], w, acc[j]);  // exact products
             }
-            if (row < mp) {
-#pragma unroll 4
-                for (int j = 0; j < 32; ++j) {
-                    const int64_t col = (int64_t)gb * OZ_BM + c0 + j;
-                    if (col < mp && row <= col) {
-                        const double x = ldexp(acc[j], er + ex[(int64_t)t * R + col]);
-                        G[row * mp + col] = x;
-                        G[col * mp + row] = x;
-                    }
-                }
+            const int64_t col0 = (int64_t)gb * OZ_BN + c0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = ldexp(acc[j], er + ex[(int64_t)t * R + col0 + j]);
+            __syncwarp();
+            // rows of the warp, lanes over columns: G[row][col] for row <= col, coalesced
+            const int64_t col = col0 + lane;
+            for (int i = 0; i < 32; ++i) {
+                const int64_t rw = row0 + i;
+                if (rw < mp && col < mp && rw <= col) G[rw * mp + col] = stg[i * 33 + lane];
             }
+            // mirror: columns of the chunk, lanes over rows: G[col][row], coalesced
+            for (int j = 0; j < 32; ++j) {
+                const int64_t cl = col0 + j;
+                if (row < mp && cl < mp && row <= cl) G[cl * mp + row] = stg[lane * 33 + j];
+            }
+            __syncwarp();
         }
+        (void)r;
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(OZ_TMEM_COLS));
     }
 }
 
@@ -285,11 +302,14 @@ int launch_ozaki_gram(const double* Z, int64_t sp, const int64_t* zoff_d, const 
     }
     const int64_t warps = mp * T;
     k_oz_split<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(Z, sp, zoff_d, T, mp, R, koff_d, Q, KP, ex);
-    TmaDesc tm;
-    if (!make_tma_i8_3d(&tm, Q, (unsigned long long)KP, (unsigned long long)R, OZ_S, OZ_KC, OZ_BM)) return -1;
+    TmaDesc tmA, tmB;
+    if (!make_tma_i8_3d(&tmA, Q, (unsigned long long)KP, (unsigned long long)R, OZ_S, OZ_KC, OZ_BM) ||
+        !make_tma_i8_3d(&tmB, Q, (unsigned long long)KP, (unsigned long long)R, OZ_S, OZ_KC, OZ_BN))
+        return -1;
     cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
-    const int nb = (int)(R / OZ_BM);
-    k_oz_gemm<<<dim3((unsigned)(nb * (nb + 1) / 2), (unsigned)T), 192, OZ_SMEM, st>>>(tm, koff_d, ex, R, nb, mp, G);
+    const int nbr = (int)(R / OZ_BM), nbc = (int)(R / OZ_BN);
+    const int tiles = nbr * nbc - nbr * (nbr - 1);  // sum over fb of (nbc - 2 fb)
+    k_oz_gemm<<<dim3((unsigned)tiles, (unsigned)T), 192, OZ_SMEM, st>>>(tmA, tmB, koff_d, ex, R, nbc, mp, G);
     k_oz_eta<<<T, 256, 0, st>>>(ex, R, m, mp, G, rows_d, eta_d);
     return 0;
 }

@@ -22,6 +22,9 @@ KEYS = [
     ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 inst executed"),
     ("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", "DMMA pipe active"),
     ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (MUFU) inst executed"),
+    ("sm__pipe_tensor_op_imma_cycles_active.avg.pct_of_peak_sustained_active", "IMMA pipe active"),
+    ("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active", "tensor (tc) pipe active"),
+    ("lts__t_bytes.sum.per_second", "L2 throughput"),
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA (fp32/int) pipe active"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
