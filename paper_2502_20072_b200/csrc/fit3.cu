@@ -48,6 +48,9 @@ namespace {
 #ifndef L0S_C34_UNROLL
 #define L0S_C34_UNROLL 1
 #endif
+#ifndef L0S_FIT_SLOT0
+#define L0S_FIT_SLOT0 0
+#endif
 #ifndef L0S_PRUNE_ROWS
 #define L0S_PRUNE_ROWS 4
 #endif
@@ -65,7 +68,10 @@ struct Cfg {
     static constexpr int IB = c.IB;
     static constexpr int KSPAN = NW * P;
     static constexpr int TS = IB * (32 + KSPAN + 2);  // C[i, j-block] | C[i, k-span] | (c_i, pad)
-    static constexpr int BS = NT * TS;
+    // SLOT0: only the first task slot is staged (its rows feed every group); the other slots
+    // are read from L2 by the few row groups that survive the first (task pruning)
+    static constexpr bool SLOT0 = (NT > 1) && L0S_FIT_SLOT0;
+    static constexpr int BS = SLOT0 ? TS : NT * TS;
     static constexpr int MINB = c.MINB;
     static constexpr int UNROLL = c.UNROLL;  // rows of the i sweep in flight per thread
     // task pruning (NT > 1): rows per vote group, and per-thread smem slots for the
@@ -174,7 +180,7 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
             fence_proxy_async();
             mbar_expect_tx(&s_bar[buf], (unsigned)(BS * sizeof(double)));
 #pragma unroll
-            for (int t = 0; t < NT; ++t) {
+            for (int t = 0; t < (C::SLOT0 ? 1 : NT); ++t) {
                 const int row = (int)(tord[t] * mp) + ib0;
                 double* Tt = base + t * TS;
                 tma_load_2d(Tt, &a.tmJ, j0, row, &s_bar[buf]);
@@ -304,12 +310,22 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
             // one task slot of one row: acc[p] -= (w^2 + Bm) / d  (NT == 1: acc = acc d - q)
             // lb_t = base_t - A_t - (w^2 + B_t)/d >= base_t - A_t - (w^2 + Bm)/d
             auto task_row = [&](double (&acc)[P], int t, int ii) {
-                const double* Tt = T0 + t * TS;
-                const double g0 = Tt[ii * 32 + lane];
-                const double ci = Tt[IB * (32 + KSPAN) + 2 * ii];
-                const double D = fma(-g0, g0, 1.0);
-                const double V = fma(-g0, w0[t], ci);
-                double gk[P];
+                double g0, ci, gk[P];
+                if (C::SLOT0 && t > 0) {
+                    // surviving group: this slot's row straight from L2 (rows < mp: padded rows are finite)
+                    const double* Gi = a.G + (int64_t)tord[t] * mp * mp + (int64_t)(ib0 + ii) * mp;
+                    g0 = Gi[j];
+                    ci = Gi[m];
+#pragma unroll
+                    for (int p = 0; p < P; p += 2) {
+                        const double2 v = *reinterpret_cast<const double2*>(Gi + kbase + p);
+                        gk[p] = v.x;
+                        gk[p + 1] = v.y;
+                    }
+                } else {
+                const double* Tt = T0 + (C::SLOT0 ? 0 : t) * TS;
+                g0 = Tt[ii * 32 + lane];
+                ci = Tt[IB * (32 + KSPAN) + 2 * ii];
                 if constexpr (P == 1) {
                     gk[0] = Tt[IB * 32 + ii * KSPAN + warp];
                 } else {
@@ -320,6 +336,9 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
                         gk[p + 1] = v.y;
                     }
                 }
+                }
+                const double D = fma(-g0, g0, 1.0);
+                const double V = fma(-g0, w0[t], ci);
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
                     const double g1 = fma(-L10[p][t], g0, gk[p]);

@@ -21,10 +21,10 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
-    "p4_ib32_b1_r2": ("L0S_C34_P=4", "L0S_C34_IB=32", "L0S_C34_MINB=1", "L0S_PRUNE_ROWS=2"),
-    "p4_ib32_b1_r4": ("L0S_C34_P=4", "L0S_C34_IB=32", "L0S_C34_MINB=1", "L0S_PRUNE_ROWS=4"),
-    "p2_ib32_b1_r4": ("L0S_C34_P=2", "L0S_C34_IB=32", "L0S_C34_MINB=1", "L0S_PRUNE_ROWS=4"),
-    "p2_ib16_b2_r2": ("L0S_C34_P=2", "L0S_C34_IB=16", "L0S_C34_MINB=2", "L0S_PRUNE_ROWS=2", "L0S_CAP=128"),
+    "base": ("L0S_C34_IB=32",),
+    "slot0_ib32": ("L0S_FIT_SLOT0=1", "L0S_C34_IB=32"),
+    "slot0_ib64": ("L0S_FIT_SLOT0=1", "L0S_C34_IB=64"),
+    "slot0_ib128": ("L0S_FIT_SLOT0=1", "L0S_C34_IB=128"),
 }
 
 
