@@ -104,6 +104,7 @@ struct l0s_ctx {
     bool gram_timed = false;     // ev[2..3] bracket the Gram kernel of this stage
     int gram_mode = 0;           // L0S_GRAM_AUTO / _DMMA / _OZAKI (l0s_set_gram_mode)
     bool gram_ozaki = false;     // the staged Gram came from the INT8 path (eta on the device)
+    bool digits_ready = false;   // the normalize kernel wrote the Ozaki digits of this stage
     DBuf oz_q, oz_ex, oz_koff;
     // binomial table (k <= binom_n) x (a <= m)
     DBuf binom;
@@ -373,6 +374,7 @@ static int stage_prepare(l0s_ctx* c, const double* values, int64_t m, int64_t s,
 }
 
 static int gram_full(l0s_ctx* c);
+static bool ozaki_planned(const l0s_ctx* c);
 
 // stage after the Gram: unit diagonal, per-feature conditioning flags, host copies
 static int stage_post(l0s_ctx* c) {
@@ -427,11 +429,15 @@ static int stage_post(l0s_ctx* c) {
 }
 
 // The whole Gram in one go: the INT8 Ozaki path (tcgen05) when selected, else DMMA.
+static bool ozaki_planned(const l0s_ctx* c) {
+    return c->gram_mode == L0S_GRAM_OZAKI ||
+           (c->gram_mode == L0S_GRAM_AUTO && c->prec == L0S_PREC_FP64 && c->m >= 256);
+}
+
 static int gram_full(l0s_ctx* c) {
     const int nb = (int)(c->mp / 64);
     c->gram_ozaki = false;
-    if (c->gram_mode == L0S_GRAM_OZAKI || (c->gram_mode == L0S_GRAM_AUTO && c->prec == L0S_PREC_FP64 &&
-                                           c->m >= 256)) {
+    if (ozaki_planned(c)) {
         int64_t KP = 0;
         const int64_t qb = ozaki_q_bytes(c->mp, c->T, c->rpad_h.data(), &KP);
         const int64_t R = (c->mp + 127) / 128 * 128;
@@ -441,7 +447,7 @@ static int gram_full(l0s_ctx* c) {
         cudaEventRecord(c->ev[2], c->st);
         if (launch_ozaki_gram(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), c->rpad_h.data(), c->T, c->m, c->mp,
                               c->rowsd.as<double>(), c->G.as<double>(), c->eta_d.as<double>(), c->oz_q.as<int8_t>(),
-                              c->oz_ex.as<int>(), c->oz_koff.as<int64_t>(), c->st) == 0) {
+                              c->oz_ex.as<int>(), c->oz_koff.as<int64_t>(), c->digits_ready, c->st) == 0) {
             cudaEventRecord(c->ev[3], c->st);
             c->gram_timed = true;
             c->gram_ozaki = true;
@@ -476,11 +482,25 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
         yd = c->in_y.as<double>();
         pd = c->in_perm.as<int64_t>();
     }
+    // the INT8 Gram's digits come out of the normalize kernel (no second pass over Z)
+    DigitOut dig{nullptr, 0, 0, nullptr, nullptr};
+    c->digits_ready = false;
+    if (gram_cols && ozaki_planned(c)) {
+        int64_t KP = 0;
+        const int64_t qb = ozaki_q_bytes(c->mp, ntasks, c->rpad_h.data(), &KP);
+        const int64_t R = (c->mp + 127) / 128 * 128;
+        CK(c->oz_q.ensure((size_t)qb));
+        CK(c->oz_ex.ensure(sizeof(int) * ntasks * R));
+        CK(c->oz_koff.ensure(sizeof(int64_t) * (ntasks + 1)));
+        ozaki_prepare_digits(m, c->mp, ntasks, c->rpad_h.data(), c->oz_q.as<int8_t>(), c->oz_ex.as<int>(),
+                             c->oz_koff.as<int64_t>(), &dig, c->st);
+        c->digits_ready = true;
+    }
     auto rows_to_z = [&](int64_t f0, int64_t f1) {
         launch_gather(vd, yd, pd, m, s, precision, c->Xp.p, c->yp.p, f0, f1, c->st);
         launch_normalize(c->Xp.p, c->yp.p, precision, m, s, c->bounds_d.as<int64_t>(), c->zoff_d.as<int64_t>(),
                          ntasks, c->sp, c->Z.as<double>(), c->qf.as<double>(), c->un2.as<double>(),
-                         c->yyu.as<double>(), f0, f1, c->st);
+                         c->yyu.as<double>(), f0, f1, dig, c->st);
     };
     const int nb = (int)(c->mp / 64);
     const bool chunked = !is_device && (double)m * (double)s * 8.0 >= 32.0 * (1 << 20) && m >= 2 * 64;
@@ -492,9 +512,8 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
         if (gram_cols) return gram_full(c);
         return L0S_OK;
     }
-    // the INT8 Gram runs once all rows have landed (its digits need whole rows)
-    const bool ozaki = gram_cols && (c->gram_mode == L0S_GRAM_OZAKI ||
-                                     (c->gram_mode == L0S_GRAM_AUTO && precision == L0S_PREC_FP64 && m >= 256));
+    // the INT8 Gram runs once all rows have landed
+    const bool ozaki = gram_cols && c->digits_ready;
     if (ozaki) gram_cols = false;
     const int64_t R = (((m + l0s_ctx::kChunks - 1) / l0s_ctx::kChunks) + 63) / 64 * 64;
     // the copy stream starts after everything queued so far (buffers may be in use by a search)

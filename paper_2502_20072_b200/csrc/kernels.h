@@ -17,9 +17,17 @@ void launch_gather(const double* values, const double* y, const int64_t* perm, i
 // Per (feature, task): center, normalize, write Z rows (features 0..m-1 unit-norm
 // centered, row m = centered y), plus q = |x_c|^2/|x|^2 and |x|^2 per (task, feature)
 // and |y|^2 per task.
+// Ozaki digit planes written by the normalize kernel (Q == nullptr: none)
+constexpr int OZ_DIGITS = 4;
+struct DigitOut {
+    int8_t* Q;             // [OZ_DIGITS][R][KP]
+    int64_t R, KP;
+    const int64_t* koff;   // (T+1,) device: task segment offsets in K (multiples of 64)
+    int* ex;               // [T][R] row exponents
+};
 void launch_normalize(const void* Xp, const void* yp, int precision, int64_t m, int64_t s,
                       const int64_t* bounds_d, const int64_t* zoff_d, int T, int64_t sp, double* Z,
-                      double* qf, double* un2, double* yyu, int64_t f0, int64_t f1, cudaStream_t st);
+                      double* qf, double* un2, double* yyu, int64_t f0, int64_t f1, DigitOut dig, cudaStream_t st);
 
 // rho, dead, rho_cap, iforce from qf / un2 (stage.cu), and NaN rows/cols of dead features in G
 void launch_feature_flags(const double* qf, const double* un2, const double* rows, int64_t m, int64_t mp, int T,
@@ -47,9 +55,13 @@ void launch_mark_dead(double* G, const int32_t* dead, int ndead, int T, int64_t 
 
 // ---- Gram on the INT8 tensor cores by Ozaki splitting (ozaki.cu) ----
 int64_t ozaki_q_bytes(int64_t mp, int T, const int64_t* rpad_h, int64_t* KP_out);
+// digits_ready: the normalize kernel already wrote Q / ex (and koff_d); otherwise split Z here
 int launch_ozaki_gram(const double* Z, int64_t sp, const int64_t* zoff_d, const int64_t* rpad_h, int T, int64_t m,
                       int64_t mp, const double* rows_d, double* G, double* eta_d, int8_t* Q, int* ex, int64_t* koff_d,
-                      cudaStream_t st);
+                      bool digits_ready, cudaStream_t st);
+// Q / ex zero fill of the rows the normalize kernel does not write (m+1 .. R-1) and koff upload
+void ozaki_prepare_digits(int64_t m, int64_t mp, int T, const int64_t* rpad_h, int8_t* Q, int* ex, int64_t* koff_d,
+                          DigitOut* out, cudaStream_t st);
 
 // ---- bit-exact Householder (exact.cu) ----
 struct ExactArgs {

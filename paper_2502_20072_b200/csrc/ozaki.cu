@@ -29,7 +29,7 @@ namespace l0s {
 
 namespace {
 
-constexpr int OZ_S = 4;             // digits per value
+constexpr int OZ_S = OZ_DIGITS;     // digits per value (kernels.h: the normalize kernel writes them)
 constexpr int OZ_NG = OZ_S;         // digit-weight groups d = 2 .. S + 1
 constexpr int OZ_BM = 128;          // tile rows (TMEM lanes)
 constexpr int OZ_BN = 64;           // tile cols: 4 groups x 64 = 256 TMEM columns -> 2 CTAs per SM
@@ -286,22 +286,32 @@ int64_t ozaki_q_bytes(int64_t mp, int T, const int64_t* rpad_h, int64_t* KP_out)
 // Z (mp x sp, task t's columns [zoff_t, +rpad_t)) -> G (T x mp x mp) and eta (T); workspaces:
 // Q (ozaki_q_bytes), ex (T x R ints), koff_d (T+1 int64, filled here).  Returns 0, or -1 when
 // the TMA descriptor could not be built.
-int launch_ozaki_gram(const double* Z, int64_t sp, const int64_t* zoff_d, const int64_t* rpad_h, int T, int64_t m,
-                      int64_t mp, const double* rows_d, double* G, double* eta_d, int8_t* Q, int* ex, int64_t* koff_d,
-                      cudaStream_t st) {
+void ozaki_prepare_digits(int64_t m, int64_t mp, int T, const int64_t* rpad_h, int8_t* Q, int* ex, int64_t* koff_d,
+                          DigitOut* out, cudaStream_t st) {
     const int64_t R = (mp + OZ_BM - 1) / OZ_BM * OZ_BM;
     std::vector<int64_t> koff((size_t)T + 1, 0);
     for (int t = 0; t < T; ++t) koff[(size_t)t + 1] = koff[(size_t)t] + (rpad_h[t] + OZ_KC - 1) / OZ_KC * OZ_KC;
     const int64_t KP = koff[(size_t)T];
-    if (cudaMemcpyAsync(koff_d, koff.data(), sizeof(int64_t) * (T + 1), cudaMemcpyHostToDevice, st) != cudaSuccess)
-        return -1;
-    if (R > mp) {
-        for (int a = 0; a < OZ_S; ++a)
-            cudaMemsetAsync(Q + ((int64_t)a * R + mp) * KP, 0, (size_t)((R - mp) * KP), st);
-        cudaMemsetAsync(ex, 0, sizeof(int) * T * R, st);
+    cudaMemcpyAsync(koff_d, koff.data(), sizeof(int64_t) * (T + 1), cudaMemcpyHostToDevice, st);
+    for (int a = 0; a < OZ_S; ++a) cudaMemsetAsync(Q + ((int64_t)a * R + m + 1) * KP, 0, (size_t)((R - m - 1) * KP), st);
+    cudaMemsetAsync(ex, 0, sizeof(int) * T * R, st);
+    *out = DigitOut{Q, R, KP, koff_d, ex};
+}
+
+int launch_ozaki_gram(const double* Z, int64_t sp, const int64_t* zoff_d, const int64_t* rpad_h, int T, int64_t m,
+                      int64_t mp, const double* rows_d, double* G, double* eta_d, int8_t* Q, int* ex, int64_t* koff_d,
+                      bool digits_ready, cudaStream_t st) {
+    const int64_t R = (mp + OZ_BM - 1) / OZ_BM * OZ_BM;
+    DigitOut dig;
+    int64_t KP = 0;
+    if (!digits_ready) {
+        ozaki_prepare_digits(mp - 1, mp, T, rpad_h, Q, ex, koff_d, &dig, st);  // rows < mp come from Z here
+        KP = dig.KP;
+        const int64_t warps = mp * T;
+        k_oz_split<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(Z, sp, zoff_d, T, mp, R, koff_d, Q, KP, ex);
+    } else {
+        for (int t = 0; t < T; ++t) KP += (rpad_h[t] + OZ_KC - 1) / OZ_KC * OZ_KC;
     }
-    const int64_t warps = mp * T;
-    k_oz_split<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(Z, sp, zoff_d, T, mp, R, koff_d, Q, KP, ex);
     TmaDesc tmA, tmB;
     if (!make_tma_i8_3d(&tmA, Q, (unsigned long long)KP, (unsigned long long)R, OZ_S, OZ_KC, OZ_BM) ||
         !make_tma_i8_3d(&tmB, Q, (unsigned long long)KP, (unsigned long long)R, OZ_S, OZ_KC, OZ_BN))

@@ -31,11 +31,13 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // One warp per (row, task) of rows [f0, f1); row m is the property.
+// With dig.Q set, the warp also writes the row's Ozaki digits for the INT8 Gram (ozaki.cu):
+// e with max |z| < 2^e, and OZ_DIGITS signed 7-bit digits of z 2^-e into each digit plane.
 template <typename W>
 __global__ void k_normalize(const W* __restrict__ Xp, const W* __restrict__ yp, int64_t m, int64_t s,
                             const int64_t* __restrict__ bounds, const int64_t* __restrict__ zoff, int T,
                             int64_t sp, double* __restrict__ Z, double* __restrict__ qf,
-                            double* __restrict__ un2, double* __restrict__ yyu, int64_t f0, int64_t f1) {
+                            double* __restrict__ un2, double* __restrict__ yyu, int64_t f0, int64_t f1, DigitOut dig) {
     int lane = threadIdx.x & 31;
     int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (wid >= (f1 - f0) * T) return;
@@ -53,21 +55,46 @@ __global__ void k_normalize(const W* __restrict__ Xp, const W* __restrict__ yp, 
     double corr = 0.0;
     for (int64_t i = lane; i < r; i += 32) corr += (double)src[i] - mean;
     mean += warp_sum(corr) / (double)r;
-    double cs = 0.0, us = 0.0;
+    double cs = 0.0, us = 0.0, mc = 0.0;
     for (int64_t i = lane; i < r; i += 32) {
         double x = (double)src[i];
         double c = x - mean;
         cs = fma(c, c, cs);
         us = fma(x, x, us);
+        mc = fmax(mc, fabs(c));
     }
     cs = warp_sum(cs);
     us = warp_sum(us);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mc = fmax(mc, __shfl_xor_sync(L0S_FULL, mc, o));
     // features: unit-norm centered rows (0/0 -> NaN for a constant feature, which the
     // reference always rejects); property: centered, not normalized.
     double scale = (f < m) ? 1.0 / sqrt(cs) : 1.0;
     double* dst = Z + f * sp + zoff[t];
     int64_t rpad = zoff[t + 1] - zoff[t];
-    for (int64_t i = lane; i < rpad; i += 32) dst[i] = (i < r) ? ((double)src[i] - mean) * scale : 0.0;
+    if (!dig.Q) {
+        for (int64_t i = lane; i < rpad; i += 32) dst[i] = (i < r) ? ((double)src[i] - mean) * scale : 0.0;
+    } else {
+        // every written z satisfies |z| <= fl(mc * scale) (rounding is monotone) < 2^e
+        const double zmax = mc * scale;
+        int e = 0;
+        const bool finite = zmax > 0.0 && zmax < INFINITY;
+        if (finite) frexp(zmax, &e);
+        const int64_t k0 = dig.koff[t], klen = dig.koff[t + 1] - k0;
+        for (int64_t i = lane; i < klen; i += 32) {
+            const double z = (i < r) ? ((double)src[i] - mean) * scale : 0.0;
+            if (i < rpad) dst[i] = z;
+            double u = finite ? ldexp(z, -e) : 0.0;
+#pragma unroll
+            for (int a = 0; a < OZ_DIGITS; ++a) {
+                const double v = u * 128.0;  // exact
+                const double q = trunc(v);   // |q| <= 127
+                u = v - q;                   // exact remainder
+                dig.Q[((int64_t)a * dig.R + f) * dig.KP + k0 + i] = (int8_t)(int)q;
+            }
+        }
+        if (lane == 0) dig.ex[(int64_t)t * dig.R + f] = e;
+    }
     if (lane == 0) {
         if (f < m) {
             qf[(int64_t)t * m + f] = cs / us;
@@ -196,16 +223,16 @@ void launch_gather(const double* values, const double* y, const int64_t* perm, i
 
 void launch_normalize(const void* Xp, const void* yp, int precision, int64_t m, int64_t s,
                       const int64_t* bounds_d, const int64_t* zoff_d, int T, int64_t sp, double* Z,
-                      double* qf, double* un2, double* yyu, int64_t f0, int64_t f1, cudaStream_t st) {
+                      double* qf, double* un2, double* yyu, int64_t f0, int64_t f1, DigitOut dig, cudaStream_t st) {
     if (f1 <= f0) return;
     int64_t warps = (f1 - f0) * T;
     unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
     if (precision == 1)
         k_normalize<float><<<blocks, 256, 0, st>>>((const float*)Xp, (const float*)yp, m, s, bounds_d, zoff_d, T,
-                                                   sp, Z, qf, un2, yyu, f0, f1);
+                                                   sp, Z, qf, un2, yyu, f0, f1, dig);
     else
         k_normalize<double><<<blocks, 256, 0, st>>>((const double*)Xp, (const double*)yp, m, s, bounds_d, zoff_d,
-                                                    T, sp, Z, qf, un2, yyu, f0, f1);
+                                                    T, sp, Z, qf, un2, yyu, f0, f1, dig);
 }
 
 }  // namespace l0s

@@ -14,7 +14,7 @@ echo "launch list rc=$?"
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_fit3 -s 2 -c 1 -f \
     -o gpurun_out/${tag}_fit3 python tools/tune_fit.py one > gpurun_out/${tag}_fit3.log 2>&1
 echo "fit3 full rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gram -s 1 -c 1 -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_oz_gemm -s 1 -c 1 -f \
     -o gpurun_out/${tag}_gram python tools/time_stage.py > gpurun_out/${tag}_gram.log 2>&1
 echo "gram full rc=$?"
 (nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap \
