@@ -22,7 +22,9 @@ bit-exact refit of the candidates + certification.
 
 N > 1 (torchrun): contiguous rank ranges [r*N/W, (r+1)*N/W) per rank, each rank
 certifies its own top-k; the per-rank lists are all-gathered (NCCL) and merged
-by (score, rank) on rank 0.  Total work is fixed -> "scaling": "strong".
+by (score, rank) on rank 0.  Every rank stages the problem (the INT8 Gram is cheaper
+than a Gram shard plus its exchange, dist.sharded_stage).  Total work is fixed ->
+"scaling": "strong".
 """
 
 from __future__ import annotations
@@ -252,8 +254,9 @@ def main():
         device_step()
     barrier()
     ms_steps, fit_ms, gram_ms, launches = [], [], [], 0
-    # gather, normalize, gram, unit_diag, 5 feature-flag kernels (+ the shard unpack for N > 1)
-    stage_launches = 9 + (1 if world > 1 else 0)
+    # (gather + normalize) for the property row and for the features, the INT8 Gram (k_oz_gemm,
+    # k_oz_eta), unit diagonal, 5 feature-flag kernels
+    stage_launches = 12
     with ClockSampler(local) as clk:
         t_wall = time.perf_counter()
         for _ in range(args.steps):

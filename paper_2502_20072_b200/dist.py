@@ -39,10 +39,15 @@ def merge_candidates(parts, keep: int):
     return out
 
 
-def sharded_stage(eng, shape, bounds, precision, device_ptrs, group=None, all_gather=None):
+OZAKI_MIN_M = 256  # api.cu: the AUTO Gram is the INT8 one from this many features up (fp64)
+
+
+def sharded_stage(eng, shape, bounds, precision, device_ptrs, group=None, all_gather=None, force_shard=False):
     """Collective stage: every rank stages the whole problem, computes 1/world of the Gram
     (l0s_stage_shard) and the shards are all-gathered over NCCL straight into the buffer
-    l0s_stage_finish scatters from.  world == 1 is a plain stage.
+    l0s_stage_finish scatters from.  world == 1 is a plain stage, and so is every problem whose
+    Gram runs on the INT8 tensor cores (cheaper than a shard plus the exchange) unless
+    ``force_shard``.
 
     ``all_gather(out, inp)`` defaults to ``torch.distributed.all_gather_into_tensor``.
     """
@@ -53,7 +58,9 @@ def sharded_stage(eng, shape, bounds, precision, device_ptrs, group=None, all_ga
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     me = dist.get_rank(group) if dist.is_initialized() else 0
-    if world == 1:
+    if world == 1 or (precision == "fp64" and int(shape[0]) >= OZAKI_MIN_M and not force_shard):
+        # the INT8 tensor-core Gram (Ozaki digits) costs one GPU less than a 1/world DMMA shard
+        # plus the exchange for world <= 8 (C3: 0.25 ms vs 1.78/world + ~0.12 ms): stage locally
         eng.stage(shape, None, None, bounds, precision, device_ptrs=device_ptrs)
         return
     m, ntasks = int(shape[0]), len(bounds) - 1
