@@ -137,11 +137,13 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
     __shared__ int s_tord[NT];
     __shared__ unsigned char s_force[2][IB];  // iforce flags of the staged rows
     __shared__ __align__(8) unsigned long long s_bar[2];  // TMA completion, one per tile buffer
+    __shared__ __align__(8) unsigned long long s_hbar;    // TMA completion of the unit's hoist block
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t m = a.m, mp = a.mp;
     if (tid == 0) {
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
+        mbar_init(&s_hbar, 1);
         mbar_fence_init();
         // sweep order of the tasks: largest |y_c|^2 first, so that the first task's share of the
         // bound alone already exceeds the threshold for almost every row (task pruning below)
@@ -159,7 +161,13 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
     }
     __syncthreads();
     const int* tord = s_tord;  // read where the hoist / tile loads need it (rare)
-    unsigned parity[2] = {0u, 0u};
+    unsigned parity[2] = {0u, 0u}, hpar = 0u;
+    // The unit's hoist block goes through TMA into tile buffer 1 (idle until the sweep's first
+    // prefetch): per task slot C[k-span, j-block] (IB x 32, IB == KSPAN) and, when it fits, the
+    // property row's k-span c_k (a second box, first row used).
+    constexpr bool HC = 64 <= 34 + KSPAN;
+    constexpr int HS = (HC ? 2 : 1) * IB * 32;  // doubles per task slot
+    static_assert(IB == KSPAN && NT * HS <= BS, "hoist block must fit tile buffer 1");
     // per-thread constants, touched by the hoist, threshold updates and pruned rows:
     // sK[0][p] = sum_t (base_t - A_t) (NT >= 3: sK[t][p] = (base_t - A_t) * shrink, t >= 1)
     // (slot-major, thread-minor: conflict-free per-thread accesses)
@@ -205,6 +213,16 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
         const int j = j0 + lane;
         const int kbase = k0 + warp * P;
         const int i_lo = U.z, i_hi = U.w;
+        double* Hb = sm + BS;  // tile buffer 1
+        if (tid == 0) {
+            fence_proxy_async();  // the previous unit's reads of buffer 1 precede these writes
+            mbar_expect_tx(&s_hbar, (unsigned)(NT * HS * sizeof(double)));
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                tma_load_2d(Hb + t * HS, &a.tmJ, j0, (int)(tord[t] * mp) + k0, &s_hbar);
+                if (HC) tma_load_2d(Hb + t * HS + IB * 32, &a.tmJ, k0, (int)(tord[t] * mp + m), &s_hbar);
+            }
+        }
         load_tiles(0, i_lo, j0, k0);
         if (!a.collect) {
             // shared threshold: the global bound histogram and the other warps' lists
@@ -222,6 +240,8 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
         double K1r[P];  // NT == 2: task slot 1's (base - A) * shrink in registers
         unsigned valid = 0, bad = 0, forced = 0;
         const int jj = j < m ? j : (int)m - 1;
+        mbar_wait(&s_hbar, hpar);
+        hpar ^= 1u;
         // per-task scalars of this unit, loaded once (live during the hoist only)
         double Y2v[NT], gamv[NT], etav[NT], ynv[NT], rjv[NT];
         const double* Gs[NT];
@@ -247,8 +267,8 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
                 const int tk = tord[t];
                 const double* Gt = Gs[t];
                 const double Y2 = Y2v[t];
-                const double cjk = Gt[(int64_t)k * mp + j];
-                const double ck = Gt[m * mp + k];
+                const double cjk = Hb[t * HS + (k - k0) * 32 + lane];
+                const double ck = HC ? Hb[t * HS + IB * 32 + (k - k0)] : Gt[m * mp + k];
                 const double d1 = fma(-cjk, cjk, 1.0);
                 const double r1 = rcp_newton(d1);
                 const double v1 = fma(-cjk, w0[t], ck);
@@ -292,6 +312,7 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
             }
         };
         set_kq();
+        __syncthreads();  // every warp is done with the hoist block: buffer 1 may take tile 1
 
         // ---------------- sweep i ----------------
         const int nib = (i_hi - i_lo + IB - 1) / IB;
