@@ -305,6 +305,8 @@ int l0s_create(int device, l0s_ctx** out) {
     }
     for (auto& e : c->ev) cudaEventCreate(&e);
     for (auto& e : c->cev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (const char* g = getenv("L0S_GRAM_MODE"))  // experiments: auto | dmma | ozaki
+        c->gram_mode = !strcmp(g, "dmma") ? L0S_GRAM_DMMA : (!strcmp(g, "ozaki") ? L0S_GRAM_OZAKI : L0S_GRAM_AUTO);
     *out = c;
     return L0S_OK;
 }
