@@ -391,7 +391,7 @@ static int stage_post(l0s_ctx* c) {
     CK(c->umin.ensure(sizeof(double) * ntasks));
     CK(c->iforce.ensure((size_t)m));
     CK(c->dead.ensure((size_t)m));
-    launch_feature_flags(c->qf.as<double>(), c->un2.as<double>(), c->rowsd.as<double>(), m, c->mp, ntasks,
+    launch_feature_flags(c->prec == L0S_PREC_FP32 ? 1e-5 : 1e-10, c->prec == L0S_PREC_FP32, c->qf.as<double>(), c->un2.as<double>(), c->rowsd.as<double>(), m, c->mp, ntasks,
                          c->umin.as<double>(), c->rho.as<double>(), c->rho_cap.as<double>(),
                          c->dead.as<unsigned char>(), c->iforce.as<unsigned char>(), c->G.as<double>(),
                          c->yyu.as<double>(), c->ynorm.as<double>(), c->st);
@@ -415,7 +415,7 @@ static int stage_post(l0s_ctx* c) {
             gram_full(c);
             c->gram_mode = prev;
             launch_unit_diag(c->G.as<double>(), ntasks, m, c->mp, c->st);
-            launch_feature_flags(c->qf.as<double>(), c->un2.as<double>(), c->rowsd.as<double>(), m, c->mp, ntasks,
+            launch_feature_flags(c->prec == L0S_PREC_FP32 ? 1e-5 : 1e-10, c->prec == L0S_PREC_FP32, c->qf.as<double>(), c->un2.as<double>(), c->rowsd.as<double>(), m, c->mp, ntasks,
                                  c->umin.as<double>(), c->rho.as<double>(), c->rho_cap.as<double>(),
                                  c->dead.as<unsigned char>(), c->iforce.as<unsigned char>(), c->G.as<double>(),
                                  c->yyu.as<double>(), c->ynorm.as<double>(), c->st);
@@ -432,8 +432,7 @@ static int stage_post(l0s_ctx* c) {
 
 // The whole Gram in one go: the INT8 Ozaki path (tcgen05) when selected, else DMMA.
 static bool ozaki_planned(const l0s_ctx* c) {
-    return c->gram_mode == L0S_GRAM_OZAKI ||
-           (c->gram_mode == L0S_GRAM_AUTO && c->prec == L0S_PREC_FP64 && c->m >= 256);
+    return c->gram_mode == L0S_GRAM_OZAKI || (c->gram_mode == L0S_GRAM_AUTO && c->m >= 256);
 }
 
 static int gram_full(l0s_ctx* c) {
@@ -677,6 +676,7 @@ static void fill_fit_common(l0s_ctx* c, FitArgs& a, int n) {
     a.N_total = binom_sat(c->m, n);
     double tol = c->prec == L0S_PREC_FP32 ? 1e-5 : 1e-10;
     a.tol2 = tol * tol;
+    a.ref_fp32 = c->prec == L0S_PREC_FP32 ? 1 : 0;
 }
 
 int l0s_screen_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags) {
@@ -758,6 +758,17 @@ static int search_exact_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_
 
 // QR screen of the `nill` ranks in c->ill, then bit-exact refit of the ones that can matter.
 static int screen_ill(l0s_ctx* c, int n, int64_t nill, int64_t keep, std::vector<Cand>& best, l0s_stats* st) {
+    if (c->prec == L0S_PREC_FP32) {
+        // the fp64 QR screen cannot bound the reference's float32 arithmetic on an
+        // ill-conditioned system: every such tuple is refit bit-exactly
+        st->n_ill_refit += nill;
+        std::vector<Cand> more;
+        int rc = exact_ranks_to_host(c, n, c->ill.as<int64_t>(), nill, more, &st->n_launches, &c->recs);
+        if (rc) return rc;
+        st->n_candidates += nill;
+        merge_best(best, more, keep);
+        return L0S_OK;
+    }
     CK(c->qr_ssr.ensure(sizeof(double) * nill * c->T));
     CK(c->qr_ratio.ensure(sizeof(double) * nill * c->T));
     CK(c->qr_score.ensure(sizeof(double) * nill));
@@ -1022,13 +1033,13 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
     cudaEventCreate(&t1);
     cudaEventRecord(t0, c->st);
     // the screen's error model is for fp64 arithmetic in the reference (precision="fp64")
-    bool fast_ok = (n >= 2 && n <= 4) && c->T <= fit3_max_tasks() && keep <= 96 && c->prec == L0S_PREC_FP64;
+    bool fast_ok = (n >= 2 && n <= 4) && c->T <= fit3_max_tasks() && keep <= 96;
     bool use_fast;
     if (mode == L0S_MODE_FAST) {
         if (!fast_ok) {
             cudaEventDestroy(t0);
             cudaEventDestroy(t1);
-            return fail(L0S_EINVAL, "screened path needs n in {2, 3, 4}, ntasks <= %d, keep <= 96, fp64",
+            return fail(L0S_EINVAL, "screened path needs n in {2, 3, 4}, ntasks <= %d, keep <= 96",
                         fit3_max_tasks());
         }
         use_fast = true;

@@ -9,6 +9,7 @@
 namespace l0s {
 
 constexpr double kEps = 1.1102230246251565e-16;  // 2^-53, unit roundoff of fp64
+constexpr double kEps32 = 5.9604644775390625e-08;  // 2^-24, unit roundoff of fp32
 
 // Order-preserving map double -> uint64 (NaN excluded) so that a global
 // threshold can be lowered with one atomicMin on an integer.

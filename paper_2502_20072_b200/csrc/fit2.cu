@@ -40,12 +40,12 @@ __device__ __noinline__ int eval_tuple2(const FitArgs& a, int64_t i, int64_t j, 
         const double* rt_ = a.rho + (int64_t)t * m;
         const double rx = fmax(rt_[i], rt_[j]);
         double At, Bt, vk;
-        task_bound(2, a.eta[t], ref_gamma(a.rowsd[t], 2), rx, Y2, a.ynorm[t], trh, At, Bt, vk);
+        task_bound(2, a.eta[t], ref_gamma(a.rowsd[t], 2, a.ref_fp32), rx, Y2, a.ynorm[t], trh, At, Bt, vk);
         const double g0 = Gt[i * mp + j], ci = Gt[i * mp + m];
         const double d = fma(-g0, g0, 1.0);
         const double w = fma(-g0, w0, ci);
         const double tr = trh + (1.0 + trh) / d;
-        if (!(d > 0.0) || !(vk * (1.0 + 2.0 * tr) <= FO_LIM) || !(At + Bt / d <= LOOSE * Y2)) cond = false;
+        if (!(d > 0.0) || !(vk * (1.0 + 2.0 * tr) <= FO_LIM) || !(At + Bt / d <= (a.ref_fp32 ? LOOSE32 : LOOSE) * Y2)) cond = false;
         lb += base - At - fma(w, w, Bt) / d;
         ub += base + At - fma(w, w, -Bt) / d;
         const int64_t f[2] = {i, j};
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256, 2) k_fit2(const __grid_constant__ FitArgs
             const double base = Y2 - w0[t] * w0[t];
             double At, Bt, vk;
             const double rh = fmax(a.rho_cap[t], a.rho[(int64_t)t * m + jj]);
-            task_bound(2, a.eta[t], ref_gamma(a.rowsd[t], 2), rh, Y2, a.ynorm[t], 1.0, At, Bt, vk);
+            task_bound(2, a.eta[t], ref_gamma(a.rowsd[t], 2, a.ref_fp32), rh, Y2, a.ynorm[t], 1.0, At, Bt, vk);
             K += base - At;
             Bm = fmax(Bm, Bt);
             if (!(vk * 3.0 <= FO_LIM)) bad = true;

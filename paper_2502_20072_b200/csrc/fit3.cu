@@ -107,7 +107,7 @@ __device__ __noinline__ int eval_tuple3(const FitArgs& a, int64_t i, int64_t j, 
         const double* rt_ = a.rho + (int64_t)t * m;
         const double rx = fmax(rt_[i], fmax(rt_[j], rt_[k]));
         double At, Bt, vk;
-        task_bound(3, a.eta[t], ref_gamma(a.rowsd[t], 3), rx, Y2, a.ynorm[t], trh, At, Bt, vk);
+        task_bound(3, a.eta[t], ref_gamma(a.rowsd[t], 3, a.ref_fp32), rx, Y2, a.ynorm[t], trh, At, Bt, vk);
         if (!(d1 > 0.0) || !(vk * (1.0 + 3.0 * trh) <= FO_LIM)) cond = false;
         const double g0 = Gt[i * mp + j], ci = Gt[i * mp + m], gk = Gt[i * mp + k];
         const double D = fma(-g0, g0, 1.0);
@@ -117,7 +117,7 @@ __device__ __noinline__ int eval_tuple3(const FitArgs& a, int64_t i, int64_t j, 
         const double d = fma(-g1, e1, D);
         const double w = fma(-e1, v1, V);
         const double tr = trh + (1.0 + trh) / d;
-        if (!(d > 0.0) || !(vk * (1.0 + 3.0 * tr) <= FO_LIM) || !(At + Bt / d <= LOOSE * Y2)) cond = false;
+        if (!(d > 0.0) || !(vk * (1.0 + 3.0 * tr) <= FO_LIM) || !(At + Bt / d <= (a.ref_fp32 ? LOOSE32 : LOOSE) * Y2)) cond = false;
         lb += base - At - fma(w, w, Bt) / d;
         ub += base + At - fma(w, w, -Bt) / d;
         const int64_t f[3] = {i, j, k};
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
             Gs[t] = a.G + (int64_t)tk * mp * mp;
             w0[t] = Gs[t][m * mp + j];
             Y2v[t] = Gs[t][m * mp + m];
-            gamv[t] = ref_gamma(a.rowsd[tk], 3);
+            gamv[t] = ref_gamma(a.rowsd[tk], 3, a.ref_fp32);
             etav[t] = a.eta[tk];
             ynv[t] = a.ynorm[tk];
             rjv[t] = fmax(a.rho_cap[tk], a.rho[(int64_t)tk * m + jj]);

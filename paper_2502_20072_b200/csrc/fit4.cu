@@ -73,7 +73,7 @@ __device__ __noinline__ int eval_tuple4(const FitArgs& a, int64_t i, int64_t j, 
         const double* rt_ = a.rho + (int64_t)t * m;
         const double rx = fmax(fmax(rt_[i], rt_[j]), fmax(rt_[k], rt_[l]));
         double At, Bt, vk;
-        task_bound(4, a.eta[t], ref_gamma(a.rowsd[t], 4), rx, Y2, a.ynorm[t], h.tr3, At, Bt, vk);
+        task_bound(4, a.eta[t], ref_gamma(a.rowsd[t], 4, a.ref_fp32), rx, Y2, a.ynorm[t], h.tr3, At, Bt, vk);
         if (!(h.d1 > 0.0) || !(h.d2 > 0.0) || !(vk * (1.0 + 4.0 * h.tr3) <= FO_LIM)) cond = false;
         const double g0 = Gt[i * mp + j], ci = Gt[i * mp + m];
         const double D = fma(-g0, g0, 1.0);
@@ -87,7 +87,7 @@ __device__ __noinline__ int eval_tuple4(const FitArgs& a, int64_t i, int64_t j, 
         const double d = fma(-t2, g2, D1);
         const double w = fma(-g2, h.s2, V1);
         const double tr = h.tr3 + (1.0 + h.tr3) / d;
-        if (!(d > 0.0) || !(vk * (1.0 + 4.0 * tr) <= FO_LIM) || !(At + Bt / d <= LOOSE * Y2)) cond = false;
+        if (!(d > 0.0) || !(vk * (1.0 + 4.0 * tr) <= FO_LIM) || !(At + Bt / d <= (a.ref_fp32 ? LOOSE32 : LOOSE) * Y2)) cond = false;
         lb += h.base - At - fma(w, w, Bt) / d;
         ub += h.base + At - fma(w, w, -Bt) / d;
         const int64_t f[4] = {i, j, k, l};
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs
                 double At, Bt, vk;
                 const double* rt_ = a.rho + (int64_t)t * m;
                 const double rh = fmax(fmax(a.rho_cap[t], rt_[jj]), fmax(rt_[k], rt_[ll]));
-                task_bound(4, a.eta[t], ref_gamma(a.rowsd[t], 4), rh, Y2, a.ynorm[t], h.tr3, At, Bt, vk);
+                task_bound(4, a.eta[t], ref_gamma(a.rowsd[t], 4, a.ref_fp32), rh, Y2, a.ynorm[t], h.tr3, At, Bt, vk);
                 L10[t] = h.L10;
                 rd1[t] = h.rd1;
                 s1[t] = h.s1;

@@ -17,19 +17,21 @@ constexpr int CAP = L0S_CAP;          // per-warp candidate buffer (K' <= CAP - 
 constexpr double FO_LIM = 1e-3;       // first-order validity: (eta + gam rho)(1 + n tr) <= FO_LIM
 constexpr double RANK_SLACK = 1.01;   // safety factor on the rank-rule certificate
 constexpr double LOOSE = 1e-3;        // bounds looser than this fraction of |y_c|^2 go to the exact kernel
+constexpr double LOOSE32 = 3e-2;      // the same for precision="fp32" (its rounding model is 2^29 x coarser)
 
 // Error model, one task, n features, tr = trace of the inverse of the
 // normalized n x n block, tr <= trh + (1 + trh)/d (trh: hoisted (n-1) x (n-1) block):
 //   |ssr_gram - ssr_true| <= 2 eta Y2 (1 + n tr)
 //   |ssr_ref  - ssr_true| <= 4 gam |y_c||y| + 2 gam rho Y2 (1 + n tr)
 // so ssr_ref >= ssr_gram - A - B/d with K = 2 (eta + gam rho),
-//   A = 2 gam (|y_c|^2 + |y|^2) + K Y2 (1 + n trh),   B = n K Y2 (1 + trh)
-// (4ab <= 2(a^2 + b^2) removes the square root), valid while vk (1 + n tr) <= FO_LIM.
+//   A = 4 gam |y_c| |y| + K Y2 (1 + n trh),   B = n K Y2 (1 + trh)
+// valid while vk (1 + n tr) <= FO_LIM.  (|y_c| = sqrt(Y2), |y| = yn: a per-task constant; the
+// product matters for a property with a large mean, |y| >> |y_c|, and for fp32's larger gam.)
 __device__ __forceinline__ void task_bound(int n, double eta, double gam, double rho, double Y2, double yn,
                                            double trh, double& A, double& B, double& vk) {
     vk = eta + gam * rho;
     const double K = 2.0 * vk;
-    A = 2.0 * gam * (Y2 + yn * yn) + K * Y2 * (1.0 + n * trh);
+    A = 4.0 * gam * sqrt(Y2) * yn + K * Y2 * (1.0 + n * trh);
     B = n * K * Y2 * (1.0 + trh);
 }
 
@@ -39,8 +41,14 @@ __device__ __forceinline__ void task_bound(int n, double eta, double gam, double
 // SIAM J. Sci. Comput. 41(5), 2019); lambda = 8 puts the failure probability below 1e-13.
 // (The worst-case r u growth would make every feature whose mean/std ratio exceeds ~1e6
 // uncertifiable at r = 5000, although the reference's actual error there is ~1e-7.)
-__device__ __host__ __forceinline__ double ref_gamma(double rows, int n) {
-    return 2.0 * 8.0 * sqrt(rows + 1.0) * (n + 2) * kEps;
+//
+// precision="fp32" (numba's mixed typing, lsq.py:61-110 on float32 data): every product is
+// rounded to float32 (relative 2^-24 per term, no growth with r because the sums run in
+// float64) and every stored reflection result is rounded to float32 once per step, so the
+// columnwise backward error is O((n+2) u32) plus the float64 accumulation term.
+__device__ __host__ __forceinline__ double ref_gamma(double rows, int n, bool fp32 = false) {
+    return fp32 ? 2.0 * 8.0 * (n + 2) * (kEps32 + sqrt(rows + 1.0) * kEps)
+                : 2.0 * 8.0 * sqrt(rows + 1.0) * (n + 2) * kEps;
 }
 
 // 1/d without the IEEE-division subroutine call: MUFU seed + two Newton steps (a few ulp,
@@ -73,7 +81,7 @@ __device__ __forceinline__ bool rank_certain(const FitArgs& a, int t, const int6
         hi = fmax(hi, u);
     }
     const double lo = fmin(fc_min / (tr * (1.0 + 4.0 * FO_LIM)), rt) / (2.0 * (1.0 + mean2 / rt));
-    const double tl = sqrt(a.tol2) + 4.0 * ref_gamma(rt, N);  // the reference's rounding of R
+    const double tl = sqrt(a.tol2) + 4.0 * ref_gamma(rt, N, a.ref_fp32);  // the reference's rounding of R
     return lo >= tl * tl * hi * RANK_SLACK;
 }
 

@@ -30,7 +30,7 @@ void launch_normalize(const void* Xp, const void* yp, int precision, int64_t m, 
                       double* qf, double* un2, double* yyu, int64_t f0, int64_t f1, DigitOut dig, cudaStream_t st);
 
 // rho, dead, rho_cap, iforce from qf / un2 (stage.cu), and NaN rows/cols of dead features in G
-void launch_feature_flags(const double* qf, const double* un2, const double* rows, int64_t m, int64_t mp, int T,
+void launch_feature_flags(double tol, int fp32, const double* qf, const double* un2, const double* rows, int64_t m, int64_t mp, int T,
                           double* umin, double* rho, double* rho_cap, unsigned char* dead, unsigned char* iforce,
                           double* G, const double* yyu, double* ynorm, cudaStream_t st);
 
@@ -149,6 +149,7 @@ struct FitArgs {
     int64_t rank_lo, rank_hi;
     int ranged;
     double tol2;             // reference rank rule: tol^2
+    int ref_fp32;            // the reference computes in float32 (precision="fp32"): its rounding model
     // candidate state
     int kc;                  // per-warp keep K'
     int collect;             // 1 = collect every lb < theta0 into coll_*

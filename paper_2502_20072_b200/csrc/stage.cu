@@ -140,7 +140,7 @@ __global__ void k_task_umin(const double* __restrict__ un2, int64_t m, double* _
     if (threadIdx.x == 0) umin[t] = v;
 }
 
-__global__ void k_feature_flags(const double* __restrict__ qf, const double* __restrict__ umin,
+__global__ void k_feature_flags(double tol, int fp32, const double* __restrict__ qf, const double* __restrict__ umin,
                                 const double* __restrict__ rows, int64_t m, int T, double* __restrict__ rho,
                                 unsigned char* __restrict__ dead) {
     const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -152,8 +152,8 @@ __global__ void k_feature_flags(const double* __restrict__ qf, const double* __r
         rho[(int64_t)t * m + f] = (rf == rf && rf < INFINITY) ? rf : INFINITY;
         // |R_nn| <= sqrt(r q) and max|R| >= min_f |f|: certain rejection (n <= 4 rounding model)
         const double r = rows[t];
-        const double gam = 2.0 * 8.0 * sqrt(r + 1.0) * 6.0 * kEps;
-        const double lim = 0.5 * 1e-10 * sqrt(umin[t] / fmax(r, 1.0)) - 4.0 * gam;
+        const double gam = fp32 ? 2.0 * 8.0 * 6.0 * (kEps32 + sqrt(r + 1.0) * kEps) : 2.0 * 8.0 * sqrt(r + 1.0) * 6.0 * kEps;
+        const double lim = 0.5 * tol * sqrt(umin[t] / fmax(r, 1.0)) - 4.0 * gam;
         if (lim > 0.0 && sqrt(q) < lim) d = true;
     }
     dead[f] = d ? 1 : 0;
@@ -200,12 +200,12 @@ __global__ void k_mark_dead_rows(double* __restrict__ G, const unsigned char* __
     }
 }
 
-void launch_feature_flags(const double* qf, const double* un2, const double* rows, int64_t m, int64_t mp, int T,
+void launch_feature_flags(double tol, int fp32, const double* qf, const double* un2, const double* rows, int64_t m, int64_t mp, int T,
                           double* umin, double* rho, double* rho_cap, unsigned char* dead, unsigned char* iforce,
                           double* G, const double* yyu, double* ynorm, cudaStream_t st) {
     const unsigned fb = (unsigned)((m + 255) / 256);
     k_task_umin<<<T, 256, 0, st>>>(un2, m, umin, yyu, ynorm);
-    k_feature_flags<<<fb, 256, 0, st>>>(qf, umin, rows, m, T, rho, dead);
+    k_feature_flags<<<fb, 256, 0, st>>>(tol, fp32, qf, umin, rows, m, T, rho, dead);
     k_task_rhocap<<<T, 256, 0, st>>>(rho, dead, m, rho_cap);
     k_feature_iforce<<<fb, 256, 0, st>>>(rho, rho_cap, dead, m, T, iforce);
     k_mark_dead_rows<<<dim3(4, (unsigned)m), 256, 0, st>>>(G, dead, m, mp, T);
