@@ -851,7 +851,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
                : n == 3 ? fit3_launch(fa, c->nsm, c->st)
                         : fit4_launch(fa, c->nsm, c->st);
     };
-    const int slots = grid * fit_slots_per_cta();
+    const int slots = grid * (n == 3 ? fit3_slots_per_cta() : fit_slots_per_cta());
     const int64_t ill_cap = (int64_t)1 << 26;  // 512 MB of ranks; overflow is reported, never dropped
     CK(c->ucount.ensure(sizeof(int) * 4));
     CK(c->theta_g.ensure(sizeof(unsigned long long)));

@@ -48,6 +48,11 @@ namespace {
 #ifndef L0S_C34_UNROLL
 #define L0S_C34_UNROLL 1
 #endif
+#ifndef L0S_FIT3_NW
+#define L0S_FIT3_NW 8
+#endif
+constexpr int NW3 = L0S_FIT3_NW;  // warps per CTA of the dim-3 sweep (k-span = NW3 x P)
+constexpr int NT3 = NW3 * 32;
 #ifndef L0S_FIT_SLOT0
 #define L0S_FIT_SLOT0 0
 #endif
@@ -66,7 +71,7 @@ struct Cfg {
     static constexpr CfgT c = (NT <= 2) ? kCfg12 : (NT <= 4 ? kCfg34 : kCfg58);
     static constexpr int P = c.P;
     static constexpr int IB = c.IB;
-    static constexpr int KSPAN = NW * P;
+    static constexpr int KSPAN = NW3 * P;
     static constexpr int TS = IB * (32 + KSPAN + 2);  // C[i, j-block] | C[i, k-span] | (c_i, pad)
     // SLOT0: only the first task slot is staged (its rows feed every group); the other slots
     // are read from L2 by the few row groups that survive the first (task pruning)
@@ -78,7 +83,7 @@ struct Cfg {
     // per-task constants (P x KS doubles: the total, then tasks 1..NT-1 for NT >= 3)
     static constexpr int R = (NT == 1) ? 1 : L0S_PRUNE_ROWS;
     static constexpr int KS = (NT >= 3) ? NT : 1;
-    static constexpr size_t smem_bytes = (size_t)2 * BS * 8 + (size_t)NW * CAP * 16 + (size_t)256 * P * KS * 8;
+    static constexpr size_t smem_bytes = (size_t)2 * BS * 8 + (size_t)NW3 * CAP * 16 + (size_t)NT3 * P * KS * 8;
 };
 
 // Exact lower bound of one tuple (i < j < k) read straight from the Gram, with the
@@ -129,7 +134,7 @@ __device__ __noinline__ int eval_tuple3(const FitArgs& a, int64_t i, int64_t j, 
 }
 
 template <int NT>
-__global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_constant__ FitArgs a) {
+__global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_constant__ FitArgs a) {
     using C = Cfg<NT>;
     constexpr int P = C::P, IB = C::IB, TS = C::TS, BS = C::BS, KSPAN = C::KSPAN, R = C::R, KS = C::KS;
     extern __shared__ __align__(128) double sm[];
@@ -167,14 +172,14 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
     // property row's k-span c_k (a second box, first row used).
     constexpr bool HC = 64 <= 34 + KSPAN;
     constexpr int HS = (HC ? 2 : 1) * IB * 32;  // doubles per task slot
-    static_assert(IB == KSPAN && NT * HS <= BS, "hoist block must fit tile buffer 1");
+    constexpr bool HT = IB == KSPAN && NT * HS <= BS;  // else the hoist reads L2
     // per-thread constants, touched by the hoist, threshold updates and pruned rows:
     // sK[0][p] = sum_t (base_t - A_t) (NT >= 3: sK[t][p] = (base_t - A_t) * shrink, t >= 1)
     // (slot-major, thread-minor: conflict-free per-thread accesses)
-    double* sKb = sm + 2 * BS + 2 * NW * CAP + tid;
-    auto sK = [&](int idx) -> double& { return sKb[idx * 256]; };
+    double* sKb = sm + 2 * BS + 2 * NW3 * CAP + tid;
+    auto sK = [&](int idx) -> double& { return sKb[idx * NT3]; };
     const double shrink = (NT == 1) ? 1.0 : (1.0 - 2.0 * kRcpRel);
-    WarpCands wc{sm + 2 * BS + warp * CAP, reinterpret_cast<int64_t*>(sm + 2 * BS + NW * CAP) + warp * CAP, 0,
+    WarpCands wc{sm + 2 * BS + warp * CAP, reinterpret_cast<int64_t*>(sm + 2 * BS + NW3 * CAP) + warp * CAP, 0,
                  a.collect ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g), 0};
     const int64_t* B2 = a.binom + 2 * (m + 1);
     const int64_t* B3 = a.binom + 3 * (m + 1);
@@ -214,7 +219,7 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
         const int kbase = k0 + warp * P;
         const int i_lo = U.z, i_hi = U.w;
         double* Hb = sm + BS;  // tile buffer 1
-        if (tid == 0) {
+        if (HT && tid == 0) {
             fence_proxy_async();  // the previous unit's reads of buffer 1 precede these writes
             mbar_expect_tx(&s_hbar, (unsigned)(NT * HS * sizeof(double)));
 #pragma unroll
@@ -240,8 +245,10 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
         double K1r[P];  // NT == 2: task slot 1's (base - A) * shrink in registers
         unsigned valid = 0, bad = 0, forced = 0;
         const int jj = j < m ? j : (int)m - 1;
-        mbar_wait(&s_hbar, hpar);
-        hpar ^= 1u;
+        if (HT) {
+            mbar_wait(&s_hbar, hpar);
+            hpar ^= 1u;
+        }
         // per-task scalars of this unit, loaded once (live during the hoist only)
         double Y2v[NT], gamv[NT], etav[NT], ynv[NT], rjv[NT];
         const double* Gs[NT];
@@ -267,8 +274,8 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
                 const int tk = tord[t];
                 const double* Gt = Gs[t];
                 const double Y2 = Y2v[t];
-                const double cjk = Hb[t * HS + (k - k0) * 32 + lane];
-                const double ck = HC ? Hb[t * HS + IB * 32 + (k - k0)] : Gt[m * mp + k];
+                const double cjk = HT ? Hb[t * HS + (k - k0) * 32 + lane] : Gt[(int64_t)k * mp + j];
+                const double ck = (HT && HC) ? Hb[t * HS + IB * 32 + (k - k0)] : Gt[m * mp + k];
                 const double d1 = fma(-cjk, cjk, 1.0);
                 const double r1 = rcp_newton(d1);
                 const double v1 = fma(-cjk, w0[t], ck);
@@ -450,7 +457,7 @@ __global__ void __launch_bounds__(256, Cfg<NT>::MINB) k_fit3(const __grid_consta
             __syncthreads();
         }
     }
-    flush_warp(a, wc, blockIdx.x * NW + warp, lane);
+    flush_warp(a, wc, blockIdx.x * NW3 + warp, lane);
 }
 
 // Same arithmetic as the fit kernel (hoist on (j, k), sweep variable i), one thread per explicit tuple.
@@ -481,11 +488,11 @@ int launch_nt(const FitArgs& a0, int nsm, cudaStream_t st) {
         return -1;
     cudaFuncSetAttribute(k_fit3<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, 256, C::smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, NT3, C::smem_bytes);
     if (per_sm < 1) per_sm = 1;
     int grid = nsm * per_sm;
     if (!a.collect) seed_launch<3, 18>(k_seed_eval3, a, st);
-    k_fit3<NT><<<grid, 256, C::smem_bytes, st>>>(a);
+    k_fit3<NT><<<grid, NT3, C::smem_bytes, st>>>(a);
     return grid;
 }
 
@@ -498,6 +505,7 @@ void launch_screen3(const FitArgs& a, const int64_t* tuples, int64_t count, doub
 
 int fit3_max_tasks() { return 8; }
 int fit_slots_per_cta() { return NW; }
+int fit3_slots_per_cta() { return NW3; }
 int fit3_kspan(int T) {
     switch (T) {
         case 1: return Cfg<1>::KSPAN;
@@ -513,7 +521,7 @@ int fit3_grid(int T, int nsm) {
 #define OCC(NT)                                                                                              \
     case NT:                                                                                                 \
         cudaFuncSetAttribute(k_fit3<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<NT>::smem_bytes); \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, 256, Cfg<NT>::smem_bytes);       \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, NT3, Cfg<NT>::smem_bytes);       \
         break;
         OCC(1) OCC(2) OCC(3) OCC(4) OCC(5) OCC(6) OCC(7) OCC(8)
 #undef OCC

@@ -174,7 +174,8 @@ struct FitArgs {
 int fit3_launch(const FitArgs& a, int nsm, cudaStream_t st);  // returns grid size (warp slots / 8)
 int fit3_grid(int T, int nsm);                                // grid fit3_launch will use
 int fit3_max_tasks();
-int fit_slots_per_cta();
+int fit_slots_per_cta();   // warp candidate slots per CTA (n = 2, 4)
+int fit3_slots_per_cta();  // the same for the n = 3 sweep
 int fit3_kspan(int T);
 std::vector<int4> fit3_units(int64_t m, int T, int64_t N_total, const std::vector<int64_t>& c2_prefix,
                              int64_t rank_lo, int64_t rank_hi);
