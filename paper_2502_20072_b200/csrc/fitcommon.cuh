@@ -345,6 +345,8 @@ __device__ int seed_subsets(const FitArgs& a, SeedSmem& S) {
         }
         __syncthreads();
     }
+    // subsets of the F winners (ascending feature order), enumerated in parallel: thread c
+    // unranks c in the lexicographic order of C(F, N)
     if (tid == 0) {
         bool ok = true;
         for (int r = 0; r < F; ++r) ok &= S.top[r] >= 0;  // fewer than F live features: no seed
@@ -354,18 +356,26 @@ __device__ int seed_subsets(const FitArgs& a, SeedSmem& S) {
                 S.top[z] = S.top[z - 1];
                 S.top[z - 1] = q;
             }
-        int c[N], cnt = 0;
-        for (int x = 0; x < N; ++x) c[x] = x;
-        while (ok && cnt < SEED_MAX) {
-            for (int x = 0; x < N; ++x) S.sub[cnt][x] = (short)c[x];
-            ++cnt;
-            int x = N - 1;
-            while (x >= 0 && c[x] == F - N + x) --x;
-            if (x < 0) break;
-            ++c[x];
-            for (int z = x + 1; z < N; ++z) c[z] = c[z - 1] + 1;
+        int total = 1;  // C(F, N)
+        for (int x = 0; x < N; ++x) total = total * (F - x) / (x + 1);
+        total = total < SEED_MAX ? total : SEED_MAX;
+        S.nsub = (ok && total >= a.kc) ? total : 0;
+    }
+    __syncthreads();
+    for (int c = tid; c < S.nsub; c += blockDim.x) {
+        int r = c, e = 0;
+        for (int x = 0; x < N; ++x) {
+            const int rem = N - 1 - x;
+            for (;;) {
+                int blk = 1;  // C(F - 1 - e, rem)
+                for (int z = 0; z < rem; ++z) blk = blk * (F - 1 - e - z) / (z + 1);
+                if (r < blk) break;
+                r -= blk;
+                ++e;
+            }
+            S.sub[c][x] = (short)e;
+            ++e;
         }
-        S.nsub = cnt >= a.kc ? cnt : 0;
     }
     __syncthreads();
     return S.nsub;
@@ -397,20 +407,32 @@ __global__ void __launch_bounds__(512, 1) k_seed_select(const __grid_constant__ 
     if (threadIdx.x == 0) *a.seed_n = ns;
 }
 
-// Seed phase 3 (one CTA of 512): the kc-th smallest upper bound becomes the starting threshold.
+// Seed phase 3 (one CTA of 512): the kc-th smallest upper bound becomes the starting threshold
+// (bitonic sort of the <= SEED_MAX bounds in shared memory).
 __global__ void __launch_bounds__(512, 1) k_seed_commit(const __grid_constant__ FitArgs a) {
     __shared__ double ub[SEED_MAX];
     const int ns = *a.seed_n;
-    for (int c = threadIdx.x; c < ns; c += blockDim.x) ub[c] = a.seed_ub[c];
+    if (ns < a.kc) return;
+    for (int c = threadIdx.x; c < SEED_MAX; c += blockDim.x) ub[c] = c < ns ? a.seed_ub[c] : INFINITY;
     __syncthreads();
-    for (int c = threadIdx.x; c < ns; c += blockDim.x) {
-        const double v = ub[c];
-        int pos = 0;
-        for (int x = 0; x < ns; ++x) {
-            const double u = ub[x];
-            pos += (u < v || (u == v && x < c)) ? 1 : 0;
+    for (int k = 2; k <= SEED_MAX; k <<= 1)
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int x = threadIdx.x; x < SEED_MAX; x += blockDim.x) {
+                const int y = x ^ jj;
+                if (y > x) {
+                    const double p = ub[x], q = ub[y];
+                    const bool up = (x & k) == 0;
+                    if ((p > q) == up) {
+                        ub[x] = q;
+                        ub[y] = p;
+                    }
+                }
+            }
+            __syncthreads();
         }
-        if (pos == a.kc - 1 && v < INFINITY) {
+    if (threadIdx.x == 0) {
+        const double v = ub[a.kc - 1];
+        if (v < INFINITY) {
             const double th = v + fabs(v) * 1e-9 + 1e-300;  // strictly above kc certified bounds
             atomicMin(a.theta_g, ord_enc(th));
         }
