@@ -528,6 +528,12 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
         cudaEventRecord(c->cev[k], c->cst);
     }
     k = 0;
+    int oz_done = 0;  // INT8 Gram: column blocks (64 wide) already launched
+    if (ozaki) {
+        cudaEventRecord(c->ev[2], c->st);
+        c->gram_timed = true;
+        c->gram_ozaki = true;
+    }
     for (int64_t r0 = 0; r0 < m; r0 += R, ++k) {
         const int64_t r1 = std::min(m, r0 + R);
         cudaStreamWaitEvent(c->st, c->cev[k], 0);
@@ -537,8 +543,21 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
             launch_gram_cols(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), ntasks, c->mp, c->G.as<double>(),
                              B0, B1, c->st);
         }
+        if (ozaki) {
+            // a tile (fb, gb) of column block gb needs rows < gb*64 + 128: ready once they landed
+            const int ncb = ozaki_col_blocks(c->mp);
+            const int upto = r1 >= m ? ncb : std::max(oz_done, (int)(r1 / 64) - 1);
+            if (launch_ozaki_tiles(ntasks, c->mp, c->rpad_h.data(), c->oz_q.as<int8_t>(), c->oz_ex.as<int>(),
+                                   c->oz_koff.as<int64_t>(), c->G.as<double>(), oz_done, upto, c->st))
+                return fail(L0S_ECUDA, "INT8 Gram: TMA descriptor");
+            oz_done = upto;
+        }
     }
-    if (ozaki) return gram_full(c);
+    if (ozaki) {
+        launch_ozaki_eta(ntasks, m, c->mp, c->oz_ex.as<int>(), c->rowsd.as<double>(), c->G.as<double>(),
+                         c->eta_d.as<double>(), c->st);
+        cudaEventRecord(c->ev[3], c->st);
+    }
     return L0S_OK;
 }
 

@@ -59,6 +59,13 @@ int64_t ozaki_q_bytes(int64_t mp, int T, const int64_t* rpad_h, int64_t* KP_out)
 int launch_ozaki_gram(const double* Z, int64_t sp, const int64_t* zoff_d, const int64_t* rpad_h, int T, int64_t m,
                       int64_t mp, const double* rows_d, double* G, double* eta_d, int8_t* Q, int* ex, int64_t* koff_d,
                       bool digits_ready, cudaStream_t st);
+// pieces of the same, for the overlapped stage: tiles of the column blocks [gb0, gb1) (64 wide)
+// and the error-bound kernel (after all tiles)
+int ozaki_col_blocks(int64_t mp);
+int launch_ozaki_tiles(int T, int64_t mp, const int64_t* rpad_h, const int8_t* Q, const int* ex,
+                       const int64_t* koff_d, double* G, int gb0, int gb1, cudaStream_t st);
+void launch_ozaki_eta(int T, int64_t m, int64_t mp, const int* ex, const double* rows_d, const double* G, double* eta_d,
+                      cudaStream_t st);
 // Q / ex zero fill of the rows the normalize kernel does not write (m+1 .. R-1) and koff upload
 void ozaki_prepare_digits(int64_t m, int64_t mp, int T, const int64_t* rpad_h, int8_t* Q, int* ex, int64_t* koff_d,
                           DigitOut* out, cudaStream_t st);

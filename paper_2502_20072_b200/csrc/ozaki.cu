@@ -118,22 +118,24 @@ __global__ void k_oz_split(const double* __restrict__ Z, int64_t sp, const int64
 
 // ---- GEMM: one 128 x 64 tile (rows fb, cols gb, gb >= 2 fb: every entry with row <= col
 // lies in exactly one such tile) of one task per CTA ----
+// Tiles are numbered column by column (gb outer, fb = 0 .. gb/2 inner) from tile g0, so a range
+// of column blocks -- the part of the Gram a landed row chunk completes -- is one launch.
 __global__ void __launch_bounds__(192, 2) k_oz_gemm(const __grid_constant__ TmaDesc tmA,
                                                    const __grid_constant__ TmaDesc tmB, const int64_t* __restrict__ koff,
                                                    const int* __restrict__ ex, int64_t R, int nbc, int64_t mp,
-                                                   double* __restrict__ Gall) {
+                                                   double* __restrict__ Gall, int g0) {
     extern __shared__ unsigned char oz_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)oz_raw + 1023) & ~(uintptr_t)1023);
     __shared__ __align__(8) unsigned long long full[OZ_ST], empty[OZ_ST], done;
     __shared__ uint32_t tmem_slot;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int t = blockIdx.y;
-    int lin = blockIdx.x, fb = 0;
-    while (lin >= nbc - 2 * fb) {
-        lin -= nbc - 2 * fb;
-        ++fb;
+    int lin = g0 + blockIdx.x, gb = 0;
+    while (lin >= gb / 2 + 1) {
+        lin -= gb / 2 + 1;
+        ++gb;
     }
-    const int gb = 2 * fb + lin;
+    const int fb = lin;
     const int64_t k0 = koff[t];
     const int nkc = (int)((koff[t + 1] - k0) / OZ_KC);
     if (threadIdx.x == 0) {
@@ -298,29 +300,51 @@ void ozaki_prepare_digits(int64_t m, int64_t mp, int T, const int64_t* rpad_h, i
     *out = DigitOut{Q, R, KP, koff_d, ex};
 }
 
-int launch_ozaki_gram(const double* Z, int64_t sp, const int64_t* zoff_d, const int64_t* rpad_h, int T, int64_t m,
-                      int64_t mp, const double* rows_d, double* G, double* eta_d, int8_t* Q, int* ex, int64_t* koff_d,
-                      bool digits_ready, cudaStream_t st) {
+static int oz_tiles_before(int gb) {  // tiles in column blocks [0, gb)
+    int n = 0;
+    for (int g = 0; g < gb; ++g) n += g / 2 + 1;
+    return n;
+}
+
+int ozaki_col_blocks(int64_t mp) { return (int)((mp + OZ_BM - 1) / OZ_BM * OZ_BM / OZ_BN); }
+
+int launch_ozaki_tiles(int T, int64_t mp, const int64_t* rpad_h, const int8_t* Q, const int* ex,
+                       const int64_t* koff_d, double* G, int gb0, int gb1, cudaStream_t st) {
     const int64_t R = (mp + OZ_BM - 1) / OZ_BM * OZ_BM;
-    DigitOut dig;
+    const int nbc = (int)(R / OZ_BN);
+    gb1 = std::min(gb1, nbc);
+    if (gb1 <= gb0) return 0;
     int64_t KP = 0;
-    if (!digits_ready) {
-        ozaki_prepare_digits(mp - 1, mp, T, rpad_h, Q, ex, koff_d, &dig, st);  // rows < mp come from Z here
-        KP = dig.KP;
-        const int64_t warps = mp * T;
-        k_oz_split<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(Z, sp, zoff_d, T, mp, R, koff_d, Q, KP, ex);
-    } else {
-        for (int t = 0; t < T; ++t) KP += (rpad_h[t] + OZ_KC - 1) / OZ_KC * OZ_KC;
-    }
+    for (int t = 0; t < T; ++t) KP += (rpad_h[t] + OZ_KC - 1) / OZ_KC * OZ_KC;
     TmaDesc tmA, tmB;
     if (!make_tma_i8_3d(&tmA, Q, (unsigned long long)KP, (unsigned long long)R, OZ_S, OZ_KC, OZ_BM) ||
         !make_tma_i8_3d(&tmB, Q, (unsigned long long)KP, (unsigned long long)R, OZ_S, OZ_KC, OZ_BN))
         return -1;
     cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM);
-    const int nbr = (int)(R / OZ_BM), nbc = (int)(R / OZ_BN);
-    const int tiles = nbr * nbc - nbr * (nbr - 1);  // sum over fb of (nbc - 2 fb)
-    k_oz_gemm<<<dim3((unsigned)tiles, (unsigned)T), 192, OZ_SMEM, st>>>(tmA, tmB, koff_d, ex, R, nbc, mp, G);
+    const int t0 = oz_tiles_before(gb0), t1 = oz_tiles_before(gb1);
+    k_oz_gemm<<<dim3((unsigned)(t1 - t0), (unsigned)T), 192, OZ_SMEM, st>>>(tmA, tmB, koff_d, ex, R, nbc, mp, G, t0);
+    return 0;
+}
+
+void launch_ozaki_eta(int T, int64_t m, int64_t mp, const int* ex, const double* rows_d, const double* G, double* eta_d,
+                      cudaStream_t st) {
+    const int64_t R = (mp + OZ_BM - 1) / OZ_BM * OZ_BM;
     k_oz_eta<<<T, 256, 0, st>>>(ex, R, m, mp, G, rows_d, eta_d);
+}
+
+int launch_ozaki_gram(const double* Z, int64_t sp, const int64_t* zoff_d, const int64_t* rpad_h, int T, int64_t m,
+                      int64_t mp, const double* rows_d, double* G, double* eta_d, int8_t* Q, int* ex, int64_t* koff_d,
+                      bool digits_ready, cudaStream_t st) {
+    const int64_t R = (mp + OZ_BM - 1) / OZ_BM * OZ_BM;
+    if (!digits_ready) {
+        DigitOut dig;
+        ozaki_prepare_digits(mp - 1, mp, T, rpad_h, Q, ex, koff_d, &dig, st);  // rows < mp come from Z here
+        const int64_t warps = mp * T;
+        k_oz_split<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(Z, sp, zoff_d, T, mp, R, koff_d, Q, dig.KP,
+                                                                          ex);
+    }
+    if (launch_ozaki_tiles(T, mp, rpad_h, Q, ex, koff_d, G, 0, ozaki_col_blocks(mp), st)) return -1;
+    launch_ozaki_eta(T, m, mp, ex, rows_d, G, eta_d, st);
     return 0;
 }
 
