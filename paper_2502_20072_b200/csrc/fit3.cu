@@ -172,7 +172,10 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
     // property row's k-span c_k (a second box, first row used).
     constexpr bool HC = 64 <= 34 + KSPAN;
     constexpr int HS = (HC ? 2 : 1) * IB * 32;  // doubles per task slot
-    constexpr bool HT = IB == KSPAN && NT * HS <= BS;  // else the hoist reads L2
+#ifndef L0S_HOIST_TMA
+#define L0S_HOIST_TMA 1
+#endif
+    constexpr bool HT = L0S_HOIST_TMA && IB == KSPAN && NT * HS <= BS;  // else the hoist reads L2
     // per-thread constants, touched by the hoist, threshold updates and pruned rows:
     // sK[0][p] = sum_t (base_t - A_t) (NT >= 3: sK[t][p] = (base_t - A_t) * shrink, t >= 1)
     // (slot-major, thread-minor: conflict-free per-thread accesses)
@@ -198,7 +201,8 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
                 double* Tt = base + t * TS;
                 tma_load_2d(Tt, &a.tmJ, j0, row, &s_bar[buf]);
                 tma_load_2d(Tt + IB * 32, &a.tmK, k0, row, &s_bar[buf]);
-                tma_load_2d(Tt + IB * (32 + KSPAN), &a.tmC, (int)m, row, &s_bar[buf]);
+                // TMA box starts must be 16-byte aligned: the pair of columns (m & ~1, +1) holds c_i
+                tma_load_2d(Tt + IB * (32 + KSPAN), &a.tmC, (int)(m & ~(int64_t)1), row, &s_bar[buf]);
             }
         }
     };
@@ -353,7 +357,7 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
                 } else {
                 const double* Tt = T0 + (C::SLOT0 ? 0 : t) * TS;
                 g0 = Tt[ii * 32 + lane];
-                ci = Tt[IB * (32 + KSPAN) + 2 * ii];
+                ci = Tt[IB * (32 + KSPAN) + 2 * ii + (int)(m & 1)];
                 if constexpr (P == 1) {
                     gk[0] = Tt[IB * 32 + ii * KSPAN + warp];
                 } else {

@@ -207,11 +207,13 @@ def test_screen_n4_lower_bound(eng, rng):
     assert np.all(ok[flags == 3])
 
 
-def test_fast_matches_oracle_random(oracle, rng):
-    """Screened search == exhaustive CPU oracle on a mid-size instance (82k tuples, 2 tasks)."""
+@pytest.mark.parametrize("m", [80, 81])
+def test_fast_matches_oracle_random(oracle, rng, m):
+    """Screened search == exhaustive CPU oracle on a mid-size instance (82k tuples, 2 tasks);
+    odd m exercises the 16-byte-aligned TMA box of the property column."""
     from paper_2502_20072_b200 import L0Config, l0_search
 
-    m, s = 80, 400
+    s = 400
     v = rng.uniform(0.5, 2.0, size=(m, s))
     y = rng.standard_normal(s)
     slices = [np.arange(0, s, 2), np.arange(1, s, 2)]
@@ -500,3 +502,34 @@ def test_fast_fp32_matches_oracle(oracle, rng, n):
     assert [md.indices for md in got] == [w["indices"] for w in want]
     assert bits_equal([md.score for md in got], [w["score"] for w in want])
     assert bits_equal(np.array([md.coefficients for md in got]), np.array([w["coefficients"] for w in want]))
+
+
+def test_chunked_stage_ozaki_equals_dmma(rng):
+    """Host inputs large enough for the overlapped, chunked stage (8 row chunks, INT8 Gram tiles per
+    chunk), awkward sizes (m not a multiple of 64, ragged tasks): same models as the DMMA Gram
+    staged from device memory."""
+    import torch
+
+    from paper_2502_20072_b200 import _lib
+
+    m, s = 707, 6001
+    v = rng.uniform(0.5, 2.0, size=(m, s)) * rng.uniform(0.5, 3.0, size=(m, 1))
+    y = v[3] - 0.7 * v[500] + 0.4 * v[701] + 0.03 * rng.standard_normal(s)
+    perm = rng.permutation(s).astype(np.int64)
+    bounds = np.array([0, 1000, 3500, s], dtype=np.int64)
+    a, b = _lib.Engine(0), _lib.Engine(0)
+    a.set_gram_mode("ozaki")
+    b.set_gram_mode("dmma")
+    a.stage(v, y, perm, bounds, "fp64")  # host inputs: chunked, overlapped
+    vd, yd, pd = (torch.from_numpy(x).cuda() for x in (v, y, perm))
+    b.stage((m, s), None, None, bounds, "fp64", device_ptrs=(vd.data_ptr(), yd.data_ptr(), pd.data_ptr()))
+    eta_a, oz_a = a.stage_info()
+    assert oz_a
+    for t in range(3):
+        ga, gb = a.gram(t), b.gram(t)
+        scale = np.ones(m + 1)
+        scale[m] = np.sqrt(gb[m, m])
+        assert (np.abs(ga - gb) / np.outer(scale, scale)).max() <= eta_a[t] + 1e-11
+    ra = a.search(3, 10, 0, 2**62, "fast")
+    rb = b.search(3, 10, 0, 2**62, "fast")
+    assert np.array_equal(ra[1], rb[1]) and bits_equal(ra[0], rb[0]) and bits_equal(ra[2], rb[2])

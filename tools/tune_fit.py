@@ -21,10 +21,8 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
-    "nw8_p4": ("L0S_FIT3_NW=8", "L0S_C34_P=4"),
-    "nw16_p2": ("L0S_FIT3_NW=16", "L0S_C34_P=2"),
-    "nw16_p2_r2": ("L0S_FIT3_NW=16", "L0S_C34_P=2", "L0S_PRUNE_ROWS=2"),
-    "nw16_p2_cap128": ("L0S_FIT3_NW=16", "L0S_C34_P=2", "L0S_CAP=128"),
+    "hoist_tma": ("L0S_HOIST_TMA=1",),
+    "hoist_l2": ("L0S_HOIST_TMA=0",),
 }
 
 
