@@ -533,3 +533,24 @@ def test_chunked_stage_ozaki_equals_dmma(rng):
     ra = a.search(3, 10, 0, 2**62, "fast")
     rb = b.search(3, 10, 0, 2**62, "fast")
     assert np.array_equal(ra[1], rb[1]) and bits_equal(ra[0], rb[0]) and bits_equal(ra[2], rb[2])
+
+
+@pytest.mark.parametrize("n,T,m", [(3, 5, 45), (3, 8, 41), (4, 2, 30), (4, 6, 26), (2, 7, 120), (3, 1, 97)])
+def test_fast_task_counts_match_oracle(oracle, rng, n, T, m):
+    """Every task-count template of the screened kernels (fit2 / fit3 / fit4, NT = 1..8) against
+    the CPU oracle, bit for bit, with ragged task sizes and a mean offset in the property."""
+    from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
+
+    s = 60 * T + 7
+    v = rng.uniform(0.5, 2.0, size=(m, s)) * rng.uniform(0.3, 3.0, size=(m, 1))
+    y = 1.2 * v[1] - 0.8 * v[m - 2] + (0.5 * v[m // 2] if n >= 3 else 0.0) + 0.1 * rng.standard_normal(s) + 3.0
+    order = rng.permutation(s)
+    cuts = np.sort(rng.choice(np.arange(8, s - 8), size=T - 1, replace=False)) if T > 1 else np.array([], int)
+    slices = [np.sort(x) for x in np.split(order, cuts)]
+    want = oracle.l0_search(v, y, slices, n, 10, "fp64", threads=os.cpu_count() or 1)
+    st = SearchStats()
+    got = l0_search(v, y, slices, L0Config(dimension=n), mode="fast", stats=st)
+    assert st.device["mode_used"] == 1 and st.device["certified"] == 1
+    assert [md.indices for md in got] == [w["indices"] for w in want]
+    assert bits_equal([md.score for md in got], [w["score"] for w in want])
+    assert bits_equal(np.array([md.coefficients for md in got]), np.array([w["coefficients"] for w in want]))
