@@ -141,6 +141,8 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
     __shared__ int s_unit;
     __shared__ int s_tord[NT];
     __shared__ unsigned char s_force[2][IB];  // iforce flags of the staged rows
+    __shared__ int s_fany[2];                 // any of them set
+    static_assert(IB <= 32, "one warp loads a tile's row flags");
     __shared__ __align__(8) unsigned long long s_bar[2];  // TMA completion, one per tile buffer
     __shared__ __align__(8) unsigned long long s_hbar;    // TMA completion of the unit's hoist block
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -190,7 +192,12 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
     // tiles per task (slot t holds task tord[t]), staged by TMA (one elected thread,
     // completion on s_bar[buf]): C[i, j-block] (IB x 32), C[i, k-span] (IB x KSPAN), (c_i, pad) (IB x 2)
     auto load_tiles = [&](int buf, int ib0, int j0, int k0) {
-        if (tid < IB) s_force[buf][tid] = (ib0 + tid < m) ? a.iforce[ib0 + tid] : 0;
+        if (warp == 0) {  // IB <= 32: the rows' iforce flags and whether any is set
+            const unsigned char fl = (lane < IB && ib0 + lane < m) ? a.iforce[ib0 + lane] : 0;
+            if (lane < IB) s_force[buf][lane] = fl;
+            const unsigned any = __ballot_sync(L0S_FULL, fl != 0);
+            if (lane == 0) s_fany[buf] = any != 0u;
+        }
         if (tid == 0) {
             double* base = sm + buf * BS;
             fence_proxy_async();
@@ -334,6 +341,9 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
             wait_tiles(buf);
             __syncthreads();  // s_force of this tile
             const double* T0 = sm + buf * BS;
+            // a clean tile (warp-uniform): every row is below every lane's j and inside the unit,
+            // and no row is iforce-flagged -- a row's pending bits are then just the sign bits
+            const bool clean = ib0 + IB <= i_hi && ib0 + IB <= j0 && !s_fany[buf];
             // pending slow-path tuples of this tile: bit (ii * P + p)
             constexpr int NPW = (IB * P + 31) / 32;  // pending-bit words
             constexpr int IPW = 32 / P;              // rows per word
@@ -428,19 +438,37 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
                             task_row(acc[r], t, pw * IPW + ig + r);
                         }
                     }
-#pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const int ii = pw * IPW + ig + r;
-                        const int i = ib0 + ii;
-                        unsigned pass = forced;
+                    if (clean) {
+                        unsigned bits = 0u;  // sign bits of the group, row-major (r * P + p)
                         if (live) {
 #pragma unroll
-                            for (int p = 0; p < P; ++p) pass |= ((unsigned)__double2hiint(acc[r][p]) >> 31) << p;
+                            for (int r = 0; r < R; ++r)
+#pragma unroll
+                                for (int p = 0; p < P; ++p)
+                                    bits |= ((unsigned)__double2hiint(acc[r][p]) >> 31) << (r * P + p);
                         }
-                        if (s_force[buf][ii]) pass |= (1u << P) - 1;  // rho_i above rho_cap: needs the actual rho
-                        pass &= valid;
-                        if (!(i < j && i < i_hi)) pass = 0;
-                        word |= pass << ((ig + r) * P);
+                        unsigned fv = forced, vv = valid;  // replicate the per-pair masks over the R rows
+#pragma unroll
+                        for (int r = 1; r < R; ++r) {
+                            fv |= forced << (r * P);
+                            vv |= valid << (r * P);
+                        }
+                        word |= ((bits | fv) & vv) << (ig * P);
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            const int ii = pw * IPW + ig + r;
+                            const int i = ib0 + ii;
+                            unsigned pass = forced;
+                            if (live) {
+#pragma unroll
+                                for (int p = 0; p < P; ++p) pass |= ((unsigned)__double2hiint(acc[r][p]) >> 31) << p;
+                            }
+                            if (s_force[buf][ii]) pass |= (1u << P) - 1;  // rho_i above rho_cap: needs the actual rho
+                            pass &= valid;
+                            if (!(i < j && i < i_hi)) pass = 0;
+                            word |= pass << ((ig + r) * P);
+                        }
                     }
                 }
                 pend[pw] = word;
