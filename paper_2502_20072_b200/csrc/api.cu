@@ -817,28 +817,24 @@ static int screen_ill(l0s_ctx* c, int n, int64_t nill, int64_t keep, std::vector
     st->ms_qr += elapsed(e0, e1);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    std::vector<double> sc((size_t)nill), mr((size_t)nill);
-    std::vector<int64_t> rk((size_t)nill);
-    CK(cudaMemcpyAsync(sc.data(), q.score, sizeof(double) * nill, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(mr.data(), q.min_ratio, sizeof(double) * nill, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(rk.data(), c->ill.p, sizeof(int64_t) * nill, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    const double tol = 1e-10;  // RANK_TOL_FACTOR["fp64"], lsq.py:23 (screened path is fp64 only)
+    const double tol = 1e-10;  // RANK_TOL_FACTOR["fp64"], lsq.py:23 (fp32 never reaches the QR screen)
     double yy = 0.0;
     for (double v : c->yyu_h) yy += v;
     const double sk = ((int64_t)best.size() >= keep) ? best[(size_t)keep - 1].score : INFINITY;
-    std::vector<int64_t> sel;
-    for (int64_t i = 0; i < nill; ++i) {
-        const double r = mr[(size_t)i];
-        if (r < tol * (1.0 - 1e-3)) continue;  // the reference's rank rule rejects it in some task
-        // QR score error ~ eps * condition; condition >= 1/ratio
-        const double margin = 1e3 * kEps * yy / (double)c->s / std::max(r, 1e-300) + 1e-9 * std::fabs(sc[(size_t)i]);
-        if (!(sc[(size_t)i] - margin > sk)) sel.push_back(rk[(size_t)i]);
-    }
+    // selection on the device: only the (usually empty) list of survivors comes back
+    CK(c->ex_ranks.ensure(sizeof(int64_t) * (size_t)std::max<int64_t>(nill, 1)));
+    CK(c->cand_cnt.ensure(sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(c->cand_cnt.p, 0, sizeof(unsigned long long), c->st));
+    launch_qr_select(q.score, q.min_ratio, c->ill.as<int64_t>(), nill, tol, sk, yy / (double)c->s,
+                     c->ex_ranks.as<int64_t>(), c->cand_cnt.as<unsigned long long>(), nill, c->st);
+    st->n_launches++;
+    unsigned long long nsel = 0;
+    CK(cudaMemcpyAsync(&nsel, c->cand_cnt.p, sizeof nsel, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    std::vector<int64_t> sel((size_t)nsel);
+    if (nsel) CK(cudaMemcpy(sel.data(), c->ex_ranks.p, sizeof(int64_t) * nsel, cudaMemcpyDeviceToHost));
     st->n_ill_refit += (int64_t)sel.size();
     if (sel.empty()) return L0S_OK;
-    CK(c->ex_ranks.ensure(sizeof(int64_t) * sel.size()));
-    CK(cudaMemcpyAsync(c->ex_ranks.p, sel.data(), sizeof(int64_t) * sel.size(), cudaMemcpyHostToDevice, c->st));
     std::vector<Cand> more;
     int rc = exact_ranks_to_host(c, n, c->ex_ranks.as<int64_t>(), (int64_t)sel.size(), more, &st->n_launches, &c->recs);
     if (rc) return rc;

@@ -222,35 +222,36 @@ struct Ops<float> {
 
 // sequential sum_{i=from}^{to-1} fl(x_i*y_i) in index order.  The loads of the next batch
 // are issued before the current batch's adds, so the chain runs at DADD latency.
-template <typename W>
+// B = elements per batch: 8 from shared memory, 32 from global memory (L2 latency).
+template <typename W, int B = 8>
 __device__ __forceinline__ double seq_dot(const W* __restrict__ x, const W* __restrict__ y, int from, int to) {
     double acc = 0.0;
     int i = from;
-    if (i + 8 <= to) {
-        W px[8], py[8];
+    if (i + B <= to) {
+        W px[B], py[B];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < B; ++u) {
             px[u] = x[i + u];
             py[u] = y[i + u];
         }
-        for (; i + 16 <= to; i += 8) {
-            W nx[8], ny[8];
+        for (; i + 2 * B <= to; i += B) {
+            W nx[B], ny[B];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                nx[u] = x[i + 8 + u];
-                ny[u] = y[i + 8 + u];
+            for (int u = 0; u < B; ++u) {
+                nx[u] = x[i + B + u];
+                ny[u] = y[i + B + u];
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) acc = Ops<W>::term(acc, px[u], py[u]);
+            for (int u = 0; u < B; ++u) acc = Ops<W>::term(acc, px[u], py[u]);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < B; ++u) {
                 px[u] = nx[u];
                 py[u] = ny[u];
             }
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc = Ops<W>::term(acc, px[u], py[u]);
-        i += 8;
+        for (int u = 0; u < B; ++u) acc = Ops<W>::term(acc, px[u], py[u]);
+        i += B;
     }
     for (; i < to; ++i) acc = Ops<W>::term(acc, x[i], y[i]);
     return acc;
@@ -265,11 +266,15 @@ __device__ __forceinline__ void cp_async_w(W* dst, const W* src) {
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src));
 }
 
-template <typename W>
+// GM: the system lives in a global scratch slot (L2-resident; systems above the shared-memory
+// budget) instead of shared memory; the sequential chains then prefetch 2 x 32 elements ahead.
+template <typename W, bool GM = false>
 __global__ void __launch_bounds__(128) k_exact_smem(ExactArgs a, int64_t g0, double* __restrict__ ssr_tmp,
                                                     int32_t* __restrict__ ok_tmp) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    W* S = reinterpret_cast<W*>(smraw);
+    constexpr int CB = GM ? 32 : 8;  // chain prefetch batch
+    W* S = GM ? reinterpret_cast<W*>(a.scratch) + (int64_t)blockIdx.x * (a.n + 2) * a.ld
+              : reinterpret_cast<W*>(smraw);
     __shared__ double s_fac[kMaxN + 2];
     __shared__ double s_vtv, s_alpha;
     __shared__ int s_skip;
@@ -292,16 +297,28 @@ __global__ void __launch_bounds__(128) k_exact_smem(ExactArgs a, int64_t g0, dou
     const W* X = (const W*)a.Xp;
     const W* Y = (const W*)a.yp;
     // the system [f_1 .. f_n | 1 | y] (lsq.py:141-147), every element in flight at once
-    for (int k = 0; k < n; ++k) {
-        const W* src = X + s_tup[k] * a.s + lo;
-        for (int i = tid; i < rows; i += blockDim.x) cp_async_w<W>(S + k * ld + i, src + i);
+    if constexpr (GM) {
+        for (int k = 0; k < n; ++k) {
+            const W* src = X + s_tup[k] * a.s + lo;
+            for (int i = tid; i < rows; i += blockDim.x) S[k * ld + i] = src[i];
+        }
+        for (int i = tid; i < rows; i += blockDim.x) {
+            S[n * ld + i] = (W)1.0;
+            S[p * ld + i] = Y[lo + i];
+        }
+        __threadfence_block();
+    } else {
+        for (int k = 0; k < n; ++k) {
+            const W* src = X + s_tup[k] * a.s + lo;
+            for (int i = tid; i < rows; i += blockDim.x) cp_async_w<W>(S + k * ld + i, src + i);
+        }
+        for (int i = tid; i < rows; i += blockDim.x) {
+            S[n * ld + i] = (W)1.0;
+            cp_async_w<W>(S + p * ld + i, Y + lo + i);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
     }
-    for (int i = tid; i < rows; i += blockDim.x) {
-        S[n * ld + i] = (W)1.0;
-        cp_async_w<W>(S + p * ld + i, Y + lo + i);
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
     __syncthreads();
     double maxdiag = 0.0;  // meaningful in thread 0
     double nrm2 = 0.0;     // thread 0: norm^2 of the next column, when produced by the fused pass
@@ -310,7 +327,7 @@ __global__ void __launch_bounds__(128) k_exact_smem(ExactArgs a, int64_t g0, dou
     for (int j = 0; j < p; ++j) {
         W* cj = S + j * ld;
         if (tid == 0) {
-            if (!have) nrm2 = seq_dot<W>(cj, cj, j, rows);
+            if (!have) nrm2 = seq_dot<W, CB>(cj, cj, j, rows);
             have = false;
             double nrm = __dsqrt_rn(nrm2);
             if (nrm == 0.0) {
@@ -335,7 +352,7 @@ __global__ void __launch_bounds__(128) k_exact_smem(ExactArgs a, int64_t g0, dou
         // w_c for c = j+1..p: independent sequential chains on lanes 0..p-j-1
         if (tid < p - j) {
             int c = j + 1 + tid;
-            double w = seq_dot<W>(cj, S + c * ld, j, rows);
+            double w = seq_dot<W, CB>(cj, S + c * ld, j, rows);
             s_fac[c] = __ddiv_rn(__dmul_rn(2.0, w), s_vtv);
         }
         __syncthreads();
@@ -350,10 +367,10 @@ __global__ void __launch_bounds__(128) k_exact_smem(ExactArgs a, int64_t g0, dou
         if (tid == 0) {
             W* c1 = S + (j + 1) * ld;
             if (j + 1 < p) {
-                nrm2 = seq_dot<W>(c1, c1, j + 1, rows);
+                nrm2 = seq_dot<W, CB>(c1, c1, j + 1, rows);
                 have = true;
             } else {
-                ssr = seq_dot<W>(c1, c1, p, rows);
+                ssr = seq_dot<W, CB>(c1, c1, p, rows);
             }
         } else if (tid >= 32) {
             for (int c = j + 2; c <= p; ++c) {
@@ -444,6 +461,20 @@ void launch_exact(const ExactArgs& a, double* ssr_tmp, int32_t* ok_tmp, cudaStre
             if (launches) ++*launches;
         }
         total = 0;  // done
+    }
+    if (total > 0 && total <= 8192 && a.n <= kMaxN) {
+        // few large systems (the screened path's candidates): one CTA per system on an
+        // L2-resident global scratch slot, scratch_threads slots per launch
+        const int64_t per = std::max<int64_t>(1, a.scratch_threads);
+        for (int64_t g0 = 0; g0 < total; g0 += per) {
+            unsigned blocks = (unsigned)std::min(per, total - g0);
+            if (a.precision == 1)
+                k_exact_smem<float, true><<<blocks, 128, 0, st>>>(a, g0, ssr_tmp, ok_tmp);
+            else
+                k_exact_smem<double, true><<<blocks, 128, 0, st>>>(a, g0, ssr_tmp, ok_tmp);
+            if (launches) ++*launches;
+        }
+        total = 0;
     }
     int64_t chunk = std::max<int64_t>(a.T, (a.scratch_threads / a.T) * a.T);
     for (int64_t g0 = 0; g0 < total; g0 += chunk) {

@@ -114,6 +114,9 @@ struct QrArgs {
     int64_t g0, total;      // set by the launcher
 };
 void launch_qr_screen(const QrArgs& a, int64_t count, cudaStream_t st, int64_t* launches);
+// ranks of the screened ill tuples that may still reach the top list (selection on the device)
+void launch_qr_select(const double* score, const double* min_ratio, const int64_t* ranks, int64_t count, double tol,
+                      double sk, double yy_s, int64_t* sel, unsigned long long* nsel, int64_t cap, cudaStream_t st);
 
 // ---- screened fit (fit3.cu) ----
 // global lower-bound histogram behind the shared threshold (fitcommon.cuh): HIST_SUB sub-bins

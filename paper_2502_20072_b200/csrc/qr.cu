@@ -166,7 +166,30 @@ __global__ void k_qr_finalize(QrArgs a, int64_t count) {
     a.min_ratio[c] = rmin;
 }
 
+// Device-side selection of the ill tuples that can still reach the top list:
+// the reference's rank rule must not certainly reject them, and their QR score minus the QR's
+// error margin (~ eps / ratio, with a large safety factor) must not exceed the keep-th score.
+__global__ void k_qr_select(const double* __restrict__ score, const double* __restrict__ min_ratio,
+                            const int64_t* __restrict__ ranks, int64_t count, double tol, double sk, double yy_s,
+                            int64_t* __restrict__ sel, unsigned long long* __restrict__ nsel, int64_t cap) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= count) return;
+    const double r = min_ratio[c], sc = score[c];
+    if (r < tol * (1.0 - 1e-3)) return;  // the reference's rank rule rejects it in some task
+    const double margin = 1e3 * kEps * yy_s / fmax(r, 1e-300) + 1e-9 * fabs(sc);
+    if (sc - margin > sk) return;
+    const unsigned long long k = atomicAdd(nsel, 1ull);
+    if ((int64_t)k < cap) sel[k] = ranks[c];
+}
+
 }  // namespace
+
+void launch_qr_select(const double* score, const double* min_ratio, const int64_t* ranks, int64_t count, double tol,
+                      double sk, double yy_s, int64_t* sel, unsigned long long* nsel, int64_t cap, cudaStream_t st) {
+    if (count > 0)
+        k_qr_select<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(score, min_ratio, ranks, count, tol, sk, yy_s, sel,
+                                                                       nsel, cap);
+}
 
 void launch_qr_screen(const QrArgs& a0, int64_t count, cudaStream_t st, int64_t* launches) {
     QrArgs a = a0;

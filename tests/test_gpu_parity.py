@@ -554,3 +554,26 @@ def test_fast_task_counts_match_oracle(oracle, rng, n, T, m):
     assert [md.indices for md in got] == [w["indices"] for w in want]
     assert bits_equal([md.score for md in got], [w["score"] for w in want])
     assert bits_equal(np.array([md.coefficients for md in got]), np.array([w["coefficients"] for w in want]))
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_exact_large_systems_global_path(oracle, rng, precision):
+    """Systems above the shared-memory budget (9000 rows x 5 columns) take the CTA-per-system
+    kernel on an L2-resident global scratch: still bit-identical to the reference arithmetic."""
+    from paper_2502_20072_b200 import _lib
+
+    m, s = 12, 9000
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    y = v[2] - 0.5 * v[7] + 0.1 * rng.standard_normal(s)
+    eng = _lib.Engine(0)
+    eng.stage(v, y, np.arange(s), np.array([0, s]), precision)
+    tup = np.array(list(itertools.combinations(range(m), 3))[:40], dtype=np.int64)
+    ok, score, coef, ssr = eng.fit_tuples(tup)
+    vals, yy, bounds, _ = oracle.prepare(v, y, None, precision)
+    tol = 1e-10 if precision == "fp64" else 1e-5
+    want = oracle.score_tuples(vals, yy, bounds, tup, tol)
+    assert bits_equal(score, want)
+    for k in (0, 17, 39):
+        okr, coef_r, ssr_r = oracle.fit_tuple_kernel(vals, yy, bounds, tup[k], tol)
+        assert bool(okr) == bool(ok[k])
+        assert bits_equal(coef[k], coef_r) and bits_equal(ssr[k], ssr_r)
