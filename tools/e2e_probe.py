@@ -25,7 +25,10 @@ def main():
         t0 = time.perf_counter()
         l0_search(vh, yh, slices, cfg, stats=st)
         t1 = time.perf_counter()
-        print(f"l0_search pinned: {1e3 * (t1 - t0):.2f} ms  stats={st}")
+        d = st.device
+        print(f"l0_search pinned: {1e3 * (t1 - t0):.2f} ms  device total {d['ms_total']:.2f} fit {d['ms_fit']:.2f} "
+              f"exact {d['ms_exact']:.2f} launches {d['n_launches']} fit_launches {d['n_fit_launches']} "
+              f"cands {d['n_candidates']} ill {d['n_ill']} certified {d['certified']} rescans {d['n_rescan']}")
     for it in range(2):
         t0 = time.perf_counter()
         l0_search(v, y, slices, cfg)
