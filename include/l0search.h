@@ -108,6 +108,16 @@ int l0s_stage(l0s_ctx *ctx, const double *values, int64_t m, int64_t s, const do
  * split across GPUs; no reference counterpart -- the reference is single-process.)
  */
 int l0s_gram_shard_size(int64_t m, int ntasks, int nshards, int64_t *out_doubles);
+
+/*
+ * Append m_new feature rows (host, (m_new, s) float64, the caller's sample
+ * order) to the problem of the previous l0s_stage (host inputs), as the
+ * pipeline's subspace grows between dimensions (screening.py:197-198,
+ * pipeline.py:181-240): only the new rows are copied; the result is the stage
+ * of the concatenated matrix.  L0S_ESTATE unless the context holds a
+ * completed stage from host inputs.
+ */
+int l0s_stage_append(l0s_ctx *ctx, const double *rows, int64_t m_new);
 int l0s_stage_shard(l0s_ctx *ctx, const double *values, int64_t m, int64_t s, const double *y,
                     const int64_t *perm, const int64_t *bounds, int ntasks, int precision,
                     int is_device, int shard, int nshards, double *pack);

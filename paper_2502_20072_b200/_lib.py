@@ -29,6 +29,7 @@ EXPORTS = (
     "l0s_search", "l0s_fit_tuples", "l0s_screen_tuples", "l0s_get_gram", "l0s_unrank", "l0s_rank",
     "l0s_count", "l0s_fp64_peak", "l0s_rcp_check", "l0s_gram_shard_size", "l0s_stage_shard",
     "l0s_stage_finish", "l0s_sis_prepare", "l0s_sis_scores", "l0s_set_gram_mode", "l0s_stage_info",
+    "l0s_stage_append",
 )
 
 
@@ -88,6 +89,7 @@ def lib():
         L.l0s_gram_shard_size.argtypes = [i64, i32, i32, P(i64)]
         L.l0s_stage_shard.argtypes = [vp, vp, i64, i64, vp, vp, vp, i32, i32, i32, i32, i32, vp]
         L.l0s_stage_finish.argtypes = [vp, vp]
+        L.l0s_stage_append.argtypes = [vp, vp, i64]
         L.l0s_set_gram_mode.argtypes = [vp, i32]
         L.l0s_stage_info.argtypes = [vp, vp, vp]
         L.l0s_sis_prepare.argtypes = [vp, vp, i32, i64, vp, vp, i32]
@@ -136,6 +138,9 @@ class Engine:
         self.handle = h
         self.device = device
         self.staged_key = None
+        # (entries, their value arrays, y, perm, bounds, precision) of the SelectedSubspace the
+        # context holds (search.l0_search's incremental stage); any other stage clears it
+        self.subspace_cache = None
 
     def close(self):
         if self.handle:
@@ -163,9 +168,18 @@ class Engine:
             args = (ctypes.c_void_p(device_ptrs[0]), m, s, ctypes.c_void_p(device_ptrs[1]),
                     ctypes.c_void_p(device_ptrs[2]))
             is_dev = 1
+        self.subspace_cache = None
         check(lib().l0s_stage(self.handle, *args, ptr(bounds), bounds.shape[0] - 1, PREC[precision], is_dev),
               "l0s_stage")
         self.m, self.s, self.T = int(m), int(s), bounds.shape[0] - 1
+
+    def stage_append(self, rows: np.ndarray) -> None:
+        """Append feature rows (host, (m_new, s)) to the staged host problem (l0s_stage_append)."""
+        rows = np.ascontiguousarray(rows, dtype=np.float64)
+        if rows.ndim != 2 or rows.shape[1] != self.s:
+            raise ValueError(f"rows must be (m_new, {self.s})")
+        check(lib().l0s_stage_append(self.handle, ptr(rows), rows.shape[0]), "l0s_stage_append")
+        self.m += rows.shape[0]
 
     @staticmethod
     def gram_shard_size(m: int, ntasks: int, nshards: int) -> int:
@@ -177,6 +191,7 @@ class Engine:
     def stage_shard(self, shape: tuple, bounds: np.ndarray, precision: str, device_ptrs: tuple, shard: int,
                     nshards: int, pack_ptr: int) -> None:
         """Stage device-resident inputs and compute this rank's Gram shard into pack_ptr (device)."""
+        self.subspace_cache = None
         bounds = np.ascontiguousarray(bounds, dtype=np.int64)
         m, s = shape
         check(lib().l0s_stage_shard(self.handle, ctypes.c_void_p(device_ptrs[0]), m, s, ctypes.c_void_p(device_ptrs[1]),

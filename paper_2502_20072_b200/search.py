@@ -115,6 +115,37 @@ def _as_matrix(subspace):
     return np.asarray(subspace), None
 
 
+def _is_subspace(subspace) -> bool:
+    return hasattr(subspace, "values_matrix") and hasattr(subspace, "expressions") and hasattr(subspace, "entries")
+
+
+def _stage_subspace(eng, subspace, y, perm, bounds, precision: str):
+    """Stage a SelectedSubspace, incrementally when it extends the one the engine holds.
+
+    The pipeline's subspace only grows by appending entries between dimensions
+    (screening.py:197-198, pipeline.py:181-240): when the first entries are the very
+    objects staged last time (same value arrays, same y / partition / precision), only the
+    new rows are sent (l0s_stage_append) -- the reference re-stacks and re-prepares the
+    whole matrix every dimension (search.py:113-127).  Entry value arrays are taken as
+    immutable records, as the pipeline treats them.
+    """
+    entries = subspace.entries
+    c = eng.subspace_cache
+    if c is not None:
+        pe, pv, py, pperm, pb, pprec = c
+        m0 = len(pe)
+        if (0 < m0 <= len(entries) and pprec == precision and np.array_equal(py, y)
+                and np.array_equal(pperm, perm) and np.array_equal(pb, bounds)
+                and all(e is a and e.values is v for e, a, v in zip(entries, pe, pv))):
+            if len(entries) > m0:
+                eng.stage_append(np.stack([e.values for e in entries[m0:]]))
+            eng.subspace_cache = (list(entries), [e.values for e in entries], py, pperm, pb, pprec)
+            return
+    eng.stage(subspace.values_matrix(), y, perm, bounds, precision)
+    eng.subspace_cache = (list(entries), [e.values for e in entries], np.array(y, copy=True), perm.copy(),
+                          bounds.copy(), precision)
+
+
 def _partition(s: int, task_slices):
     """Index half of search._prepare (search.py:113-127): permutation and bounds."""
     if task_slices is None:
@@ -196,8 +227,13 @@ def l0_search(
     """
     if config is None:
         raise ValueError("config is required")
-    values, expressions = _as_matrix(subspace)
-    m = values.shape[0]
+    incremental = _is_subspace(subspace) and len(subspace) > 0
+    if incremental:  # rows are stacked only as far as the device does not hold them already
+        expressions = subspace.expressions
+        m, s = len(subspace), int(np.asarray(subspace.entries[0].values).shape[0])
+    else:
+        values, expressions = _as_matrix(subspace)
+        m, s = values.shape[0], values.shape[1]
     n = config.dimension
     if m < n:
         raise ValueError(f"subspace holds {m} features, need at least {n}")
@@ -206,14 +242,17 @@ def l0_search(
         raise CapacityError(f"{total} candidate tuples exceed the enumerable range")
     if config.precision not in RANK_TOL_FACTOR:
         raise KeyError(config.precision)
-    s = values.shape[1]
     perm, bounds, slices = _partition(s, task_slices)
     keep = max(1, config.n_models_store)
     batch = max(1, config.batch_size)
     lo, hi = (0, total) if rank_range is None else (max(0, int(rank_range[0])), min(total, int(rank_range[1])))
 
     eng = _lib.engine(device)
-    eng.stage(np.asarray(values), np.asarray(property_values, dtype=np.float64), perm, bounds, config.precision)
+    y = np.asarray(property_values, dtype=np.float64)
+    if incremental:
+        _stage_subspace(eng, subspace, y, perm, bounds, config.precision)
+    else:
+        eng.stage(np.asarray(values), y, perm, bounds, config.precision)
     t0 = time.perf_counter()
     scores, ranks, coef, ssr, dst = eng.search(n, keep, lo, hi, mode)
     elapsed = time.perf_counter() - t0

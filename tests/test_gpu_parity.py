@@ -309,6 +309,74 @@ def test_pipeline_drop_in_model_files(tmp_path, name):
             assert got == want
 
 
+class _Entry:
+    def __init__(self, key, values):
+        self.expression = key
+        self.values = values
+
+
+class _Subspace:
+    """The parts of screening.SelectedSubspace that l0_search reads (screening.py:171-198)."""
+
+    def __init__(self, entries):
+        self.entries = list(entries)
+
+    def __len__(self):
+        return len(self.entries)
+
+    @property
+    def expressions(self):
+        return [e.expression for e in self.entries]
+
+    def values_matrix(self):
+        return np.stack([e.values for e in self.entries])
+
+    def extended(self, new):
+        return _Subspace(self.entries + list(new))
+
+
+@pytest.mark.parametrize("shape", [(30, 25, 2, 600), (300, 200, 2, 3000)])
+def test_incremental_stage_across_dimensions(monkeypatch, shape):
+    """The pipeline's subspace grows by appending between dimensions: l0_search then sends only
+    the new rows (l0s_stage_append) and returns exactly what a full stage of the concatenated
+    matrix returns; a changed property or partition restages in full."""
+    from paper_2502_20072_b200 import L0Config, _lib, l0_search
+
+    m0, m1, T, s = shape
+    rng = np.random.default_rng(5)
+    v = rng.uniform(0.5, 2.0, size=(m0 + m1, s))
+    slices = [np.arange(t, s, T) for t in range(T)]
+    y = 1.2 * v[3] - 0.7 * v[m0 + 4] + 0.4 * v[m0 + 9] + 0.01 * rng.standard_normal(s)
+    entries = [_Entry(f"f{i}", v[i].copy()) for i in range(m0 + m1)]
+    sub0 = _Subspace(entries[:m0])
+    sub1 = sub0.extended(entries[m0:])
+    calls = []
+    orig = _lib.Engine.stage_append
+    monkeypatch.setattr(_lib.Engine, "stage_append", lambda self, rows: (calls.append(rows.shape), orig(self, rows)))
+    for n in (1, 2):
+        l0_search(sub0, y, slices, L0Config(dimension=n))
+    assert calls == []
+    got = l0_search(sub1, y, slices, L0Config(dimension=3))
+    assert calls == [(m1, s)]
+    again = l0_search(sub1, y, slices, L0Config(dimension=2))  # same subspace: nothing to send
+    assert calls == [(m1, s)]
+    want = l0_search(np.stack([e.values for e in sub1.entries]), y, slices, L0Config(dimension=3))
+    want2 = l0_search(np.stack([e.values for e in sub1.entries]), y, slices, L0Config(dimension=2))
+    for g, w in ((got, want), (again, want2)):
+        assert [md.indices for md in g] == [md.indices for md in w]
+        assert bits_equal([md.score for md in g], [md.score for md in w])
+        assert all(bits_equal(a.coefficients, b.coefficients) for a, b in zip(g, w))
+    assert got[0].expressions is not None and got[0].expressions[0] == "f3"
+    # a different property: full restage (no append), same answer as a fresh stage
+    l0_search(sub0, y, slices, L0Config(dimension=2))
+    y2 = y + 0.1 * v[7]
+    got2 = l0_search(sub1, y2, slices, L0Config(dimension=2))
+    assert calls == [(m1, s)]
+    want3 = l0_search(np.stack([e.values for e in sub1.entries]), y2, slices, L0Config(dimension=2))
+    assert [md.indices for md in got2] == [md.indices for md in want3]
+    assert bits_equal([md.score for md in got2], [md.score for md in want3])
+
+
 @pytest.mark.parametrize("W", [2, 3, 8])
 def test_sharded_gram_equals_single_gpu(rng, W):
     """Multi-GPU staging emulated on one device: W engines each compute their Gram shard into
