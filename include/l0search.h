@@ -118,6 +118,47 @@ int l0s_gram_shard_size(int64_t m, int ntasks, int nshards, int64_t *out_doubles
  * completed stage from host inputs.
  */
 int l0s_stage_append(l0s_ctx *ctx, const double *rows, int64_t m_new);
+
+/*
+ * Final-rung candidates on the device (generation.iter_final_rung,
+ * generation.py:331-393; values: expressions.apply_operator_values,
+ * expressions.py:168-192; validity: generation._validity_mask, :107-118).
+ *
+ * l0s_gen_pool: the pool's value rows (host, (n_pool, s), float64 or, with
+ *   fp32 = 1, float32 -- the pool's dtype), resident until the next call.
+ * l0s_gen_eval: candidates c < count of one operator kind (L0S_GEN_*):
+ *   children pi[c], pj[c] (pj NULL or -1 for unary kinds); kind
+ *   L0S_GEN_VALUES takes the rows from `values` ((count, s), pool dtype)
+ *   instead.  Writes out_valid[c] (the reference's validity rule with limits
+ *   min_abs / max_abs / dedup_tol compared in the pool's dtype) and
+ *   out_hash[2c..2c+1] (128-bit fingerprint of float64(v) rounded to `tol`,
+ *   half to even, -0 == +0: equal iff the rounded vectors are equal, up to
+ *   hash collisions).  The values stay on the device (fp64).
+ * l0s_gen_take: rows[] of the last evaluation into a compact fp64 device
+ *   block (*dev_out, valid until the next l0s_gen_* call; feed it to
+ *   l0s_sis_scores with is_device = 1) and, if host_out, to the host in the
+ *   pool's dtype.
+ * l0s_gen_fetch: rows[] of the taken block to the host (pool dtype).
+ */
+#define L0S_GEN_COPY 0
+#define L0S_GEN_ADD 1
+#define L0S_GEN_SUB 2
+#define L0S_GEN_MUL 3
+#define L0S_GEN_DIV 4
+#define L0S_GEN_ABS_DIFF 5
+#define L0S_GEN_SQRT 6
+#define L0S_GEN_SQ 7
+#define L0S_GEN_CB 8
+#define L0S_GEN_INV 9
+#define L0S_GEN_ABS 10
+#define L0S_GEN_VALUES 11
+int l0s_gen_pool(l0s_ctx *ctx, const void *values, int64_t n_pool, int64_t s, int fp32);
+int l0s_gen_eval(l0s_ctx *ctx, int kind, const int32_t *pi, const int32_t *pj, int64_t count,
+                 const void *values, double tol, double min_abs, double max_abs, double dedup_tol,
+                 uint8_t *out_valid, uint64_t *out_hash);
+int l0s_gen_take(l0s_ctx *ctx, const int32_t *rows, int64_t count, void *host_out,
+                 const double **dev_out);
+int l0s_gen_fetch(l0s_ctx *ctx, const int32_t *rows, int64_t count, void *host_out);
 int l0s_stage_shard(l0s_ctx *ctx, const double *values, int64_t m, int64_t s, const double *y,
                     const int64_t *perm, const int64_t *bounds, int ntasks, int precision,
                     int is_device, int shard, int nshards, double *pack);

@@ -29,7 +29,7 @@ EXPORTS = (
     "l0s_search", "l0s_fit_tuples", "l0s_screen_tuples", "l0s_get_gram", "l0s_unrank", "l0s_rank",
     "l0s_count", "l0s_fp64_peak", "l0s_rcp_check", "l0s_gram_shard_size", "l0s_stage_shard",
     "l0s_stage_finish", "l0s_sis_prepare", "l0s_sis_scores", "l0s_set_gram_mode", "l0s_stage_info",
-    "l0s_stage_append",
+    "l0s_stage_append", "l0s_gen_pool", "l0s_gen_eval", "l0s_gen_take", "l0s_gen_fetch",
 )
 
 
@@ -90,6 +90,10 @@ def lib():
         L.l0s_stage_shard.argtypes = [vp, vp, i64, i64, vp, vp, vp, i32, i32, i32, i32, i32, vp]
         L.l0s_stage_finish.argtypes = [vp, vp]
         L.l0s_stage_append.argtypes = [vp, vp, i64]
+        L.l0s_gen_pool.argtypes = [vp, vp, i64, i64, i32]
+        L.l0s_gen_eval.argtypes = [vp, i32, vp, vp, i64, vp, dbl, dbl, dbl, dbl, vp, vp]
+        L.l0s_gen_take.argtypes = [vp, vp, i64, vp, P(vp)]
+        L.l0s_gen_fetch.argtypes = [vp, vp, i64, vp]
         L.l0s_set_gram_mode.argtypes = [vp, i32]
         L.l0s_stage_info.argtypes = [vp, vp, vp]
         L.l0s_sis_prepare.argtypes = [vp, vp, i32, i64, vp, vp, i32]
@@ -232,6 +236,49 @@ class Engine:
             src, is_dev = ctypes.c_void_p(device_ptr), 1
         out = np.empty(int(k), dtype=np.float64)
         check(lib().l0s_sis_scores(self.handle, src, int(k), is_dev, ptr(out)), "l0s_sis_scores")
+        return out
+
+    # ---- final-rung candidates (csrc/gen.cu) ----
+    def gen_pool(self, values: np.ndarray) -> None:
+        """The pool's rows ((n_pool, s), float32 or float64: the pool's dtype) to the device."""
+        fp32 = values.dtype == np.float32
+        values = np.ascontiguousarray(values, dtype=np.float32 if fp32 else np.float64)
+        check(lib().l0s_gen_pool(self.handle, ptr(values), values.shape[0], values.shape[1], int(fp32)), "l0s_gen_pool")
+        self.gen_dtype = values.dtype
+        self.gen_s = values.shape[1]
+
+    def gen_eval(self, kind: int, pi=None, pj=None, values=None, *, tol: float, min_abs: float, max_abs: float,
+                 dedup_tol: float):
+        """Evaluate one chunk of candidates; returns (valid bool (k,), fingerprints bytes (16 k))."""
+        if values is not None:
+            values = np.ascontiguousarray(values, dtype=self.gen_dtype)
+            k = values.shape[0]
+            a = b = None
+        else:
+            a = np.ascontiguousarray(pi, dtype=np.int32)
+            b = None if pj is None else np.ascontiguousarray(pj, dtype=np.int32)
+            k = a.shape[0]
+        valid = np.empty(k, dtype=np.uint8)
+        h = np.empty(2 * k, dtype=np.uint64)
+        check(lib().l0s_gen_eval(self.handle, int(kind), None if a is None else ptr(a), None if b is None else ptr(b), k,
+                                 None if values is None else ptr(values), float(tol), float(min_abs), float(max_abs),
+                                 float(dedup_tol), ptr(valid), ptr(h)), "l0s_gen_eval")
+        return valid.view(bool), h.tobytes()
+
+    def gen_take(self, rows, host: bool = False):
+        """Compact rows of the last evaluation on the device; returns (host rows or None, device pointer)."""
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        out = np.empty((rows.shape[0], self.gen_s), dtype=self.gen_dtype) if host else None
+        dev = ctypes.c_void_p()
+        check(lib().l0s_gen_take(self.handle, ptr(rows), rows.shape[0], None if out is None else ptr(out),
+                                 ctypes.byref(dev)), "l0s_gen_take")
+        return out, dev.value
+
+    def gen_fetch(self, rows) -> np.ndarray:
+        """Rows of the taken block to the host (pool dtype)."""
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        out = np.empty((rows.shape[0], self.gen_s), dtype=self.gen_dtype)
+        check(lib().l0s_gen_fetch(self.handle, ptr(rows), rows.shape[0], ptr(out)), "l0s_gen_fetch")
         return out
 
     def search(self, n: int, keep: int, rank_begin: int = 0, rank_end: int = 2**63 - 1, mode: str = "auto"):

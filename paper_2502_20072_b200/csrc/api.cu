@@ -138,6 +138,10 @@ struct l0s_ctx {
     DBuf qr_ssr, qr_ratio, qr_score, qr_minr;
     // SIS projection scores
     DBuf sis_y, sis_yc, sis_sy, sis_perm, sis_bounds, sis_F, sis_out, sis_dest, sis_tE, sis_tpoff;
+    // final-rung candidates (gen.cu)
+    DBuf gen_pool, gen_pi, gen_pj, gen_vals, gen_valid, gen_hash, gen_take, gen_rows, gen_out;
+    int64_t gen_n = 0, gen_s = 0, gen_count = 0, gen_taken = 0;
+    int gen_fp32 = 0;
     int sis_R = 0, sis_T = 0, sis_rowlen = 0;
     int64_t sis_s = 0;
     std::unordered_map<int64_t, Rec> recs;  // records of this search's refit candidates
@@ -150,7 +154,8 @@ struct l0s_ctx {
                        &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
                        &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr, &sis_y, &sis_yc, &sis_sy, &sis_perm,
-                       &sis_bounds, &sis_F, &sis_out, &sis_dest, &sis_tE, &sis_tpoff, &oz_q, &oz_ex, &oz_koff};
+                       &sis_bounds, &sis_F, &sis_out, &sis_dest, &sis_tE, &sis_tpoff, &oz_q, &oz_ex, &oz_koff,
+                       &gen_pool, &gen_pi, &gen_pj, &gen_vals, &gen_valid, &gen_hash, &gen_take, &gen_rows, &gen_out};
         for (DBuf* b : all) b->release();
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -1248,6 +1253,118 @@ int l0s_sis_scores(l0s_ctx* c, const double* F, int64_t k, int is_device, double
         return fail(L0S_EINVAL, "%lld samples exceed the SIS kernel's shared-memory row", (long long)s);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out, c->sis_out.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return L0S_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Final-rung candidates (generation.iter_final_rung, generation.py:331-393)
+// ---------------------------------------------------------------------------
+
+int l0s_gen_pool(l0s_ctx* c, const void* values, int64_t n_pool, int64_t s, int fp32) {
+    if (!c) return fail(L0S_EINVAL, "null context");
+    if (n_pool < 0 || s < 1) return fail(L0S_EINVAL, "need n_pool >= 0 and s >= 1");
+    CK(cudaSetDevice(c->dev));
+    const size_t w = fp32 ? 4 : 8;
+    CK(c->gen_pool.ensure(w * std::max<int64_t>(n_pool, 1) * s));
+    if (n_pool) CK(cudaMemcpyAsync(c->gen_pool.p, values, w * n_pool * s, cudaMemcpyHostToDevice, c->st));
+    c->gen_n = n_pool;
+    c->gen_s = s;
+    c->gen_fp32 = fp32 ? 1 : 0;
+    c->gen_count = 0;
+    c->gen_taken = 0;
+    return L0S_OK;
+}
+
+int l0s_gen_eval(l0s_ctx* c, int kind, const int32_t* pi, const int32_t* pj, int64_t count, const void* values,
+                 double tol, double min_abs, double max_abs, double dedup_tol, uint8_t* out_valid,
+                 uint64_t* out_hash) {
+    if (!c || c->gen_s < 1) return fail(L0S_ESTATE, "l0s_gen_pool must be called first");
+    if (kind < GEN_COPY || kind > GEN_VALUES) return fail(L0S_EINVAL, "bad operator kind %d", kind);
+    if (count < 0 || count > (int64_t)1 << 30) return fail(L0S_EINVAL, "bad candidate count %lld", (long long)count);
+    if (kind == GEN_VALUES ? values == nullptr : pi == nullptr) return fail(L0S_EINVAL, "missing candidate input");
+    CK(cudaSetDevice(c->dev));
+    const int64_t s = c->gen_s;
+    const size_t w = c->gen_fp32 ? 4 : 8;
+    c->gen_count = 0;
+    c->gen_taken = 0;
+    if (count == 0) return L0S_OK;
+    const void* A = c->gen_pool.p;
+    const int* dpi = nullptr;
+    const int* dpj = nullptr;
+    if (kind == GEN_VALUES) {
+        CK(c->gen_take.ensure(w * count * s));  // staging for the precomputed rows
+        CK(cudaMemcpyAsync(c->gen_take.p, values, w * count * s, cudaMemcpyHostToDevice, c->st));
+        A = c->gen_take.p;
+    } else {
+        for (int64_t x = 0; x < count; ++x) {
+            if (pi[x] < 0 || pi[x] >= c->gen_n || (pj && (pj[x] < -1 || pj[x] >= c->gen_n)))
+                return fail(L0S_EINVAL, "candidate %lld: child index outside the pool", (long long)x);
+        }
+        CK(c->gen_pi.ensure(sizeof(int) * count));
+        CK(cudaMemcpyAsync(c->gen_pi.p, pi, sizeof(int) * count, cudaMemcpyHostToDevice, c->st));
+        dpi = c->gen_pi.as<int>();
+        if (pj) {
+            CK(c->gen_pj.ensure(sizeof(int) * count));
+            CK(cudaMemcpyAsync(c->gen_pj.p, pj, sizeof(int) * count, cudaMemcpyHostToDevice, c->st));
+            dpj = c->gen_pj.as<int>();
+        }
+    }
+    CK(c->gen_vals.ensure(sizeof(double) * count * s));
+    CK(c->gen_valid.ensure((size_t)count));
+    CK(c->gen_hash.ensure(sizeof(uint64_t) * 2 * count));
+    launch_gen_eval(A, c->gen_fp32, s, dpi, dpj, (int)count, kind, tol, min_abs, max_abs, dedup_tol,
+                    c->gen_vals.as<double>(), c->gen_valid.as<unsigned char>(), c->gen_hash.as<unsigned long long>(),
+                    c->st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out_valid, c->gen_valid.p, (size_t)count, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(out_hash, c->gen_hash.p, sizeof(uint64_t) * 2 * count, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    c->gen_count = count;
+    return L0S_OK;
+}
+
+int l0s_gen_take(l0s_ctx* c, const int32_t* rows, int64_t count, void* host_out, const double** dev_out) {
+    if (!c || c->gen_count < 1) return fail(L0S_ESTATE, "no evaluated candidates (l0s_gen_eval)");
+    if (count < 0) return fail(L0S_EINVAL, "negative row count");
+    for (int64_t x = 0; x < count; ++x)
+        if (rows[x] < 0 || rows[x] >= c->gen_count) return fail(L0S_EINVAL, "row %d outside the chunk", rows[x]);
+    CK(cudaSetDevice(c->dev));
+    const int64_t s = c->gen_s;
+    CK(c->gen_rows.ensure(sizeof(int) * std::max<int64_t>(count, 1)));
+    CK(c->gen_take.ensure(sizeof(double) * std::max<int64_t>(count, 1) * s));
+    if (count) {
+        CK(cudaMemcpyAsync(c->gen_rows.p, rows, sizeof(int) * count, cudaMemcpyHostToDevice, c->st));
+        launch_gen_gather(c->gen_vals.as<double>(), s, c->gen_rows.as<int>(), (int)count, 0, c->gen_take.p, c->st);
+        CK(cudaGetLastError());
+    }
+    c->gen_taken = count;
+    if (host_out && count) {
+        const size_t w = c->gen_fp32 ? 4 : 8;
+        CK(c->gen_out.ensure(w * count * s));
+        launch_gen_gather(c->gen_vals.as<double>(), s, c->gen_rows.as<int>(), (int)count, c->gen_fp32, c->gen_out.p,
+                          c->st);
+        CK(cudaMemcpyAsync(host_out, c->gen_out.p, w * count * s, cudaMemcpyDeviceToHost, c->st));
+    }
+    CK(cudaStreamSynchronize(c->st));
+    if (dev_out) *dev_out = c->gen_take.as<double>();
+    return L0S_OK;
+}
+
+int l0s_gen_fetch(l0s_ctx* c, const int32_t* rows, int64_t count, void* host_out) {
+    if (!c || c->gen_taken < 1) return fail(L0S_ESTATE, "no taken rows (l0s_gen_take)");
+    for (int64_t x = 0; x < count; ++x)
+        if (rows[x] < 0 || rows[x] >= c->gen_taken) return fail(L0S_EINVAL, "row %d outside the taken rows", rows[x]);
+    if (count <= 0) return L0S_OK;
+    CK(cudaSetDevice(c->dev));
+    const int64_t s = c->gen_s;
+    const size_t w = c->gen_fp32 ? 4 : 8;
+    CK(c->gen_rows.ensure(sizeof(int) * count));
+    CK(c->gen_out.ensure(w * count * s));
+    CK(cudaMemcpyAsync(c->gen_rows.p, rows, sizeof(int) * count, cudaMemcpyHostToDevice, c->st));
+    launch_gen_gather(c->gen_take.as<double>(), s, c->gen_rows.as<int>(), (int)count, c->gen_fp32, c->gen_out.p, c->st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(host_out, c->gen_out.p, w * count * s, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     return L0S_OK;
 }

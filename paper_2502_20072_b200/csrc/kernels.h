@@ -234,6 +234,27 @@ int launch_sis_scores(const double* F, int64_t k, int64_t s, const int64_t* perm
                       const int64_t* bounds, const int* tE, const int* tpoff, int rowlen, int T, const double* yc,
                       const double* sy, int R, double* out, int nsm, cudaStream_t st);
 
+// ---- final-rung candidates (gen.cu): values, validity, fingerprints ----
+enum GenKind {
+    GEN_COPY = 0,  // the row itself (the pool's own fingerprints)
+    GEN_ADD = 1,
+    GEN_SUB = 2,
+    GEN_MUL = 3,
+    GEN_DIV = 4,
+    GEN_ABS_DIFF = 5,
+    GEN_SQRT = 6,
+    GEN_SQ = 7,
+    GEN_CB = 8,
+    GEN_INV = 9,
+    GEN_ABS = 10,
+    GEN_VALUES = 11,  // precomputed candidate rows (libm operators)
+};
+void launch_gen_eval(const void* A, int fp32, int64_t s, const int* pi, const int* pj, int count, int kind, double tol,
+                     double min_abs, double max_abs, double dedup_tol, double* vals, unsigned char* valid,
+                     unsigned long long* hash, cudaStream_t st);
+void launch_gen_gather(const double* vals, int64_t s, const int* rows, int count, int fp32, void* out,
+                       cudaStream_t st);
+
 // ---- misc ----
 double fp64_peak_tflops(int dev);
 

@@ -49,8 +49,8 @@ def chunk_scores(matrix, target, *, device: int | None = None) -> np.ndarray:
         return _scores_locked(F, target, device)
 
 
-def _scores_locked(F, target, device):
-    eng = _lib.engine(device)
+def _scores_locked(F, target, device, eng=None, dev=None):
+    eng = eng if eng is not None else _lib.engine(device)
     groups = [target.targets[i:i + _MAX_TARGETS] for i in range(0, len(target.targets), _MAX_TARGETS)]
     out = None
     for g, tg in enumerate(groups):
@@ -61,9 +61,65 @@ def _scores_locked(F, target, device):
             eng.sis_prepare(np.stack([np.asarray(t, dtype=np.float64) for t in tg]), perm, bounds)
             eng._sis_target = weakref.ref(target)
             eng._sis_key = key
-        sc = eng.sis_scores(F)
+        sc = eng.sis_scores(F) if dev is None else eng.sis_scores(None, device_ptr=dev[0], k=dev[1])
         out = sc if out is None else np.maximum(out, sc)
     return out
+
+
+def device_chunk_scores(eng, dev_ptr: int, k: int, target) -> np.ndarray:
+    """Scores of k fp64 rows already on the engine's device (a generation.DeviceChunk)."""
+    if k == 0:
+        return np.zeros(0)
+    with _lock:
+        return _scores_locked(None, target, None, eng=eng, dev=(dev_ptr, k))
+
+
+def sis_select(source, target, n_sis_select: int, already_selected=None, workers: int = 1, chunk_size: int = 65536):
+    """Screen a candidate stream and grow the selected subspace (screening.sis_select,
+    screening.py:201-257): the same entries, scores and order -- the top ``n_sis_select`` new
+    candidates by (score desc, canonical key asc).
+
+    Chunks may be host matrices (scored through ``chunk_scores``) or ``DeviceChunk`` blocks
+    from ``generation.iter_final_rung(on_device=True)``, scored where they lie; a row's
+    values are copied out only when it enters the running top list (the reference copies
+    every new row of every chunk).  ``workers`` is accepted for the signature.
+    """
+    from descsearch.generation import FeatureSpace
+    from descsearch.screening import EmptySpace, SelectedSubspace, SubspaceEntry
+
+    from .generation import DeviceChunk
+
+    if n_sis_select < 1:
+        raise ValueError("n_sis_select must be positive")
+    prior = already_selected if already_selected is not None else SelectedSubspace()
+    taken = prior.keys()
+    chunks = source.iter_batches(chunk_size) if isinstance(source, FeatureSpace) else iter(source)
+    best: list = []  # [-score, key, expr, values or None, row] ascending
+    n_new_seen = 0
+    for exprs, matrix in chunks:
+        on_dev = isinstance(matrix, DeviceChunk)
+        scores = matrix.sis_scores(target) if on_dev else chunk_scores(matrix, target)
+        cand = []
+        for i, expr in enumerate(exprs):
+            if expr.key in taken:
+                continue
+            n_new_seen += 1
+            cand.append([-float(scores[i]), expr.key, expr, None, i])
+        if not cand:
+            continue
+        best = sorted(best + cand, key=lambda item: (item[0], item[1]))[:n_sis_select]
+        fresh = [item for item in best if item[3] is None]
+        if fresh:
+            if on_dev:
+                rows = matrix.rows([item[4] for item in fresh])
+                for item, r in zip(fresh, rows):
+                    item[3] = np.array(r, copy=True)
+            else:
+                for item in fresh:
+                    item[3] = np.array(matrix[item[4]], copy=True)
+    if n_new_seen == 0:
+        raise EmptySpace("no unselected candidates in the screened space")
+    return prior.extended([SubspaceEntry(expr, -neg, vals) for neg, _, expr, vals, _ in best])
 
 
 def projection_score(feature_values, target, *, device: int | None = None) -> float:
@@ -72,4 +128,4 @@ def projection_score(feature_values, target, *, device: int | None = None) -> fl
     return float(chunk_scores(v[None, :], target, device=device)[0])
 
 
-__all__ = ["chunk_scores", "projection_score"]
+__all__ = ["chunk_scores", "device_chunk_scores", "projection_score", "sis_select"]

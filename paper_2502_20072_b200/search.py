@@ -290,12 +290,15 @@ def fit_tuples(values, property_values, tuples, task_slices=None, precision: str
     return eng.fit_tuples(np.asarray(tuples, dtype=np.int64))
 
 
-def install(sis: bool = True):
+def install(sis: bool = True, gen: bool = True):
     """Route the reference package's l0 entry points to this implementation.
 
     Patches descsearch.search.{l0_search, fit_tuple}, the names the pipeline
     bound at import (pipeline.py:34) and the package re-exports; with ``sis``
-    also the SIS projection scores (screening._chunk_scores, screening.py:126).
+    also the SIS projection scores (screening._chunk_scores, screening.py:126);
+    with ``gen`` the streamed last rung (generation.iter_final_rung,
+    generation.py:331-393) and the pipeline's screen of it (pipeline.py:25-33:
+    candidates evaluated, screened and kept on the device, ``generation.py`` here).
     Returns a callable that restores the originals.
     """
     import sys
@@ -321,6 +324,19 @@ def install(sis: bool = True):
     if sis:  # SIS projection scores (screening._chunk_scores, looked up by sis_select at call time)
         saved.append((ref_screening, "_chunk_scores", ref_screening._chunk_scores))
         ref_screening._chunk_scores = lambda matrix, target: gpu_screening.chunk_scores(matrix, target)
+    if gen:  # the streamed last rung: evaluated on the device, screened there by the pipeline
+        import functools
+
+        import descsearch.generation as ref_generation
+
+        from . import generation as gpu_generation
+
+        saved += [(ref_generation, "iter_final_rung", ref_generation.iter_final_rung),
+                  (pipeline, "iter_final_rung", pipeline.iter_final_rung),
+                  (pipeline, "sis_select", pipeline.sis_select)]
+        ref_generation.iter_final_rung = gpu_generation.iter_final_rung
+        pipeline.iter_final_rung = functools.partial(gpu_generation.iter_final_rung, on_device=True)
+        pipeline.sis_select = gpu_screening.sis_select
     ref_search.l0_search = l0_search
     ref_search.fit_tuple = fit_tuple
     pipeline.l0_search = l0_search

@@ -1,0 +1,145 @@
+"""Streamed last rung on the device against the reference.
+
+* iter_final_rung: the kept expressions, chunk sizes, value bytes (blake2b per chunk) and
+  RungStats equal the reference's own run (tests/golden/make_golden_gen.py), for IEEE
+  operators, libm operators (values from numpy, validity / fingerprints on the device) and
+  a float32 pool;
+* sis_select over the device stream returns the reference's entries (keys, score bits,
+  value bits);
+* run_pipeline with the last rung streamed writes the reference's model files byte for byte.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import bits_equal
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+CASES = {
+    "stream_c1": (dict(n_primary=10, n_samples=100, n_tasks=1, seed=0), ["add", "sub", "mul", "div", "sqrt"], 2,
+                  "fp64", 50_000, {}),
+    "stream_ops": (dict(n_primary=6, n_samples=90, n_tasks=3, seed=4),
+                   ["abs_diff", "sq", "cb", "inv", "abs", "exp", "log", "cbrt"], 2, "fp64", 7_000, {}),
+    "stream_fp32": (dict(n_primary=7, n_samples=64, n_tasks=2, seed=7), ["add", "mul", "div", "sqrt", "sub"], 2,
+                    "fp32", 100_000, dict(min_abs_value=1e-3, max_abs_value=1e3)),
+}
+
+
+def _reference():
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if os.path.isdir(ref) and ref not in sys.path:
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_l0s")
+        sys.path.append(ref)
+    try:
+        import descsearch  # noqa: F401
+    except Exception:
+        pytest.skip("reference package not importable here")
+
+
+def _pool(name):
+    from descsearch.dataio import make_synthetic_dataset
+    from descsearch.expressions import get_operator
+    from descsearch.generation import FeatureSpace, GenerationConfig, generate_rung
+
+    dsk, ops, max_rung, precision, vbs, limits = CASES[name]
+    ds = make_synthetic_dataset(**dsk)
+    pool = FeatureSpace.from_primaries(ds.primary_names, ds.primary_units, ds.primary_values, precision=precision,
+                                       dedup_tolerance=1e-12)
+    gcfg = GenerationConfig(operators=[get_operator(o) for o in ops], max_rung=max_rung, materialize_last_rung=False,
+                            value_batch_size=vbs, **limits)
+    for r in range(1, max_rung):
+        generate_rung(pool, r, gcfg)
+    return ds, pool, gcfg
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_iter_final_rung_matches_reference(name):
+    _reference()
+    from descsearch.expressions import render
+    from descsearch.generation import RungStats
+
+    from paper_2502_20072_b200.generation import iter_final_rung
+
+    g = np.load(os.path.join(GOLDEN, f"gen_{name}.npz"))
+    _, pool, gcfg = _pool(name)
+    assert len(pool) == int(g["pool_size"])
+    stats = RungStats(rung=gcfg.max_rung)
+    exprs, sizes, digests = [], [], []
+    for ex, mat in iter_final_rung(pool, gcfg, 1, None, stats):
+        assert mat.dtype == pool.dtype and mat.flags.c_contiguous
+        exprs.extend(render(e) for e in ex)
+        sizes.append(len(ex))
+        digests.append(hashlib.blake2b(mat.tobytes(), digest_size=16).hexdigest())
+    assert [stats.n_pairs, stats.n_invalid, stats.n_dup_key, stats.n_dup_value, stats.n_kept] == g["stats"].tolist()
+    assert sizes == g["sizes"].tolist()
+    assert exprs == g["exprs"].tolist()
+    assert digests == g["digests"].tolist()
+
+
+@pytest.mark.parametrize("name", ["stream_c1", "stream_fp32"])
+def test_device_stream_and_sis_select_match_reference(name):
+    """The device stream (DeviceChunk blocks) holds the same rows, and sis_select over it picks
+    the reference sis_select's entries from the reference stream."""
+    _reference()
+    from descsearch.generation import iter_final_rung as ref_iter
+    from descsearch.screening import ScreeningTarget, SelectedSubspace
+    from descsearch.screening import sis_select as ref_sis
+
+    from paper_2502_20072_b200.generation import DeviceChunk, iter_final_rung
+    from paper_2502_20072_b200.screening import sis_select
+
+    ds, pool, gcfg = _pool(name)
+    labels, slices = ds.task_partition()
+    y = np.asarray(ds.property_values, dtype=np.float64)
+    h_host, h_dev, n = hashlib.blake2b(digest_size=16), hashlib.blake2b(digest_size=16), 0
+    for _, mat in iter_final_rung(pool, gcfg):
+        h_host.update(mat.tobytes())
+    for ex, chunk in iter_final_rung(pool, gcfg, on_device=True):
+        assert isinstance(chunk, DeviceChunk) and chunk.shape[0] == len(ex)
+        h_dev.update(np.asarray(chunk).tobytes())
+        n += len(ex)
+    assert h_host.digest() == h_dev.digest() and n > 0
+    target = ScreeningTarget([y, y * y], slices, labels)
+    prior = SelectedSubspace()
+    want = ref_sis(ref_iter(pool, gcfg), target, 17, prior)
+    got = sis_select(iter_final_rung(pool, gcfg, on_device=True), target, 17, prior)
+    assert [e.expression.key for e in got.entries] == [e.expression.key for e in want.entries]
+    assert bits_equal([e.score for e in got.entries], [e.score for e in want.entries])
+    for a, b in zip(got.entries, want.entries):
+        assert a.values.dtype == b.values.dtype and bits_equal(a.values, b.values)
+
+
+@pytest.mark.parametrize("name,dim,n_sis", [("stream_c1", 2, 20), ("stream_ops", 2, 15), ("stream_fp32", 2, 12)])
+def test_streamed_pipeline_model_files(tmp_path, name, dim, n_sis):
+    """run_pipeline with the last rung streamed through the device (install(): generation,
+    screen, SIS scores, l0 search) writes the reference's model files byte for byte."""
+    _reference()
+    from descsearch.dataio import RunConfig, make_synthetic_dataset
+    from descsearch.expressions import render
+    from descsearch.pipeline import run_pipeline, write_outputs
+
+    import paper_2502_20072_b200 as l0
+
+    g = np.load(os.path.join(GOLDEN, f"pipe_{name}.npz"))
+    dsk, ops, max_rung, precision, vbs, limits = CASES[name]
+    ds = make_synthetic_dataset(**dsk)
+    cfg = RunConfig(property_key="target", operators=ops, max_rung=max_rung, dimension=dim, n_sis_select=n_sis,
+                    autotune=False, materialize_last_rung=False, precision=precision, value_batch_size=vbs,
+                    **limits)
+    undo = l0.install()
+    try:
+        res = run_pipeline(ds, cfg)
+        write_outputs(res, cfg, str(tmp_path))
+    finally:
+        undo()
+    assert [render(e.expression) for e in res.subspace.entries] == g["subspace"].tolist()
+    for d in range(1, dim + 1):
+        assert (tmp_path / f"models_dim{d}.txt").read_bytes() == g[f"d{d}_models_file"].tobytes()
