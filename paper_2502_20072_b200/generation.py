@@ -19,8 +19,9 @@ device: a GPU libm differs from numpy's in the last ulp, which would move the va
 dedup decisions.
 
 ``on_device=True`` (what ``install()`` wires into the pipeline together with
-``screening.sis_select``) yields ``DeviceChunk`` blocks instead of host matrices: the kept
-rows never leave the device unless the screen selects them.
+``screening.sis_select``) yields ``DeviceChunk`` blocks instead of host matrices, and
+``PendingExpr`` records (canonical key now, expression node on ``build()``): the kept rows
+never leave the device and the nodes are never built unless the screen selects them.
 """
 
 from __future__ import annotations
@@ -69,6 +70,76 @@ class DeviceChunk:
         return a if dtype is None else a.astype(dtype)
 
 
+def _key(op, ka: str, kb: str | None) -> str:
+    """expressions.apply's canonical key (expressions.py:152-161), without building the node."""
+    if kb is None:
+        return f"{op.kind}({ka})"
+    if op.commutative:
+        ab, ba = ka + "," + kb, kb + "," + ka
+        return f"{op.kind}({ab if ab <= ba else ba})"
+    return f"{op.kind}({ka},{kb})"
+
+
+class PendingExpr:
+    """A kept candidate of the device stream: its canonical key now, the expression node
+    (expressions.apply) when ``build()`` is called -- sis_select builds only the ones it keeps."""
+
+    __slots__ = ("op", "a", "b", "key")
+
+    def __init__(self, op, a, b, key):
+        self.op, self.a, self.b, self.key = op, a, b, key
+
+    def build(self):
+        from descsearch.expressions import apply
+
+        return apply(self.op, self.a) if self.b is None else apply(self.op, self.a, self.b)
+
+
+def pair_arrays(op, pool, target_rung: int):
+    """generation.generate_pairs (generation.py:205-242) as index arrays (pj = -1: unary):
+    the same pairs in the same order (first child ascending, second ascending within it),
+    built with numpy masks over the eligible features instead of a Python double loop; the
+    unit rule (expressions.check_unit) is evaluated once per distinct unit pair."""
+    from descsearch.expressions import check_unit
+
+    prev = target_rung - 1
+    if prev < 0:
+        raise ValueError("target_rung must be at least 1")
+    feats = pool.features
+    if op.arity == 1:
+        idx = [i for i in pool.rung_indices(prev) if check_unit(op, (feats[i].unit,)) is not None]
+        return np.asarray(idx, dtype=np.int32), np.full(len(idx), -1, dtype=np.int32)
+    elig = [i for i in range(len(pool)) if feats[i].rung <= prev]
+    if not elig:
+        return np.zeros(0, dtype=np.int32), np.zeros(0, dtype=np.int32)
+    units, uid = {}, []
+    for i in elig:
+        uid.append(units.setdefault(feats[i].unit, len(units)))
+    ulist = list(units)
+    ok = np.array([[check_unit(op, (ua, ub)) is not None for ub in ulist] for ua in ulist], dtype=bool)
+    e = np.asarray(elig, dtype=np.int64)
+    u = np.asarray(uid, dtype=np.int64)
+    r = np.asarray([feats[i].rung for i in elig], dtype=np.int64)
+    zero_b = np.asarray([pool._has_zero[i] for i in elig], dtype=bool) if op.kind == "div" else None
+    n = len(elig)
+    out_i, out_j = [], []
+    step = max(1, (1 << 22) // max(n, 1))  # first children per block: ~4M candidate cells
+    for a0 in range(0, n, step):
+        a1 = min(n, a0 + step)
+        A = np.arange(a0, a1)[:, None]
+        B = np.arange(n)[None, :]
+        m = np.maximum(r[A], r[B]) == prev
+        if op.commutative:
+            m &= B >= A
+        m &= ok[u[A], u[B]]
+        if zero_b is not None:
+            m &= ~zero_b[B]
+        aa, bb = np.nonzero(m)  # row-major: first child, then second
+        out_i.append(e[aa + a0])
+        out_j.append(e[bb])
+    return (np.concatenate(out_i).astype(np.int32), np.concatenate(out_j).astype(np.int32))
+
+
 def pool_fingerprints(eng, pool) -> set:
     """The pool's own fingerprints, in the device's scheme (pool.dedup_state()'s role)."""
     n = len(pool)
@@ -85,7 +156,7 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
     (generation.iter_final_rung, generation.py:331-393): same (expressions, values) chunks in
     the same order, same ``stats`` counters; ``workers`` is accepted for the signature."""
     from descsearch.expressions import apply, apply_operator_values
-    from descsearch.generation import RungStats, generate_pairs
+    from descsearch.generation import RungStats
 
     target_rung = config.max_rung
     if stats is None:
@@ -96,6 +167,7 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
     eng.gen_pool(pool.values_matrix())
     fps = pool_fingerprints(eng, pool)
     feats = pool.features
+    fkeys = [f.key for f in feats]
     vals = pool.values
     tol = config.dedup_tolerance
     limits = dict(tol=tol, min_abs=config.min_abs_value, max_abs=config.max_abs_value, dedup_tol=tol)
@@ -104,40 +176,44 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
 
     for op in config.operators:
         t0 = time.perf_counter()
-        pairs = generate_pairs(op, pool, target_rung).pairs
-        stats.n_pairs += len(pairs)
+        all_i, all_j = pair_arrays(op, pool, target_rung)
+        stats.n_pairs += len(all_i)
         kind = DEVICE_KINDS.get(op.kind)
         spent += time.perf_counter() - t0
-        for start in range(0, len(pairs), batch):  # the reference's value batches
+        for start in range(0, len(all_i), batch):  # the reference's value batches
             t0 = time.perf_counter()
-            chunk = pairs[start:start + batch]
+            stop = min(len(all_i), start + batch)
             out_exprs, out_rows = [], []
-            for sub in range(0, len(chunk), SUB_CHUNK):
-                sc = chunk[sub:sub + SUB_CHUNK]
+            for sub in range(start, stop, SUB_CHUNK):
+                pi, pj = all_i[sub:min(stop, sub + SUB_CHUNK)], all_j[sub:min(stop, sub + SUB_CHUNK)]
                 if kind is None:
-                    host = np.stack([apply_operator_values(op.kind, vals[i]) if j is None
-                                     else apply_operator_values(op.kind, vals[i], vals[j]) for i, j in sc])
+                    host = np.stack([apply_operator_values(op.kind, vals[i]) if j < 0
+                                     else apply_operator_values(op.kind, vals[i], vals[j])
+                                     for i, j in zip(pi.tolist(), pj.tolist())])
                     valid, h = eng.gen_eval(GEN_VALUES, values=host, **limits)
                 else:
-                    pi = np.fromiter((p[0] for p in sc), dtype=np.int32, count=len(sc))
-                    pj = np.fromiter((-1 if p[1] is None else p[1] for p in sc), dtype=np.int32, count=len(sc))
                     valid, h = eng.gen_eval(kind, pi=pi, pj=pj, **limits)
                 exprs, kept = [], []
-                for row, (i, j) in enumerate(sc):
-                    if not valid[row]:
-                        stats.n_invalid += 1
-                        continue
-                    expr = apply(op, feats[i]) if j is None else apply(op, feats[i], feats[j])
-                    if expr.key in keys:
+                rows_ok = np.flatnonzero(valid)
+                stats.n_invalid += len(pi) - len(rows_ok)
+                li, lj = pi[rows_ok].tolist(), pj[rows_ok].tolist()
+                for row, i, j in zip(rows_ok.tolist(), li, lj):  # the reference's ordered walk (generation.py:364-385)
+                    if j < 0:
+                        j = None
+                    key = _key(op, fkeys[i], None if j is None else fkeys[j])
+                    if key in keys:
                         stats.n_dup_key += 1
                         continue
                     fp = h[16 * row:16 * row + 16]
                     if fp in fps:
                         stats.n_dup_value += 1
                         continue
-                    keys.add(expr.key)
+                    keys.add(key)
                     fps.add(fp)
-                    exprs.append(expr)
+                    if on_device:
+                        exprs.append(PendingExpr(op, feats[i], None if j is None else feats[j], key))
+                    else:
+                        exprs.append(apply(op, feats[i]) if j is None else apply(op, feats[i], feats[j]))
                     kept.append(row)
                     stats.n_kept += 1
                 if not exprs:
@@ -164,4 +240,4 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
         timer.add(spent)
 
 
-__all__ = ["DeviceChunk", "iter_final_rung", "pool_fingerprints", "DEVICE_KINDS"]
+__all__ = ["DeviceChunk", "PendingExpr", "iter_final_rung", "pair_arrays", "pool_fingerprints", "DEVICE_KINDS"]

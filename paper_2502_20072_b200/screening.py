@@ -87,7 +87,7 @@ def sis_select(source, target, n_sis_select: int, already_selected=None, workers
     from descsearch.generation import FeatureSpace
     from descsearch.screening import EmptySpace, SelectedSubspace, SubspaceEntry
 
-    from .generation import DeviceChunk
+    from .generation import DeviceChunk, PendingExpr
 
     if n_sis_select < 1:
         raise ValueError("n_sis_select must be positive")
@@ -98,13 +98,11 @@ def sis_select(source, target, n_sis_select: int, already_selected=None, workers
     n_new_seen = 0
     for exprs, matrix in chunks:
         on_dev = isinstance(matrix, DeviceChunk)
-        scores = matrix.sis_scores(target) if on_dev else chunk_scores(matrix, target)
-        cand = []
-        for i, expr in enumerate(exprs):
-            if expr.key in taken:
-                continue
-            n_new_seen += 1
-            cand.append([-float(scores[i]), expr.key, expr, None, i])
+        scores = np.asarray(matrix.sis_scores(target) if on_dev else chunk_scores(matrix, target))
+        n_new_seen += len(exprs) - (sum(1 for e in exprs if e.key in taken) if taken else 0)
+        # only a score at or above the current n-th can enter the list (ties go by key)
+        idx = np.flatnonzero(scores >= -best[-1][0]) if len(best) >= n_sis_select else range(len(exprs))
+        cand = [[-float(scores[i]), exprs[i].key, exprs[i], None, i] for i in idx if exprs[i].key not in taken]
         if not cand:
             continue
         best = sorted(best + cand, key=lambda item: (item[0], item[1]))[:n_sis_select]
@@ -119,7 +117,8 @@ def sis_select(source, target, n_sis_select: int, already_selected=None, workers
                     item[3] = np.array(matrix[item[4]], copy=True)
     if n_new_seen == 0:
         raise EmptySpace("no unselected candidates in the screened space")
-    return prior.extended([SubspaceEntry(expr, -neg, vals) for neg, _, expr, vals, _ in best])
+    return prior.extended([SubspaceEntry(expr.build() if isinstance(expr, PendingExpr) else expr, -neg, vals)
+                           for neg, _, expr, vals, _ in best])
 
 
 def projection_score(feature_values, target, *, device: int | None = None) -> float:

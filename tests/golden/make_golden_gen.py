@@ -8,7 +8,7 @@ Imports descsearch from /root/reference/pkg/src and writes, next to this file:
                     pipeline builds (rungs < max_rung materialized by generate_rung): the
                     kept expressions per yielded chunk (rendered), a blake2b digest of each
                     chunk's value matrix bytes, and the RungStats counters.
-* pipe_<name>.npz : run_pipeline with materialize_last_rung=False -- the models_dim<d>.txt
+* pipestream_<name>.npz : run_pipeline with materialize_last_rung=False -- the models_dim<d>.txt
                     bytes written by write_outputs (the same layout as make_golden.py's).
 
 The GPU box never runs this script; the tests read the committed fixtures.
@@ -89,9 +89,9 @@ def record_stream_pipeline(name, dim, n_sis):
             with open(os.path.join(td, f"models_dim{d}.txt"), "rb") as fh:
                 files[f"d{d}_models_file"] = np.frombuffer(fh.read(), dtype=np.uint8)
     keys = [render(e.expression) for e in result.subspace.entries]
-    np.savez_compressed(os.path.join(HERE, f"pipe_{name}.npz"), n_dims=np.int64(dim), subspace=np.array(keys),
+    np.savez_compressed(os.path.join(HERE, f"pipestream_{name}.npz"), n_dims=np.int64(dim), subspace=np.array(keys),
                         **files)
-    print(f"pipe_{name}: subspace {len(keys)}")
+    print(f"pipestream_{name}: subspace {len(keys)}")
 
 
 def main():

@@ -128,7 +128,7 @@ def test_streamed_pipeline_model_files(tmp_path, name, dim, n_sis):
 
     import paper_2502_20072_b200 as l0
 
-    g = np.load(os.path.join(GOLDEN, f"pipe_{name}.npz"))
+    g = np.load(os.path.join(GOLDEN, f"pipestream_{name}.npz"))
     dsk, ops, max_rung, precision, vbs, limits = CASES[name]
     ds = make_synthetic_dataset(**dsk)
     cfg = RunConfig(property_key="target", operators=ops, max_rung=max_rung, dimension=dim, n_sis_select=n_sis,
