@@ -1220,6 +1220,14 @@ int l0s_sis_prepare(l0s_ctx* c, const double* targets, int R, int64_t s, const i
         off += (int)(nsb * 32 * (E + 1));
     }
     c->sis_rowlen = off;
+    // slot of raw sample j (the kernel reads rows coalesced and scatters into shared memory)
+    std::vector<int> rdest((size_t)s, -1);
+    for (int64_t i = 0; i < s; ++i) {
+        if (perm[i] < 0 || perm[i] >= s || rdest[(size_t)perm[i]] >= 0)
+            return fail(L0S_EINVAL, "perm must be a permutation of [0, s)");
+        rdest[(size_t)perm[i]] = dest[(size_t)i];
+    }
+    dest.swap(rdest);
     CK(c->sis_dest.ensure(sizeof(int) * s));
     CK(c->sis_tE.ensure(sizeof(int) * ntasks));
     CK(c->sis_tpoff.ensure(sizeof(int) * ntasks));

@@ -228,7 +228,7 @@ void sort_pairs(double* lb, int64_t* rank, double* lb_tmp, int64_t* rank_tmp, in
 int sis_max_targets();
 void launch_sis_targets(const double* y, int R, int64_t s, const int64_t* perm, const int64_t* bounds, int T,
                         double* yc, double* sy, cudaStream_t st);
-// dest[j]: shared-memory slot of gathered sample j (task t's segment at tpoff[t], lane stride
+// dest[j]: shared-memory slot of raw sample j (task t's segment at tpoff[t], lane stride
 // tE[t] + 1 with tE[t] = max(1, pow2ceil(n_t) / 32)); rowlen = the padded row length
 int launch_sis_scores(const double* F, int64_t k, int64_t s, const int64_t* perm, const int* dest,
                       const int64_t* bounds, const int* tE, const int* tpoff, int rowlen, int T, const double* yc,

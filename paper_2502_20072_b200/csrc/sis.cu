@@ -24,7 +24,6 @@ namespace l0s {
 
 namespace {
 
-constexpr int SIS_WARPS = 4;  // features (warps) per CTA
 constexpr int SIS_MAXR = 8;  // targets per launch
 
 // Balanced tree over the zero-padded power-of-two row x[0 .. W) (x(i) = 0 for i >= ns):
@@ -103,6 +102,63 @@ __device__ __forceinline__ double sb_tree(int W, int ns, int lane, Get& x) {
     return __shfl_sync(L0S_FULL, total, 0);
 }
 
+// Two trees at once (the same shape), for two targets sharing the feature's loads.
+template <int E, typename Get>
+__device__ __forceinline__ double2 sb_tree2(int W, int ns, int lane, Get& x) {
+    constexpr int SB = 32 * E;
+    const int nsb = W > SB ? W / SB : 1;
+    const int width = W / E < 32 ? W / E : 32;
+    double t0 = 0.0, t1 = 0.0;
+    for (int q = 0; q < nsb; ++q) {
+        const int base = q * SB + lane * E;
+        double p0 = 0.0, p1 = 0.0;
+        if (lane < width) {
+            double v0[E], v1[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                if (base + e < ns) {
+                    const double2 xv = x(q, lane, e);
+                    v0[e] = xv.x;
+                    v1[e] = xv.y;
+                } else {
+                    v0[e] = 0.0;
+                    v1[e] = 0.0;
+                }
+            }
+#pragma unroll
+            for (int st = 1; st < E; st <<= 1)
+#pragma unroll
+                for (int e = 0; e < E; e += 2 * st) {
+                    v0[e] = __dadd_rn(v0[e], v0[e + st]);
+                    v1[e] = __dadd_rn(v1[e], v1[e + st]);
+                }
+            p0 = v0[0];
+            p1 = v1[0];
+        }
+        p0 = shfl_tree32(p0, lane, width);
+        p1 = shfl_tree32(p1, lane, width);
+        const double q0 = __shfl_sync(L0S_FULL, p0, 0), q1 = __shfl_sync(L0S_FULL, p1, 0);
+        if (lane == q) {
+            t0 = q0;
+            t1 = q1;
+        }
+    }
+    t0 = shfl_tree32(t0, lane, nsb);
+    t1 = shfl_tree32(t1, lane, nsb);
+    return make_double2(__shfl_sync(L0S_FULL, t0, 0), __shfl_sync(L0S_FULL, t1, 0));
+}
+
+template <typename Get>
+__device__ __forceinline__ double2 lane_tree2_any(int W, int ns, int lane, Get x) {
+    switch (W >= 512 ? 16 : (W >= 32 ? W / 32 : 1)) {
+        case 1: return sb_tree2<1>(W, ns, lane, x);
+        case 2: return sb_tree2<2>(W, ns, lane, x);
+        case 4: return sb_tree2<4>(W, ns, lane, x);
+        case 8: return sb_tree2<8>(W, ns, lane, x);
+        default: return sb_tree2<16>(W, ns, lane, x);
+    }
+}
+
 template <typename Get>
 __device__ __forceinline__ double lane_tree_any(int W, int ns, int lane, Get x) {
     switch (W >= 512 ? 16 : (W >= 32 ? W / 32 : 1)) {
@@ -147,28 +203,35 @@ __global__ void k_sis_targets(const double* __restrict__ y, int R, int64_t s, co
 }
 
 // scores[f] for the rows of F (k x s, row-major, dataset sample order).  Persistent: each
-// warp takes features f = warp_global, += total_warps.  A feature row is gathered (cp.async,
-// all in flight) into shared memory in task order, each task's segment laid out for the lane
-// trees (lane stride E_t + 1).
-__global__ void __launch_bounds__(SIS_WARPS * 32) k_sis_scores(
-    const double* __restrict__ F, int64_t k, int64_t s, const int64_t* __restrict__ perm,
-    const int* __restrict__ dest, const int64_t* __restrict__ bounds, const int* __restrict__ tE,
-    const int* __restrict__ tpoff, int rowlen, int T, const double* __restrict__ yc, const double* __restrict__ sy,
-    int R, double* __restrict__ out) {
-    extern __shared__ double srow[];  // SIS_WARPS rows of rowlen doubles, then src (int32), dest (int32)
+// warp takes features f = warp_global, += total_warps.  A feature row is read coalesced
+// (cp.async, all in flight) and scattered into shared memory in task order, each task's
+// segment laid out for the lane trees (lane stride E_t + 1).  The centered targets of this
+// launch's group (targets r0 .. r0 + R - 1) sit in shared memory in the same layout, so the
+// product trees read only shared memory.  accumulate: fold into out[] (np.maximum, NaN
+// propagating) -- target groups of one chunk run as consecutive launches.
+__global__ void k_sis_scores(const double* __restrict__ F, int64_t k, int64_t s, const int64_t* __restrict__ perm,
+                             const int* __restrict__ dest, const int64_t* __restrict__ bounds,
+                             const int* __restrict__ tE, const int* __restrict__ tpoff, int rowlen, int T,
+                             const double* __restrict__ yc, const double* __restrict__ sy, int R, int accumulate,
+                             double* __restrict__ out) {
+    extern __shared__ double smem[];  // R target rows, then one row per warp (rowlen doubles each),
+                                      // then the slot of each raw sample (int32)
+    const int nw = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* row = srow + (int64_t)warp * rowlen;
-    int* ssrc = reinterpret_cast<int*>(srow + (int64_t)SIS_WARPS * rowlen);
-    int* sdst = ssrc + s;
-    for (int64_t i = threadIdx.x; i < s; i += blockDim.x) {
-        ssrc[i] = (int)perm[i];
-        sdst[i] = dest[i];
-    }
+    double* ys = smem;
+    double* row = smem + (int64_t)(R + warp) * rowlen;
+    int* sdst = reinterpret_cast<int*>(smem + (int64_t)(R + nw) * rowlen);
+    for (int64_t i = threadIdx.x; i < s; i += blockDim.x) sdst[i] = dest[i];  // dest[j]: slot of raw sample j
+    __syncthreads();
+    // yc is in task order: position p holds raw sample perm[p]
+    for (int r = 0; r < R; ++r)
+        for (int64_t p = threadIdx.x; p < s; p += blockDim.x) ys[(int64_t)r * rowlen + sdst[perm[p]]] = yc[(int64_t)r * s + p];
     __syncthreads();
     const double total = (double)s;
-    for (int64_t f = (int64_t)blockIdx.x * SIS_WARPS + warp; f < k; f += (int64_t)gridDim.x * SIS_WARPS) {
+    for (int64_t f = (int64_t)blockIdx.x * nw + warp; f < k; f += (int64_t)gridDim.x * nw) {
         const double* src = F + f * s;
-        for (int64_t i = lane; i < s; i += 32) cp_async8(row + sdst[i], src + ssrc[i]);
+        // coalesced row read (raw sample order), scattered into the task-ordered layout
+        for (int64_t j = lane; j < s; j += 32) cp_async8(row + sdst[j], src + j);
         cp_async_commit();
         cp_async_wait<0>();
         __syncwarp();
@@ -180,26 +243,63 @@ __global__ void __launch_bounds__(SIS_WARPS * 32) k_sis_scores(
             if (ns == 0) continue;
             const int W = pow2_ge(ns);
             const int Et = tE[t];  // min(16, W / 32), >= 1
-            const double* xr = row + tpoff[t];
-            // element (super-block q, lane l, e) and its sample index within the task
+            const int off = tpoff[t];
+            const double* xr = row + off;
+            // element (super-block q, lane l, e) of the task's segment
             auto at = [&](int q, int l, int e) { return xr[(q * 32 + l) * (Et + 1) + e]; };
             const double w = (double)ns / total;
             const double mean = lane_tree_any(W, ns, lane, at) / (double)ns;
+            // center in place (Xc = X - mean, the reference's one rounding): every later tree
+            // reads Xc; a lane touches only its own slots
+            {
+                const int SBt = 32 * Et, nsb = W > SBt ? W / SBt : 1;
+                for (int q = 0; q < nsb; ++q)
+                    for (int e = 0; e < Et; ++e) {
+                        if (q * SBt + lane * Et + e < ns) {
+                            double* p = row + off + (q * 32 + lane) * (Et + 1) + e;
+                            *p = __dsub_rn(*p, mean);
+                        }
+                    }
+                __syncwarp();
+            }
             const double sxx = lane_tree_any(W, ns, lane, [&](int q, int l, int e) {
-                const double c = __dsub_rn(at(q, l, e), mean);
+                const double c = at(q, l, e);
                 return __dmul_rn(c, c);
             });
-            for (int r = 0; r < R; ++r) {
+            // targets in pairs: one pass over Xc feeds two product trees
+            int r = 0;
+            for (; r + 1 < R; r += 2) {
+                const double sy0 = sy[r * T + t], sy1 = sy[(r + 1) * T + t];
+                if (sy0 == 0.0 && sy1 == 0.0) continue;  // the reference skips the task for a target
+                const double* y0 = ys + (int64_t)r * rowlen + off;
+                const double* y1 = y0 + rowlen;
+                const double2 num = lane_tree2_any(W, ns, lane, [&](int q, int l, int e) {
+                    const int x = (q * 32 + l) * (Et + 1) + e;
+                    const double c = xr[x];
+                    return make_double2(__dmul_rn(c, y0[x]), __dmul_rn(c, y1[x]));
+                });
+                if (sy0 != 0.0) {
+                    const double den = __dsqrt_rn(__dmul_rn(sxx, sy0));
+                    const double rr = (den > 0.0) ? __ddiv_rn(fabs(num.x), den) : 0.0;
+                    acc[r] = __dadd_rn(acc[r], __dmul_rn(w, rr));  // numpy: acc += w * r, two roundings
+                }
+                if (sy1 != 0.0) {
+                    const double den = __dsqrt_rn(__dmul_rn(sxx, sy1));
+                    const double rr = (den > 0.0) ? __ddiv_rn(fabs(num.y), den) : 0.0;
+                    acc[r + 1] = __dadd_rn(acc[r + 1], __dmul_rn(w, rr));
+                }
+            }
+            for (; r < R; ++r) {
                 const double syr = sy[r * T + t];
-                if (syr == 0.0) continue;  // the reference skips the task for this target
-                const double* ycr = yc + (int64_t)r * s + lo;
-                const int SBt = 32 * Et;
+                if (syr == 0.0) continue;
+                const double* yr = ys + (int64_t)r * rowlen + off;
                 const double num = lane_tree_any(W, ns, lane, [&](int q, int l, int e) {
-                    return __dmul_rn(__dsub_rn(at(q, l, e), mean), ycr[q * SBt + l * Et + e]);
+                    const int x = (q * 32 + l) * (Et + 1) + e;
+                    return __dmul_rn(xr[x], yr[x]);
                 });
                 const double den = __dsqrt_rn(__dmul_rn(sxx, syr));
                 const double rr = (den > 0.0) ? __ddiv_rn(fabs(num), den) : 0.0;
-                acc[r] = __dadd_rn(acc[r], __dmul_rn(w, rr));  // numpy: acc += w * r, two roundings
+                acc[r] = __dadd_rn(acc[r], __dmul_rn(w, rr));
             }
         }
         if (lane == 0) {
@@ -211,6 +311,10 @@ __global__ void __launch_bounds__(SIS_WARPS * 32) k_sis_scores(
             }
             double sc = nan ? __longlong_as_double(0x7ff8000000000000ll) : best;
             if (!nan) sc = sc < 0.0 ? 0.0 : (sc > 1.0 ? 1.0 : sc);
+            if (accumulate) {  // clip is monotone: max of clipped group maxima = clip of the max
+                const double o = out[f];
+                sc = (o != o || sc != sc) ? __longlong_as_double(0x7ff8000000000000ll) : (o > sc ? o : sc);
+            }
             out[f] = sc;
         }
         __syncwarp();  // the row buffer is reused by the next feature
@@ -230,17 +334,25 @@ void launch_sis_targets(const double* y, int R, int64_t s, const int64_t* perm, 
 int launch_sis_scores(const double* F, int64_t k, int64_t s, const int64_t* perm, const int* dest,
                       const int64_t* bounds, const int* tE, const int* tpoff, int rowlen, int T, const double* yc,
                       const double* sy, int R, double* out, int nsm, cudaStream_t st) {
-    const size_t smem = (size_t)SIS_WARPS * (size_t)rowlen * sizeof(double) + 2 * (size_t)s * sizeof(int);
-    if (smem > 200 * 1024 || s > 8192) return -1;
-    cudaFuncSetAttribute(k_sis_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sis_scores, SIS_WARPS * 32, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int64_t need = (k + SIS_WARPS - 1) / SIS_WARPS;
-    const unsigned blocks = (unsigned)std::min<int64_t>(need, (int64_t)nsm * per_sm);
-    if (blocks)
-        k_sis_scores<<<blocks, SIS_WARPS * 32, smem, st>>>(F, k, s, perm, dest, bounds, tE, tpoff, rowlen, T, yc, sy,
-                                                          R, out);
+    // shared memory: target rows of a group + one row per warp + the slot map; groups of targets
+    // keep at least 8 warps per SM (one CTA per SM) and run as consecutive launches
+    const size_t budget = 227 * 1024;
+    const size_t rb = (size_t)rowlen * sizeof(double), mb = (size_t)s * sizeof(int);
+    if (s > 8192 || mb + 2 * rb > budget) return -1;
+    const int rows_fit = (int)((budget - mb) / rb);
+    const int G = std::max(1, std::min(R, rows_fit - 8));  // targets per launch
+    const int nw = std::max(1, std::min(16, rows_fit - G));
+    const size_t smem = (size_t)(G + nw) * rb + mb;
+    cudaFuncSetAttribute(k_sis_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
+    const int64_t need = (k + nw - 1) / nw;
+    const unsigned blocks = (unsigned)std::min<int64_t>(need, (int64_t)nsm);
+    if (!blocks) return 0;
+    for (int r0 = 0; r0 < R; r0 += G) {
+        const int g = std::min(G, R - r0);
+        k_sis_scores<<<blocks, nw * 32, smem, st>>>(F, k, s, perm, dest, bounds, tE, tpoff, rowlen, T,
+                                                    yc + (int64_t)r0 * s, sy + (int64_t)r0 * T, g, r0 > 0 ? 1 : 0,
+                                                    out);
+    }
     return 0;
 }
 
