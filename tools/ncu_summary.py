@@ -11,6 +11,8 @@ KEYS = [
     ("gpu__time_duration.sum", "duration"),
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
+    ("dram__bytes.sum.per_second", "DRAM throughput"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak"),
     ("lts__t_sector_hit_rate.pct", "L2 hit rate"),
     ("launch__registers_per_thread", "registers/thread"),
     ("launch__grid_size", "grid"),
