@@ -151,7 +151,11 @@ def _partition(s: int, task_slices):
     if task_slices is None:
         task_slices = [np.arange(s)]
     perm = np.concatenate([np.asarray(sl, dtype=np.intp) for sl in task_slices]).astype(np.int64)
-    if perm.shape[0] != s or not np.array_equal(np.sort(perm), np.arange(s)):
+    if perm.shape[0] != s or (s and (perm.min() < 0 or perm.max() >= s)):
+        raise ValueError("task_slices must partition the sample axis")
+    seen = np.zeros(s, dtype=bool)
+    seen[perm] = True
+    if not seen.all():  # s indices in range, all distinct
         raise ValueError("task_slices must partition the sample axis")
     bounds = np.zeros(len(task_slices) + 1, dtype=np.int64)
     np.cumsum([len(sl) for sl in task_slices], out=bounds[1:])
@@ -164,9 +168,10 @@ def _labels_for(task_slices, task_labels):
     return tuple(str(i) for i in range(len(task_slices)))
 
 
-def _model(tup, expressions, coef, ssr, bounds, s, labels) -> Model:
+def _model(tup, expressions, coef, ssr, bounds, s, labels, sizes=None) -> Model:
     # the same numpy expressions as search.fit_tuple (search.py:162-170)
-    sizes = np.diff(bounds).astype(np.float64)
+    if sizes is None:
+        sizes = np.diff(bounds).astype(np.float64)
     return Model(
         indices=tuple(int(i) for i in tup),
         expressions=tuple(expressions[i] for i in tup) if expressions is not None else None,
@@ -269,11 +274,9 @@ def l0_search(
         stats.device = dst.as_dict()
 
     labels = _labels_for(slices, task_labels)
-    out = []
-    for i in range(len(scores)):
-        tup = unrank_tuple(int(ranks[i]), m, n)
-        out.append(_model(tup, expressions, coef[i], ssr[i], bounds, s, labels))
-    return out
+    sizes = np.diff(bounds).astype(np.float64)
+    return [_model(unrank_tuple(int(ranks[i]), m, n), expressions, coef[i], ssr[i], bounds, s, labels, sizes)
+            for i in range(len(scores))]
 
 
 def fit_tuples(values, property_values, tuples, task_slices=None, precision: str = "fp64",
