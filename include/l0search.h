@@ -120,6 +120,17 @@ int l0s_gram_shard_size(int64_t m, int ntasks, int nshards, int64_t *out_doubles
 int l0s_stage_append(l0s_ctx *ctx, const double *rows, int64_t m_new);
 
 /*
+ * l0s_stage / l0s_stage_append with the feature rows given as m (m_new) host
+ * pointers to s float64 each -- a SelectedSubspace's entry arrays
+ * (screening.py:165-198) copied row by row, never stacked on the host
+ * (values_matrix, screening.py:191-195, costs a host copy of the whole
+ * matrix per call).
+ */
+int l0s_stage_rows(l0s_ctx *ctx, const double *const *rows, int64_t m, int64_t s, const double *y,
+                   const int64_t *perm, const int64_t *bounds, int ntasks, int precision);
+int l0s_stage_append_rows(l0s_ctx *ctx, const double *const *rows, int64_t m_new);
+
+/*
  * Final-rung candidates on the device (generation.iter_final_rung,
  * generation.py:331-393; values: expressions.apply_operator_values,
  * expressions.py:168-192; validity: generation._validity_mask, :107-118).

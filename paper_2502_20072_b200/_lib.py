@@ -29,7 +29,7 @@ EXPORTS = (
     "l0s_search", "l0s_fit_tuples", "l0s_screen_tuples", "l0s_get_gram", "l0s_unrank", "l0s_rank",
     "l0s_count", "l0s_fp64_peak", "l0s_rcp_check", "l0s_gram_shard_size", "l0s_stage_shard",
     "l0s_stage_finish", "l0s_sis_prepare", "l0s_sis_scores", "l0s_set_gram_mode", "l0s_stage_info",
-    "l0s_stage_append", "l0s_gen_pool", "l0s_gen_eval", "l0s_gen_take", "l0s_gen_fetch",
+    "l0s_stage_append", "l0s_stage_rows", "l0s_stage_append_rows", "l0s_gen_pool", "l0s_gen_eval", "l0s_gen_take", "l0s_gen_fetch",
 )
 
 
@@ -90,6 +90,8 @@ def lib():
         L.l0s_stage_shard.argtypes = [vp, vp, i64, i64, vp, vp, vp, i32, i32, i32, i32, i32, vp]
         L.l0s_stage_finish.argtypes = [vp, vp]
         L.l0s_stage_append.argtypes = [vp, vp, i64]
+        L.l0s_stage_rows.argtypes = [vp, vp, i64, i64, vp, vp, vp, i32, i32]
+        L.l0s_stage_append_rows.argtypes = [vp, vp, i64]
         L.l0s_gen_pool.argtypes = [vp, vp, i64, i64, i32]
         L.l0s_gen_eval.argtypes = [vp, i32, vp, vp, i64, vp, dbl, dbl, dbl, dbl, vp, vp]
         L.l0s_gen_take.argtypes = [vp, vp, i64, vp, P(vp)]
@@ -176,6 +178,32 @@ class Engine:
         check(lib().l0s_stage(self.handle, *args, ptr(bounds), bounds.shape[0] - 1, PREC[precision], is_dev),
               "l0s_stage")
         self.m, self.s, self.T = int(m), int(s), bounds.shape[0] - 1
+
+    @staticmethod
+    def _row_pointers(arrays, s: int):
+        rows = [np.ascontiguousarray(a, dtype=np.float64) for a in arrays]
+        for r in rows:
+            if r.ndim != 1 or r.shape[0] != s:
+                raise ValueError(f"every row must hold {s} samples")
+        return rows, (ctypes.c_void_p * len(rows))(*[r.ctypes.data for r in rows])
+
+    def stage_rows(self, arrays, y: np.ndarray, perm: np.ndarray, bounds: np.ndarray, precision: str) -> None:
+        """Stage host feature rows given as separate arrays (no host stacking; l0s_stage_rows)."""
+        bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        perm = np.ascontiguousarray(perm, dtype=np.int64)
+        s = y.shape[0]
+        keep, ptrs = self._row_pointers(arrays, s)
+        self.subspace_cache = None
+        check(lib().l0s_stage_rows(self.handle, ptrs, len(keep), s, ptr(y), ptr(perm), ptr(bounds),
+                                   bounds.shape[0] - 1, PREC[precision]), "l0s_stage_rows")
+        self.m, self.s, self.T = len(keep), int(s), bounds.shape[0] - 1
+
+    def stage_append_rows(self, arrays) -> None:
+        """Append feature rows given as separate host arrays (l0s_stage_append_rows)."""
+        keep, ptrs = self._row_pointers(arrays, self.s)
+        check(lib().l0s_stage_append_rows(self.handle, ptrs, len(keep)), "l0s_stage_append_rows")
+        self.m += len(keep)
 
     def stage_append(self, rows: np.ndarray) -> None:
         """Append feature rows (host, (m_new, s)) to the staged host problem (l0s_stage_append)."""

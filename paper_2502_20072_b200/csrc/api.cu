@@ -493,8 +493,26 @@ static int gram_full(l0s_ctx* c) {
 // chunks (multiples of the Gram's 64-row blocks) on the copy stream while the compute stream
 // gathers and normalizes each chunk as it lands and computes every Gram block whose later
 // block-row it completes.  Only the last chunk's blocks remain after the copy.
+// Host rows [r0, r1) of the input into in_values on stream `st`: one contiguous copy, or one
+// copy per row when the caller passed row pointers (a SelectedSubspace's entries, never stacked).
+static cudaError_t copy_rows(l0s_ctx* c, const double* values, const double* const* rows, int64_t r0, int64_t r1,
+                             int64_t dst_row, cudaStream_t st) {
+    const int64_t s = c->s;
+    double* dst = c->in_values.as<double>() + dst_row * s;
+    if (!rows) return cudaMemcpyAsync(dst, values + r0 * s, sizeof(double) * (r1 - r0) * s, cudaMemcpyHostToDevice, st);
+    for (int64_t r = r0; r < r1;) {
+        int64_t e = r + 1;  // rows adjacent in host memory travel as one copy
+        while (e < r1 && rows[e] == rows[e - 1] + s) ++e;
+        const cudaError_t err =
+            cudaMemcpyAsync(dst + (r - r0) * s, rows[r], sizeof(double) * (e - r) * s, cudaMemcpyHostToDevice, st);
+        if (err != cudaSuccess) return err;
+        r = e;
+    }
+    return cudaSuccess;
+}
+
 static int stage_fill(l0s_ctx* c, const double* values, const double* y, const int64_t* perm, int is_device,
-                      bool gram_cols) {
+                      bool gram_cols, const double* const* rows = nullptr) {
     const int64_t m = c->m, s = c->s;
     const int ntasks = c->T, precision = c->prec;
     const double *vd = values, *yd = y;
@@ -535,7 +553,7 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
     rows_to_z(m, m + 1);  // the property first: every Gram column block needs it
     if (!chunked) {
         if (!is_device)
-            CK(cudaMemcpyAsync(c->in_values.p, values, sizeof(double) * m * s, cudaMemcpyHostToDevice, c->st));
+            CK(copy_rows(c, values, rows, 0, m, 0, c->st));
         rows_to_z(0, m);
         if (gram_cols) return gram_full(c);
         return L0S_OK;
@@ -550,8 +568,7 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
     int k = 0;
     for (int64_t r0 = 0; r0 < m; r0 += R, ++k) {
         const int64_t r1 = std::min(m, r0 + R);
-        CK(cudaMemcpyAsync(c->in_values.as<double>() + r0 * s, values + r0 * s, sizeof(double) * (r1 - r0) * s,
-                           cudaMemcpyHostToDevice, c->cst));
+        CK(copy_rows(c, values, rows, r0, r1, r0, c->cst));
         cudaEventRecord(c->cev[k], c->cst);
     }
     k = 0;
@@ -598,11 +615,35 @@ int l0s_stage(l0s_ctx* c, const double* values, int64_t m, int64_t s, const doub
     return stage_post(c);
 }
 
+int l0s_stage_rows(l0s_ctx* c, const double* const* rows, int64_t m, int64_t s, const double* y, const int64_t* perm,
+                   const int64_t* bounds, int ntasks, int precision) {
+    if (!rows && m > 0) return fail(L0S_EINVAL, "null row pointers");
+    for (int64_t r = 0; r < m; ++r)
+        if (!rows[r]) return fail(L0S_EINVAL, "row %lld: null pointer", (long long)r);
+    int rc = stage_prepare(c, nullptr, m, s, y, perm, bounds, ntasks, precision, 0);
+    if (rc) return rc;
+    rc = stage_fill(c, nullptr, y, perm, 0, true, rows);
+    if (rc) return rc;
+    CK(cudaGetLastError());
+    return stage_post(c);
+}
+
 // Incremental stage across the pipeline's dimensions: the subspace only grows
 // by appending (screening.py:197-198), so only the new rows cross PCIe; the device keeps the
 // previous inputs and restages from them (gather, normalize, Gram and flags are device work:
 // 0.6 ms at C3 against 2.9 ms for the copy of the old rows).
-int l0s_stage_append(l0s_ctx* c, const double* rows, int64_t m_new) {
+static int stage_append(l0s_ctx* c, const double* values, const double* const* rows, int64_t m_new);
+
+int l0s_stage_append(l0s_ctx* c, const double* rows, int64_t m_new) { return stage_append(c, rows, nullptr, m_new); }
+
+int l0s_stage_append_rows(l0s_ctx* c, const double* const* rows, int64_t m_new) {
+    if (!rows && m_new > 0) return fail(L0S_EINVAL, "null row pointers");
+    for (int64_t r = 0; r < m_new; ++r)
+        if (!rows[r]) return fail(L0S_EINVAL, "row %lld: null pointer", (long long)r);
+    return stage_append(c, nullptr, rows, m_new);
+}
+
+static int stage_append(l0s_ctx* c, const double* values, const double* const* rows, int64_t m_new) {
     if (!c) return fail(L0S_EINVAL, "null context");
     if (!c->staged || !c->host_staged || c->shard_pending)
         return fail(L0S_ESTATE, "l0s_stage_append needs a completed stage from host inputs");
@@ -612,8 +653,7 @@ int l0s_stage_append(l0s_ctx* c, const double* rows, int64_t m_new) {
     const int64_t m0 = c->m, s = c->s, m1 = m0 + m_new;
     CK(cudaStreamSynchronize(c->st));
     CK(c->in_values.grow(sizeof(double) * m1 * s, sizeof(double) * m0 * s, c->st));
-    CK(cudaMemcpyAsync(c->in_values.as<double>() + m0 * s, rows, sizeof(double) * m_new * s, cudaMemcpyHostToDevice,
-                       c->st));
+    CK(copy_rows(c, values, rows, 0, m_new, m0, c->st));
     const std::vector<int64_t> bounds = c->bounds_h;
     int rc = stage_prepare(c, c->in_values.as<double>(), m1, s, c->in_y.as<double>(), c->in_perm.as<int64_t>(),
                            bounds.data(), c->T, c->prec, 1);

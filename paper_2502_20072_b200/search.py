@@ -125,9 +125,10 @@ def _stage_subspace(eng, subspace, y, perm, bounds, precision: str):
     The pipeline's subspace only grows by appending entries between dimensions
     (screening.py:197-198, pipeline.py:181-240): when the first entries are the very
     objects staged last time (same value arrays, same y / partition / precision), only the
-    new rows are sent (l0s_stage_append) -- the reference re-stacks and re-prepares the
-    whole matrix every dimension (search.py:113-127).  Entry value arrays are taken as
-    immutable records, as the pipeline treats them.
+    new rows are sent (l0s_stage_append_rows) -- the reference re-stacks and re-prepares the
+    whole matrix every dimension (search.py:113-127).  Rows go to the device one entry at a
+    time, never stacked on the host.  Entry value arrays are taken as immutable records, as
+    the pipeline treats them.
     """
     entries = subspace.entries
     c = eng.subspace_cache
@@ -138,10 +139,11 @@ def _stage_subspace(eng, subspace, y, perm, bounds, precision: str):
                 and np.array_equal(pperm, perm) and np.array_equal(pb, bounds)
                 and all(e is a and e.values is v for e, a, v in zip(entries, pe, pv))):
             if len(entries) > m0:
-                eng.stage_append(np.stack([e.values for e in entries[m0:]]))
+                eng.stage_append_rows([e.values for e in entries[m0:]])
             eng.subspace_cache = (list(entries), [e.values for e in entries], py, pperm, pb, pprec)
             return
-    eng.stage(subspace.values_matrix(), y, perm, bounds, precision)
+    # rows straight from the entries (values_matrix would stack a host copy first)
+    eng.stage_rows([e.values for e in entries], y, perm, bounds, precision)
     eng.subspace_cache = (list(entries), [e.values for e in entries], np.array(y, copy=True), perm.copy(),
                           bounds.copy(), precision)
 

@@ -351,8 +351,8 @@ def test_incremental_stage_across_dimensions(monkeypatch, shape):
     sub0 = _Subspace(entries[:m0])
     sub1 = sub0.extended(entries[m0:])
     calls = []
-    orig = _lib.Engine.stage_append
-    monkeypatch.setattr(_lib.Engine, "stage_append", lambda self, rows: (calls.append(rows.shape), orig(self, rows)))
+    orig = _lib.Engine.stage_append_rows
+    monkeypatch.setattr(_lib.Engine, "stage_append_rows", lambda self, rows: (calls.append((len(rows), len(rows[0]))), orig(self, rows)))
     for n in (1, 2):
         l0_search(sub0, y, slices, L0Config(dimension=n))
     assert calls == []
@@ -375,6 +375,34 @@ def test_incremental_stage_across_dimensions(monkeypatch, shape):
     want3 = l0_search(np.stack([e.values for e in sub1.entries]), y2, slices, L0Config(dimension=2))
     assert [md.indices for md in got2] == [md.indices for md in want3]
     assert bits_equal([md.score for md in got2], [md.score for md in want3])
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_stage_append_and_rows_equal_full_stage(precision):
+    """l0s_stage_append (one block) and l0s_stage_rows (row pointers) stage exactly what
+    l0s_stage of the concatenated matrix stages: same Gram, same search."""
+    from paper_2502_20072_b200 import _lib
+    from paper_2502_20072_b200.search import _partition
+
+    rng = np.random.default_rng(21)
+    m0, m1, s, T = 40, 23, 700, 3
+    v = rng.uniform(0.5, 2.0, size=(m0 + m1, s))
+    y = v[2] - 0.5 * v[m0 + 3] + 0.01 * rng.standard_normal(s)
+    perm, bounds, _ = _partition(s, [np.arange(t, s, T) for t in range(T)])
+    eng = _lib.engine(0)
+    eng.stage(v, y, perm, bounds, precision)
+    want = eng.search(3, 10, 0, 2**63 - 1, "exact")
+    g_want = [eng.gram(t) for t in range(T)]
+    eng.stage(v[:m0], y, perm, bounds, precision)
+    eng.stage_append(v[m0:])
+    got = eng.search(3, 10, 0, 2**63 - 1, "exact")
+    assert all(bits_equal(eng.gram(t), g) for t, g in enumerate(g_want))
+    eng.stage_rows(list(v), y, perm, bounds, precision)
+    got2 = eng.search(3, 10, 0, 2**63 - 1, "exact")
+    assert all(bits_equal(eng.gram(t), g) for t, g in enumerate(g_want))
+    for g in (got, got2):
+        for a, b in zip(g[:4], want[:4]):
+            assert bits_equal(a, b)
 
 
 @pytest.mark.parametrize("W", [2, 3, 8])
