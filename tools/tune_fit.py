@@ -33,7 +33,6 @@ def build_all():
     for name, defs in VARIANTS.items():
         out = os.path.join(VDIR, f"lib_{name}.so")
         b.build(force=True, defines=defs, out=out)
-        log = open(os.path.join(os.path.dirname(b.OBJ), "_obj_" + str(abs(hash(defs)) % 10**8), "ptxas.log")).read()
         print(name, out)
 
 
