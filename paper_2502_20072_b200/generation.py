@@ -81,18 +81,60 @@ def _key(op, ka: str, kb: str | None) -> str:
 
 
 class PendingExpr:
-    """A kept candidate of the device stream: its canonical key now, the expression node
-    (expressions.apply) when ``build()`` is called -- sis_select builds only the ones it keeps."""
+    """A kept candidate of the device stream: the canonical key on first access, the
+    expression node (expressions.apply) when ``build()`` is called -- sis_select builds only
+    the ones it keeps."""
 
-    __slots__ = ("op", "a", "b", "key")
+    __slots__ = ("op", "a", "b", "_key")
 
-    def __init__(self, op, a, b, key):
-        self.op, self.a, self.b, self.key = op, a, b, key
+    def __init__(self, op, a, b, key=None):
+        self.op, self.a, self.b, self._key = op, a, b, key
+
+    @property
+    def key(self) -> str:
+        if self._key is None:
+            self._key = _key(self.op, self.a.key, None if self.b is None else self.b.key)
+        return self._key
 
     def build(self):
         from descsearch.expressions import apply
 
         return apply(self.op, self.a) if self.b is None else apply(self.op, self.a, self.b)
+
+
+class PendingExprs:
+    """The kept candidates of one device pass as index arrays; items (``PendingExpr``) are
+    made on access.  ``not_taken(entries)`` masks out candidates that are the expressions of
+    already-selected entries without building any key (sis_select's ``taken`` test)."""
+
+    def __init__(self, op, pi, pj, feats, index_of):
+        self.op, self.pi, self.pj, self._feats, self._index_of = op, pi, pj, feats, index_of
+
+    def __len__(self):
+        return len(self.pi)
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self[x] for x in range(*k.indices(len(self)))]
+        i, j = int(self.pi[k]), int(self.pj[k])
+        return PendingExpr(self.op, self._feats[i], None if j < 0 else self._feats[j])
+
+    def __iter__(self):
+        return (self[k] for k in range(len(self)))
+
+    def not_taken(self, entries) -> np.ndarray:
+        n = len(self._feats)
+        codes = []
+        for e in entries:
+            ex = e.expression
+            if ex.op is None or ex.op.kind != self.op.kind:
+                continue
+            ch = [self._index_of.get(c.key) for c in ex.children]
+            if any(c is None for c in ch):
+                continue
+            codes.append(ch[0] * (n + 1) + (ch[1] + 1 if len(ch) > 1 else 0))
+        mine = self.pi.astype(np.int64) * (n + 1) + (self.pj.astype(np.int64) + 1)
+        return ~np.isin(mine, np.asarray(codes, dtype=np.int64)) if codes else np.ones(len(self), dtype=bool)
 
 
 def pair_arrays(op, pool, target_rung: int):
@@ -168,7 +210,17 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
     fps = pool_fingerprints(eng, pool)
     feats = pool.features
     fkeys = [f.key for f in feats]
+    index_of = {k: x for x, k in enumerate(fkeys)}
     vals = pool.values
+    # A final-rung key is op(child keys): its nesting depth is its rung, so it never equals a
+    # pool key (rungs < max), and it is unique per (operator, pair).  With distinct operator
+    # kinds the key test can therefore never fire: keys are then built only on demand.
+    kinds = [op.kind for op in config.operators]
+    keys_free = len(set(kinds)) == len(kinds) and (len(pool) == 0 or pool.max_rung() < target_rung)
+    # fingerprints: the first 64 bits index the set, the full 128 bits decide
+    fp64 = {}
+    for fp in fps:
+        fp64.setdefault(int.from_bytes(fp[:8], "little"), []).append(fp)
     tol = config.dedup_tolerance
     limits = dict(tol=tol, min_abs=config.min_abs_value, max_abs=config.max_abs_value, dedup_tol=tol)
     batch = max(1, config.value_batch_size)
@@ -193,32 +245,38 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
                     valid, h = eng.gen_eval(GEN_VALUES, values=host, **limits)
                 else:
                     valid, h = eng.gen_eval(kind, pi=pi, pj=pj, **limits)
-                exprs, kept = [], []
+                kept = []
                 rows_ok = np.flatnonzero(valid)
                 stats.n_invalid += len(pi) - len(rows_ok)
+                h64 = np.frombuffer(h, dtype="<u8")[0::2][rows_ok].tolist()
+                hv = np.frombuffer(h, dtype="V16")[rows_ok].tolist() if len(rows_ok) else []
                 li, lj = pi[rows_ok].tolist(), pj[rows_ok].tolist()
-                for row, i, j in zip(rows_ok.tolist(), li, lj):  # the reference's ordered walk (generation.py:364-385)
-                    if j < 0:
-                        j = None
-                    key = _key(op, fkeys[i], None if j is None else fkeys[j])
-                    if key in keys:
-                        stats.n_dup_key += 1
-                        continue
-                    fp = h[16 * row:16 * row + 16]
-                    if fp in fps:
+                # the reference's ordered walk (generation.py:364-385): invalid, key, fingerprint
+                for x, row in enumerate(rows_ok.tolist()):
+                    key = None
+                    if not keys_free:
+                        i, j = li[x], lj[x]
+                        key = _key(op, fkeys[i], None if j < 0 else fkeys[j])
+                        if key in keys:
+                            stats.n_dup_key += 1
+                            continue
+                    fp, f = hv[x], h64[x]
+                    same = fp64.get(f)
+                    if same is not None and fp in same:
                         stats.n_dup_value += 1
                         continue
-                    keys.add(key)
-                    fps.add(fp)
-                    if on_device:
-                        exprs.append(PendingExpr(op, feats[i], None if j is None else feats[j], key))
+                    if key is not None:
+                        keys.add(key)
+                    if same is None:
+                        fp64[f] = [fp]
                     else:
-                        exprs.append(apply(op, feats[i]) if j is None else apply(op, feats[i], feats[j]))
+                        same.append(fp)
                     kept.append(row)
-                    stats.n_kept += 1
-                if not exprs:
+                stats.n_kept += len(kept)
+                if not kept:
                     continue
                 if on_device:
+                    exprs = PendingExprs(op, pi[kept], pj[kept], feats, index_of)
                     _, ptr = eng.gen_take(kept)
                     spent += time.perf_counter() - t0
                     if timer is not None:
@@ -228,7 +286,8 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
                     t0 = time.perf_counter()
                 else:
                     rows, _ = eng.gen_take(kept, host=True)
-                    out_exprs.extend(exprs)
+                    out_exprs.extend(apply(op, feats[i]) if j < 0 else apply(op, feats[i], feats[j])
+                                     for i, j in zip(pi[kept].tolist(), pj[kept].tolist()))
                     out_rows.append(rows)
             spent += time.perf_counter() - t0
             if out_exprs:
@@ -240,4 +299,4 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
         timer.add(spent)
 
 
-__all__ = ["DeviceChunk", "PendingExpr", "iter_final_rung", "pair_arrays", "pool_fingerprints", "DEVICE_KINDS"]
+__all__ = ["DeviceChunk", "PendingExpr", "PendingExprs", "iter_final_rung", "pair_arrays", "pool_fingerprints", "DEVICE_KINDS"]

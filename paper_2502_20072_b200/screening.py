@@ -87,7 +87,7 @@ def sis_select(source, target, n_sis_select: int, already_selected=None, workers
     from descsearch.generation import FeatureSpace
     from descsearch.screening import EmptySpace, SelectedSubspace, SubspaceEntry
 
-    from .generation import DeviceChunk, PendingExpr
+    from .generation import DeviceChunk, PendingExpr, PendingExprs
 
     if n_sis_select < 1:
         raise ValueError("n_sis_select must be positive")
@@ -99,10 +99,14 @@ def sis_select(source, target, n_sis_select: int, already_selected=None, workers
     for exprs, matrix in chunks:
         on_dev = isinstance(matrix, DeviceChunk)
         scores = np.asarray(matrix.sis_scores(target) if on_dev else chunk_scores(matrix, target))
-        n_new_seen += len(exprs) - (sum(1 for e in exprs if e.key in taken) if taken else 0)
+        if isinstance(exprs, PendingExprs):  # device stream: the taken test on index pairs
+            new = exprs.not_taken(prior.entries) if taken else np.ones(len(exprs), dtype=bool)
+        else:
+            new = np.fromiter((e.key not in taken for e in exprs), dtype=bool, count=len(exprs))
+        n_new_seen += int(new.sum())
         # only a score at or above the current n-th can enter the list (ties go by key)
-        idx = np.flatnonzero(scores >= -best[-1][0]) if len(best) >= n_sis_select else range(len(exprs))
-        cand = [[-float(scores[i]), exprs[i].key, exprs[i], None, i] for i in idx if exprs[i].key not in taken]
+        ok = new & (scores >= -best[-1][0]) if len(best) >= n_sis_select else new
+        cand = [[-float(scores[i]), exprs[i].key, exprs[i], None, i] for i in np.flatnonzero(ok).tolist()]
         if not cand:
             continue
         best = sorted(best + cand, key=lambda item: (item[0], item[1]))[:n_sis_select]

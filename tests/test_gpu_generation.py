@@ -143,3 +143,27 @@ def test_streamed_pipeline_model_files(tmp_path, name, dim, n_sis):
     assert [render(e.expression) for e in res.subspace.entries] == g["subspace"].tolist()
     for d in range(1, dim + 1):
         assert (tmp_path / f"models_dim{d}.txt").read_bytes() == g[f"d{d}_models_file"].tobytes()
+
+
+def test_iter_final_rung_repeated_operator_matches_live_reference():
+    """A repeated operator kind makes the key test fire (every candidate of the second copy is
+    a key duplicate): the general walk, against the reference run live."""
+    _reference()
+    from descsearch.expressions import get_operator, render
+    from descsearch.generation import RungStats
+    from descsearch.generation import iter_final_rung as ref_iter
+
+    from paper_2502_20072_b200.generation import iter_final_rung
+
+    _, pool, gcfg = _pool("stream_fp32")
+    gcfg.operators = [get_operator(o) for o in ["add", "div", "add", "sqrt"]]
+    out = []
+    for fn in (ref_iter, iter_final_rung):
+        st = RungStats(rung=gcfg.max_rung)
+        ex, h = [], hashlib.blake2b(digest_size=16)
+        for e, mat in fn(pool, gcfg, 1, None, st):
+            ex.extend(render(x) for x in e)
+            h.update(np.ascontiguousarray(mat).tobytes())
+        out.append((ex, h.digest(), [st.n_pairs, st.n_invalid, st.n_dup_key, st.n_dup_value, st.n_kept]))
+    assert out[0][2][2] > 0  # the key test fired
+    assert out[1] == out[0]
