@@ -54,3 +54,37 @@ def test_pair_arrays_equal_generate_pairs(seed):
             pi, pj = pair_arrays(op, pool, rung)
             got = [(i, None if j < 0 else j) for i, j in zip(pi.tolist(), pj.tolist())]
             assert got == want, (name, rung)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_keys_and_pending_records_match_apply(seed):
+    """The device stream's canonical keys (generation._key) are expressions.apply's, and the
+    index-pair records rebuild the same nodes; their taken test agrees with the key test."""
+    _reference()
+    from descsearch.expressions import apply, get_operator
+    from descsearch.screening import SelectedSubspace, SubspaceEntry
+    from descsearch.units import Unit
+
+    from paper_2502_20072_b200.generation import PendingExprs, _key, pair_arrays
+
+    units = [Unit.of(m=1), Unit.of(m=1), Unit.of(s=1), Unit(), Unit.of(m=1, s=-1), Unit()]
+    pool = _pool(units, ["add", "sub", "mul", "div", "sqrt", "inv"], seed)
+    feats = pool.features
+    index_of = {f.key: i for i, f in enumerate(feats)}
+    for name in ["add", "sub", "mul", "div", "abs_diff", "sqrt", "inv", "exp"]:
+        op = get_operator(name)
+        pi, pj = pair_arrays(op, pool, 2)
+        if len(pi) == 0:
+            continue
+        rec = PendingExprs(op, pi, pj, feats, index_of)
+        nodes = [apply(op, feats[i]) if j < 0 else apply(op, feats[i], feats[j])
+                 for i, j in zip(pi.tolist(), pj.tolist())]
+        for k in range(0, len(nodes), max(1, len(nodes) // 50)):
+            i, j = int(pi[k]), int(pj[k])
+            assert _key(op, feats[i].key, None if j < 0 else feats[j].key) == nodes[k].key
+            assert rec[k].key == nodes[k].key and rec[k].build().key == nodes[k].key
+        chosen = nodes[:: max(1, len(nodes) // 7)]
+        prior = SelectedSubspace([SubspaceEntry(e, 0.5, np.zeros(3)) for e in chosen + feats[:3]])
+        taken = prior.keys()
+        want = np.array([n.key not in taken for n in nodes])
+        assert np.array_equal(rec.not_taken(prior.entries), want)
