@@ -588,9 +588,9 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
                              B0, B1, c->st);
         }
         if (ozaki) {
-            // a tile (fb, gb) of column block gb needs rows < gb*64 + 128: ready once they landed
+            // a column block is complete once every row its tiles cover has landed (ozaki_blocks_ready)
             const int ncb = ozaki_col_blocks(c->mp);
-            const int upto = r1 >= m ? ncb : std::max(oz_done, (int)(r1 / 64) - 1);
+            const int upto = r1 >= m ? ncb : std::max(oz_done, std::min(ncb, ozaki_blocks_ready(r1)));
             if (launch_ozaki_tiles(ntasks, c->mp, c->rpad_h.data(), c->oz_q.as<int8_t>(), c->oz_ex.as<int>(),
                                    c->oz_koff.as<int64_t>(), c->G.as<double>(), oz_done, upto, c->st))
                 return fail(L0S_ECUDA, "INT8 Gram: TMA descriptor");

@@ -62,6 +62,7 @@ int launch_ozaki_gram(const double* Z, int64_t sp, const int64_t* zoff_d, const 
 // pieces of the same, for the overlapped stage: tiles of the column blocks [gb0, gb1) (64 wide)
 // and the error-bound kernel (after all tiles)
 int ozaki_col_blocks(int64_t mp);
+int ozaki_blocks_ready(int64_t r1);  // column blocks complete once rows < r1 have landed
 int launch_ozaki_tiles(int T, int64_t mp, const int64_t* rpad_h, const int8_t* Q, const int* ex,
                        const int64_t* koff_d, double* G, int gb0, int gb1, cudaStream_t st);
 void launch_ozaki_eta(int T, int64_t m, int64_t mp, const int* ex, const double* rows_d, const double* G, double* eta_d,

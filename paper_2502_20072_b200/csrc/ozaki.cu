@@ -32,14 +32,20 @@ namespace {
 constexpr int OZ_S = OZ_DIGITS;     // digits per value (kernels.h: the normalize kernel writes them)
 constexpr int OZ_NG = OZ_S;         // digit-weight groups d = 2 .. S + 1
 constexpr int OZ_BM = 128;          // tile rows (TMEM lanes)
-constexpr int OZ_BN = 64;           // tile cols: 4 groups x 64 = 256 TMEM columns -> 2 CTAs per SM
+#ifndef L0S_OZ_BN
+#define L0S_OZ_BN 128
+#endif
+// tile cols: 4 groups x 128 = all 512 TMEM columns (one CTA per SM, N = 128 MMAs run at the
+// full rate); 64 gives two CTAs per SM with half-width MMAs
+constexpr int OZ_BN = L0S_OZ_BN;
 constexpr int OZ_KC = 64;           // K bytes per stage
-constexpr int OZ_ST = 2;            // stages (per CTA; two CTAs per SM overlap)
+constexpr int OZ_ST = OZ_BN >= 128 ? 3 : 2;  // stages per CTA
+constexpr int OZ_CTAS = OZ_BN >= 128 ? 1 : 2;  // CTAs per SM (TMEM)
 constexpr int OZ_TA = OZ_BM * OZ_KC;                // 8 KB: one digit plane of A
 constexpr int OZ_TB = OZ_BN * OZ_KC;                // 4 KB: one digit plane of B
 constexpr int OZ_STAGE = OZ_S * (OZ_TA + OZ_TB);    // 48 KB
 constexpr int OZ_SMEM = OZ_ST * OZ_STAGE + 1024;    // + alignment slack
-constexpr int OZ_TMEM_COLS = OZ_NG * OZ_BN;         // 256
+constexpr int OZ_TMEM_COLS = OZ_NG * OZ_BN;         // 512 (256 for 64-wide tiles)
 constexpr double OZ_C = 1.9e-8;     // error constant per unit-scaled entry and sample (S = 4)
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -120,7 +126,10 @@ __global__ void k_oz_split(const double* __restrict__ Z, int64_t sp, const int64
 // lies in exactly one such tile) of one task per CTA ----
 // Tiles are numbered column by column (gb outer, fb = 0 .. gb/2 inner) from tile g0, so a range
 // of column blocks -- the part of the Gram a landed row chunk completes -- is one launch.
-__global__ void __launch_bounds__(192, 2) k_oz_gemm(const __grid_constant__ TmaDesc tmA,
+// tiles of column block gb: row blocks fb with fb * BM <= the block's last column
+__host__ __device__ constexpr int oz_tiles_in_block(int gb) { return ((gb + 1) * OZ_BN - 1) / OZ_BM + 1; }
+
+__global__ void __launch_bounds__(192, OZ_CTAS) k_oz_gemm(const __grid_constant__ TmaDesc tmA,
                                                    const __grid_constant__ TmaDesc tmB, const int64_t* __restrict__ koff,
                                                    const int* __restrict__ ex, int64_t R, int nbc, int64_t mp,
                                                    double* __restrict__ Gall, int g0) {
@@ -131,8 +140,8 @@ __global__ void __launch_bounds__(192, 2) k_oz_gemm(const __grid_constant__ TmaD
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int t = blockIdx.y;
     int lin = g0 + blockIdx.x, gb = 0;
-    while (lin >= gb / 2 + 1) {
-        lin -= gb / 2 + 1;
+    while (lin >= oz_tiles_in_block(gb)) {
+        lin -= oz_tiles_in_block(gb);
         ++gb;
     }
     const int fb = lin;
@@ -302,8 +311,15 @@ void ozaki_prepare_digits(int64_t m, int64_t mp, int T, const int64_t* rpad_h, i
 
 static int oz_tiles_before(int gb) {  // tiles in column blocks [0, gb)
     int n = 0;
-    for (int g = 0; g < gb; ++g) n += g / 2 + 1;
+    for (int g = 0; g < gb; ++g) n += oz_tiles_in_block(g);
     return n;
+}
+
+// column blocks [0, upto) whose tiles only need rows < r1 (a landed row chunk completes them)
+int ozaki_blocks_ready(int64_t r1) {
+    int gb = 0;
+    while ((int64_t)oz_tiles_in_block(gb) * OZ_BM <= r1) ++gb;
+    return gb;
 }
 
 int ozaki_col_blocks(int64_t mp) { return (int)((mp + OZ_BM - 1) / OZ_BM * OZ_BM / OZ_BN); }
