@@ -673,3 +673,39 @@ def test_exact_large_systems_global_path(oracle, rng, precision):
         okr, coef_r, ssr_r = oracle.fit_tuple_kernel(vals, yy, bounds, tup[k], tol)
         assert bool(okr) == bool(ok[k])
         assert bits_equal(coef[k], coef_r) and bits_equal(ssr[k], ssr_r)
+
+
+@pytest.mark.parametrize("n", [3, 4])
+@pytest.mark.parametrize("planted_pair", [False, True])
+def test_qr_screen_ill_tuples_match_oracle(oracle, n, planted_pair):
+    """C4-style ill conditioning in miniature: near-copies spanning the 1e-10 rank rule, near-
+    constants colliding with the intercept and an exact duplicate.  The Gram screen routes
+    their tuples to the QR screen; with planted_pair the best model itself holds a resolvable
+    near-copy pair, so QR survivors go through the bit-exact refit.  Same models as the
+    exhaustive oracle."""
+    from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
+
+    rng = np.random.default_rng(40 + n)
+    m, s, T = 44, 240, 2
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    for c, d in enumerate([1e-4, 1e-6, 1e-8, 1e-9, 1e-11, 1e-13]):
+        v[30 + c] = v[c] + d * rng.standard_normal(s)
+    for c, d in enumerate([1e-5, 1e-12]):
+        v[38 + c] = 1.0 + c + d * rng.standard_normal(s)
+    v[41] = v[10]
+    slices = [np.arange(t, s, T) for t in range(T)]
+    if planted_pair:  # y lives on (x1, x31 = x1 + 1e-6 noise) and others
+        y = 1e6 * (v[31] - v[1]) + 0.7 * v[12] + (0.4 * v[20] if n == 4 else 0.0) + 0.01 * rng.standard_normal(s)
+    else:
+        y = 1.3 * v[12] - 0.6 * v[20] + (0.5 * v[25] if n == 4 else 0.0) + 0.01 * rng.standard_normal(s)
+    want = oracle.l0_search(v, y, slices, n, 10, "fp64", threads=os.cpu_count() or 1)
+    st = SearchStats()
+    got = l0_search(v, y, slices, L0Config(dimension=n), mode="fast", stats=st)
+    d = st.device
+    assert d["certified"] == 1 and d["n_ill"] > 0
+    if planted_pair:
+        assert got[0].indices[:1] == (1,) and 31 in got[0].indices
+    assert [md.indices for md in got] == [w["indices"] for w in want]
+    assert bits_equal([md.score for md in got], [w["score"] for w in want])
+    for md, w in zip(got, want):
+        assert bits_equal(md.coefficients, w["coefficients"])
