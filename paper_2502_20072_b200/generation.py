@@ -31,6 +31,7 @@ import time
 import numpy as np
 
 from . import _lib
+from .screening import _lock  # one context per device is shared with the SIS scores (threads)
 
 DEVICE_KINDS = {"add": 1, "sub": 2, "mul": 3, "div": 4, "abs_diff": 5, "sqrt": 6, "sq": 7, "cb": 8, "inv": 9,
                 "abs": 10}
@@ -60,7 +61,8 @@ class DeviceChunk:
         return device_chunk_scores(self._eng, self._ptr, self.shape[0], target)
 
     def rows(self, idx) -> np.ndarray:
-        return self._eng.gen_fetch(np.asarray(idx, dtype=np.int32))
+        with _lock:
+            return self._eng.gen_fetch(np.asarray(idx, dtype=np.int32))
 
     def __getitem__(self, i):
         return self.rows([int(i)])[0]
@@ -187,8 +189,9 @@ def pool_fingerprints(eng, pool) -> set:
     n = len(pool)
     if n == 0:
         return set()
-    _, h = eng.gen_eval(GEN_COPY, pi=np.arange(n, dtype=np.int32), tol=pool.dedup_tolerance, min_abs=0.0,
-                        max_abs=np.inf, dedup_tol=0.0)
+    with _lock:
+        _, h = eng.gen_eval(GEN_COPY, pi=np.arange(n, dtype=np.int32), tol=pool.dedup_tolerance, min_abs=0.0,
+                            max_abs=np.inf, dedup_tol=0.0)
     return {h[16 * r:16 * r + 16] for r in range(n)}
 
 
@@ -206,7 +209,8 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
     t0 = time.perf_counter()
     keys = set(pool.dedup_state()[0])
     eng = _lib.engine(device)
-    eng.gen_pool(pool.values_matrix())
+    with _lock:
+        eng.gen_pool(pool.values_matrix())
     fps = pool_fingerprints(eng, pool)
     feats = pool.features
     fkeys = [f.key for f in feats]
@@ -242,9 +246,11 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
                     host = np.stack([apply_operator_values(op.kind, vals[i]) if j < 0
                                      else apply_operator_values(op.kind, vals[i], vals[j])
                                      for i, j in zip(pi.tolist(), pj.tolist())])
-                    valid, h = eng.gen_eval(GEN_VALUES, values=host, **limits)
+                    with _lock:
+                        valid, h = eng.gen_eval(GEN_VALUES, values=host, **limits)
                 else:
-                    valid, h = eng.gen_eval(kind, pi=pi, pj=pj, **limits)
+                    with _lock:
+                        valid, h = eng.gen_eval(kind, pi=pi, pj=pj, **limits)
                 kept = []
                 rows_ok = np.flatnonzero(valid)
                 stats.n_invalid += len(pi) - len(rows_ok)
@@ -277,7 +283,8 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
                     continue
                 if on_device:
                     exprs = PendingExprs(op, pi[kept], pj[kept], feats, index_of)
-                    _, ptr = eng.gen_take(kept)
+                    with _lock:
+                        _, ptr = eng.gen_take(kept)
                     spent += time.perf_counter() - t0
                     if timer is not None:
                         timer.add(spent)
@@ -285,7 +292,8 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
                     yield exprs, DeviceChunk(eng, ptr, len(kept), eng.gen_s, eng.gen_dtype)
                     t0 = time.perf_counter()
                 else:
-                    rows, _ = eng.gen_take(kept, host=True)
+                    with _lock:
+                        rows, _ = eng.gen_take(kept, host=True)
                     out_exprs.extend(apply(op, feats[i]) if j < 0 else apply(op, feats[i], feats[j])
                                      for i, j in zip(pi[kept].tolist(), pj[kept].tolist()))
                     out_rows.append(rows)
