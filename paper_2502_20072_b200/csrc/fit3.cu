@@ -167,6 +167,17 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
             }
     }
     __syncthreads();
+    // unit-independent per-task scalars of the hoist, in slot order, once per CTA (shared
+    // memory instead of a global load chain per unit)
+    __shared__ double s_ts[4][NT];  // Y2, gamma, eta, |y|
+    if (tid < NT) {
+        const int tk = s_tord[tid];
+        s_ts[0][tid] = a.G[(int64_t)tk * mp * mp + m * mp + m];
+        s_ts[1][tid] = ref_gamma(a.rowsd[tk], 3, a.ref_fp32);
+        s_ts[2][tid] = a.eta[tk];
+        s_ts[3][tid] = a.ynorm[tk];
+    }
+    __syncthreads();
     const int* tord = s_tord;  // read where the hoist / tile loads need it (rare)
     unsigned parity[2] = {0u, 0u}, hpar = 0u;
     // The unit's hoist block goes through TMA into tile buffer 1 (idle until the sweep's first
@@ -268,10 +279,10 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
             const int tk = tord[t];
             Gs[t] = a.G + (int64_t)tk * mp * mp;
             w0[t] = Gs[t][m * mp + j];
-            Y2v[t] = Gs[t][m * mp + m];
-            gamv[t] = ref_gamma(a.rowsd[tk], 3, a.ref_fp32);
-            etav[t] = a.eta[tk];
-            ynv[t] = a.ynorm[tk];
+            Y2v[t] = s_ts[0][t];
+            gamv[t] = s_ts[1][t];
+            etav[t] = s_ts[2][t];
+            ynv[t] = s_ts[3][t];
             rjv[t] = fmax(a.rho_cap[tk], a.rho[(int64_t)tk * m + jj]);
         }
 #pragma unroll
