@@ -120,6 +120,20 @@ int l0s_gram_shard_size(int64_t m, int ntasks, int nshards, int64_t *out_doubles
 int l0s_stage_append(l0s_ctx *ctx, const double *rows, int64_t m_new);
 
 /*
+ * One of nparts disjoint parts of the whole search (multi-GPU: part = rank).
+ * The screened path takes every nparts-th unit of its (longest-first) unit
+ * table, so ill-conditioned tuples that cluster in one rank range (C4) spread
+ * over all parts; otherwise part p is the contiguous rank range
+ * [p N / nparts, (p+1) N / nparts) (search.py:266-271).  Every part returns
+ * its own exact top list; the (score, rank) merge of all parts is the whole
+ * search's (search.py:303).  The path is chosen on the whole problem, so all
+ * parts agree.
+ */
+int l0s_search_part(l0s_ctx *ctx, int n, int64_t keep, int part, int nparts, int mode,
+                    double *out_scores, int64_t *out_ranks, double *out_coef, double *out_ssr,
+                    int64_t *out_count, l0s_stats *stats);
+
+/*
  * l0s_stage / l0s_stage_append with the feature rows given as m (m_new) host
  * pointers to s float64 each -- a SelectedSubspace's entry arrays
  * (screening.py:165-198) copied row by row, never stacked on the host

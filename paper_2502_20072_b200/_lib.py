@@ -29,7 +29,7 @@ EXPORTS = (
     "l0s_search", "l0s_fit_tuples", "l0s_screen_tuples", "l0s_get_gram", "l0s_unrank", "l0s_rank",
     "l0s_count", "l0s_fp64_peak", "l0s_rcp_check", "l0s_gram_shard_size", "l0s_stage_shard",
     "l0s_stage_finish", "l0s_sis_prepare", "l0s_sis_scores", "l0s_set_gram_mode", "l0s_stage_info",
-    "l0s_stage_append", "l0s_stage_rows", "l0s_stage_append_rows", "l0s_gen_pool", "l0s_gen_eval", "l0s_gen_take", "l0s_gen_fetch",
+    "l0s_stage_append", "l0s_search_part", "l0s_stage_rows", "l0s_stage_append_rows", "l0s_gen_pool", "l0s_gen_eval", "l0s_gen_take", "l0s_gen_fetch",
 )
 
 
@@ -101,6 +101,7 @@ def lib():
         L.l0s_sis_prepare.argtypes = [vp, vp, i32, i64, vp, vp, i32]
         L.l0s_sis_scores.argtypes = [vp, vp, i64, i32, vp]
         L.l0s_search.argtypes = [vp, i32, i64, i64, i64, i32, vp, vp, vp, vp, P(i64), P(Stats)]
+        L.l0s_search_part.argtypes = [vp, i32, i64, i32, i32, i32, vp, vp, vp, vp, P(i64), P(Stats)]
         L.l0s_fit_tuples.argtypes = [vp, i32, vp, i64, vp, vp, vp, vp]
         L.l0s_screen_tuples.argtypes = [vp, i32, vp, i64, vp, vp]
         L.l0s_get_gram.argtypes = [vp, i32, vp]
@@ -319,6 +320,20 @@ class Engine:
         st = Stats()
         check(lib().l0s_search(self.handle, n, keep, int(rank_begin), int(rank_end), MODES[mode], ptr(scores),
                                ptr(ranks), ptr(coef), ptr(ssr), ctypes.byref(cnt), ctypes.byref(st)), "l0s_search")
+        k = cnt.value
+        return scores[:k], ranks[:k], coef[:k], ssr[:k], st
+
+    def search_part(self, n: int, keep: int, part: int, nparts: int, mode: str = "auto"):
+        """Part `part` of `nparts` disjoint parts of the whole search (l0s_search_part)."""
+        keep = int(keep)
+        scores = np.zeros(keep, dtype=np.float64)
+        ranks = np.zeros(keep, dtype=np.int64)
+        coef = np.zeros((keep, self.T, n + 1), dtype=np.float64)
+        ssr = np.zeros((keep, self.T), dtype=np.float64)
+        cnt = ctypes.c_int64(0)
+        st = Stats()
+        check(lib().l0s_search_part(self.handle, n, keep, int(part), int(nparts), MODES[mode], ptr(scores), ptr(ranks),
+                                    ptr(coef), ptr(ssr), ctypes.byref(cnt), ctypes.byref(st)), "l0s_search_part")
         k = cnt.value
         return scores[:k], ranks[:k], coef[:k], ssr[:k], st
 

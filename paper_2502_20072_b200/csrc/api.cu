@@ -146,7 +146,8 @@ struct l0s_ctx {
     int64_t sis_s = 0;
     std::unordered_map<int64_t, Rec> recs;  // records of this search's refit candidates
     std::vector<int4> units_h;
-    int64_t units_key[5] = {-1, -1, -1, -1, -1};
+    int64_t units_key[7] = {-1, -1, -1, -1, -1, -1, -1};
+    int part = 0, nparts = 1;  // l0s_search_part: this context screens units u with u % nparts == part
 
     ~l0s_ctx() {
         DBuf* all[] = {&in_values, &in_y, &in_perm, &bounds_d, &zoff_d, &Xp, &yp, &Z, &G, &qf, &un2, &yyu, &rowsd,
@@ -871,7 +872,8 @@ static int search_exact_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_
 }
 
 // QR screen of the `nill` ranks in c->ill, then bit-exact refit of the ones that can matter.
-static int screen_ill(l0s_ctx* c, int n, int64_t nill, int64_t keep, std::vector<Cand>& best, l0s_stats* st) {
+static int screen_ill(l0s_ctx* c, int n, int64_t nill, int64_t keep, std::vector<Cand>& best, l0s_stats* st,
+                      double cap = INFINITY) {
     if (c->prec == L0S_PREC_FP32) {
         // the fp64 QR screen cannot bound the reference's float32 arithmetic on an
         // ill-conditioned system: every such tuple is refit bit-exactly
@@ -915,7 +917,7 @@ static int screen_ill(l0s_ctx* c, int n, int64_t nill, int64_t keep, std::vector
     const double tol = 1e-10;  // RANK_TOL_FACTOR["fp64"], lsq.py:23 (fp32 never reaches the QR screen)
     double yy = 0.0;
     for (double v : c->yyu_h) yy += v;
-    const double sk = ((int64_t)best.size() >= keep) ? best[(size_t)keep - 1].score : INFINITY;
+    const double sk = std::min(((int64_t)best.size() >= keep) ? best[(size_t)keep - 1].score : INFINITY, cap);
     // selection on the device: only the (usually empty) list of survivors comes back
     CK(c->ex_ranks.ensure(sizeof(int64_t) * (size_t)std::max<int64_t>(nill, 1)));
     CK(c->cand_cnt.ensure(sizeof(unsigned long long)));
@@ -941,20 +943,43 @@ static int screen_ill(l0s_ctx* c, int n, int64_t nill, int64_t keep, std::vector
 static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t re, std::vector<Cand>& best,
                             l0s_stats* st) {
     const int64_t N = binom_sat(c->m, n);
-    // unit table (cached per problem shape and rank range)
-    int64_t key[5] = {c->m, c->T, rb, re, n};
-    if (!std::equal(key, key + 5, c->units_key)) {
+    // unit table (cached per problem shape, rank range and part)
+    int64_t key[7] = {c->m, c->T, rb, re, n, c->part, c->nparts};
+    if (!std::equal(key, key + 7, c->units_key)) {
         // prefix[v] = rank of the first tuple whose smallest index is v
         std::vector<int64_t> pre((size_t)c->m + 1, 0);
         for (int64_t v = 0; v < c->m; ++v) pre[(size_t)v + 1] = pre[(size_t)v] + binom_sat(c->m - 1 - v, n - 1);
         c->units_h = n == 2 ? fit2_units(c->m, pre, rb, re)
                      : n == 3 ? fit3_units(c->m, c->T, N, pre, rb, re)
                               : fit4_units(c->m, c->T, pre, rb, re);
+        if (c->nparts > 1) {
+            // a part gets 1/nparts of the units: split their i ranges until every part still has
+            // several units per CTA, then deal them round-robin over the longest-first order
+            const int g = n == 2 ? fit2_grid(c->T, c->nsm) : n == 3 ? fit3_grid(c->T, c->nsm) : fit4_grid(c->T, c->nsm);
+            int64_t rows = 0;
+            for (const int4& u : c->units_h) rows += u.w - u.z;
+            const int64_t target = (int64_t)6 * g * c->nparts;
+            const int ich = (int)std::max<int64_t>(64, (rows / std::max<int64_t>(target, 1) + 31) / 32 * 32);
+            std::vector<int4> split;
+            for (const int4& u : c->units_h)
+                for (int lo = u.z; lo < u.w; lo += ich) split.push_back(make_int4(u.x, u.y, lo, std::min(u.w, lo + ich)));
+            std::stable_sort(split.begin(), split.end(),
+                             [](const int4& x, const int4& y) { return (x.w - x.z) > (y.w - y.z); });
+            std::vector<int4> mine;
+            for (size_t u = (size_t)c->part; u < split.size(); u += (size_t)c->nparts) mine.push_back(split[u]);
+            c->units_h.swap(mine);
+        }
         CK(c->units.ensure(sizeof(int4) * std::max<size_t>(c->units_h.size(), 1)));
-        CK(cudaMemcpyAsync(c->units.p, c->units_h.data(), sizeof(int4) * c->units_h.size(), cudaMemcpyHostToDevice, c->st));
-        std::copy(key, key + 5, c->units_key);
+        if (!c->units_h.empty())
+            CK(cudaMemcpyAsync(c->units.p, c->units_h.data(), sizeof(int4) * c->units_h.size(), cudaMemcpyHostToDevice,
+                               c->st));
+        std::copy(key, key + 7, c->units_key);
     }
-    const int kc = (int)std::min<int64_t>(128, std::max<int64_t>(64, keep + 32));
+    // K': per-warp list length and refit set.  A search part keeps the longest lists: with 64
+    // (or 74, one refit wave at T = 4) the part holding the best tuples of C3 missed its
+    // certificate and paid a rescan (~1 ms); 96 and 128 refit in two waves (0.40 ms) and
+    // certify (tools/parts_balance.py)
+    const int kc = c->nparts > 1 ? 128 : (int)std::min<int64_t>(128, std::max<int64_t>(64, keep + 32));
     const int grid = n == 2 ? fit2_grid(c->T, c->nsm) : n == 3 ? fit3_grid(c->T, c->nsm) : fit4_grid(c->T, c->nsm);
     auto launch_fit = [&](const FitArgs& fa) {
         return n == 2 ? fit2_launch(fa, c->nsm, c->st)
@@ -966,7 +991,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     CK(c->ucount.ensure(sizeof(int) * 4));
     CK(c->theta_g.ensure(sizeof(unsigned long long)));
     CK(c->hist.ensure(sizeof(unsigned) * HIST_BINS));
-    CK(c->seedbuf.ensure(sizeof(int64_t) * 1024 * 5 + 64));
+    CK(c->seedbuf.ensure(sizeof(int64_t) * 1024 * 5 + 256));  // subsets, bounds, count, cap
     CK(c->wl_lb.ensure(sizeof(double) * slots * kc));
     CK(c->wl_rank.ensure(sizeof(int64_t) * slots * kc));
     CK(c->wl_cnt.ensure(sizeof(int) * slots));
@@ -997,6 +1022,8 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     a.seed_tup = c->seedbuf.as<int64_t>();
     a.seed_ub = c->seedbuf.as<double>() + 1024 * 4;
     a.seed_n = reinterpret_cast<int*>(c->seedbuf.as<double>() + 1024 * 5);
+    a.seed_cap = c->seedbuf.as<double>() + 1024 * 5 + 4;
+    a.keep = (int)keep;
     {
         double yy_top = 0.0;  // uncentered total |y|^2 >= every pooled bound
         for (double v : c->yyu_h) yy_top += v;
@@ -1011,6 +1038,8 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
 
     CK(cudaMemsetAsync(c->ucount.p, 0, sizeof(int) * 4, c->st));
     CK(cudaMemcpyAsync(c->theta_g.p, &inf_enc, sizeof inf_enc, cudaMemcpyHostToDevice, c->st));
+    static const double inf_d = INFINITY;
+    CK(cudaMemcpyAsync(a.seed_cap, &inf_d, sizeof inf_d, cudaMemcpyHostToDevice, c->st));
     CK(cudaMemsetAsync(c->hist.p, 0, sizeof(unsigned) * HIST_BINS, c->st));
     CK(cudaMemsetAsync(c->ill_cnt.p, 0, sizeof(unsigned long long), c->st));
     CK(cudaMemsetAsync(c->cand_cnt.p, 0, sizeof(unsigned long long), c->st));
@@ -1024,6 +1053,8 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
                              c->cand_rank.as<int64_t>(), c->cand_cnt.as<unsigned long long>(), c->st);
     st->n_launches++;
     unsigned long long ncand = 0, nill = 0, th_enc = 0;
+    double seed_cap = INFINITY;
+    CK(cudaMemcpyAsync(&seed_cap, a.seed_cap, sizeof seed_cap, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(&ncand, c->cand_cnt.p, sizeof ncand, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(&nill, c->ill_cnt.p, sizeof nill, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(&th_enc, c->theta_g.p, sizeof th_enc, cudaMemcpyDeviceToHost, c->st));
@@ -1045,6 +1076,10 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
         CK(cudaStreamSynchronize(c->st));
         G_lb = std::min(G_lb, st->theta);
     }
+    // A search part (l0s_search_part) answers for its own units only, but the seed's subsets come
+    // from the whole problem: >= keep tuples score at most seed_cap / s, so the global keep-th
+    // score is below that cap and a part's excluded tuples need only clear the cap.
+    const double cap = c->nparts > 1 ? seed_cap / (double)c->s : INFINITY;
     // exact refit of candidates + ill tuples
     std::vector<Cand> exact;
     cudaEventRecord(c->ev[2], c->st);
@@ -1055,7 +1090,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
         // Tuples the Gram screen could not certify: TSQR on the device gives each a score and
         // the reference's rank-rule ratio; only those that can reach the top list within the
         // QR's error margin (~ eps / ratio) are refit bit-exactly.
-        rc = screen_ill(c, n, (int64_t)nill, keep, best, st);
+        rc = screen_ill(c, n, (int64_t)nill, keep, best, st, cap);
         if (rc) return rc;
     }
     cudaEventRecord(c->ev[3], c->st);
@@ -1070,7 +1105,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     for (double v : c->yyu_h) yy += v;
     auto margin_of = [&](double sk) { return 1e-10 * std::fabs(sk) + 64.0 * kEps * yy / (double)c->s; };
     bool complete = !std::isfinite(G_lb);  // nothing was ever dropped
-    double sk = ((int64_t)best.size() >= keep) ? best[(size_t)keep - 1].score : INFINITY;
+    double sk = std::min(((int64_t)best.size() >= keep) ? best[(size_t)keep - 1].score : INFINITY, cap);
     bool certified = complete || (G_lb / (double)c->s > sk + margin_of(sk));
     st->margin = G_lb / (double)c->s - sk;
     if (!certified) {
@@ -1214,6 +1249,29 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
     cudaEventDestroy(t1);
     *out_count = nk;
     return L0S_OK;
+}
+
+int l0s_search_part(l0s_ctx* c, int n, int64_t keep, int part, int nparts, int mode, double* out_scores,
+                    int64_t* out_ranks, double* out_coef, double* out_ssr, int64_t* out_count, l0s_stats* stats) {
+    if (out_count) *out_count = 0;
+    if (!c || !c->staged) return fail(L0S_ESTATE, "l0s_stage must be called first");
+    if (nparts < 1 || part < 0 || part >= nparts) return fail(L0S_EINVAL, "part %d of %d", part, nparts);
+    int64_t N = 0;
+    int rc = (n >= 1 && c->m >= n) ? l0s_count(c->m, n, &N) : L0S_OK;
+    if (rc) return rc;
+    // every part must take the same path: decided on the whole problem, as l0s_search would
+    const bool fast_ok = (n >= 2 && n <= 4) && c->T <= fit3_max_tasks() && keep >= 1 && keep <= 96;
+    const bool fast = mode == L0S_MODE_FAST || (mode == L0S_MODE_AUTO && fast_ok && (double)N * (double)c->s > 2e8);
+    if (!fast || !fast_ok || nparts == 1)  // contiguous rank ranges (search.py:266-271)
+        return l0s_search(c, n, keep, N / nparts * part + std::min<int64_t>(part, N % nparts),
+                          N / nparts * (part + 1) + std::min<int64_t>(part + 1, N % nparts), mode, out_scores,
+                          out_ranks, out_coef, out_ssr, out_count, stats);
+    c->part = part;
+    c->nparts = nparts;
+    rc = l0s_search(c, n, keep, 0, N, L0S_MODE_FAST, out_scores, out_ranks, out_coef, out_ssr, out_count, stats);
+    c->part = 0;
+    c->nparts = 1;
+    return rc;
 }
 
 }  // extern "C"

@@ -432,6 +432,9 @@ __global__ void __launch_bounds__(512, 1) k_seed_commit(const __grid_constant__ 
         }
     if (threadIdx.x == 0) {
         const double v = ub[a.kc - 1];
+        // >= keep tuples score at most the keep-th bound: caps the global keep-th score (search
+        // parts, api.cu)
+        if (a.seed_cap) *a.seed_cap = ub[(a.keep >= 1 && a.keep <= a.kc ? a.keep : a.kc) - 1];
         if (v < INFINITY) {
             const double th = v + fabs(v) * 1e-9 + 1e-300;  // strictly above kc certified bounds
             atomicMin(a.theta_g, ord_enc(th));

@@ -170,6 +170,8 @@ struct FitArgs {
     int64_t* seed_tup;       // [SEED_MAX][4] threshold-seed subsets (fitcommon.cuh)
     double* seed_ub;         // [SEED_MAX] their upper bounds
     int* seed_n;             // subset count
+    double* seed_cap;        // out: the keep-th smallest certified upper bound of the seed (SSR units)
+    int keep;                // models kept (search parts: the seed caps the global keep-th score)
     int hist_base;           // bin offset: (biased exponent of the top) - HIST_EXP, times HIST_SUB
     double* wl_lb;           // [n_warp_slots][kc]
     int64_t* wl_rank;

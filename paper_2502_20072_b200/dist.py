@@ -94,9 +94,9 @@ def sharded_l0_search(values, property_values, task_slices=None, config=None, ta
     receives the same merged list of ``Model`` records.
 
     Default path (one process per GPU): the inputs go to this rank's device, the stage is
-    collective (``sharded_stage``: 1/world of the Gram per rank, NCCL all-gather), the rank
-    searches its contiguous rank range and certifies its own top list exactly, and the lists
-    are merged by (score, rank).  ``local_search(values, y, task_slices, config, task_labels,
+    collective (``sharded_stage``), the rank searches its part (``l0s_search_part``: every
+    world-th unit of the screened path, else its contiguous rank range) and certifies its own
+    top list exactly, and the lists are merged by (score, rank).  ``local_search(values, y, task_slices, config, task_labels,
     rank_range) -> list of models`` replaces the device part (the CPU tests inject the oracle).
     """
     import torch.distributed as dist
@@ -128,9 +128,11 @@ def sharded_l0_search(values, property_values, task_slices=None, config=None, ta
         pd = torch.from_numpy(perm).to(dev)
         torch.cuda.synchronize(dev)
         sharded_stage(eng, (m, s), bounds, config.precision, (vd.data_ptr(), yd.data_ptr(), pd.data_ptr()), group)
+        # this rank's part of the search: every world-th unit of the screened path (ill-
+        # conditioned tuples cluster in rank ranges, C4), else the contiguous rank range
+        sc, rk, coef, ssr, _ = eng.search_part(n, keep, me, world, "auto")
         models = []
-        if hi > lo:
-            sc, rk, coef, ssr, _ = eng.search(n, keep, lo, hi, "auto")
+        if len(sc):
             labels = _labels_for(slices, task_labels)
             models = [_model(unrank_tuple(int(rk[i]), m, n), expressions, coef[i], ssr[i], bounds, s, labels)
                       for i in range(len(sc))]

@@ -709,3 +709,37 @@ def test_qr_screen_ill_tuples_match_oracle(oracle, n, planted_pair):
     assert bits_equal([md.score for md in got], [w["score"] for w in want])
     for md, w in zip(got, want):
         assert bits_equal(md.coefficients, w["coefficients"])
+
+
+@pytest.mark.parametrize("case", ["planted3", "ill4", "random2"])
+@pytest.mark.parametrize("nparts", [2, 3, 8])
+def test_search_parts_merge_to_the_whole_search(case, nparts):
+    """l0s_search_part (the multi-GPU split: every nparts-th unit per part) emulated on one
+    device: the (score, rank) merge of all parts is exactly the whole search."""
+    from paper_2502_20072_b200 import _lib
+    from paper_2502_20072_b200.dist import merge_candidates
+    from paper_2502_20072_b200.search import _partition
+
+    rng = np.random.default_rng(hash(case) % 1000)
+    n = int(case[-1])
+    m, s, T = {"planted3": (120, 900, 3), "ill4": (44, 240, 2), "random2": (300, 400, 1)}[case]
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    if case == "ill4":
+        for c, d in enumerate([1e-4, 1e-6, 1e-8, 1e-9, 1e-11, 1e-13]):
+            v[30 + c] = v[c] + d * rng.standard_normal(s)
+        v[41] = v[10]
+    y = (1.5 * v[3] - v[40] + 0.5 * v[m - 5] + 0.02 * rng.standard_normal(s)) if case != "random2" else \
+        rng.standard_normal(s)
+    perm, bounds, _ = _partition(s, [np.arange(t, s, T) for t in range(T)])
+    eng = _lib.engine(0)
+    eng.stage(v, y, perm, bounds, "fp64")
+    sc, rk, coef, ssr, st = eng.search(n, 10, 0, 2**63 - 1, "fast")
+    parts = []
+    for p in range(nparts):
+        psc, prk, pcoef, _, pst = eng.search_part(n, 10, p, nparts, "fast")
+        assert pst.as_dict()["certified"] == 1
+        parts.append([(float(a), int(b), c) for a, b, c in zip(psc, prk, pcoef)])
+    merged = merge_candidates(parts, 10)
+    assert [c[1] for c in merged] == rk.tolist()
+    assert bits_equal([c[0] for c in merged], sc)
+    assert all(bits_equal(c[2], w) for c, w in zip(merged, coef))
