@@ -1080,10 +1080,25 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     // from the whole problem: >= keep tuples score at most seed_cap / s, so the global keep-th
     // score is below that cap and a part's excluded tuples need only clear the cap.
     const double cap = c->nparts > 1 ? seed_cap / (double)c->s : INFINITY;
+    double yy = 0.0;
+    for (double v : c->yyu_h) yy += v;
+    auto margin_of = [&](double sk) { return 1e-10 * std::fabs(sk) + 64.0 * kEps * yy / (double)c->s; };
+    // a part refits only the candidates that can reach the global top list: the sorted bounds
+    // above the cap (+ margin) are excluded like the rest (G_lb drops to the first of them)
+    int64_t nref = nc;
+    if (std::isfinite(cap) && nc > 0) {
+        std::vector<double> lbs((size_t)nc);
+        CK(cudaMemcpyAsync(lbs.data(), c->cand_lb.p, sizeof(double) * nc, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        const double lim = (cap + margin_of(cap)) * (double)c->s;
+        nref = 0;
+        while (nref < nc && lbs[(size_t)nref] <= lim) ++nref;
+        if (nref < nc) G_lb = std::min(G_lb, lbs[(size_t)nref]);
+    }
     // exact refit of candidates + ill tuples
     std::vector<Cand> exact;
     cudaEventRecord(c->ev[2], c->st);
-    int rc = exact_ranks_to_host(c, n, c->cand_rank.as<int64_t>(), nc, exact, &st->n_launches, &c->recs);
+    int rc = exact_ranks_to_host(c, n, c->cand_rank.as<int64_t>(), nref, exact, &st->n_launches, &c->recs);
     if (rc) return rc;
     merge_best(best, exact, keep);
     if (nill > 0) {
@@ -1096,14 +1111,11 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     cudaEventRecord(c->ev[3], c->st);
     CK(cudaStreamSynchronize(c->st));
     st->ms_exact += elapsed(c->ev[2], c->ev[3]);
-    st->n_candidates = nc;
+    st->n_candidates = nref;
     st->n_ill = (int64_t)nill;
 
     // certification: an excluded tuple has exact score >= lb / s >= G_lb / s; it cannot
     // displace the keep-th exact score if G_lb / s exceeds it by the reference's own error margin
-    double yy = 0.0;
-    for (double v : c->yyu_h) yy += v;
-    auto margin_of = [&](double sk) { return 1e-10 * std::fabs(sk) + 64.0 * kEps * yy / (double)c->s; };
     bool complete = !std::isfinite(G_lb);  // nothing was ever dropped
     double sk = std::min(((int64_t)best.size() >= keep) ? best[(size_t)keep - 1].score : INFINITY, cap);
     bool certified = complete || (G_lb / (double)c->s > sk + margin_of(sk));
