@@ -743,3 +743,55 @@ def test_search_parts_merge_to_the_whole_search(case, nparts):
     assert [c[1] for c in merged] == rk.tolist()
     assert bits_equal([c[0] for c in merged], sc)
     assert all(bits_equal(c[2], w) for c, w in zip(merged, coef))
+
+
+def _sharded_worker(rank, world, port, case, out_q):
+    import sys
+
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2502_20072_b200 import L0Config
+    from paper_2502_20072_b200.dist import sharded_l0_search
+
+    v, y, slices, n = case
+    got = sharded_l0_search(v, y, slices, L0Config(dimension=n), device=0)
+    out_q.put((rank, [(md.indices, md.score, md.coefficients) for md in got]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [3, 4])
+def test_sharded_l0_search_two_ranks_on_one_device(n):
+    """The public multi-GPU API (collective stage, search parts, merge) with two gloo ranks
+    sharing the device: every rank returns exactly the single-process l0_search."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_2502_20072_b200 import L0Config, l0_search
+
+    rng = np.random.default_rng(70 + n)
+    m, s, T = (300, 2000, 2) if n == 3 else (60, 600, 2)
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    v[m - 1] = v[2] + 1e-7 * rng.standard_normal(s)
+    y = 1.2 * v[2] - 0.8 * v[m // 2] + 0.5 * v[m - 3] + 0.02 * rng.standard_normal(s)
+    slices = [np.arange(t, s, T) for t in range(T)]
+    want = l0_search(v, y, slices, L0Config(dimension=n), mode="fast")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, (v, y, slices, n), q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+    for _, got in res:
+        assert [g[0] for g in got] == [w.indices for w in want]
+        assert bits_equal([g[1] for g in got], [w.score for w in want])
+        assert all(bits_equal(g[2], w.coefficients) for g, w in zip(got, want))
