@@ -346,7 +346,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (numpy default_rng(2), planted y)",
         "config": {"workload": "C3: l0 search dim 3, n_sis_total=2000, 10k samples, 4 tasks, keep 10",
-                   "tuples_per_step": total, "parallelism": f"search parts x{world} (every {world}-th unit per rank)",
+                   "tuples_per_step": total, "parallelism": f"search parts x{world} (unit u on rank u mod {world})",
                    "l2": "inputs (160 MB) and Gram (128 MB) exceed the 126 MB L2"},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
