@@ -965,8 +965,12 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
                 for (int lo = u.z; lo < u.w; lo += ich) split.push_back(make_int4(u.x, u.y, lo, std::min(u.w, lo + ich)));
             std::stable_sort(split.begin(), split.end(),
                              [](const int4& x, const int4& y) { return (x.w - x.z) > (y.w - y.z); });
-            std::vector<int4> mine;
-            for (size_t u = (size_t)c->part; u < split.size(); u += (size_t)c->nparts) mine.push_back(split[u]);
+            std::vector<int4> mine;  // snake order (0..P-1, P-1..0, ...): equal shares of long units
+            const size_t P = (size_t)c->nparts;
+            for (size_t u = 0; u < split.size(); ++u) {
+                const size_t r = u % (2 * P);
+                if ((r < P ? r : 2 * P - 1 - r) == (size_t)c->part) mine.push_back(split[u]);
+            }
             c->units_h.swap(mine);
         }
         CK(c->units.ensure(sizeof(int4) * std::max<size_t>(c->units_h.size(), 1)));
