@@ -795,3 +795,29 @@ def test_sharded_l0_search_two_ranks_on_one_device(n):
         assert [g[0] for g in got] == [w.indices for w in want]
         assert bits_equal([g[1] for g in got], [w.score for w in want])
         assert all(bits_equal(g[2], w.coefficients) for g, w in zip(got, want))
+
+
+@pytest.mark.parametrize("n,precision,mode", [(3, "fp32", "fast"), (1, "fp64", "auto"), (5, "fp64", "auto"),
+                                              (2, "fp64", "exact")])
+def test_search_parts_other_paths(n, precision, mode):
+    """Parts on the fp32 screen and on the exact path (contiguous rank ranges) merge to the
+    whole search too."""
+    from paper_2502_20072_b200 import _lib
+    from paper_2502_20072_b200.dist import merge_candidates
+    from paper_2502_20072_b200.search import _partition
+
+    rng = np.random.default_rng(90 + n)
+    m, s, T = (40, 300, 2) if n != 5 else (16, 120, 2)
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    y = 1.1 * v[1] - 0.7 * v[m - 2] + 0.02 * rng.standard_normal(s)
+    perm, bounds, _ = _partition(s, [np.arange(t, s, T) for t in range(T)])
+    eng = _lib.engine(0)
+    eng.stage(v, y, perm, bounds, precision)
+    sc, rk, coef, _, _ = eng.search(n, 10, 0, 2**63 - 1, mode)
+    for nparts in (2, 5):
+        parts = [[(float(a), int(b), c) for a, b, c in zip(*eng.search_part(n, 10, p, nparts, mode)[:3])]
+                 for p in range(nparts)]
+        merged = merge_candidates(parts, 10)
+        assert [c[1] for c in merged] == rk.tolist()
+        assert bits_equal([c[0] for c in merged], sc)
+        assert all(bits_equal(c[2], w) for c, w in zip(merged, coef))
