@@ -255,7 +255,7 @@ int l0s_count(int64_t m, int n, int64_t *out_count); /* C(m,n); L0S_ECAPACITY if
 /* Microbenchmarks used by bench.py for the roofline denominator. */
 int l0s_fp64_peak(l0s_ctx *ctx, double *out_tflops);
 /* Worst relative error of the screen's fast reciprocal over `count` hashed doubles
- * (the screen assumes <= 2^-17; tests/test_gpu_kernels.py checks it). */
+ * (the screen assumes <= 2^-17; tests/test_gpu_parity.py::test_rcp_fast_bound checks it). */
 int l0s_rcp_check(int64_t count, double *out_max_rel);
 
 #ifdef __cplusplus

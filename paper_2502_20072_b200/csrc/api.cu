@@ -232,6 +232,9 @@ int run_exact(l0s_ctx* c, int n, const int64_t* ranks_d, const int64_t* tuples_d
     return L0S_OK;
 }
 
+// CTAs assumed when splitting units into search parts (a B200's 148 SMs, one CTA each)
+constexpr int kPartGridCtas = 148;
+
 struct Cand {
     double score;
     int64_t rank;
@@ -950,12 +953,14 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
         std::vector<int64_t> pre((size_t)c->m + 1, 0);
         for (int64_t v = 0; v < c->m; ++v) pre[(size_t)v + 1] = pre[(size_t)v] + binom_sat(c->m - 1 - v, n - 1);
         c->units_h = n == 2 ? fit2_units(c->m, pre, rb, re)
-                     : n == 3 ? fit3_units(c->m, c->T, N, pre, rb, re)
+                     : n == 3 ? fit3_units(c->m, c->T, N, pre, rb, re, c->nparts == 1)
                               : fit4_units(c->m, c->T, pre, rb, re);
         if (c->nparts > 1) {
             // a part gets 1/nparts of the units: split their i ranges until every part still has
             // several units per CTA, then deal them round-robin over the longest-first order
-            const int g = n == 2 ? fit2_grid(c->T, c->nsm) : n == 3 ? fit3_grid(c->T, c->nsm) : fit4_grid(c->T, c->nsm);
+            // from shared values only (not this device's SM count or occupancy): every rank must
+            // build the same split table, or parts would overlap or leave gaps
+            const int g = kPartGridCtas;
             int64_t rows = 0;
             for (const int4& u : c->units_h) rows += u.w - u.z;
             const int64_t target = (int64_t)6 * g * c->nparts;

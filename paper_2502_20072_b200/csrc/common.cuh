@@ -76,7 +76,7 @@ __device__ __forceinline__ void unrank_lex(int64_t rank, int64_t m, int n, const
 // 1/|d| from the MUFU.RCP64H unit: one integer LOP (sign clear, low word
 // dropped) and one MUFU op, no FP64-pipe instruction.  Relative error is
 // bounded by kRcpRel (measured exhaustively over mantissas by
-// tests/test_gpu_kernels.py::test_rcp_fast_bound); the screen absorbs it by
+// tests/test_gpu_parity.py::test_rcp_fast_bound); the screen absorbs it by
 // shrinking its threshold, so a tuple is never dropped because of it.
 constexpr double kRcpRel = 1.0 / 65536.0;  // 2^-16, conservative (measured < 2^-17)
 __device__ __forceinline__ double rcp_fast_abs(double d) {

@@ -21,8 +21,9 @@
 //
 // Layout: one unit = 32 j (lanes) x KSPAN k (8 warps x P) x up to 128 i.
 // The i-dependent Gram rows C[i, j-block], C[i, k-span], c_i are staged in
-// shared memory by cp.async (double-buffered over IB-row tiles); the (j, k)
-// state lives in registers.  Persistent CTAs pull units from an atomic counter.
+// shared memory by TMA (cp.async.bulk.tensor, mbarrier completion, double-buffered
+// over IB-row tiles); the (j, k) state lives in registers.  Persistent CTAs pull
+// units from an atomic counter.
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -590,14 +591,16 @@ int fit3_launch(const FitArgs& a, int nsm, cudaStream_t st) {
 
 // Unit table for n = 3: (j-block of 32, k-span, i range), i < j < k < m.
 std::vector<int4> fit3_units(int64_t m, int T, int64_t N_total, const std::vector<int64_t>& c2_prefix,
-                             int64_t rank_lo, int64_t rank_hi) {
+                             int64_t rank_lo, int64_t rank_hi, bool tunable) {
     const int kspan = fit3_kspan(T);
-    // i rows per unit: amortizes the (j, k) hoist; L0S_ICH overrides (tuning)
-    static const int ich = [] {
+    // i rows per unit: amortizes the (j, k) hoist; L0S_ICH overrides (tuning, single searches
+    // only: search parts on different ranks must build identical tables)
+    static const int ich_env = [] {
         const char* e = getenv("L0S_ICH");
         const int v = e ? atoi(e) : 0;
         return v > 0 ? v : 4096;
     }();
+    const int ich = tunable ? ich_env : 4096;
     std::vector<int4> units;
     int nJ = (int)((m + 31) / 32);
     int nK = (int)((m + kspan - 1) / kspan);

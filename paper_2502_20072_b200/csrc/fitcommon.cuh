@@ -434,7 +434,8 @@ __global__ void __launch_bounds__(512, 1) k_seed_commit(const __grid_constant__ 
         const double v = ub[a.kc - 1];
         // >= keep tuples score at most the keep-th bound: caps the global keep-th score (search
         // parts, api.cu)
-        if (a.seed_cap) *a.seed_cap = ub[(a.keep >= 1 && a.keep <= a.kc ? a.keep : a.kc) - 1];
+        // (only when keep <= kc: the kc-th bound guarantees kc tuples below it, not keep)
+        if (a.seed_cap) *a.seed_cap = (a.keep >= 1 && a.keep <= a.kc) ? ub[a.keep - 1] : INFINITY;
         if (v < INFINITY) {
             const double th = v + fabs(v) * 1e-9 + 1e-300;  // strictly above kc certified bounds
             atomicMin(a.theta_g, ord_enc(th));

@@ -191,7 +191,7 @@ int fit_slots_per_cta();   // warp candidate slots per CTA (n = 2, 4)
 int fit3_slots_per_cta();  // the same for the n = 3 sweep
 int fit3_kspan(int T);
 std::vector<int4> fit3_units(int64_t m, int T, int64_t N_total, const std::vector<int64_t>& c2_prefix,
-                             int64_t rank_lo, int64_t rank_hi);
+                             int64_t rank_lo, int64_t rank_hi, bool tunable = true);
 // lower bound + flags for explicit 3-tuples (same arithmetic as the fit kernel's slow path)
 void launch_screen3(const FitArgs& a, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags,
                     cudaStream_t st);

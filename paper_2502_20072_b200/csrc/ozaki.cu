@@ -12,13 +12,14 @@
 // which the screen's error model takes in place of the fp64 dot-product bound; a task whose
 // eta exceeds OZ_ETA_MAX falls back to the DMMA Gram (spiky rows).
 //
-// GEMM: one CTA per 128 x 64 upper-triangle tile of one task, two CTAs per SM (256 TMEM
-// columns and 97 KB of shared memory each, so one CTA's epilogue overlaps the other's main
-// loop); 192 threads = TMA producer warp, MMA warp (one elected thread issues tcgen05.mma; it
-// also owns the TMEM allocation) and 4 epilogue warps (tcgen05.ld by TMEM lane quadrant,
-// stores staged through shared memory so both G[r][c] and its mirror G[c][r] are coalesced).
-// A pipeline stage is one 64-byte K chunk of all 4 digit planes of both operands (8 TMA boxes,
-// SWIZZLE_64B, 48 KB), 2 stages; each stage feeds 10 digit pairs x 2 MMAs of 128 x 64 x 32.
+// GEMM: one CTA per 128 x 128 upper-triangle tile of one task, one CTA per SM (all 512 TMEM
+// columns: four 128-column accumulators, one per digit weight; 64-wide tiles with two CTAs per
+// SM were 6 % slower); 192 threads = TMA producer warp, MMA warp (one elected thread issues
+// tcgen05.mma; it also owns the TMEM allocation) and 4 epilogue warps (tcgen05.ld by TMEM lane
+// quadrant, stores staged through shared memory so both G[r][c] and its mirror G[c][r] are
+// coalesced).  A pipeline stage is one 64-byte K chunk of all 4 digit planes of both operands
+// (8 TMA boxes, SWIZZLE_64B, 64 KB), 3 stages; each stage feeds 10 digit pairs x 2 MMAs of
+// 128 x 128 x 32.
 #include <algorithm>
 #include <cstdlib>
 

@@ -131,12 +131,15 @@ def sharded_l0_search(values, property_values, task_slices=None, config=None, ta
         # this rank's part of the search: every world-th unit of the screened path (ill-
         # conditioned tuples cluster in rank ranges, C4), else the contiguous rank range
         sc, rk, coef, ssr, _ = eng.search_part(n, keep, me, world, "auto")
-        models = []
-        if len(sc):
-            labels = _labels_for(slices, task_labels)
-            models = [_model(unrank_tuple(int(rk[i]), m, n), expressions, coef[i], ssr[i], bounds, s, labels)
-                      for i in range(len(sc))]
-    mine = [(float(md.score), rank_tuple(md.indices, m, n), md) for md in models]
+        labels = _labels_for(slices, task_labels)
+        # merge key: the device score (score_tuples' sequential task sum, search.py:303), not
+        # Model.score (numpy's ssr.sum(), which may differ in the last bit for 8 tasks)
+        mine = [(float(sc[i]), int(rk[i]),
+                 _model(unrank_tuple(int(rk[i]), m, n), expressions, coef[i], ssr[i], bounds, s, labels))
+                for i in range(len(sc))]
+        models = None
+    if models is not None:
+        mine = [(float(md.score), rank_tuple(md.indices, m, n), md) for md in models]
     parts = [None] * world
     dist.all_gather_object(parts, mine, group=group)
     return [c[2] for c in merge_candidates(parts, keep)]
