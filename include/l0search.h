@@ -70,6 +70,10 @@ typedef struct {
     double ms_qr;            /* QR screen of the uncertifiable tuples                 */
     int64_t n_ill_refit;     /* of those, refit bit-exactly                           */
     double ms_gram_kernel;   /* the Gram kernel alone (device-resident, unchunked stage) */
+    double ms_records;       /* final records: refit of kept tuples not already refit (excluded from
+                                SearchStats.seconds like the reference's per-model fit_tuple)    */
+    int64_t n_eval;          /* task-tuple evaluations the screened sweep executed (one (i, j, k, task)
+                                bound term; the physical work behind the roofline)             */
 } l0s_stats;
 
 const char *l0s_last_error(void);
@@ -243,6 +247,10 @@ int l0s_sis_scores(l0s_ctx *ctx, const double *F, int64_t k, int is_device, doub
 int l0s_set_gram_mode(l0s_ctx *ctx, int mode);
 /* Per-task entry error bound of the staged Gram (ntasks values) and whether it is the INT8 one. */
 int l0s_stage_info(l0s_ctx *ctx, double *eta_out, int *ozaki_out);
+/* Device times (ms) of the last stage when its inputs were device-resident (unchunked):
+ * [gather (search._prepare's permutation + cast), normalize (+ INT8 digits), Gram, feature
+ * flags]; zeros after a chunked host stage. */
+int l0s_stage_timings(l0s_ctx *ctx, double *out_ms);
 
 /* Copy of the staged normalized Gram of one task ((m+1) x (m+1), last row/col = y). */
 int l0s_get_gram(l0s_ctx *ctx, int task, double *out);

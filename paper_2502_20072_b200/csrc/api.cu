@@ -109,6 +109,8 @@ struct l0s_ctx {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     static constexpr int kChunks = 8;
     cudaEvent_t cev[kChunks + 1] = {};
+    cudaEvent_t sev[5] = {};         // unchunked stage: gather | normalize | (Gram: ev[2..3]) | flags
+    bool stage_timed = false;
     // staged problem
     bool staged = false;
     int64_t m = 0, s = 0, mp = 0, sp = 0, ld = 0;
@@ -132,7 +134,7 @@ struct l0s_ctx {
     int binom_n = -1;
     int64_t binom_m = -1;
     // search workspace
-    DBuf units, ucount, theta_g, hist, seedbuf, wl_lb, wl_rank, wl_cnt, ill, ill_cnt, cand_lb, cand_rank, cand_cnt, sort_tmp,
+    DBuf units, ucount, n_eval, theta_g, hist, seedbuf, wl_lb, wl_rank, wl_cnt, ill, ill_cnt, cand_lb, cand_rank, cand_cnt, sort_tmp,
         lb_tmp, rank_tmp, coll_lb, coll_rank, coll_cnt;
     DBuf ex_scratch, ex_ssr_tmp, ex_ok_tmp, ex_ok, ex_score, ex_coef, ex_ssr, ex_ranks, ex_tuples;
     DBuf qr_ssr, qr_ratio, qr_score, qr_minr;
@@ -151,7 +153,7 @@ struct l0s_ctx {
 
     ~l0s_ctx() {
         DBuf* all[] = {&in_values, &in_y, &in_perm, &bounds_d, &zoff_d, &Xp, &yp, &Z, &G, &qf, &un2, &yyu, &rowsd,
-                       &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &umin, &binom, &units, &ucount, &theta_g, &hist, &seedbuf, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
+                       &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &umin, &binom, &units, &ucount, &n_eval, &theta_g, &hist, &seedbuf, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
                        &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
                        &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr, &sis_y, &sis_yc, &sis_sy, &sis_perm,
@@ -161,6 +163,8 @@ struct l0s_ctx {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         for (auto& e : cev)
+            if (e) cudaEventDestroy(e);
+        for (auto& e : sev)
             if (e) cudaEventDestroy(e);
         if (st) cudaStreamDestroy(st);
         if (cst) cudaStreamDestroy(cst);
@@ -335,6 +339,7 @@ int l0s_create(int device, l0s_ctx** out) {
     }
     for (auto& e : c->ev) cudaEventCreate(&e);
     for (auto& e : c->cev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    for (auto& e : c->sev) cudaEventCreate(&e);
     if (const char* g = getenv("L0S_GRAM_MODE"))  // experiments: auto | dmma | ozaki
         c->gram_mode = !strcmp(g, "dmma") ? L0S_GRAM_DMMA : (!strcmp(g, "ozaki") ? L0S_GRAM_OZAKI : L0S_GRAM_AUTO);
     *out = c;
@@ -412,6 +417,7 @@ static bool ozaki_planned(const l0s_ctx* c);
 static int stage_post(l0s_ctx* c) {
     const int64_t m = c->m;
     const int ntasks = c->T;
+    cudaEventRecord(c->sev[3], c->st);
     launch_unit_diag(c->G.as<double>(), ntasks, m, c->mp, c->st);
     CK(cudaGetLastError());
     // per-feature conditioning flags on the device (stage.cu: launch_feature_flags)
@@ -427,6 +433,7 @@ static int stage_post(l0s_ctx* c) {
                          c->yyu.as<double>(), c->ynorm.as<double>(), c->st);
     CK(cudaGetLastError());
     cudaEventRecord(c->ev[1], c->st);
+    cudaEventRecord(c->sev[4], c->st);
     c->yyu_h.assign((size_t)ntasks, 0.0);
     CK(cudaMemcpyAsync(c->yyu_h.data(), c->yyu.p, sizeof(double) * ntasks, cudaMemcpyDeviceToHost, c->st));
     if (c->gram_ozaki)
@@ -558,10 +565,19 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
     if (!chunked) {
         if (!is_device)
             CK(copy_rows(c, values, rows, 0, m, 0, c->st));
-        rows_to_z(0, m);
+        // the two staging passes timed apart (bench.py reports their HBM rates)
+        cudaEventRecord(c->sev[0], c->st);
+        launch_gather(vd, yd, pd, m, s, precision, c->Xp.p, c->yp.p, 0, m, c->st);
+        cudaEventRecord(c->sev[1], c->st);
+        launch_normalize(c->Xp.p, c->yp.p, precision, m, s, c->bounds_d.as<int64_t>(), c->zoff_d.as<int64_t>(),
+                         ntasks, c->sp, c->Z.as<double>(), c->qf.as<double>(), c->un2.as<double>(),
+                         c->yyu.as<double>(), 0, m, dig, c->st);
+        cudaEventRecord(c->sev[2], c->st);
+        c->stage_timed = true;
         if (gram_cols) return gram_full(c);
         return L0S_OK;
     }
+    c->stage_timed = false;
     // the INT8 Gram runs once all rows have landed
     const bool ozaki = gram_cols && c->digits_ready;
     if (ozaki) gram_cols = false;
@@ -998,6 +1014,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     const int slots = grid * (n == 3 ? fit3_slots_per_cta() : fit_slots_per_cta());
     const int64_t ill_cap = (int64_t)1 << 26;  // 512 MB of ranks; overflow is reported, never dropped
     CK(c->ucount.ensure(sizeof(int) * 4));
+    CK(c->n_eval.ensure(sizeof(unsigned long long)));
     CK(c->theta_g.ensure(sizeof(unsigned long long)));
     CK(c->hist.ensure(sizeof(unsigned) * HIST_BINS));
     CK(c->seedbuf.ensure(sizeof(int64_t) * 1024 * 5 + 256));  // subsets, bounds, count, cap
@@ -1044,8 +1061,10 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     a.ill = c->ill.as<int64_t>();
     a.ill_cnt = c->ill_cnt.as<unsigned long long>();
     a.ill_cap = ill_cap;
+    a.n_eval = c->n_eval.as<unsigned long long>();
 
     CK(cudaMemsetAsync(c->ucount.p, 0, sizeof(int) * 4, c->st));
+    CK(cudaMemsetAsync(c->n_eval.p, 0, sizeof(unsigned long long), c->st));
     CK(cudaMemcpyAsync(c->theta_g.p, &inf_enc, sizeof inf_enc, cudaMemcpyHostToDevice, c->st));
     static const double inf_d = INFINITY;
     CK(cudaMemcpyAsync(a.seed_cap, &inf_d, sizeof inf_d, cudaMemcpyHostToDevice, c->st));
@@ -1061,14 +1080,16 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     launch_gather_candidates(a.wl_lb, a.wl_rank, a.wl_cnt, slots, kc, a.theta_g, c->cand_lb.as<double>(),
                              c->cand_rank.as<int64_t>(), c->cand_cnt.as<unsigned long long>(), c->st);
     st->n_launches++;
-    unsigned long long ncand = 0, nill = 0, th_enc = 0;
+    unsigned long long ncand = 0, nill = 0, th_enc = 0, nev = 0;
     double seed_cap = INFINITY;
+    CK(cudaMemcpyAsync(&nev, c->n_eval.p, sizeof nev, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(&seed_cap, a.seed_cap, sizeof seed_cap, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(&ncand, c->cand_cnt.p, sizeof ncand, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(&nill, c->ill_cnt.p, sizeof nill, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(&th_enc, c->theta_g.p, sizeof th_enc, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     st->ms_fit += elapsed(c->ev[2], c->ev[3]);
+    st->n_eval += (int64_t)nev;
     st->theta = ord_dec(th_enc);
     if ((int64_t)nill > ill_cap)
         return fail(L0S_ECAPACITY, "%llu ill-conditioned tuples exceed the routing buffer (%lld)",
@@ -1156,8 +1177,10 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
         st->n_launches++;
         unsigned long long ncoll = 0;
         CK(cudaMemcpyAsync(&ncoll, c->coll_cnt.p, sizeof ncoll, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(&nev, c->n_eval.p, sizeof nev, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
         st->ms_fit += elapsed(c->ev[2], c->ev[3]);
+        st->n_eval = (int64_t)nev;  // the counter accumulates over both sweeps
         if ((int64_t)ncoll > coll_cap)
             return fail(L0S_ECAPACITY, "%llu tuples below the certification threshold exceed the rescan buffer",
                         (unsigned long long)ncoll);
@@ -1237,6 +1260,7 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
             out_ranks[i] = best[(size_t)i].rank;
         }
     } else if (nk > 0) {
+        cudaEventRecord(c->ev[2], c->st);
         std::vector<int64_t> rk((size_t)nk);
         for (int64_t i = 0; i < nk; ++i) rk[(size_t)i] = best[(size_t)i].rank;
         CK(c->ex_ranks.ensure(sizeof(int64_t) * std::max<int64_t>(nk, 1 << 10)));
@@ -1252,7 +1276,9 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
         CK(cudaMemcpyAsync(sc.data(), c->ex_score.p, sizeof(double) * nk, cudaMemcpyDeviceToHost, c->st));
         if (out_coef) CK(cudaMemcpyAsync(out_coef, c->ex_coef.p, sizeof(double) * nk * c->T * p, cudaMemcpyDeviceToHost, c->st));
         if (out_ssr) CK(cudaMemcpyAsync(out_ssr, c->ex_ssr.p, sizeof(double) * nk * c->T, cudaMemcpyDeviceToHost, c->st));
+        cudaEventRecord(c->ev[3], c->st);
         CK(cudaStreamSynchronize(c->st));
+        st->ms_records = elapsed(c->ev[2], c->ev[3]);
         for (int64_t i = 0; i < nk; ++i) {
             if (sc[(size_t)i] != best[(size_t)i].score) {
                 cudaEventDestroy(t0);
@@ -1500,6 +1526,17 @@ int l0s_set_gram_mode(l0s_ctx* c, int mode) {
     if (!c) return fail(L0S_EINVAL, "null context");
     if (mode < L0S_GRAM_AUTO || mode > L0S_GRAM_OZAKI) return fail(L0S_EINVAL, "bad gram mode %d", mode);
     c->gram_mode = mode;
+    return L0S_OK;
+}
+
+int l0s_stage_timings(l0s_ctx* c, double* out_ms) {
+    if (!c || !c->staged) return fail(L0S_ESTATE, "l0s_stage must be called first");
+    for (int x = 0; x < 4; ++x) out_ms[x] = 0.0;
+    if (!c->stage_timed) return L0S_OK;
+    out_ms[0] = elapsed(c->sev[0], c->sev[1]);
+    out_ms[1] = elapsed(c->sev[1], c->sev[2]);
+    out_ms[2] = c->ms_gram_k;
+    out_ms[3] = elapsed(c->sev[3], c->sev[4]);
     return L0S_OK;
 }
 

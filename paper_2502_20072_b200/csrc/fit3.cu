@@ -60,6 +60,16 @@ constexpr int NT3 = NW3 * 32;
 #ifndef L0S_PRUNE_ROWS
 #define L0S_PRUNE_ROWS 4
 #endif
+#ifndef L0S_DIVFREE
+#define L0S_DIVFREE 0
+#endif
+#ifndef L0S_WREL
+#define L0S_WREL 0
+#endif
+// DF: the first task slot's test is division-free, (K - theta) d - q < 0, one FMA and no MUFU;
+// only groups that survive it re-evaluate that slot with the reciprocal (as NT == 1 always does).
+// WREL: tile buffers are released per warp (mbarrier + last-arriver refill), no CTA barrier per tile.
+constexpr bool WREL = L0S_WREL;
 struct CfgT {
     int P, IB, MINB, UNROLL;
 };
@@ -138,6 +148,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_constant__ FitArgs a) {
     using C = Cfg<NT>;
     constexpr int P = C::P, IB = C::IB, TS = C::TS, BS = C::BS, KSPAN = C::KSPAN, R = C::R, KS = C::KS;
+    constexpr bool DF = L0S_DIVFREE && NT > 1 && !C::SLOT0 && (P % 2 == 0);
     extern __shared__ __align__(128) double sm[];
     __shared__ int s_unit;
     __shared__ int s_tord[NT];
@@ -146,9 +157,12 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
     static_assert(IB <= 32, "one warp loads a tile's row flags");
     __shared__ __align__(8) unsigned long long s_bar[2];  // TMA completion, one per tile buffer
     __shared__ __align__(8) unsigned long long s_hbar;    // TMA completion of the unit's hoist block
+    __shared__ unsigned s_rel[2];                           // WREL: warps done with the buffer's tile
+    unsigned long long n_ev = 0;                            // row-group task evaluations (warp-uniform)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t m = a.m, mp = a.mp;
     if (tid == 0) {
+        s_rel[0] = s_rel[1] = 0u;
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
         mbar_init(&s_hbar, 1);
@@ -203,14 +217,16 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
 
     // tiles per task (slot t holds task tord[t]), staged by TMA (one elected thread,
     // completion on s_bar[buf]): C[i, j-block] (IB x 32), C[i, k-span] (IB x KSPAN), (c_i, pad) (IB x 2)
-    auto load_tiles = [&](int buf, int ib0, int j0, int k0) {
-        if (warp == 0) {  // IB <= 32: the rows' iforce flags and whether any is set
+    // Issued by one whole warp (`by`): its lanes write the rows' iforce flags, its lane 0 the TMA.
+    auto load_tiles = [&](int buf, int ib0, int j0, int k0, int by = 0) {
+        if (warp == by) {  // IB <= 32: the rows' iforce flags and whether any is set
             const unsigned char fl = (lane < IB && ib0 + lane < m) ? a.iforce[ib0 + lane] : 0;
             if (lane < IB) s_force[buf][lane] = fl;
             const unsigned any = __ballot_sync(L0S_FULL, fl != 0);
             if (lane == 0) s_fany[buf] = any != 0u;
+            __syncwarp();  // the flags precede lane 0's arrive (release) on the tile's barrier
         }
-        if (tid == 0) {
+        if (warp == by && lane == 0) {
             double* base = sm + buf * BS;
             fence_proxy_async();
             mbar_expect_tx(&s_bar[buf], (unsigned)(BS * sizeof(double)));
@@ -323,12 +339,13 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
                 if (cjk != cjk || ck != ck || w0[t] != w0[t]) isnan_ = true;
             }
             sK(p) = kr;
-            Bm[p] = bm;
+            Bm[p] = fmax(bm, 1e-300);  // q = w^2 + Bm > 0: d <= 0 always reads as "below theta"
             if (j < k && k < m && !isnan_) valid |= 1u << p;
             if (isbad) bad |= 1u << p;
         }
         // Kq = (first slot's share - theta) * shrink for NT > 1 (the remaining slots are added as the
-        // rows survive), (total - theta) for NT == 1; forced = pairs whose whole bound is below theta
+        // rows survive; DF: unshrunk, the first slot's test is division-free), (total - theta) for
+        // NT == 1; forced = pairs whose whole bound is below theta
         double K0[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) K0[p] = Kq[p];
@@ -338,7 +355,7 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
             for (int p = 0; p < P; ++p) {
                 const double x = sK(p) - wc.theta;
                 if (!(x > 0.0)) forced |= 1u << p;
-                Kq[p] = (NT == 1) ? x : (K0[p] - wc.theta) * shrink;
+                Kq[p] = (NT == 1) ? x : (DF ? (K0[p] - wc.theta) : (K0[p] - wc.theta) * shrink);
             }
         };
         set_kq();
@@ -346,12 +363,13 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
 
         // ---------------- sweep i ----------------
         const int nib = (i_hi - i_lo + IB - 1) / IB;
+        if (WREL && nib > 1) load_tiles(1, i_lo + IB, j0, k0);
         for (int bi = 0; bi < nib; ++bi) {
             const int buf = bi & 1;
             const int ib0 = i_lo + bi * IB;
-            if (bi + 1 < nib) load_tiles(buf ^ 1, ib0 + IB, j0, k0);
+            if (!WREL && bi + 1 < nib) load_tiles(buf ^ 1, ib0 + IB, j0, k0);
             wait_tiles(buf);
-            __syncthreads();  // s_force of this tile
+            if (!WREL) __syncthreads();  // s_force of this tile (WREL: ordered by the tile's mbarrier)
             const double* T0 = sm + buf * BS;
             // a clean tile (warp-uniform): every row is below every lane's j and inside the unit,
             // and no row is iforce-flagged -- a row's pending bits are then just the sign bits
@@ -406,24 +424,67 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
                         acc[p] = fma(-q, fabs(rcp_sweep(d)), acc[p]);  // 1/|d|: d <= 0 drives acc down
                 }
             };
+            // DF: slot 0 of one row, division-free: sign bit of (K0 - theta) d - q for every pair
+            // (d <= 0 with K0 > theta: negative since q > 0 -- still alive, as in the NT == 1 form)
+            auto task_row_df = [&](unsigned& sg, int ii) {
+                const double* Tt = T0;
+                const double g0 = Tt[ii * 32 + lane];
+                const double ci = Tt[IB * (32 + KSPAN) + 2 * ii + (int)(m & 1)];
+                double gk[P];
+#pragma unroll
+                for (int p = 0; p < P; p += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(Tt + IB * 32 + ii * KSPAN + warp * P + p);
+                    gk[p] = v.x;
+                    gk[p + 1] = v.y;
+                }
+                const double D = fma(-g0, g0, 1.0);
+                const double V = fma(-g0, w0[0], ci);
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const double g1 = fma(-L10[p][0], g0, gk[p]);
+                    const double e1 = g1 * rd1[p][0];
+                    const double w = fma(-g1, s1[p][0], V);
+                    const double d = fma(-g1, e1, D);
+                    const double q = fma(w, w, Bm[p]);
+                    sg |= (unsigned)__double2hiint(fma(Kq[p], d, -q));
+                }
+            };
 #pragma unroll
             for (int pw = 0; pw < NPW; ++pw) {
                 unsigned word = 0u;
 #pragma unroll(C::UNROLL)
                 for (int ig = 0; ig < IPW; ig += R) {
                     double acc[R][P];
-#pragma unroll
-                    for (int r = 0; r < R; ++r) {
-#pragma unroll
-                        for (int p = 0; p < P; ++p) acc[r][p] = Kq[p];
-                        task_row(acc[r], 0, pw * IPW + ig + r);
-                    }
                     // Task pruning: every task's reference SSR is >= 0, so the slots swept so far
                     // already bound the pooled SSR from below.  Once no (row, lane, pair) of the
                     // group is below theta on them, the group is done (warp-uniform exit).
                     bool live = true;
+                    if constexpr (DF) {
+                        unsigned sg = 0u;
 #pragma unroll
-                    for (int t = 1; t < NT; ++t) {
+                        for (int r = 0; r < R; ++r) task_row_df(sg, pw * IPW + ig + r);
+                        ++n_ev;
+                        live = __any_sync(L0S_FULL, (int)sg < 0);
+                        if (live) {  // survivors: slot 0 again with the reciprocal, then the others
+#pragma unroll
+                            for (int r = 0; r < R; ++r) {
+#pragma unroll
+                                for (int p = 0; p < P; ++p) acc[r][p] = Kq[p] * shrink;
+                                task_row(acc[r], 0, pw * IPW + ig + r);
+                            }
+                            ++n_ev;
+                        }
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+#pragma unroll
+                            for (int p = 0; p < P; ++p) acc[r][p] = Kq[p];
+                            task_row(acc[r], 0, pw * IPW + ig + r);
+                        }
+                        ++n_ev;
+                    }
+#pragma unroll
+                    for (int t = 1; t < NT && live; ++t) {
                         // sign bits OR-ed as integers (acc < 0 or -0: still alive; cheaper than
                         // predicate chains, which the compiler turns into an fmin reduction)
                         unsigned sgn = 0u;
@@ -449,6 +510,7 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
                             for (int p = 0; p < P; ++p) acc[r][p] += kt[p];
                             task_row(acc[r], t, pw * IPW + ig + r);
                         }
+                        ++n_ev;
                     }
                     if (clean) {
                         unsigned bits = 0u;  // sign bits of the group, row-major (r * P + p)
@@ -498,9 +560,24 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
                     return eval_tuple3(a, i, j, k, lbv) == 3 ? 1 : 2;
                 },
                 set_kq);
-            __syncthreads();
+            if (WREL) {
+                // per-warp release instead of a CTA barrier: the last warp done with this buffer
+                // refills it with tile bi + 2 (a warp deep in its slow path delays only that load)
+                __syncwarp();
+                unsigned last = 0;
+                if (lane == 0) last = atomicAdd(&s_rel[buf], 1u) == NW3 - 1;
+                last = __shfl_sync(L0S_FULL, last, 0);
+                if (last) {
+                    if (lane == 0) s_rel[buf] = 0u;
+                    if (bi + 2 < nib) load_tiles(buf, ib0 + 2 * IB, j0, k0, warp);
+                }
+            } else {
+                __syncthreads();
+            }
         }
+        if (WREL) __syncthreads();  // the unit's tiles are consumed before the next unit's loads
     }
+    if (lane == 0 && a.n_eval) atomicAdd(a.n_eval, n_ev * (unsigned long long)(R * P * 32));
     flush_warp(a, wc, blockIdx.x * NW3 + warp, lane);
 }
 

@@ -183,6 +183,7 @@ struct FitArgs {
     int64_t* coll_rank;
     unsigned long long* coll_cnt;
     int64_t coll_cap;
+    unsigned long long* n_eval;  // out (optional): task-tuple evaluations of the sweep (executed work)
 };
 int fit3_launch(const FitArgs& a, int nsm, cudaStream_t st);  // returns grid size (warp slots / 8)
 int fit3_grid(int T, int nsm);                                // grid fit3_launch will use

@@ -21,8 +21,10 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
-    "hoist_tma": ("L0S_HOIST_TMA=1",),
-    "hoist_l2": ("L0S_HOIST_TMA=0",),
+    "base": ("L0S_DIVFREE=0", "L0S_WREL=0"),
+    "wrel": ("L0S_DIVFREE=0", "L0S_WREL=1"),
+    "df": ("L0S_DIVFREE=1", "L0S_WREL=0"),
+    "df_wrel": ("L0S_DIVFREE=1", "L0S_WREL=1"),
 }
 
 
@@ -43,16 +45,20 @@ def time_one(steps: int = 5):
     from paper_2502_20072_b200 import _lib
     from paper_2502_20072_b200.search import _partition
 
-    v, y, slices = bench.make_c3()
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import scale_cases
+
+    v, y, slices = scale_cases.c3(os.environ.get("L0S_TUNE_Y", "planted"))
     perm, bounds, _ = _partition(bench.S, slices)
     eng = _lib.engine(0)
     eng.stage(v, y, perm, bounds, "fp64")
     res = []
     for _ in range(steps + 2):
         sc, rk, coef, ssr, st = eng.search(3, 10, 0, 2**62, "fast")
-        res.append((st.ms_fit, st.ms_total, st.n_candidates))
+        res.append((st.ms_fit, st.ms_total, st.n_candidates, st.n_eval, st.n_rescan))
     fit = sorted(r[0] for r in res[2:])
     print(json.dumps({"fit_ms_min": fit[0], "fit_ms_med": fit[len(fit) // 2], "total_ms": res[-1][1],
+                      "n_eval": res[-1][3], "n_cand": res[-1][2], "n_rescan": res[-1][4],
                       "ranks": rk.tolist(), "scores": [float(x) for x in sc]}))
 
 
