@@ -47,6 +47,10 @@ sys.path.insert(0, ROOT)
 
 M, S, T, N_DIM = 2000, 10000, 4, 3
 F_TASK = {2: 29, 3: 54, 4: 90}
+# fp64 flops of one (tuple, task) bound evaluation in the sweep (fit3.cu): g1, w, d, q and the
+# accumulate are FMAs (2 flops each), e1 a multiply (1), and the row's D and V (2 FMAs) are shared
+# by the P = 4 pairs of a thread (1 flop per evaluation) -> 5*2 + 1 + 1 = 12
+FLOP_PER_EVAL = 12
 METRIC = "l0 tuples fitted/sec at dim 3 (1/2/4/8 B200, % FP64 roofline) vs CPU ref"
 
 
@@ -115,26 +119,92 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def gram_roofline(eng, gram_ms, gram_tf, fp64_peak):
-    """Secondary roofline: the Gram.  INT8 path (Ozaki digits on tcgen05): physical int8 ops
-    (10 digit-pair GEMMs over the 128 x 64 upper-triangle tiles, K padded to 64) against the
-    dense INT8 tensor peak; DMMA path: fp64 flops against the FP64 peak."""
+def gram_roofline(eng, gram_ms):
+    """Secondary roofline: the INT8 Ozaki Gram (k_oz_gemm, tcgen05): the int8 ops its tiles issue
+    (10 digit-pair GEMMs over the 128 x 128 upper-triangle tiles, K padded to 64) against the
+    dense INT8 datasheet peak (MEASURED_PEAKS.json measures bf16 only)."""
     if not gram_ms:
         return None
     _, ozaki = eng.stage_info()
-    if ozaki:
-        R = -(-(M + 34) // 128) * 128
-        nbr, nbc = R // 128, R // 64
-        tiles = T * (nbr * nbc - nbr * (nbr - 1))
-        K = -(-(S // T) // 64) * 64
-        ops = tiles * 128 * 64 * 2 * K * 10
-        achieved = ops / (gram_ms * 1e-3) / 1e12
-        return {"bound": "int8 tensor (tcgen05.mma kind::i8, TMEM)", "kernel": "k_oz_split + k_oz_gemm + k_oz_eta",
-                "achieved": achieved, "peak": 4500.0, "unit": "TOPS", "frac": achieved / 4500.0,
-                "peak_source": "B200 dense INT8 datasheet (4.5 POPS)", "ms": gram_ms,
-                "fp64_equivalent_tflops": gram_tf, "fp64_equivalent_frac": gram_tf / fp64_peak}
-    return {"bound": "fp64 tensor (DMMA.8x8x4)", "kernel": "k_gram", "achieved": gram_tf, "peak": fp64_peak,
-            "unit": "TFLOP/s", "frac": gram_tf / fp64_peak, "ms": gram_ms, "flops": M * (M + 3) * S}
+    if not ozaki:
+        return {"kernel": "k_gram (DMMA)", "ms": gram_ms}
+    R = -(-(M + 34) // 128) * 128
+    nb = R // 128
+    tiles = T * nb * (nb + 1) // 2
+    K = -(-(S // T) // 64) * 64
+    ops = tiles * 128 * 128 * 2 * K * 10
+    achieved = ops / (gram_ms * 1e-3) / 1e12
+    return {"bound": "int8 tensor (tcgen05.mma kind::i8, TMEM)", "kernel": "k_oz_gemm + k_oz_eta",
+            "achieved": achieved, "peak": 4500.0, "unit": "TOPS", "frac": achieved / 4500.0,
+            "peak_source": "B200 dense INT8 datasheet (4.5 POPS)", "ms": gram_ms}
+
+
+def _hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def stage_roofline(stage_ms):
+    """HBM rooflines of the two staging passes (device-resident inputs, l0s_stage_timings):
+    gather reads the (m, s) values and writes the task-ordered copy (16 B per element, SURVEY 8(d)'s
+    staging bytes are 16 m s + 8 s for both passes together); normalize reads that copy and writes
+    the unit-norm rows Z (8 B) and their four INT8 digit planes (4 B): 20 B per element."""
+    if not stage_ms or not stage_ms.get("gather"):
+        return None
+    peak, src = _hbm_peak()
+    out = {"peak": peak, "unit": "GB/s", "peak_source": src}
+    for name, per in (("gather", 16), ("normalize", 20)):
+        ms = stage_ms[name]
+        gbs = per * M * S / (ms * 1e-3) / 1e9
+        out[name] = {"ms": ms, "bytes": per * M * S, "achieved": gbs, "frac": gbs / peak}
+    out["flags_ms"] = stage_ms["flags"]
+    return out
+
+
+def profile_figures():
+    """FP64-pipe fraction and DRAM bytes of k_fit3<4> from the ncu capture committed for this
+    code (profiles/fit3_profile.json, written by tools/profile.sh together with the commit it
+    profiled); (None, None, None) when absent."""
+    path = os.path.join(ROOT, "profiles", "fit3_profile.json")
+    try:
+        pj = json.load(open(path))
+        return pj.get("dram_bytes_per_launch"), pj.get("fp64_pipe_active_frac"), \
+            {"file": "profiles/fit3_profile.json", "commit": pj.get("commit"), "capture": pj.get("capture")}
+    except Exception:
+        return None, None, None
+
+
+def random_y_line(eng, vd, pd, bounds, args, local):
+    """C3 with y ~ N(0,1) (tests/scale_cases.py): the same device step, timed the same way."""
+    import torch
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import scale_cases
+
+    _, yr, _ = scale_cases.c3("random")
+    yd = torch.from_numpy(yr).to(f"cuda:{local}")
+    torch.cuda.synchronize()
+    ptrs = (vd.data_ptr(), yd.data_ptr(), pd.data_ptr())
+    total = comb(M, N_DIM)
+    for _ in range(args.warmup):
+        eng.stage((M, S), None, None, bounds, "fp64", device_ptrs=ptrs)
+        eng.search(N_DIM, 10, 0, total, "fast")
+    ms, fit, ev = [], [], []
+    for _ in range(args.steps):
+        eng.stage((M, S), None, None, bounds, "fp64", device_ptrs=ptrs)
+        sc, rk, _, _, st = eng.search(N_DIM, 10, 0, total, "fast")
+        ms.append(st.ms_gram + st.ms_total)
+        fit.append(st.ms_fit / max(1, st.n_fit_launches))
+        ev.append(st.n_eval / max(1, st.n_fit_launches))
+    peak = eng.fp64_peak()
+    f = statistics.mean(fit)
+    ach = statistics.mean(ev) * FLOP_PER_EVAL / (f * 1e-3) / 1e12
+    return {"value": total * args.steps / (sum(ms) * 1e-3), "unit": "tuples/s", "ms_per_step": sum(ms) / args.steps,
+            "fit_ms": f, "evals_per_tuple": statistics.mean(ev) / total, "fit_achieved_tflops": ach,
+            "fit_frac": ach / peak, "certified": int(st.certified), "n_rescan": int(st.n_rescan),
+            "data": "tests/scale_cases.py c3('random'): the bench's features, y ~ N(0,1)"}
 
 
 def dist_setup():
@@ -313,7 +383,7 @@ def main():
     for _ in range(args.warmup):
         device_step()
     barrier()
-    ms_steps, fit_ms, gram_ms, launches = [], [], [], 0
+    ms_steps, fit_ms, gram_ms, eval_counts, launches = [], [], [], [], 0
     # (gather + normalize) for the property row and for the features, the INT8 Gram (k_oz_gemm,
     # k_oz_eta), unit diagonal, 5 feature-flag kernels
     stage_launches = 12
@@ -324,6 +394,8 @@ def main():
             ms_steps.append(st.ms_gram + st.ms_total)
             gram_ms.append(st.ms_gram_kernel)
             fit_ms.append(st.ms_fit / max(1, st.n_fit_launches))
+            eval_counts.append(st.n_eval / max(1, st.n_fit_launches))
+            stage_ms = eng.stage_timings()
             launches += int(st.n_launches) + stage_launches
         barrier()
         wall = time.perf_counter() - t_wall
@@ -349,9 +421,12 @@ def main():
         best_rank = int(rk[0]) if len(rk) else None
     value = total * args.steps / (dev_ms * 1e-3)
 
-    # ---- end to end through the public API on pinned host buffers ----
-    vh = torch.from_numpy(v).pin_memory().numpy()
-    yh = torch.from_numpy(y).pin_memory().numpy()
+    # ---- the same search with y ~ N(0,1): dense near-ties, little task pruning (no headline) ----
+    random_y = random_y_line(eng, vd, pd, bounds, args, local) if world == 1 else None
+
+    # ---- end to end through the public API from plain numpy arrays (pageable host memory, what
+    # the pipeline passes, pipeline.py:219-229): H2D of the 160 MB matrix inside the timed region ----
+    vh, yh = v, y
     cfg = L0Config(dimension=N_DIM)
     e2e_ms = []
     if world > 1:
@@ -388,20 +463,15 @@ def main():
         return
 
     peak = eng.fp64_peak()
-    flops_per_launch = (total // world) * T * F_TASK[N_DIM]  # rank 0's part: ~1/world of the tuples
     fit_avg = statistics.mean(fit_ms)
-    achieved = flops_per_launch / (fit_avg * 1e-3) / 1e12
-    # secondary roofline: the Gram on the FP64 tensor path (DMMA), F_gram = m (m + 3) s
+    # executed work: the sweep counts its (tuple, task) bound evaluations (l0s_stats.n_eval); each is
+    # FLOP_PER_EVAL fp64 flops (module docstring); the algorithmic count of SURVEY 8(d) (216 per
+    # tuple at T = 4, a full normal-equations solve per task) is reported beside it as a search rate
+    evals = statistics.mean(eval_counts)
+    achieved = evals * FLOP_PER_EVAL / (fit_avg * 1e-3) / 1e12
+    algorithmic = (total // world) * T * F_TASK[N_DIM] / (fit_avg * 1e-3) / 1e12
     gram_avg = statistics.mean(gram_ms) if gram_ms and min(gram_ms) > 0 else None
-    gram_tf = (M * (M + 3) * S) / (gram_avg * 1e-3) / 1e12 if gram_avg else None
-    prof = os.path.join(ROOT, "profiles", "fit3_traffic.json")
-    traffic, pipe = None, None
-    if os.path.exists(prof):
-        try:
-            pj = json.load(open(prof))
-            traffic, pipe = pj.get("dram_bytes_per_launch"), pj.get("fp64_pipe_active_frac")
-        except Exception:
-            traffic = None
+    traffic, pipe, prof_src = profile_figures()
     line = {
         "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "strong",
@@ -411,18 +481,23 @@ def main():
                    "l2": "inputs (160 MB) and Gram (128 MB) exceed the 126 MB L2"},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_fit3<4>", "flops_per_tuple": T * F_TASK[N_DIM],
-                     "peak_source": "measured DFMA microbenchmark (l0s_fp64_peak); datasheet 37 TF/s",
-                     "physical_fp64_pipe_frac": pipe,
-                     "note": "achieved counts SURVEY 8(d)'s normal-equations flops per tuple (216 at T=4) for every "
-                             "tuple; the kernel hoists the (j,k) LDL^T out of the i sweep (~6.5 FP64 ops per "
-                             "task-tuple) and prunes a row group after its first task once that task alone bounds "
-                             "the pooled SSR above the threshold, so the algorithmic frac exceeds 1; the FP64 pipe "
-                             "is physical_fp64_pipe_frac busy (ncu, profiles/)"},
-        "roofline_gram": gram_roofline(eng, gram_avg, gram_tf, peak),
+                     "kernel": "k_fit3<4>", "work": f"{evals:.4g} (tuple, task) bound evaluations per launch "
+                                                   f"x {FLOP_PER_EVAL} fp64 flops (counted on the device)",
+                     "peak_source": "FP64 DFMA microbenchmark measured in this run (l0s_fp64_peak; "
+                                    "MEASURED_PEAKS.json has no FP64 entry); datasheet 37 TF/s",
+                     "physical_fp64_pipe_frac": pipe, "profile": prof_src,
+                     "search_rate_algorithmic_tflops": algorithmic,
+                     "note": "search_rate_algorithmic_tflops = SURVEY 8(d)'s normal-equations flops (216 per tuple "
+                             "at T=4) for every tuple / fit time: a search rate, not work done -- the sweep hoists "
+                             "the (j,k) block and prunes row groups after their first task (evaluations per tuple "
+                             f"{evals / (total // world):.3f} of {T})"},
+        "roofline_gram": gram_roofline(eng, gram_avg),
+        "roofline_stage": stage_roofline(stage_ms),
+        "random_y": random_y,
         "e2e": {"value": e2e_value, "unit": "tuples/s", "h2d_bytes_per_step": int(v.nbytes + y.nbytes + perm.nbytes
                                                                                   + bounds.nbytes),
-                "d2h_bytes_per_step": int(10 * (8 + 8 + T * (N_DIM + 1) * 8 + T * 8))},
+                "d2h_bytes_per_step": int(10 * (8 + 8 + T * (N_DIM + 1) * 8 + T * 8)),
+                "host_memory": "pageable (plain numpy arrays, as the pipeline passes them)"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "detail": {"fit_ms": fit_avg, "stage_gram_ms": st.ms_gram, "search_ms": st.ms_total,

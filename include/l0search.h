@@ -252,6 +252,11 @@ int l0s_stage_info(l0s_ctx *ctx, double *eta_out, int *ozaki_out);
  * flags]; zeros after a chunked host stage. */
 int l0s_stage_timings(l0s_ctx *ctx, double *out_ms);
 
+/* Diagnostics: the device QR screen (warp TSQR) of explicit tuples: pooled score sum_t ssr_t / s
+ * and the smallest rank-rule ratio min_j |R_jj| / max_j |R_jj| over the tasks. */
+int l0s_qr_tuples(l0s_ctx *ctx, int n, const int64_t *tuples, int64_t count, double *out_score,
+                  double *out_ratio);
+
 /* Copy of the staged normalized Gram of one task ((m+1) x (m+1), last row/col = y). */
 int l0s_get_gram(l0s_ctx *ctx, int task, double *out);
 

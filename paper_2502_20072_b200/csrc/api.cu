@@ -150,8 +150,10 @@ struct l0s_ctx {
     std::vector<int4> units_h;
     int64_t units_key[7] = {-1, -1, -1, -1, -1, -1, -1};
     int part = 0, nparts = 1;  // l0s_search_part: this context screens units u with u % nparts == part
+    HostStager* stager = nullptr;  // pinned ring for pageable host inputs (hostcopy.cu), on first use
 
     ~l0s_ctx() {
+        if (stager) host_stager_destroy(stager);
         DBuf* all[] = {&in_values, &in_y, &in_perm, &bounds_d, &zoff_d, &Xp, &yp, &Z, &G, &qf, &un2, &yyu, &rowsd,
                        &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &umin, &binom, &units, &ucount, &n_eval, &theta_g, &hist, &seedbuf, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
                        &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
@@ -510,6 +512,16 @@ static cudaError_t copy_rows(l0s_ctx* c, const double* values, const double* con
                              int64_t dst_row, cudaStream_t st) {
     const int64_t s = c->s;
     double* dst = c->in_values.as<double>() + dst_row * s;
+    // pageable sources (plain numpy arrays, the pipeline's real input) stream through the pinned
+    // ring with parallel host copies (hostcopy.cu); pinned ones go straight to the copy engine
+    const double* probe = rows ? rows[r0] : values + r0 * s;
+    if (r1 > r0 && (size_t)(r1 - r0) * s * sizeof(double) >= ((size_t)1 << 20) && !host_is_pinned(probe)) {
+        if (!c->stager) c->stager = host_stager_create();
+        if (c->stager) {
+            auto row = [&](int64_t r) -> const void* { return rows ? rows[r0 + r] : values + (r0 + r) * s; };
+            return host_stager_copy_rows(c->stager, dst, row, r1 - r0, sizeof(double) * s, st);
+        }
+    }
     if (!rows) return cudaMemcpyAsync(dst, values + r0 * s, sizeof(double) * (r1 - r0) * s, cudaMemcpyHostToDevice, st);
     for (int64_t r = r0; r < r1;) {
         int64_t e = r + 1;  // rows adjacent in host memory travel as one copy
@@ -586,20 +598,18 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
     cudaEventRecord(c->cev[l0s_ctx::kChunks], c->st);
     cudaStreamWaitEvent(c->cst, c->cev[l0s_ctx::kChunks], 0);
     int k = 0;
-    for (int64_t r0 = 0; r0 < m; r0 += R, ++k) {
-        const int64_t r1 = std::min(m, r0 + R);
-        CK(copy_rows(c, values, rows, r0, r1, r0, c->cst));
-        cudaEventRecord(c->cev[k], c->cst);
-    }
-    k = 0;
     int oz_done = 0;  // INT8 Gram: column blocks (64 wide) already launched
     if (ozaki) {
         cudaEventRecord(c->ev[2], c->st);
         c->gram_timed = true;
         c->gram_ozaki = true;
     }
+    // chunk k's copy is issued, then its compute is queued behind it: from pageable memory the
+    // host is busy copying chunk k + 1 into the pinned ring while the device stages chunk k
     for (int64_t r0 = 0; r0 < m; r0 += R, ++k) {
         const int64_t r1 = std::min(m, r0 + R);
+        CK(copy_rows(c, values, rows, r0, r1, r0, c->cst));
+        cudaEventRecord(c->cev[k], c->cst);
         cudaStreamWaitEvent(c->st, c->cev[k], 0);
         rows_to_z(r0, r1);
         if (gram_cols) {
@@ -839,6 +849,46 @@ int l0s_screen_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, d
     return L0S_OK;
 }
 
+int l0s_qr_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, double* out_score, double* out_ratio) {
+    if (!c || !c->staged) return fail(L0S_ESTATE, "l0s_stage must be called first");
+    if (n < 1 || n > 6) return fail(L0S_EINVAL, "the QR screen takes n in [1, 6]");
+    if (count <= 0) return L0S_OK;
+    CK(cudaSetDevice(c->dev));
+    int rc = ensure_binom(c, n);
+    if (rc) return rc;
+    std::vector<int64_t> rk((size_t)count);
+    for (int64_t i = 0; i < count; ++i) {
+        rc = l0s_rank(tuples + i * n, c->m, n, &rk[(size_t)i]);
+        if (rc) return rc;
+    }
+    CK(c->ex_ranks.ensure(sizeof(int64_t) * count));
+    CK(c->qr_ssr.ensure(sizeof(double) * count * c->T));
+    CK(c->qr_ratio.ensure(sizeof(double) * count * c->T));
+    CK(c->qr_score.ensure(sizeof(double) * count));
+    CK(c->qr_minr.ensure(sizeof(double) * count));
+    CK(cudaMemcpyAsync(c->ex_ranks.p, rk.data(), sizeof(int64_t) * count, cudaMemcpyHostToDevice, c->st));
+    QrArgs q{};
+    q.Xp = c->Xp.as<double>();
+    q.yp = c->yp.as<double>();
+    q.bounds = c->bounds_d.as<int64_t>();
+    q.T = c->T;
+    q.m = c->m;
+    q.s = c->s;
+    q.n = n;
+    q.ranks = c->ex_ranks.as<int64_t>();
+    q.binom = c->binom.as<int64_t>();
+    q.ssr = c->qr_ssr.as<double>();
+    q.ratio = c->qr_ratio.as<double>();
+    q.score = c->qr_score.as<double>();
+    q.min_ratio = c->qr_minr.as<double>();
+    launch_qr_screen(q, count, c->st, nullptr);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out_score, c->qr_score.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(out_ratio, c->qr_minr.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return L0S_OK;
+}
+
 int l0s_get_gram(l0s_ctx* c, int task, double* out) {
     if (!c || !c->staged) return fail(L0S_ESTATE, "l0s_stage must be called first");
     if (task < 0 || task >= c->T) return fail(L0S_EINVAL, "task out of range");
@@ -1011,7 +1061,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
                : n == 3 ? fit3_launch(fa, c->nsm, c->st)
                         : fit4_launch(fa, c->nsm, c->st);
     };
-    const int slots = grid * (n == 3 ? fit3_slots_per_cta() : fit_slots_per_cta());
+    const int slots = grid * (n == 3 ? fit3_slots_per_cta(c->T) : fit_slots_per_cta());
     const int64_t ill_cap = (int64_t)1 << 26;  // 512 MB of ranks; overflow is reported, never dropped
     CK(c->ucount.ensure(sizeof(int) * 4));
     CK(c->n_eval.ensure(sizeof(unsigned long long)));

@@ -200,7 +200,7 @@ int fit2_launch(const FitArgs& a, int nsm, cudaStream_t st) {
         case 6: return launch2<6>(a, nsm, st);
         case 7: return launch2<7>(a, nsm, st);
         case 8: return launch2<8>(a, nsm, st);
-        default: return -1;
+        default: return a.T > 8 ? launch2<8>(a, nsm, st) : -1;  // T > 8: the first 8 tasks bound the sweep
     }
 }
 
@@ -214,7 +214,7 @@ int fit2_grid(int T, int nsm) {
         case 6: return grid2<6>(nsm);
         case 7: return grid2<7>(nsm);
         case 8: return grid2<8>(nsm);
-        default: return -1;
+        default: return T > 8 ? grid2<8>(nsm) : -1;
     }
 }
 

@@ -36,7 +36,7 @@ using namespace fit;
 
 namespace {
 
-// (P, IB, MINB, UNROLL) for 3-4 tasks; overridable (-DL0S_C34_P=... etc.) for tuning builds
+// (P, IB, MINB, UNROLL, NW) for 3-4 tasks; overridable (-DL0S_C34_P=... etc.) for tuning builds
 #ifndef L0S_C34_P
 #define L0S_C34_P 4
 #endif
@@ -49,11 +49,12 @@ namespace {
 #ifndef L0S_C34_UNROLL
 #define L0S_C34_UNROLL 1
 #endif
-#ifndef L0S_FIT3_NW
-#define L0S_FIT3_NW 8
+#ifndef L0S_C34_NW
+#define L0S_C34_NW 8
 #endif
-constexpr int NW3 = L0S_FIT3_NW;  // warps per CTA of the dim-3 sweep (k-span = NW3 x P)
-constexpr int NT3 = NW3 * 32;
+#ifndef L0S_C34_NBUF
+#define L0S_C34_NBUF 2
+#endif
 #ifndef L0S_FIT_SLOT0
 #define L0S_FIT_SLOT0 0
 #endif
@@ -71,30 +72,38 @@ constexpr int NT3 = NW3 * 32;
 // WREL: tile buffers are released per warp (mbarrier + last-arriver refill), no CTA barrier per tile.
 constexpr bool WREL = L0S_WREL;
 struct CfgT {
-    int P, IB, MINB, UNROLL;
+    int P, IB, MINB, UNROLL, NW, NBUF;
 };
-constexpr CfgT kCfg34{L0S_C34_P, L0S_C34_IB, L0S_C34_MINB, L0S_C34_UNROLL};
-constexpr CfgT kCfg12{4, 32, 2, 2};
-constexpr CfgT kCfg58{2, 16, 1, 1};
-// Per task count: P = (j,k) pairs per thread, IB = rows per i-tile, MINB = CTAs per SM.
+// 3-4 tasks: 16 warps of 2 pairs (<= 128 registers: the pair constants of every task stay in
+// registers and the compiler can interleave the rows; 8 warps of 4 pairs ran at 255 registers
+// with the FP64 pipe 34 % busy)
+constexpr CfgT kCfg34{L0S_C34_P, L0S_C34_IB, L0S_C34_MINB, L0S_C34_UNROLL, L0S_C34_NW, L0S_C34_NBUF};
+constexpr CfgT kCfg12{4, 32, 2, 2, 8, 2};
+constexpr CfgT kCfg58{2, 16, 1, 1, 8, 2};
+// Per task count: P = (j,k) pairs per thread, IB = rows per i-tile, MINB = CTAs per SM,
+// NW = warps per CTA (k-span = NW x P; the unit table follows it, fit3_kspan).
 template <int NT>
 struct Cfg {
     static constexpr CfgT c = (NT <= 2) ? kCfg12 : (NT <= 4 ? kCfg34 : kCfg58);
     static constexpr int P = c.P;
     static constexpr int IB = c.IB;
-    static constexpr int KSPAN = NW3 * P;
+    static constexpr int NW = c.NW;
+    static constexpr int NTH = NW * 32;
+    static constexpr int KSPAN = NW * P;
     static constexpr int TS = IB * (32 + KSPAN + 2);  // C[i, j-block] | C[i, k-span] | (c_i, pad)
     // SLOT0: only the first task slot is staged (its rows feed every group); the other slots
     // are read from L2 by the few row groups that survive the first (task pruning)
     static constexpr bool SLOT0 = (NT > 1) && L0S_FIT_SLOT0;
     static constexpr int BS = SLOT0 ? TS : NT * TS;
+    // tile ring depth (WREL: warps may run NBUF - 1 tiles apart; without it two buffers)
+    static constexpr int NBUF = WREL ? c.NBUF : 2;
     static constexpr int MINB = c.MINB;
     static constexpr int UNROLL = c.UNROLL;  // rows of the i sweep in flight per thread
     // task pruning (NT > 1): rows per vote group, and per-thread smem slots for the
     // per-task constants (P x KS doubles: the total, then tasks 1..NT-1 for NT >= 3)
     static constexpr int R = (NT == 1) ? 1 : L0S_PRUNE_ROWS;
     static constexpr int KS = (NT >= 3) ? NT : 1;
-    static constexpr size_t smem_bytes = (size_t)2 * BS * 8 + (size_t)NW3 * CAP * 16 + (size_t)NT3 * P * KS * 8;
+    static constexpr size_t smem_bytes = (size_t)NBUF * BS * 8 + (size_t)NW * CAP * 16 + (size_t)NTH * P * KS * 8;
 };
 
 // Exact lower bound of one tuple (i < j < k) read straight from the Gram, with the
@@ -145,72 +154,92 @@ __device__ __noinline__ int eval_tuple3(const FitArgs& a, int64_t i, int64_t j, 
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_constant__ FitArgs a) {
+__global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __grid_constant__ FitArgs a) {
     using C = Cfg<NT>;
-    constexpr int P = C::P, IB = C::IB, TS = C::TS, BS = C::BS, KSPAN = C::KSPAN, R = C::R, KS = C::KS;
+    constexpr int NW3 = C::NW, NT3 = C::NTH;
+    constexpr int P = C::P, IB = C::IB, TS = C::TS, BS = C::BS, KSPAN = C::KSPAN, R = C::R, NB = C::NBUF;
     constexpr bool DF = L0S_DIVFREE && NT > 1 && !C::SLOT0 && (P % 2 == 0);
     extern __shared__ __align__(128) double sm[];
     __shared__ int s_unit;
     __shared__ int s_tord[NT];
-    __shared__ unsigned char s_force[2][IB];  // iforce flags of the staged rows
-    __shared__ int s_fany[2];                 // any of them set
+    __shared__ unsigned char s_force[NB][IB];  // iforce flags of the staged rows
+    __shared__ int s_fany[NB];                 // any of them set
     static_assert(IB <= 32, "one warp loads a tile's row flags");
-    __shared__ __align__(8) unsigned long long s_bar[2];  // TMA completion, one per tile buffer
-    __shared__ __align__(8) unsigned long long s_hbar;    // TMA completion of the unit's hoist block
-    __shared__ unsigned s_rel[2];                           // WREL: warps done with the buffer's tile
+    __shared__ __align__(8) unsigned long long s_bar[NB];  // TMA completion, one per tile buffer
+    __shared__ __align__(8) unsigned long long s_hbar;     // TMA completion of the unit's hoist block
+    __shared__ unsigned s_rel[NB];                           // WREL: warps done with the buffer's tile
+    __shared__ double s_th;                                 // the unit's shared threshold
     unsigned long long n_ev = 0;                            // row-group task evaluations (warp-uniform)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t m = a.m, mp = a.mp;
     if (tid == 0) {
-        s_rel[0] = s_rel[1] = 0u;
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
+        for (int b = 0; b < NB; ++b) {
+            s_rel[b] = 0u;
+            mbar_init(&s_bar[b], 1);
+        }
         mbar_init(&s_hbar, 1);
         mbar_fence_init();
         // sweep order of the tasks: largest |y_c|^2 first, so that the first task's share of the
-        // bound alone already exceeds the threshold for almost every row (task pruning below)
+        // bound alone already exceeds the threshold for almost every row (task pruning below);
+        // with more than NT tasks the slots take the NT largest (a subset bounds the pooled SSR)
         double y2[NT];
-        for (int t = 0; t < NT; ++t) {
-            y2[t] = a.G[(int64_t)t * mp * mp + m * mp + m];
-            s_tord[t] = t;
-        }
-        for (int x = 1; x < NT; ++x)
-            for (int z = x; z > 0 && y2[s_tord[z]] > y2[s_tord[z - 1]]; --z) {
+        int cnt = 0;
+        for (int t = 0; t < a.T; ++t) {
+            const double v = a.G[(int64_t)t * mp * mp + m * mp + m];
+            int z;
+            if (cnt < NT) {
+                z = cnt++;
+            } else if (v > y2[NT - 1]) {
+                z = NT - 1;
+            } else {
+                continue;
+            }
+            y2[z] = v;
+            s_tord[z] = t;
+            for (; z > 0 && y2[z] > y2[z - 1]; --z) {
+                const double w = y2[z];
+                y2[z] = y2[z - 1];
+                y2[z - 1] = w;
                 const int q = s_tord[z];
                 s_tord[z] = s_tord[z - 1];
                 s_tord[z - 1] = q;
             }
+        }
     }
     __syncthreads();
     // unit-independent per-task scalars of the hoist, in slot order, once per CTA (shared
     // memory instead of a global load chain per unit)
-    __shared__ double s_ts[4][NT];  // Y2, gamma, eta, |y|
+    __shared__ double s_ts[4][NT];  // Y2, gamma, eta, A0 = 4 gamma |y_c| |y| (task_bound's constant term)
     if (tid < NT) {
         const int tk = s_tord[tid];
-        s_ts[0][tid] = a.G[(int64_t)tk * mp * mp + m * mp + m];
-        s_ts[1][tid] = ref_gamma(a.rowsd[tk], 3, a.ref_fp32);
+        const double Y2 = a.G[(int64_t)tk * mp * mp + m * mp + m], gam = ref_gamma(a.rowsd[tk], 3, a.ref_fp32);
+        s_ts[0][tid] = Y2;
+        s_ts[1][tid] = gam;
         s_ts[2][tid] = a.eta[tk];
-        s_ts[3][tid] = a.ynorm[tk];
+        s_ts[3][tid] = 4.0 * gam * sqrt(Y2) * a.ynorm[tk];
     }
+    // the unit's hoist inputs besides C[k, j] (TMA block below), per task slot, staged by all
+    // threads with coalesced loads: c_j and max(rho_cap, rho_j) over the j-block, c_k and rho_k
+    // over the k-span (a per-pair global load chain stalled the hoist on the LSU queue)
+    __shared__ double s_hu[NT][4][32];
+    static_assert(KSPAN <= 32, "k-span staged in 32-wide rows");
     __syncthreads();
     const int* tord = s_tord;  // read where the hoist / tile loads need it (rare)
-    unsigned parity[2] = {0u, 0u}, hpar = 0u;
-    // The unit's hoist block goes through TMA into tile buffer 1 (idle until the sweep's first
-    // prefetch): per task slot C[k-span, j-block] (IB x 32, IB == KSPAN) and, when it fits, the
-    // property row's k-span c_k (a second box, first row used).
-    constexpr bool HC = 64 <= 34 + KSPAN;
-    constexpr int HS = (HC ? 2 : 1) * IB * 32;  // doubles per task slot
+    unsigned parity = 0u, hpar = 0u;  // full-barrier phase bit per tile buffer
+    // The unit's hoist block goes through TMA into tile buffers 1.. (idle until the sweep's first
+    // prefetch): per task slot C[k-span, j-block] (KSPAN x 32).
+    constexpr int HS = KSPAN * 32;  // doubles per task slot: C[k-span, j-block]
 #ifndef L0S_HOIST_TMA
 #define L0S_HOIST_TMA 1
 #endif
-    constexpr bool HT = L0S_HOIST_TMA && IB == KSPAN && NT * HS <= BS;  // else the hoist reads L2
+    constexpr bool HT = L0S_HOIST_TMA && NT * HS <= (NB - 1) * BS;  // else the hoist reads L2
     // per-thread constants, touched by the hoist, threshold updates and pruned rows:
     // sK[0][p] = sum_t (base_t - A_t) (NT >= 3: sK[t][p] = (base_t - A_t) * shrink, t >= 1)
     // (slot-major, thread-minor: conflict-free per-thread accesses)
-    double* sKb = sm + 2 * BS + 2 * NW3 * CAP + tid;
+    double* sKb = sm + NB * BS + 2 * NW3 * CAP + tid;
     auto sK = [&](int idx) -> double& { return sKb[idx * NT3]; };
     const double shrink = (NT == 1) ? 1.0 : (1.0 - 2.0 * kRcpRel);
-    WarpCands wc{sm + 2 * BS + warp * CAP, reinterpret_cast<int64_t*>(sm + 2 * BS + NW3 * CAP) + warp * CAP, 0,
+    WarpCands wc{sm + NB * BS + warp * CAP, reinterpret_cast<int64_t*>(sm + NB * BS + NW3 * CAP) + warp * CAP, 0,
                  a.collect ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g), 0};
     const int64_t* B2 = a.binom + 2 * (m + 1);
     const int64_t* B3 = a.binom + 3 * (m + 1);
@@ -242,8 +271,8 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
         }
     };
     auto wait_tiles = [&](int buf) {
-        mbar_wait(&s_bar[buf], parity[buf]);
-        parity[buf] ^= 1u;
+        mbar_wait(&s_bar[buf], (parity >> buf) & 1u);
+        parity ^= 1u << buf;
     };
 
     for (;;) {
@@ -257,25 +286,38 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
         const int j = j0 + lane;
         const int kbase = k0 + warp * P;
         const int i_lo = U.z, i_hi = U.w;
-        double* Hb = sm + BS;  // tile buffer 1
+        double* Hb = sm + BS;  // tile buffers 1..
         if (HT && tid == 0) {
             fence_proxy_async();  // the previous unit's reads of buffer 1 precede these writes
             mbar_expect_tx(&s_hbar, (unsigned)(NT * HS * sizeof(double)));
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-                tma_load_2d(Hb + t * HS, &a.tmJ, j0, (int)(tord[t] * mp) + k0, &s_hbar);
-                if (HC) tma_load_2d(Hb + t * HS + IB * 32, &a.tmJ, k0, (int)(tord[t] * mp + m), &s_hbar);
+                tma_load_2d(Hb + t * HS, &a.tmH, j0, (int)(tord[t] * mp) + k0, &s_hbar);
             }
         }
         load_tiles(0, i_lo, j0, k0);
-        if (!a.collect) {
-            // shared threshold: the global bound histogram and the other warps' lists
-            double th = fmin(hist_theta(a, lane), ord_dec(*(volatile unsigned long long*)a.theta_g));
-            if (th < wc.theta) {
-                wc.theta = th;
-                if (lane == 0) atomicMin(a.theta_g, ord_enc(th));
+        for (int x = tid; x < NT * 128; x += NT3) {
+            const int t = x >> 7, w = (x >> 5) & 3, l = x & 31;
+            const int tk = tord[t];
+            const int f = (w < 2 ? j0 : k0) + l, ff = f < m ? f : (int)m - 1;
+            double v;
+            if (w == 0 || w == 2)
+                v = a.G[(int64_t)tk * mp * mp + m * mp + f];  // c_j / c_k (columns < mp: padded, finite)
+            else
+                v = w == 1 ? fmax(a.rho_cap[tk], a.rho[(int64_t)tk * m + ff]) : a.rho[(int64_t)tk * m + ff];
+            s_hu[t][w][l] = v;
+        }
+        if (!a.collect && warp == NW3 - 1) {
+            // shared threshold: the global bound histogram and the other warps' lists (one warp
+            // per CTA reads them; the histogram scan is a long load chain)
+            const double th = fmin(hist_theta(a, lane), ord_dec(*(volatile unsigned long long*)a.theta_g));
+            if (lane == 0) {
+                s_th = th;
+                atomicMin(a.theta_g, ord_enc(th));
             }
         }
+        __syncthreads();
+        if (!a.collect && s_th < wc.theta) wc.theta = s_th;
 
         // ---------------- hoist: (j, k_p) state per task (slot order) ----------------
         // L10 = C_jk, rd1 = 1/(1 - C_jk^2), s1 = rd1 (c_k - C_jk c_j); the bound's B_t/d term
@@ -283,38 +325,23 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
         double L10[P][NT], rd1[P][NT], s1[P][NT], w0[NT], Kq[P], Bm[P];
         double K1r[P];  // NT == 2: task slot 1's (base - A) * shrink in registers
         unsigned valid = 0, bad = 0, forced = 0;
-        const int jj = j < m ? j : (int)m - 1;
         if (HT) {
             mbar_wait(&s_hbar, hpar);
             hpar ^= 1u;
         }
-        // per-task scalars of this unit, loaded once (live during the hoist only)
-        double Y2v[NT], gamv[NT], etav[NT], ynv[NT], rjv[NT];
-        const double* Gs[NT];
 #pragma unroll
-        for (int t = 0; t < NT; ++t) {
-            const int tk = tord[t];
-            Gs[t] = a.G + (int64_t)tk * mp * mp;
-            w0[t] = Gs[t][m * mp + j];
-            Y2v[t] = s_ts[0][t];
-            gamv[t] = s_ts[1][t];
-            etav[t] = s_ts[2][t];
-            ynv[t] = s_ts[3][t];
-            rjv[t] = fmax(a.rho_cap[tk], a.rho[(int64_t)tk * m + jj]);
-        }
+        for (int t = 0; t < NT; ++t) w0[t] = s_hu[t][0][lane];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             const int k = kbase + p;
-            const int kk = k < m ? k : (int)m - 1;
             double kr = 0.0, bm = 0.0;
             bool isbad = false, isnan_ = false;
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-                const int tk = tord[t];
-                const double* Gt = Gs[t];
-                const double Y2 = Y2v[t];
-                const double cjk = HT ? Hb[t * HS + (k - k0) * 32 + lane] : Gt[(int64_t)k * mp + j];
-                const double ck = (HT && HC) ? Hb[t * HS + IB * 32 + (k - k0)] : Gt[m * mp + k];
+                const double Y2 = s_ts[0][t];
+                const double cjk = HT ? Hb[t * HS + (k - k0) * 32 + lane]
+                                      : a.G[(int64_t)tord[t] * mp * mp + (int64_t)k * mp + j];
+                const double ck = s_hu[t][2][k - k0];
                 const double d1 = fma(-cjk, cjk, 1.0);
                 const double r1 = rcp_newton(d1);
                 const double v1 = fma(-cjk, w0[t], ck);
@@ -322,8 +349,8 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
                 const double trh = 2.0 * r1;
                 double At, Bt, vk;
                 // rho of the hoisted pair (the sweep feature's rho is covered by rho_cap or s_force)
-                const double rh = fmax(rjv[t], a.rho[(int64_t)tk * m + kk]);
-                task_bound(3, etav[t], gamv[t], rh, Y2, ynv[t], trh, At, Bt, vk);
+                const double rh = fmax(s_hu[t][1][lane], s_hu[t][3][k - k0]);
+                task_bound_a0(3, s_ts[2][t], s_ts[1][t], rh, Y2, s_ts[3][t], trh, At, Bt, vk);
                 L10[p][t] = cjk;
                 rd1[p][t] = r1;
                 s1[p][t] = v1 * r1;
@@ -363,9 +390,10 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
 
         // ---------------- sweep i ----------------
         const int nib = (i_hi - i_lo + IB - 1) / IB;
-        if (WREL && nib > 1) load_tiles(1, i_lo + IB, j0, k0);
+        if (WREL)
+            for (int b = 1; b < NB && b < nib; ++b) load_tiles(b, i_lo + b * IB, j0, k0);
         for (int bi = 0; bi < nib; ++bi) {
-            const int buf = bi & 1;
+            const int buf = WREL ? bi % NB : (bi & 1);
             const int ib0 = i_lo + bi * IB;
             if (!WREL && bi + 1 < nib) load_tiles(buf ^ 1, ib0 + IB, j0, k0);
             wait_tiles(buf);
@@ -569,7 +597,7 @@ __global__ void __launch_bounds__(NT3, Cfg<NT>::MINB) k_fit3(const __grid_consta
                 last = __shfl_sync(L0S_FULL, last, 0);
                 if (last) {
                     if (lane == 0) s_rel[buf] = 0u;
-                    if (bi + 2 < nib) load_tiles(buf, ib0 + 2 * IB, j0, k0, warp);
+                    if (bi + NB < nib) load_tiles(buf, ib0 + NB * IB, j0, k0, warp);
                 }
             } else {
                 __syncthreads();
@@ -605,15 +633,15 @@ int launch_nt(const FitArgs& a0, int nsm, cudaStream_t st) {
     FitArgs a = a0;
     const unsigned long long rows = (unsigned long long)a.T * a.mp, cols = (unsigned long long)a.mp;
     if (!make_tma_2d(&a.tmJ, a.G, cols, rows, 32, C::IB) || !make_tma_2d(&a.tmK, a.G, cols, rows, C::KSPAN, C::IB) ||
-        !make_tma_2d(&a.tmC, a.G, cols, rows, 2, C::IB))
+        !make_tma_2d(&a.tmC, a.G, cols, rows, 2, C::IB) || !make_tma_2d(&a.tmH, a.G, cols, rows, 32, C::KSPAN))
         return -1;
     cudaFuncSetAttribute(k_fit3<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, NT3, C::smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, C::NTH, C::smem_bytes);
     if (per_sm < 1) per_sm = 1;
     int grid = nsm * per_sm;
     if (!a.collect) seed_launch<3, 18>(k_seed_eval3, a, st);
-    k_fit3<NT><<<grid, NT3, C::smem_bytes, st>>>(a);
+    k_fit3<NT><<<grid, C::NTH, C::smem_bytes, st>>>(a);
     return grid;
 }
 
@@ -624,9 +652,14 @@ void launch_screen3(const FitArgs& a, const int64_t* tuples, int64_t count, doub
     if (count > 0) k_screen3<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(a, tuples, count, out_lb, out_flags);
 }
 
-int fit3_max_tasks() { return 8; }
+// More tasks than the sweep's 8 slots: the slots hold the 8 tasks of largest |y_c|^2, whose bound
+// terms alone bound the pooled SSR from below (every task's SSR is >= 0); the slow path, the
+// certificates and the exact refit take every task.
+int fit3_max_tasks() { return 1 << 16; }
 int fit_slots_per_cta() { return NW; }
-int fit3_slots_per_cta() { return NW3; }
+int fit3_slots_per_cta(int T) {
+    return T <= 2 ? Cfg<1>::NW : (T <= 4 ? Cfg<4>::NW : Cfg<8>::NW);
+}
 int fit3_kspan(int T) {
     switch (T) {
         case 1: return Cfg<1>::KSPAN;
@@ -642,12 +675,14 @@ int fit3_grid(int T, int nsm) {
 #define OCC(NT)                                                                                              \
     case NT:                                                                                                 \
         cudaFuncSetAttribute(k_fit3<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<NT>::smem_bytes); \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, NT3, Cfg<NT>::smem_bytes);       \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, Cfg<NT>::NTH, Cfg<NT>::smem_bytes); \
         break;
         OCC(1) OCC(2) OCC(3) OCC(4) OCC(5) OCC(6) OCC(7) OCC(8)
 #undef OCC
         default:
-            return -1;
+            if (T < 1) return -1;
+            cudaFuncSetAttribute(k_fit3<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<8>::smem_bytes);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<8>, Cfg<8>::NTH, Cfg<8>::smem_bytes);
     }
     return nsm * (per_sm < 1 ? 1 : per_sm);
 }
@@ -662,7 +697,7 @@ int fit3_launch(const FitArgs& a, int nsm, cudaStream_t st) {
         case 6: return launch_nt<6>(a, nsm, st);
         case 7: return launch_nt<7>(a, nsm, st);
         case 8: return launch_nt<8>(a, nsm, st);
-        default: return -1;
+        default: return a.T > 8 ? launch_nt<8>(a, nsm, st) : -1;  // T > 8: 8 tasks bound the sweep
     }
 }
 

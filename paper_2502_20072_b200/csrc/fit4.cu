@@ -189,7 +189,10 @@ __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs
                 kr += h.base - At;
                 bm = fmax(bm, Bt);
                 if (!(h.d1 > 0.0) || !(h.d2 > 0.0) || !(vk * (1.0 + 4.0 * h.tr3) <= FO_LIM)) isbad = true;
-                if (!(h.base == h.base) || !(h.L21 == h.L21)) isnan_ = true;
+                // dead features (NaN Gram rows) drop the pair; a NaN produced by a near-singular
+                // (j, k, l) block (d1 or d2 <= 0) is `bad` and goes to the exact kernel instead
+                const double raw = h.w0 + h.L10 + h.L20 + Gt[l * mp + k] + Gt[m * mp + k] + Gt[m * mp + l];
+                if (raw != raw) isnan_ = true;
             }
             sKraw[p] = kr;
             Bm[p] = bm;
@@ -347,7 +350,7 @@ int fit4_grid(int T, int nsm) {
         case 6: return occupancy4<6>(nsm);
         case 7: return occupancy4<7>(nsm);
         case 8: return occupancy4<8>(nsm);
-        default: return -1;
+        default: return T > 8 ? occupancy4<8>(nsm) : -1;
     }
 }
 
@@ -361,7 +364,7 @@ int fit4_launch(const FitArgs& a, int nsm, cudaStream_t st) {
         case 6: return launch4<6>(a, nsm, st);
         case 7: return launch4<7>(a, nsm, st);
         case 8: return launch4<8>(a, nsm, st);
-        default: return -1;
+        default: return a.T > 8 ? launch4<8>(a, nsm, st) : -1;  // T > 8: the first 8 tasks bound the sweep
     }
 }
 

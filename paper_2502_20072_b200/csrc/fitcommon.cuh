@@ -35,6 +35,15 @@ __device__ __forceinline__ void task_bound(int n, double eta, double gam, double
     B = n * K * Y2 * (1.0 + trh);
 }
 
+// The same with the pair-independent term precomputed: A0 = 4 gam |y_c| |y|.
+__device__ __forceinline__ void task_bound_a0(int n, double eta, double gam, double rho, double Y2, double A0,
+                                              double trh, double& A, double& B, double& vk) {
+    vk = eta + gam * rho;
+    const double K = 2.0 * vk;
+    A = A0 + K * Y2 * (1.0 + n * trh);
+    B = n * K * Y2 * (1.0 + trh);
+}
+
 // Householder QR columnwise backward-error constant for r rows, n features + intercept + rhs,
 // with the inner products' rounding bounded probabilistically: |error| <= lambda sqrt(r) u
 // with probability >= 1 - 2 exp(-lambda^2 (1-u)^2 / 2) per inner product (Higham & Mary,
@@ -166,9 +175,14 @@ __device__ __forceinline__ void hist_count(const FitArgs& a, WarpCands& wc, int 
 // Smallest histogram edge with >= kc counted bounds below it (+inf when fewer).
 __device__ __forceinline__ double hist_theta(const FitArgs& a, int lane) {
     constexpr int PER = HIST_BINS / 32;
+    static_assert(PER % 4 == 0, "each lane's bins load as uint4");
     const unsigned* h = a.hist + lane * PER;
     unsigned sum = 0;
-    for (int x = 0; x < PER; ++x) sum += __ldcg(h + x);
+#pragma unroll
+    for (int x = 0; x < PER; x += 4) {  // 16-byte loads: a quarter of the strided transactions
+        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(h + x));
+        sum += v.x + v.y + v.z + v.w;
+    }
     unsigned inc = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <vector>
 
 namespace l0s {
@@ -136,10 +137,19 @@ inline int hist_base_for(double top) {
 struct alignas(64) TmaDesc {
     unsigned long long opaque[16];
 };
+// ---- host -> device copies from pageable memory (hostcopy.cu) ----
+struct HostStager;
+HostStager* host_stager_create();  // nullptr when no pinned memory could be had
+void host_stager_destroy(HostStager* h);
+bool host_is_pinned(const void* p);
+cudaError_t host_stager_copy_rows(HostStager* h, void* dst, const std::function<const void*(int64_t)>& row,
+                                  int64_t nrows, size_t row_bytes, cudaStream_t st);
+
 struct FitArgs {
     TmaDesc tmJ;  // box: 32 columns (j-block) x IB rows
     TmaDesc tmK;  // box: KSPAN columns (k- or l-span) x IB rows
     TmaDesc tmC;  // box: 2 columns (one Gram column + its neighbour) x IB rows
+    TmaDesc tmH;  // box: 32 columns (j-block) x KSPAN rows (the unit's hoist block C[k-span, j-block])
     const double* G;         // [T][mp][mp] normalized Gram, y at index m
     const double* qf;        // [T][m]
     const double* un2;       // [T][m]
@@ -189,7 +199,7 @@ int fit3_launch(const FitArgs& a, int nsm, cudaStream_t st);  // returns grid si
 int fit3_grid(int T, int nsm);                                // grid fit3_launch will use
 int fit3_max_tasks();
 int fit_slots_per_cta();   // warp candidate slots per CTA (n = 2, 4)
-int fit3_slots_per_cta();  // the same for the n = 3 sweep
+int fit3_slots_per_cta(int T);  // the same for the n = 3 sweep (T tasks)
 int fit3_kspan(int T);
 std::vector<int4> fit3_units(int64_t m, int T, int64_t N_total, const std::vector<int64_t>& c2_prefix,
                              int64_t rank_lo, int64_t rank_hi, bool tunable = true);

@@ -1,5 +1,5 @@
 import os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
 import numpy as np
 import test_gpu_scale as t
@@ -11,9 +11,10 @@ c = t._stress_instance(k)
 orc.build()
 n = c["n"]
 want = orc.l0_search(c["v"], c["y"], c["slices"], n, c["keep"], c["precision"], threads=8)
-for mode in ("fast", "exact"):
+res = {}
+for mode in ("exact", "fast"):
     st = SearchStats()
-    got = l0_search(c["v"], c["y"], c["slices"], L0Config(dimension=n, n_models_store=c["keep"], precision=c["precision"]), stats=st, mode=mode)
+    got = res[mode] = l0_search(c["v"], c["y"], c["slices"], L0Config(dimension=n, n_models_store=c["keep"], precision=c["precision"]), stats=st, mode=mode)
     print(mode, {k2: v for k2, v in st.device.items() if k2.startswith("n_") or k2 in ("certified", "theta", "margin")})
     for i in range(max(len(got), len(want))):
         g = got[i] if i < len(got) else None
@@ -30,4 +31,5 @@ for w in miss:
     tup = np.array([w["indices"]], dtype=np.int64)
     ok, score, _, _ = eng.fit_tuples(tup)
     lb, fl = eng.screen_tuples(tup)
-    print("missing", w["indices"], "rank", rank_tuple(w["indices"], m, n), "ref", w["score"] * s, "dev", score[0] * s, "lb", lb[0], "flags", fl[0])
+    qs, qr = eng.qr_tuples(tup)
+    print("missing", w["indices"], "rank", rank_tuple(w["indices"], m, n), "ref", w["score"] * s, "dev", score[0] * s, "lb", lb[0], "flags", fl[0], "qr", qs[0], qr[0])

@@ -21,10 +21,10 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
-    "base": ("L0S_DIVFREE=0", "L0S_WREL=0"),
-    "wrel": ("L0S_DIVFREE=0", "L0S_WREL=1"),
-    "df": ("L0S_DIVFREE=1", "L0S_WREL=0"),
-    "df_wrel": ("L0S_DIVFREE=1", "L0S_WREL=1"),
+    "base": (),
+    "wrel3_ib24": ("L0S_WREL=1", "L0S_C34_NBUF=3", "L0S_C34_IB=24"),
+    "wrel4_ib16": ("L0S_WREL=1", "L0S_C34_NBUF=4", "L0S_C34_IB=16"),
+    "wrel8_ib8": ("L0S_WREL=1", "L0S_C34_NBUF=8", "L0S_C34_IB=8"),
 }
 
 
