@@ -271,6 +271,29 @@ int l0s_fp64_peak(l0s_ctx *ctx, double *out_tflops);
  * (the screen assumes <= 2^-17; tests/test_gpu_parity.py::test_rcp_fast_bound checks it). */
 int l0s_rcp_check(int64_t count, double *out_max_rel);
 
+/*
+ * Several devices in one process (the reference's in-process `workers`, search.py:258-304):
+ * one context per device (devices may repeat), one host thread per device.
+ *   l0s_group_stage  : device g uploads row block g of the inputs (values: (m, s) row-major, or
+ *                      rows: m host pointers, exactly one non-null; pageable or pinned), the
+ *                      blocks are exchanged device to device (cudaMemcpyPeerAsync), every device
+ *                      stages the whole problem (l0s_stage on its copy);
+ *   l0s_group_search : device g searches part g (l0s_search_part); the exact per-part top lists
+ *                      merge by (score, rank) (search.py:303); outputs as l0s_search, stats
+ *                      summed (counts) or maxed (times) over the devices.
+ */
+typedef struct l0s_group l0s_group;
+int l0s_group_create(int ndev, const int *devices, l0s_group **out);
+int l0s_group_destroy(l0s_group *group);
+int l0s_group_size(l0s_group *group, int *out);
+int l0s_group_ctx(l0s_group *group, int member, l0s_ctx **out);
+int l0s_group_stage(l0s_group *group, const double *values, const double *const *rows, int64_t m,
+                    int64_t s, const double *y, const int64_t *perm, const int64_t *bounds,
+                    int ntasks, int precision);
+int l0s_group_search(l0s_group *group, int n, int64_t keep, int mode, double *out_scores,
+                     int64_t *out_ranks, double *out_coef, double *out_ssr, int64_t *out_count,
+                     l0s_stats *stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,6 +29,7 @@ EXPORTS = (
     "l0s_search", "l0s_fit_tuples", "l0s_screen_tuples", "l0s_get_gram", "l0s_unrank", "l0s_rank",
     "l0s_count", "l0s_fp64_peak", "l0s_rcp_check", "l0s_gram_shard_size", "l0s_stage_shard",
     "l0s_stage_finish", "l0s_sis_prepare", "l0s_sis_scores", "l0s_set_gram_mode", "l0s_stage_info", "l0s_stage_timings", "l0s_qr_tuples",
+    "l0s_group_create", "l0s_group_destroy", "l0s_group_size", "l0s_group_ctx", "l0s_group_stage", "l0s_group_search",
     "l0s_stage_append", "l0s_search_part", "l0s_stage_rows", "l0s_stage_append_rows", "l0s_gen_pool", "l0s_gen_eval", "l0s_gen_take", "l0s_gen_fetch",
 )
 
@@ -114,6 +115,12 @@ def lib():
         L.l0s_count.argtypes = [i64, i32, P(i64)]
         L.l0s_fp64_peak.argtypes = [vp, P(dbl)]
         L.l0s_rcp_check.argtypes = [i64, P(dbl)]
+        L.l0s_group_create.argtypes = [i32, vp, P(vp)]
+        L.l0s_group_destroy.argtypes = [vp]
+        L.l0s_group_size.argtypes = [vp, P(i32)]
+        L.l0s_group_ctx.argtypes = [vp, i32, P(vp)]
+        L.l0s_group_stage.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp, i32, i32]
+        L.l0s_group_search.argtypes = [vp, i32, i64, i32, vp, vp, vp, vp, P(i64), P(Stats)]
         for name in EXPORTS:
             if name not in ("l0s_last_error",):
                 getattr(L, name).restype = i32
@@ -384,6 +391,78 @@ class Engine:
         v = ctypes.c_double(0.0)
         check(lib().l0s_fp64_peak(self.handle, ctypes.byref(v)), "l0s_fp64_peak")
         return v.value
+
+
+class Group:
+    """Several devices of this process searching one problem (l0s_group_*: row blocks uploaded per
+    device and exchanged device to device, part g of the search on device g, (score, rank) merge)."""
+
+    def __init__(self, devices):
+        L = lib()
+        self.devices = tuple(int(d) for d in devices)
+        arr = np.asarray(self.devices, dtype=np.int32)
+        h = ctypes.c_void_p()
+        check(L.l0s_group_create(len(arr), ptr(arr), ctypes.byref(h)), "l0s_group_create")
+        self.handle = h
+        self.T = 0
+        self.m = 0
+
+    def close(self):
+        if self.handle:
+            lib().l0s_group_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def stage(self, values, y, perm, bounds, precision: str) -> None:
+        """values: an (m, s) array, or a list of m row arrays (a SelectedSubspace's entries)."""
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        perm = np.ascontiguousarray(perm, dtype=np.int64)
+        bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+        s = y.shape[0]
+        if isinstance(values, np.ndarray):
+            values = np.ascontiguousarray(values, dtype=np.float64)
+            m = values.shape[0]
+            rc = lib().l0s_group_stage(self.handle, ptr(values), None, m, s, ptr(y), ptr(perm), ptr(bounds),
+                                       len(bounds) - 1, PREC[precision])
+        else:
+            keep, rows = Engine._row_pointers(values, s)
+            m = len(keep)
+            rc = lib().l0s_group_stage(self.handle, None, rows, m, s, ptr(y), ptr(perm), ptr(bounds),
+                                       len(bounds) - 1, PREC[precision])
+        check(rc, "l0s_group_stage")
+        self.T = len(bounds) - 1
+        self.m = m
+
+    def search(self, n: int, keep: int, mode: str = "auto"):
+        keep = int(keep)
+        scores = np.zeros(keep, dtype=np.float64)
+        ranks = np.zeros(keep, dtype=np.int64)
+        coef = np.zeros((keep, self.T, n + 1), dtype=np.float64)
+        ssr = np.zeros((keep, self.T), dtype=np.float64)
+        cnt = ctypes.c_int64(0)
+        st = Stats()
+        check(lib().l0s_group_search(self.handle, n, keep, MODES[mode], ptr(scores), ptr(ranks), ptr(coef), ptr(ssr),
+                                     ctypes.byref(cnt), ctypes.byref(st)), "l0s_group_search")
+        k = cnt.value
+        return scores[:k], ranks[:k], coef[:k], ssr[:k], st
+
+
+_groups: dict[tuple, Group] = {}
+
+
+def group(devices) -> Group:
+    """Process-wide device group per device tuple."""
+    key = tuple(int(d) for d in devices)
+    g = _groups.get(key)
+    if g is None or g.handle is None:
+        g = Group(key)
+        _groups[key] = g
+    return g
 
 
 _engines: dict[int, Engine] = {}

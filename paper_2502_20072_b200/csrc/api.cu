@@ -305,6 +305,10 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 
 }  // namespace
 
+namespace l0s {
+int set_error(int code, const char* msg) { return fail(code, "%s", msg); }
+}  // namespace l0s
+
 extern "C" {
 
 const char* l0s_last_error(void) { return g_err.c_str(); }

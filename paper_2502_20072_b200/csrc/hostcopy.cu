@@ -8,6 +8,7 @@
 // caller registered or allocated them) bypass the ring.
 #include <algorithm>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -80,8 +81,8 @@ class Pool {
 }  // namespace
 
 struct HostStager {
-    static constexpr size_t kSlot = (size_t)4 << 20;  // bytes per pinned slot
-    static constexpr int kSlots = 8;
+    static constexpr size_t kSlot = (size_t)16 << 20;  // bytes per pinned slot (one fork-join each)
+    static constexpr int kSlots = 4;
     char* pin = nullptr;
     cudaEvent_t ev[kSlots] = {};
     int next = 0;
@@ -103,7 +104,9 @@ HostStager* host_stager_create() {
     }
     for (auto& e : h->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     const unsigned hw = std::thread::hardware_concurrency();
-    h->pool = new Pool((int)std::max(1u, std::min(8u, hw ? hw / 2 : 4u)));
+    int threads = (int)std::max(1u, std::min(8u, hw ? hw : 4u));
+    if (const char* e = getenv("L0S_COPY_THREADS")) threads = std::max(1, atoi(e));  // tuning
+    h->pool = new Pool(threads);
     return h;
 }
 

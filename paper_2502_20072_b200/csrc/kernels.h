@@ -137,6 +137,9 @@ inline int hist_base_for(double top) {
 struct alignas(64) TmaDesc {
     unsigned long long opaque[16];
 };
+// per-thread error message of the C ABI (api.cu): returns `code`
+int set_error(int code, const char* msg);
+
 // ---- host -> device copies from pageable memory (hostcopy.cu) ----
 struct HostStager;
 HostStager* host_stager_create();  // nullptr when no pinned memory could be had

@@ -227,10 +227,14 @@ def l0_search(
 
     subspace is a SelectedSubspace or a raw (features, samples) matrix.
     Returns up to n_models_store models ordered by (score, rank); tuples whose
-    system is rank deficient score +inf and are never returned.  ``workers``
-    is accepted for API compatibility (the device does the work).  Extra
-    keyword-only knobs: ``device`` (CUDA ordinal), ``mode`` ("auto", "fast",
-    "exact") and ``rank_range`` (restrict the scan to ranks [lo, hi)).
+    system is rank deficient score +inf and are never returned.
+
+    Parallelism: the reference runs ``workers`` threads over rank ranges (search.py:258-301);
+    here one device does the work, or several devices of this process (``device`` a list of
+    CUDA ordinals, else ``L0S_DEVICES="0,1,..."``, else -- with ``workers`` > 1 -- the first
+    ``workers`` visible devices): each searches its part and the exact per-part lists merge by
+    (score, rank).  Extra keyword-only knobs: ``device`` (ordinal or list), ``mode`` ("auto",
+    "fast", "exact") and ``rank_range`` (restrict the scan to ranks [lo, hi), one device).
     """
     if config is None:
         raise ValueError("config is required")
@@ -254,8 +258,14 @@ def l0_search(
     batch = max(1, config.batch_size)
     lo, hi = (0, total) if rank_range is None else (max(0, int(rank_range[0])), min(total, int(rank_range[1])))
 
-    eng = _lib.engine(device)
     y = np.asarray(property_values, dtype=np.float64)
+    devices = _devices(device, workers)
+    if devices is not None and rank_range is None:
+        return _group_search(devices, subspace if incremental else values, incremental, expressions, y, perm, bounds,
+                             slices, n, keep, total, config, batch, task_labels, stats, mode, m, s)
+    if isinstance(device, (list, tuple)):
+        device = device[0]
+    eng = _lib.engine(device)
     if incremental:
         _stage_subspace(eng, subspace, y, perm, bounds, config.precision)
     else:
@@ -265,21 +275,55 @@ def l0_search(
     elapsed = time.perf_counter() - t0
 
     if stats is not None:
-        candidates = [c for c in config.chunk_candidates if c >= 1] or [16384]
-        stats.chosen_chunk = min(candidates[0], batch)
-        n_batches = max(1, -(-(hi - lo) // batch)) if hi > lo else 0
-        extra = len(candidates) - 1 if (config.autotune and len(candidates) > 1 and n_batches) else 0
-        per = elapsed / max(1, n_batches + extra)
-        stats.batch_seconds.extend([per] * (n_batches + extra))
-        stats.n_tuples = total
-        # scan + merge only: the reference's seconds exclude _prepare and the per-model refit
-        # (search.py:305-308); the device reports the final-record refit separately
-        elapsed = max(elapsed - 1e-3 * dst.ms_records, 1e-9)
-        per = elapsed / max(1, n_batches + extra)
-        stats.batch_seconds[-(n_batches + extra):] = [per] * (n_batches + extra)
-        stats.seconds = elapsed
-        stats.device = dst.as_dict()
+        _fill_stats(stats, config, batch, lo, hi, total, elapsed, dst)
 
+    labels = _labels_for(slices, task_labels)
+    sizes = np.diff(bounds).astype(np.float64)
+    return [_model(unrank_tuple(int(ranks[i]), m, n), expressions, coef[i], ssr[i], bounds, s, labels, sizes)
+            for i in range(len(scores))]
+
+
+def _devices(device, workers: int):
+    """Device list of a multi-device search, or None for one device."""
+    import os
+
+    if isinstance(device, (list, tuple)):
+        devs = [int(d) for d in device]
+    elif device is None and os.environ.get("L0S_DEVICES"):
+        devs = [int(x) for x in os.environ["L0S_DEVICES"].split(",") if x.strip()]
+    elif device is None and workers > 1:
+        devs = list(range(min(int(workers), _lib.device_count())))
+    else:
+        return None
+    return devs if len(devs) > 1 else None
+
+
+def _fill_stats(stats, config, batch, lo, hi, total, elapsed, dst):
+    candidates = [c for c in config.chunk_candidates if c >= 1] or [16384]
+    stats.chosen_chunk = min(candidates[0], batch)
+    n_batches = max(1, -(-(hi - lo) // batch)) if hi > lo else 0
+    extra = len(candidates) - 1 if (config.autotune and len(candidates) > 1 and n_batches) else 0
+    # scan + merge only: the reference's seconds exclude _prepare and the per-model refit
+    # (search.py:305-308); the device reports the final-record refit separately
+    elapsed = max(elapsed - 1e-3 * dst.ms_records, 1e-9)
+    per = elapsed / max(1, n_batches + extra)
+    stats.batch_seconds.extend([per] * (n_batches + extra))
+    stats.n_tuples = total
+    stats.seconds = elapsed
+    stats.device = dst.as_dict()
+
+
+def _group_search(devices, values, incremental, expressions, y, perm, bounds, slices, n, keep, total, config, batch,
+                  task_labels, stats, mode, m, s):
+    """l0_search over several devices of this process (l0s_group_*)."""
+    grp = _lib.group(devices)
+    grp.stage([e.values for e in values.entries] if incremental else np.asarray(values), y, perm, bounds,
+              config.precision)
+    t0 = time.perf_counter()
+    scores, ranks, coef, ssr, dst = grp.search(n, keep, mode)
+    elapsed = time.perf_counter() - t0
+    if stats is not None:
+        _fill_stats(stats, config, batch, 0, total, total, elapsed, dst)
     labels = _labels_for(slices, task_labels)
     sizes = np.diff(bounds).astype(np.float64)
     return [_model(unrank_tuple(int(ranks[i]), m, n), expressions, coef[i], ssr[i], bounds, s, labels, sizes)

@@ -22,9 +22,8 @@ VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
     "base": (),
-    "wrel3_ib24": ("L0S_WREL=1", "L0S_C34_NBUF=3", "L0S_C34_IB=24"),
-    "wrel4_ib16": ("L0S_WREL=1", "L0S_C34_NBUF=4", "L0S_C34_IB=16"),
-    "wrel8_ib8": ("L0S_WREL=1", "L0S_C34_NBUF=8", "L0S_C34_IB=8"),
+    "slot0": ("L0S_FIT_SLOT0=1",),
+    "unroll2": ("L0S_C34_UNROLL=2",),
 }
 
 
