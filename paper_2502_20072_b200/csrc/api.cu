@@ -241,6 +241,11 @@ int run_exact(l0s_ctx* c, int n, const int64_t* ranks_d, const int64_t* tuples_d
 // CTAs assumed when splitting units into search parts (a B200's 148 SMs, one CTA each)
 constexpr int kPartGridCtas = 148;
 
+// keep above which the screened path collects candidates globally instead of per-warp lists,
+// and the largest keep it takes (K' = keep + 32 candidates refit exactly)
+constexpr int64_t kKeepLists = 96;
+constexpr int64_t kKeepMax = 4064;
+
 struct Cand {
     double score;
     int64_t rank;
@@ -1058,7 +1063,12 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     // (or 74, one refit wave at T = 4) the part holding the best tuples of C3 missed its
     // certificate and paid a rescan (~1 ms); 96 and 128 refit in two waves (0.40 ms) and
     // certify (tools/parts_balance.py)
-    const int kc = c->nparts > 1 ? 128 : (int)std::min<int64_t>(128, std::max<int64_t>(64, keep + 32));
+    // Large keep (> kKeepLists): no per-warp lists; every accepted bound goes to a global candidate
+    // list below the histogram threshold of K' = keep + 32 (collect mode 2, fitcommon.cuh)
+    const bool big = keep > kKeepLists;
+    const int kc = big ? (int)(keep + 32)
+                       : (c->nparts > 1 ? 128 : (int)std::min<int64_t>(128, std::max<int64_t>(64, keep + 32)));
+    const int64_t coll_cap = (int64_t)1 << 24;
     const int grid = n == 2 ? fit2_grid(c->T, c->nsm) : n == 3 ? fit3_grid(c->T, c->nsm) : fit4_grid(c->T, c->nsm);
     auto launch_fit = [&](const FitArgs& fa) {
         return n == 2 ? fit2_launch(fa, c->nsm, c->st)
@@ -1072,17 +1082,18 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     CK(c->theta_g.ensure(sizeof(unsigned long long)));
     CK(c->hist.ensure(sizeof(unsigned) * HIST_BINS));
     CK(c->seedbuf.ensure(sizeof(int64_t) * 1024 * 5 + 256));  // subsets, bounds, count, cap
-    CK(c->wl_lb.ensure(sizeof(double) * slots * kc));
-    CK(c->wl_rank.ensure(sizeof(int64_t) * slots * kc));
+    CK(c->wl_lb.ensure(sizeof(double) * slots * (big ? 1 : kc)));
+    CK(c->wl_rank.ensure(sizeof(int64_t) * slots * (big ? 1 : kc)));
     CK(c->wl_cnt.ensure(sizeof(int) * slots));
     CK(c->ill.ensure(sizeof(int64_t) * ill_cap));
     CK(c->ill_cnt.ensure(sizeof(unsigned long long)));
-    CK(c->cand_lb.ensure(sizeof(double) * slots * kc));
-    CK(c->cand_rank.ensure(sizeof(int64_t) * slots * kc));
+    const int64_t lists = (int64_t)slots * (big ? 1 : kc);
+    CK(c->cand_lb.ensure(sizeof(double) * lists));
+    CK(c->cand_rank.ensure(sizeof(int64_t) * lists));
     CK(c->cand_cnt.ensure(sizeof(unsigned long long)));
-    CK(c->lb_tmp.ensure(sizeof(double) * slots * kc));
-    CK(c->rank_tmp.ensure(sizeof(int64_t) * slots * kc));
-    size_t tb = sort_pairs_temp_bytes((int64_t)slots * kc);
+    CK(c->lb_tmp.ensure(sizeof(double) * lists));
+    CK(c->rank_tmp.ensure(sizeof(int64_t) * lists));
+    size_t tb = sort_pairs_temp_bytes(lists);
     CK(c->sort_tmp.ensure(tb));
     unsigned long long inf_enc = ord_enc(INFINITY);
 
@@ -1095,8 +1106,18 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     a.rank_hi = re;
     a.ranged = (rb > 0 || re < N) ? 1 : 0;
     a.kc = kc;
-    a.collect = 0;
+    a.collect = big ? 2 : 0;
     a.theta0 = INFINITY;
+    if (big) {
+        CK(c->coll_lb.ensure(sizeof(double) * coll_cap));
+        CK(c->coll_rank.ensure(sizeof(int64_t) * coll_cap));
+        CK(c->coll_cnt.ensure(sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(c->coll_cnt.p, 0, sizeof(unsigned long long), c->st));
+        a.coll_lb = c->coll_lb.as<double>();
+        a.coll_rank = c->coll_rank.as<int64_t>();
+        a.coll_cnt = c->coll_cnt.as<unsigned long long>();
+        a.coll_cap = coll_cap;
+    }
     a.theta_g = c->theta_g.as<unsigned long long>();
     a.hist = c->hist.as<unsigned>();
     a.seed_tup = c->seedbuf.as<int64_t>();
@@ -1131,14 +1152,19 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     CK(cudaGetLastError());
     st->n_fit_launches++;
     st->n_launches += 4;  // threshold seed (select, eval, commit) + sweep
-    launch_gather_candidates(a.wl_lb, a.wl_rank, a.wl_cnt, slots, kc, a.theta_g, c->cand_lb.as<double>(),
-                             c->cand_rank.as<int64_t>(), c->cand_cnt.as<unsigned long long>(), c->st);
-    st->n_launches++;
+    if (!big) {
+        launch_gather_candidates(a.wl_lb, a.wl_rank, a.wl_cnt, slots, kc, a.theta_g, c->cand_lb.as<double>(),
+                                 c->cand_rank.as<int64_t>(), c->cand_cnt.as<unsigned long long>(), c->st);
+        st->n_launches++;
+    }
+    // the candidate set: the gathered warp lists, or (large keep) the global collect list
+    double* cl = big ? c->coll_lb.as<double>() : c->cand_lb.as<double>();
+    int64_t* cr = big ? c->coll_rank.as<int64_t>() : c->cand_rank.as<int64_t>();
     unsigned long long ncand = 0, nill = 0, th_enc = 0, nev = 0;
     double seed_cap = INFINITY;
     CK(cudaMemcpyAsync(&nev, c->n_eval.p, sizeof nev, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(&seed_cap, a.seed_cap, sizeof seed_cap, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(&ncand, c->cand_cnt.p, sizeof ncand, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(&ncand, big ? c->coll_cnt.p : c->cand_cnt.p, sizeof ncand, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(&nill, c->ill_cnt.p, sizeof nill, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(&th_enc, c->theta_g.p, sizeof th_enc, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
@@ -1148,15 +1174,23 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     if ((int64_t)nill > ill_cap)
         return fail(L0S_ECAPACITY, "%llu ill-conditioned tuples exceed the routing buffer (%lld)",
                     (unsigned long long)nill, (long long)ill_cap);
-    sort_pairs(c->cand_lb.as<double>(), c->cand_rank.as<int64_t>(), c->lb_tmp.as<double>(), c->rank_tmp.as<int64_t>(),
-               (int64_t)ncand, c->sort_tmp.p, tb, c->st);
+    if (big) {
+        if ((int64_t)ncand > coll_cap)
+            return fail(L0S_ECAPACITY, "%llu candidates exceed the collect buffer (%lld)", (unsigned long long)ncand,
+                        (long long)coll_cap);
+        CK(c->lb_tmp.ensure(sizeof(double) * std::max<unsigned long long>(ncand, 1)));
+        CK(c->rank_tmp.ensure(sizeof(int64_t) * std::max<unsigned long long>(ncand, 1)));
+        tb = sort_pairs_temp_bytes((int64_t)ncand);
+        CK(c->sort_tmp.ensure(tb));
+    }
+    sort_pairs(cl, cr, c->lb_tmp.as<double>(), c->rank_tmp.as<int64_t>(), (int64_t)ncand, c->sort_tmp.p, tb, c->st);
     st->n_launches += 3;
     const int64_t nc = std::min<int64_t>((int64_t)ncand, kc);
     // every excluded tuple has lb >= G_lb (SSR units): the K'-th smallest gathered bound, or
     // -- fewer gathered -- the final shared threshold (+inf: nothing was ever dropped)
     double G_lb = st->theta;
     if ((int64_t)ncand >= kc) {
-        CK(cudaMemcpyAsync(&G_lb, c->cand_lb.as<double>() + (kc - 1), sizeof(double), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(&G_lb, cl + (kc - 1), sizeof(double), cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
         G_lb = std::min(G_lb, st->theta);
     }
@@ -1172,7 +1206,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     int64_t nref = nc;
     if (std::isfinite(cap) && nc > 0) {
         std::vector<double> lbs((size_t)nc);
-        CK(cudaMemcpyAsync(lbs.data(), c->cand_lb.p, sizeof(double) * nc, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(lbs.data(), cl, sizeof(double) * nc, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
         const double lim = (cap + margin_of(cap)) * (double)c->s;
         nref = 0;
@@ -1182,7 +1216,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     // exact refit of candidates + ill tuples
     std::vector<Cand> exact;
     cudaEventRecord(c->ev[2], c->st);
-    int rc = exact_ranks_to_host(c, n, c->cand_rank.as<int64_t>(), nref, exact, &st->n_launches, &c->recs);
+    int rc = exact_ranks_to_host(c, n, cr, nref, exact, &st->n_launches, &c->recs);
     if (rc) return rc;
     merge_best(best, exact, keep);
     if (nill > 0) {
@@ -1207,10 +1241,9 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     if (!certified) {
         // rescan: collect every tuple whose bound is below the keep-th exact score (+ margin)
         st->n_rescan++;
+        // (fewer than keep finite scores among the K' candidates: collect every finite bound; a
+        // collect buffer that overflows splits the rank range, l0s_search)
         double theta_star = std::isfinite(sk) ? (sk + margin_of(sk)) * (double)c->s : INFINITY;
-        if (!std::isfinite(theta_star))
-            return fail(L0S_ECAPACITY, "cannot certify: fewer than %lld finite candidates among %d", (long long)keep, kc);
-        const int64_t coll_cap = (int64_t)1 << 24;
         CK(c->coll_lb.ensure(sizeof(double) * coll_cap));
         CK(c->coll_rank.ensure(sizeof(int64_t) * coll_cap));
         CK(c->coll_cnt.ensure(sizeof(unsigned long long)));
@@ -1249,6 +1282,29 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     return L0S_OK;
 }
 
+}  // extern "C"
+
+// The screened search of [rb, re); a fixed device buffer that overflows (ill-conditioned tuples,
+// collected candidates, rescan) splits the range in halves, each certified on its own, and the
+// (score, rank) merge of certified ranges is the whole range's (search.py:303).
+static int search_fast_split(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t re, std::vector<Cand>& best,
+                             l0s_stats* st, int depth) {
+    std::vector<Cand> mine = best;
+    int rc = search_fast_mode(c, n, keep, rb, re, mine, st);
+    if (rc == L0S_OK) {
+        best.swap(mine);
+        return rc;
+    }
+    if (rc != L0S_ECAPACITY || depth >= 24 || re - rb < 2) return rc;
+    const int64_t mid = rb + (re - rb) / 2;
+    st->n_rescan++;  // counted as a rescan: the range is searched again in two halves
+    rc = search_fast_split(c, n, keep, rb, mid, best, st, depth + 1);
+    if (rc) return rc;
+    return search_fast_split(c, n, keep, mid, re, best, st, depth + 1);
+}
+
+extern "C" {
+
 int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank_end, int mode, double* out_scores,
                int64_t* out_ranks, double* out_coef, double* out_ssr, int64_t* out_count, l0s_stats* stats) {
     l0s_stats local{};
@@ -1276,14 +1332,14 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
     cudaEventCreate(&t1);
     cudaEventRecord(t0, c->st);
     // the screen's error model is for fp64 arithmetic in the reference (precision="fp64")
-    bool fast_ok = (n >= 2 && n <= 4) && c->T <= fit3_max_tasks() && keep <= 96;
+    bool fast_ok = (n >= 2 && n <= 4) && c->T <= fit3_max_tasks() && keep <= kKeepMax;
     bool use_fast;
     if (mode == L0S_MODE_FAST) {
         if (!fast_ok) {
             cudaEventDestroy(t0);
             cudaEventDestroy(t1);
-            return fail(L0S_EINVAL, "screened path needs n in {2, 3, 4}, ntasks <= %d, keep <= 96",
-                        fit3_max_tasks());
+            return fail(L0S_EINVAL, "screened path needs n in {2, 3, 4}, ntasks <= %d, keep <= %lld",
+                        fit3_max_tasks(), (long long)kKeepMax);
         }
         use_fast = true;
     } else if (mode == L0S_MODE_EXACT) {
@@ -1293,7 +1349,7 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
         use_fast = fast_ok && work > 2e8;
     }
     std::vector<Cand> best;
-    rc = use_fast ? search_fast_mode(c, n, keep, rb, re, best, st) : search_exact_mode(c, n, keep, rb, re, best, st);
+    rc = use_fast ? search_fast_split(c, n, keep, rb, re, best, st, 0) : search_exact_mode(c, n, keep, rb, re, best, st);
     if (rc) {
         cudaEventDestroy(t0);
         cudaEventDestroy(t1);
@@ -1361,7 +1417,7 @@ int l0s_search_part(l0s_ctx* c, int n, int64_t keep, int part, int nparts, int m
     int rc = (n >= 1 && c->m >= n) ? l0s_count(c->m, n, &N) : L0S_OK;
     if (rc) return rc;
     // every part must take the same path: decided on the whole problem, as l0s_search would
-    const bool fast_ok = (n >= 2 && n <= 4) && c->T <= fit3_max_tasks() && keep >= 1 && keep <= 96;
+    const bool fast_ok = (n >= 2 && n <= 4) && c->T <= fit3_max_tasks() && keep >= 1 && keep <= kKeepMax;
     const bool fast = mode == L0S_MODE_FAST || (mode == L0S_MODE_AUTO && fast_ok && (double)N * (double)c->s > 2e8);
     if (!fast || !fast_ok || nparts == 1)  // contiguous rank ranges (search.py:266-271)
         return l0s_search(c, n, keep, N / nparts * part + std::min<int64_t>(part, N % nparts),

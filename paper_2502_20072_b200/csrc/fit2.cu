@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(256, 2) k_fit2(const __grid_constant__ FitArgs
     const int64_t m = a.m, mp = a.mp;
     const double shrink = (NT == 1) ? 1.0 : (1.0 - 2.0 * kRcpRel);
     WarpCands wc{sm + warp * CAP, reinterpret_cast<int64_t*>(sm + NW * CAP) + warp * CAP, 0,
-                 a.collect ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g), 0};
+                 a.collect == 1 ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g), 0};
     const int64_t* B2 = a.binom + 2 * (m + 1);
     for (;;) {
         if (tid == 0) s_unit = atomicAdd(a.unit_counter, 1);
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256, 2) k_fit2(const __grid_constant__ FitArgs
         const int j = U.x * 32 + lane;
         const int jj = j < m ? j : (int)m - 1;
         const int i_lo = U.z, i_hi = U.w;
-        if (!a.collect) {
+        if (a.collect != 1) {
             const double th = fmin(hist_theta(a, lane), ord_dec(*(volatile unsigned long long*)a.theta_g));
             if (th < wc.theta) {
                 wc.theta = th;
@@ -175,7 +175,7 @@ int launch2(const FitArgs& a, int nsm, cudaStream_t st) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit2<NT>, 256, kSmem2);
     const int grid = nsm * (per_sm < 1 ? 1 : per_sm);
-    if (!a.collect) seed_launch<2, 24>(k_seed_eval2, a, st);
+    if (a.collect != 1) seed_launch<2, 24>(k_seed_eval2, a, st);
     k_fit2<NT><<<grid, 256, kSmem2, st>>>(a);
     return grid;
 }

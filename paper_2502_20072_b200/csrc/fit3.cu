@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
     auto sK = [&](int idx) -> double& { return sKb[idx * NT3]; };
     const double shrink = (NT == 1) ? 1.0 : (1.0 - 2.0 * kRcpRel);
     WarpCands wc{sm + NB * BS + warp * CAP, reinterpret_cast<int64_t*>(sm + NB * BS + NW3 * CAP) + warp * CAP, 0,
-                 a.collect ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g), 0};
+                 a.collect == 1 ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g), 0};
     const int64_t* B2 = a.binom + 2 * (m + 1);
     const int64_t* B3 = a.binom + 3 * (m + 1);
 
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
                 v = w == 1 ? fmax(a.rho_cap[tk], a.rho[(int64_t)tk * m + ff]) : a.rho[(int64_t)tk * m + ff];
             s_hu[t][w][l] = v;
         }
-        if (!a.collect && warp == NW3 - 1) {
+        if (a.collect != 1 && warp == NW3 - 1) {
             // shared threshold: the global bound histogram and the other warps' lists (one warp
             // per CTA reads them; the histogram scan is a long load chain)
             const double th = fmin(hist_theta(a, lane), ord_dec(*(volatile unsigned long long*)a.theta_g));
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
             }
         }
         __syncthreads();
-        if (!a.collect && s_th < wc.theta) wc.theta = s_th;
+        if (a.collect != 1 && s_th < wc.theta) wc.theta = s_th;
 
         // ---------------- hoist: (j, k_p) state per task (slot order) ----------------
         // L10 = C_jk, rd1 = 1/(1 - C_jk^2), s1 = rd1 (c_k - C_jk c_j); the bound's B_t/d term
@@ -640,7 +640,7 @@ int launch_nt(const FitArgs& a0, int nsm, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, C::NTH, C::smem_bytes);
     if (per_sm < 1) per_sm = 1;
     int grid = nsm * per_sm;
-    if (!a.collect) seed_launch<3, 18>(k_seed_eval3, a, st);
+    if (a.collect != 1) seed_launch<3, 18>(k_seed_eval3, a, st);
     k_fit3<NT><<<grid, C::NTH, C::smem_bytes, st>>>(a);
     return grid;
 }

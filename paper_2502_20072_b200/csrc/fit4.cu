@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs
     const int64_t m = a.m, mp = a.mp;
     const double shrink = (NT == 1) ? 1.0 : (1.0 - 2.0 * kRcpRel);
     WarpCands wc{sm + 2 * BS + warp * CAP, reinterpret_cast<int64_t*>(sm + 2 * BS + NW * CAP) + warp * CAP, 0,
-                 a.collect ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g), 0};
+                 a.collect == 1 ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g), 0};
     const int64_t* B2 = a.binom + 2 * (m + 1);
     const int64_t* B3 = a.binom + 3 * (m + 1);
     const int64_t* B4 = a.binom + 4 * (m + 1);
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs
         const int lbase = l0 + warp * P;
         const int i_lo = U.z, i_hi = U.w;
         load_tiles(0, i_lo, j0, k, l0);
-        if (!a.collect) {
+        if (a.collect != 1) {
             // shared threshold: the global bound histogram and the other warps' lists
             double th = fmin(hist_theta(a, lane), ord_dec(*(volatile unsigned long long*)a.theta_g));
             if (th < wc.theta) {
@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(128) k_seed_eval4(const __grid_constant__ FitA
 template <int NT>
 int launch4(const FitArgs& a, int nsm, cudaStream_t st) {
     const int grid = occupancy4<NT>(nsm);
-    if (!a.collect) seed_launch<4, 12>(k_seed_eval4, a, st);
+    if (a.collect != 1) seed_launch<4, 12>(k_seed_eval4, a, st);
     k_fit4<NT><<<grid, 256, Cfg4<NT>::smem_bytes, st>>>(a);
     return grid;
 }

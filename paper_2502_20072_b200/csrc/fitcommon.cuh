@@ -206,6 +206,31 @@ __device__ __forceinline__ double hist_theta(const FitArgs& a, int lane) {
     return __shfl_sync(L0S_FULL, th, L);
 }
 
+// Collect modes: append the warp's buffer to the global candidate list (collect == 2, the
+// histogram-threshold mode of large keep: only the entries still below the warp's threshold;
+// the others are above the final threshold too).
+__device__ __forceinline__ void flush_collect(const FitArgs& a, WarpCands& wc, int lane) {
+    const unsigned lt = lanemask_lt();
+    for (int x0 = 0; x0 < wc.cnt; x0 += 32) {
+        const int x = x0 + lane;
+        const bool on = x < wc.cnt && (a.collect == 1 || wc.lb[x] < wc.theta);
+        const unsigned bal = __ballot_sync(L0S_FULL, on);
+        unsigned long long b0 = 0;
+        if (lane == 0 && bal) b0 = atomicAdd(a.coll_cnt, (unsigned long long)__popc(bal));
+        b0 = __shfl_sync(L0S_FULL, b0, 0);
+        if (on) {
+            const unsigned long long idx = b0 + __popc(bal & lt);
+            if ((int64_t)idx < a.coll_cap) {
+                a.coll_lb[idx] = wc.lb[x];
+                a.coll_rank[idx] = wc.rk[x];
+            }
+        }
+    }
+    wc.cnt = 0;
+    wc.counted = 0;
+    __syncwarp();
+}
+
 // Deferred slow path: drain the pending bits (one tuple per lane per round).
 //   eval(b, &lb, &rank) -> 0 drop, 1 insert (lb < theta checked here), 2 exact kernel
 //   on_theta()          -> called after the warp's threshold dropped (refresh hoisted constants)
@@ -237,7 +262,7 @@ __device__ __forceinline__ void drain_pending(const FitArgs& a, unsigned (&pend)
                 wc.rk[pos] = rkv;
             }
             wc.cnt += __popc(im);
-            if (!a.collect) {
+            if (a.collect != 1) {
                 // count the new entries in the global histogram right away (the shared
                 // threshold must not wait for this warp's buffer to fill)
                 int hb = (kind == 1) ? hist_bin(lbv, a.hist_base) : -1;
@@ -261,16 +286,17 @@ __device__ __forceinline__ void drain_pending(const FitArgs& a, unsigned (&pend)
         __syncwarp();
         if (wc.cnt > CAP - 32) {
             if (a.collect) {
-                unsigned long long b0 = 0;
-                if (lane == 0) b0 = atomicAdd(a.coll_cnt, (unsigned long long)wc.cnt);
-                b0 = __shfl_sync(L0S_FULL, b0, 0);
-                for (int x = lane; x < wc.cnt; x += 32)
-                    if ((int64_t)(b0 + x) < a.coll_cap) {
-                        a.coll_lb[b0 + x] = wc.lb[x];
-                        a.coll_rank[b0 + x] = wc.rk[x];
+                flush_collect(a, wc, lane);
+                if (a.collect == 2) {
+                    // histogram threshold (large keep): the K'-th smallest bound counted anywhere
+                    const double th = fmin(hist_theta(a, lane), ord_dec(*(volatile unsigned long long*)a.theta_g));
+                    if (th < wc.theta) {
+                        wc.theta = th;
+                        if (lane == 0) atomicMin(a.theta_g, ord_enc(wc.theta));
+                        on_theta();
                     }
-                wc.cnt = 0;
-                __syncwarp();
+                    __syncwarp();
+                }
             } else {
                 hist_count(a, wc, lane);
                 warp_sort(wc.lb, wc.rk, wc.cnt, lane);
@@ -472,14 +498,7 @@ inline void seed_launch(E eval_kernel, const FitArgs& a, cudaStream_t st) {
 // End of the persistent loop: write the warp's list (or flush the collect buffer).
 __device__ __forceinline__ void flush_warp(const FitArgs& a, WarpCands& wc, int slot, int lane) {
     if (a.collect) {
-        unsigned long long b0 = 0;
-        if (lane == 0 && wc.cnt > 0) b0 = atomicAdd(a.coll_cnt, (unsigned long long)wc.cnt);
-        b0 = __shfl_sync(L0S_FULL, b0, 0);
-        for (int x = lane; x < wc.cnt; x += 32)
-            if ((int64_t)(b0 + x) < a.coll_cap) {
-                a.coll_lb[b0 + x] = wc.lb[x];
-                a.coll_rank[b0 + x] = wc.rk[x];
-            }
+        flush_collect(a, wc, lane);
         if (lane == 0) a.wl_cnt[slot] = 0;
     } else {
         warp_sort(wc.lb, wc.rk, wc.cnt, lane);

@@ -176,7 +176,8 @@ struct FitArgs {
     int ref_fp32;            // the reference computes in float32 (precision="fp32"): its rounding model
     // candidate state
     int kc;                  // per-warp keep K'
-    int collect;             // 1 = collect every lb < theta0 into coll_*
+    int collect;             // 0 = per-warp top-K' lists; 1 = collect every lb < theta0 into coll_*;
+                             // 2 = collect below the histogram threshold (large keep, K' = kc)
     double theta0;
     unsigned long long* theta_g;
     unsigned* hist;          // [HIST_BINS] global lower-bound histogram (fitcommon.cuh)

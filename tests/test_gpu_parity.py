@@ -56,8 +56,8 @@ def test_l0_search_matches_reference(name, mode):
     from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
 
     c = search_case(name)
-    if mode == "fast" and (c["n"] not in (2, 3, 4) or len(c["slices"]) > 8 or c["keep"] > 96):
-        pytest.skip("screened path covers n in {2, 3, 4}, <= 8 tasks, keep <= 96")
+    if mode == "fast" and c["n"] not in (2, 3, 4):
+        pytest.skip("the screened path covers n in {2, 3, 4} (n = 1 and n >= 5 run the exact kernel)")
     cfg = L0Config(dimension=c["n"], n_models_store=c["keep"], precision=c["precision"], autotune=False)
     st = SearchStats()
     models = l0_search(c["values"], c["y"], c["slices"], cfg, stats=st, mode=mode)

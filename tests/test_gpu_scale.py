@@ -123,7 +123,7 @@ KINDS = ("random", "planted", "tie", "collinear", "large_mean", "scales", "noise
 def _stress_instance(k):
     rng = np.random.default_rng(7000 + k)
     n = (2, 3, 4)[k % 3]
-    T = 1 + (k // 3) % 8
+    T = 1 + (k // 3) % 12  # more than 8 tasks: the sweep bounds with 8 of them
     kind = KINDS[(k // 24 + k) % len(KINDS)]
     precision = "fp32" if k % 5 == 4 else "fp64"
     m = int(rng.integers(*{2: (60, 301), 3: (40, 121), 4: (24, 51)}[n]))
@@ -154,7 +154,7 @@ def _stress_instance(k):
     order = rng.permutation(s)
     cuts = np.linspace(0, s, T + 1).astype(int)
     slices = [np.sort(order[cuts[t]:cuts[t + 1]]) for t in range(T)]
-    keep = int(rng.integers(1, 41))
+    keep = int(rng.integers(1, 41)) if k % 7 else int(rng.integers(97, 300))  # > 96: global candidate list
     return dict(v=v, y=y, slices=slices, n=n, keep=keep, precision=precision, kind=kind)
 
 
@@ -179,3 +179,24 @@ def test_stress_loop_matches_oracle(oracle, block):
             check_models(got, exp)
         except AssertionError as e:
             raise AssertionError(f"instance {tag}: {e}") from e
+
+
+@pytest.mark.parametrize("keep", [97, 250, 1000])
+@pytest.mark.parametrize("n", [2, 3, 4])
+def test_large_keep_matches_oracle(oracle, n, keep):
+    """keep > 96: the screened path collects candidates globally below the histogram threshold."""
+    from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
+
+    rng = np.random.default_rng(keep + n)
+    m, s, T = {2: 160, 3: 60, 4: 32}[n], 240, 3
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    y = rng.standard_normal(s) if keep != 250 else v[1] - v[7] + 0.5 * v[m - 2] + 0.1 * rng.standard_normal(s)
+    slices = [np.arange(t, s, T) for t in range(T)]
+    want = oracle.l0_search(v, y, slices, n, keep, "fp64", threads=THREADS)
+    st = SearchStats()
+    got = l0_search(v, y, slices, L0Config(dimension=n, n_models_store=keep), stats=st, mode="fast")
+    assert st.device["mode_used"] == 1 and st.device["certified"] == 1
+    exp = {"exp_indices": np.array([w["indices"] for w in want]), "exp_score": np.array([w["score"] for w in want]),
+           "exp_coef": np.array([w["coefficients"] for w in want]),
+           "exp_rmse": np.array([w["rmse_per_task"] for w in want])}
+    check_models(got, exp)

@@ -55,6 +55,23 @@ def main():
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         print(f"raw H2D {v.nbytes / 1e6:.0f} MB: {1e3 * dt:.2f} ms ({v.nbytes / dt / 1e9:.1f} GB/s)")
+    # what pinning the caller's pageable pages in place would cost (cudaHostRegister)
+    import ctypes
+
+    cudart = ctypes.CDLL("libcudart.so.12") if os.path.exists("/usr/local/cuda/lib64/libcudart.so.12") else None
+    if cudart is not None:
+        for it in range(3):
+            w = np.array(v)
+            t0 = time.perf_counter()
+            rc = cudart.cudaHostRegister(ctypes.c_void_p(w.ctypes.data), ctypes.c_size_t(w.nbytes), 0)
+            t1 = time.perf_counter()
+            cudart.cudaHostUnregister(ctypes.c_void_p(w.ctypes.data))
+            t2 = time.perf_counter()
+            print(f"cudaHostRegister 160 MB rc={rc}: {1e3 * (t1 - t0):.2f} ms, unregister {1e3 * (t2 - t1):.2f} ms")
+    for it in range(4):
+        t0 = time.perf_counter()
+        l0_search(v, y, slices, cfg)
+        print(f"l0_search pageable: {1e3 * (time.perf_counter() - t0):.2f} ms")
 
 
 if __name__ == "__main__":
