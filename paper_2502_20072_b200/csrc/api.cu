@@ -682,6 +682,89 @@ int l0s_stage_append_rows(l0s_ctx* c, const double* const* rows, int64_t m_new) 
     return stage_append(c, nullptr, rows, m_new);
 }
 
+// Extend a staged problem (INT8 Gram) from m0 to m1 features whose new rows already sit in
+// in_values: the old feature block of the Gram, the old rows of Z / Xp, their INT8 digits and
+// exponents and their per-task norms move to the new layout (device copies, the property row
+// is re-staged at index m1), only the new rows are gathered and normalized, and only the Gram
+// column blocks that hold a new column (and the property's) are recomputed -- every entry of the
+// INT8 Gram depends only on its two rows' digits, so the result is the full stage's bit for bit.
+static int stage_extend(l0s_ctx* c, int64_t m1) {
+    const int64_t m0 = c->m, s = c->s, sp = c->sp;
+    const int T = c->T;
+    const int64_t mp0 = c->mp, mp1 = ((m1 + 1 + 32 + 63) / 64) * 64;
+    const int64_t R0 = (mp0 + 127) / 128 * 128, R1 = (mp1 + 127) / 128 * 128;
+    const size_t wsz = c->prec == L0S_PREC_FP32 ? 4 : 8;
+    int64_t KP = 0;
+    const int64_t qb1 = ozaki_q_bytes(mp1, T, c->rpad_h.data(), &KP);
+    cudaEventRecord(c->ev[0], c->st);
+    // relayout into fresh buffers (old contents copied), then swap
+    DBuf G1, Q1, ex1, qf1, un21;
+    CK(G1.ensure(sizeof(double) * mp1 * mp1 * T));
+    CK(Q1.ensure((size_t)qb1));
+    CK(ex1.ensure(sizeof(int) * T * R1));
+    CK(qf1.ensure(sizeof(double) * m1 * T));
+    CK(un21.ensure(sizeof(double) * m1 * T));
+    for (int t = 0; t < T; ++t) {
+        CK(cudaMemcpy2DAsync(G1.as<double>() + (int64_t)t * mp1 * mp1, sizeof(double) * mp1,
+                             c->G.as<double>() + (int64_t)t * mp0 * mp0, sizeof(double) * mp0, sizeof(double) * m0,
+                             (size_t)m0, cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaMemcpyAsync(ex1.as<int>() + (int64_t)t * R1, c->oz_ex.as<int>() + (int64_t)t * R0, sizeof(int) * m0,
+                           cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaMemcpyAsync(qf1.as<double>() + (int64_t)t * m1, c->qf.as<double>() + (int64_t)t * m0,
+                           sizeof(double) * m0, cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaMemcpyAsync(un21.as<double>() + (int64_t)t * m1, c->un2.as<double>() + (int64_t)t * m0,
+                           sizeof(double) * m0, cudaMemcpyDeviceToDevice, c->st));
+    }
+    for (int a = 0; a < OZ_DIGITS; ++a)
+        CK(cudaMemcpyAsync(Q1.as<int8_t>() + (int64_t)a * R1 * KP, c->oz_q.as<int8_t>() + (int64_t)a * R0 * KP,
+                           (size_t)(m0 * KP), cudaMemcpyDeviceToDevice, c->st));
+    std::swap(c->G, G1);
+    std::swap(c->oz_q, Q1);
+    std::swap(c->oz_ex, ex1);
+    std::swap(c->qf, qf1);
+    std::swap(c->un2, un21);
+    CK(cudaStreamSynchronize(c->st));  // the old buffers are released on return
+    CK(c->Z.grow(sizeof(double) * mp1 * sp, sizeof(double) * m0 * sp, c->st));
+    CK(c->Xp.grow(wsz * m1 * s, wsz * m0 * s, c->st));
+    c->m = m1;
+    c->mp = mp1;
+    c->staged = false;
+    CK(cudaMemsetAsync(c->Z.as<double>() + (m1 + 1) * sp, 0, sizeof(double) * (mp1 - m1 - 1) * sp, c->st));
+    // digit rows past the property (padding) and their exponents: zero
+    for (int a = 0; a < OZ_DIGITS; ++a)
+        CK(cudaMemsetAsync(c->oz_q.as<int8_t>() + ((int64_t)a * R1 + m1 + 1) * KP, 0, (size_t)((R1 - m1 - 1) * KP), c->st));
+    for (int t = 0; t < T; ++t)
+        CK(cudaMemsetAsync(c->oz_ex.as<int>() + (int64_t)t * R1 + m1 + 1, 0, sizeof(int) * (R1 - m1 - 1), c->st));
+    DigitOut dig{c->oz_q.as<int8_t>(), R1, KP, c->oz_koff.as<int64_t>(), c->oz_ex.as<int>()};
+    const double* vd = c->in_values.as<double>();
+    const double* yd = c->in_y.as<double>();
+    const int64_t* pd = c->in_perm.as<int64_t>();
+    for (int64_t f0 : {m1, m0}) {  // the property (row m1), then the new features (rows m0 .. m1-1)
+        const int64_t f1 = f0 == m1 ? m1 + 1 : m1;
+        launch_gather(vd, yd, pd, m1, s, c->prec, c->Xp.p, c->yp.p, f0, f1, c->st);
+        launch_normalize(c->Xp.p, c->yp.p, c->prec, m1, s, c->bounds_d.as<int64_t>(), c->zoff_d.as<int64_t>(), T, sp,
+                         c->Z.as<double>(), c->qf.as<double>(), c->un2.as<double>(), c->yyu.as<double>(), f0, f1, dig,
+                         c->st);
+    }
+    // column blocks holding a new column or the property's (their tiles cover every row)
+    cudaEventRecord(c->ev[2], c->st);
+    if (launch_ozaki_tiles(T, mp1, c->rpad_h.data(), c->oz_q.as<int8_t>(), c->oz_ex.as<int>(),
+                           c->oz_koff.as<int64_t>(), c->G.as<double>(), (int)(m0 / 128), ozaki_col_blocks(mp1), c->st))
+        return fail(L0S_ECUDA, "INT8 Gram: TMA descriptor");
+    // the per-task entry bound over every row's exponent (old rows' exponents moved above)
+    launch_ozaki_eta(T, m1, mp1, c->oz_ex.as<int>(), c->rowsd.as<double>(), c->G.as<double>(), c->eta_d.as<double>(),
+                     c->st);
+    cudaEventRecord(c->ev[3], c->st);
+    c->gram_timed = true;
+    c->gram_ozaki = true;
+    c->stage_timed = false;
+    c->binom_m = -1;
+    CK(cudaGetLastError());
+    const int rc = stage_post(c);
+    c->host_staged = true;
+    return rc;
+}
+
 static int stage_append(l0s_ctx* c, const double* values, const double* const* rows, int64_t m_new) {
     if (!c) return fail(L0S_EINVAL, "null context");
     if (!c->staged || !c->host_staged || c->shard_pending)
@@ -693,6 +776,7 @@ static int stage_append(l0s_ctx* c, const double* values, const double* const* r
     CK(cudaStreamSynchronize(c->st));
     CK(c->in_values.grow(sizeof(double) * m1 * s, sizeof(double) * m0 * s, c->st));
     CK(copy_rows(c, values, rows, 0, m_new, m0, c->st));
+    if (c->gram_ozaki && c->digits_ready && c->gram_mode != L0S_GRAM_DMMA) return stage_extend(c, m1);
     const std::vector<int64_t> bounds = c->bounds_h;
     int rc = stage_prepare(c, c->in_values.as<double>(), m1, s, c->in_y.as<double>(), c->in_perm.as<int64_t>(),
                            bounds.data(), c->T, c->prec, 1);
@@ -1066,7 +1150,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     // Large keep (> kKeepLists): no per-warp lists; every accepted bound goes to a global candidate
     // list below the histogram threshold of K' = keep + 32 (collect mode 2, fitcommon.cuh)
     const bool big = keep > kKeepLists;
-    const int kc = big ? (int)(keep + 32)
+    const int kc = big ? (int)(keep + std::max<int64_t>(32, keep / 2))  // slack: near-ties among the keep best
                        : (c->nparts > 1 ? 128 : (int)std::min<int64_t>(128, std::max<int64_t>(64, keep + 32)));
     const int64_t coll_cap = (int64_t)1 << 24;
     const int grid = n == 2 ? fit2_grid(c->T, c->nsm) : n == 3 ? fit3_grid(c->T, c->nsm) : fit4_grid(c->T, c->nsm);

@@ -802,3 +802,32 @@ def test_search_parts_other_paths(n, precision, mode):
         assert [c[1] for c in merged] == rk.tolist()
         assert bits_equal([c[0] for c in merged], sc)
         assert all(bits_equal(c[2], w) for c, w in zip(merged, coef))
+
+
+@pytest.mark.parametrize("m0,m_new", [(300, 150), (300, 1), (260, 700)])
+def test_stage_extend_int8_gram_equals_full_stage(m0, m_new):
+    """Appending rows to an INT8-Gram stage (stage_extend: old Gram block, digits and norms moved,
+    only the new column blocks recomputed) gives the full stage's Gram, bound and search bit for bit."""
+    from paper_2502_20072_b200 import _lib
+    from paper_2502_20072_b200.search import _partition
+
+    rng = np.random.default_rng(m0 + m_new)
+    s, T = 1200, 3
+    v = rng.uniform(0.5, 2.0, size=(m0 + m_new, s))
+    v[m0 + m_new - 1] *= 37.0  # a new row with a larger exponent (the bound eta must follow it)
+    y = v[5] - 0.5 * v[m0 + m_new // 2] + 0.01 * rng.standard_normal(s)
+    perm, bounds, _ = _partition(s, [np.arange(t, s, T) for t in range(T)])
+    eng = _lib.engine(0)
+    eng.stage(v, y, perm, bounds, "fp64")
+    eta_full, oz = eng.stage_info()
+    assert oz
+    want = eng.search(3, 10, 0, 2**63 - 1, "fast")
+    g_want = [eng.gram(t) for t in range(T)]
+    eng.stage(v[:m0], y, perm, bounds, "fp64")
+    eng.stage_append(v[m0:])
+    eta_inc, oz2 = eng.stage_info()
+    assert oz2 and bits_equal(eta_inc, eta_full)
+    assert all(bits_equal(eng.gram(t), g) for t, g in enumerate(g_want))
+    got = eng.search(3, 10, 0, 2**63 - 1, "fast")
+    for a, b in zip(got[:4], want[:4]):
+        assert bits_equal(a, b)
