@@ -149,13 +149,13 @@ def _hbm_peak():
 def stage_roofline(stage_ms):
     """HBM rooflines of the two staging passes (device-resident inputs, l0s_stage_timings):
     gather reads the (m, s) values and writes the task-ordered copy (16 B per element, SURVEY 8(d)'s
-    staging bytes are 16 m s + 8 s for both passes together); normalize reads that copy and writes
-    the unit-norm rows Z (8 B) and their four INT8 digit planes (4 B): 20 B per element."""
+    staging bytes are 16 m s + 8 s for both passes together); normalize reads that copy (8 B) and
+    writes the rows' four INT8 digit planes (4 B; the fp64 rows Z only for a DMMA Gram): 12 B."""
     if not stage_ms or not stage_ms.get("gather"):
         return None
     peak, src = _hbm_peak()
     out = {"peak": peak, "unit": "GB/s", "peak_source": src}
-    for name, per in (("gather", 16), ("normalize", 20)):
+    for name, per in (("gather", 16), ("normalize", 12)):
         ms = stage_ms[name]
         gbs = per * M * S / (ms * 1e-3) / 1e9
         out[name] = {"ms": ms, "bytes": per * M * S, "achieved": gbs, "frac": gbs / peak}

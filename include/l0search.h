@@ -257,6 +257,15 @@ int l0s_stage_timings(l0s_ctx *ctx, double *out_ms);
 int l0s_qr_tuples(l0s_ctx *ctx, int n, const int64_t *tuples, int64_t count, double *out_score,
                   double *out_ratio);
 
+/*
+ * Residual targets of the next SIS round (models.residuals / predict, models.py:44-83) from the
+ * staged inputs: out[c][i] = y[i] - (coef[c][t][n] + sum_k coef[c][t][k] x_{tup[c][k]}[i]) for every
+ * sample i (caller's order) of task t, numpy's operation order.  tuples (count, n) index the
+ * staged features; coef (count, ntasks, n+1) float64 (a Model's coefficients); out (count, s).
+ */
+int l0s_residuals(l0s_ctx *ctx, int n, const int64_t *tuples, const double *coef, int64_t count,
+                  double *out);
+
 /* Copy of the staged normalized Gram of one task ((m+1) x (m+1), last row/col = y). */
 int l0s_get_gram(l0s_ctx *ctx, int task, double *out);
 

@@ -23,6 +23,7 @@ from .search import (  # noqa: F401
     install,
     l0_search,
     rank_tuple,
+    residuals,
     unrank_tuple,
 )
 

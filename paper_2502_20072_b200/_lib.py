@@ -28,7 +28,7 @@ EXPORTS = (
     "l0s_last_error", "l0s_version", "l0s_device_count", "l0s_create", "l0s_destroy", "l0s_stage",
     "l0s_search", "l0s_fit_tuples", "l0s_screen_tuples", "l0s_get_gram", "l0s_unrank", "l0s_rank",
     "l0s_count", "l0s_fp64_peak", "l0s_rcp_check", "l0s_gram_shard_size", "l0s_stage_shard",
-    "l0s_stage_finish", "l0s_sis_prepare", "l0s_sis_scores", "l0s_set_gram_mode", "l0s_stage_info", "l0s_stage_timings", "l0s_qr_tuples",
+    "l0s_stage_finish", "l0s_sis_prepare", "l0s_sis_scores", "l0s_set_gram_mode", "l0s_stage_info", "l0s_stage_timings", "l0s_qr_tuples", "l0s_residuals",
     "l0s_group_create", "l0s_group_destroy", "l0s_group_size", "l0s_group_ctx", "l0s_group_stage", "l0s_group_search",
     "l0s_stage_append", "l0s_search_part", "l0s_stage_rows", "l0s_stage_append_rows", "l0s_gen_pool", "l0s_gen_eval", "l0s_gen_take", "l0s_gen_fetch",
 )
@@ -103,6 +103,7 @@ def lib():
         L.l0s_stage_info.argtypes = [vp, vp, vp]
         L.l0s_stage_timings.argtypes = [vp, vp]
         L.l0s_qr_tuples.argtypes = [vp, i32, vp, i64, vp, vp]
+        L.l0s_residuals.argtypes = [vp, i32, vp, vp, i64, vp]
         L.l0s_sis_prepare.argtypes = [vp, vp, i32, i64, vp, vp, i32]
         L.l0s_sis_scores.argtypes = [vp, vp, i64, i32, vp]
         L.l0s_search.argtypes = [vp, i32, i64, i64, i64, i32, vp, vp, vp, vp, P(i64), P(Stats)]
@@ -258,6 +259,15 @@ class Engine:
         oz = ctypes.c_int(0)
         check(lib().l0s_stage_info(self.handle, ptr(eta), ctypes.byref(oz)), "l0s_stage_info")
         return eta, bool(oz.value)
+
+    def residuals(self, tuples: np.ndarray, coef: np.ndarray) -> np.ndarray:
+        """y - prediction of each model (tuple of staged features, (T, n+1) coefficients), float64 (count, s)."""
+        tuples = np.ascontiguousarray(np.atleast_2d(tuples), dtype=np.int64)
+        coef = np.ascontiguousarray(coef, dtype=np.float64).reshape(len(tuples), self.T, tuples.shape[1] + 1)
+        out = np.empty((len(tuples), self.s), dtype=np.float64)
+        check(lib().l0s_residuals(self.handle, tuples.shape[1], ptr(tuples), ptr(coef), len(tuples), ptr(out)),
+              "l0s_residuals")
+        return out
 
     def qr_tuples(self, tuples: np.ndarray):
         """Device QR screen of explicit tuples: (pooled score, min rank-rule ratio over tasks)."""
@@ -437,6 +447,17 @@ class Group:
         check(rc, "l0s_group_stage")
         self.T = len(bounds) - 1
         self.m = m
+        self.s = s
+
+    def residuals(self, tuples: np.ndarray, coef: np.ndarray) -> np.ndarray:
+        """l0s_residuals on member 0 (every member staged the whole problem)."""
+        h = ctypes.c_void_p()
+        check(lib().l0s_group_ctx(self.handle, 0, ctypes.byref(h)), "l0s_group_ctx")
+        tuples = np.ascontiguousarray(np.atleast_2d(tuples), dtype=np.int64)
+        coef = np.ascontiguousarray(coef, dtype=np.float64)
+        out = np.empty((len(tuples), self.s), dtype=np.float64)
+        check(lib().l0s_residuals(h, tuples.shape[1], ptr(tuples), ptr(coef), len(tuples), ptr(out)), "l0s_residuals")
+        return out
 
     def search(self, n: int, keep: int, mode: str = "auto"):
         keep = int(keep)

@@ -151,6 +151,10 @@ struct l0s_ctx {
     int64_t units_key[7] = {-1, -1, -1, -1, -1, -1, -1};
     int part = 0, nparts = 1;  // l0s_search_part: this context screens units u with u % nparts == part
     HostStager* stager = nullptr;  // pinned ring for pageable host inputs (hostcopy.cu), on first use
+    const double* src_values = nullptr;  // the staged inputs, caller's sample order (device)
+    const double* src_y = nullptr;
+    const int64_t* src_perm = nullptr;
+    DBuf res_tup, res_coef, res_out;
 
     ~l0s_ctx() {
         if (stager) host_stager_destroy(stager);
@@ -160,7 +164,7 @@ struct l0s_ctx {
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
                        &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr, &sis_y, &sis_yc, &sis_sy, &sis_perm,
                        &sis_bounds, &sis_F, &sis_out, &sis_dest, &sis_tE, &sis_tpoff, &oz_q, &oz_ex, &oz_koff,
-                       &gen_pool, &gen_pi, &gen_pj, &gen_vals, &gen_valid, &gen_hash, &gen_take, &gen_rows, &gen_out};
+                       &res_tup, &res_coef, &res_out, &gen_pool, &gen_pi, &gen_pj, &gen_vals, &gen_valid, &gen_hash, &gen_take, &gen_rows, &gen_out};
         for (DBuf* b : all) b->release();
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -460,6 +464,10 @@ static int stage_post(l0s_ctx* c) {
             CK(cudaMemcpyAsync(c->eta_d.p, c->eta_h.data(), sizeof(double) * ntasks, cudaMemcpyHostToDevice, c->st));
             const int prev = c->gram_mode;
             c->gram_mode = L0S_GRAM_DMMA;
+            if (c->digits_ready)  // the INT8 path skipped Z: write it now for the DMMA Gram
+                launch_normalize(c->Xp.p, c->yp.p, c->prec, m, c->s, c->bounds_d.as<int64_t>(), c->zoff_d.as<int64_t>(),
+                                 ntasks, c->sp, c->Z.as<double>(), c->qf.as<double>(), c->un2.as<double>(),
+                                 c->yyu.as<double>(), 0, m + 1, DigitOut{nullptr, 0, 0, nullptr, nullptr}, c->st);
             gram_full(c);
             c->gram_mode = prev;
             launch_unit_diag(c->G.as<double>(), ntasks, m, c->mp, c->st);
@@ -560,6 +568,9 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
         yd = c->in_y.as<double>();
         pd = c->in_perm.as<int64_t>();
     }
+    c->src_values = vd;  // the inputs in the caller's sample order (l0s_residuals reads them)
+    c->src_y = yd;
+    c->src_perm = pd;
     // the INT8 Gram's digits come out of the normalize kernel (no second pass over Z)
     DigitOut dig{nullptr, 0, 0, nullptr, nullptr};
     c->digits_ready = false;
@@ -572,6 +583,7 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
         CK(c->oz_koff.ensure(sizeof(int64_t) * (ntasks + 1)));
         ozaki_prepare_digits(m, c->mp, ntasks, c->rpad_h.data(), c->oz_q.as<int8_t>(), c->oz_ex.as<int>(),
                              c->oz_koff.as<int64_t>(), &dig, c->st);
+        dig.write_z = false;  // the INT8 Gram reads the digits; Z is written only for a DMMA fallback
         c->digits_ready = true;
     }
     auto rows_to_z = [&](int64_t f0, int64_t f1) {
@@ -735,7 +747,7 @@ static int stage_extend(l0s_ctx* c, int64_t m1) {
         CK(cudaMemsetAsync(c->oz_q.as<int8_t>() + ((int64_t)a * R1 + m1 + 1) * KP, 0, (size_t)((R1 - m1 - 1) * KP), c->st));
     for (int t = 0; t < T; ++t)
         CK(cudaMemsetAsync(c->oz_ex.as<int>() + (int64_t)t * R1 + m1 + 1, 0, sizeof(int) * (R1 - m1 - 1), c->st));
-    DigitOut dig{c->oz_q.as<int8_t>(), R1, KP, c->oz_koff.as<int64_t>(), c->oz_ex.as<int>()};
+    DigitOut dig{c->oz_q.as<int8_t>(), R1, KP, c->oz_koff.as<int64_t>(), c->oz_ex.as<int>(), false};
     const double* vd = c->in_values.as<double>();
     const double* yd = c->in_y.as<double>();
     const int64_t* pd = c->in_perm.as<int64_t>();
@@ -978,6 +990,27 @@ int l0s_qr_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, doubl
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out_score, c->qr_score.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(out_ratio, c->qr_minr.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return L0S_OK;
+}
+
+int l0s_residuals(l0s_ctx* c, int n, const int64_t* tuples, const double* coef, int64_t count, double* out) {
+    if (!c || !c->staged || !c->src_values) return fail(L0S_ESTATE, "l0s_stage must be called first");
+    if (n < 1 || n > 15) return fail(L0S_EINVAL, "dimension %d outside [1, 15]", n);
+    if (count <= 0) return L0S_OK;
+    for (int64_t i = 0; i < count * n; ++i)
+        if (tuples[i] < 0 || tuples[i] >= c->m) return fail(L0S_EINVAL, "feature index outside the staged subspace");
+    CK(cudaSetDevice(c->dev));
+    const int p = n + 1;
+    CK(c->res_tup.ensure(sizeof(int64_t) * count * n));
+    CK(c->res_coef.ensure(sizeof(double) * count * c->T * p));
+    CK(c->res_out.ensure(sizeof(double) * count * c->s));
+    CK(cudaMemcpyAsync(c->res_tup.p, tuples, sizeof(int64_t) * count * n, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->res_coef.p, coef, sizeof(double) * count * c->T * p, cudaMemcpyHostToDevice, c->st));
+    launch_residuals(c->src_values, c->src_y, c->src_perm, c->bounds_d.as<int64_t>(), c->T, c->s, n,
+                     c->res_tup.as<int64_t>(), c->res_coef.as<double>(), count, c->res_out.as<double>(), c->st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, c->res_out.p, sizeof(double) * count * c->s, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     return L0S_OK;
 }

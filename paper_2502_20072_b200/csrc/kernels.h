@@ -25,10 +25,18 @@ struct DigitOut {
     int64_t R, KP;
     const int64_t* koff;   // (T+1,) device: task segment offsets in K (multiples of 64)
     int* ex;               // [T][R] row exponents
+    bool write_z = true;   // also write the fp64 rows Z (only the DMMA Gram reads them)
 };
 void launch_normalize(const void* Xp, const void* yp, int precision, int64_t m, int64_t s,
                       const int64_t* bounds_d, const int64_t* zoff_d, int T, int64_t sp, double* Z,
                       double* qf, double* un2, double* yyu, int64_t f0, int64_t f1, DigitOut dig, cudaStream_t st);
+
+// Residuals of `count` models (models.residuals / predict, models.py:44-83): out[c][i] =
+// y[i] - (coef[c][t][n] + sum_k coef[c][t][k] * values[tup[c][k]][i]) for sample i of task t,
+// numpy's operation order (explicit roundings), in the caller's sample order.
+void launch_residuals(const double* values, const double* y, const int64_t* perm, const int64_t* bounds, int T,
+                      int64_t s, int n, const int64_t* tup, const double* coef, int64_t count, double* out,
+                      cudaStream_t st);
 
 // rho, dead, rho_cap, iforce from qf / un2 (stage.cu), and NaN rows/cols of dead features in G
 void launch_feature_flags(double tol, int fp32, const double* qf, const double* un2, const double* rows, int64_t m, int64_t mp, int T,

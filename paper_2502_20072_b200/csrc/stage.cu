@@ -9,18 +9,32 @@
 
 namespace l0s {
 
-// rows f0 + blockIdx.y (row m is the property)
+// rows [f0 + GR * blockIdx.y, + GR) of [f0, f1) (row m is the property); one permutation index per
+// thread serves GR rows (GR independent loads in flight, the index read once)
+constexpr int GR = 8;
 template <typename W>
-__global__ void k_gather(const double* __restrict__ values, const double* __restrict__ y,
-                         const int64_t* __restrict__ perm, int64_t m, int64_t s, W* __restrict__ Xp,
-                         W* __restrict__ yp, int64_t f0) {
-    int64_t f = f0 + blockIdx.y;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t src = perm[i];
-        if (f < m)
-            Xp[f * s + i] = (W)values[f * s + src];  // float64 -> float32 rounds to nearest (numpy astype)
-        else
-            yp[i] = (W)y[src];
+__global__ void __launch_bounds__(256) k_gather(const double* __restrict__ values, const double* __restrict__ y,
+                                                const int64_t* __restrict__ perm, int64_t m, int64_t s,
+                                                W* __restrict__ Xp, W* __restrict__ yp, int64_t f0, int64_t f1) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= s) return;
+    const int64_t src = __ldg(perm + i);
+    const int64_t fa = f0 + (int64_t)GR * blockIdx.y, fb = fa + GR < f1 ? fa + GR : f1;
+    double v[GR];
+#pragma unroll
+    for (int r = 0; r < GR; ++r) {
+        const int64_t f = fa + r;
+        v[r] = f < fb ? (f < m ? values[f * s + src] : y[src]) : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < GR; ++r) {
+        const int64_t f = fa + r;
+        if (f < fb) {
+            if (f < m)
+                Xp[f * s + i] = (W)v[r];  // float64 -> float32 rounds to nearest (numpy astype)
+            else
+                yp[i] = (W)v[r];
+        }
     }
 }
 
@@ -48,25 +62,34 @@ __global__ void k_normalize(const W* __restrict__ Xp, const W* __restrict__ yp, 
     double sum = 0.0;
     for (int64_t i = lane; i < r; i += 32) sum += (double)src[i];
     sum = warp_sum(sum);
-    double mean = sum / (double)r;
-    // second pass refines the mean to the rounding level of the *centered* values: an offset
-    // of the computed mean would leave the columns uncentered by (mu - mean), an error the
-    // Gram bound does not cover for near-constant features (mean/std ratio rho >> 1)
-    double corr = 0.0;
-    for (int64_t i = lane; i < r; i += 32) corr += (double)src[i] - mean;
-    mean += warp_sum(corr) / (double)r;
-    double cs = 0.0, us = 0.0, mc = 0.0;
+    const double mean0 = sum / (double)r;
+    // the second pass refines the mean to the rounding level of the *centered* values (an
+    // offset of the computed mean would leave the columns uncentered by (mu - mean), an error the
+    // Gram bound does not cover for near-constant features, mean/std ratio rho >> 1) and takes
+    // the centered statistics in the same pass: with c0 = x - mean0, corr = sum c0 and
+    // d = corr / r, sum (c0 - d)^2 = sum c0^2 - corr d and max |c0 - d| = max(max c0 - d, d - min c0)
+    double corr = 0.0, s0 = 0.0, us = 0.0, cmax = -INFINITY, cmin = INFINITY;
     for (int64_t i = lane; i < r; i += 32) {
-        double x = (double)src[i];
-        double c = x - mean;
-        cs = fma(c, c, cs);
+        const double x = (double)src[i];
+        const double c = x - mean0;
+        corr += c;
+        s0 = fma(c, c, s0);
         us = fma(x, x, us);
-        mc = fmax(mc, fabs(c));
+        cmax = fmax(cmax, c);
+        cmin = fmin(cmin, c);
     }
-    cs = warp_sum(cs);
+    corr = warp_sum(corr);
+    s0 = warp_sum(s0);
     us = warp_sum(us);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mc = fmax(mc, __shfl_xor_sync(L0S_FULL, mc, o));
+    for (int o = 16; o > 0; o >>= 1) {
+        cmax = fmax(cmax, __shfl_xor_sync(L0S_FULL, cmax, o));
+        cmin = fmin(cmin, __shfl_xor_sync(L0S_FULL, cmin, o));
+    }
+    const double dlt = corr / (double)r;
+    const double mean = mean0 + dlt;
+    const double cs = fmax(s0 - corr * dlt, 0.0);
+    const double mc = fmax(cmax - dlt, dlt - cmin);
     // features: unit-norm centered rows (0/0 -> NaN for a constant feature, which the
     // reference always rejects); property: centered, not normalized.
     double scale = (f < m) ? 1.0 / sqrt(cs) : 1.0;
@@ -83,7 +106,7 @@ __global__ void k_normalize(const W* __restrict__ Xp, const W* __restrict__ yp, 
         const int64_t k0 = dig.koff[t], klen = dig.koff[t + 1] - k0;
         for (int64_t i = lane; i < klen; i += 32) {
             const double z = (i < r) ? ((double)src[i] - mean) * scale : 0.0;
-            if (i < rpad) dst[i] = z;
+            if (dig.write_z && i < rpad) dst[i] = z;  // Z only for a DMMA fallback (INT8 Gram: digits)
             double u = finite ? ldexp(z, -e) : 0.0;
 #pragma unroll
             for (int a = 0; a < OZ_DIGITS; ++a) {
@@ -211,14 +234,39 @@ void launch_feature_flags(double tol, int fp32, const double* qf, const double* 
     k_mark_dead_rows<<<dim3(4, (unsigned)m), 256, 0, st>>>(G, dead, m, mp, T);
 }
 
+// one thread per (model, permuted position p): sample i = perm[p] of task t (bounds)
+__global__ void k_residuals(const double* __restrict__ values, const double* __restrict__ y,
+                            const int64_t* __restrict__ perm, const int64_t* __restrict__ bounds, int T, int64_t s,
+                            int n, const int64_t* __restrict__ tup, const double* __restrict__ coef,
+                            double* __restrict__ out) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t c = blockIdx.y;
+    if (p >= s) return;
+    int t = 0;
+    while (t + 1 < T && p >= bounds[t + 1]) ++t;
+    const int64_t i = perm[p];
+    const double* ct = coef + (c * T + t) * (n + 1);
+    double acc = ct[n];  // np.full(len(sl), c[-1])
+    for (int k = 0; k < n; ++k) acc = __dadd_rn(acc, __dmul_rn(ct[k], values[tup[c * n + k] * s + i]));
+    out[c * s + i] = __dadd_rn(y[i], -acc);
+}
+
+void launch_residuals(const double* values, const double* y, const int64_t* perm, const int64_t* bounds, int T,
+                      int64_t s, int n, const int64_t* tup, const double* coef, int64_t count, double* out,
+                      cudaStream_t st) {
+    if (count <= 0) return;
+    k_residuals<<<dim3((unsigned)((s + 255) / 256), (unsigned)count), 256, 0, st>>>(values, y, perm, bounds, T, s, n,
+                                                                                      tup, coef, out);
+}
+
 void launch_gather(const double* values, const double* y, const int64_t* perm, int64_t m, int64_t s,
                    int precision, void* Xp, void* yp, int64_t f0, int64_t f1, cudaStream_t st) {
     if (f1 <= f0) return;
-    dim3 grid((unsigned)((s + 255) / 256 < 64 ? (s + 255) / 256 : 64), (unsigned)(f1 - f0));
+    dim3 grid((unsigned)((s + 255) / 256), (unsigned)((f1 - f0 + GR - 1) / GR));
     if (precision == 1)
-        k_gather<float><<<grid, 256, 0, st>>>(values, y, perm, m, s, (float*)Xp, (float*)yp, f0);
+        k_gather<float><<<grid, 256, 0, st>>>(values, y, perm, m, s, (float*)Xp, (float*)yp, f0, f1);
     else
-        k_gather<double><<<grid, 256, 0, st>>>(values, y, perm, m, s, (double*)Xp, (double*)yp, f0);
+        k_gather<double><<<grid, 256, 0, st>>>(values, y, perm, m, s, (double*)Xp, (double*)yp, f0, f1);
 }
 
 void launch_normalize(const void* Xp, const void* yp, int precision, int64_t m, int64_t s,

@@ -279,6 +279,7 @@ def l0_search(
 
     labels = _labels_for(slices, task_labels)
     sizes = np.diff(bounds).astype(np.float64)
+    _remember_stage(grp, expressions, y, slices, config.precision)
     return [_model(unrank_tuple(int(ranks[i]), m, n), expressions, coef[i], ssr[i], bounds, s, labels, sizes)
             for i in range(len(scores))]
 
@@ -326,8 +327,52 @@ def _group_search(devices, values, incremental, expressions, y, perm, bounds, sl
         _fill_stats(stats, config, batch, 0, total, total, elapsed, dst)
     labels = _labels_for(slices, task_labels)
     sizes = np.diff(bounds).astype(np.float64)
+    _remember_stage(eng, expressions, y, slices, config.precision)
     return [_model(unrank_tuple(int(ranks[i]), m, n), expressions, coef[i], ssr[i], bounds, s, labels, sizes)
             for i in range(len(scores))]
+
+
+# the last l0_search's staged subspace: (engine or group, expressions, y, task slices, precision)
+_last_stage = None
+
+
+def _remember_stage(owner, expressions, y, slices, precision):
+    global _last_stage
+    _last_stage = (owner, expressions, y, slices, precision)
+
+
+def residuals(models, property_values, primary_values, task_slices=None, n_residual=None):
+    """models.residuals (models.py:69-83): y minus each model's prediction, float64.
+
+    On the device when the models index the subspace the last l0_search staged (the pipeline's
+    call right after its search, pipeline.py:239): the columns are the staged feature rows and
+    the arithmetic is predict's (intercept, then + c_k x_k per feature, then y - acc) with
+    explicit roundings (l0s_residuals).  Otherwise -- other models, precision "fp32" (predict
+    re-evaluates the expressions in float64, not the float32 pool values) -- the reference's
+    host function runs.
+    """
+    chosen = models if n_residual is None else models[:n_residual]
+    y = np.asarray(property_values, dtype=np.float64)
+    st = _last_stage
+    ok = (st is not None and st[4] == "fp64" and st[1] is not None and len(chosen) > 0
+          and all(md.expressions is not None and len(md.indices) == len(chosen[0].indices)
+                  and all(md.expressions[k] is st[1][i] for k, i in enumerate(md.indices)) for md in chosen)
+          and np.array_equal(np.asarray(st[2]), y) and _same_slices(st[3], task_slices))
+    if not ok:
+        from descsearch.models import residuals as ref_residuals
+
+        return ref_residuals(models, property_values, primary_values, task_slices, n_residual)
+    tup = np.array([md.indices for md in chosen], dtype=np.int64)
+    coef = np.array([md.coefficients for md in chosen], dtype=np.float64)
+    return list(st[0].residuals(tup, coef))
+
+
+def _same_slices(a, b):
+    if b is None:
+        return a is None or len(a) == 1
+    if a is None or len(a) != len(b):
+        return False
+    return all(np.array_equal(np.asarray(x), np.asarray(z)) for x, z in zip(a, b))
 
 
 def fit_tuples(values, property_values, tuples, task_slices=None, precision: str = "fp64",
@@ -391,6 +436,9 @@ def install(sis: bool = True, gen: bool = True):
         ref_generation.iter_final_rung = gpu_generation.iter_final_rung
         pipeline.iter_final_rung = functools.partial(gpu_generation.iter_final_rung, on_device=True)
         pipeline.sis_select = gpu_screening.sis_select
+    # residual targets of the next dimension's SIS (pipeline.py:239), from the staged rows
+    saved.append((pipeline, "residuals", pipeline.residuals))
+    pipeline.residuals = residuals
     ref_search.l0_search = l0_search
     ref_search.fit_tuple = fit_tuple
     pipeline.l0_search = l0_search

@@ -271,15 +271,37 @@ def test_pipeline_drop_in_model_files(tmp_path, name):
         pytest.skip("reference package not importable here")
     import paper_2502_20072_b200 as l0
 
+    from paper_2502_20072_b200 import _lib
+
     g = load_golden("pipe", name)
     ds, cfgmap = _pipeline_case(name)
+    calls = []
+    real = _lib.Engine.residuals
+
+    def counted(self, tup, coef):
+        calls.append(len(tup))
+        return real(self, tup, coef)
+
+    _lib.Engine.residuals = counted
     undo = l0.install()
     try:
         cfg = RunConfig(**cfgmap)
         res = run_pipeline(ds, cfg)
         write_outputs(res, cfg, str(tmp_path))
+        # the pipeline's residual targets ran on the device (pipeline.py:239) ...
+        assert len(calls) == cfg.dimension - 1
+        # ... and equal the reference's host residuals bit for bit (the last dimension's models,
+        # whose subspace the device still holds)
+        from descsearch.models import residuals as ref_residuals
+
+        _, slices = ds.task_partition()
+        models = res.dimensions[-1].models
+        got = l0.search.residuals(models, ds.property_values, ds.primary_values, slices, 3)
+        want = ref_residuals(models, ds.property_values, ds.primary_values, slices, 3)
+        assert len(calls) == cfg.dimension and all(bits_equal(a, b) for a, b in zip(got, want))
     finally:
         undo()
+        _lib.Engine.residuals = real
     for d in range(1, cfg.dimension + 1):
         got = (tmp_path / f"models_dim{d}.txt").read_bytes()
         want = g[f"d{d}_models_file"].tobytes()

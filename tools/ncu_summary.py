@@ -40,12 +40,36 @@ KEYS = [
 ]
 
 
+def to_json(rows, head, commit, capture):
+    """profiles/fit3_profile.json for bench.py: the first k_fit3 launch of the capture."""
+    import json
+
+    for r in rows[2:]:
+        d = dict(zip(head, r))
+        if "k_fit3" not in d.get("Kernel Name", ""):
+            continue
+        num = lambda k: float(d[k].replace(",", "")) if k in d else None  # noqa: E731
+        mb = 1e6  # ncu reports Mbyte here
+        return {"kernel": d["Kernel Name"], "commit": commit, "capture": capture,
+                "duration_ms": num("gpu__time_duration.sum"),
+                "dram_bytes_per_launch": (num("dram__bytes_read.sum") + num("dram__bytes_write.sum")) * mb,
+                "fp64_pipe_active_frac": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active") / 100.0,
+                "issue_active_frac": num("sm__issue_active.avg.pct_of_peak_sustained_elapsed") / 100.0}
+    return None
+
+
 def main():
     rep = sys.argv[1]
     title = sys.argv[2] if len(sys.argv) > 2 else rep
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     head, units = rows[0], rows[1]
+    if "--json" in sys.argv:
+        import json
+
+        commit = sys.argv[sys.argv.index("--json") + 1]
+        print(json.dumps(to_json(rows, head, commit, rep), indent=1))
+        return
     print(f"# {title}")
     for r in rows[2:]:
         d = dict(zip(head, r))
