@@ -279,7 +279,7 @@ def l0_search(
 
     labels = _labels_for(slices, task_labels)
     sizes = np.diff(bounds).astype(np.float64)
-    _remember_stage(grp, expressions, y, slices, config.precision)
+    _remember_stage(eng, expressions, y, slices, config.precision)
     return [_model(unrank_tuple(int(ranks[i]), m, n), expressions, coef[i], ssr[i], bounds, s, labels, sizes)
             for i in range(len(scores))]
 
@@ -327,7 +327,7 @@ def _group_search(devices, values, incremental, expressions, y, perm, bounds, sl
         _fill_stats(stats, config, batch, 0, total, total, elapsed, dst)
     labels = _labels_for(slices, task_labels)
     sizes = np.diff(bounds).astype(np.float64)
-    _remember_stage(eng, expressions, y, slices, config.precision)
+    _remember_stage(grp, expressions, y, slices, config.precision)
     return [_model(unrank_tuple(int(ranks[i]), m, n), expressions, coef[i], ssr[i], bounds, s, labels, sizes)
             for i in range(len(scores))]
 

@@ -21,7 +21,7 @@ for y in planted random; do
   ncu -i gpurun_out/${tag}_fit3_${y}.ncu-rep --page source --csv --print-source sass > gpurun_out/${tag}_fit3_${y}_src.csv 2>/dev/null
   python tools/ncu_blocks.py gpurun_out/${tag}_fit3_${y}_src.csv 10 > gpurun_out/${tag}_fit3_${y}_blocks.txt 2>&1
 done
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gather|k_normalize|k_oz_gemm" -s 6 -c 3 -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gather|k_normalize|k_oz_gemm" -s 5 -c 5 -f \
     -o gpurun_out/${tag}_stage python tools/time_stage.py > gpurun_out/${tag}_stage.log 2>&1
 echo "stage full rc=$?"
 python tools/ncu_summary.py gpurun_out/${tag}_stage.ncu-rep "${tag}: staging kernels and the INT8 Gram on C3" > gpurun_out/${tag}_stage_ncu.txt
