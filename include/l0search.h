@@ -281,6 +281,17 @@ int l0s_fp64_peak(l0s_ctx *ctx, double *out_tflops);
 int l0s_rcp_check(int64_t count, double *out_max_rel);
 
 /*
+ * The streamed last rung's value dedup on the device (the reference's ordered walk,
+ * generation.py:364-385, for operator lists without repeated kinds, where the key test
+ * cannot fire).  l0s_gen_dedup_reset seeds a device set with the pool's 128-bit fingerprints
+ * (count x 2 uint64, as l0s_gen_eval writes them); l0s_gen_dedup marks, for the candidates of
+ * the last l0s_gen_eval, out_kept[x] = 1 iff x is valid and no earlier candidate of the stream
+ * (or pool entry) has its fingerprint, and adds the kept fingerprints to the set.
+ */
+int l0s_gen_dedup_reset(l0s_ctx *ctx, const uint64_t *seed, int64_t count);
+int l0s_gen_dedup(l0s_ctx *ctx, uint8_t *out_kept, int64_t *out_count);
+
+/*
  * Several devices in one process (the reference's in-process `workers`, search.py:258-304):
  * one context per device (devices may repeat), one host thread per device.
  *   l0s_group_stage  : device g uploads row block g of the inputs (values: (m, s) row-major, or

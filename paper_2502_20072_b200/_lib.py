@@ -29,6 +29,7 @@ EXPORTS = (
     "l0s_search", "l0s_fit_tuples", "l0s_screen_tuples", "l0s_get_gram", "l0s_unrank", "l0s_rank",
     "l0s_count", "l0s_fp64_peak", "l0s_rcp_check", "l0s_gram_shard_size", "l0s_stage_shard",
     "l0s_stage_finish", "l0s_sis_prepare", "l0s_sis_scores", "l0s_set_gram_mode", "l0s_stage_info", "l0s_stage_timings", "l0s_qr_tuples", "l0s_residuals",
+    "l0s_gen_dedup_reset", "l0s_gen_dedup",
     "l0s_group_create", "l0s_group_destroy", "l0s_group_size", "l0s_group_ctx", "l0s_group_stage", "l0s_group_search",
     "l0s_stage_append", "l0s_search_part", "l0s_stage_rows", "l0s_stage_append_rows", "l0s_gen_pool", "l0s_gen_eval", "l0s_gen_take", "l0s_gen_fetch",
 )
@@ -104,6 +105,8 @@ def lib():
         L.l0s_stage_timings.argtypes = [vp, vp]
         L.l0s_qr_tuples.argtypes = [vp, i32, vp, i64, vp, vp]
         L.l0s_residuals.argtypes = [vp, i32, vp, vp, i64, vp]
+        L.l0s_gen_dedup_reset.argtypes = [vp, vp, i64]
+        L.l0s_gen_dedup.argtypes = [vp, vp, P(i64)]
         L.l0s_sis_prepare.argtypes = [vp, vp, i32, i64, vp, vp, i32]
         L.l0s_sis_scores.argtypes = [vp, vp, i64, i32, vp]
         L.l0s_search.argtypes = [vp, i32, i64, i64, i64, i32, vp, vp, vp, vp, P(i64), P(Stats)]
@@ -328,6 +331,7 @@ class Engine:
         check(lib().l0s_gen_eval(self.handle, int(kind), None if a is None else ptr(a), None if b is None else ptr(b), k,
                                  None if values is None else ptr(values), float(tol), float(min_abs), float(max_abs),
                                  float(dedup_tol), ptr(valid), ptr(h)), "l0s_gen_eval")
+        self._gen_last_count = k
         return valid.view(bool), h.tobytes()
 
     def gen_take(self, rows, host: bool = False):
@@ -338,6 +342,23 @@ class Engine:
         check(lib().l0s_gen_take(self.handle, ptr(rows), rows.shape[0], None if out is None else ptr(out),
                                  ctypes.byref(dev)), "l0s_gen_take")
         return out, dev.value
+
+    def gen_dedup_reset(self, fingerprints) -> None:
+        """Seed the device fingerprint set (iterable of 16-byte fingerprints, or a (k, 2) uint64 array)."""
+        if isinstance(fingerprints, np.ndarray):
+            seed = np.ascontiguousarray(fingerprints, dtype=np.uint64).reshape(-1, 2)
+        else:
+            seed = np.frombuffer(b"".join(bytes(f) for f in fingerprints), dtype="<u8").reshape(-1, 2)
+            seed = np.ascontiguousarray(seed)
+        check(lib().l0s_gen_dedup_reset(self.handle, ptr(seed) if len(seed) else None, len(seed)), "l0s_gen_dedup_reset")
+
+    def gen_dedup(self) -> np.ndarray:
+        """Kept flags of the last gen_eval's candidates (valid, fingerprint not seen earlier in the stream)."""
+        n = self._gen_last_count
+        kept = np.zeros(n, dtype=np.uint8)
+        cnt = ctypes.c_int64(0)
+        check(lib().l0s_gen_dedup(self.handle, ptr(kept), ctypes.byref(cnt)), "l0s_gen_dedup")
+        return kept.astype(bool)
 
     def gen_fetch(self, rows) -> np.ndarray:
         """Rows of the taken block to the host (pool dtype)."""

@@ -155,6 +155,8 @@ struct l0s_ctx {
     const double* src_y = nullptr;
     const int64_t* src_perm = nullptr;
     DBuf res_tup, res_coef, res_out;
+    DBuf dd_lo, dd_hi, dd_owner, dd_state, dd_used, dd_kept, dd_seed;  // last-rung value dedup (dedup.cu)
+    unsigned long long dd_mask = 0, dd_epoch = 0;
 
     ~l0s_ctx() {
         if (stager) host_stager_destroy(stager);
@@ -164,7 +166,7 @@ struct l0s_ctx {
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
                        &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr, &sis_y, &sis_yc, &sis_sy, &sis_perm,
                        &sis_bounds, &sis_F, &sis_out, &sis_dest, &sis_tE, &sis_tpoff, &oz_q, &oz_ex, &oz_koff,
-                       &res_tup, &res_coef, &res_out, &gen_pool, &gen_pi, &gen_pj, &gen_vals, &gen_valid, &gen_hash, &gen_take, &gen_rows, &gen_out};
+                       &res_tup, &res_coef, &res_out, &dd_lo, &dd_hi, &dd_owner, &dd_state, &dd_used, &dd_kept, &dd_seed, &gen_pool, &gen_pi, &gen_pj, &gen_vals, &gen_valid, &gen_hash, &gen_take, &gen_rows, &gen_out};
         for (DBuf* b : all) b->release();
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -1746,6 +1748,95 @@ int l0s_gen_fetch(l0s_ctx* c, const int32_t* rows, int64_t count, void* host_out
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(host_out, c->gen_out.p, w * count * s, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
+    return L0S_OK;
+}
+
+// ---------------------------------------------------------------------------
+// The last rung's value dedup on the device (dedup.cu; generation.py:364-385)
+// ---------------------------------------------------------------------------
+
+static DedupTable dedup_view(l0s_ctx* c) {
+    return DedupTable{c->dd_lo.as<unsigned long long>(), c->dd_hi.as<unsigned long long>(),
+                      c->dd_owner.as<unsigned long long>(), c->dd_state.as<unsigned>(),
+                      c->dd_used.as<unsigned long long>(), c->dd_mask};
+}
+
+static int dedup_alloc(l0s_ctx* c, unsigned long long cap) {
+    CK(c->dd_lo.ensure(sizeof(unsigned long long) * cap));
+    CK(c->dd_hi.ensure(sizeof(unsigned long long) * cap));
+    CK(c->dd_owner.ensure(sizeof(unsigned long long) * cap));
+    CK(c->dd_state.ensure(sizeof(unsigned) * cap));
+    CK(c->dd_used.ensure(sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(c->dd_state.p, 0, sizeof(unsigned) * cap, c->st));
+    CK(cudaMemsetAsync(c->dd_used.p, 0, sizeof(unsigned long long), c->st));
+    c->dd_mask = cap - 1;
+    return L0S_OK;
+}
+
+// keep the load factor <= 1/2 for `more` further insertions (rehash into a doubled table)
+static int dedup_reserve(l0s_ctx* c, int64_t more) {
+    unsigned long long used = 0;
+    CK(cudaMemcpyAsync(&used, c->dd_used.p, sizeof used, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    unsigned long long cap = c->dd_mask + 1;
+    if (2 * (used + (unsigned long long)more) <= cap) return L0S_OK;
+    while (2 * (used + (unsigned long long)more) > cap) cap *= 2;
+    DBuf lo, hi, own, stt, usd;
+    std::swap(lo, c->dd_lo);
+    std::swap(hi, c->dd_hi);
+    std::swap(own, c->dd_owner);
+    std::swap(stt, c->dd_state);
+    std::swap(usd, c->dd_used);
+    const DedupTable from{lo.as<unsigned long long>(), hi.as<unsigned long long>(), own.as<unsigned long long>(),
+                          stt.as<unsigned>(), usd.as<unsigned long long>(), c->dd_mask};
+    int rc = dedup_alloc(c, cap);
+    if (rc) return rc;
+    launch_dedup_rehash(from, dedup_view(c), c->st);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->st));  // the old table is released on return
+    return L0S_OK;
+}
+
+int l0s_gen_dedup_reset(l0s_ctx* c, const uint64_t* seed, int64_t count) {
+    if (!c) return fail(L0S_EINVAL, "null context");
+    if (count < 0) return fail(L0S_EINVAL, "negative seed count");
+    CK(cudaSetDevice(c->dev));
+    unsigned long long cap = (unsigned long long)1 << 20;
+    while (cap < 4ull * (unsigned long long)count) cap *= 2;
+    int rc = dedup_alloc(c, cap);
+    if (rc) return rc;
+    c->dd_epoch = 0;  // the seed (the pool's fingerprints) owns epoch 0
+    if (count > 0) {
+        CK(c->dd_seed.ensure(sizeof(uint64_t) * 2 * count));
+        CK(cudaMemcpyAsync(c->dd_seed.p, seed, sizeof(uint64_t) * 2 * count, cudaMemcpyHostToDevice, c->st));
+        launch_dedup_insert(dedup_view(c), nullptr, c->dd_seed.as<unsigned long long>(), count, 0, c->st);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(c->st));
+    return L0S_OK;
+}
+
+int l0s_gen_dedup(l0s_ctx* c, uint8_t* out_kept, int64_t* out_count) {
+    if (!c || c->dd_mask == 0) return fail(L0S_ESTATE, "l0s_gen_dedup_reset must be called first");
+    if (c->gen_count < 1) return fail(L0S_ESTATE, "no evaluated candidates (l0s_gen_eval)");
+    CK(cudaSetDevice(c->dev));
+    const int64_t n = c->gen_count;
+    int rc = dedup_reserve(c, n);
+    if (rc) return rc;
+    ++c->dd_epoch;
+    CK(c->dd_kept.ensure((size_t)n));
+    launch_dedup_insert(dedup_view(c), c->gen_valid.as<unsigned char>(), c->gen_hash.as<unsigned long long>(), n,
+                        c->dd_epoch, c->st);
+    launch_dedup_mark(dedup_view(c), c->gen_valid.as<unsigned char>(), c->gen_hash.as<unsigned long long>(), n,
+                      c->dd_epoch, c->dd_kept.as<unsigned char>(), c->st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out_kept, c->dd_kept.p, (size_t)n, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (out_count) {
+        int64_t k = 0;
+        for (int64_t x = 0; x < n; ++x) k += out_kept[x] != 0;
+        *out_count = k;
+    }
     return L0S_OK;
 }
 

@@ -148,6 +148,21 @@ struct alignas(64) TmaDesc {
 // per-thread error message of the C ABI (api.cu): returns `code`
 int set_error(int code, const char* msg);
 
+// ---- streamed last rung: value dedup on the device (dedup.cu) ----
+struct DedupTable {
+    unsigned long long* lo;     // [mask + 1] fingerprint words
+    unsigned long long* hi;
+    unsigned long long* owner;  // (epoch << 32) | index of the first occurrence
+    unsigned* state;            // 0 empty, 1 being written, 2 ready
+    unsigned long long* used;   // entries inserted
+    unsigned long long mask;    // capacity - 1 (a power of two)
+};
+void launch_dedup_insert(DedupTable t, const unsigned char* valid, const unsigned long long* hash, int64_t count,
+                         unsigned long long epoch, cudaStream_t st);
+void launch_dedup_mark(DedupTable t, const unsigned char* valid, const unsigned long long* hash, int64_t count,
+                       unsigned long long epoch, unsigned char* kept, cudaStream_t st);
+void launch_dedup_rehash(DedupTable from, DedupTable to, cudaStream_t st);
+
 // ---- host -> device copies from pageable memory (hostcopy.cu) ----
 struct HostStager;
 HostStager* host_stager_create();  // nullptr when no pinned memory could be had

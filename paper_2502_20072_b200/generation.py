@@ -212,6 +212,11 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
     with _lock:
         eng.gen_pool(pool.values_matrix())
     fps = pool_fingerprints(eng, pool)
+    kinds0 = [op.kind for op in config.operators]
+    device_walk = len(set(kinds0)) == len(kinds0) and (len(pool) == 0 or pool.max_rung() < target_rung)
+    if device_walk:  # the value dedup runs on the device, seeded with the pool's fingerprints
+        with _lock:
+            eng.gen_dedup_reset(fps)
     feats = pool.features
     fkeys = [f.key for f in feats]
     index_of = {k: x for x, k in enumerate(fkeys)}
@@ -251,9 +256,17 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
                 else:
                     with _lock:
                         valid, h = eng.gen_eval(kind, pi=pi, pj=pj, **limits)
-                kept = []
                 rows_ok = np.flatnonzero(valid)
                 stats.n_invalid += len(pi) - len(rows_ok)
+                if device_walk:
+                    # keys cannot collide (distinct operator kinds): only the value test remains, and
+                    # the device's ordered-first-owner set decides it (dedup.cu)
+                    with _lock:
+                        kept = np.flatnonzero(eng.gen_dedup()).tolist()
+                    stats.n_dup_value += len(rows_ok) - len(kept)
+                    rows_ok = rows_ok[:0]
+                else:
+                    kept = []
                 h64 = np.frombuffer(h, dtype="<u8")[0::2][rows_ok].tolist()
                 hv = np.frombuffer(h, dtype="V16")[rows_ok].tolist() if len(rows_ok) else []
                 li, lj = pi[rows_ok].tolist(), pj[rows_ok].tolist()
