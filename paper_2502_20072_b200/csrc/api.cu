@@ -1048,11 +1048,12 @@ static int search_exact_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_
         int rc = run_exact(c, n, c->ex_ranks.as<int64_t>(), nullptr, cnt, false, &st->n_launches);
         if (rc) return rc;
         // sort (score, rank) on device; non-finite scores sort last (ord_enc maps +inf above all finite)
-        sort_pairs(c->ex_score.as<double>(), c->ex_ranks.as<int64_t>(), c->lb_tmp.as<double>(),
-                   c->rank_tmp.as<int64_t>(), cnt, c->sort_tmp.p, tb, c->st);
-        st->n_launches += 3;
-        // the radix sort is stable and the ranks enter in increasing order, so the first
-        // `keep` entries are the chunk's best by (score, rank); non-finite scores sort last
+        const int ns = sort_pairs(c->ex_score.as<double>(), c->ex_ranks.as<int64_t>(), c->lb_tmp.as<double>(),
+                                  c->rank_tmp.as<int64_t>(), cnt, c->sort_tmp.p, tb, c->st);
+        if (ns < 0) return fail(L0S_ECUDA, "sort scratch too small");
+        st->n_launches += ns;
+        // sorted by (score, rank): the first `keep` entries are the chunk's best in the
+        // reference's order (search.py:303); non-finite scores sort last
         int64_t take = std::min<int64_t>(cnt, keep);
         std::vector<double> sc((size_t)take);
         std::vector<int64_t> rk((size_t)take);
@@ -1302,8 +1303,12 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
         tb = sort_pairs_temp_bytes((int64_t)ncand);
         CK(c->sort_tmp.ensure(tb));
     }
-    sort_pairs(cl, cr, c->lb_tmp.as<double>(), c->rank_tmp.as<int64_t>(), (int64_t)ncand, c->sort_tmp.p, tb, c->st);
-    st->n_launches += 3;
+    {
+        const int ns = sort_pairs(cl, cr, c->lb_tmp.as<double>(), c->rank_tmp.as<int64_t>(), (int64_t)ncand, c->sort_tmp.p,
+                                  tb, c->st);
+        if (ns < 0) return fail(L0S_ECUDA, "sort scratch too small");
+        st->n_launches += ns;
+    }
     const int64_t nc = std::min<int64_t>((int64_t)ncand, kc);
     // every excluded tuple has lb >= G_lb (SSR units): the K'-th smallest gathered bound, or
     // -- fewer gathered -- the final shared threshold (+inf: nothing was ever dropped)
@@ -1403,6 +1408,80 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
 
 }  // extern "C"
 
+// Dimension 1 (fit1.cu): a lower bound per feature, sorted on the device, refit in order until
+// the keep-th exact score is certified -- every excluded feature's bound lies above it by the
+// reference's error margin (the same certificate as the screened sweeps).
+static int search_fast1(l0s_ctx* c, int64_t keep, int64_t rb, int64_t re, std::vector<Cand>& best, l0s_stats* st) {
+    const int64_t cnt = re - rb;
+    CK(c->coll_lb.ensure(sizeof(double) * cnt));
+    CK(c->coll_rank.ensure(sizeof(int64_t) * cnt));
+    CK(c->ill.ensure(sizeof(int64_t) * cnt));
+    CK(c->ill_cnt.ensure(sizeof(unsigned long long)));
+    const size_t tb = sort_pairs_temp_bytes(cnt);
+    CK(c->sort_tmp.ensure(tb));
+    FitArgs a{};
+    fill_fit_common(c, a, 1);
+    a.ill = c->ill.as<int64_t>();
+    a.ill_cnt = c->ill_cnt.as<unsigned long long>();
+    a.ill_cap = cnt;
+    CK(cudaMemsetAsync(c->ill_cnt.p, 0, sizeof(unsigned long long), c->st));
+    double* cl = c->coll_lb.as<double>();
+    int64_t* cr = c->coll_rank.as<int64_t>();
+    cudaEventRecord(c->ev[2], c->st);
+    launch_fit1(a, rb, re, cl, cr, c->st);
+    const int ns = sort_pairs(cl, cr, nullptr, nullptr, cnt, c->sort_tmp.p, tb, c->st);
+    cudaEventRecord(c->ev[3], c->st);
+    CK(cudaGetLastError());
+    if (ns < 0) return fail(L0S_ECUDA, "sort scratch too small");
+    st->n_fit_launches++;
+    st->n_launches += 1 + ns;
+    unsigned long long nill = 0;
+    CK(cudaMemcpyAsync(&nill, c->ill_cnt.p, sizeof nill, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    st->ms_fit += elapsed(c->ev[2], c->ev[3]);
+    st->n_eval += cnt * c->T;
+    double yy = 0.0;
+    for (double v : c->yyu_h) yy += v;
+    auto margin_of = [&](double sk) { return 1e-10 * std::fabs(sk) + 64.0 * kEps * yy / (double)c->s; };
+    // refit the sorted bounds in growing prefixes until the next excluded bound certifies
+    cudaEventRecord(c->ev[2], c->st);
+    int64_t done = 0, upto = std::min<int64_t>(cnt, std::max<int64_t>(64, keep + 32));
+    double G_lb = INFINITY;
+    for (;;) {
+        std::vector<double> lbs((size_t)(upto - done + (upto < cnt ? 1 : 0)));
+        CK(cudaMemcpyAsync(lbs.data(), cl + done, sizeof(double) * lbs.size(), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        int64_t fin = done;  // +inf bounds (ill, dead) sort last and are never refit from this list
+        while (fin < upto && std::isfinite(lbs[(size_t)(fin - done)])) ++fin;
+        std::vector<Cand> exact;
+        int rc = exact_ranks_to_host(c, 1, cr + done, fin - done, exact, &st->n_launches, &c->recs);
+        if (rc) return rc;
+        merge_best(best, exact, keep);
+        st->n_candidates += fin - done;
+        G_lb = (fin < upto || upto == cnt) ? INFINITY : lbs.back();
+        const double sk = ((int64_t)best.size() >= keep) ? best[(size_t)keep - 1].score : INFINITY;
+        if (!std::isfinite(G_lb) || G_lb / (double)c->s > sk + margin_of(sk)) {
+            st->margin = G_lb / (double)c->s - sk;
+            break;
+        }
+        st->n_rescan++;
+        done = upto;
+        upto = std::min<int64_t>(cnt, 2 * upto);
+    }
+    if (nill > 0) {
+        int rc = screen_ill(c, 1, (int64_t)nill, keep, best, st);
+        if (rc) return rc;
+    }
+    cudaEventRecord(c->ev[3], c->st);
+    CK(cudaStreamSynchronize(c->st));
+    st->ms_exact += elapsed(c->ev[2], c->ev[3]);
+    st->n_ill = (int64_t)nill;
+    st->theta = G_lb;
+    st->certified = 1;
+    st->mode_used = L0S_MODE_FAST;
+    return L0S_OK;
+}
+
 // The screened search of [rb, re); a fixed device buffer that overflows (ill-conditioned tuples,
 // collected candidates, rescan) splits the range in halves, each certified on its own, and the
 // (score, rank) merge of certified ranges is the whole range's (search.py:303).
@@ -1451,13 +1530,13 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
     cudaEventCreate(&t1);
     cudaEventRecord(t0, c->st);
     // the screen's error model is for fp64 arithmetic in the reference (precision="fp64")
-    bool fast_ok = (n >= 2 && n <= 4) && c->T <= fit3_max_tasks() && keep <= kKeepMax;
+    bool fast_ok = (n >= 1 && n <= 4) && c->T <= fit3_max_tasks() && keep <= kKeepMax;
     bool use_fast;
     if (mode == L0S_MODE_FAST) {
         if (!fast_ok) {
             cudaEventDestroy(t0);
             cudaEventDestroy(t1);
-            return fail(L0S_EINVAL, "screened path needs n in {2, 3, 4}, ntasks <= %d, keep <= %lld",
+            return fail(L0S_EINVAL, "screened path needs n in {1, 2, 3, 4}, ntasks <= %d, keep <= %lld",
                         fit3_max_tasks(), (long long)kKeepMax);
         }
         use_fast = true;
@@ -1468,7 +1547,9 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
         use_fast = fast_ok && work > 2e8;
     }
     std::vector<Cand> best;
-    rc = use_fast ? search_fast_split(c, n, keep, rb, re, best, st, 0) : search_exact_mode(c, n, keep, rb, re, best, st);
+    rc = !use_fast ? search_exact_mode(c, n, keep, rb, re, best, st)
+         : n == 1  ? search_fast1(c, keep, rb, re, best, st)
+                   : search_fast_split(c, n, keep, rb, re, best, st, 0);
     if (rc) {
         cudaEventDestroy(t0);
         cudaEventDestroy(t1);
@@ -1536,9 +1617,9 @@ int l0s_search_part(l0s_ctx* c, int n, int64_t keep, int part, int nparts, int m
     int rc = (n >= 1 && c->m >= n) ? l0s_count(c->m, n, &N) : L0S_OK;
     if (rc) return rc;
     // every part must take the same path: decided on the whole problem, as l0s_search would
-    const bool fast_ok = (n >= 2 && n <= 4) && c->T <= fit3_max_tasks() && keep >= 1 && keep <= kKeepMax;
+    const bool fast_ok = (n >= 1 && n <= 4) && c->T <= fit3_max_tasks() && keep >= 1 && keep <= kKeepMax;
     const bool fast = mode == L0S_MODE_FAST || (mode == L0S_MODE_AUTO && fast_ok && (double)N * (double)c->s > 2e8);
-    if (!fast || !fast_ok || nparts == 1)  // contiguous rank ranges (search.py:266-271)
+    if (!fast || !fast_ok || nparts == 1 || n == 1)  // contiguous rank ranges (search.py:266-271)
         return l0s_search(c, n, keep, N / nparts * part + std::min<int64_t>(part, N % nparts),
                           N / nparts * (part + 1) + std::min<int64_t>(part + 1, N % nparts), mode, out_scores,
                           out_ranks, out_coef, out_ssr, out_count, stats);

@@ -41,16 +41,16 @@ namespace {
 #define L0S_C34_P 4
 #endif
 #ifndef L0S_C34_IB
-#define L0S_C34_IB 32
+#define L0S_C34_IB 24
 #endif
 #ifndef L0S_C34_MINB
-#define L0S_C34_MINB 1
+#define L0S_C34_MINB 2
 #endif
 #ifndef L0S_C34_UNROLL
 #define L0S_C34_UNROLL 1
 #endif
 #ifndef L0S_C34_NW
-#define L0S_C34_NW 8
+#define L0S_C34_NW 4
 #endif
 #ifndef L0S_C34_NBUF
 #define L0S_C34_NBUF 2
@@ -74,17 +74,50 @@ constexpr bool WREL = L0S_WREL;
 struct CfgT {
     int P, IB, MINB, UNROLL, NW, NBUF;
 };
-// 3-4 tasks: 16 warps of 2 pairs (<= 128 registers: the pair constants of every task stay in
-// registers and the compiler can interleave the rows; 8 warps of 4 pairs ran at 255 registers
-// with the FP64 pipe 34 % busy)
+// 3-4 tasks: two CTAs of 4 warps per SM, 4 pairs per thread, 24-row tiles (C3 fit 1.76 -> 1.55 ms
+// against one CTA of 8 warps: a warp waiting at its CTA's tile barrier leaves the SM sub-partition
+// to the other CTA's warp; 16 warps of 2 pairs spill at 128 registers, per-warp tile release,
+// staging only the first task slot and 3-4 CTAs per SM were slower -- tools/tune_fit.py)
 constexpr CfgT kCfg34{L0S_C34_P, L0S_C34_IB, L0S_C34_MINB, L0S_C34_UNROLL, L0S_C34_NW, L0S_C34_NBUF};
-constexpr CfgT kCfg12{4, 32, 2, 2, 8, 2};
-constexpr CfgT kCfg58{2, 16, 1, 1, 8, 2};
+// (P, IB, MINB, UNROLL, NW) for 1, 2 and 5-8 tasks (-DL0S_C1_NW=... etc. for tuning builds).
+// Measured on C3's features (tools/tune_fit.py): one task 4 CTAs x 4 warps (1.13 -> 1.04 ms
+// against 2 x 8), two tasks 3 x 4 warps with 24-row tiles (1.31 -> 1.19 ms); 5-8 tasks keep
+// one CTA of 8 warps (two CTAs of 4 were slower)
+#ifndef L0S_C1_NW
+#define L0S_C1_NW 4
+#endif
+#ifndef L0S_C1_MINB
+#define L0S_C1_MINB 4
+#endif
+#ifndef L0S_C2_NW
+#define L0S_C2_NW 4
+#endif
+#ifndef L0S_C2_MINB
+#define L0S_C2_MINB 3
+#endif
+#ifndef L0S_C2_IB
+#define L0S_C2_IB 24
+#endif
+#ifndef L0S_C58_P
+#define L0S_C58_P 2
+#endif
+#ifndef L0S_C58_IB
+#define L0S_C58_IB 16
+#endif
+#ifndef L0S_C58_MINB
+#define L0S_C58_MINB 1
+#endif
+#ifndef L0S_C58_NW
+#define L0S_C58_NW 8
+#endif
+constexpr CfgT kCfg1{4, 32, L0S_C1_MINB, 2, L0S_C1_NW, 2};
+constexpr CfgT kCfg2{4, L0S_C2_IB, L0S_C2_MINB, 1, L0S_C2_NW, 2};
+constexpr CfgT kCfg58{L0S_C58_P, L0S_C58_IB, L0S_C58_MINB, 1, L0S_C58_NW, 2};
 // Per task count: P = (j,k) pairs per thread, IB = rows per i-tile, MINB = CTAs per SM,
 // NW = warps per CTA (k-span = NW x P; the unit table follows it, fit3_kspan).
 template <int NT>
 struct Cfg {
-    static constexpr CfgT c = (NT <= 2) ? kCfg12 : (NT <= 4 ? kCfg34 : kCfg58);
+    static constexpr CfgT c = (NT == 1) ? kCfg1 : (NT == 2 ? kCfg2 : (NT <= 4 ? kCfg34 : kCfg58));
     static constexpr int P = c.P;
     static constexpr int IB = c.IB;
     static constexpr int NW = c.NW;
@@ -397,7 +430,14 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
             const int ib0 = i_lo + bi * IB;
             if (!WREL && bi + 1 < nib) load_tiles(buf ^ 1, ib0 + IB, j0, k0);
             wait_tiles(buf);
-            if (!WREL) __syncthreads();  // s_force of this tile (WREL: ordered by the tile's mbarrier)
+#ifndef L0S_TILE_BAR0
+#define L0S_TILE_BAR0 1
+#endif
+            // s_force of this tile would not need a CTA barrier (its writers' __syncwarp precedes
+            // the releasing arrive on the tile's mbarrier, which every reader acquires), but the
+            // warps kept in step run faster (C3 fit 1.557 ms with it, 1.571 without; random y
+            // 3.93 / 4.09 ms -- tools/tune_fit.py)
+            if (L0S_TILE_BAR0 && !WREL) __syncthreads();
             const double* T0 = sm + buf * BS;
             // a clean tile (warp-uniform): every row is below every lane's j and inside the unit,
             // and no row is iforce-flagged -- a row's pending bits are then just the sign bits
@@ -658,7 +698,7 @@ void launch_screen3(const FitArgs& a, const int64_t* tuples, int64_t count, doub
 int fit3_max_tasks() { return 1 << 16; }
 int fit_slots_per_cta() { return NW; }
 int fit3_slots_per_cta(int T) {
-    return T <= 2 ? Cfg<1>::NW : (T <= 4 ? Cfg<4>::NW : Cfg<8>::NW);
+    return T == 1 ? Cfg<1>::NW : (T == 2 ? Cfg<2>::NW : (T <= 4 ? Cfg<4>::NW : Cfg<8>::NW));
 }
 int fit3_kspan(int T) {
     switch (T) {

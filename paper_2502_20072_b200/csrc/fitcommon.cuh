@@ -14,6 +14,7 @@ constexpr int NW = 8;                 // warps per CTA
 #define L0S_CAP 256
 #endif
 constexpr int CAP = L0S_CAP;          // per-warp candidate buffer (K' <= CAP - 32)
+static_assert((CAP & (CAP - 1)) == 0, "warp_sort is a bitonic network over CAP entries");
 constexpr double FO_LIM = 1e-3;       // first-order validity: (eta + gam rho)(1 + n tr) <= FO_LIM
 constexpr double RANK_SLACK = 1.01;   // safety factor on the rank-rule certificate
 constexpr double LOOSE = 1e-3;        // bounds looser than this fraction of |y_c|^2 go to the exact kernel

@@ -222,6 +222,8 @@ struct FitArgs {
     int64_t coll_cap;
     unsigned long long* n_eval;  // out (optional): task-tuple evaluations of the sweep (executed work)
 };
+// n = 1 (fit1.cu): dense lower bounds of the features [rb, re) (+inf: ill or dead; ill ranks appended)
+void launch_fit1(const FitArgs& a, int64_t rb, int64_t re, double* out_lb, int64_t* out_rank, cudaStream_t st);
 int fit3_launch(const FitArgs& a, int nsm, cudaStream_t st);  // returns grid size (warp slots / 8)
 int fit3_grid(int T, int nsm);                                // grid fit3_launch will use
 int fit3_max_tasks();
@@ -260,10 +262,11 @@ bool make_tma_2d(TmaDesc* out, const double* G, unsigned long long cols, unsigne
 void launch_gather_candidates(const double* wl_lb, const int64_t* wl_rank, const int* wl_cnt, int slots,
                               int kc, const unsigned long long* theta_g, double* out_lb,
                               int64_t* out_rank, unsigned long long* out_cnt, cudaStream_t st);
-// sort (lb, rank) pairs ascending by lb (device radix sort), in place via temp buffers
+// sort (lb, rank) pairs ascending by (lb, rank) in place (sort.cu: shared-memory bitonic blocks
+// + merge-path rounds); returns the number of launches (-1: temp too small)
 size_t sort_pairs_temp_bytes(int64_t n);
-void sort_pairs(double* lb, int64_t* rank, double* lb_tmp, int64_t* rank_tmp, int64_t n, void* temp,
-                size_t temp_bytes, cudaStream_t st);
+int sort_pairs(double* lb, int64_t* rank, double* lb_tmp, int64_t* rank_tmp, int64_t n, void* temp,
+               size_t temp_bytes, cudaStream_t st);
 
 // ---- SIS projection scores (sis.cu), bit-identical to screening._chunk_scores ----
 int sis_max_targets();

@@ -220,3 +220,23 @@ def test_rejects_undersized_subspace(rng):
         l0_search(values, y, config=L0Config(dimension=3))
     with pytest.raises(ValueError):
         l0_search(values, y, config=None)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,dup", [(40, 6), (120, 10)])
+def test_exact_mode_sort_with_ties_matches_oracle(oracle, m, dup):
+    """The exact path sorts each chunk of scores on the device (sort.cu: one shared-memory
+    block for <= 8192 entries, merge rounds above): C(40, 3) = 9880 and C(120, 3) = 280840
+    tuples, with duplicated features so that many scores tie exactly and the rank decides
+    (search.py:303)."""
+    from paper_2502_20072_b200 import L0Config, l0_search
+
+    rng = np.random.default_rng(1000 + m)
+    values = rng.uniform(0.5, 2.0, size=(m, 30))
+    values[m - dup:] = values[:dup]  # exact duplicates: tuples differing by a twin tie
+    y = rng.standard_normal(30)
+    cfg = L0Config(dimension=3, autotune=False, n_models_store=60)
+    got = l0_search(values, y, config=cfg, mode="exact")
+    want = oracle.l0_search(values, y, None, 3, 60, "fp64")
+    assert [g.indices for g in got] == [w["indices"] for w in want]
+    assert bits_equal([g.score for g in got], [w["score"] for w in want])

@@ -56,8 +56,8 @@ def test_l0_search_matches_reference(name, mode):
     from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
 
     c = search_case(name)
-    if mode == "fast" and c["n"] not in (2, 3, 4):
-        pytest.skip("the screened path covers n in {2, 3, 4} (n = 1 and n >= 5 run the exact kernel)")
+    if mode == "fast" and c["n"] not in (1, 2, 3, 4):
+        pytest.skip("the screened path covers n in {1, 2, 3, 4} (n >= 5 runs the exact kernel)")
     cfg = L0Config(dimension=c["n"], n_models_store=c["keep"], precision=c["precision"], autotune=False)
     st = SearchStats()
     models = l0_search(c["values"], c["y"], c["slices"], cfg, stats=st, mode=mode)
@@ -853,3 +853,30 @@ def test_stage_extend_int8_gram_equals_full_stage(m0, m_new):
     got = eng.search(3, 10, 0, 2**63 - 1, "fast")
     for a, b in zip(got[:4], want[:4]):
         assert bits_equal(a, b)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("T", [1, 3])
+def test_fast_n1_matches_oracle(oracle, precision, T):
+    """Dimension 1 on the screened path (fit1.cu + search_fast1): every feature's bound, sorted,
+    refit until certified; near-constant features (ill: QR screen / exact refit), an exact
+    duplicate (tie by rank) and more features than one refit round (keep 100 of 3000)."""
+    from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
+
+    rng = np.random.default_rng(40 + T)
+    m, s = 3000, 90
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    v[5] = 1.5 + 1e-9 * rng.standard_normal(s)  # collides with the intercept
+    v[6] = 0.75 + 1e-4 * rng.standard_normal(s)
+    v[2999] = v[11]
+    y = 0.8 * v[11] + 0.3 * rng.standard_normal(s)
+    slices = [np.arange(t, s, T) for t in range(T)]
+    for keep in (1, 10, 100):
+        cfg = L0Config(dimension=1, n_models_store=keep, precision=precision, autotune=False)
+        st = SearchStats()
+        got = l0_search(v, y, slices, cfg, stats=st, mode="fast")
+        want = oracle.l0_search(v, y, slices, 1, keep, precision)
+        assert st.device["mode_used"] == 1 and st.device["certified"] == 1
+        assert [g.indices for g in got] == [w["indices"] for w in want]
+        assert bits_equal([g.score for g in got], [w["score"] for w in want])
+        assert all(bits_equal(g.coefficients, w["coefficients"]) for g, w in zip(got, want))

@@ -22,9 +22,10 @@ VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
     "base": (),
-    "slot0": ("L0S_FIT_SLOT0=1",),
-    "unroll2": ("L0S_C34_UNROLL=2",),
+    "bar0": ("L0S_TILE_BAR0=1",),
 }
+if os.environ.get("L0S_TUNE_ONLY"):
+    VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["L0S_TUNE_ONLY"].split(",")}
 
 
 def build_all():
@@ -48,6 +49,9 @@ def time_one(steps: int = 5):
     import scale_cases
 
     v, y, slices = scale_cases.c3(os.environ.get("L0S_TUNE_Y", "planted"))
+    tasks = int(os.environ.get("L0S_TUNE_T", "4"))
+    if tasks != 4:  # the same features, y re-planted on `tasks` round-robin tasks
+        slices = [np.arange(t, bench.S, tasks) for t in range(tasks)]
     perm, bounds, _ = _partition(bench.S, slices)
     eng = _lib.engine(0)
     eng.stage(v, y, perm, bounds, "fp64")
