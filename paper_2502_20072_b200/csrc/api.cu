@@ -932,7 +932,7 @@ static void fill_fit_common(l0s_ctx* c, FitArgs& a, int n) {
 
 int l0s_screen_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags) {
     if (!c || !c->staged) return fail(L0S_ESTATE, "l0s_stage must be called first");
-    if (n < 2 || n > 4) return fail(L0S_EINVAL, "screened bounds are implemented for n = 2, 3 and 4");
+    if (n < 2 || n > 5) return fail(L0S_EINVAL, "screened bounds are implemented for n = 2 to 5");
     if (count <= 0) return L0S_OK;
     CK(cudaSetDevice(c->dev));
     int rc = ensure_binom(c, n);
@@ -947,8 +947,10 @@ int l0s_screen_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, d
         launch_screen2(a, c->ex_tuples.as<int64_t>(), count, c->cand_lb.as<double>(), c->ex_ok.as<int32_t>(), c->st);
     else if (n == 3)
         launch_screen3(a, c->ex_tuples.as<int64_t>(), count, c->cand_lb.as<double>(), c->ex_ok.as<int32_t>(), c->st);
-    else
+    else if (n == 4)
         launch_screen4(a, c->ex_tuples.as<int64_t>(), count, c->cand_lb.as<double>(), c->ex_ok.as<int32_t>(), c->st);
+    else
+        launch_screen5(a, c->ex_tuples.as<int64_t>(), count, c->cand_lb.as<double>(), c->ex_ok.as<int32_t>(), c->st);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out_lb, c->cand_lb.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(out_flags, c->ex_ok.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, c->st));
@@ -1149,7 +1151,8 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
         for (int64_t v = 0; v < c->m; ++v) pre[(size_t)v + 1] = pre[(size_t)v] + binom_sat(c->m - 1 - v, n - 1);
         c->units_h = n == 2 ? fit2_units(c->m, pre, rb, re)
                      : n == 3 ? fit3_units(c->m, c->T, N, pre, rb, re, c->nparts == 1)
-                              : fit4_units(c->m, c->T, pre, rb, re);
+                     : n == 4 ? fit4_units(c->m, c->T, pre, rb, re)
+                              : fit5_units(c->m, c->T, pre, rb, re);
         if (c->nparts > 1) {
             // a part gets 1/nparts of the units: split their i ranges until every part still has
             // several units per CTA, then deal them round-robin over the longest-first order
@@ -1189,11 +1192,15 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     const int kc = big ? (int)(keep + std::max<int64_t>(32, keep / 2))  // slack: near-ties among the keep best
                        : (c->nparts > 1 ? 128 : (int)std::min<int64_t>(128, std::max<int64_t>(64, keep + 32)));
     const int64_t coll_cap = (int64_t)1 << 24;
-    const int grid = n == 2 ? fit2_grid(c->T, c->nsm) : n == 3 ? fit3_grid(c->T, c->nsm) : fit4_grid(c->T, c->nsm);
+    const int grid = n == 2   ? fit2_grid(c->T, c->nsm)
+                     : n == 3 ? fit3_grid(c->T, c->nsm)
+                     : n == 4 ? fit4_grid(c->T, c->nsm)
+                              : fit5_grid(c->T, c->nsm);
     auto launch_fit = [&](const FitArgs& fa) {
-        return n == 2 ? fit2_launch(fa, c->nsm, c->st)
+        return n == 2   ? fit2_launch(fa, c->nsm, c->st)
                : n == 3 ? fit3_launch(fa, c->nsm, c->st)
-                        : fit4_launch(fa, c->nsm, c->st);
+               : n == 4 ? fit4_launch(fa, c->nsm, c->st)
+                        : fit5_launch(fa, c->nsm, c->st);
     };
     const int slots = grid * (n == 3 ? fit3_slots_per_cta(c->T) : fit_slots_per_cta());
     const int64_t ill_cap = (int64_t)1 << 26;  // 512 MB of ranks; overflow is reported, never dropped
@@ -1201,7 +1208,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     CK(c->n_eval.ensure(sizeof(unsigned long long)));
     CK(c->theta_g.ensure(sizeof(unsigned long long)));
     CK(c->hist.ensure(sizeof(unsigned) * HIST_BINS));
-    CK(c->seedbuf.ensure(sizeof(int64_t) * 1024 * 5 + 256));  // subsets, bounds, count, cap
+    CK(c->seedbuf.ensure(sizeof(int64_t) * 1024 * (kSeedW + 1) + 256));  // subsets, bounds, count, cap
     CK(c->wl_lb.ensure(sizeof(double) * slots * (big ? 1 : kc)));
     CK(c->wl_rank.ensure(sizeof(int64_t) * slots * (big ? 1 : kc)));
     CK(c->wl_cnt.ensure(sizeof(int) * slots));
@@ -1241,9 +1248,9 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     a.theta_g = c->theta_g.as<unsigned long long>();
     a.hist = c->hist.as<unsigned>();
     a.seed_tup = c->seedbuf.as<int64_t>();
-    a.seed_ub = c->seedbuf.as<double>() + 1024 * 4;
-    a.seed_n = reinterpret_cast<int*>(c->seedbuf.as<double>() + 1024 * 5);
-    a.seed_cap = c->seedbuf.as<double>() + 1024 * 5 + 4;
+    a.seed_ub = c->seedbuf.as<double>() + 1024 * kSeedW;
+    a.seed_n = reinterpret_cast<int*>(c->seedbuf.as<double>() + 1024 * (kSeedW + 1));
+    a.seed_cap = c->seedbuf.as<double>() + 1024 * (kSeedW + 1) + 4;
     a.keep = (int)keep;
     {
         double yy_top = 0.0;  // uncentered total |y|^2 >= every pooled bound
@@ -1530,13 +1537,13 @@ int l0s_search(l0s_ctx* c, int n, int64_t keep, int64_t rank_begin, int64_t rank
     cudaEventCreate(&t1);
     cudaEventRecord(t0, c->st);
     // the screen's error model is for fp64 arithmetic in the reference (precision="fp64")
-    bool fast_ok = (n >= 1 && n <= 4) && c->T <= fit3_max_tasks() && keep <= kKeepMax;
+    bool fast_ok = (n >= 1 && n <= 4 || (n == 5 && c->m < 32768)) && c->T <= fit3_max_tasks() && keep <= kKeepMax;
     bool use_fast;
     if (mode == L0S_MODE_FAST) {
         if (!fast_ok) {
             cudaEventDestroy(t0);
             cudaEventDestroy(t1);
-            return fail(L0S_EINVAL, "screened path needs n in {1, 2, 3, 4}, ntasks <= %d, keep <= %lld",
+            return fail(L0S_EINVAL, "screened path needs n in 1..5, ntasks <= %d, keep <= %lld",
                         fit3_max_tasks(), (long long)kKeepMax);
         }
         use_fast = true;
@@ -1617,7 +1624,8 @@ int l0s_search_part(l0s_ctx* c, int n, int64_t keep, int part, int nparts, int m
     int rc = (n >= 1 && c->m >= n) ? l0s_count(c->m, n, &N) : L0S_OK;
     if (rc) return rc;
     // every part must take the same path: decided on the whole problem, as l0s_search would
-    const bool fast_ok = (n >= 1 && n <= 4) && c->T <= fit3_max_tasks() && keep >= 1 && keep <= kKeepMax;
+    const bool fast_ok = (n >= 1 && n <= 4 || (n == 5 && c->m < 32768)) && c->T <= fit3_max_tasks() && keep >= 1 &&
+                         keep <= kKeepMax;
     const bool fast = mode == L0S_MODE_FAST || (mode == L0S_MODE_AUTO && fast_ok && (double)N * (double)c->s > 2e8);
     if (!fast || !fast_ok || nparts == 1 || n == 1)  // contiguous rank ranges (search.py:266-271)
         return l0s_search(c, n, keep, N / nparts * part + std::min<int64_t>(part, N % nparts),

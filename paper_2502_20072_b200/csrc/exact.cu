@@ -445,12 +445,9 @@ void launch_exact(const ExactArgs& a, double* ssr_tmp, int32_t* ok_tmp, cudaStre
     const size_t wsz = a.precision == 1 ? 4 : 8;
     const size_t smem = (size_t)a.ld * (size_t)(a.n + 2) * wsz;
     if (smem <= (size_t)200 * 1024 && a.n <= kMaxN) {
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaFuncSetAttribute(k_exact_smem<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            cudaFuncSetAttribute(k_exact_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            attr_set = true;
-        }
+        // per device (a process may drive several, api.cu l0s_group_*): set on every call
+        cudaFuncSetAttribute(k_exact_smem<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_exact_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         const int64_t max_grid = (int64_t)1 << 30;
         for (int64_t g0 = 0; g0 < total; g0 += max_grid) {
             unsigned blocks = (unsigned)std::min(max_grid, total - g0);

@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(128) k_seed_eval4(const __grid_constant__ FitA
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= *a.seed_n) return;
     double lb = 0.0, ub = INFINITY;
-    const int fl = a.seed_tup[c * 4] >= 0 ? eval_tuple4(a, a.seed_tup[c * 4 + 0], a.seed_tup[c * 4 + 1], a.seed_tup[c * 4 + 2], a.seed_tup[c * 4 + 3], &lb, &ub) : 0;
+    const int fl = a.seed_tup[c * kSeedW] >= 0 ? eval_tuple4(a, a.seed_tup[c * kSeedW + 0], a.seed_tup[c * kSeedW + 1], a.seed_tup[c * kSeedW + 2], a.seed_tup[c * kSeedW + 3], &lb, &ub) : 0;
     a.seed_ub[c] = (fl == 3 && ub == ub) ? ub : INFINITY;
 }
 

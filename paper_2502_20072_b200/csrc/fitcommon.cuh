@@ -327,7 +327,7 @@ constexpr int SEED_MAX = 1024;
 constexpr int SEED_POOL = 16384;  // candidate features of the seed (dynamic smem doubles)
 struct SeedSmem {
     double ub[SEED_MAX];
-    short sub[SEED_MAX][4];
+    short sub[SEED_MAX][kSeedW];
     int top[32];
     double rv[32];
     int ri[32];
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(512, 1) k_seed_select(const __grid_constant__ 
     for (int c = threadIdx.x; c < ns; c += blockDim.x) {
         int64_t f[N];
         const bool in = seed_tuple<N>(a, S, c, f);
-        for (int x = 0; x < N; ++x) a.seed_tup[c * 4 + x] = in ? f[x] : -1;
+        for (int x = 0; x < N; ++x) a.seed_tup[c * kSeedW + x] = in ? f[x] : -1;
     }
     if (threadIdx.x == 0) *a.seed_n = ns;
 }

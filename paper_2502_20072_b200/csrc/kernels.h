@@ -171,6 +171,7 @@ bool host_is_pinned(const void* p);
 cudaError_t host_stager_copy_rows(HostStager* h, void* dst, const std::function<const void*(int64_t)>& row,
                                   int64_t nrows, size_t row_bytes, cudaStream_t st);
 
+constexpr int kSeedW = 5;  // int64 slots per threshold-seed subset (n <= 5)
 struct FitArgs {
     TmaDesc tmJ;  // box: 32 columns (j-block) x IB rows
     TmaDesc tmK;  // box: KSPAN columns (k- or l-span) x IB rows
@@ -204,7 +205,7 @@ struct FitArgs {
     double theta0;
     unsigned long long* theta_g;
     unsigned* hist;          // [HIST_BINS] global lower-bound histogram (fitcommon.cuh)
-    int64_t* seed_tup;       // [SEED_MAX][4] threshold-seed subsets (fitcommon.cuh)
+    int64_t* seed_tup;       // [SEED_MAX][kSeedW] threshold-seed subsets (fitcommon.cuh)
     double* seed_ub;         // [SEED_MAX] their upper bounds
     int* seed_n;             // subset count
     double* seed_cap;        // out: the keep-th smallest certified upper bound of the seed (SSR units)
@@ -248,6 +249,13 @@ int fit4_launch(const FitArgs& a, int nsm, cudaStream_t st);
 int fit4_grid(int T, int nsm);
 std::vector<int4> fit4_units(int64_t m, int T, const std::vector<int64_t>& c3_prefix, int64_t rank_lo,
                              int64_t rank_hi);
+// ---- screened fit, n = 5 (fit5.cu) ----
+int fit5_launch(const FitArgs& a, int nsm, cudaStream_t st);
+int fit5_grid(int T, int nsm);
+std::vector<int4> fit5_units(int64_t m, int T, const std::vector<int64_t>& c4_prefix, int64_t rank_lo,
+                             int64_t rank_hi);
+void launch_screen5(const FitArgs& a, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags,
+                    cudaStream_t st);
 void launch_screen4(const FitArgs& a, const int64_t* tuples, int64_t count, double* out_lb, int32_t* out_flags,
                     cudaStream_t st);
 

@@ -56,8 +56,6 @@ def test_l0_search_matches_reference(name, mode):
     from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
 
     c = search_case(name)
-    if mode == "fast" and c["n"] not in (1, 2, 3, 4):
-        pytest.skip("the screened path covers n in {1, 2, 3, 4} (n >= 5 runs the exact kernel)")
     cfg = L0Config(dimension=c["n"], n_models_store=c["keep"], precision=c["precision"], autotune=False)
     st = SearchStats()
     models = l0_search(c["values"], c["y"], c["slices"], cfg, stats=st, mode=mode)
@@ -880,3 +878,32 @@ def test_fast_n1_matches_oracle(oracle, precision, T):
         assert [g.indices for g in got] == [w["indices"] for w in want]
         assert bits_equal([g.score for g in got], [w["score"] for w in want])
         assert all(bits_equal(g.coefficients, w["coefficients"]) for g, w in zip(got, want))
+
+
+@pytest.mark.parametrize("T", [1, 2, 5])
+@pytest.mark.parametrize("kind", ["planted", "random", "collinear"])
+def test_fast_n5_matches_oracle(oracle, T, kind):
+    """Dimension 5 on the screened path (fit5.cu): exhaustive oracle parity on C(26, 5) = 65780
+    tuples -- planted, random (dense near-ties) and near-collinear features (the QR screen /
+    exact refit of ill tuples), 1, 2 and 5 tasks (5 > the sweep's 4 task slots)."""
+    from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
+
+    rng = np.random.default_rng({"planted": 1, "random": 2, "collinear": 3}[kind] * 10 + T)
+    m, s = 26, 80
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    if kind == "collinear":
+        v[7] = v[3] + 1e-7 * rng.standard_normal(s)
+        v[20] = v[12] + 1e-11 * rng.standard_normal(s)
+    if kind == "random":
+        y = rng.standard_normal(s)
+    else:
+        y = 1.2 * v[2] - 0.8 * v[9] + 0.5 * v[14] + 0.3 * v[21] - 0.6 * v[25] + 0.02 * rng.standard_normal(s)
+    slices = [np.arange(t, s, T) for t in range(T)]
+    cfg = L0Config(dimension=5, n_models_store=12, autotune=False)
+    st = SearchStats()
+    got = l0_search(v, y, slices, cfg, stats=st, mode="fast")
+    want = oracle.l0_search(v, y, slices, 5, 12, "fp64")
+    assert st.device["mode_used"] == 1 and st.device["certified"] == 1
+    assert [g.indices for g in got] == [w["indices"] for w in want]
+    assert bits_equal([g.score for g in got], [w["score"] for w in want])
+    assert all(bits_equal(g.coefficients, w["coefficients"]) for g, w in zip(got, want))
