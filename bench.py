@@ -155,6 +155,15 @@ def stage_roofline(stage_ms):
         return None
     peak, src = _hbm_peak()
     out = {"peak": peak, "unit": "GB/s", "peak_source": src}
+    if stage_ms.get("normalize") == 0.0:
+        # fused gather + normalize (stage.cu k_stage_rows): reads the values (8 B), writes the
+        # task-ordered copy (8 B) and the four INT8 digit planes (4 B) per element
+        ms = stage_ms["gather"]
+        gbs = 20 * M * S / (ms * 1e-3) / 1e9
+        out["stage_rows"] = {"ms": ms, "bytes": 20 * M * S, "achieved": gbs, "frac": gbs / peak,
+                             "kernel": "k_stage_rows (gather + normalize + digits, one pass)"}
+        out["flags_ms"] = stage_ms["flags"]
+        return out
     for name, per in (("gather", 16), ("normalize", 12)):
         ms = stage_ms[name]
         gbs = per * M * S / (ms * 1e-3) / 1e9

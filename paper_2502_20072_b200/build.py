@@ -36,7 +36,7 @@ def nvcc() -> str:
 
 
 def sources() -> list[str]:
-    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
 
 
 def _deps_mtime() -> float:
@@ -46,8 +46,11 @@ def _deps_mtime() -> float:
 
 
 def _compile(src: str, objdir: str = OBJ, defines: tuple = ()) -> tuple[str, str]:
-    obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
+    obj = os.path.join(objdir, os.path.splitext(os.path.basename(src))[0] + ".o")
+    if src.endswith(".cpp"):  # host-only code (intrinsics): the host compiler directly
+        cmd = ["g++", "-O3", "-fPIC", "-std=c++17", f"-I{INCLUDE}", *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
+    else:
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

@@ -31,6 +31,14 @@ void launch_normalize(const void* Xp, const void* yp, int precision, int64_t m, 
                       const int64_t* bounds_d, const int64_t* zoff_d, int T, int64_t sp, double* Z,
                       double* qf, double* un2, double* yyu, int64_t f0, int64_t f1, DigitOut dig, cudaStream_t st);
 
+// gather + normalize fused (stage.cu k_stage_rows) when a task segment fits in shared memory
+// (max_rows rows), else the two kernels above
+bool stage_rows_fused(int64_t max_rows, const DigitOut& dig);
+void launch_stage_rows(const double* values, const double* y, const int64_t* perm, int64_t m, int64_t s, int precision,
+                       void* Xp, void* yp, const int64_t* bounds_d, const int64_t* zoff_d, int T, int64_t sp,
+                       double* Z, double* qf, double* un2, double* yyu, int64_t f0, int64_t f1, DigitOut dig,
+                       int64_t max_rows, cudaStream_t st);
+
 // Residuals of `count` models (models.residuals / predict, models.py:44-83): out[c][i] =
 // y[i] - (coef[c][t][n] + sum_k coef[c][t][k] * values[tup[c][k]][i]) for sample i of task t,
 // numpy's operation order (explicit roundings), in the caller's sample order.

@@ -4,6 +4,8 @@
 // centering / normalization that the Gram path needs.  HBM-bound: the input
 // matrix is read once for the gather and the permuted copy twice (L2-resident
 // per row segment) for the statistics and the normalized write.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -125,6 +127,175 @@ __global__ void k_normalize(const W* __restrict__ Xp, const W* __restrict__ yp, 
         } else {
             yyu[t] = us;
         }
+    }
+}
+
+// Fused gather + normalize: one CTA per (row, task) segment, the task's samples gathered from
+// the caller's order (perm) into shared memory and the task-ordered copy (one HBM read of the
+// values, one write of Xp), the statistics of k_normalize from shared memory, then the Ozaki
+// digits (four 7-bit planes, 4 consecutive samples per thread: 32-bit stores) and/or Z.
+// Same statistics and the same rounding of every written value as k_gather + k_normalize.
+constexpr int SR_THREADS = 256;
+template <typename W>
+__global__ void __launch_bounds__(SR_THREADS) k_stage_rows(const double* __restrict__ values, const double* __restrict__ y,
+                                                          const int64_t* __restrict__ perm, int64_t m, int64_t s,
+                                                          const int64_t* __restrict__ bounds,
+                                                          const int64_t* __restrict__ zoff, int T, int64_t sp,
+                                                          W* __restrict__ Xp, W* __restrict__ yp, double* __restrict__ Z,
+                                                          double* __restrict__ qf, double* __restrict__ un2,
+                                                          double* __restrict__ yyu, int64_t f0, DigitOut dig) {
+    extern __shared__ double seg[];
+    __shared__ double red[5][SR_THREADS / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int t = (int)(blockIdx.x % T);
+    const int64_t f = f0 + blockIdx.x / T;
+    const int64_t lo = bounds[t], r = bounds[t + 1] - lo;
+    const double* row = f < m ? values + f * s : y;
+    W* dx = f < m ? Xp + f * s + lo : yp + lo;
+    // gather (+ the working dtype's rounding, numpy astype) and the first sum
+    // (batches of SR_B indices, then SR_B value loads in flight per thread)
+    constexpr int SR_B = 8;
+    double sum = 0.0;
+    for (int64_t i0 = tid; i0 < r; i0 += SR_B * SR_THREADS) {
+        int64_t src[SR_B];
+#pragma unroll
+        for (int b = 0; b < SR_B; ++b) {
+            const int64_t i = i0 + (int64_t)b * SR_THREADS;
+            src[b] = i < r ? __ldg(perm + lo + i) : -1;
+        }
+        double v[SR_B];
+#pragma unroll
+        for (int b = 0; b < SR_B; ++b) v[b] = src[b] >= 0 ? row[src[b]] : 0.0;
+#pragma unroll
+        for (int b = 0; b < SR_B; ++b) {
+            const int64_t i = i0 + (int64_t)b * SR_THREADS;
+            if (i < r) {
+                const W w = (W)v[b];
+                dx[i] = w;
+                const double x = (double)w;
+                seg[i] = x;
+                sum += x;
+            }
+        }
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) red[0][warp] = sum;
+    __syncthreads();
+    sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < SR_THREADS / 32; ++w) sum += red[0][w];
+    const double mean0 = sum / (double)r;
+    // centered statistics around mean0 (see k_normalize: the mean refined to the centered rounding)
+    double corr = 0.0, s0 = 0.0, us = 0.0, cmax = -INFINITY, cmin = INFINITY;
+    for (int64_t i = tid; i < r; i += SR_THREADS) {
+        const double x = seg[i];
+        const double c = x - mean0;
+        corr += c;
+        s0 = fma(c, c, s0);
+        us = fma(x, x, us);
+        cmax = fmax(cmax, c);
+        cmin = fmin(cmin, c);
+    }
+    corr = warp_sum(corr);
+    s0 = warp_sum(s0);
+    us = warp_sum(us);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        cmax = fmax(cmax, __shfl_xor_sync(L0S_FULL, cmax, o));
+        cmin = fmin(cmin, __shfl_xor_sync(L0S_FULL, cmin, o));
+    }
+    __syncthreads();  // red[0] is read above by every thread before being reused
+    if (lane == 0) {
+        red[0][warp] = corr;
+        red[1][warp] = s0;
+        red[2][warp] = us;
+        red[3][warp] = cmax;
+        red[4][warp] = cmin;
+    }
+    __syncthreads();
+    corr = s0 = us = 0.0;
+    cmax = -INFINITY;
+    cmin = INFINITY;
+#pragma unroll
+    for (int w = 0; w < SR_THREADS / 32; ++w) {
+        corr += red[0][w];
+        s0 += red[1][w];
+        us += red[2][w];
+        cmax = fmax(cmax, red[3][w]);
+        cmin = fmin(cmin, red[4][w]);
+    }
+    const double dlt = corr / (double)r;
+    const double mean = mean0 + dlt;
+    const double cs = fmax(s0 - corr * dlt, 0.0);
+    const double mc = fmax(cmax - dlt, dlt - cmin);
+    const double scale = (f < m) ? 1.0 / sqrt(cs) : 1.0;
+    double* dst = Z + f * sp + zoff[t];
+    const int64_t rpad = zoff[t + 1] - zoff[t];
+    if (!dig.Q || dig.write_z)
+        for (int64_t i = tid; i < rpad; i += SR_THREADS) dst[i] = (i < r) ? (seg[i] - mean) * scale : 0.0;
+    if (dig.Q) {
+        const double zmax = mc * scale;
+        int e = 0;
+        const bool finite = zmax > 0.0 && zmax < INFINITY;
+        if (finite) frexp(zmax, &e);
+        const int64_t k0 = dig.koff[t], klen = dig.koff[t + 1] - k0;  // multiples of 64
+        for (int64_t i0 = 4 * (int64_t)tid; i0 < klen; i0 += 4 * SR_THREADS) {
+            unsigned pk[OZ_DIGITS] = {};
+#pragma unroll
+            for (int e4 = 0; e4 < 4; ++e4) {
+                const int64_t i = i0 + e4;
+                const double z = (i < r) ? (seg[i] - mean) * scale : 0.0;
+                double u = finite ? ldexp(z, -e) : 0.0;
+#pragma unroll
+                for (int a = 0; a < OZ_DIGITS; ++a) {
+                    const double v = u * 128.0;  // exact
+                    const double q = trunc(v);   // |q| <= 127
+                    u = v - q;                   // exact remainder
+                    pk[a] |= ((unsigned)(int)q & 0xffu) << (8 * e4);
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < OZ_DIGITS; ++a)
+                *reinterpret_cast<unsigned*>(dig.Q + ((int64_t)a * dig.R + f) * dig.KP + k0 + i0) = pk[a];
+        }
+        if (tid == 0) dig.ex[(int64_t)t * dig.R + f] = e;
+    }
+    if (tid == 0) {
+        if (f < m) {
+            qf[(int64_t)t * m + f] = cs / us;
+            un2[(int64_t)t * m + f] = us;
+        } else {
+            yyu[t] = us;
+        }
+    }
+}
+
+constexpr int64_t kStageRowsMaxSmem = 96 * 1024;
+
+bool stage_rows_fused(int64_t max_rows, const DigitOut& dig) {
+    return 8 * std::max<int64_t>(max_rows, 1) <= kStageRowsMaxSmem && !(dig.Q && dig.KP % 4 != 0);
+}
+
+void launch_stage_rows(const double* values, const double* y, const int64_t* perm, int64_t m, int64_t s, int precision,
+                       void* Xp, void* yp, const int64_t* bounds_d, const int64_t* zoff_d, int T, int64_t sp,
+                       double* Z, double* qf, double* un2, double* yyu, int64_t f0, int64_t f1, DigitOut dig,
+                       int64_t max_rows, cudaStream_t st) {
+    if (f1 <= f0) return;
+    const int64_t smem = 8 * std::max<int64_t>(max_rows, 1);
+    if (!stage_rows_fused(max_rows, dig)) {  // segments too long: the two passes
+        launch_gather(values, y, perm, m, s, precision, Xp, yp, f0, f1, st);
+        launch_normalize(Xp, yp, precision, m, s, bounds_d, zoff_d, T, sp, Z, qf, un2, yyu, f0, f1, dig, st);
+        return;
+    }
+    const unsigned blocks = (unsigned)((f1 - f0) * T);
+    if (precision == 1) {
+        cudaFuncSetAttribute(k_stage_rows<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageRowsMaxSmem);
+        k_stage_rows<float><<<blocks, SR_THREADS, smem, st>>>(values, y, perm, m, s, bounds_d, zoff_d, T, sp,
+                                                               (float*)Xp, (float*)yp, Z, qf, un2, yyu, f0, dig);
+    } else {
+        cudaFuncSetAttribute(k_stage_rows<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageRowsMaxSmem);
+        k_stage_rows<double><<<blocks, SR_THREADS, smem, st>>>(values, y, perm, m, s, bounds_d, zoff_d, T, sp,
+                                                                (double*)Xp, (double*)yp, Z, qf, un2, yyu, f0, dig);
     }
 }
 
