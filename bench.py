@@ -208,11 +208,13 @@ def random_y_line(eng, vd, pd, bounds, args, local):
         fit.append(st.ms_fit / max(1, st.n_fit_launches))
         ev.append(st.n_eval / max(1, st.n_fit_launches))
     peak = eng.fp64_peak()
+    loose, ozaki = eng.stage_loose_rows(), eng.stage_info()[1]
     f = statistics.mean(fit)
     ach = statistics.mean(ev) * FLOP_PER_EVAL / (f * 1e-3) / 1e12
     return {"value": total * args.steps / (sum(ms) * 1e-3), "unit": "tuples/s", "ms_per_step": sum(ms) / args.steps,
             "fit_ms": f, "evals_per_tuple": statistics.mean(ev) / total, "fit_achieved_tflops": ach,
             "fit_frac": ach / peak, "certified": int(st.certified), "n_rescan": int(st.n_rescan),
+            "gram": ("INT8 Ozaki" if ozaki else "DMMA fp64") + f", {loose} loose rows recomputed in fp64",
             "data": "tests/scale_cases.py c3('random'): the bench's features, y ~ N(0,1)"}
 
 

@@ -247,6 +247,10 @@ int l0s_sis_scores(l0s_ctx *ctx, const double *F, int64_t k, int is_device, doub
 int l0s_set_gram_mode(l0s_ctx *ctx, int mode);
 /* Per-task entry error bound of the staged Gram (ntasks values) and whether it is the INT8 one. */
 int l0s_stage_info(l0s_ctx *ctx, double *eta_out, int *ozaki_out);
+/* Rows of the last INT8 Gram whose own error term exceeded the screen's limit (spiky rows, max |z|
+ * close to 1; e.g. a Gaussian property): up to 64 of them were recomputed in fp64 and left out of
+ * eta; with more, the whole Gram was recomputed on DMMA (l0s_stage_info then reports ozaki 0). */
+int l0s_stage_loose_rows(l0s_ctx *ctx, int *out_count);
 /* Device times (ms) of the last stage when its inputs were device-resident (unchunked):
  * [gather (search._prepare's permutation + cast), normalize (+ INT8 digits), Gram, feature
  * flags]; zeros after a chunked host stage. */

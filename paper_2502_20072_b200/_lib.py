@@ -28,7 +28,7 @@ EXPORTS = (
     "l0s_last_error", "l0s_version", "l0s_device_count", "l0s_create", "l0s_destroy", "l0s_stage",
     "l0s_search", "l0s_fit_tuples", "l0s_screen_tuples", "l0s_get_gram", "l0s_unrank", "l0s_rank",
     "l0s_count", "l0s_fp64_peak", "l0s_rcp_check", "l0s_gram_shard_size", "l0s_stage_shard",
-    "l0s_stage_finish", "l0s_sis_prepare", "l0s_sis_scores", "l0s_set_gram_mode", "l0s_stage_info", "l0s_stage_timings", "l0s_qr_tuples", "l0s_residuals",
+    "l0s_stage_finish", "l0s_sis_prepare", "l0s_sis_scores", "l0s_set_gram_mode", "l0s_stage_info", "l0s_stage_loose_rows", "l0s_stage_timings", "l0s_qr_tuples", "l0s_residuals",
     "l0s_gen_dedup_reset", "l0s_gen_dedup",
     "l0s_group_create", "l0s_group_destroy", "l0s_group_size", "l0s_group_ctx", "l0s_group_stage", "l0s_group_search",
     "l0s_stage_append", "l0s_search_part", "l0s_stage_rows", "l0s_stage_append_rows", "l0s_gen_pool", "l0s_gen_eval", "l0s_gen_take", "l0s_gen_fetch",
@@ -102,6 +102,7 @@ def lib():
         L.l0s_gen_fetch.argtypes = [vp, vp, i64, vp]
         L.l0s_set_gram_mode.argtypes = [vp, i32]
         L.l0s_stage_info.argtypes = [vp, vp, vp]
+        L.l0s_stage_loose_rows.argtypes = [vp, vp]
         L.l0s_stage_timings.argtypes = [vp, vp]
         L.l0s_qr_tuples.argtypes = [vp, i32, vp, i64, vp, vp]
         L.l0s_residuals.argtypes = [vp, i32, vp, vp, i64, vp]
@@ -262,6 +263,12 @@ class Engine:
         oz = ctypes.c_int(0)
         check(lib().l0s_stage_info(self.handle, ptr(eta), ctypes.byref(oz)), "l0s_stage_info")
         return eta, bool(oz.value)
+
+    def stage_loose_rows(self) -> int:
+        """Rows of the last INT8 Gram recomputed in fp64 (their own error term was too large)."""
+        n = ctypes.c_int(0)
+        check(lib().l0s_stage_loose_rows(self.handle, ctypes.byref(n)), "l0s_stage_loose_rows")
+        return int(n.value)
 
     def residuals(self, tuples: np.ndarray, coef: np.ndarray) -> np.ndarray:
         """y - prediction of each model (tuple of staged features, (T, n+1) coefficients), float64 (count, s)."""

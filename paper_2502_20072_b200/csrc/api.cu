@@ -130,6 +130,12 @@ struct l0s_ctx {
     bool gram_ozaki = false;     // the staged Gram came from the INT8 path (eta on the device)
     bool digits_ready = false;   // the normalize kernel wrote the Ozaki digits of this stage
     DBuf oz_q, oz_ex, oz_koff;
+    // loose rows of the INT8 Gram (a row's own error term above OZ_ETA_MAX) recomputed in fp64:
+    // oz_musc = the rows' (mean, scale) beside their digits, oz_fix = (kFixCap rows, count)
+    static constexpr int kFixCap = 64;
+    DBuf oz_musc, oz_fix;
+    bool fix_on = false;  // this stage's eta left the listed rows out; k_oz_fixup is due
+    int fix_count = 0;    // loose rows of the last stage (l0s_stage_info)
     // binomial table (k <= binom_n) x (a <= m)
     DBuf binom;
     int binom_n = -1;
@@ -166,7 +172,7 @@ struct l0s_ctx {
                        &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
                        &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr, &sis_y, &sis_yc, &sis_sy, &sis_perm,
-                       &sis_bounds, &sis_F, &sis_out, &sis_dest, &sis_tE, &sis_tpoff, &oz_q, &oz_ex, &oz_koff,
+                       &sis_bounds, &sis_F, &sis_out, &sis_dest, &sis_tE, &sis_tpoff, &oz_q, &oz_ex, &oz_koff, &oz_musc, &oz_fix,
                        &res_tup, &res_coef, &res_out, &dd_lo, &dd_hi, &dd_owner, &dd_state, &dd_used, &dd_kept, &dd_seed, &gen_pool, &gen_pi, &gen_pj, &gen_vals, &gen_valid, &gen_hash, &gen_take, &gen_rows, &gen_out};
         for (DBuf* b : all) b->release();
         for (auto& e : ev)
@@ -383,6 +389,7 @@ static int stage_prepare(l0s_ctx* c, const double* values, int64_t m, int64_t s,
         if (bounds[t + 1] < bounds[t]) return fail(L0S_EINVAL, "bounds must be non-decreasing");
     CK(cudaSetDevice(c->dev));
     c->staged = false;
+    c->fix_on = false;
     c->m = m;
     c->s = s;
     c->T = ntasks;
@@ -431,11 +438,39 @@ static int stage_prepare(l0s_ctx* c, const double* values, int64_t m, int64_t s,
 static int gram_full(l0s_ctx* c);
 static bool ozaki_planned(const l0s_ctx* c);
 
+static OzFix oz_fix_of(l0s_ctx* c) {
+    return OzFix{c->oz_fix.as<int>(), c->oz_fix.as<int>() + l0s_ctx::kFixCap, l0s_ctx::kFixCap};
+}
+
+// the INT8 Gram's error bound with the loose rows left out when their (mean, scale) were stored
+// (the staging kernels wrote the digits): k_oz_fixup then recomputes them in stage_post
+static int ozaki_fix_prepare(l0s_ctx* c, OzFix* fx) {
+    c->fix_on = c->digits_ready && c->oz_musc.p != nullptr;
+    if (c->fix_on) {
+        CK(c->oz_fix.ensure(sizeof(int) * (l0s_ctx::kFixCap + 1)));
+        *fx = oz_fix_of(c);
+    }
+    return L0S_OK;
+}
+
+static int ozaki_eta(l0s_ctx* c, int T, int64_t m, int64_t mp) {
+    OzFix fx{};
+    const int rc = ozaki_fix_prepare(c, &fx);
+    if (rc) return rc;
+    launch_ozaki_eta(T, m, mp, c->oz_ex.as<int>(), c->rowsd.as<double>(), c->G.as<double>(), c->eta_d.as<double>(),
+                     c->st, c->fix_on ? &fx : nullptr);
+    return L0S_OK;
+}
+
 // stage after the Gram: unit diagonal, per-feature conditioning flags, host copies
 static int stage_post(l0s_ctx* c) {
     const int64_t m = c->m;
     const int ntasks = c->T;
     cudaEventRecord(c->sev[3], c->st);
+    if (c->gram_ozaki && c->fix_on)  // loose rows of the INT8 Gram: their fp64 rows first
+        launch_ozaki_fixup(c->Xp.p, c->yp.p, c->prec, m, c->s, c->bounds_d.as<int64_t>(), ntasks,
+                           c->oz_musc.as<double>(), (c->mp + 127) / 128 * 128, c->mp, oz_fix_of(c), c->G.as<double>(),
+                           c->st);
     launch_unit_diag(c->G.as<double>(), ntasks, m, c->mp, c->st);
     CK(cudaGetLastError());
     // per-feature conditioning flags on the device (stage.cu: launch_feature_flags)
@@ -456,12 +491,17 @@ static int stage_post(l0s_ctx* c) {
     CK(cudaMemcpyAsync(c->yyu_h.data(), c->yyu.p, sizeof(double) * ntasks, cudaMemcpyDeviceToHost, c->st));
     if (c->gram_ozaki)
         CK(cudaMemcpyAsync(c->eta_h.data(), c->eta_d.p, sizeof(double) * ntasks, cudaMemcpyDeviceToHost, c->st));
+    c->fix_count = 0;
+    if (c->gram_ozaki && c->fix_on)
+        CK(cudaMemcpyAsync(&c->fix_count, c->oz_fix.as<int>() + l0s_ctx::kFixCap, sizeof(int), cudaMemcpyDeviceToHost,
+                           c->st));
     CK(cudaStreamSynchronize(c->st));
     if (c->gram_ozaki) {
         // the INT8 Gram's error bound must stay well inside the screen's first-order regime;
-        // spiky rows (max |z| close to 1) make it too loose: redo the Gram in fp64 (DMMA)
-        bool loose = false;
-        for (int t = 0; t < ntasks; ++t) loose |= !(c->eta_h[(size_t)t] <= 1e-6);
+        // spiky rows (max |z| close to 1) make it too loose: up to kFixCap such rows were
+        // recomputed in fp64 above (k_oz_fixup), more redo the whole Gram in fp64 (DMMA)
+        bool loose = c->fix_count > l0s_ctx::kFixCap;
+        for (int t = 0; t < ntasks; ++t) loose |= !(c->eta_h[(size_t)t] <= OZ_ETA_MAX);
         if (loose) {
             for (int t = 0; t < ntasks; ++t) c->eta_h[(size_t)t] = 4.0 * (c->rows_h[(size_t)t] + 8.0) * kEps;
             CK(cudaMemcpyAsync(c->eta_d.p, c->eta_h.data(), sizeof(double) * ntasks, cudaMemcpyHostToDevice, c->st));
@@ -497,7 +537,11 @@ static bool ozaki_planned(const l0s_ctx* c) {
 static int gram_full(l0s_ctx* c) {
     const int nb = (int)(c->mp / 64);
     c->gram_ozaki = false;
+    c->fix_on = false;
     if (ozaki_planned(c)) {
+        OzFix fx{};
+        const int frc = ozaki_fix_prepare(c, &fx);
+        if (frc) return frc;
         int64_t KP = 0;
         const int64_t qb = ozaki_q_bytes(c->mp, c->T, c->rpad_h.data(), &KP);
         const int64_t R = (c->mp + 127) / 128 * 128;
@@ -507,12 +551,14 @@ static int gram_full(l0s_ctx* c) {
         cudaEventRecord(c->ev[2], c->st);
         if (launch_ozaki_gram(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), c->rpad_h.data(), c->T, c->m, c->mp,
                               c->rowsd.as<double>(), c->G.as<double>(), c->eta_d.as<double>(), c->oz_q.as<int8_t>(),
-                              c->oz_ex.as<int>(), c->oz_koff.as<int64_t>(), c->digits_ready, c->st) == 0) {
+                              c->oz_ex.as<int>(), c->oz_koff.as<int64_t>(), c->digits_ready, c->st,
+                              c->fix_on ? &fx : nullptr) == 0) {
             cudaEventRecord(c->ev[3], c->st);
             c->gram_timed = true;
             c->gram_ozaki = true;
             return L0S_OK;
         }
+        c->fix_on = false;
     }
     cudaEventRecord(c->ev[2], c->st);
     launch_gram_cols(c->Z.as<double>(), c->sp, c->zoff_d.as<int64_t>(), c->T, c->mp, c->G.as<double>(), 0, nb, c->st);
@@ -584,8 +630,9 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
         CK(c->oz_q.ensure((size_t)qb));
         CK(c->oz_ex.ensure(sizeof(int) * ntasks * R));
         CK(c->oz_koff.ensure(sizeof(int64_t) * (ntasks + 1)));
+        CK(c->oz_musc.ensure(sizeof(double) * 2 * ntasks * R));
         ozaki_prepare_digits(m, c->mp, ntasks, c->rpad_h.data(), c->oz_q.as<int8_t>(), c->oz_ex.as<int>(),
-                             c->oz_koff.as<int64_t>(), &dig, c->st);
+                             c->oz_koff.as<int64_t>(), &dig, c->st, c->oz_musc.as<double>());
         dig.write_z = false;  // the INT8 Gram reads the digits; Z is written only for a DMMA fallback
         c->digits_ready = true;
     }
@@ -651,8 +698,8 @@ static int stage_fill(l0s_ctx* c, const double* values, const double* y, const i
         }
     }
     if (ozaki) {
-        launch_ozaki_eta(ntasks, m, c->mp, c->oz_ex.as<int>(), c->rowsd.as<double>(), c->G.as<double>(),
-                         c->eta_d.as<double>(), c->st);
+        const int rc = ozaki_eta(c, ntasks, m, c->mp);
+        if (rc) return rc;
         cudaEventRecord(c->ev[3], c->st);
     }
     return L0S_OK;
@@ -712,10 +759,12 @@ static int stage_extend(l0s_ctx* c, int64_t m1) {
     const int64_t qb1 = ozaki_q_bytes(mp1, T, c->rpad_h.data(), &KP);
     cudaEventRecord(c->ev[0], c->st);
     // relayout into fresh buffers (old contents copied), then swap
-    DBuf G1, Q1, ex1, qf1, un21;
+    DBuf G1, Q1, ex1, qf1, un21, ms1;
     CK(G1.ensure(sizeof(double) * mp1 * mp1 * T));
     CK(Q1.ensure((size_t)qb1));
     CK(ex1.ensure(sizeof(int) * T * R1));
+    const bool musc = c->oz_musc.p != nullptr;
+    if (musc) CK(ms1.ensure(sizeof(double) * 2 * T * R1));
     CK(qf1.ensure(sizeof(double) * m1 * T));
     CK(un21.ensure(sizeof(double) * m1 * T));
     for (int t = 0; t < T; ++t) {
@@ -724,6 +773,9 @@ static int stage_extend(l0s_ctx* c, int64_t m1) {
                              (size_t)m0, cudaMemcpyDeviceToDevice, c->st));
         CK(cudaMemcpyAsync(ex1.as<int>() + (int64_t)t * R1, c->oz_ex.as<int>() + (int64_t)t * R0, sizeof(int) * m0,
                            cudaMemcpyDeviceToDevice, c->st));
+        if (musc)
+            CK(cudaMemcpyAsync(ms1.as<double>() + 2 * (int64_t)t * R1, c->oz_musc.as<double>() + 2 * (int64_t)t * R0,
+                               sizeof(double) * 2 * m0, cudaMemcpyDeviceToDevice, c->st));
         CK(cudaMemcpyAsync(qf1.as<double>() + (int64_t)t * m1, c->qf.as<double>() + (int64_t)t * m0,
                            sizeof(double) * m0, cudaMemcpyDeviceToDevice, c->st));
         CK(cudaMemcpyAsync(un21.as<double>() + (int64_t)t * m1, c->un2.as<double>() + (int64_t)t * m0,
@@ -735,6 +787,7 @@ static int stage_extend(l0s_ctx* c, int64_t m1) {
     std::swap(c->G, G1);
     std::swap(c->oz_q, Q1);
     std::swap(c->oz_ex, ex1);
+    if (musc) std::swap(c->oz_musc, ms1);
     std::swap(c->qf, qf1);
     std::swap(c->un2, un21);
     CK(cudaStreamSynchronize(c->st));  // the old buffers are released on return
@@ -749,7 +802,8 @@ static int stage_extend(l0s_ctx* c, int64_t m1) {
         CK(cudaMemsetAsync(c->oz_q.as<int8_t>() + ((int64_t)a * R1 + m1 + 1) * KP, 0, (size_t)((R1 - m1 - 1) * KP), c->st));
     for (int t = 0; t < T; ++t)
         CK(cudaMemsetAsync(c->oz_ex.as<int>() + (int64_t)t * R1 + m1 + 1, 0, sizeof(int) * (R1 - m1 - 1), c->st));
-    DigitOut dig{c->oz_q.as<int8_t>(), R1, KP, c->oz_koff.as<int64_t>(), c->oz_ex.as<int>(), false};
+    DigitOut dig{c->oz_q.as<int8_t>(), R1, KP, c->oz_koff.as<int64_t>(), c->oz_ex.as<int>(), false,
+                 musc ? c->oz_musc.as<double>() : nullptr};
     const double* vd = c->in_values.as<double>();
     const double* yd = c->in_y.as<double>();
     const int64_t* pd = c->in_perm.as<int64_t>();
@@ -767,8 +821,10 @@ static int stage_extend(l0s_ctx* c, int64_t m1) {
                            c->oz_koff.as<int64_t>(), c->G.as<double>(), (int)(m0 / 128), ozaki_col_blocks(mp1), c->st))
         return fail(L0S_ECUDA, "INT8 Gram: TMA descriptor");
     // the per-task entry bound over every row's exponent (old rows' exponents moved above)
-    launch_ozaki_eta(T, m1, mp1, c->oz_ex.as<int>(), c->rowsd.as<double>(), c->G.as<double>(), c->eta_d.as<double>(),
-                     c->st);
+    {
+        const int rc = ozaki_eta(c, T, m1, mp1);
+        if (rc) return rc;
+    }
     cudaEventRecord(c->ev[3], c->st);
     c->gram_timed = true;
     c->gram_ozaki = true;
@@ -1945,6 +2001,12 @@ int l0s_stage_timings(l0s_ctx* c, double* out_ms) {
     out_ms[1] = c->stage_fused ? 0.0 : elapsed(c->sev[1], c->sev[2]);  // fused: one pass, out_ms[0]
     out_ms[2] = c->ms_gram_k;
     out_ms[3] = elapsed(c->sev[3], c->sev[4]);
+    return L0S_OK;
+}
+
+int l0s_stage_loose_rows(l0s_ctx* c, int* out_count) {
+    if (!c || !c->staged) return fail(L0S_ESTATE, "l0s_stage must be called first");
+    *out_count = c->fix_count;
     return L0S_OK;
 }
 

@@ -26,6 +26,7 @@ struct DigitOut {
     const int64_t* koff;   // (T+1,) device: task segment offsets in K (multiples of 64)
     int* ex;               // [T][R] row exponents
     bool write_z = true;   // also write the fp64 rows Z (only the DMMA Gram reads them)
+    double* musc = nullptr;  // [T][R][2] the rows' (mean, scale): z = (x - mean) * scale (k_oz_fixup)
 };
 void launch_normalize(const void* Xp, const void* yp, int precision, int64_t m, int64_t s,
                       const int64_t* bounds_d, const int64_t* zoff_d, int T, int64_t sp, double* Z,
@@ -71,22 +72,35 @@ void launch_unit_diag(double* G, int T, int64_t m, int64_t mp, cudaStream_t st);
 void launch_mark_dead(double* G, const int32_t* dead, int ndead, int T, int64_t mp, cudaStream_t st);
 
 // ---- Gram on the INT8 tensor cores by Ozaki splitting (ozaki.cu) ----
+struct OzFix {
+    int* rows;      // (cap,) loose rows (device)
+    int* count;     // loose rows found (device, may exceed cap)
+    int cap;
+};
 int64_t ozaki_q_bytes(int64_t mp, int T, const int64_t* rpad_h, int64_t* KP_out);
 // digits_ready: the normalize kernel already wrote Q / ex (and koff_d); otherwise split Z here
 int launch_ozaki_gram(const double* Z, int64_t sp, const int64_t* zoff_d, const int64_t* rpad_h, int T, int64_t m,
                       int64_t mp, const double* rows_d, double* G, double* eta_d, int8_t* Q, int* ex, int64_t* koff_d,
-                      bool digits_ready, cudaStream_t st);
+                      bool digits_ready, cudaStream_t st, const OzFix* fix = nullptr);
 // pieces of the same, for the overlapped stage: tiles of the column blocks [gb0, gb1) (64 wide)
 // and the error-bound kernel (after all tiles)
 int ozaki_col_blocks(int64_t mp);
 int ozaki_blocks_ready(int64_t r1);  // column blocks complete once rows < r1 have landed
 int launch_ozaki_tiles(int T, int64_t mp, const int64_t* rpad_h, const int8_t* Q, const int* ex,
                        const int64_t* koff_d, double* G, int gb0, int gb1, cudaStream_t st);
+// eta_t (see ozaki.cu).  fix != nullptr: rows whose own error term exceeds OZ_ETA_MAX in some task
+// are listed in fix->rows (count in fix->count, at most fix->cap listed) and left out of eta_t:
+// launch_ozaki_fixup recomputes their Gram rows in fp64
+constexpr double OZ_ETA_MAX = 1e-6;  // the screen's limit on eta_t (larger: DMMA Gram)
 void launch_ozaki_eta(int T, int64_t m, int64_t mp, const int* ex, const double* rows_d, const double* G, double* eta_d,
-                      cudaStream_t st);
+                      cudaStream_t st, const OzFix* fix = nullptr);
+// fp64 Gram rows and columns of the listed loose rows from Xp / yp and the stored (mean, scale)
+// (every task; a no-op when the count is 0 or above cap -- the host then takes the DMMA Gram)
+void launch_ozaki_fixup(const void* Xp, const void* yp, int precision, int64_t m, int64_t s, const int64_t* bounds_d,
+                        int T, const double* musc, int64_t R, int64_t mp, const OzFix& fix, double* G, cudaStream_t st);
 // Q / ex zero fill of the rows the normalize kernel does not write (m+1 .. R-1) and koff upload
 void ozaki_prepare_digits(int64_t m, int64_t mp, int T, const int64_t* rpad_h, int8_t* Q, int* ex, int64_t* koff_d,
-                          DigitOut* out, cudaStream_t st);
+                          DigitOut* out, cudaStream_t st, double* musc = nullptr);
 
 // ---- bit-exact Householder (exact.cu) ----
 struct ExactArgs {

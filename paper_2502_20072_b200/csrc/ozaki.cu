@@ -263,26 +263,145 @@ __global__ void __launch_bounds__(192, OZ_CTAS) k_oz_gemm(const __grid_constant_
 }
 
 // eta_t = C r_t max over rows of 2^(2 e) / |row|^2 (features: unit rows; the property row: Y2)
-__global__ void k_oz_eta(const int* __restrict__ ex, int64_t R, int64_t m, int64_t mp, const double* __restrict__ Gall,
-                         const double* __restrict__ rows, double* __restrict__ eta) {
-    const int t = blockIdx.x;
-    double mx = 0.0;
-    for (int64_t f = threadIdx.x; f <= m; f += blockDim.x) {
+// eta_t = C r_t max_f 2^(2 e_f) (the property row relative to |y_c|^2).  With a fix-up list
+// (rows != nullptr), rows whose own term exceeds `lim` in some task are loose: listed (any order:
+// k_oz_fixup's result does not depend on it), counted, and left out of the maximum, which is
+// floored at the fp64 dot-product bound their recomputed entries carry.  One CTA.
+__global__ void __launch_bounds__(1024) k_oz_eta(const int* __restrict__ ex, int64_t R, int T, int64_t m, int64_t mp,
+                                                 const double* __restrict__ Gall, const double* __restrict__ rows,
+                                                 double lim, double* __restrict__ eta, int* __restrict__ fix_rows,
+                                                 int* __restrict__ fix_count, int fix_cap) {
+    __shared__ double red[32];
+    __shared__ int s_cnt;
+    extern __shared__ unsigned char s_loose[];  // (m + 1,) when fixing up
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    auto term = [&](int t, int64_t f) {
         double v = ldexp(1.0, 2 * ex[(int64_t)t * R + f]);
         if (f == m) {
             const double y2 = Gall[(int64_t)t * mp * mp + m * mp + m];
             v = y2 > 0.0 ? v / y2 : 0.0;
         }
-        mx = fmax(mx, v);
-    }
-    __shared__ double red[256];
-    red[threadIdx.x] = mx;
+        return OZ_C * rows[t] * v * (1.0 + 1e-6);
+    };
+    const bool fixing = fix_rows != nullptr;
+    if (tid == 0) s_cnt = 0;
     __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if ((int)threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    if (fixing) {
+        for (int64_t f = tid; f <= m; f += blockDim.x) {
+            bool loose = false;
+            for (int t = 0; t < T && !loose; ++t) loose = !(term(t, f) <= lim);
+            s_loose[f] = loose;
+            if (loose) {
+                const int k = atomicAdd(&s_cnt, 1);
+                if (k < fix_cap) fix_rows[k] = (int)f;
+            }
+        }
         __syncthreads();
     }
-    if (threadIdx.x == 0) eta[t] = OZ_C * rows[t] * red[0] * (1.0 + 1e-6);
+    for (int t = 0; t < T; ++t) {
+        double mx = 0.0;
+        for (int64_t f = tid; f <= m; f += blockDim.x)
+            if (!fixing || !s_loose[f]) mx = fmax(mx, term(t, f));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(L0S_FULL, mx, o));
+        if (lane == 0) red[warp] = mx;
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < nw; ++w) mx = fmax(mx, red[w]);
+            eta[t] = fixing ? fmax(mx, 4.0 * (rows[t] + 8.0) * 1.1102230246251565e-16) : mx;
+        }
+        __syncthreads();
+    }
+    if (tid == 0 && fix_count) *fix_count = fixing ? s_cnt : 0;
+}
+
+// fp64 Gram entries G[t][f][g] = G[t][g][f] = sum_i z_f(i) z_g(i) of the loose rows f (k_oz_eta's
+// list) against every row g <= m, z = (x - mean) * scale exactly as the staging kernel computed
+// the digits' values (mean, scale stored beside them).  CTA: one task, FX loose rows staged in
+// shared memory chunk by chunk, FG rows g per warp (lanes stride the samples, FG x FX fp64
+// accumulators per lane, warp sums at the end).
+constexpr int FX = 8, FG = 4, FCH = 256, FTH = 256;
+template <typename W>
+__global__ void __launch_bounds__(FTH) k_oz_fixup(const W* __restrict__ Xp, const W* __restrict__ yp, int64_t m, int64_t s,
+                                                  const int64_t* __restrict__ bounds, const double* __restrict__ musc,
+                                                  int64_t R, int64_t mp, const int* __restrict__ fix_rows,
+                                                  const int* __restrict__ fix_count, int fix_cap, double* __restrict__ G) {
+    const int nl = *fix_count;
+    if (nl > fix_cap) return;  // too many: the host recomputes the whole Gram on DMMA
+    const int l0 = blockIdx.y * FX;
+    if (l0 >= nl) return;
+    __shared__ double zf[FX][FCH];
+    __shared__ double fms[FX][2];
+    __shared__ int frow[FX];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int t = blockIdx.z;
+    const int64_t lo = bounds[t], r = bounds[t + 1] - lo;
+    const double* ms = musc + 2 * (int64_t)t * R;
+    if (tid < FX) {
+        const int f = l0 + tid < nl ? fix_rows[l0 + tid] : -1;
+        frow[tid] = f;
+        fms[tid][0] = f >= 0 ? ms[2 * f] : 0.0;
+        fms[tid][1] = f >= 0 ? ms[2 * f + 1] : 0.0;
+    }
+    const int64_t g0 = ((int64_t)blockIdx.x * (FTH / 32) + warp) * FG;
+    double gmu[FG], gsc[FG];
+    const W* grow[FG];
+#pragma unroll
+    for (int q = 0; q < FG; ++q) {
+        const int64_t g = g0 + q <= m ? g0 + q : m;
+        gmu[q] = ms[2 * g];
+        gsc[q] = ms[2 * g + 1];
+        grow[q] = (g < m ? Xp + g * s : yp) + lo;
+    }
+    double acc[FG][FX];
+#pragma unroll
+    for (int q = 0; q < FG; ++q)
+#pragma unroll
+        for (int l = 0; l < FX; ++l) acc[q][l] = 0.0;
+    for (int64_t c0 = 0; c0 < r; c0 += FCH) {
+        __syncthreads();  // frow / fms (first chunk), the previous chunk's reads (later ones)
+        for (int x = tid; x < FX * FCH; x += FTH) {
+            const int l = x / FCH, i = x % FCH;
+            const int f = frow[l];
+            double z = 0.0;
+            if (f >= 0 && c0 + i < r) {
+                const W* src = (f < m ? Xp + (int64_t)f * s : yp) + lo;
+                z = ((double)src[c0 + i] - fms[l][0]) * fms[l][1];
+            }
+            zf[l][i] = z;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < FCH / 32; ++k) {
+            const int i = k * 32 + lane;
+            const bool in = c0 + i < r;
+            double zf_[FX];
+#pragma unroll
+            for (int l = 0; l < FX; ++l) zf_[l] = zf[l][i];
+#pragma unroll
+            for (int q = 0; q < FG; ++q) {
+                const double zg = in ? ((double)grow[q][c0 + i] - gmu[q]) * gsc[q] : 0.0;
+#pragma unroll
+                for (int l = 0; l < FX; ++l) acc[q][l] = fma(zg, zf_[l], acc[q][l]);
+            }
+        }
+    }
+    double* Gt = G + (int64_t)t * mp * mp;
+#pragma unroll
+    for (int q = 0; q < FG; ++q) {
+#pragma unroll
+        for (int l = 0; l < FX; ++l) {
+            double v = acc[q][l];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(L0S_FULL, v, o);
+            const int64_t g = g0 + q;
+            const int f = frow[l];
+            if (lane == 0 && f >= 0 && g <= m) {
+                Gt[(int64_t)f * mp + g] = v;
+                Gt[g * mp + f] = v;
+            }
+        }
+    }
 }
 
 }  // namespace
@@ -299,7 +418,7 @@ int64_t ozaki_q_bytes(int64_t mp, int T, const int64_t* rpad_h, int64_t* KP_out)
 // Q (ozaki_q_bytes), ex (T x R ints), koff_d (T+1 int64, filled here).  Returns 0, or -1 when
 // the TMA descriptor could not be built.
 void ozaki_prepare_digits(int64_t m, int64_t mp, int T, const int64_t* rpad_h, int8_t* Q, int* ex, int64_t* koff_d,
-                          DigitOut* out, cudaStream_t st) {
+                          DigitOut* out, cudaStream_t st, double* musc) {
     const int64_t R = (mp + OZ_BM - 1) / OZ_BM * OZ_BM;
     std::vector<int64_t> koff((size_t)T + 1, 0);
     for (int t = 0; t < T; ++t) koff[(size_t)t + 1] = koff[(size_t)t] + (rpad_h[t] + OZ_KC - 1) / OZ_KC * OZ_KC;
@@ -308,6 +427,7 @@ void ozaki_prepare_digits(int64_t m, int64_t mp, int T, const int64_t* rpad_h, i
     for (int a = 0; a < OZ_S; ++a) cudaMemsetAsync(Q + ((int64_t)a * R + m + 1) * KP, 0, (size_t)((R - m - 1) * KP), st);
     cudaMemsetAsync(ex, 0, sizeof(int) * T * R, st);
     *out = DigitOut{Q, R, KP, koff_d, ex};
+    out->musc = musc;
 }
 
 static int oz_tiles_before(int gb) {  // tiles in column blocks [0, gb)
@@ -344,14 +464,29 @@ int launch_ozaki_tiles(int T, int64_t mp, const int64_t* rpad_h, const int8_t* Q
 }
 
 void launch_ozaki_eta(int T, int64_t m, int64_t mp, const int* ex, const double* rows_d, const double* G, double* eta_d,
-                      cudaStream_t st) {
+                      cudaStream_t st, const OzFix* fix) {
     const int64_t R = (mp + OZ_BM - 1) / OZ_BM * OZ_BM;
-    k_oz_eta<<<T, 256, 0, st>>>(ex, R, m, mp, G, rows_d, eta_d);
+    const size_t smem = fix ? (size_t)(m + 1) : 0;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_oz_eta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_oz_eta<<<1, 1024, smem, st>>>(ex, R, T, m, mp, G, rows_d, OZ_ETA_MAX, eta_d, fix ? fix->rows : nullptr,
+                                    fix ? fix->count : nullptr, fix ? fix->cap : 0);
+}
+
+void launch_ozaki_fixup(const void* Xp, const void* yp, int precision, int64_t m, int64_t s, const int64_t* bounds_d,
+                        int T, const double* musc, int64_t R, int64_t mp, const OzFix& fix, double* G, cudaStream_t st) {
+    const int64_t per = (FTH / 32) * FG;
+    const dim3 grid((unsigned)((m + 1 + per - 1) / per), (unsigned)((fix.cap + FX - 1) / FX), (unsigned)T);
+    if (precision == 1)
+        k_oz_fixup<float><<<grid, FTH, 0, st>>>((const float*)Xp, (const float*)yp, m, s, bounds_d, musc, R, mp, fix.rows,
+                                                fix.count, fix.cap, G);
+    else
+        k_oz_fixup<double><<<grid, FTH, 0, st>>>((const double*)Xp, (const double*)yp, m, s, bounds_d, musc, R, mp,
+                                                 fix.rows, fix.count, fix.cap, G);
 }
 
 int launch_ozaki_gram(const double* Z, int64_t sp, const int64_t* zoff_d, const int64_t* rpad_h, int T, int64_t m,
                       int64_t mp, const double* rows_d, double* G, double* eta_d, int8_t* Q, int* ex, int64_t* koff_d,
-                      bool digits_ready, cudaStream_t st) {
+                      bool digits_ready, cudaStream_t st, const OzFix* fix) {
     const int64_t R = (mp + OZ_BM - 1) / OZ_BM * OZ_BM;
     if (!digits_ready) {
         DigitOut dig;
@@ -361,7 +496,7 @@ int launch_ozaki_gram(const double* Z, int64_t sp, const int64_t* zoff_d, const 
                                                                           ex);
     }
     if (launch_ozaki_tiles(T, mp, rpad_h, Q, ex, koff_d, G, 0, ozaki_col_blocks(mp), st)) return -1;
-    launch_ozaki_eta(T, m, mp, ex, rows_d, G, eta_d, st);
+    launch_ozaki_eta(T, m, mp, ex, rows_d, G, eta_d, st, digits_ready ? fix : nullptr);
     return 0;
 }
 

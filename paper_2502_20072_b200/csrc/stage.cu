@@ -118,7 +118,13 @@ __global__ void k_normalize(const W* __restrict__ Xp, const W* __restrict__ yp, 
                 dig.Q[((int64_t)a * dig.R + f) * dig.KP + k0 + i] = (int8_t)(int)q;
             }
         }
-        if (lane == 0) dig.ex[(int64_t)t * dig.R + f] = e;
+        if (lane == 0) {
+            dig.ex[(int64_t)t * dig.R + f] = e;
+            if (dig.musc) {
+                dig.musc[2 * ((int64_t)t * dig.R + f)] = mean;
+                dig.musc[2 * ((int64_t)t * dig.R + f) + 1] = scale;
+            }
+        }
     }
     if (lane == 0) {
         if (f < m) {
@@ -258,7 +264,13 @@ __global__ void __launch_bounds__(SR_THREADS) k_stage_rows(const double* __restr
             for (int a = 0; a < OZ_DIGITS; ++a)
                 *reinterpret_cast<unsigned*>(dig.Q + ((int64_t)a * dig.R + f) * dig.KP + k0 + i0) = pk[a];
         }
-        if (tid == 0) dig.ex[(int64_t)t * dig.R + f] = e;
+        if (tid == 0) {
+            dig.ex[(int64_t)t * dig.R + f] = e;
+            if (dig.musc) {
+                dig.musc[2 * ((int64_t)t * dig.R + f)] = mean;
+                dig.musc[2 * ((int64_t)t * dig.R + f) + 1] = scale;
+            }
+        }
     }
     if (tid == 0) {
         if (f < m) {

@@ -907,3 +907,75 @@ def test_fast_n5_matches_oracle(oracle, T, kind):
     assert [g.indices for g in got] == [w["indices"] for w in want]
     assert bits_equal([g.score for g in got], [w["score"] for w in want])
     assert all(bits_equal(g.coefficients, w["coefficients"]) for g, w in zip(got, want))
+
+
+def _loose_rows(v, y, slices):
+    """Rows whose own INT8-Gram error term 1.9e-8 r 2^(2e) (max |z| < 2^e; the property relative
+    to |y_c|^2) exceeds 1e-6 in some task (ozaki.cu k_oz_eta)."""
+    out = set()
+    for sl in slices:
+        r = len(sl)
+        for f in range(len(v) + 1):
+            x = (v[f] if f < len(v) else y)[sl]
+            c = x - x.mean()
+            n2 = float(c @ c)
+            mx = np.abs(c).max() / (np.sqrt(n2) if f < len(v) else 1.0)
+            e = np.frexp(mx)[1]
+            term = 1.9e-8 * r * 2.0 ** (2 * e) / (n2 if f == len(v) else 1.0)
+            if term > 1e-6 * (1 - 1e-9):
+                out.add(f)
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_spiky", [3, 90])
+def test_ozaki_loose_rows_recomputed_in_fp64(rng, n_spiky):
+    """Spiky rows (one dominant sample) and a Gaussian property make single rows' INT8 error terms
+    too large: up to 64 of them are recomputed in fp64 (k_oz_fixup) and left out of eta, more fall
+    back to the DMMA Gram.  Either way every entry stays within the bounds, and the search returns
+    the DMMA-Gram search's models bit for bit and the oracle's top list."""
+    from oracle import oracle as orc
+    from paper_2502_20072_b200 import _lib
+
+    m, s, T = 140, 1600, 2
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    spiky = rng.choice(m, size=n_spiky, replace=False)
+    for f in spiky:
+        v[f, rng.integers(s)] += 40.0
+    y = rng.standard_normal(s) * 0.3 + 1.2 * v[5] - 0.8 * v[60] + 0.6 * v[99]
+    y[rng.integers(s)] += 6.0  # a spiky property too
+    slices = [np.arange(t, s, T) for t in range(T)]
+    want_loose = _loose_rows(v, y, slices)
+    assert m in want_loose and len(want_loose) >= n_spiky
+    perm = np.concatenate(slices).astype(np.int64)
+    bounds = np.array([0] + [len(sl) for sl in slices]).cumsum().astype(np.int64)
+    d, o = _lib.Engine(0), _lib.Engine(0)
+    d.set_gram_mode("dmma")
+    o.set_gram_mode("ozaki")
+    d.stage(v, y, perm, bounds, "fp64")
+    o.stage(v, y, perm, bounds, "fp64")
+    eta_d, _ = d.stage_info()
+    eta_o, oz_o = o.stage_info()
+    assert o.stage_loose_rows() == len(want_loose)
+    assert oz_o == (len(want_loose) <= 64)
+    assert (eta_o <= 1e-6).all()
+    for t in range(T):
+        gd, go = d.gram(t), o.gram(t)
+        scale = np.ones(m + 1)
+        scale[m] = np.sqrt(gd[m, m])
+        err = np.abs(go - gd) / np.outer(scale, scale)
+        assert err.max() <= eta_o[t] + eta_d[t], (t, err.max(), eta_o[t])
+        if oz_o:
+            rows = sorted(want_loose)
+            assert err[rows].max() <= 2 * eta_d[t] and err[:, rows].max() <= 2 * eta_d[t]
+    a = d.search(3, 10, 0, 2**62, "fast")
+    b = o.search(3, 10, 0, 2**62, "fast")
+    assert np.array_equal(a[1], b[1]) and bits_equal(a[0], b[0]) and bits_equal(a[2], b[2])
+    want = orc.l0_search(v, y, slices, 3, 10, "fp64")
+    assert [tuple(int(i) for i in _unrank(r, m)) for r in b[1]] == [w["indices"] for w in want]
+
+
+def _unrank(rank, m):
+    from paper_2502_20072_b200.search import unrank_tuple
+
+    return unrank_tuple(int(rank), m, 3)
