@@ -1374,14 +1374,16 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
         st->n_launches += ns;
     }
     const int64_t nc = std::min<int64_t>((int64_t)ncand, kc);
+    // the candidates' sorted bounds (SSR units) on the host: certificate thresholds below
+    std::vector<double> lbs((size_t)nc);
+    if (nc > 0) {
+        CK(cudaMemcpyAsync(lbs.data(), cl, sizeof(double) * nc, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    }
     // every excluded tuple has lb >= G_lb (SSR units): the K'-th smallest gathered bound, or
     // -- fewer gathered -- the final shared threshold (+inf: nothing was ever dropped)
     double G_lb = st->theta;
-    if ((int64_t)ncand >= kc) {
-        CK(cudaMemcpyAsync(&G_lb, cl + (kc - 1), sizeof(double), cudaMemcpyDeviceToHost, c->st));
-        CK(cudaStreamSynchronize(c->st));
-        G_lb = std::min(G_lb, st->theta);
-    }
+    if ((int64_t)ncand >= kc) G_lb = std::min(lbs[(size_t)kc - 1], st->theta);
     // A search part (l0s_search_part) answers for its own units only, but the seed's subsets come
     // from the whole problem: >= keep tuples score at most seed_cap / s, so the global keep-th
     // score is below that cap and a part's excluded tuples need only clear the cap.
@@ -1393,20 +1395,38 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     // above the cap (+ margin) are excluded like the rest (G_lb drops to the first of them)
     int64_t nref = nc;
     if (std::isfinite(cap) && nc > 0) {
-        std::vector<double> lbs((size_t)nc);
-        CK(cudaMemcpyAsync(lbs.data(), cl, sizeof(double) * nc, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaStreamSynchronize(c->st));
         const double lim = (cap + margin_of(cap)) * (double)c->s;
         nref = 0;
         while (nref < nc && lbs[(size_t)nref] <= lim) ++nref;
         if (nref < nc) G_lb = std::min(G_lb, lbs[(size_t)nref]);
     }
-    // exact refit of candidates + ill tuples
-    std::vector<Cand> exact;
+    // exact refit of the candidates in waves, lowest bounds first: the first wave (about one pass
+    // of k_exact_smem over the device at T tasks) usually certifies alone -- the candidates after
+    // it have lb >= lbs[done] -- and the rest are refit only when it does not.  Results are the
+    // full refit's: an excluded candidate scores above the keep-th exact score by the margin.
     cudaEventRecord(c->ev[2], c->st);
-    int rc = exact_ranks_to_host(c, n, cr, nref, exact, &st->n_launches, &c->recs);
-    if (rc) return rc;
-    merge_best(best, exact, keep);
+    int rc = L0S_OK;
+    {
+        const int64_t wave = std::max<int64_t>(keep + 8, 256 / std::max(1, c->T));
+        int64_t done = 0;
+        while (done < nref) {
+            const int64_t nb = done == 0 ? std::min(nref, wave) : nref - done;
+            std::vector<Cand> exact;
+            rc = exact_ranks_to_host(c, n, cr + done, nb, exact, &st->n_launches, &c->recs);
+            if (rc) return rc;
+            merge_best(best, exact, keep);
+            done += nb;
+            if (done < nref) {
+                const double sk = std::min(((int64_t)best.size() >= keep) ? best[(size_t)keep - 1].score : INFINITY,
+                                           cap);
+                if (lbs[(size_t)done] / (double)c->s > sk + margin_of(sk)) {
+                    G_lb = std::min(G_lb, lbs[(size_t)done]);
+                    break;
+                }
+            }
+        }
+        nref = done;
+    }
     if (nill > 0) {
         // Tuples the Gram screen could not certify: TSQR on the device gives each a score and
         // the reference's rank-rule ratio; only those that can reach the top list within the

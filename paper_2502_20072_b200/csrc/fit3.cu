@@ -67,6 +67,22 @@ namespace {
 #ifndef L0S_WREL
 #define L0S_WREL 0
 #endif
+// PA (phase A, NT > 1): before the per-group task loop, the first slot of every row of the tile is
+// tested division-free, (K - theta) d - q < 0 with the same shrunk K (no MUFU, no per-group vote:
+// one OR-reduction per tile); only groups with a survivor run the task loop.  A warp switches it
+// off while more than PA_NUM / PA_DEN of its groups survive the first slot (dense near-ties: the
+// test would only add work) and back on when fewer do.  Off: measured slower (C3 planted fit 1.565 ->
+// 1.77 ms, random y 3.94 -> 4.00 ms; the per-group vote is not what limits the sweep, and the extra
+// live ranges spill -- tools/tune_fit.py).
+#ifndef L0S_PHASEA
+#define L0S_PHASEA 0
+#endif
+#ifndef L0S_PA_NUM
+#define L0S_PA_NUM 2
+#endif
+#ifndef L0S_PA_DEN
+#define L0S_PA_DEN 5
+#endif
 // DF: the first task slot's test is division-free, (K - theta) d - q < 0, one FMA and no MUFU;
 // only groups that survive it re-evaluate that slot with the reciprocal (as NT == 1 always does).
 // WREL: tile buffers are released per warp (mbarrier + last-arriver refill), no CTA barrier per tile.
@@ -192,6 +208,10 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
     constexpr int NW3 = C::NW, NT3 = C::NTH;
     constexpr int P = C::P, IB = C::IB, TS = C::TS, BS = C::BS, KSPAN = C::KSPAN, R = C::R, NB = C::NBUF;
     constexpr bool DF = L0S_DIVFREE && NT > 1 && !C::SLOT0 && (P % 2 == 0);
+    constexpr bool PA = L0S_PHASEA && NT > 1 && !DF && !C::SLOT0 && (P % 2 == 0);
+    constexpr int NG = IB / R;  // vote groups per tile
+    static_assert(!PA || NG <= 32, "group bits in one word");
+    int pa_tot = 0, pa_surv = 0;  // groups seen / surviving the first slot (warp-uniform, decayed)
     extern __shared__ __align__(128) double sm[];
     __shared__ int s_unit;
     __shared__ int s_tord[NT];
@@ -517,6 +537,57 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
                     sg |= (unsigned)__double2hiint(fma(Kq[p], d, -q));
                 }
             };
+            // PA: slot 0 of one row, division-free with the shrunk Kq: sign bit of Kq d - q (alive when
+            // negative: d > 0 and lb_0 below theta, or d <= 0), OR-ed into sg
+            auto task_row_a = [&](unsigned& sg, int ii) {
+                const double* Tt = T0;
+                const double g0 = Tt[ii * 32 + lane];
+                const double ci = Tt[IB * (32 + KSPAN) + 2 * ii + (int)(m & 1)];
+                double gk[P];
+#pragma unroll
+                for (int p = 0; p < P; p += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(Tt + IB * 32 + ii * KSPAN + warp * P + p);
+                    gk[p] = v.x;
+                    gk[p + 1] = v.y;
+                }
+                const double D = fma(-g0, g0, 1.0);
+                const double V = fma(-g0, w0[0], ci);
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const double g1 = fma(-L10[p][0], g0, gk[p]);
+                    const double e1 = g1 * rd1[p][0];
+                    const double w = fma(-g1, s1[p][0], V);
+                    const double d = fma(-g1, e1, D);
+                    const double q = fma(w, w, Bm[p]);
+                    sg |= (unsigned)__double2hiint(fma(Kq[p], d, -q));
+                }
+            };
+            // phase A (PA): division-free first-slot test of every row, one bit per group
+            unsigned gal = ~0u;
+            bool use_a = false;
+            if constexpr (PA) {
+                use_a = pa_surv * L0S_PA_DEN <= pa_tot * L0S_PA_NUM;
+                if (use_a) {
+                    unsigned lb = 0u;
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        unsigned sg = 0u;
+#pragma unroll
+                        for (int r = 0; r < R; ++r) task_row_a(sg, g * R + r);
+                        lb |= (sg >> 31) << g;
+                    }
+                    gal = __reduce_or_sync(L0S_FULL, lb);
+                    n_ev += NG;
+                    pa_tot += NG;
+                    pa_surv += __popc(gal);
+                } else {
+                    pa_tot += NG;  // pa_surv counts the groups passing the first slot's vote below
+                }
+                if (pa_tot >= 512) {
+                    pa_tot >>= 1;
+                    pa_surv >>= 1;
+                }
+            }
 #pragma unroll
             for (int pw = 0; pw < NPW; ++pw) {
                 unsigned word = 0u;
@@ -542,6 +613,8 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
                             }
                             ++n_ev;
                         }
+                    } else if (PA && !((gal >> ((pw * IPW + ig) / R)) & 1u)) {
+                        live = false;  // no lane's first slot is below theta (phase A)
                     } else {
 #pragma unroll
                         for (int r = 0; r < R; ++r) {
@@ -564,6 +637,7 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
                             live = false;
                             break;
                         }
+                        if (PA && t == 1 && !use_a) ++pa_surv;
                         double kt[P];
 #pragma unroll
                         for (int p = 0; p < P; ++p) {

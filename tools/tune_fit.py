@@ -22,12 +22,10 @@ VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
     "base": (),
-    "df": ("L0S_DIVFREE=1",),
-    "unroll2": ("L0S_C34_UNROLL=2",),
-    "r8": ("L0S_PRUNE_ROWS=8",),
-    "r2": ("L0S_PRUNE_ROWS=2",),
-    "p2nw8m2": ("L0S_C34_P=2", "L0S_C34_NW=8", "L0S_C34_IB=32"),
-    "ib32m2nw4": ("L0S_C34_IB=32", "L0S_CAP=128"),
+    "nopa": ("L0S_PHASEA=0",),
+    "pa_always": ("L0S_PA_DEN=0",),
+    "pa_35": ("L0S_PA_NUM=3", "L0S_PA_DEN=5"),
+    "pa_15": ("L0S_PA_NUM=1", "L0S_PA_DEN=5"),
 }
 if os.environ.get("L0S_TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["L0S_TUNE_ONLY"].split(",")}
