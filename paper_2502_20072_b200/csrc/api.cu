@@ -145,6 +145,8 @@ struct l0s_ctx {
         lb_tmp, rank_tmp, coll_lb, coll_rank, coll_cnt;
     DBuf ex_scratch, ex_ssr_tmp, ex_ok_tmp, ex_ok, ex_score, ex_coef, ex_ssr, ex_ranks, ex_tuples;
     DBuf qr_ssr, qr_ratio, qr_score, qr_minr;
+    DBuf ddg_hi, ddg_lo;     // double-double Gram of the staged columns (ddgram.cu), on first use
+    bool ddg_ready = false;  // ... for the current stage
     // SIS projection scores
     DBuf sis_y, sis_yc, sis_sy, sis_perm, sis_bounds, sis_F, sis_out, sis_dest, sis_tE, sis_tpoff;
     // final-rung candidates (gen.cu)
@@ -171,7 +173,7 @@ struct l0s_ctx {
                        &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &umin, &binom, &units, &ucount, &n_eval, &theta_g, &hist, &seedbuf, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
                        &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
-                       &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr, &sis_y, &sis_yc, &sis_sy, &sis_perm,
+                       &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr, &ddg_hi, &ddg_lo, &sis_y, &sis_yc, &sis_sy, &sis_perm,
                        &sis_bounds, &sis_F, &sis_out, &sis_dest, &sis_tE, &sis_tpoff, &oz_q, &oz_ex, &oz_koff, &oz_musc, &oz_fix,
                        &res_tup, &res_coef, &res_out, &dd_lo, &dd_hi, &dd_owner, &dd_state, &dd_used, &dd_kept, &dd_seed, &gen_pool, &gen_pi, &gen_pj, &gen_vals, &gen_valid, &gen_hash, &gen_take, &gen_rows, &gen_out};
         for (DBuf* b : all) b->release();
@@ -521,6 +523,7 @@ static int stage_post(l0s_ctx* c) {
             CK(cudaStreamSynchronize(c->st));
         }
     }
+    c->ddg_ready = false;
     c->ms_gram = elapsed(c->ev[0], c->ev[1]);
     c->ms_gram_k = c->gram_timed ? elapsed(c->ev[2], c->ev[3]) : 0.0;
     c->gram_timed = false;
@@ -1015,6 +1018,8 @@ int l0s_screen_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, d
     return L0S_OK;
 }
 
+static int run_qr_screen(l0s_ctx* c, QrArgs& q, int n, int64_t count, int64_t* launches, bool allow_dd);
+
 int l0s_qr_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, double* out_score, double* out_ratio) {
     if (!c || !c->staged) return fail(L0S_ESTATE, "l0s_stage must be called first");
     if (n < 1 || n > 6) return fail(L0S_EINVAL, "the QR screen takes n in [1, 6]");
@@ -1047,8 +1052,8 @@ int l0s_qr_tuples(l0s_ctx* c, int n, const int64_t* tuples, int64_t count, doubl
     q.ratio = c->qr_ratio.as<double>();
     q.score = c->qr_score.as<double>();
     q.min_ratio = c->qr_minr.as<double>();
-    launch_qr_screen(q, count, c->st, nullptr);
-    CK(cudaGetLastError());
+    rc = run_qr_screen(c, q, n, count, nullptr, false);  // diagnostics: TSQR unless L0S_QR_SCREEN=dd
+    if (rc) return rc;
     CK(cudaMemcpyAsync(out_score, c->qr_score.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(out_ratio, c->qr_minr.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
@@ -1129,6 +1134,34 @@ static int search_exact_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_
 }
 
 // QR screen of the `nill` ranks in c->ill, then bit-exact refit of the ones that can matter.
+// L0S_QR_SCREEN=dd | tsqr forces the ill-tuple screen (tests, experiments); else chosen by cost
+static int qr_screen_forced() {
+    const char* e = getenv("L0S_QR_SCREEN");
+    return !e ? 0 : (!strcmp(e, "dd") ? 2 : (!strcmp(e, "tsqr") ? 1 : 0));
+}
+
+// the QR screen of `count` ranks already in q.ranks (scores and min ratios in q.score / q.min_ratio)
+static int run_qr_screen(l0s_ctx* c, QrArgs& q, int n, int64_t count, int64_t* launches, bool allow_dd) {
+    const int forced = qr_screen_forced();
+    bool dd = forced == 2 || (forced == 0 && allow_dd && dd_screen_pays(count, n, c->T, c->m, c->s));
+    if (dd) {
+        const int64_t LD = dd_gram_ld(c->m);
+        const size_t bytes = sizeof(double) * (size_t)c->T * LD * LD;
+        dd = c->ddg_hi.ensure(bytes) == cudaSuccess && c->ddg_lo.ensure(bytes) == cudaSuccess;
+        if (!dd) cudaGetLastError();
+    }
+    if (dd) {
+        launch_dd_screen(q, count, c->ddg_hi.as<double>(), c->ddg_lo.as<double>(), c->ddg_ready, c->st, launches);
+        c->ddg_ready = true;
+        q.total = count * q.T;
+        launch_qr_finalize(q, count, c->st, launches);
+    } else {
+        launch_qr_screen(q, count, c->st, launches);
+    }
+    CK(cudaGetLastError());
+    return L0S_OK;
+}
+
 static int screen_ill(l0s_ctx* c, int n, int64_t nill, int64_t keep, std::vector<Cand>& best, l0s_stats* st,
                       double cap = INFINITY) {
     if (c->prec == L0S_PREC_FP32) {
@@ -1164,7 +1197,12 @@ static int screen_ill(l0s_ctx* c, int n, int64_t nill, int64_t keep, std::vector
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, c->st);
-    launch_qr_screen(q, nill, c->st, &st->n_launches);
+    // many ill tuples: one double-double Gram of every column, then a (n + 2)-block LDL^T per
+    // tuple (ddgram.cu); few: the TSQR screen reads each tuple's columns
+    {
+        const int rc = run_qr_screen(c, q, n, nill, &st->n_launches, true);
+        if (rc) return rc;
+    }
     cudaEventRecord(e1, c->st);
     CK(cudaGetLastError());
     CK(cudaEventSynchronize(e1));

@@ -146,6 +146,13 @@ struct QrArgs {
     int64_t g0, total;      // set by the launcher
 };
 void launch_qr_screen(const QrArgs& a, int64_t count, cudaStream_t st, int64_t* launches);
+// the same screen through a double-double Gram of every staged column (ddgram.cu): Hhi / Hlo
+// (T x LD x LD each, LD = dd_gram_ld(m)) are filled unless gram_ready
+void launch_qr_finalize(const QrArgs& a, int64_t count, cudaStream_t st, int64_t* launches);  // score, min_ratio
+int64_t dd_gram_ld(int64_t m);
+bool dd_screen_pays(int64_t nill, int n, int T, int64_t m, int64_t s);
+void launch_dd_screen(const QrArgs& a, int64_t count, double* Hhi, double* Hlo, bool gram_ready, cudaStream_t st,
+                      int64_t* launches);
 // ranks of the screened ill tuples that may still reach the top list (selection on the device)
 void launch_qr_select(const double* score, const double* min_ratio, const int64_t* ranks, int64_t count, double tol,
                       double sk, double yy_s, int64_t* sel, unsigned long long* nsel, int64_t cap, cudaStream_t st);

@@ -184,6 +184,13 @@ __global__ void k_qr_select(const double* __restrict__ score, const double* __re
 
 }  // namespace
 
+void launch_qr_finalize(const QrArgs& a, int64_t count, cudaStream_t st, int64_t* launches) {
+    if (count > 0) {
+        k_qr_finalize<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(a, count);
+        if (launches) ++*launches;
+    }
+}
+
 void launch_qr_select(const double* score, const double* min_ratio, const int64_t* ranks, int64_t count, double tol,
                       double sk, double yy_s, int64_t* sel, unsigned long long* nsel, int64_t cap, cudaStream_t st) {
     if (count > 0)

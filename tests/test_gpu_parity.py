@@ -979,3 +979,74 @@ def _unrank(rank, m):
     from paper_2502_20072_b200.search import unrank_tuple
 
     return unrank_tuple(int(rank), m, 3)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [3, 4])
+def test_dd_screen_matches_tsqr(rng, monkeypatch, n):
+    """The double-double Gram screen (ddgram.cu) against the TSQR screen on tuples holding near-
+    copies from 1e-4 down to 1e-13, near-constants and duplicates: equal rank-rule decisions where
+    the ratio is clear of the 1e-10 tolerance, ratios within 1e-3 relative and scores within the
+    select kernel's margin (api.cu screen_ill) wherever the rank rule keeps the tuple."""
+    from paper_2502_20072_b200 import _lib
+
+    m, s, T = 60, 700, 2
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    for c, d in enumerate([1e-4, 1e-6, 1e-8, 1e-9, 1e-10, 1e-11, 1e-12, 1e-13]):
+        v[40 + c] = v[c] + d * rng.standard_normal(s)
+    for c, d in enumerate([1e-5, 1e-9, 1e-12]):
+        v[50 + c] = 1.0 + c + d * rng.standard_normal(s)
+    v[55] = v[20]
+    y = 1.3 * v[12] - 0.6 * v[21] + 1e5 * (v[41] - v[1]) + 0.01 * rng.standard_normal(s)
+    slices = [np.arange(t, s, T) for t in range(T)]
+    perm = np.concatenate(slices).astype(np.int64)
+    bounds = np.array([0] + [len(sl) for sl in slices]).cumsum().astype(np.int64)
+    eng = _lib.Engine(0)
+    eng.stage(v, y, perm, bounds, "fp64")
+    tups = set()
+    for a in list(range(40, 56)):
+        for _ in range(40):
+            rest = rng.choice([f for f in range(m) if f != a], size=n - 1, replace=False)
+            tups.add(tuple(sorted([a, *rest.tolist()])))
+    while len(tups) < 1500:
+        tups.add(tuple(sorted(rng.choice(m, size=n, replace=False).tolist())))
+    tup = np.array(sorted(tups), dtype=np.int64)
+    monkeypatch.setenv("L0S_QR_SCREEN", "tsqr")
+    sc_q, r_q = eng.qr_tuples(tup)
+    monkeypatch.setenv("L0S_QR_SCREEN", "dd")
+    sc_d, r_d = eng.qr_tuples(tup)
+    tol = 1e-10
+    clear = (r_q > 2 * tol) | (r_q < 0.5 * tol)
+    assert np.array_equal(r_q[clear] < tol, r_d[clear] < tol)
+    keep = r_q > 2 * tol
+    assert np.all(np.abs(r_d[keep] - r_q[keep]) <= 1e-3 * r_q[keep])
+    yy = sum(float(np.sum((y[sl] - y[sl].mean()) ** 2)) for sl in slices) / s
+    margin = 1e3 * 2.220446049250313e-16 * yy / r_q[keep] + 1e-9 * np.abs(sc_q[keep])
+    assert np.all(np.abs(sc_d[keep] - sc_q[keep]) <= margin)
+    assert keep.sum() > 1000 and (~keep).sum() > 50
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [3, 4])
+def test_qr_screen_dd_search_matches_oracle(oracle, monkeypatch, n):
+    """The ill-conditioned miniature of test_qr_screen_ill_tuples_match_oracle with the double-double
+    screen forced: same models as the exhaustive oracle, bit for bit."""
+    from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
+
+    monkeypatch.setenv("L0S_QR_SCREEN", "dd")
+    rng = np.random.default_rng(40 + n)
+    m, s, T = 44, 240, 2
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    for c, d in enumerate([1e-4, 1e-6, 1e-8, 1e-9, 1e-11, 1e-13]):
+        v[30 + c] = v[c] + d * rng.standard_normal(s)
+    for c, d in enumerate([1e-5, 1e-12]):
+        v[38 + c] = 1.0 + c + d * rng.standard_normal(s)
+    v[41] = v[10]
+    slices = [np.arange(t, s, T) for t in range(T)]
+    y = 1e6 * (v[31] - v[1]) + 0.7 * v[12] + (0.4 * v[20] if n == 4 else 0.0) + 0.01 * rng.standard_normal(s)
+    want = oracle.l0_search(v, y, slices, n, 10, "fp64", threads=os.cpu_count() or 1)
+    st = SearchStats()
+    got = l0_search(v, y, slices, L0Config(dimension=n), mode="fast", stats=st)
+    assert st.device["certified"] == 1 and st.device["n_ill"] > 0
+    assert [md.indices for md in got] == [w["indices"] for w in want]
+    assert bits_equal([md.score for md in got], [w["score"] for w in want])

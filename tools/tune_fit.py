@@ -22,10 +22,11 @@ VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
     "base": (),
-    "nopa": ("L0S_PHASEA=0",),
-    "pa_always": ("L0S_PA_DEN=0",),
-    "pa_35": ("L0S_PA_NUM=3", "L0S_PA_DEN=5"),
-    "pa_15": ("L0S_PA_NUM=1", "L0S_PA_DEN=5"),
+    "p2m3ib16": ("L0S_C34_P=2", "L0S_C34_MINB=3", "L0S_C34_IB=16"),
+    "p2m3ib24": ("L0S_C34_P=2", "L0S_C34_MINB=3", "L0S_C34_IB=24"),
+    "p2m4ib16": ("L0S_C34_P=2", "L0S_C34_MINB=4", "L0S_C34_IB=16"),
+    "p2m2ib24": ("L0S_C34_P=2", "L0S_C34_MINB=2", "L0S_C34_IB=24"),
+    "p4m3ib16": ("L0S_C34_MINB=3", "L0S_C34_IB=16"),
 }
 if os.environ.get("L0S_TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["L0S_TUNE_ONLY"].split(",")}
