@@ -1147,7 +1147,8 @@ static int run_qr_screen(l0s_ctx* c, QrArgs& q, int n, int64_t count, int64_t* l
     if (dd) {
         const int64_t LD = dd_gram_ld(c->m);
         const size_t bytes = sizeof(double) * (size_t)c->T * LD * LD;
-        dd = c->ddg_hi.ensure(bytes) == cudaSuccess && c->ddg_lo.ensure(bytes) == cudaSuccess;
+        dd = c->ddg_hi.ensure(bytes) == cudaSuccess &&
+             c->ddg_lo.ensure(sizeof(double) * (size_t)dd_gram_lo_doubles(c->m, c->T)) == cudaSuccess;
         if (!dd) cudaGetLastError();
     }
     if (dd) {
@@ -1281,11 +1282,21 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     // (or 74, one refit wave at T = 4) the part holding the best tuples of C3 missed its
     // certificate and paid a rescan (~1 ms); 96 and 128 refit in two waves (0.40 ms) and
     // certify (tools/parts_balance.py)
+    // Dimension >= 4 sweeps keep 512-entry lists (fitcommon.cuh CAP_WIDE) and K' = 320: C4's ~260
+    // near-ties within the margin of the 10th score then certify without a rescan sweep
+    // (168 -> ~95 ms); the refit waves still stop after the first wave when it certifies.
     // Large keep (> kKeepLists): no per-warp lists; every accepted bound goes to a global candidate
-    // list below the histogram threshold of K' = keep + 32 (collect mode 2, fitcommon.cuh)
-    const bool big = keep > kKeepLists;
-    const int kc = big ? (int)(keep + std::max<int64_t>(32, keep / 2))  // slack: near-ties among the keep best
-                       : (c->nparts > 1 ? 128 : (int)std::min<int64_t>(128, std::max<int64_t>(64, keep + 32)));
+    // list below the histogram threshold of K' = keep + 32 (collect mode 2, fitcommon.cuh; a global
+    // list for every search was tried: dense near-ties flood it, C3 random y 3.9 -> 8.3 ms)
+    static const int kprime_env = [] {
+        const char* e = getenv("L0S_KPRIME");  // experiments: global list of this K'
+        return e ? atoi(e) : 0;
+    }();
+    const bool big = keep > kKeepLists || kprime_env > 0;
+    const int kc = kprime_env > 0 ? std::max<int>(kprime_env, (int)keep + 32)
+                   : big ? (int)(keep + std::max<int64_t>(32, keep / 2))  // slack: near-ties among the keep best
+                   : n >= 4 ? (int)std::min<int64_t>(480, std::max<int64_t>(320, keep + 32))  // CAP_WIDE lists
+                            : (c->nparts > 1 ? 128 : (int)std::min<int64_t>(128, std::max<int64_t>(64, keep + 32)));
     const int64_t coll_cap = (int64_t)1 << 24;
     const int grid = n == 2   ? fit2_grid(c->T, c->nsm)
                      : n == 3 ? fit3_grid(c->T, c->nsm)

@@ -183,6 +183,11 @@ __global__ void __launch_bounds__(128) k_dd_ill(QrArgs a, const double* __restri
 }  // namespace
 
 int64_t dd_gram_ld(int64_t m) { return (m + 2 + DG_T - 1) / DG_T * DG_T; }
+// doubles of the lo buffer: T x LD x LD plus the tile list
+int64_t dd_gram_lo_doubles(int64_t m, int T) {
+    const int64_t LD = dd_gram_ld(m), nb = LD / DG_T;
+    return (int64_t)T * LD * LD + nb * (nb + 1) / 2;
+}
 
 // The double-double screen pays for its Gram when the TSQR screen would read far more:
 // TSQR ~ 60 flops per row per column pair, the Gram ~ 10 flops per (pair, row) once.
@@ -203,12 +208,14 @@ void launch_dd_screen(const QrArgs& a0, int64_t count, double* Hhi, double* Hlo,
         std::vector<int2> tl;
         for (int x = 0; x < nb; ++x)
             for (int y = x; y < nb; ++y) tl.push_back(make_int2(x, y));
-        int2* tiles = nullptr;
-        cudaMallocAsync(&tiles, sizeof(int2) * tl.size(), st);
+        // the tile list rides behind the lo buffer's T matrices (dd_gram_lo_doubles): no
+        // allocation on the stream (a cudaMallocAsync / cudaFreeAsync pair here made single
+        // searches intermittently ~0.7 s slower)
+        static_assert(sizeof(int2) == 8, "int2 packs into one double slot");
+        int2* tiles = reinterpret_cast<int2*>(Hlo + (int64_t)a0.T * LD * LD);
         cudaMemcpyAsync(tiles, tl.data(), sizeof(int2) * tl.size(), cudaMemcpyHostToDevice, st);
         k_ddgram<<<dim3((unsigned)tl.size(), (unsigned)a0.T), 256, 0, st>>>(a0.Xp, a0.yp, a0.m, a0.s, a0.bounds, LD,
                                                                              tiles, Hhi, Hlo);
-        cudaFreeAsync(tiles, st);
         if (launches) ++*launches;
     }
     QrArgs a = a0;

@@ -29,7 +29,7 @@ struct Cfg4 {
     static constexpr int LSPAN = NW * P;
     static constexpr int TS = IB * (32 + LSPAN + 2);  // C[i, j-block] | C[i, l-span] | C[i, k] | c_i
     static constexpr int BS = NT * TS;
-    static constexpr size_t smem_bytes = (size_t)2 * BS * 8 + (size_t)NW * CAP * 16 + (size_t)256 * P * 8;
+    static constexpr size_t smem_bytes = (size_t)2 * BS * 8 + (size_t)NW * CAP_WIDE * 16 + (size_t)256 * P * 8;
 };
 
 // Hoisted LDL^T of (j, k, l) for one task (normalized, centered), plus the bound's trace term.
@@ -106,11 +106,11 @@ __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs
     __shared__ int s_unit;
     __shared__ unsigned char s_force[2][IB];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    double* sKraw = sm + 2 * BS + 2 * NW * CAP + tid * P;
+    double* sKraw = sm + 2 * BS + 2 * NW * CAP_WIDE + tid * P;
     const int64_t m = a.m, mp = a.mp;
     const double shrink = (NT == 1) ? 1.0 : (1.0 - 2.0 * kRcpRel);
-    WarpCands wc{sm + 2 * BS + warp * CAP, reinterpret_cast<int64_t*>(sm + 2 * BS + NW * CAP) + warp * CAP, 0,
-                 a.collect == 1 ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g), 0};
+    WarpCands wc{sm + 2 * BS + warp * CAP_WIDE, reinterpret_cast<int64_t*>(sm + 2 * BS + NW * CAP_WIDE) + warp * CAP_WIDE, 0,
+                 a.collect == 1 ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g), 0, CAP_WIDE};
     const int64_t* B2 = a.binom + 2 * (m + 1);
     const int64_t* B3 = a.binom + 3 * (m + 1);
     const int64_t* B4 = a.binom + 4 * (m + 1);

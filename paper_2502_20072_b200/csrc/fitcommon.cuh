@@ -14,6 +14,10 @@ constexpr int NW = 8;                 // warps per CTA
 #define L0S_CAP 256
 #endif
 constexpr int CAP = L0S_CAP;          // per-warp candidate buffer (K' <= CAP - 32)
+// dimension >= 4 sweeps (one CTA per SM, shared memory to spare) keep longer lists: dense near-
+// ties among the keep best (C4: ~260 tuples within the margin of the 10th score) then certify
+// in one sweep instead of two
+constexpr int CAP_WIDE = 512;
 static_assert((CAP & (CAP - 1)) == 0, "warp_sort is a bitonic network over CAP entries");
 constexpr double FO_LIM = 1e-3;       // first-order validity: (eta + gam rho)(1 + n tr) <= FO_LIM
 constexpr double RANK_SLACK = 1.01;   // safety factor on the rank-rule certificate
@@ -105,16 +109,16 @@ __device__ __forceinline__ bool cand_gt(double a, int64_t ra, double b, int64_t 
     return a > b || (a == b && ra > rb);
 }
 
-// Warp-wide bitonic sort of the CAP-entry buffer by (lb, rank); entries [cnt, CAP) are padding.
-__device__ __forceinline__ void warp_sort(double* lb, int64_t* rk, int cnt, int lane) {
-    for (int x = cnt + lane; x < CAP; x += 32) {
+// Warp-wide bitonic sort of the cap-entry buffer by (lb, rank); entries [cnt, cap) are padding.
+__device__ __forceinline__ void warp_sort(double* lb, int64_t* rk, int cnt, int lane, int cap) {
+    for (int x = cnt + lane; x < cap; x += 32) {
         lb[x] = __longlong_as_double(0x7ff0000000000000ll);
         rk[x] = 0x7fffffffffffffffll;
     }
     __syncwarp();
-    for (int k = 2; k <= CAP; k <<= 1) {
+    for (int k = 2; k <= cap; k <<= 1) {
         for (int jj = k >> 1; jj > 0; jj >>= 1) {
-            for (int x = lane; x < CAP; x += 32) {
+            for (int x = lane; x < cap; x += 32) {
                 int y = x ^ jj;
                 if (y > x) {
                     bool up = (x & k) == 0;
@@ -140,6 +144,7 @@ struct WarpCands {
     int cnt;
     double theta;
     int counted;  // entries [0, counted) are already in the global histogram
+    int cap = CAP;  // buffer entries (a power of two; K' <= cap - 32)
 };
 
 // ---- global lower-bound histogram (the shared threshold) ----
@@ -285,7 +290,7 @@ __device__ __forceinline__ void drain_pending(const FitArgs& a, unsigned (&pend)
             }
         }
         __syncwarp();
-        if (wc.cnt > CAP - 32) {
+        if (wc.cnt > wc.cap - 32) {
             if (a.collect) {
                 flush_collect(a, wc, lane);
                 if (a.collect == 2) {
@@ -300,7 +305,7 @@ __device__ __forceinline__ void drain_pending(const FitArgs& a, unsigned (&pend)
                 }
             } else {
                 hist_count(a, wc, lane);
-                warp_sort(wc.lb, wc.rk, wc.cnt, lane);
+                warp_sort(wc.lb, wc.rk, wc.cnt, lane, wc.cap);
                 if (wc.cnt > a.kc) wc.cnt = a.kc;
                 wc.counted = wc.cnt;
                 double th = hist_theta(a, lane);
@@ -502,7 +507,7 @@ __device__ __forceinline__ void flush_warp(const FitArgs& a, WarpCands& wc, int 
         flush_collect(a, wc, lane);
         if (lane == 0) a.wl_cnt[slot] = 0;
     } else {
-        warp_sort(wc.lb, wc.rk, wc.cnt, lane);
+        warp_sort(wc.lb, wc.rk, wc.cnt, lane, wc.cap);
         if (wc.cnt > a.kc) wc.cnt = a.kc;
         for (int x = lane; x < wc.cnt; x += 32) {
             a.wl_lb[(int64_t)slot * a.kc + x] = wc.lb[x];

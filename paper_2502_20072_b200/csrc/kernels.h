@@ -150,6 +150,7 @@ void launch_qr_screen(const QrArgs& a, int64_t count, cudaStream_t st, int64_t* 
 // (T x LD x LD each, LD = dd_gram_ld(m)) are filled unless gram_ready
 void launch_qr_finalize(const QrArgs& a, int64_t count, cudaStream_t st, int64_t* launches);  // score, min_ratio
 int64_t dd_gram_ld(int64_t m);
+int64_t dd_gram_lo_doubles(int64_t m, int T);
 bool dd_screen_pays(int64_t nill, int n, int T, int64_t m, int64_t s);
 void launch_dd_screen(const QrArgs& a, int64_t count, double* Hhi, double* Hlo, bool gram_ready, cudaStream_t st,
                       int64_t* launches);
