@@ -337,7 +337,7 @@ class _Subspace:
 
 
 @pytest.mark.parametrize("shape", [(30, 25, 2, 600), (300, 200, 2, 3000)])
-def test_incremental_stage_across_dimensions(monkeypatch, shape):
+def test_incremental_stage_across_dimensions(monkeypatch, oracle, shape):
     """The pipeline's subspace grows by appending between dimensions: l0_search then sends only
     the new rows (l0s_stage_append) and returns exactly what a full stage of the concatenated
     matrix returns; a changed property or partition restages in full."""
@@ -368,6 +368,12 @@ def test_incremental_stage_across_dimensions(monkeypatch, shape):
         assert bits_equal([md.score for md in g], [md.score for md in w])
         assert all(bits_equal(a.coefficients, b.coefficients) for a, b in zip(g, w))
     assert got[0].expressions is not None and got[0].expressions[0] == "f3"
+    if m0 + m1 <= 80:  # and the reference's answer (oracle, pinned to the reference's goldens)
+        ref = oracle.l0_search(np.stack([e.values for e in sub1.entries]), y, slices, 3, 10, "fp64",
+                               threads=os.cpu_count() or 1)
+        assert [md.indices for md in got] == [w["indices"] for w in ref]
+        assert bits_equal([md.score for md in got], [w["score"] for w in ref])
+        assert all(bits_equal(a.coefficients, w["coefficients"]) for a, w in zip(got, ref))
     # a different property: full restage (no append), same answer as a fresh stage
     l0_search(sub0, y, slices, L0Config(dimension=2))
     y2 = y + 0.1 * v[7]

@@ -1,7 +1,8 @@
 """A small workload touching every kernel family once, for compute-sanitizer (racecheck /
 synccheck / memcheck): screened n = 2, 3, 4 searches (TMA + mbarrier sweeps, seeds, merge),
 the INT8 Ozaki Gram (tcgen05 + TMEM + TMA), the QR screen, the exact kernels, SIS scores and
-the final-rung evaluator.  Checks every result against the oracle."""
+the final-rung evaluator, the INT8 Gram fix-up rows and the double-double ill-tuple screen.
+Checks every result against the oracle."""
 import os
 import sys
 
@@ -43,6 +44,20 @@ def main():
     check(got, orc.l0_search(v2, y2, None, 2, 150, "fp64", threads=16))
     got = l0_search(v2, y2, None, L0Config(dimension=1), mode="exact")
     check(got, orc.l0_search(v2, y2, None, 1, 10, "fp64", threads=16))
+    # spiky rows and a spiky property: INT8 Gram with fp64 fix-up rows (k_oz_fixup)
+    vs = v.copy()
+    for f in (7, 77, 177):
+        vs[f, rng.integers(s)] += 40.0
+    ys = y.copy()
+    ys[rng.integers(s)] += 3.0
+    got = l0_search(vs, ys, sl, L0Config(dimension=3), mode="fast")
+    check(got, orc.l0_search(vs, ys, sl, 3, 10, "fp64", threads=16))
+    assert _lib.engine(0).stage_loose_rows() > 0, "no loose rows"
+    # ill tuples through the double-double Gram screen (ddgram.cu)
+    os.environ["L0S_QR_SCREEN"] = "dd"
+    got = l0_search(v2, y2, None, L0Config(dimension=4), mode="fast")
+    check(got, orc.l0_search(v2, y2, None, 4, 10, "fp64", threads=16))
+    del os.environ["L0S_QR_SCREEN"]
     # SIS scores
     eng = _lib.engine(0)
     eng.sis_prepare(np.stack([y, y ** 2]), np.concatenate(sl), np.array([0, 200, 400]))
