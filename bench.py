@@ -391,6 +391,10 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    if world > 1:  # the parts certify against the keep-th of their union (one all-gather)
+        from paper_2502_20072_b200.dist import exchange_keepth
+
+        eng.set_part_exchange(lambda scores: exchange_keepth(scores, 10))
     for _ in range(args.warmup):
         device_step()
     barrier()

@@ -138,6 +138,21 @@ int l0s_search_part(l0s_ctx *ctx, int n, int64_t keep, int part, int nparts, int
                     int64_t *out_count, l0s_stats *stats);
 
 /*
+ * Cross-part exchange for l0s_search_part (multi-GPU; no reference counterpart: the reference's
+ * workers share one process and merge at the end, search.py:258-304).  When set, every
+ * screened search part calls fn exactly once, after refitting its first candidates and before
+ * certifying: scores = the part's best exact scores so far (ascending, count <= keep).  fn must
+ * return an upper bound on the whole search's keep-th score -- a collective: the keep-th of the
+ * union of every part's list (all-gather + merge), or +inf.  The part then certifies against
+ * it instead of its own keep-th, so a part holding dense near-ties need not rescan for tuples
+ * other parts have already beaten.  A part that fails before the exchange leaves the others
+ * waiting in fn: the caller's collective must handle that (the group API's does).  fn == NULL
+ * clears it.
+ */
+typedef double (*l0s_exchange_fn)(const double *scores, int64_t count, void *user);
+int l0s_set_part_exchange(l0s_ctx *ctx, l0s_exchange_fn fn, void *user);
+
+/*
  * l0s_stage / l0s_stage_append with the feature rows given as m (m_new) host
  * pointers to s float64 each -- a SelectedSubspace's entry arrays
  * (screening.py:165-198) copied row by row, never stacked on the host

@@ -31,8 +31,12 @@ EXPORTS = (
     "l0s_stage_finish", "l0s_sis_prepare", "l0s_sis_scores", "l0s_set_gram_mode", "l0s_stage_info", "l0s_stage_loose_rows", "l0s_stage_timings", "l0s_qr_tuples", "l0s_residuals",
     "l0s_gen_dedup_reset", "l0s_gen_dedup",
     "l0s_group_create", "l0s_group_destroy", "l0s_group_size", "l0s_group_ctx", "l0s_group_stage", "l0s_group_search",
-    "l0s_stage_append", "l0s_search_part", "l0s_stage_rows", "l0s_stage_append_rows", "l0s_gen_pool", "l0s_gen_eval", "l0s_gen_take", "l0s_gen_fetch",
+    "l0s_stage_append", "l0s_search_part", "l0s_set_part_exchange", "l0s_stage_rows", "l0s_stage_append_rows", "l0s_gen_pool", "l0s_gen_eval", "l0s_gen_take", "l0s_gen_fetch",
 )
+
+
+# l0s_exchange_fn: double (*)(const double* scores, int64_t count, void* user)
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_void_p)
 
 
 class Stats(ctypes.Structure):
@@ -103,6 +107,7 @@ def lib():
         L.l0s_set_gram_mode.argtypes = [vp, i32]
         L.l0s_stage_info.argtypes = [vp, vp, vp]
         L.l0s_stage_loose_rows.argtypes = [vp, vp]
+        L.l0s_set_part_exchange.argtypes = [vp, vp, vp]
         L.l0s_stage_timings.argtypes = [vp, vp]
         L.l0s_qr_tuples.argtypes = [vp, i32, vp, i64, vp, vp]
         L.l0s_residuals.argtypes = [vp, i32, vp, vp, i64, vp]
@@ -400,6 +405,25 @@ class Engine:
                                     ptr(coef), ptr(ssr), ctypes.byref(cnt), ctypes.byref(st)), "l0s_search_part")
         k = cnt.value
         return scores[:k], ranks[:k], coef[:k], ssr[:k], st
+
+    def set_part_exchange(self, fn) -> None:
+        """fn(scores: np.ndarray) -> float: the collective of l0s_set_part_exchange (the keep-th
+        score of the union of every part's best exact scores); None clears it."""
+        if fn is None:
+            check(lib().l0s_set_part_exchange(self.handle, None, None), "l0s_set_part_exchange")
+            self._exchange = None
+            return
+
+        def cb(scores, count, _user):
+            try:
+                arr = np.ctypeslib.as_array(scores, shape=(count,)).copy() if count > 0 else np.zeros(0)
+                return float(fn(arr))
+            except Exception:  # noqa: BLE001 -- never unwind through the C caller
+                return float("inf")
+
+        self._exchange = EXCHANGE_FN(cb)  # kept alive while registered
+        check(lib().l0s_set_part_exchange(self.handle, ctypes.cast(self._exchange, ctypes.c_void_p), None),
+              "l0s_set_part_exchange")
 
     def fit_tuples(self, tuples: np.ndarray):
         tuples = np.ascontiguousarray(tuples, dtype=np.int64)

@@ -159,6 +159,9 @@ struct l0s_ctx {
     std::vector<int4> units_h;
     int64_t units_key[7] = {-1, -1, -1, -1, -1, -1, -1};
     int part = 0, nparts = 1;  // l0s_search_part: this context screens units u with u % nparts == part
+    l0s_exchange_fn exch = nullptr;  // l0s_set_part_exchange
+    void* exch_user = nullptr;
+    bool exch_pending = false;  // this l0s_search_part call has not exchanged yet
     HostStager* stager = nullptr;  // pinned ring for pageable host inputs (hostcopy.cu), on first use
     const double* src_values = nullptr;  // the staged inputs, caller's sample order (device)
     const double* src_y = nullptr;
@@ -1436,7 +1439,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     // A search part (l0s_search_part) answers for its own units only, but the seed's subsets come
     // from the whole problem: >= keep tuples score at most seed_cap / s, so the global keep-th
     // score is below that cap and a part's excluded tuples need only clear the cap.
-    const double cap = c->nparts > 1 ? seed_cap / (double)c->s : INFINITY;
+    double cap = c->nparts > 1 ? seed_cap / (double)c->s : INFINITY;
     double yy = 0.0;
     for (double v : c->yyu_h) yy += v;
     auto margin_of = [&](double sk) { return 1e-10 * std::fabs(sk) + 64.0 * kEps * yy / (double)c->s; };
@@ -1488,6 +1491,16 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     st->ms_exact += elapsed(c->ev[2], c->ev[3]);
     st->n_candidates = nref;
     st->n_ill = (int64_t)nill;
+    // search parts: one exchange of the parts' best exact scores (l0s_set_part_exchange) -- the
+    // keep-th of their union bounds the whole search's keep-th score, usually far below this
+    // part's own when the part holds only some of the near-ties
+    if (c->exch_pending) {
+        c->exch_pending = false;
+        std::vector<double> mine;
+        for (size_t x = 0; x < best.size() && (int64_t)x < keep; ++x) mine.push_back(best[x].score);
+        const double g = c->exch(mine.data(), (int64_t)mine.size(), c->exch_user);
+        if (g < cap) cap = g;  // NaN leaves the cap
+    }
 
     // certification: an excluded tuple has exact score >= lb / s >= G_lb / s; it cannot
     // displace the keep-th exact score if G_lb / s exceeds it by the reference's own error margin
@@ -1759,10 +1772,23 @@ int l0s_search_part(l0s_ctx* c, int n, int64_t keep, int part, int nparts, int m
                           out_ranks, out_coef, out_ssr, out_count, stats);
     c->part = part;
     c->nparts = nparts;
+    c->exch_pending = c->exch != nullptr;
     rc = l0s_search(c, n, keep, 0, N, L0S_MODE_FAST, out_scores, out_ranks, out_coef, out_ssr, out_count, stats);
+    if (rc == L0S_OK && c->exch_pending) {  // the exchange is a collective: take part even if unused
+        std::vector<double> mine(out_scores, out_scores + (out_count ? *out_count : 0));
+        c->exch(mine.data(), (int64_t)mine.size(), c->exch_user);
+    }
+    c->exch_pending = false;
     c->part = 0;
     c->nparts = 1;
     return rc;
+}
+
+int l0s_set_part_exchange(l0s_ctx* c, l0s_exchange_fn fn, void* user) {
+    if (!c) return fail(L0S_EINVAL, "null context");
+    c->exch = fn;
+    c->exch_user = user;
+    return L0S_OK;
 }
 
 }  // extern "C"

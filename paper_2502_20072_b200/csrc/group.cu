@@ -18,7 +18,10 @@
 // Devices may repeat (several contexts on one device): the same code path, used by the tests
 // on a one-GPU box.
 #include <algorithm>
+#include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -62,6 +65,41 @@ int run_all(l0s_group* g, F f) {
         if (rc[i]) return set_error(rc[i], ("device member " + std::to_string(i) + ": " + msg[i]).c_str());
     return L0S_OK;
 }
+
+// The parts' exchange (l0s_set_part_exchange) inside one process: every member thread brings
+// its best exact scores; the last to arrive merges them and wakes the others with the keep-th
+// of the union.  A member that fails before arriving aborts the round (the others get +inf
+// and certify against their own lists).
+struct PartExchange {
+    std::mutex mu;
+    std::condition_variable cv;
+    int G = 0, arrived = 0;
+    int64_t keep = 0;
+    bool aborted = false;
+    std::vector<double> all;
+    double result = INFINITY;
+    bool done = false;
+
+    static double call(const double* scores, int64_t count, void* user) {
+        auto* x = static_cast<PartExchange*>(user);
+        std::unique_lock<std::mutex> lk(x->mu);
+        x->all.insert(x->all.end(), scores, scores + count);
+        if (++x->arrived == x->G) {
+            std::sort(x->all.begin(), x->all.end());
+            x->result = (int64_t)x->all.size() >= x->keep ? x->all[(size_t)x->keep - 1] : INFINITY;
+            x->done = true;
+            x->cv.notify_all();
+        } else {
+            x->cv.wait(lk, [x] { return x->done || x->aborted; });
+        }
+        return x->done ? x->result : INFINITY;
+    }
+    void abort() {
+        std::lock_guard<std::mutex> lk(mu);
+        aborted = true;
+        cv.notify_all();
+    }
+};
 
 int cuda_fail(cudaError_t e, const char* what) {
     return set_error(L0S_ECUDA, (std::string(what) + ": " + cudaGetErrorString(e)).c_str());
@@ -239,10 +277,18 @@ int l0s_group_search(l0s_group* g, int n, int64_t keep, int mode, double* out_sc
         cf[i].resize((size_t)keep * T * p);
         ss[i].resize((size_t)keep * T);
     }
+    // the parts certify against the keep-th of their union (one exchange per search)
+    PartExchange ex;
+    ex.G = G;
+    ex.keep = keep;
+    for (int i = 0; i < G && G > 1; ++i) l0s_set_part_exchange(g->ctx[i], &PartExchange::call, &ex);
     int rc = run_all(g, [&](int i) -> int {
-        return l0s_search_part(g->ctx[i], n, keep, i, G, mode, sc[i].data(), rk[i].data(), cf[i].data(), ss[i].data(),
-                               &cnt[i], &st[i]);
+        const int r = l0s_search_part(g->ctx[i], n, keep, i, G, mode, sc[i].data(), rk[i].data(), cf[i].data(),
+                                      ss[i].data(), &cnt[i], &st[i]);
+        if (r) ex.abort();
+        return r;
     });
+    for (int i = 0; i < G && G > 1; ++i) l0s_set_part_exchange(g->ctx[i], nullptr, nullptr);
     if (rc) return rc;
     std::vector<Entry> all;
     for (int i = 0; i < G; ++i)

@@ -88,6 +88,25 @@ def sharded_stage(eng, shape, bounds, precision, device_ptrs, group=None, all_ga
     eng.stage_finish(recv.data_ptr())
 
 
+def exchange_keepth(scores, keep: int, group=None) -> float:
+    """The parts' exchange (l0s_set_part_exchange): all-gather every rank's best exact scores
+    (at most keep, ascending) and return the keep-th of their union (+inf when fewer)."""
+    import torch
+    import torch.distributed as dist
+
+    buf = torch.full((keep,), float("inf"), dtype=torch.float64)
+    k = min(len(scores), keep)
+    if k:
+        buf[:k] = torch.from_numpy(np.asarray(scores[:k], dtype=np.float64))
+    if dist.get_backend(group) == "nccl":
+        buf = buf.cuda()
+    out = [torch.empty_like(buf) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(out, buf, group=group)
+    allv = torch.cat(out).cpu().numpy()
+    allv.sort()
+    return float(allv[keep - 1]) if len(allv) >= keep else float("inf")
+
+
 def sharded_l0_search(values, property_values, task_slices=None, config=None, task_labels=None,
                       group=None, local_search=None, device=None):
     """Collective l0_search: every rank must call it with the same inputs; every rank
@@ -129,8 +148,15 @@ def sharded_l0_search(values, property_values, task_slices=None, config=None, ta
         torch.cuda.synchronize(dev)
         sharded_stage(eng, (m, s), bounds, config.precision, (vd.data_ptr(), yd.data_ptr(), pd.data_ptr()), group)
         # this rank's part of the search: every world-th unit of the screened path (ill-
-        # conditioned tuples cluster in rank ranges, C4), else the contiguous rank range
-        sc, rk, coef, ssr, _ = eng.search_part(n, keep, me, world, "auto")
+        # conditioned tuples cluster in rank ranges, C4), else the contiguous rank range; the
+        # parts certify against the keep-th of the union of their best scores (one all-gather)
+        if world > 1:
+            eng.set_part_exchange(lambda scores: exchange_keepth(scores, keep, group))
+        try:
+            sc, rk, coef, ssr, _ = eng.search_part(n, keep, me, world, "auto")
+        finally:
+            if world > 1:
+                eng.set_part_exchange(None)
         labels = _labels_for(slices, task_labels)
         # merge key: the device score (score_tuples' sequential task sum, search.py:303), not
         # Model.score (numpy's ssr.sum(), which may differ in the last bit for 8 tasks)
@@ -145,4 +171,4 @@ def sharded_l0_search(values, property_values, task_slices=None, config=None, ta
     return [c[2] for c in merge_candidates(parts, keep)]
 
 
-__all__ = ["rank_range", "merge_candidates", "sharded_stage", "sharded_l0_search", "comb"]
+__all__ = ["rank_range", "merge_candidates", "sharded_stage", "sharded_l0_search", "exchange_keepth", "comb"]

@@ -100,3 +100,32 @@ def test_two_ranks_gloo_equals_single_process():
     want = orc.l0_search(v, y, [np.arange(0, 40, 2), np.arange(1, 40, 2)], 3, 7, "fp64")
     assert [g[0] for g in got] == [w["indices"] for w in want]
     assert [np.float64(g[1]).view(np.int64) for g in got] == [np.float64(w["score"]).view(np.int64) for w in want]
+
+
+def _exchange_worker(rank, world, port, out_q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2502_20072_b200.dist import exchange_keepth
+
+    mine = [np.array([0.5, 1.0, 3.0]), np.array([0.7, 0.9])][rank]
+    out_q.put((rank, exchange_keepth(mine, 3), exchange_keepth(mine, 6)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_part_exchange_keepth_gloo():
+    """The search parts' exchange (l0s_set_part_exchange's collective over torch.distributed):
+    every rank receives the keep-th score of the union of the ranks' lists, +inf when fewer."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert got == [(0, 0.9, float("inf")), (1, 0.9, float("inf"))]

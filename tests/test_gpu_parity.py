@@ -750,6 +750,27 @@ def test_search_parts_merge_to_the_whole_search(case, nparts):
     assert [c[1] for c in merged] == rk.tolist()
     assert bits_equal([c[0] for c in merged], sc)
     assert all(bits_equal(c[2], w) for c, w in zip(merged, coef))
+    # with the parts' exchange (l0s_set_part_exchange), emulated in two passes: first every part
+    # records the scores it brings to the exchange, then each part runs again receiving the
+    # keep-th of their union -- what the collective returns when the parts run concurrently
+    brought = []
+    eng.set_part_exchange(lambda x: (brought.append(np.array(x)), float("inf"))[1])
+    for p in range(nparts):
+        eng.search_part(n, 10, p, nparts, "fast")
+    assert len(brought) == nparts
+    union = np.sort(np.concatenate(brought))
+    g = float(union[9]) if len(union) >= 10 else float("inf")
+    eng.set_part_exchange(lambda x: g)
+    parts = []
+    for p in range(nparts):
+        psc, prk, pcoef, _, pst = eng.search_part(n, 10, p, nparts, "fast")
+        assert pst.as_dict()["certified"] == 1
+        parts.append([(float(a), int(b), c) for a, b, c in zip(psc, prk, pcoef)])
+    eng.set_part_exchange(None)
+    merged = merge_candidates(parts, 10)
+    assert [c[1] for c in merged] == rk.tolist()
+    assert bits_equal([c[0] for c in merged], sc)
+    assert all(bits_equal(c[2], w) for c, w in zip(merged, coef))
 
 
 def _sharded_worker(rank, world, port, case, out_q):

@@ -32,7 +32,25 @@ def main():
     total = comb(v.shape[0], n)
     eng.search(n, 10, 0, 2**63 - 1, "fast")  # warm-up
     out = {"config": which, "parts": N}
-    for label, run in (("units", lambda p: eng.search_part(n, 10, p, N, "fast")),
+    # the parts' exchange (l0s_set_part_exchange) emulated in two passes: the scores every part
+    # brings, then each part again receiving the keep-th of their union (what the collective
+    # returns when the parts run concurrently on N GPUs)
+    brought = []
+    eng.set_part_exchange(lambda x: (brought.append(np.array(x)), float("inf"))[1])
+    for p in range(N):
+        eng.search_part(n, 10, p, N, "fast")
+    union = np.sort(np.concatenate(brought)) if brought else np.zeros(0)
+    g = float(union[9]) if len(union) >= 10 else float("inf")
+    eng.set_part_exchange(None)
+
+    def with_exchange(p):
+        eng.set_part_exchange(lambda x: g)
+        try:
+            return eng.search_part(n, 10, p, N, "fast")
+        finally:
+            eng.set_part_exchange(None)
+
+    for label, run in (("units_exchange", with_exchange), ("units", lambda p: eng.search_part(n, 10, p, N, "fast")),
                        ("ranges", lambda p: eng.search(n, 10, total * p // N, total * (p + 1) // N, "fast"))):
         ms, ill, fit, ex, cand, resc = [], [], [], [], [], []
         for p in range(N):
