@@ -217,7 +217,6 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
     __shared__ int s_tord[NT];
     __shared__ unsigned char s_force[NB][IB];  // iforce flags of the staged rows
     __shared__ int s_fany[NB];                 // any of them set
-    static_assert(IB <= 32, "one warp loads a tile's row flags");
     __shared__ __align__(8) unsigned long long s_bar[NB];  // TMA completion, one per tile buffer
     __shared__ __align__(8) unsigned long long s_hbar;     // TMA completion of the unit's hoist block
     __shared__ unsigned s_rel[NB];                           // WREL: warps done with the buffer's tile
@@ -301,10 +300,15 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
     // completion on s_bar[buf]): C[i, j-block] (IB x 32), C[i, k-span] (IB x KSPAN), (c_i, pad) (IB x 2)
     // Issued by one whole warp (`by`): its lanes write the rows' iforce flags, its lane 0 the TMA.
     auto load_tiles = [&](int buf, int ib0, int j0, int k0, int by = 0) {
-        if (warp == by) {  // IB <= 32: the rows' iforce flags and whether any is set
-            const unsigned char fl = (lane < IB && ib0 + lane < m) ? a.iforce[ib0 + lane] : 0;
-            if (lane < IB) s_force[buf][lane] = fl;
-            const unsigned any = __ballot_sync(L0S_FULL, fl != 0);
+        if (warp == by) {  // the rows' iforce flags and whether any is set
+            unsigned any = 0u;
+#pragma unroll
+            for (int r0 = 0; r0 < IB; r0 += 32) {
+                const int r = r0 + lane;
+                const unsigned char fl = (r < IB && ib0 + r < m) ? a.iforce[ib0 + r] : 0;
+                if (r < IB) s_force[buf][r] = fl;
+                any |= __ballot_sync(L0S_FULL, fl != 0);
+            }
             if (lane == 0) s_fany[buf] = any != 0u;
             __syncwarp();  // the flags precede lane 0's arrive (release) on the tile's barrier
         }

@@ -46,6 +46,22 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// The OZ_DIGITS signed 7-bit Ozaki digits of u = z 2^-e (|u| < 1), byte a = digit a: exactly
+// what the iteration v = 128 u, q_a = trunc(v), u = v - q_a (every step exact) yields, i.e.
+// q_a = sign(u) (floor(|u| 2^(7(a+1))) mod 128), from one truncation of t = z p2 with
+// p2 = 2^(7 OZ_DIGITS - e) (an exact scaling; |t| < 2^28) and integer field extraction.
+__device__ __forceinline__ unsigned oz_digits(double z, double p2) {
+    const int q = __double2int_rz(z * p2);
+    const unsigned au = (unsigned)(q < 0 ? -q : q), neg = q < 0 ? 0xffu : 0u;
+    unsigned w = 0u;
+#pragma unroll
+    for (int a = 0; a < OZ_DIGITS; ++a) {
+        const unsigned d = (au >> (7 * (OZ_DIGITS - 1 - a))) & 127u;
+        w |= (((d ^ neg) + (neg & 1u)) & 0xffu) << (8 * a);  // two's complement byte of -d when negative
+    }
+    return w;
+}
+
 // One warp per (row, task) of rows [f0, f1); row m is the property.
 // With dig.Q set, the warp also writes the row's Ozaki digits for the INT8 Gram (ozaki.cu):
 // e with max |z| < 2^e, and OZ_DIGITS signed 7-bit digits of z 2^-e into each digit plane.
@@ -106,17 +122,14 @@ __global__ void k_normalize(const W* __restrict__ Xp, const W* __restrict__ yp, 
         const bool finite = zmax > 0.0 && zmax < INFINITY;
         if (finite) frexp(zmax, &e);
         const int64_t k0 = dig.koff[t], klen = dig.koff[t + 1] - k0;
+        const double p2 = finite ? ldexp(1.0, 7 * OZ_DIGITS - e) : 0.0;
         for (int64_t i = lane; i < klen; i += 32) {
             const double z = (i < r) ? ((double)src[i] - mean) * scale : 0.0;
             if (dig.write_z && i < rpad) dst[i] = z;  // Z only for a DMMA fallback (INT8 Gram: digits)
-            double u = finite ? ldexp(z, -e) : 0.0;
+            const unsigned w = oz_digits(z, p2);
 #pragma unroll
-            for (int a = 0; a < OZ_DIGITS; ++a) {
-                const double v = u * 128.0;  // exact
-                const double q = trunc(v);   // |q| <= 127
-                u = v - q;                   // exact remainder
-                dig.Q[((int64_t)a * dig.R + f) * dig.KP + k0 + i] = (int8_t)(int)q;
-            }
+            for (int a = 0; a < OZ_DIGITS; ++a)
+                dig.Q[((int64_t)a * dig.R + f) * dig.KP + k0 + i] = (int8_t)((w >> (8 * a)) & 0xffu);
         }
         if (lane == 0) {
             dig.ex[(int64_t)t * dig.R + f] = e;
@@ -141,7 +154,10 @@ __global__ void k_normalize(const W* __restrict__ Xp, const W* __restrict__ yp, 
 // values, one write of Xp), the statistics of k_normalize from shared memory, then the Ozaki
 // digits (four 7-bit planes, 4 consecutive samples per thread: 32-bit stores) and/or Z.
 // Same statistics and the same rounding of every written value as k_gather + k_normalize.
-constexpr int SR_THREADS = 256;
+#ifndef L0S_SR_THREADS
+#define L0S_SR_THREADS 256
+#endif
+constexpr int SR_THREADS = L0S_SR_THREADS;
 template <typename W>
 __global__ void __launch_bounds__(SR_THREADS) k_stage_rows(const double* __restrict__ values, const double* __restrict__ y,
                                                           const int64_t* __restrict__ perm, int64_t m, int64_t s,
@@ -245,20 +261,16 @@ __global__ void __launch_bounds__(SR_THREADS) k_stage_rows(const double* __restr
         const bool finite = zmax > 0.0 && zmax < INFINITY;
         if (finite) frexp(zmax, &e);
         const int64_t k0 = dig.koff[t], klen = dig.koff[t + 1] - k0;  // multiples of 64
+        const double p2 = finite ? ldexp(1.0, 7 * OZ_DIGITS - e) : 0.0;
         for (int64_t i0 = 4 * (int64_t)tid; i0 < klen; i0 += 4 * SR_THREADS) {
             unsigned pk[OZ_DIGITS] = {};
 #pragma unroll
             for (int e4 = 0; e4 < 4; ++e4) {
                 const int64_t i = i0 + e4;
                 const double z = (i < r) ? (seg[i] - mean) * scale : 0.0;
-                double u = finite ? ldexp(z, -e) : 0.0;
+                const unsigned w = oz_digits(z, p2);
 #pragma unroll
-                for (int a = 0; a < OZ_DIGITS; ++a) {
-                    const double v = u * 128.0;  // exact
-                    const double q = trunc(v);   // |q| <= 127
-                    u = v - q;                   // exact remainder
-                    pk[a] |= ((unsigned)(int)q & 0xffu) << (8 * e4);
-                }
+                for (int a = 0; a < OZ_DIGITS; ++a) pk[a] |= ((w >> (8 * a)) & 0xffu) << (8 * e4);
             }
 #pragma unroll
             for (int a = 0; a < OZ_DIGITS; ++a)

@@ -22,11 +22,9 @@ VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
     "base": (),
-    "p2m3ib16": ("L0S_C34_P=2", "L0S_C34_MINB=3", "L0S_C34_IB=16"),
-    "p2m3ib24": ("L0S_C34_P=2", "L0S_C34_MINB=3", "L0S_C34_IB=24"),
-    "p2m4ib16": ("L0S_C34_P=2", "L0S_C34_MINB=4", "L0S_C34_IB=16"),
-    "p2m2ib24": ("L0S_C34_P=2", "L0S_C34_MINB=2", "L0S_C34_IB=24"),
-    "p4m3ib16": ("L0S_C34_MINB=3", "L0S_C34_IB=16"),
+    "slot0_ib48": ("L0S_FIT_SLOT0=1", "L0S_C34_IB=48"),
+    "slot0_ib64": ("L0S_FIT_SLOT0=1", "L0S_C34_IB=64"),
+    "slot0_ib96": ("L0S_FIT_SLOT0=1", "L0S_C34_IB=96"),
 }
 if os.environ.get("L0S_TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["L0S_TUNE_ONLY"].split(",")}
