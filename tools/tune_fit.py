@@ -22,9 +22,8 @@ VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
     "base": (),
-    "slot0_ib48": ("L0S_FIT_SLOT0=1", "L0S_C34_IB=48"),
-    "slot0_ib64": ("L0S_FIT_SLOT0=1", "L0S_C34_IB=64"),
-    "slot0_ib96": ("L0S_FIT_SLOT0=1", "L0S_C34_IB=96"),
+    "ib16": ("L0S_C34_IB=16",),
+    "cap128": ("L0S_CAP=128",),
 }
 if os.environ.get("L0S_TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["L0S_TUNE_ONLY"].split(",")}
