@@ -27,6 +27,7 @@ never leave the device and the nodes are never built unless the screen selects t
 from __future__ import annotations
 
 import time
+import weakref
 
 import numpy as np
 
@@ -139,11 +140,31 @@ class PendingExprs:
         return ~np.isin(mine, np.asarray(codes, dtype=np.int64)) if codes else np.ones(len(self), dtype=bool)
 
 
+_PAIRS = weakref.WeakKeyDictionary()  # pool -> {(len, operator, rung): (pi, pj)}
+
+
 def pair_arrays(op, pool, target_rung: int):
     """generation.generate_pairs (generation.py:205-242) as index arrays (pj = -1: unary):
     the same pairs in the same order (first child ascending, second ascending within it),
     built with numpy masks over the eligible features instead of a Python double loop; the
-    unit rule (expressions.check_unit) is evaluated once per distinct unit pair."""
+    unit rule (expressions.check_unit) is evaluated once per distinct unit pair.  The pool only
+    grows by appending, so the arrays are kept per (pool, its length, operator, rung): the
+    pipeline streams the same last rung once per dimension (pipeline.py:181-240)."""
+    key = (len(pool), op.kind, op.arity, bool(getattr(op, "commutative", False)), int(target_rung))
+    try:
+        cache = _PAIRS.setdefault(pool, {})
+    except TypeError:  # a pool that cannot be weakly referenced: no cache
+        cache = {}
+    hit = cache.get(key)
+    if hit is None:
+        hit = _pair_arrays(op, pool, target_rung)
+        for x in hit:
+            x.setflags(write=False)  # shared between calls
+        cache[key] = hit
+    return hit
+
+
+def _pair_arrays(op, pool, target_rung: int):
     from descsearch.expressions import check_unit
 
     prev = target_rung - 1
@@ -262,7 +283,7 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
                     # keys cannot collide (distinct operator kinds): only the value test remains, and
                     # the device's ordered-first-owner set decides it (dedup.cu)
                     with _lock:
-                        kept = np.flatnonzero(eng.gen_dedup()).tolist()
+                        kept = np.flatnonzero(eng.gen_dedup())  # an index array: never a Python list
                     stats.n_dup_value += len(rows_ok) - len(kept)
                     rows_ok = rows_ok[:0]
                 else:
@@ -291,8 +312,9 @@ def iter_final_rung(pool, config, workers: int = 1, timer=None, stats=None, *, d
                     else:
                         same.append(fp)
                     kept.append(row)
+                kept = np.asarray(kept, dtype=np.int64)
                 stats.n_kept += len(kept)
-                if not kept:
+                if len(kept) == 0:
                     continue
                 if on_device:
                     exprs = PendingExprs(op, pi[kept], pj[kept], feats, index_of)
