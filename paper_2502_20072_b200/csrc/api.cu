@@ -444,7 +444,9 @@ static int gram_full(l0s_ctx* c);
 static bool ozaki_planned(const l0s_ctx* c);
 
 static OzFix oz_fix_of(l0s_ctx* c) {
-    return OzFix{c->oz_fix.as<int>(), c->oz_fix.as<int>() + l0s_ctx::kFixCap, l0s_ctx::kFixCap};
+    int* base = c->oz_fix.as<int>();
+    return OzFix{base, base + l0s_ctx::kFixCap, l0s_ctx::kFixCap,
+                 reinterpret_cast<unsigned char*>(base + l0s_ctx::kFixCap + 1)};
 }
 
 // the INT8 Gram's error bound with the loose rows left out when their (mean, scale) were stored
@@ -452,7 +454,7 @@ static OzFix oz_fix_of(l0s_ctx* c) {
 static int ozaki_fix_prepare(l0s_ctx* c, OzFix* fx) {
     c->fix_on = c->digits_ready && c->oz_musc.p != nullptr;
     if (c->fix_on) {
-        CK(c->oz_fix.ensure(sizeof(int) * (l0s_ctx::kFixCap + 1)));
+        CK(c->oz_fix.ensure(sizeof(int) * (l0s_ctx::kFixCap + 1) + (size_t)(c->m + 1)));
         *fx = oz_fix_of(c);
     }
     return L0S_OK;

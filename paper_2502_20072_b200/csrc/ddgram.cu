@@ -230,7 +230,8 @@ void launch_dd_screen(const QrArgs& a0, int64_t count, double* Hhi, double* Hlo,
             case 2: k_dd_ill<4><<<blocks, 128, 0, st>>>(a, Hhi, Hlo, LD); break;
             case 3: k_dd_ill<5><<<blocks, 128, 0, st>>>(a, Hhi, Hlo, LD); break;
             case 4: k_dd_ill<6><<<blocks, 128, 0, st>>>(a, Hhi, Hlo, LD); break;
-            default: k_dd_ill<7><<<blocks, 128, 0, st>>>(a, Hhi, Hlo, LD); break;
+            case 5: k_dd_ill<7><<<blocks, 128, 0, st>>>(a, Hhi, Hlo, LD); break;
+            default: k_dd_ill<8><<<blocks, 128, 0, st>>>(a, Hhi, Hlo, LD); break;  // n = 6 (l0s_qr_tuples' limit)
         }
         if (launches) ++*launches;
     }

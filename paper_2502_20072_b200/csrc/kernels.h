@@ -76,6 +76,7 @@ struct OzFix {
     int* rows;      // (cap,) loose rows (device)
     int* count;     // loose rows found (device, may exceed cap)
     int cap;
+    unsigned char* flags;  // (m + 1,) device scratch: the rows' loose flags
 };
 int64_t ozaki_q_bytes(int64_t mp, int T, const int64_t* rpad_h, int64_t* KP_out);
 // digits_ready: the normalize kernel already wrote Q / ex (and koff_d); otherwise split Z here

@@ -270,10 +270,10 @@ __global__ void __launch_bounds__(192, OZ_CTAS) k_oz_gemm(const __grid_constant_
 __global__ void __launch_bounds__(1024) k_oz_eta(const int* __restrict__ ex, int64_t R, int T, int64_t m, int64_t mp,
                                                  const double* __restrict__ Gall, const double* __restrict__ rows,
                                                  double lim, double* __restrict__ eta, int* __restrict__ fix_rows,
-                                                 int* __restrict__ fix_count, int fix_cap) {
+                                                 int* __restrict__ fix_count, int fix_cap,
+                                                 unsigned char* __restrict__ s_loose) {  // (m + 1,) when fixing up
     __shared__ double red[32];
     __shared__ int s_cnt;
-    extern __shared__ unsigned char s_loose[];  // (m + 1,) when fixing up
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     auto term = [&](int t, int64_t f) {
         double v = ldexp(1.0, 2 * ex[(int64_t)t * R + f]);
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(1024) k_oz_eta(const int* __restrict__ ex, int
         for (int64_t f = tid; f <= m; f += blockDim.x) {
             bool loose = false;
             for (int t = 0; t < T && !loose; ++t) loose = !(term(t, f) <= lim);
-            s_loose[f] = loose;
+            s_loose[f] = loose;  // global: read back below by this CTA only (after the barrier)
             if (loose) {
                 const int k = atomicAdd(&s_cnt, 1);
                 if (k < fix_cap) fix_rows[k] = (int)f;
@@ -466,10 +466,8 @@ int launch_ozaki_tiles(int T, int64_t mp, const int64_t* rpad_h, const int8_t* Q
 void launch_ozaki_eta(int T, int64_t m, int64_t mp, const int* ex, const double* rows_d, const double* G, double* eta_d,
                       cudaStream_t st, const OzFix* fix) {
     const int64_t R = (mp + OZ_BM - 1) / OZ_BM * OZ_BM;
-    const size_t smem = fix ? (size_t)(m + 1) : 0;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_oz_eta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_oz_eta<<<1, 1024, smem, st>>>(ex, R, T, m, mp, G, rows_d, OZ_ETA_MAX, eta_d, fix ? fix->rows : nullptr,
-                                    fix ? fix->count : nullptr, fix ? fix->cap : 0);
+    k_oz_eta<<<1, 1024, 0, st>>>(ex, R, T, m, mp, G, rows_d, OZ_ETA_MAX, eta_d, fix ? fix->rows : nullptr,
+                                 fix ? fix->count : nullptr, fix ? fix->cap : 0, fix ? fix->flags : nullptr);
 }
 
 void launch_ozaki_fixup(const void* Xp, const void* yp, int precision, int64_t m, int64_t s, const int64_t* bounds_d,
