@@ -24,11 +24,15 @@ for y in planted random; do
 done
 python tools/ncu_summary.py gpurun_out/${tag}_fit3_planted.ncu-rep x --json "$commit" > gpurun_out/${tag}_fit3_profile.json
 cp gpurun_out/${tag}_fit3_profile.json profiles/fit3_profile.json
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_stage_rows|k_oz_gemm" -s 2 -c 2 -f \
-    -o gpurun_out/${tag}_stage python tools/time_stage.py > gpurun_out/${tag}_stage.log 2>&1
-echo "stage full rc=$?"
-python tools/ncu_summary.py gpurun_out/${tag}_stage.ncu-rep "${tag} (${commit}): k_stage_rows and the INT8 Gram on C3" > gpurun_out/${tag}_stage_ncu.txt
-grep -E "kernel|duration|DRAM throughput|DRAM read|DRAM write|tensor|issue" gpurun_out/${tag}_stage_ncu.txt
+for k in k_stage_rows k_oz_gemm k_exact_smem; do
+  # the third k_stage_rows launch is a feature-row pass (the first of each stage is the property row)
+  skip=2; [ $k = k_stage_rows ] && skip=3
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c 1 -f \
+      -o gpurun_out/${tag}_$k python tools/time_stage.py > gpurun_out/${tag}_$k.log 2>&1
+  echo "$k full rc=$?"
+  python tools/ncu_summary.py gpurun_out/${tag}_$k.ncu-rep "${tag} (${commit}): $k on C3" > gpurun_out/${tag}_${k}_ncu.txt
+  grep -E "kernel|duration|DRAM throughput|tensor \(tc\)|issue active|FP64 pipe" gpurun_out/${tag}_${k}_ncu.txt
+done
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline \
     > gpurun_out/${tag}_launch_run.log 2>&1
