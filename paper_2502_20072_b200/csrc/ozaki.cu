@@ -327,81 +327,82 @@ __global__ void __launch_bounds__(FTH) k_oz_fixup(const W* __restrict__ Xp, cons
                                                   int64_t R, int64_t mp, const int* __restrict__ fix_rows,
                                                   const int* __restrict__ fix_count, int fix_cap, double* __restrict__ G) {
     const int nl = *fix_count;
-    if (nl > fix_cap) return;  // too many: the host recomputes the whole Gram on DMMA
-    const int l0 = blockIdx.y * FX;
-    if (l0 >= nl) return;
+    if (nl == 0 || nl > fix_cap) return;  // none, or too many: the host then recomputes the Gram on DMMA
     __shared__ double zf[FX][FCH];
     __shared__ double fms[FX][2];
     __shared__ int frow[FX];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int t = blockIdx.z;
+    const int t = blockIdx.y;
     const int64_t lo = bounds[t], r = bounds[t + 1] - lo;
     const double* ms = musc + 2 * (int64_t)t * R;
-    if (tid < FX) {
-        const int f = l0 + tid < nl ? fix_rows[l0 + tid] : -1;
-        frow[tid] = f;
-        fms[tid][0] = f >= 0 ? ms[2 * f] : 0.0;
-        fms[tid][1] = f >= 0 ? ms[2 * f + 1] : 0.0;
-    }
-    const int64_t g0 = ((int64_t)blockIdx.x * (FTH / 32) + warp) * FG;
-    double gmu[FG], gsc[FG];
-    const W* grow[FG];
-#pragma unroll
-    for (int q = 0; q < FG; ++q) {
-        const int64_t g = g0 + q <= m ? g0 + q : m;
-        gmu[q] = ms[2 * g];
-        gsc[q] = ms[2 * g + 1];
-        grow[q] = (g < m ? Xp + g * s : yp) + lo;
-    }
-    double acc[FG][FX];
-#pragma unroll
-    for (int q = 0; q < FG; ++q)
-#pragma unroll
-        for (int l = 0; l < FX; ++l) acc[q][l] = 0.0;
-    for (int64_t c0 = 0; c0 < r; c0 += FCH) {
-        __syncthreads();  // frow / fms (first chunk), the previous chunk's reads (later ones)
-        for (int x = tid; x < FX * FCH; x += FTH) {
-            const int l = x / FCH, i = x % FCH;
-            const int f = frow[l];
-            double z = 0.0;
-            if (f >= 0 && c0 + i < r) {
-                const W* src = (f < m ? Xp + (int64_t)f * s : yp) + lo;
-                z = ((double)src[c0 + i] - fms[l][0]) * fms[l][1];
-            }
-            zf[l][i] = z;
+    for (int l0 = 0; l0 < nl; l0 += FX) {  // batches of FX loose rows
+        __syncthreads();  // the previous batch's frow / fms / zf reads are done
+        if (tid < FX) {
+            const int f = l0 + tid < nl ? fix_rows[l0 + tid] : -1;
+            frow[tid] = f;
+            fms[tid][0] = f >= 0 ? ms[2 * f] : 0.0;
+            fms[tid][1] = f >= 0 ? ms[2 * f + 1] : 0.0;
         }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < FCH / 32; ++k) {
-            const int i = k * 32 + lane;
-            const bool in = c0 + i < r;
-            double zf_[FX];
-#pragma unroll
-            for (int l = 0; l < FX; ++l) zf_[l] = zf[l][i];
-#pragma unroll
-            for (int q = 0; q < FG; ++q) {
-                const double zg = in ? ((double)grow[q][c0 + i] - gmu[q]) * gsc[q] : 0.0;
-#pragma unroll
-                for (int l = 0; l < FX; ++l) acc[q][l] = fma(zg, zf_[l], acc[q][l]);
-            }
+        const int64_t g0 = ((int64_t)blockIdx.x * (FTH / 32) + warp) * FG;
+        double gmu[FG], gsc[FG];
+        const W* grow[FG];
+    #pragma unroll
+        for (int q = 0; q < FG; ++q) {
+            const int64_t g = g0 + q <= m ? g0 + q : m;
+            gmu[q] = ms[2 * g];
+            gsc[q] = ms[2 * g + 1];
+            grow[q] = (g < m ? Xp + g * s : yp) + lo;
         }
-    }
-    double* Gt = G + (int64_t)t * mp * mp;
-#pragma unroll
-    for (int q = 0; q < FG; ++q) {
-#pragma unroll
-        for (int l = 0; l < FX; ++l) {
-            double v = acc[q][l];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(L0S_FULL, v, o);
-            const int64_t g = g0 + q;
-            const int f = frow[l];
-            if (lane == 0 && f >= 0 && g <= m) {
-                Gt[(int64_t)f * mp + g] = v;
-                Gt[g * mp + f] = v;
+        double acc[FG][FX];
+    #pragma unroll
+        for (int q = 0; q < FG; ++q)
+    #pragma unroll
+            for (int l = 0; l < FX; ++l) acc[q][l] = 0.0;
+        for (int64_t c0 = 0; c0 < r; c0 += FCH) {
+            __syncthreads();  // frow / fms (first chunk), the previous chunk's reads (later ones)
+            for (int x = tid; x < FX * FCH; x += FTH) {
+                const int l = x / FCH, i = x % FCH;
+                const int f = frow[l];
+                double z = 0.0;
+                if (f >= 0 && c0 + i < r) {
+                    const W* src = (f < m ? Xp + (int64_t)f * s : yp) + lo;
+                    z = ((double)src[c0 + i] - fms[l][0]) * fms[l][1];
+                }
+                zf[l][i] = z;
+            }
+            __syncthreads();
+    #pragma unroll
+            for (int k = 0; k < FCH / 32; ++k) {
+                const int i = k * 32 + lane;
+                const bool in = c0 + i < r;
+                double zf_[FX];
+    #pragma unroll
+                for (int l = 0; l < FX; ++l) zf_[l] = zf[l][i];
+    #pragma unroll
+                for (int q = 0; q < FG; ++q) {
+                    const double zg = in ? ((double)grow[q][c0 + i] - gmu[q]) * gsc[q] : 0.0;
+    #pragma unroll
+                    for (int l = 0; l < FX; ++l) acc[q][l] = fma(zg, zf_[l], acc[q][l]);
+                }
             }
         }
-    }
+        double* Gt = G + (int64_t)t * mp * mp;
+    #pragma unroll
+        for (int q = 0; q < FG; ++q) {
+    #pragma unroll
+            for (int l = 0; l < FX; ++l) {
+                double v = acc[q][l];
+    #pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(L0S_FULL, v, o);
+                const int64_t g = g0 + q;
+                const int f = frow[l];
+                if (lane == 0 && f >= 0 && g <= m) {
+                    Gt[(int64_t)f * mp + g] = v;
+                    Gt[g * mp + f] = v;
+                }
+            }
+        }
+    }  // batches
 }
 
 }  // namespace
@@ -473,7 +474,7 @@ void launch_ozaki_eta(int T, int64_t m, int64_t mp, const int* ex, const double*
 void launch_ozaki_fixup(const void* Xp, const void* yp, int precision, int64_t m, int64_t s, const int64_t* bounds_d,
                         int T, const double* musc, int64_t R, int64_t mp, const OzFix& fix, double* G, cudaStream_t st) {
     const int64_t per = (FTH / 32) * FG;
-    const dim3 grid((unsigned)((m + 1 + per - 1) / per), (unsigned)((fix.cap + FX - 1) / FX), (unsigned)T);
+    const dim3 grid((unsigned)((m + 1 + per - 1) / per), (unsigned)T);
     if (precision == 1)
         k_oz_fixup<float><<<grid, FTH, 0, st>>>((const float*)Xp, (const float*)yp, m, s, bounds_d, musc, R, mp, fix.rows,
                                                 fix.count, fix.cap, G);
