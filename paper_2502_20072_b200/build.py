@@ -16,6 +16,7 @@ import os
 import shutil
 import subprocess
 import sys
+import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -63,7 +64,8 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, d
     lib_path = out or LIB
     if not force and os.path.exists(lib_path) and os.path.getmtime(lib_path) >= _deps_mtime():
         return lib_path
-    objdir = OBJ if not defines else OBJ + "_" + str(abs(hash(defines)) % 10**8)
+    # tuning variants compile in a scratch directory outside the tree (removed after linking)
+    objdir = OBJ if not defines else tempfile.mkdtemp(prefix="l0s_variant_obj_")
     os.makedirs(objdir, exist_ok=True)
     srcs = sources()
     jobs = jobs or min(len(srcs), os.cpu_count() or 4)
@@ -80,6 +82,9 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, d
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     os.replace(tmp, LIB_OUT)
+    if defines:
+        shutil.rmtree(objdir, ignore_errors=True)
+        return LIB_OUT
     with open(os.path.join(objdir, "ptxas.log"), "w") as fh:
         for _, log in results:
             fh.write(log)

@@ -22,9 +22,9 @@ VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
     "base": (),
-    "wrel_nb3_ib16": ("L0S_WREL=1", "L0S_C34_NBUF=3", "L0S_C34_IB=16"),
-    "wrel_nb2_ib24": ("L0S_WREL=1",),
-    "wrel_nb3_ib16_cap128": ("L0S_WREL=1", "L0S_C34_NBUF=3", "L0S_C34_IB=16", "L0S_CAP=128"),
+    "r8": ("L0S_PRUNE_ROWS=8",),
+    "r2": ("L0S_PRUNE_ROWS=2",),
+    "unroll2": ("L0S_C34_UNROLL=2",),
 }
 if os.environ.get("L0S_TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["L0S_TUNE_ONLY"].split(",")}
