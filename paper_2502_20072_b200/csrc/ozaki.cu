@@ -213,31 +213,45 @@ __global__ void __launch_bounds__(192, OZ_CTAS) k_oz_gemm(const __grid_constant_
         double* G = Gall + (int64_t)t * mp * mp;
         // staging for coalesced row stores: this warp's 32 rows x 32 cols (stage buffers are idle now)
         double* stg = reinterpret_cast<double*>(sm) + quad * 32 * 33;
+        // the tile's column scales 2^e_c, once per warp in shared memory behind the staging area
+        // (e_f + e_g >= -1022 for unit rows: 2^e_f 2^e_g is exact, and acc * 2^(e_f + e_g) is the
+        // same single rounding ldexp performs)
+        double* csc = reinterpret_cast<double*>(sm) + 4 * 32 * 33 + quad * OZ_BN;
+        for (int c = lane; c < OZ_BN; c += 32) csc[c] = ldexp(1.0, ex[(int64_t)t * R + (int64_t)gb * OZ_BN + c]);
+        const double rsc = ldexp(1.0, er);
+        __syncwarp();
         for (int c0 = 0; c0 < OZ_BN; c0 += 32) {
             double acc[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) acc[j] = 0.0;
 #pragma unroll
-            for (int g = 0; g < OZ_NG; ++g) {
-                uint32_t v[32];
-                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(g * OZ_BN + c0);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                const double w = ldexp(1.0, -7 * (g + 2));
+            for (int g = 0; g < OZ_NG; g += 2) {  // two accumulators per wait
+                uint32_t v[2][32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) acc[j] = fma((double)(int)v[j], w, acc[j]);  // exact products
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)((g + h) * OZ_BN + c0);
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+                        "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                        : "=r"(v[h][0]), "=r"(v[h][1]), "=r"(v[h][2]), "=r"(v[h][3]), "=r"(v[h][4]), "=r"(v[h][5]),
+                          "=r"(v[h][6]), "=r"(v[h][7]), "=r"(v[h][8]), "=r"(v[h][9]), "=r"(v[h][10]), "=r"(v[h][11]),
+                          "=r"(v[h][12]), "=r"(v[h][13]), "=r"(v[h][14]), "=r"(v[h][15]), "=r"(v[h][16]),
+                          "=r"(v[h][17]), "=r"(v[h][18]), "=r"(v[h][19]), "=r"(v[h][20]), "=r"(v[h][21]),
+                          "=r"(v[h][22]), "=r"(v[h][23]), "=r"(v[h][24]), "=r"(v[h][25]), "=r"(v[h][26]),
+                          "=r"(v[h][27]), "=r"(v[h][28]), "=r"(v[h][29]), "=r"(v[h][30]), "=r"(v[h][31])
+                        : "r"(taddr));
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double w = ldexp(1.0, -7 * (g + h + 2));
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) acc[j] = fma((double)(int)v[h][j], w, acc[j]);  // exact products
+                }
             }
             const int64_t col0 = (int64_t)gb * OZ_BN + c0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = ldexp(acc[j], er + ex[(int64_t)t * R + col0 + j]);
+            for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = acc[j] * (rsc * csc[c0 + j]);
             __syncwarp();
             // rows of the warp, lanes over columns: G[row][col] for row <= col, coalesced
             const int64_t col = col0 + lane;
