@@ -22,9 +22,9 @@ VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
     "base": (),
-    "r8": ("L0S_PRUNE_ROWS=8",),
-    "r2": ("L0S_PRUNE_ROWS=2",),
-    "unroll2": ("L0S_C34_UNROLL=2",),
+    "nw8m1": ("L0S_C34_NW=8", "L0S_C34_MINB=1"),
+    "nw8m1ib16": ("L0S_C34_NW=8", "L0S_C34_MINB=1", "L0S_C34_IB=16"),
+    "nw8m1ib32": ("L0S_C34_NW=8", "L0S_C34_MINB=1", "L0S_C34_IB=32"),
 }
 if os.environ.get("L0S_TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["L0S_TUNE_ONLY"].split(",")}
