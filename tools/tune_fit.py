@@ -22,9 +22,9 @@ VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
     "base": (),
-    "nw8m1": ("L0S_C34_NW=8", "L0S_C34_MINB=1"),
-    "nw8m1ib16": ("L0S_C34_NW=8", "L0S_C34_MINB=1", "L0S_C34_IB=16"),
-    "nw8m1ib32": ("L0S_C34_NW=8", "L0S_C34_MINB=1", "L0S_C34_IB=32"),
+    "wrel_nb6_ib8": ("L0S_WREL=1", "L0S_C34_NBUF=6", "L0S_C34_IB=8"),
+    "wrel_nb4_ib8": ("L0S_WREL=1", "L0S_C34_NBUF=4", "L0S_C34_IB=8"),
+    "bar_ib8": ("L0S_C34_IB=8",),
 }
 if os.environ.get("L0S_TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["L0S_TUNE_ONLY"].split(",")}
