@@ -289,35 +289,61 @@ void merge_best(std::vector<Cand>& best, const std::vector<Cand>& more, int64_t 
 // Exact scores for device ranks [0, count) of c->ex_ranks; appends finite (score, rank) to out.
 // Exact scores for `count` device ranks; with `recs`, also keep each tuple's coefficients and
 // per-task ssr (small candidate sets), so the final records need no second launch.
-int exact_ranks_to_host(l0s_ctx* c, int n, const int64_t* ranks_d, int64_t count, std::vector<Cand>& out,
-                        int64_t* launches, std::unordered_map<int64_t, Rec>* recs = nullptr) {
+// The exact refit of `count` ranks on the device, split so a caller can queue more work (and
+// host copies) between the launch and the collection: exact_launch queues the kernels and the
+// result copies into `pend`, exact_collect waits and appends (score, rank) to `out`.
+struct ExactPending {
+    int64_t count = 0;
+    bool keep_rec = false;
+    std::vector<double> sc, cf, ss;
+    std::vector<int64_t> rk;
+};
+
+int exact_launch(l0s_ctx* c, int n, const int64_t* ranks_d, int64_t count, ExactPending& pend, int64_t* launches,
+                 bool want_rec) {
+    pend.count = count;
     if (count <= 0) return L0S_OK;
-    const bool keep_rec = recs != nullptr && count <= 4096;
-    int rc = run_exact(c, n, ranks_d, nullptr, count, keep_rec, launches);
+    pend.keep_rec = want_rec && count <= 4096;
+    int rc = run_exact(c, n, ranks_d, nullptr, count, pend.keep_rec, launches);
     if (rc) return rc;
-    std::vector<double> sc((size_t)count);
-    std::vector<int64_t> rk((size_t)count);
-    std::vector<double> cf, ss;
     const int p = n + 1;
-    CK(cudaMemcpyAsync(sc.data(), c->ex_score.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(rk.data(), ranks_d, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, c->st));
-    if (keep_rec) {
-        cf.resize((size_t)(count * c->T * p));
-        ss.resize((size_t)(count * c->T));
-        CK(cudaMemcpyAsync(cf.data(), c->ex_coef.p, sizeof(double) * cf.size(), cudaMemcpyDeviceToHost, c->st));
-        CK(cudaMemcpyAsync(ss.data(), c->ex_ssr.p, sizeof(double) * ss.size(), cudaMemcpyDeviceToHost, c->st));
-    }
-    CK(cudaStreamSynchronize(c->st));
-    for (int64_t i = 0; i < count; ++i) {
-        out.push_back({sc[(size_t)i], rk[(size_t)i]});
-        if (keep_rec && std::isfinite(sc[(size_t)i])) {
-            Rec& r = (*recs)[rk[(size_t)i]];
-            r.score = sc[(size_t)i];
-            r.coef.assign(cf.begin() + i * c->T * p, cf.begin() + (i + 1) * c->T * p);
-            r.ssr.assign(ss.begin() + i * c->T, ss.begin() + (i + 1) * c->T);
-        }
+    pend.sc.resize((size_t)count);
+    pend.rk.resize((size_t)count);
+    CK(cudaMemcpyAsync(pend.sc.data(), c->ex_score.p, sizeof(double) * count, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(pend.rk.data(), ranks_d, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, c->st));
+    if (pend.keep_rec) {
+        pend.cf.resize((size_t)(count * c->T * p));
+        pend.ss.resize((size_t)(count * c->T));
+        CK(cudaMemcpyAsync(pend.cf.data(), c->ex_coef.p, sizeof(double) * pend.cf.size(), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(pend.ss.data(), c->ex_ssr.p, sizeof(double) * pend.ss.size(), cudaMemcpyDeviceToHost, c->st));
     }
     return L0S_OK;
+}
+
+int exact_collect(l0s_ctx* c, int n, ExactPending& pend, std::vector<Cand>& out,
+                  std::unordered_map<int64_t, Rec>* recs) {
+    if (pend.count <= 0) return L0S_OK;
+    CK(cudaStreamSynchronize(c->st));
+    const int p = n + 1;
+    for (int64_t i = 0; i < pend.count; ++i) {
+        out.push_back({pend.sc[(size_t)i], pend.rk[(size_t)i]});
+        if (pend.keep_rec && recs && std::isfinite(pend.sc[(size_t)i])) {
+            Rec& r = (*recs)[pend.rk[(size_t)i]];
+            r.score = pend.sc[(size_t)i];
+            r.coef.assign(pend.cf.begin() + i * c->T * p, pend.cf.begin() + (i + 1) * c->T * p);
+            r.ssr.assign(pend.ss.begin() + i * c->T, pend.ss.begin() + (i + 1) * c->T);
+        }
+    }
+    pend.count = 0;
+    return L0S_OK;
+}
+
+int exact_ranks_to_host(l0s_ctx* c, int n, const int64_t* ranks_d, int64_t count, std::vector<Cand>& out,
+                        int64_t* launches, std::unordered_map<int64_t, Rec>* recs = nullptr) {
+    ExactPending pend;
+    int rc = exact_launch(c, n, ranks_d, count, pend, launches, recs != nullptr);
+    if (rc) return rc;
+    return exact_collect(c, n, pend, out, recs);
 }
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -1428,6 +1454,16 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
         st->n_launches += ns;
     }
     const int64_t nc = std::min<int64_t>((int64_t)ncand, kc);
+    const int64_t wave = std::max<int64_t>(keep + 8, 256 / std::max(1, c->T));
+    // without a cap (single searches) the first refit wave needs no host decision: it is queued
+    // right behind the sort, and its results come back with the candidates' bounds in one sync
+    cudaEventRecord(c->ev[2], c->st);
+    ExactPending first;
+    const bool early = c->nparts == 1 && nc > 0;
+    if (early) {
+        const int erc = exact_launch(c, n, cr, std::min(nc, wave), first, &st->n_launches, true);
+        if (erc) return erc;
+    }
     // the candidates' sorted bounds (SSR units) on the host: certificate thresholds below
     std::vector<double> lbs((size_t)nc);
     if (nc > 0) {
@@ -1458,15 +1494,17 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     // of k_exact_smem over the device at T tasks) usually certifies alone -- the candidates after
     // it have lb >= lbs[done] -- and the rest are refit only when it does not.  Results are the
     // full refit's: an excluded candidate scores above the keep-th exact score by the margin.
-    cudaEventRecord(c->ev[2], c->st);
     int rc = L0S_OK;
     {
-        const int64_t wave = std::max<int64_t>(keep + 8, 256 / std::max(1, c->T));
         int64_t done = 0;
         while (done < nref) {
             const int64_t nb = done == 0 ? std::min(nref, wave) : nref - done;
             std::vector<Cand> exact;
-            rc = exact_ranks_to_host(c, n, cr + done, nb, exact, &st->n_launches, &c->recs);
+            if (done == 0 && early) {  // nref == nc here: the queued wave is this one
+                rc = exact_collect(c, n, first, exact, &c->recs);
+            } else {
+                rc = exact_ranks_to_host(c, n, cr + done, nb, exact, &st->n_launches, &c->recs);
+            }
             if (rc) return rc;
             merge_best(best, exact, keep);
             done += nb;
