@@ -174,7 +174,7 @@ def stage_roofline(stage_ms):
 
 def profile_figures():
     """FP64-pipe fraction and DRAM bytes of k_fit3<4> from the ncu capture committed for this
-    code (profiles/fit3_profile.json, written by tools/profile.sh together with the commit it
+    code (profiles/fit3_profile.json, written by tools/r2_full.sh together with the commit it
     profiled); (None, None, None) when absent."""
     path = os.path.join(ROOT, "profiles", "fit3_profile.json")
     try:
