@@ -399,9 +399,9 @@ def main():
         device_step()
     barrier()
     ms_steps, fit_ms, gram_ms, eval_counts, launches = [], [], [], [], 0
-    # (gather + normalize) for the property row and for the features, the INT8 Gram (k_oz_gemm,
-    # k_oz_eta), unit diagonal, 5 feature-flag kernels
-    stage_launches = 12
+    # the fused staging pass for the property row and for the features (2 x k_stage_rows), the
+    # INT8 Gram (k_oz_gemm, k_oz_eta, k_oz_fixup), the unit diagonal and 5 feature-flag kernels
+    stage_launches = 11
     with ClockSampler(local) as clk:
         t_wall = time.perf_counter()
         for _ in range(args.steps):
