@@ -1077,3 +1077,57 @@ def test_qr_screen_dd_search_matches_oracle(oracle, monkeypatch, n):
     assert st.device["certified"] == 1 and st.device["n_ill"] > 0
     assert [md.indices for md in got] == [w["indices"] for w in want]
     assert bits_equal([md.score for md in got], [w["score"] for w in want])
+
+
+@pytest.mark.gpu
+def test_incremental_stage_with_loose_rows_equals_full_stage(monkeypatch):
+    """The growing subspace with spiky rows (one dominant sample) and a Gaussian property: the
+    incremental INT8 stage (old block relaid, new column blocks, fp64 fix-up of the loose rows)
+    gives the full stage's Gram bit for bit and the same models."""
+    from paper_2502_20072_b200 import L0Config, _lib, l0_search
+
+    rng = np.random.default_rng(21)
+    m0, m1, T, s = 200, 120, 2, 1200
+    v = rng.uniform(0.5, 2.0, size=(m0 + m1, s))
+    for f in (3, 150, m0 + 7):  # spiky rows in the old and in the appended block
+        v[f, rng.integers(s)] += 40.0
+    y = rng.standard_normal(s) + 1.1 * v[10] - 0.7 * v[m0 + 30]
+    slices = [np.arange(t, s, T) for t in range(T)]
+    entries = [_Entry(f"f{i}", v[i].copy()) for i in range(m0 + m1)]
+    sub0 = _Subspace(entries[:m0])
+    sub1 = sub0.extended(entries[m0:])
+    l0_search(sub0, y, slices, L0Config(dimension=2))
+    eng = _lib.engine(None)
+    got = l0_search(sub1, y, slices, L0Config(dimension=3))
+    g_inc = [eng.gram(t).copy() for t in range(T)]
+    assert eng.stage_loose_rows() >= 3 and eng.stage_info()[1]
+    want = l0_search(np.stack([e.values for e in sub1.entries]), y, slices, L0Config(dimension=3))
+    g_full = [eng.gram(t).copy() for t in range(T)]
+    for a, b in zip(g_inc, g_full):
+        assert bits_equal(a, b)
+    assert [md.indices for md in got] == [md.indices for md in want]
+    assert bits_equal([md.score for md in got], [md.score for md in want])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [3, 4])
+def test_dd_screen_multitask_matches_oracle(oracle, monkeypatch, n):
+    """The double-double ill screen with three tasks (per-task Gram blocks and pivots, the pooled
+    score and the worst ratio over tasks) against the exhaustive oracle."""
+    from paper_2502_20072_b200 import L0Config, SearchStats, l0_search
+
+    monkeypatch.setenv("L0S_QR_SCREEN", "dd")
+    rng = np.random.default_rng(70 + n)
+    m, s, T = 40, 300, 3
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    for c, d in enumerate([1e-5, 1e-7, 1e-9, 1e-11]):
+        v[30 + c] = v[2 * c] + d * rng.standard_normal(s)
+    v[36] = 1.0 + 1e-6 * rng.standard_normal(s)
+    slices = [np.arange(t, s, T) for t in range(T)]
+    y = 1e5 * (v[31] - v[2]) + 0.8 * v[15] + (0.3 * v[22] if n == 4 else 0.0) + 0.02 * rng.standard_normal(s)
+    want = oracle.l0_search(v, y, slices, n, 10, "fp64", threads=os.cpu_count() or 1)
+    st = SearchStats()
+    got = l0_search(v, y, slices, L0Config(dimension=n), mode="fast", stats=st)
+    assert st.device["certified"] == 1 and st.device["n_ill"] > 0
+    assert [md.indices for md in got] == [w["indices"] for w in want]
+    assert bits_equal([md.score for md in got], [w["score"] for w in want])
