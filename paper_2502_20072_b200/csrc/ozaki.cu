@@ -123,10 +123,10 @@ __global__ void k_oz_split(const double* __restrict__ Z, int64_t sp, const int64
     if (lane == 0) ex[(int64_t)t * R + f] = e;
 }
 
-// ---- GEMM: one 128 x 64 tile (rows fb, cols gb, gb >= 2 fb: every entry with row <= col
-// lies in exactly one such tile) of one task per CTA ----
-// Tiles are numbered column by column (gb outer, fb = 0 .. gb/2 inner) from tile g0, so a range
-// of column blocks -- the part of the Gram a landed row chunk completes -- is one launch.
+// ---- GEMM: one OZ_BM x OZ_BN tile (rows fb, cols gb, fb * OZ_BM <= the block's last column:
+// every entry with row <= col lies in exactly one such tile) of one task per CTA ----
+// Tiles are numbered column by column (gb outer, fb = 0 .. inner) from tile g0, so a range of
+// column blocks -- the part of the Gram a landed row chunk completes -- is one launch.
 // tiles of column block gb: row blocks fb with fb * BM <= the block's last column
 __host__ __device__ constexpr int oz_tiles_in_block(int gb) { return ((gb + 1) * OZ_BN - 1) / OZ_BM + 1; }
 
