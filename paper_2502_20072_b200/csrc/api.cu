@@ -121,7 +121,7 @@ struct l0s_ctx {
     double ms_gram = 0.0;
     double ms_gram_k = 0.0;  // the Gram kernel alone (unchunked stage)
     DBuf in_values, in_y, in_perm, bounds_d, zoff_d, Xp, yp, Z, G, qf, un2, yyu, rowsd, eta_d;
-    DBuf rho, rho_cap, ynorm, iforce, dead, umin;
+    DBuf rho, rho_cap, ynorm, iforce, dead, umin, tmax;
     int64_t n_dead = 0, n_iforce = 0;
     bool shard_pending = false;  // l0s_stage_shard done, l0s_stage_finish due
     bool host_staged = false;    // in_values / in_y / in_perm hold the staged problem's inputs
@@ -173,7 +173,7 @@ struct l0s_ctx {
     ~l0s_ctx() {
         if (stager) host_stager_destroy(stager);
         DBuf* all[] = {&in_values, &in_y, &in_perm, &bounds_d, &zoff_d, &Xp, &yp, &Z, &G, &qf, &un2, &yyu, &rowsd,
-                       &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &umin, &binom, &units, &ucount, &n_eval, &theta_g, &hist, &seedbuf, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
+                       &eta_d, &rho, &rho_cap, &ynorm, &iforce, &dead, &umin, &tmax, &binom, &units, &ucount, &n_eval, &theta_g, &hist, &seedbuf, &wl_lb, &wl_rank, &wl_cnt, &ill, &ill_cnt,
                        &cand_lb, &cand_rank, &cand_cnt, &sort_tmp, &lb_tmp, &rank_tmp, &coll_lb, &coll_rank,
                        &coll_cnt, &ex_scratch, &ex_ssr_tmp, &ex_ok_tmp, &ex_ok, &ex_score, &ex_coef, &ex_ssr,
                        &ex_ranks, &ex_tuples, &qr_ssr, &qr_ratio, &qr_score, &qr_minr, &ddg_hi, &ddg_lo, &sis_y, &sis_yc, &sis_sy, &sis_perm,
@@ -1389,6 +1389,13 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     a.seed_n = reinterpret_cast<int*>(c->seedbuf.as<double>() + 1024 * (kSeedW + 1));
     a.seed_cap = c->seedbuf.as<double>() + 1024 * (kSeedW + 1) + 4;
     a.keep = (int)keep;
+    if (n == 3 && (c->m + 7) / 8 <= 65535) {  // the sweep's tile screen (fit3.cu: k_tile_max)
+        const int64_t nt = fit3_tmax_doubles(c->m, c->mp);
+        if (nt > 0) {
+            CK(c->tmax.ensure(sizeof(double) * nt));
+            a.tmax = c->tmax.as<double>();
+        }
+    }
     {
         double yy_top = 0.0;  // uncentered total |y|^2 >= every pooled bound
         for (double v : c->yyu_h) yy_top += v;
@@ -1415,7 +1422,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     cudaEventRecord(c->ev[3], c->st);
     CK(cudaGetLastError());
     st->n_fit_launches++;
-    st->n_launches += 4;  // threshold seed (select, eval, commit) + sweep
+    st->n_launches += a.tmax ? 6 : 4;  // threshold seed (select, eval, commit) + tile maxima + the screened and plain sweeps
     if (!big) {
         launch_gather_candidates(a.wl_lb, a.wl_rank, a.wl_cnt, slots, kc, a.theta_g, c->cand_lb.as<double>(),
                                  c->cand_rank.as<int64_t>(), c->cand_cnt.as<unsigned long long>(), c->st);
@@ -1571,7 +1578,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
         cudaEventRecord(c->ev[3], c->st);
         CK(cudaGetLastError());
         st->n_fit_launches++;
-        st->n_launches++;
+        st->n_launches += a.tmax ? 3 : 1;
         unsigned long long ncoll = 0;
         CK(cudaMemcpyAsync(&ncoll, c->coll_cnt.p, sizeof ncoll, cudaMemcpyDeviceToHost, c->st));
         CK(cudaMemcpyAsync(&nev, c->n_eval.p, sizeof nev, cudaMemcpyDeviceToHost, c->st));

@@ -87,6 +87,28 @@ namespace {
 // only groups that survive it re-evaluate that slot with the reciprocal (as NT == 1 always does).
 // WREL: tile buffers are released per warp (mbarrier + last-arriver refill), no CTA barrier per tile.
 constexpr bool WREL = L0S_WREL;
+// TSK: tile screen.  Before a unit's sweep every warp bounds its first task slot over each i-tile
+// from row-block maxima of the Gram (k_tile_max): with a = max |C_ij|, b_p = max |C_ik_p|,
+// c = max |c_i| over the tile's rows,
+//   |g1| <= G1 = b_p + |C_jk| a,   d >= 1 - a^2 - G1^2 / d1,   |w| <= c + a |w0 - C_jk s1| + b_p |s1|,
+// so when (K0 - theta) d_min > (w_max^2 + Bm) (1 + 4 kRcpRel) for every valid pair of the warp,
+// every row of the tile would leave the first slot's test non-negative (pruned) and the warp
+// skips the tile; tiles no warp needs are not loaded at all.  Results are unchanged: a skipped
+// tuple's first-slot bound is at or above the threshold, which is the task pruning's own test.
+#ifndef L0S_TSK_NOCALL
+#define L0S_TSK_NOCALL 0
+#endif
+#ifndef L0S_TSKIP
+#define L0S_TSKIP 1
+#endif
+constexpr bool TSK = L0S_TSKIP && !L0S_WREL;
+constexpr int TSK_WORDS = 8;
+// TSK_CTA: tiles no warp of the CTA needs are not loaded (else every tile is loaded and only the
+// warps' compute is skipped)
+#ifndef L0S_TSK_CTA
+#define L0S_TSK_CTA 1
+#endif
+constexpr bool TSK_CTA = L0S_TSK_CTA;  // tile mask words per unit (units of more than 256 tiles are not screened)
 struct CfgT {
     int P, IB, MINB, UNROLL, NW, NBUF;
 };
@@ -136,6 +158,7 @@ struct Cfg {
     static constexpr CfgT c = (NT == 1) ? kCfg1 : (NT == 2 ? kCfg2 : (NT <= 4 ? kCfg34 : kCfg58));
     static constexpr int P = c.P;
     static constexpr int IB = c.IB;
+    static_assert(IB >= 16, "fit3_tmax_doubles sizes the tile screen's tables for tile heights >= 16");
     static constexpr int NW = c.NW;
     static constexpr int NTH = NW * 32;
     static constexpr int KSPAN = NW * P;
@@ -202,9 +225,121 @@ __device__ __noinline__ int eval_tuple3(const FitArgs& a, int64_t i, int64_t j, 
     return (cond ? 1 : 0) | (rank_ok ? 2 : 0);
 }
 
+// The first task slot's hoisted state of a warp's P pairs, as the tile screen reads it.
+template <int P>
+struct PairSlot0 {
+    double la[P];   // |C_jk|
+    double sa[P];   // |s1|
+    double wja[P];  // |c_j - C_jk s1|
+    double r1[P];   // 1 / (1 - C_jk^2)
+    double kq[P];   // the pair's first-slot margin (K0 - theta) * shrink (NT == 1: whole bound - theta)
+    double bm[P];   // max_t B_t
+    double aw0;     // |c_j|
+    unsigned cand;  // pairs a tile bound may retire: valid, not forced, kq > 0
+    unsigned valid;
+};
+
+// Tile screen (TSK) of one warp over its unit's i-tiles.  Lane l gathers the row-block maxima
+// (k_tile_max) of tile 32 w + l; groups of 4 tiles are tested first on the group's maxima, and
+// only groups that fail are tested tile by tile.  Writes the warp's need bits (wneed[word]) and
+// ORs them into the CTA's (need_cta[word]).  Out of line: its registers stay out of the sweep's.
+template <int P, int IB>
+__device__ __noinline__ void tile_screen(const FitArgs& a, const PairSlot0<P> ps, int lane, int kbase, int jb, int i_lo,
+                                         int i_hi, int nib, unsigned* need_cta, unsigned* wneed) {
+    const int64_t m = a.m;
+    const bool all = __any_sync(L0S_FULL, (ps.valid & ~ps.cand) != 0u);
+    const int nbk = (int)((m + IB - 1) / IB);
+    const double* MT = a.tmax;                                   // [col][block], col <= m
+    const double* MJ = a.tmax + (m + 1) * nbk + (int64_t)jb * nbk;  // this j-block's row
+    constexpr double F = 1.0 + 4.0 * kRcpRel;
+    // the bound of one row set with maxima (am, cm, ka[]): true = some pair still needs it
+    auto needs = [&](double am, double cm, const double (&ka)[P]) {
+        bool need = false;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            if (!((ps.valid >> p) & 1u)) continue;
+            // the sweep's rounding (a few ulp of O(1) terms) is covered by the 1e-14 / 1e-15 terms
+            const double g1 = fma(ps.la[p], am, ka[p]) * (1.0 + 1e-15);
+            const double gg = g1 * g1 * ps.r1[p];
+            const double db = (1.0 - fma(am, am, gg)) - 1e-14 * (1.0 + gg);
+            const double wb = fma(ka[p], ps.sa[p], fma(am, ps.wja[p], cm)) + 1e-15 * fma(g1, ps.sa[p], fma(am, ps.aw0, cm));
+            const double q = fma(wb, wb, ps.bm[p]);
+            // NaN / inf (flagged rows) fail the comparison: needed
+            need |= !(db > 1e-6 && ps.kq[p] * db > q * F);
+        }
+        return __any_sync(L0S_FULL, need);
+    };
+    for (int wd = 0; wd * 32 < nib; ++wd) {
+        unsigned word = all ? ~0u : 0u;
+        if (!all) {
+            double amx = 0.0, cmx = 0.0, kmx[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) kmx[p] = 0.0;
+            const int tl = wd * 32 + lane;
+            if (tl < nib) {
+                const int r0 = i_lo + tl * IB, r1 = min(r0 + IB, i_hi);
+                for (int b = r0 / IB; b <= (r1 - 1) / IB; ++b) {
+                    amx = fmax(amx, MJ[b]);
+                    cmx = fmax(cmx, MT[m * nbk + b]);
+#pragma unroll
+                    for (int p = 0; p < P; ++p) kmx[p] = fmax(kmx[p], MT[(kbase + p < m ? kbase + p : m - 1) * nbk + b]);
+                }
+            }
+            // group maxima over lanes 4g .. 4g + 3 (tiles past nib hold zeros: harmless in a max)
+            double gam = amx, gcm = cmx, gk[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) gk[p] = kmx[p];
+#pragma unroll
+            for (int o = 1; o < 4; o <<= 1) {
+                gam = fmax(gam, __shfl_xor_sync(L0S_FULL, gam, o));
+                gcm = fmax(gcm, __shfl_xor_sync(L0S_FULL, gcm, o));
+#pragma unroll
+                for (int p = 0; p < P; ++p) gk[p] = fmax(gk[p], __shfl_xor_sync(L0S_FULL, gk[p], o));
+            }
+            const int nt = min(32, nib - wd * 32);
+            for (int g = 0; g * 4 < nt; ++g) {
+                double ka[P];
+#pragma unroll
+                for (int p = 0; p < P; ++p) ka[p] = __shfl_sync(L0S_FULL, gk[p], 4 * g);
+                if (!needs(__shfl_sync(L0S_FULL, gam, 4 * g), __shfl_sync(L0S_FULL, gcm, 4 * g), ka)) continue;
+                for (int bb = 4 * g; bb < min(4 * g + 4, nt); ++bb) {
+#pragma unroll
+                    for (int p = 0; p < P; ++p) ka[p] = __shfl_sync(L0S_FULL, kmx[p], bb);
+                    if (needs(__shfl_sync(L0S_FULL, amx, bb), __shfl_sync(L0S_FULL, cmx, bb), ka)) word |= 1u << bb;
+                }
+            }
+        }
+        if (lane == 0) {
+            wneed[wd] = word;
+            atomicOr(&need_cta[wd], word);
+        }
+    }
+}
+
+// The sweep's static shared state (one instance per CTA, whichever instantiation runs).
 template <int NT>
-__global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __grid_constant__ FitArgs a) {
+struct FitShared {
     using C = Cfg<NT>;
+    int unit;
+    int tord[NT];
+    unsigned char force[C::NBUF][C::IB];  // iforce flags of the staged rows
+    int fany[C::NBUF];                    // any of them set
+    alignas(8) unsigned long long bar[C::NBUF];  // TMA completion, one per tile buffer
+    alignas(8) unsigned long long hbar;          // TMA completion of the unit's hoist block
+    unsigned rel[C::NBUF];                       // WREL: warps done with the buffer's tile
+    double th;                                   // the unit's shared threshold
+    unsigned need[TSK_WORDS];                    // TSK: tiles some warp needs
+    unsigned wneed[C::NW][TSK_WORDS];            // TSK: tiles this warp needs
+    double ts[4][NT];  // Y2, gamma, eta, A0 = 4 gamma |y_c| |y| (task_bound's constant term)
+    // the unit's hoist inputs besides C[k, j] (TMA block), per task slot: c_j and max(rho_cap,
+    // rho_j) over the j-block, c_k and rho_k over the k-span
+    double hu[NT][4][32];
+};
+
+template <int NT, bool SCR>
+__device__ __forceinline__ void fit3_sweep(const FitArgs& a, FitShared<NT>& S) {
+    using C = Cfg<NT>;
+    constexpr bool TSKB = TSK && SCR;  // this instantiation runs the tile screen
     constexpr int NW3 = C::NW, NT3 = C::NTH;
     constexpr int P = C::P, IB = C::IB, TS = C::TS, BS = C::BS, KSPAN = C::KSPAN, R = C::R, NB = C::NBUF;
     constexpr bool DF = L0S_DIVFREE && NT > 1 && !C::SLOT0 && (P % 2 == 0);
@@ -213,14 +348,18 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
     static_assert(!PA || NG <= 32, "group bits in one word");
     int pa_tot = 0, pa_surv = 0;  // groups seen / surviving the first slot (warp-uniform, decayed)
     extern __shared__ __align__(128) double sm[];
-    __shared__ int s_unit;
-    __shared__ int s_tord[NT];
-    __shared__ unsigned char s_force[NB][IB];  // iforce flags of the staged rows
-    __shared__ int s_fany[NB];                 // any of them set
-    __shared__ __align__(8) unsigned long long s_bar[NB];  // TMA completion, one per tile buffer
-    __shared__ __align__(8) unsigned long long s_hbar;     // TMA completion of the unit's hoist block
-    __shared__ unsigned s_rel[NB];                           // WREL: warps done with the buffer's tile
-    __shared__ double s_th;                                 // the unit's shared threshold
+    auto& s_unit = S.unit;
+    auto& s_tord = S.tord;
+    auto& s_force = S.force;
+    auto& s_fany = S.fany;
+    auto& s_bar = S.bar;
+    auto& s_hbar = S.hbar;
+    auto& s_rel = S.rel;
+    auto& s_th = S.th;
+    auto& s_need = S.need;
+    auto& s_wneed = S.wneed;
+    auto& s_ts = S.ts;
+    auto& s_hu = S.hu;
     unsigned long long n_ev = 0;                            // row-group task evaluations (warp-uniform)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t m = a.m, mp = a.mp;
@@ -261,7 +400,6 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
     __syncthreads();
     // unit-independent per-task scalars of the hoist, in slot order, once per CTA (shared
     // memory instead of a global load chain per unit)
-    __shared__ double s_ts[4][NT];  // Y2, gamma, eta, A0 = 4 gamma |y_c| |y| (task_bound's constant term)
     if (tid < NT) {
         const int tk = s_tord[tid];
         const double Y2 = a.G[(int64_t)tk * mp * mp + m * mp + m], gam = ref_gamma(a.rowsd[tk], 3, a.ref_fp32);
@@ -273,11 +411,13 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
     // the unit's hoist inputs besides C[k, j] (TMA block below), per task slot, staged by all
     // threads with coalesced loads: c_j and max(rho_cap, rho_j) over the j-block, c_k and rho_k
     // over the k-span (a per-pair global load chain stalled the hoist on the LSU queue)
-    __shared__ double s_hu[NT][4][32];
     static_assert(KSPAN <= 32, "k-span staged in 32-wide rows");
     __syncthreads();
     const int* tord = s_tord;  // read where the hoist / tile loads need it (rare)
     unsigned parity = 0u, hpar = 0u;  // full-barrier phase bit per tile buffer
+    // TSKB: the block maxima must be those of this kernel's first slot (k_tile_max picks the same task)
+    const bool tsk_on = TSKB && a.tmax != nullptr &&
+                        a.tmax[(m + 1 + (m + 31) / 32) * ((m + IB - 1) / IB)] == (double)tord[0];
     // The unit's hoist block goes through TMA into tile buffers 1.. (idle until the sweep's first
     // prefetch): per task slot C[k-span, j-block] (KSPAN x 32).
     constexpr int HS = KSPAN * 32;  // doubles per task slot: C[k-span, j-block]
@@ -343,6 +483,7 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
         const int j = j0 + lane;
         const int kbase = k0 + warp * P;
         const int i_lo = U.z, i_hi = U.w;
+        if (TSKB && tid < TSK_WORDS) s_need[tid] = 0u;  // ordered before the screen's atomics by the hoist's barriers
         double* Hb = sm + BS;  // tile buffers 1..
         if (HT && tid == 0) {
             fence_proxy_async();  // the previous unit's reads of buffer 1 precede these writes
@@ -376,16 +517,20 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
         __syncthreads();
         if (a.collect != 1 && s_th < wc.theta) wc.theta = s_th;
 
+        if (HT) {
+            mbar_wait(&s_hbar, hpar);
+            hpar ^= 1u;
+        }
+        // ---------------- tile screen (TSKB, out of line: its registers stay out of the sweep's) ----------------
+        const int nib = (i_hi - i_lo + IB - 1) / IB;
+        const bool scr = tsk_on && nib <= 32 * TSK_WORDS;
+
         // ---------------- hoist: (j, k_p) state per task (slot order) ----------------
         // L10 = C_jk, rd1 = 1/(1 - C_jk^2), s1 = rd1 (c_k - C_jk c_j); the bound's B_t/d term
         // uses Bm = max_t B_t per pair, so the sweep needs one extra register per pair only
         double L10[P][NT], rd1[P][NT], s1[P][NT], w0[NT], Kq[P], Bm[P];
         double K1r[P];  // NT == 2: task slot 1's (base - A) * shrink in registers
         unsigned valid = 0, bad = 0, forced = 0;
-        if (HT) {
-            mbar_wait(&s_hbar, hpar);
-            hpar ^= 1u;
-        }
 #pragma unroll
         for (int t = 0; t < NT; ++t) w0[t] = s_hu[t][0][lane];
 #pragma unroll
@@ -443,16 +588,59 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
             }
         };
         set_kq();
+        if (scr && !L0S_TSK_NOCALL) {
+            PairSlot0<P> ps;
+            ps.aw0 = fabs(w0[0]);
+            ps.valid = valid;
+            ps.cand = 0u;
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                ps.la[p] = fabs(L10[p][0]);
+                ps.sa[p] = fabs(s1[p][0]);
+                ps.wja[p] = fabs(fma(-L10[p][0], s1[p][0], w0[0]));
+                ps.r1[p] = rd1[p][0];
+                ps.kq[p] = Kq[p];
+                ps.bm[p] = Bm[p];
+                if (!((forced >> p) & 1u) && Kq[p] > 0.0) ps.cand |= 1u << p;
+            }
+            tile_screen<P, IB>(a, ps, lane, kbase, U.x, i_lo, i_hi, nib, s_need, s_wneed[warp]);
+        } else if (TSKB && lane < TSK_WORDS) {  // no screen: every tile (the sweep reads the masks alone)
+            s_wneed[warp][lane] = ~0u;
+            atomicOr(&s_need[lane], ~0u);
+        }
         __syncthreads();  // every warp is done with the hoist block: buffer 1 may take tile 1
 
+        // first tile at or after b that some warp needs (TSKB; the masks are all ones without a screen)
+        auto next_needed = [&](int b) {
+            if (TSKB && TSK_CTA)
+                while (b < nib && b < 32 * TSK_WORDS && !((s_need[b >> 5] >> (b & 31)) & 1u)) ++b;
+            return b;
+        };
+
         // ---------------- sweep i ----------------
-        const int nib = (i_hi - i_lo + IB - 1) / IB;
         if (WREL)
             for (int b = 1; b < NB && b < nib; ++b) load_tiles(b, i_lo + b * IB, j0, k0);
+        {
+            const int bf = next_needed(0);
+            if (TSKB && bf != 0) {
+                // tile 0 was loaded before the hoist but no warp needs it: retire its load and
+                // stage the first needed tile (buffer bf & 1; buffer 1 is free after the hoist)
+                wait_tiles(0);
+                __syncthreads();  // (every warp past the wait before the buffer is rewritten)
+                if (bf < nib) load_tiles(bf & 1, i_lo + bf * IB, j0, k0);
+            }
+        }
+        // The tile counter stays a plain loop variable (warp-uniform to the compiler: the sweep's
+        // shared-memory addressing stays scalar); tiles no warp needs are passed over, and tile bi
+        // sits in buffer bi & 1 -- a next needed tile of the same parity is staged after this one.
         for (int bi = 0; bi < nib; ++bi) {
+            if (TSKB && TSK_CTA && bi < 32 * TSK_WORDS && !((s_need[bi >> 5] >> (bi & 31)) & 1u)) continue;
             const int buf = WREL ? bi % NB : (bi & 1);
             const int ib0 = i_lo + bi * IB;
-            if (!WREL && bi + 1 < nib) load_tiles(buf ^ 1, ib0 + IB, j0, k0);
+            if (!WREL) {
+                const int bn = next_needed(bi + 1);
+                if (bn < nib && (bn & 1) != (bi & 1)) load_tiles(buf ^ 1, i_lo + bn * IB, j0, k0);
+            }
             wait_tiles(buf);
 #ifndef L0S_TILE_BAR0
 #define L0S_TILE_BAR0 1
@@ -592,6 +780,11 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
                     pa_surv >>= 1;
                 }
             }
+            // TSKB: a warp whose pairs all clear this tile's bound has nothing pending in it
+            const bool wneed = !TSKB || __any_sync(L0S_FULL, bi >= 32 * TSK_WORDS || ((s_wneed[warp][bi >> 5] >> (bi & 31)) & 1u));
+#pragma unroll
+            for (int pw = 0; pw < NPW; ++pw) pend[pw] = 0u;
+            if (wneed) {
 #pragma unroll
             for (int pw = 0; pw < NPW; ++pw) {
                 unsigned word = 0u;
@@ -693,6 +886,7 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
                 }
                 pend[pw] = word;
             }
+            }
 
             // ---------------- slow path (rare), after the tile ----------------
             drain_pending<NPW>(
@@ -719,12 +913,39 @@ __global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __gr
                 }
             } else {
                 __syncthreads();
+                if (TSKB && TSK_CTA) {
+                    const int bn = next_needed(bi + 1);
+                    if (bn < nib && (bn & 1) == (bi & 1)) load_tiles(buf, i_lo + bn * IB, j0, k0);
+                }
             }
         }
         if (WREL) __syncthreads();  // the unit's tiles are consumed before the next unit's loads
     }
     if (lane == 0 && a.n_eval) atomicAdd(a.n_eval, n_ev * (unsigned long long)(R * P * 32));
     flush_warp(a, wc, blockIdx.x * NW3 + warp, lane);
+}
+
+// The tile screen pays only while the threshold is below the first slot's |y_c|^2 (a pair's first-
+// slot margin K0 - theta is positive): dense near-ties (random y over several tasks) never get
+// there.  Two kernels are launched back to back, the screened one first; each CTA tests the
+// threshold at its start and only the matching kernel sweeps (the threshold only falls while the
+// screened one runs, so the second then finds it below too and exits).  Separate kernels keep the
+// unscreened sweep's code exactly the plain one (sharing one kernel cost it 3-5 %, C3 random y).
+template <int NT, bool SCR>
+__global__ void __launch_bounds__(Cfg<NT>::NTH, Cfg<NT>::MINB) k_fit3(const __grid_constant__ FitArgs a) {
+    __shared__ FitShared<NT> S;
+    if constexpr (TSK) {
+        __shared__ int s_use;
+        if (threadIdx.x == 0) {
+            double y2 = 0.0;
+            for (int t = 0; t < a.T; ++t) y2 = fmax(y2, a.G[(int64_t)t * a.mp * a.mp + a.m * a.mp + a.m]);
+            const double th = a.collect == 1 ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g);
+            s_use = a.tmax != nullptr && th < y2;
+        }
+        __syncthreads();
+        if ((s_use != 0) != SCR) return;
+    }
+    fit3_sweep<NT, SCR>(a, S);
 }
 
 // Same arithmetic as the fit kernel (hoist on (j, k), sweep variable i), one thread per explicit tuple.
@@ -745,6 +966,50 @@ __global__ void __launch_bounds__(128) k_seed_eval3(const __grid_constant__ FitA
     a.seed_ub[c] = (fl == 3 && ub == ub) ? ub : INFINITY;
 }
 
+// Row-block maxima for the tile screen (TSK), blocks of IB rows (the sweep's tile height,
+// aligned at row 0) of the first task slot (the task of largest |y_c|^2, first on ties, as k_fit3
+// orders them): [col][block] max |C[i, col]| for col <= m (col = m: max |c_i|), then
+// [j-block][block] the maximum over the j-block's 32 columns, then the slot's task index.  +inf
+// where a row is iforce-flagged (column m) or an entry is NaN.  One read of one task's Gram.
+template <int IB>
+__global__ void __launch_bounds__(256) k_tile_max(const double* __restrict__ G, const unsigned char* __restrict__ iforce,
+                                                  int64_t m, int64_t mp, int T, double* __restrict__ out) {
+    __shared__ int s_t0;
+    const int64_t nbk = (m + IB - 1) / IB, nJ = (m + 31) / 32;
+    if (threadIdx.x == 0) {
+        int best = 0;
+        double bv = G[m * mp + m];
+        for (int t = 1; t < T; ++t) {
+            const double v = G[(int64_t)t * mp * mp + m * mp + m];
+            if (v > bv) {
+                bv = v;
+                best = t;
+            }
+        }
+        s_t0 = best;
+        if (blockIdx.x == 0 && blockIdx.y == 0) out[(m + 1 + nJ) * nbk] = (double)best;
+    }
+    __syncthreads();
+    const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t b = blockIdx.y;
+    const double* Gt = G + (int64_t)s_t0 * mp * mp;
+    double mx = 0.0;
+    if (col <= m) {
+        bool bad = false;
+        for (int64_t i = b * IB; i < min(b * IB + IB, m); ++i) {
+            const double v = Gt[i * mp + col];
+            bad |= (v != v) || (col == m && iforce[i]);
+            mx = fmax(mx, fabs(v));
+        }
+        if (bad) mx = INFINITY;
+        out[col * nbk + b] = mx;
+    }
+    double jm = col < m ? mx : 0.0;  // warps cover whole j-blocks (blockDim and the x offset are multiples of 32)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) jm = fmax(jm, __shfl_xor_sync(L0S_FULL, jm, o));
+    if ((threadIdx.x & 31) == 0 && col < m) out[(m + 1) * nbk + (col >> 5) * nbk + b] = jm;
+}
+
 template <int NT>
 int launch_nt(const FitArgs& a0, int nsm, cudaStream_t st) {
     using C = Cfg<NT>;
@@ -753,13 +1018,19 @@ int launch_nt(const FitArgs& a0, int nsm, cudaStream_t st) {
     if (!make_tma_2d(&a.tmJ, a.G, cols, rows, 32, C::IB) || !make_tma_2d(&a.tmK, a.G, cols, rows, C::KSPAN, C::IB) ||
         !make_tma_2d(&a.tmC, a.G, cols, rows, 2, C::IB) || !make_tma_2d(&a.tmH, a.G, cols, rows, 32, C::KSPAN))
         return -1;
-    cudaFuncSetAttribute(k_fit3<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes);
+    cudaFuncSetAttribute(k_fit3<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, C::NTH, C::smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT, false>, C::NTH, C::smem_bytes);
     if (per_sm < 1) per_sm = 1;
     int grid = nsm * per_sm;
     if (a.collect != 1) seed_launch<3, 18>(k_seed_eval3, a, st);
-    k_fit3<NT><<<grid, C::NTH, C::smem_bytes, st>>>(a);
+    if (TSK && a.tmax) {
+        k_tile_max<C::IB><<<dim3((unsigned)((a.m + 256) / 256), (unsigned)((a.m + C::IB - 1) / C::IB)), 256, 0, st>>>(
+            a.G, a.iforce, a.m, a.mp, a.T, a.tmax);
+        cudaFuncSetAttribute(k_fit3<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes);
+        k_fit3<NT, true><<<grid, C::NTH, C::smem_bytes, st>>>(a);
+    }
+    k_fit3<NT, false><<<grid, C::NTH, C::smem_bytes, st>>>(a);
     return grid;
 }
 
@@ -774,6 +1045,10 @@ void launch_screen3(const FitArgs& a, const int64_t* tuples, int64_t count, doub
 // terms alone bound the pooled SSR from below (every task's SSR is >= 0); the slow path, the
 // certificates and the exact refit take every task.
 int fit3_max_tasks() { return 1 << 16; }
+int64_t fit3_tmax_doubles(int64_t m, int64_t mp) {
+    (void)mp;
+    return TSK ? (m + 1 + (m + 31) / 32) * ((m + 15) / 16) + 1 : 0;  // tile heights >= 16
+}
 int fit_slots_per_cta() { return NW; }
 int fit3_slots_per_cta(int T) {
     return T == 1 ? Cfg<1>::NW : (T == 2 ? Cfg<2>::NW : (T <= 4 ? Cfg<4>::NW : Cfg<8>::NW));
@@ -792,15 +1067,15 @@ int fit3_grid(int T, int nsm) {
     switch (T) {
 #define OCC(NT)                                                                                              \
     case NT:                                                                                                 \
-        cudaFuncSetAttribute(k_fit3<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<NT>::smem_bytes); \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT>, Cfg<NT>::NTH, Cfg<NT>::smem_bytes); \
+        cudaFuncSetAttribute(k_fit3<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<NT>::smem_bytes); \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<NT, false>, Cfg<NT>::NTH, Cfg<NT>::smem_bytes); \
         break;
         OCC(1) OCC(2) OCC(3) OCC(4) OCC(5) OCC(6) OCC(7) OCC(8)
 #undef OCC
         default:
             if (T < 1) return -1;
-            cudaFuncSetAttribute(k_fit3<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<8>::smem_bytes);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<8>, Cfg<8>::NTH, Cfg<8>::smem_bytes);
+            cudaFuncSetAttribute(k_fit3<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<8>::smem_bytes);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit3<8, false>, Cfg<8>::NTH, Cfg<8>::smem_bytes);
     }
     return nsm * (per_sm < 1 ? 1 : per_sm);
 }

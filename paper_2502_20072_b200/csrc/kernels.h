@@ -253,7 +253,13 @@ struct FitArgs {
     unsigned long long* coll_cnt;
     int64_t coll_cap;
     unsigned long long* n_eval;  // out (optional): task-tuple evaluations of the sweep (executed work)
+    // (optional, n = 3) row-block maxima of the first task slot's Gram for the tile screen, blocks
+    // of the sweep's tile height: [col <= m][block] max |C[i, col]| (col = m: max |c_i|; +inf for a
+    // flagged or NaN row), [j-block][block], then the slot's task index (fit3.cu: k_tile_max)
+    double* tmax = nullptr;
 };
+// doubles fit3_launch needs in FitArgs::tmax for an m-feature problem
+int64_t fit3_tmax_doubles(int64_t m, int64_t mp);
 // n = 1 (fit1.cu): dense lower bounds of the features [rb, re) (+inf: ill or dead; ill ranks appended)
 void launch_fit1(const FitArgs& a, int64_t rb, int64_t re, double* out_lb, int64_t* out_rank, cudaStream_t st);
 int fit3_launch(const FitArgs& a, int nsm, cudaStream_t st);  // returns grid size (warp slots / 8)

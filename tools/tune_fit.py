@@ -22,9 +22,8 @@ VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
     "base": (),
-    "wrel_nb6_ib8": ("L0S_WREL=1", "L0S_C34_NBUF=6", "L0S_C34_IB=8"),
-    "wrel_nb4_ib8": ("L0S_WREL=1", "L0S_C34_NBUF=4", "L0S_C34_IB=8"),
-    "bar_ib8": ("L0S_C34_IB=8",),
+    "warp_only": ("L0S_TSK_CTA=0",),
+    "no_tile_screen": ("L0S_TSKIP=0",),
 }
 if os.environ.get("L0S_TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["L0S_TUNE_ONLY"].split(",")}
@@ -69,13 +68,17 @@ def time_one(steps: int = 5):
 
 def run_all():
     out = {}
-    for name in VARIANTS:
+    rounds = int(os.environ.get("L0S_TUNE_ROUNDS", "1"))
+    for name in [v for _ in range(rounds) for v in VARIANTS]:  # interleaved rounds: min over rounds
         path = os.path.join(VDIR, f"lib_{name}.so")
         env = dict(os.environ, L0S_LIB=path)
         r = subprocess.run([sys.executable, __file__, "one"], env=env, capture_output=True, text=True, timeout=600)
         line = [x for x in r.stdout.splitlines() if x.startswith("{")]
-        out[name] = json.loads(line[-1]) if line else {"error": r.stderr[-400:]}
-        print(name, {k: v for k, v in out[name].items() if k not in ("ranks", "scores")}, flush=True)
+        o = json.loads(line[-1]) if line else {"error": r.stderr[-400:]}
+        if name in out and "fit_ms_min" in out[name] and "fit_ms_min" in o:
+            o["fit_ms_min"] = min(o["fit_ms_min"], out[name]["fit_ms_min"])
+        out[name] = o
+        print(name, {k: v for k, v in o.items() if k not in ("ranks", "scores")}, flush=True)
     ref = next((o for o in out.values() if "ranks" in o), None)
     for name, o in out.items():
         if "ranks" in o:
