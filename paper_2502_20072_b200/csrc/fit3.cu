@@ -493,7 +493,7 @@ __device__ __forceinline__ void fit3_sweep(const FitArgs& a, FitShared<NT>& S) {
                 tma_load_2d(Hb + t * HS, &a.tmH, j0, (int)(tord[t] * mp) + k0, &s_hbar);
             }
         }
-        load_tiles(0, i_lo, j0, k0);
+        if (!TSKB) load_tiles(0, i_lo, j0, k0);  // (with the screen: the first needed tile, below)
         for (int x = tid; x < NT * 128; x += NT3) {
             const int t = x >> 7, w = (x >> 5) & 3, l = x & 31;
             const int tk = tord[t];
@@ -522,8 +522,75 @@ __device__ __forceinline__ void fit3_sweep(const FitArgs& a, FitShared<NT>& S) {
             hpar ^= 1u;
         }
         // ---------------- tile screen (TSKB, out of line: its registers stay out of the sweep's) ----------------
+        // Before the hoist, from the first slot's exact hoist of each pair plus, over every slot, the
+        // finiteness / conditioning flags and an upper bound on Bm = max_t B_t (1/d1 rounded up in
+        // float): a unit no warp needs a tile of skips the hoist and the sweep altogether.
         const int nib = (i_hi - i_lo + IB - 1) / IB;
         const bool scr = tsk_on && nib <= 32 * TSK_WORDS;
+        if constexpr (TSKB) {
+            if (scr && !L0S_TSK_NOCALL) {
+                PairSlot0<P> ps;
+                const double wj0 = s_hu[0][0][lane];
+                ps.aw0 = fabs(wj0);
+                ps.valid = 0u;
+                ps.cand = 0u;
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const int k = kbase + p;
+                    bool ok = true, fin = true;
+                    double bm = 0.0;
+                    {
+                        const double Y2 = s_ts[0][0];
+                        const double cjk = HT ? Hb[(k - k0) * 32 + lane] : a.G[(int64_t)tord[0] * mp * mp + (int64_t)k * mp + j];
+                        const double ck = s_hu[0][2][k - k0];
+                        const double d1 = fma(-cjk, cjk, 1.0);
+                        const double r1 = rcp_newton(d1);
+                        const double v1 = fma(-cjk, wj0, ck);
+                        const double base = Y2 - wj0 * wj0 - v1 * v1 * r1;
+                        const double trh = 2.0 * r1;
+                        double At, Bt, vk;
+                        const double rh = fmax(s_hu[0][1][lane], s_hu[0][3][k - k0]);
+                        task_bound_a0(3, s_ts[2][0], s_ts[1][0], rh, Y2, s_ts[3][0], trh, At, Bt, vk);
+                        if (!(d1 > 0.0) || !(vk * (1.0 + 3.0 * trh) <= FO_LIM)) ok = false;
+                        if (cjk != cjk || ck != ck || wj0 != wj0) fin = false;
+                        bm = Bt;
+                        const double s1v = v1 * r1;
+                        ps.la[p] = fabs(cjk);
+                        ps.sa[p] = fabs(s1v);
+                        ps.wja[p] = fabs(fma(-cjk, s1v, wj0));
+                        ps.r1[p] = r1;
+                        ps.kq[p] = (NT == 1) ? (base - At) - wc.theta : ((base - At) - wc.theta) * shrink;
+                    }
+#pragma unroll
+                    for (int t = 1; t < NT; ++t) {
+                        const double cjk = HT ? Hb[t * HS + (k - k0) * 32 + lane] : a.G[(int64_t)tord[t] * mp * mp + (int64_t)k * mp + j];
+                        const double ck = s_hu[t][2][k - k0], wj = s_hu[t][0][lane];
+                        const double d1 = fma(-cjk, cjk, 1.0);
+                        // 1/d1 from above: d1 rounded down to float, its reciprocal rounded up (0 or
+                        // denormal: inf, the pair is then never retired)
+                        const double trh = 2.0 * (double)__frcp_ru(__double2float_rd(d1));
+                        double At, Bt, vk;
+                        const double rh = fmax(s_hu[t][1][lane], s_hu[t][3][k - k0]);
+                        task_bound_a0(3, s_ts[2][t], s_ts[1][t], rh, s_ts[0][t], s_ts[3][t], trh, At, Bt, vk);
+                        if (!(d1 > 0.0) || !(vk * (1.0 + 3.0 * trh) <= FO_LIM)) ok = false;
+                        if (cjk != cjk || ck != ck || wj != wj) fin = false;
+                        bm = fmax(bm, Bt);
+                    }
+                    ps.bm[p] = fmax(bm, 1e-300);
+                    if (j < k && k < m && fin) ps.valid |= 1u << p;
+                    if (ok && fin && ps.kq[p] > 0.0 && bm == bm) ps.cand |= 1u << p;
+                }
+                tile_screen<P, IB>(a, ps, lane, kbase, U.x, i_lo, i_hi, nib, s_need, s_wneed[warp]);
+            } else if (lane < TSK_WORDS) {  // no screen: every tile (the sweep reads the masks alone)
+                s_wneed[warp][lane] = ~0u;
+                atomicOr(&s_need[lane], ~0u);
+            }
+            __syncthreads();
+            unsigned anyw = 0u;
+#pragma unroll
+            for (int w = 0; w < TSK_WORDS; ++w) anyw |= s_need[w];
+            if (anyw == 0u) continue;  // no warp needs a tile of this unit: no hoist, no sweep
+        }
 
         // ---------------- hoist: (j, k_p) state per task (slot order) ----------------
         // L10 = C_jk, rd1 = 1/(1 - C_jk^2), s1 = rd1 (c_k - C_jk c_j); the bound's B_t/d term
@@ -588,58 +655,47 @@ __device__ __forceinline__ void fit3_sweep(const FitArgs& a, FitShared<NT>& S) {
             }
         };
         set_kq();
-        if (scr && !L0S_TSK_NOCALL) {
-            PairSlot0<P> ps;
-            ps.aw0 = fabs(w0[0]);
-            ps.valid = valid;
-            ps.cand = 0u;
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                ps.la[p] = fabs(L10[p][0]);
-                ps.sa[p] = fabs(s1[p][0]);
-                ps.wja[p] = fabs(fma(-L10[p][0], s1[p][0], w0[0]));
-                ps.r1[p] = rd1[p][0];
-                ps.kq[p] = Kq[p];
-                ps.bm[p] = Bm[p];
-                if (!((forced >> p) & 1u) && Kq[p] > 0.0) ps.cand |= 1u << p;
-            }
-            tile_screen<P, IB>(a, ps, lane, kbase, U.x, i_lo, i_hi, nib, s_need, s_wneed[warp]);
-        } else if (TSKB && lane < TSK_WORDS) {  // no screen: every tile (the sweep reads the masks alone)
-            s_wneed[warp][lane] = ~0u;
-            atomicOr(&s_need[lane], ~0u);
-        }
         __syncthreads();  // every warp is done with the hoist block: buffer 1 may take tile 1
 
         // first tile at or after b that some warp needs (TSKB; the masks are all ones without a screen)
-        auto next_needed = [&](int b) {
-            if (TSKB && TSK_CTA)
-                while (b < nib && b < 32 * TSK_WORDS && !((s_need[b >> 5] >> (b & 31)) & 1u)) ++b;
-            return b;
+        // (word-wise, and made warp-uniform by a reduction so that the sweep's addressing stays scalar)
+        auto next_needed = [&](int b) -> int {
+            if constexpr (TSKB && TSK_CTA) {
+                int r = b;  // past the screened range: every tile
+                if (b < 32 * TSK_WORDS) {
+                    r = nib;
+                    for (int w = b >> 5; w < TSK_WORDS && w * 32 < nib; ++w) {
+                        unsigned msk = s_need[w];
+                        if (w == (b >> 5)) msk &= ~0u << (b & 31);
+                        if (msk) {
+                            r = w * 32 + __ffs(msk) - 1;
+                            break;
+                        }
+                    }
+                }
+                return (int)__reduce_min_sync(L0S_FULL, (unsigned)min(r, nib));
+            } else {
+                return b;
+            }
         };
 
         // ---------------- sweep i ----------------
         if (WREL)
             for (int b = 1; b < NB && b < nib; ++b) load_tiles(b, i_lo + b * IB, j0, k0);
-        {
+        // the screened sweep stages the first needed tile only now (buffer 0; the hoist used 1..)
+        if (TSKB) {
             const int bf = next_needed(0);
-            if (TSKB && bf != 0) {
-                // tile 0 was loaded before the hoist but no warp needs it: retire its load and
-                // stage the first needed tile (buffer bf & 1; buffer 1 is free after the hoist)
-                wait_tiles(0);
-                __syncthreads();  // (every warp past the wait before the buffer is rewritten)
-                if (bf < nib) load_tiles(bf & 1, i_lo + bf * IB, j0, k0);
-            }
+            if (bf < nib) load_tiles(0, i_lo + bf * IB, j0, k0);
         }
-        // The tile counter stays a plain loop variable (warp-uniform to the compiler: the sweep's
-        // shared-memory addressing stays scalar); tiles no warp needs are passed over, and tile bi
-        // sits in buffer bi & 1 -- a next needed tile of the same parity is staged after this one.
-        for (int bi = 0; bi < nib; ++bi) {
-            if (TSKB && TSK_CTA && bi < 32 * TSK_WORDS && !((s_need[bi >> 5] >> (bi & 31)) & 1u)) continue;
-            const int buf = WREL ? bi % NB : (bi & 1);
+        // needed tiles in order, alternating between the two buffers (pb); the next one is staged
+        // while this one is swept
+        int pb = 0;
+        for (int bi = next_needed(0); bi < nib; bi = next_needed(bi + 1), pb ^= 1) {
+            const int buf = WREL ? bi % NB : (TSKB ? pb : (bi & 1));
             const int ib0 = i_lo + bi * IB;
             if (!WREL) {
                 const int bn = next_needed(bi + 1);
-                if (bn < nib && (bn & 1) != (bi & 1)) load_tiles(buf ^ 1, i_lo + bn * IB, j0, k0);
+                if (bn < nib) load_tiles(buf ^ 1, i_lo + bn * IB, j0, k0);
             }
             wait_tiles(buf);
 #ifndef L0S_TILE_BAR0
@@ -913,10 +969,6 @@ __device__ __forceinline__ void fit3_sweep(const FitArgs& a, FitShared<NT>& S) {
                 }
             } else {
                 __syncthreads();
-                if (TSKB && TSK_CTA) {
-                    const int bn = next_needed(bi + 1);
-                    if (bn < nib && (bn & 1) == (bi & 1)) load_tiles(buf, i_lo + bn * IB, j0, k0);
-                }
             }
         }
         if (WREL) __syncthreads();  // the unit's tiles are consumed before the next unit's loads
@@ -968,7 +1020,8 @@ __global__ void __launch_bounds__(128) k_seed_eval3(const __grid_constant__ FitA
 
 // Row-block maxima for the tile screen (TSK), blocks of IB rows (the sweep's tile height,
 // aligned at row 0) of the first task slot (the task of largest |y_c|^2, first on ties, as k_fit3
-// orders them): [col][block] max |C[i, col]| for col <= m (col = m: max |c_i|), then
+// orders them): [col][block] max |C[i, col]| over i != col for col <= m (col = m: max |c_i|;
+// the diagonal is left out -- every tile that reaches a lane's own j or k would fail), then
 // [j-block][block] the maximum over the j-block's 32 columns, then the slot's task index.  +inf
 // where a row is iforce-flagged (column m) or an entry is NaN.  One read of one task's Gram.
 template <int IB>
@@ -997,6 +1050,7 @@ __global__ void __launch_bounds__(256) k_tile_max(const double* __restrict__ G, 
     if (col <= m) {
         bool bad = false;
         for (int64_t i = b * IB; i < min(b * IB + IB, m); ++i) {
+            if (i == col) continue;  // C_jj = 1: a tuple never repeats a feature (i < j < k)
             const double v = Gt[i * mp + col];
             bad |= (v != v) || (col == m && iforce[i]);
             mx = fmax(mx, fabs(v));
