@@ -229,12 +229,12 @@ __device__ __noinline__ int eval_tuple3(const FitArgs& a, int64_t i, int64_t j, 
 template <int P>
 struct PairSlot0 {
     double la[P];   // |C_jk|
-    double sa[P];   // |s1|
-    double wja[P];  // |c_j - C_jk s1|
-    double r1[P];   // 1 / (1 - C_jk^2)
-    double kq[P];   // the pair's first-slot margin (K0 - theta) * shrink (NT == 1: whole bound - theta)
-    double bm[P];   // max_t B_t
-    double aw0;     // |c_j|
+    double sa[P];   // |s1| (1 + 2e-15)
+    double wja[P];  // |c_j - C_jk s1| + 1e-15 (|C_jk| |s1| + |c_j|)
+    double r1[P];   // 1 / (1 - C_jk^2), times (1 + 2e-14)
+    double kq[P];   // the pair's first-slot margin (K0 - theta) * shrink (NT == 1: whole bound - theta),
+                    // divided by (1 + 4 kRcpRel) (1 + 1e-12)
+    double bm[P];   // an upper bound on max_t B_t
     unsigned cand;  // pairs a tile bound may retire: valid, not forced, kq > 0
     unsigned valid;
 };
@@ -251,21 +251,23 @@ __device__ __noinline__ void tile_screen(const FitArgs& a, const PairSlot0<P> ps
     const int nbk = (int)((m + IB - 1) / IB);
     const double* MT = a.tmax;                                   // [col][block], col <= m
     const double* MJ = a.tmax + (m + 1) * nbk + (int64_t)jb * nbk;  // this j-block's row
-    constexpr double F = 1.0 + 4.0 * kRcpRel;
-    // the bound of one row set with maxima (am, cm, ka[]): true = some pair still needs it
+    // the bound of one row set with maxima (am, cm, ka[]): true = some pair still needs it.
+    //   |g1| <= G1 = |C_jk| am + ka,  d >= 1 - am^2 - G1^2 / d1,  |w| <= cm + am |c_j - C_jk s1| + ka |s1|,
+    // retired when K d_min > (w_max^2 + Bm); the sweep's own rounding (a few ulp of O(1) terms) and
+    // its reciprocal's error are folded into the per-pair constants (PairSlot0) and the 1e-14 here
     auto needs = [&](double am, double cm, const double (&ka)[P]) {
+        const double c1 = fma(-am, am, 1.0 - 1e-14);
+        const double cw = cm * (1.0 + 1e-15);
         bool need = false;
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             if (!((ps.valid >> p) & 1u)) continue;
-            // the sweep's rounding (a few ulp of O(1) terms) is covered by the 1e-14 / 1e-15 terms
-            const double g1 = fma(ps.la[p], am, ka[p]) * (1.0 + 1e-15);
-            const double gg = g1 * g1 * ps.r1[p];
-            const double db = (1.0 - fma(am, am, gg)) - 1e-14 * (1.0 + gg);
-            const double wb = fma(ka[p], ps.sa[p], fma(am, ps.wja[p], cm)) + 1e-15 * fma(g1, ps.sa[p], fma(am, ps.aw0, cm));
+            const double g1 = fma(ps.la[p], am, ka[p]);
+            const double db = fma(-g1 * g1, ps.r1[p], c1);
+            const double wb = fma(ka[p], ps.sa[p], fma(am, ps.wja[p], cw));
             const double q = fma(wb, wb, ps.bm[p]);
-            // NaN / inf (flagged rows) fail the comparison: needed
-            need |= !(db > 1e-6 && ps.kq[p] * db > q * F);
+            // NaN / inf (flagged rows) fail the comparisons: needed
+            need |= !(db > 1e-6 && fma(ps.kq[p], db, -q) > 0.0);
         }
         return __any_sync(L0S_FULL, need);
     };
@@ -531,14 +533,25 @@ __device__ __forceinline__ void fit3_sweep(const FitArgs& a, FitShared<NT>& S) {
             if (scr && !L0S_TSK_NOCALL) {
                 PairSlot0<P> ps;
                 const double wj0 = s_hu[0][0][lane];
-                ps.aw0 = fabs(wj0);
                 ps.valid = 0u;
                 ps.cand = 0u;
+                // slots 1..: B_t = 3 K_t Y2_t (1 + 2/d1_t) <= 6 (eta + gamma rho) Y2 (1 + 2/d1) with
+                // each factor's maximum over the slots (rho over the pair's j and k)
+                double etx = 0.0, gmx = 0.0, y2x = 0.0, rjx = 0.0;
+                bool fj = true;
+#pragma unroll
+                for (int t = 1; t < NT; ++t) {
+                    y2x = fmax(y2x, s_ts[0][t]);
+                    gmx = fmax(gmx, s_ts[1][t]);
+                    etx = fmax(etx, s_ts[2][t]);
+                    rjx = fmax(rjx, s_hu[t][1][lane]);
+                    fj = fj && isfinite(s_hu[t][0][lane]);
+                }
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
                     const int k = kbase + p;
-                    bool ok = true, fin = true;
-                    double bm = 0.0;
+                    bool ok = fj, fin = fj;
+                    double bm;
                     {
                         const double Y2 = s_ts[0][0];
                         const double cjk = HT ? Hb[(k - k0) * 32 + lane] : a.G[(int64_t)tord[0] * mp * mp + (int64_t)k * mp + j];
@@ -552,29 +565,32 @@ __device__ __forceinline__ void fit3_sweep(const FitArgs& a, FitShared<NT>& S) {
                         const double rh = fmax(s_hu[0][1][lane], s_hu[0][3][k - k0]);
                         task_bound_a0(3, s_ts[2][0], s_ts[1][0], rh, Y2, s_ts[3][0], trh, At, Bt, vk);
                         if (!(d1 > 0.0) || !(vk * (1.0 + 3.0 * trh) <= FO_LIM)) ok = false;
-                        if (cjk != cjk || ck != ck || wj0 != wj0) fin = false;
+                        if (!isfinite(cjk + ck + wj0)) fin = false;
                         bm = Bt;
-                        const double s1v = v1 * r1;
-                        ps.la[p] = fabs(cjk);
-                        ps.sa[p] = fabs(s1v);
-                        ps.wja[p] = fabs(fma(-cjk, s1v, wj0));
-                        ps.r1[p] = r1;
-                        ps.kq[p] = (NT == 1) ? (base - At) - wc.theta : ((base - At) - wc.theta) * shrink;
+                        const double s1v = v1 * r1, la = fabs(cjk), sa = fabs(s1v);
+                        // the sweep's rounding folded in (PairSlot0; a few ulp of O(1) terms)
+                        ps.la[p] = la;
+                        ps.sa[p] = sa * (1.0 + 2e-15);
+                        ps.wja[p] = fabs(fma(-cjk, s1v, wj0)) + 1e-15 * fma(la, sa, fabs(wj0));
+                        ps.r1[p] = r1 * (1.0 + 2e-14);
+                        const double kq = (NT == 1) ? (base - At) - wc.theta : ((base - At) - wc.theta) * shrink;
+                        ps.kq[p] = kq * (1.0 / ((1.0 + 4.0 * kRcpRel) * (1.0 + 1e-12)));
                     }
+                    if (NT > 1) {
+                        double dmin = 1.0, rkx = 0.0;
 #pragma unroll
-                    for (int t = 1; t < NT; ++t) {
-                        const double cjk = HT ? Hb[t * HS + (k - k0) * 32 + lane] : a.G[(int64_t)tord[t] * mp * mp + (int64_t)k * mp + j];
-                        const double ck = s_hu[t][2][k - k0], wj = s_hu[t][0][lane];
-                        const double d1 = fma(-cjk, cjk, 1.0);
+                        for (int t = 1; t < NT; ++t) {
+                            const double cjk = HT ? Hb[t * HS + (k - k0) * 32 + lane] : a.G[(int64_t)tord[t] * mp * mp + (int64_t)k * mp + j];
+                            dmin = fmin(dmin, fma(-cjk, cjk, 1.0));
+                            rkx = fmax(rkx, s_hu[t][3][k - k0]);
+                            if (!isfinite(cjk + s_hu[t][2][k - k0])) fin = false;
+                        }
                         // 1/d1 from above: d1 rounded down to float, its reciprocal rounded up (0 or
                         // denormal: inf, the pair is then never retired)
-                        const double trh = 2.0 * (double)__frcp_ru(__double2float_rd(d1));
-                        double At, Bt, vk;
-                        const double rh = fmax(s_hu[t][1][lane], s_hu[t][3][k - k0]);
-                        task_bound_a0(3, s_ts[2][t], s_ts[1][t], rh, s_ts[0][t], s_ts[3][t], trh, At, Bt, vk);
-                        if (!(d1 > 0.0) || !(vk * (1.0 + 3.0 * trh) <= FO_LIM)) ok = false;
-                        if (cjk != cjk || ck != ck || wj != wj) fin = false;
-                        bm = fmax(bm, Bt);
+                        const double rup = (double)__frcp_ru(__double2float_rd(dmin));
+                        const double kx = 2.0 * fma(gmx, fmax(rjx, rkx), etx) * (1.0 + 1e-12);
+                        bm = fmax(bm, 3.0 * kx * y2x * (1.0 + 2.0 * rup) * (1.0 + 1e-12));
+                        if (!(dmin > 0.0)) ok = false;
                     }
                     ps.bm[p] = fmax(bm, 1e-300);
                     if (j < k && k < m && fin) ps.valid |= 1u << p;

@@ -198,18 +198,27 @@ __device__ __forceinline__ double hist_theta(const FitArgs& a, int lane) {
     const unsigned hit = __ballot_sync(L0S_FULL, inc >= (unsigned)a.kc);
     if (!hit) return INFINITY;
     const int L = __ffs(hit) - 1;
-    double th = INFINITY;
-    if (lane == L) {
-        unsigned c = inc - sum;
-        for (int x = 0; x < PER; ++x) {
-            c += __ldcg(h + x);
-            if (c >= (unsigned)a.kc) {
-                th = hist_upper(lane * PER + x, a.hist_base);
-                break;
-            }
+    // lane L's bins again, spread over the warp (two per lane) and scanned: the first bin where the
+    // running count reaches kc (counts only grow, so the re-read total still reaches it)
+    static_assert(PER <= 64, "two bins per lane");
+    const unsigned before = __shfl_sync(L0S_FULL, inc - sum, L);
+    const unsigned* hL = a.hist + L * PER;
+    unsigned s0 = lane < PER ? __ldcg(hL + lane) : 0u;
+    unsigned s1 = lane + 32 < PER ? __ldcg(hL + 32 + lane) : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v0 = __shfl_up_sync(L0S_FULL, s0, o), v1 = __shfl_up_sync(L0S_FULL, s1, o);
+        if (lane >= o) {
+            s0 += v0;
+            s1 += v1;
         }
     }
-    return __shfl_sync(L0S_FULL, th, L);
+    s1 += __shfl_sync(L0S_FULL, s0, 31);
+    const unsigned h0 = __ballot_sync(L0S_FULL, before + s0 >= (unsigned)a.kc);
+    const unsigned h1 = __ballot_sync(L0S_FULL, lane + 32 < PER && before + s1 >= (unsigned)a.kc);
+    if (h0) return hist_upper(L * PER + __ffs(h0) - 1, a.hist_base);
+    if (h1) return hist_upper(L * PER + 32 + __ffs(h1) - 1, a.hist_base);
+    return INFINITY;
 }
 
 // Collect modes: append the warp's buffer to the global candidate list (collect == 2, the
