@@ -51,6 +51,10 @@ F_TASK = {2: 29, 3: 54, 4: 90}
 # accumulate are FMAs (2 flops each), e1 a multiply (1), and the row's D and V (2 FMAs) are shared
 # by the P = 4 pairs of a thread (1 flop per evaluation) -> 5*2 + 1 + 1 = 12
 FLOP_PER_EVAL = 12
+# fp64 flops of one tile-screen test (fit3.cu tile_screen, one warp): per pair g1 (FMA), g1^2 (MUL),
+# d_min, w_max (2 FMAs), q and the test (FMAs) = 13, times P = 4 pairs, plus 3 per tile row set,
+# times 32 lanes
+FLOP_PER_TEST = 32 * (4 * 13 + 3)
 METRIC = "l0 tuples fitted/sec at dim 3 (1/2/4/8 B200, % FP64 roofline) vs CPU ref"
 
 
@@ -206,7 +210,7 @@ def random_y_line(eng, vd, pd, bounds, args, local):
         sc, rk, _, _, st = eng.search(N_DIM, 10, 0, total, "fast")
         ms.append(st.ms_gram + st.ms_total)
         fit.append(st.ms_fit / max(1, st.n_fit_launches))
-        ev.append(st.n_eval / max(1, st.n_fit_launches))
+        ev.append((st.n_eval * FLOP_PER_EVAL + st.n_screen * FLOP_PER_TEST) / FLOP_PER_EVAL / max(1, st.n_fit_launches))
     peak = eng.fp64_peak()
     loose, ozaki = eng.stage_loose_rows(), eng.stage_info()[1]
     f = statistics.mean(fit)
@@ -398,7 +402,7 @@ def main():
     for _ in range(args.warmup):
         device_step()
     barrier()
-    ms_steps, fit_ms, gram_ms, eval_counts, launches = [], [], [], [], 0
+    ms_steps, fit_ms, gram_ms, eval_counts, screen_counts, launches = [], [], [], [], [], 0
     # the fused staging pass for the property row and for the features (2 x k_stage_rows), the
     # INT8 Gram (k_oz_gemm, k_oz_eta, k_oz_fixup), the unit diagonal and 5 feature-flag kernels
     stage_launches = 11
@@ -410,6 +414,7 @@ def main():
             gram_ms.append(st.ms_gram_kernel)
             fit_ms.append(st.ms_fit / max(1, st.n_fit_launches))
             eval_counts.append(st.n_eval / max(1, st.n_fit_launches))
+            screen_counts.append(st.n_screen / max(1, st.n_fit_launches))
             stage_ms = eng.stage_timings()
             launches += int(st.n_launches) + stage_launches
         barrier()
@@ -483,7 +488,8 @@ def main():
     # FLOP_PER_EVAL fp64 flops (module docstring); the algorithmic count of SURVEY 8(d) (216 per
     # tuple at T = 4, a full normal-equations solve per task) is reported beside it as a search rate
     evals = statistics.mean(eval_counts)
-    achieved = evals * FLOP_PER_EVAL / (fit_avg * 1e-3) / 1e12
+    tests = statistics.mean(screen_counts)
+    achieved = (evals * FLOP_PER_EVAL + tests * FLOP_PER_TEST) / (fit_avg * 1e-3) / 1e12
     algorithmic = (total // world) * T * F_TASK[N_DIM] / (fit_avg * 1e-3) / 1e12
     gram_avg = statistics.mean(gram_ms) if gram_ms and min(gram_ms) > 0 else None
     traffic, pipe, prof_src = profile_figures()
@@ -496,16 +502,19 @@ def main():
                    "l2": "inputs (160 MB) and Gram (128 MB) exceed the 126 MB L2"},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_fit3<4>", "work": f"{evals:.4g} (tuple, task) bound evaluations per launch "
-                                                   f"x {FLOP_PER_EVAL} fp64 flops (counted on the device)",
+                     "kernel": "k_fit3<4> (tile-screened sweep)",
+                     "work": f"{evals:.4g} (tuple, task) bound evaluations x {FLOP_PER_EVAL} fp64 flops + "
+                             f"{tests:.4g} tile-screen tests x {FLOP_PER_TEST} per launch (counted on the device)",
                      "peak_source": "FP64 DFMA microbenchmark measured in this run (l0s_fp64_peak; "
                                     "MEASURED_PEAKS.json has no FP64 entry); datasheet 37 TF/s",
                      "physical_fp64_pipe_frac": pipe, "profile": prof_src,
                      "search_rate_algorithmic_tflops": algorithmic,
                      "note": "search_rate_algorithmic_tflops = SURVEY 8(d)'s normal-equations flops (216 per tuple "
                              "at T=4) for every tuple / fit time: a search rate, not work done -- the sweep hoists "
-                             "the (j,k) block and prunes row groups after their first task (evaluations per tuple "
-                             f"{evals / (total // world):.3f} of {T})"},
+                             "the (j,k) block, retires whole i-tiles by a row-block bound (tile screen) and prunes "
+                             "row groups after their first task (evaluations per tuple "
+                             f"{evals / (total // world):.4f} of {T}); with the screen the sweep is bound by its "
+                             "per-unit latency (hoist, threshold scan, barriers), not the FP64 pipe"},
         "roofline_gram": gram_roofline(eng, gram_avg),
         "roofline_stage": stage_roofline(stage_ms),
         "random_y": random_y,

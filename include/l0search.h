@@ -74,6 +74,8 @@ typedef struct {
                                 SearchStats.seconds like the reference's per-model fit_tuple)    */
     int64_t n_eval;          /* task-tuple evaluations the screened sweep executed (one (i, j, k, task)
                                 bound term; the physical work behind the roofline)             */
+    int64_t n_screen;        /* tile-screen tests of the n = 3 sweep (one warp: 32 j x P pairs bounded
+                                over a group of i-tiles or one tile; fit3.cu tile_screen)      */
 } l0s_stats;
 
 const char *l0s_last_error(void);

@@ -62,6 +62,7 @@ class Stats(ctypes.Structure):
         ("ms_gram_kernel", ctypes.c_double),
         ("ms_records", ctypes.c_double),
         ("n_eval", ctypes.c_int64),
+        ("n_screen", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

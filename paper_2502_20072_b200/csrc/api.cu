@@ -1342,7 +1342,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     const int slots = grid * (n == 3 ? fit3_slots_per_cta(c->T) : fit_slots_per_cta());
     const int64_t ill_cap = (int64_t)1 << 26;  // 512 MB of ranks; overflow is reported, never dropped
     CK(c->ucount.ensure(sizeof(int) * 4));
-    CK(c->n_eval.ensure(sizeof(unsigned long long)));
+    CK(c->n_eval.ensure(2 * sizeof(unsigned long long)));  // [0] evaluations, [1] tile-screen tests
     CK(c->theta_g.ensure(sizeof(unsigned long long)));
     CK(c->hist.ensure(sizeof(unsigned) * HIST_BINS));
     CK(c->seedbuf.ensure(sizeof(int64_t) * 1024 * (kSeedW + 1) + 256));  // subsets, bounds, count, cap
@@ -1389,7 +1389,11 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     a.seed_n = reinterpret_cast<int*>(c->seedbuf.as<double>() + 1024 * (kSeedW + 1));
     a.seed_cap = c->seedbuf.as<double>() + 1024 * (kSeedW + 1) + 4;
     a.keep = (int)keep;
-    if (n == 3 && (c->m + 7) / 8 <= 65535) {  // the sweep's tile screen (fit3.cu: k_tile_max)
+    static const bool tsk_off = [] {  // L0S_TILE_SCREEN=0: the plain sweep only (tests, experiments)
+        const char* e = getenv("L0S_TILE_SCREEN");
+        return e && e[0] == '0';
+    }();
+    if (n == 3 && !tsk_off && (c->m + 7) / 8 <= 65535) {  // the sweep's tile screen (fit3.cu: k_tile_max)
         const int64_t nt = fit3_tmax_doubles(c->m, c->mp);
         if (nt > 0) {
             CK(c->tmax.ensure(sizeof(double) * nt));
@@ -1408,9 +1412,10 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     a.ill_cnt = c->ill_cnt.as<unsigned long long>();
     a.ill_cap = ill_cap;
     a.n_eval = c->n_eval.as<unsigned long long>();
+    a.n_screen = c->n_eval.as<unsigned long long>() + 1;
 
     CK(cudaMemsetAsync(c->ucount.p, 0, sizeof(int) * 4, c->st));
-    CK(cudaMemsetAsync(c->n_eval.p, 0, sizeof(unsigned long long), c->st));
+    CK(cudaMemsetAsync(c->n_eval.p, 0, 2 * sizeof(unsigned long long), c->st));
     CK(cudaMemcpyAsync(c->theta_g.p, &inf_enc, sizeof inf_enc, cudaMemcpyHostToDevice, c->st));
     static const double inf_d = INFINITY;
     CK(cudaMemcpyAsync(a.seed_cap, &inf_d, sizeof inf_d, cudaMemcpyHostToDevice, c->st));
@@ -1431,9 +1436,10 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     // the candidate set: the gathered warp lists, or (large keep) the global collect list
     double* cl = big ? c->coll_lb.as<double>() : c->cand_lb.as<double>();
     int64_t* cr = big ? c->coll_rank.as<int64_t>() : c->cand_rank.as<int64_t>();
-    unsigned long long ncand = 0, nill = 0, th_enc = 0, nev = 0;
+    unsigned long long ncand = 0, nill = 0, th_enc = 0, nev = 0, nscr = 0;
     double seed_cap = INFINITY;
     CK(cudaMemcpyAsync(&nev, c->n_eval.p, sizeof nev, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(&nscr, c->n_eval.as<unsigned long long>() + 1, sizeof nscr, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(&seed_cap, a.seed_cap, sizeof seed_cap, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(&ncand, big ? c->coll_cnt.p : c->cand_cnt.p, sizeof ncand, cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(&nill, c->ill_cnt.p, sizeof nill, cudaMemcpyDeviceToHost, c->st));
@@ -1441,6 +1447,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
     CK(cudaStreamSynchronize(c->st));
     st->ms_fit += elapsed(c->ev[2], c->ev[3]);
     st->n_eval += (int64_t)nev;
+    st->n_screen += (int64_t)nscr;
     st->theta = ord_dec(th_enc);
     if ((int64_t)nill > ill_cap)
         return fail(L0S_ECAPACITY, "%llu ill-conditioned tuples exceed the routing buffer (%lld)",
@@ -1582,9 +1589,11 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
         unsigned long long ncoll = 0;
         CK(cudaMemcpyAsync(&ncoll, c->coll_cnt.p, sizeof ncoll, cudaMemcpyDeviceToHost, c->st));
         CK(cudaMemcpyAsync(&nev, c->n_eval.p, sizeof nev, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(&nscr, c->n_eval.as<unsigned long long>() + 1, sizeof nscr, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));
         st->ms_fit += elapsed(c->ev[2], c->ev[3]);
-        st->n_eval = (int64_t)nev;  // the counter accumulates over both sweeps
+        st->n_eval = (int64_t)nev;  // the counters accumulate over both sweeps
+        st->n_screen = (int64_t)nscr;
         if ((int64_t)ncoll > coll_cap)
             return fail(L0S_ECAPACITY, "%llu tuples below the certification threshold exceed the rescan buffer",
                         (unsigned long long)ncoll);

@@ -271,6 +271,7 @@ __device__ __noinline__ void tile_screen(const FitArgs& a, const PairSlot0<P> ps
         }
         return __any_sync(L0S_FULL, need);
     };
+    unsigned tests = 0;
     for (int wd = 0; wd * 32 < nib; ++wd) {
         unsigned word = all ? ~0u : 0u;
         if (!all) {
@@ -303,10 +304,12 @@ __device__ __noinline__ void tile_screen(const FitArgs& a, const PairSlot0<P> ps
                 double ka[P];
 #pragma unroll
                 for (int p = 0; p < P; ++p) ka[p] = __shfl_sync(L0S_FULL, gk[p], 4 * g);
+                ++tests;
                 if (!needs(__shfl_sync(L0S_FULL, gam, 4 * g), __shfl_sync(L0S_FULL, gcm, 4 * g), ka)) continue;
                 for (int bb = 4 * g; bb < min(4 * g + 4, nt); ++bb) {
 #pragma unroll
                     for (int p = 0; p < P; ++p) ka[p] = __shfl_sync(L0S_FULL, kmx[p], bb);
+                    ++tests;
                     if (needs(__shfl_sync(L0S_FULL, amx, bb), __shfl_sync(L0S_FULL, cmx, bb), ka)) word |= 1u << bb;
                 }
             }
@@ -316,6 +319,7 @@ __device__ __noinline__ void tile_screen(const FitArgs& a, const PairSlot0<P> ps
             atomicOr(&need_cta[wd], word);
         }
     }
+    if (lane == 0 && tests && a.n_screen) atomicAdd(a.n_screen, (unsigned long long)tests);
 }
 
 // The sweep's static shared state (one instance per CTA, whichever instantiation runs).

@@ -332,6 +332,7 @@ int l0s_group_search(l0s_group* g, int n, int64_t keep, int mode, double* out_sc
             a.ms_gram_kernel = std::max(a.ms_gram_kernel, b.ms_gram_kernel);
             a.ms_records = std::max(a.ms_records, b.ms_records);
             a.n_eval += b.n_eval;
+            a.n_screen += b.n_screen;
         }
         a.n_tuples = total;  // parts of one search (screened parts each report the whole range)
         *stats = a;

@@ -257,6 +257,7 @@ struct FitArgs {
     // of the sweep's tile height: [col <= m][block] max |C[i, col]| (col = m: max |c_i|; +inf for a
     // flagged or NaN row), [j-block][block], then the slot's task index (fit3.cu: k_tile_max)
     double* tmax = nullptr;
+    unsigned long long* n_screen = nullptr;  // out (optional): tile-screen tests (warp-level)
 };
 // doubles fit3_launch needs in FitArgs::tmax for an m-feature problem
 int64_t fit3_tmax_doubles(int64_t m, int64_t mp);

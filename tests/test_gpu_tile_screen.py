@@ -1,0 +1,145 @@
+"""The dim-3 sweep's tile screen (fit3.cu: k_tile_max + tile_screen) changes which i-tiles are
+swept, never the answer: the screened search returns the plain sweep's models bit for bit.
+
+Each case runs in two subprocesses, one with the screen (default) and one with
+L0S_TILE_SCREEN=0 (read once per process by api.cu; the plain sweep is the one the oracle tests
+pin).  Cases cover every task-slot template the screen instantiates (tile heights 32 / 24 /
+16), planted and random properties, near-duplicate features (|C_ij| ~ 1 off the diagonal, the
+case the block maxima must not hide), a feature whose rho exceeds rho_cap (iforce rows), keep
+beyond the per-warp lists (collect mode 2) and a search split in rank ranges.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+from paper_2502_20072_b200 import _lib
+from math import comb
+
+def case():
+    rng = np.random.default_rng({seed})
+    m, s, T, kind = {m}, {s}, {T}, {kind!r}
+    v = rng.uniform(0.5, 2.0, size=(m, s))
+    if kind == "dup":
+        for c in range(6):
+            v[m - 1 - c] = v[c] + [1e-3, 1e-6, 1e-9, 1e-12, 0.0, 1e-4][c] * rng.standard_normal(s)
+    if kind == "offset":  # large means: rho above rho_cap for a few features (iforce rows)
+        v[5] += 1e4
+        v[77 % m] += 3e3
+    y = np.empty(s)
+    sl = [np.arange(t, s, T) for t in range(T)]
+    for t, x in enumerate(sl):
+        if kind == "random":
+            y[x] = rng.standard_normal(len(x))
+        else:
+            y[x] = (2.0 + 0.5 * t) * v[3, x] - (1.0 + 0.25 * t) * v[m // 2, x] + 0.5 * v[m - 9, x] + 0.75 \
+                + 0.01 * rng.standard_normal(len(x))
+    return v, y, sl
+
+v, y, sl = case()
+m, s = v.shape
+perm = np.concatenate(sl)
+bounds = np.cumsum([0] + [len(x) for x in sl])
+eng = _lib.engine(0)
+eng.stage(v, y, perm, bounds, "fp64")
+out = []
+total = comb(m, 3)
+for keep, lo, hi in {runs}:
+    hi = total if hi is None else hi
+    sc, rk, coef, ssr, st = eng.search(3, keep, lo, hi, "fast")
+    out.append({{"ranks": [int(x) for x in rk], "scores": [float(x).hex() for x in sc],
+                 "coef": [float(x).hex() for x in np.asarray(coef).ravel()],
+                 "certified": int(st.certified), "n_eval": int(st.n_eval), "n_screen": int(st.n_screen)}})
+print(json.dumps(out))
+"""
+
+CASES = {
+    # name: (m, s, T, kind, seed)
+    "planted_t4": (400, 2400, 4, "planted", 11),
+    "planted_t1": (300, 1500, 1, "planted", 12),
+    "random_t1": (300, 1500, 1, "random", 13),
+    "planted_t2": (350, 1800, 2, "planted", 14),
+    "planted_t6": (260, 3000, 6, "planted", 15),
+    "random_t4": (200, 1600, 4, "random", 16),
+    "dup_t4": (300, 2000, 4, "dup", 17),
+    "offset_t3": (240, 1500, 3, "offset", 18),
+}
+RUNS = [(10, 0, None), (200, 0, None), (10, 12345, 987654)]
+
+
+def _run(name, screen: bool):
+    m, s, T, kind, seed = CASES[name]
+    code = _SCRIPT.format(root=ROOT, seed=seed, m=m, s=s, T=T, kind=kind, runs=RUNS)
+    env = dict(os.environ)
+    env.pop("L0S_TILE_SCREEN", None)
+    if not screen:
+        env["L0S_TILE_SCREEN"] = "0"
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_tile_screen_matches_plain_sweep(name):
+    on, off = _run(name, True), _run(name, False)
+    for a, b in zip(on, off):
+        assert a["certified"] == 1 and b["certified"] == 1
+        assert a["ranks"] == b["ranks"]
+        assert a["scores"] == b["scores"]
+        assert a["coef"] == b["coef"]
+        assert b["n_screen"] == 0
+    if CASES[name][3] == "planted":
+        # the screen engaged and retired work on the planted cases (keep 10, whole range)
+        assert on[0]["n_screen"] > 0 and on[0]["n_eval"] < off[0]["n_eval"]
+
+
+def test_tile_screen_c3_planted_and_random():
+    """At C3's full size (bench workload) the screened and plain sweeps agree on the top 10 for the
+    planted and the random property."""
+    code = r"""
+import json, sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, {root!r} + "/tests")
+import numpy as np
+from math import comb
+import scale_cases
+from paper_2502_20072_b200 import _lib
+from paper_2502_20072_b200.search import _partition
+res = []
+for variant in ("planted", "random"):
+    v, y, sl = scale_cases.c3(variant)
+    perm, bounds, _ = _partition(v.shape[1], sl)
+    eng = _lib.engine(0)
+    eng.stage(v, y, perm, bounds, "fp64")
+    sc, rk, coef, ssr, st = eng.search(3, 10, 0, comb(v.shape[0], 3), "fast")
+    res.append({{"ranks": [int(x) for x in rk], "scores": [float(x).hex() for x in sc], "n_screen": int(st.n_screen),
+                 "certified": int(st.certified)}})
+print(json.dumps(res))
+""".format(root=ROOT)
+    outs = []
+    for screen in (True, False):
+        env = dict(os.environ)
+        env.pop("L0S_TILE_SCREEN", None)
+        if not screen:
+            env["L0S_TILE_SCREEN"] = "0"
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    on, off = outs
+    for a, b in zip(on, off):
+        assert a["certified"] == b["certified"] == 1
+        assert a["ranks"] == b["ranks"] and a["scores"] == b["scores"]
+    assert on[0]["n_screen"] > 0  # planted: screened
+    assert on[1]["n_screen"] == 0  # random y over 4 tasks: the threshold stays above the first slot's |y_c|^2
