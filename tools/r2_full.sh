@@ -13,11 +13,14 @@ if [ -z "${SKIP_TESTS:-}" ]; then
   timeout 1800 python -m pytest tests -m gpu -q --timeout 1200 -p no:cacheprovider --durations=10 > gpurun_out/${tag}_tests.log 2>&1
   echo "tests rc=$?"; grep -E "passed|failed|FAILED|Error" gpurun_out/${tag}_tests.log | tail -8
 fi
+# planted y: the tile-screened sweep k_fit3<4, true>; random y: the plain sweep k_fit3<4, false> (the screened
+# kernel's CTAs exit at once there -- fit3.cu, k_fit3)
 for y in planted random; do
-  L0S_TUNE_Y=$y timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_fit3 -s 2 -c 1 -f \
+  if [ $y = planted ]; then kre='regex:k_fit3.*bool.1'; kname='k_fit3<4, true> (tile screen)'; else kre='regex:k_fit3.*bool.0'; kname='k_fit3<4, false>'; fi
+  L0S_TUNE_Y=$y timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "$kre" -s 1 -c 1 -f \
       -o gpurun_out/${tag}_fit3_${y} python tools/tune_fit.py one > gpurun_out/${tag}_fit3_${y}.log 2>&1
   echo "fit3 $y rc=$?"
-  python tools/ncu_summary.py gpurun_out/${tag}_fit3_${y}.ncu-rep "${tag} (${commit}): k_fit3<4> on C3, ${y} y" > gpurun_out/${tag}_fit3_${y}_ncu.txt
+  python tools/ncu_summary.py gpurun_out/${tag}_fit3_${y}.ncu-rep "${tag} (${commit}): ${kname} on C3, ${y} y" > gpurun_out/${tag}_fit3_${y}_ncu.txt
   ncu -i gpurun_out/${tag}_fit3_${y}.ncu-rep --page source --csv --print-source sass > gpurun_out/${tag}_fit3_${y}_src.csv 2>/dev/null
   python tools/ncu_blocks.py gpurun_out/${tag}_fit3_${y}_src.csv 12 > gpurun_out/${tag}_fit3_${y}_blocks.txt 2>&1
   grep -E "duration|FP64 pipe|occupancy|issue active" gpurun_out/${tag}_fit3_${y}_ncu.txt
