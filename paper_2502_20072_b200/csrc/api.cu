@@ -1393,7 +1393,7 @@ static int search_fast_mode(l0s_ctx* c, int n, int64_t keep, int64_t rb, int64_t
         const char* e = getenv("L0S_TILE_SCREEN");
         return e && e[0] == '0';
     }();
-    if (n == 3 && !tsk_off && (c->m + 7) / 8 <= 65535) {  // the sweep's tile screen (fit3.cu: k_tile_max)
+    if ((n == 3 || n == 4) && !tsk_off && (c->m + 7) / 8 <= 65535) {  // the sweeps' tile screen (k_tile_max)
         const int64_t nt = fit3_tmax_doubles(c->m, c->mp);
         if (nt > 0) {
             CK(c->tmax.ensure(sizeof(double) * nt));

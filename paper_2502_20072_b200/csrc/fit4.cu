@@ -98,13 +98,98 @@ __device__ __noinline__ int eval_tuple4(const FitArgs& a, int64_t i, int64_t j, 
     return (cond ? 1 : 0) | (rank_ok ? 2 : 0);
 }
 
-template <int NT>
+// Tile screen of the n = 4 sweep (fit3.cu's TSK, one task slot t0 -- the task of largest |y_c|^2,
+// whose row-block maxima k_tile_max holds): with a = max |C_ij| (j-block), b_k = max |C_ik|,
+// b_l = max |C_il_p|, c = max |c_i| over an i-tile,
+//   |g1| <= G1 = b_k + |L10| a,  |g2| <= G2 = b_l + |L20| a + |L21| G1,
+//   d >= 1 - a^2 - G1^2 / d1 - G2^2 / d2,  |w| <= c + a |c_j| + G1 |s1| + G2 |s2|,
+// and a tile is retired for the warp when (K0 - theta) d_min > (w_max^2 + Bm)(1 + 4 kRcpRel) for
+// every valid, unforced pair: every tuple of it has t0's share of the pooled bound at or above
+// the threshold (the pooled SSR is at least that share: every task's SSR is >= 0).  Lanes gather
+// the maxima of tile `lane` (a unit holds at most 128 rows); returns this warp's need bits.
+struct Slot4 {
+    double la10, rd1, as1, aw0;  // |L10|, 1/d1 (1 + 2e-14), |s1|, |c_j| of slot t0
+};
+template <int P, int IB>
+__device__ __noinline__ unsigned tile_screen4(const FitArgs& a, const Slot4 h, const double (&l20)[P],
+                                              const double (&l21)[P], const double (&rd2)[P], const double (&as2)[P],
+                                              const double (&kq)[P], const double (&bm)[P], unsigned valid,
+                                              unsigned cand, int lane, int jb, int k, int lbase, int i_lo, int i_hi,
+                                              int nib) {
+    const int64_t m = a.m;
+    if (__any_sync(L0S_FULL, (valid & ~cand) != 0u)) return (nib >= 32) ? ~0u : ((1u << nib) - 1u);
+    const int nbk = (int)((m + IB - 1) / IB);
+    const double* MT = a.tmax;
+    const double* MJ = a.tmax + (m + 1) * nbk + (int64_t)jb * nbk;
+    double amx = 0.0, bkx = 0.0, cmx = 0.0, blx[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) blx[p] = 0.0;
+    if (lane < nib) {
+        const int r0 = i_lo + lane * IB, r1 = min(r0 + IB, i_hi);
+        for (int b = r0 / IB; b <= (r1 - 1) / IB; ++b) {
+            amx = fmax(amx, MJ[b]);
+            bkx = fmax(bkx, MT[(int64_t)k * nbk + b]);
+            cmx = fmax(cmx, MT[m * nbk + b]);
+#pragma unroll
+            for (int p = 0; p < P; ++p) blx[p] = fmax(blx[p], MT[(int64_t)(lbase + p < m ? lbase + p : m - 1) * nbk + b]);
+        }
+    }
+    unsigned word = 0u;
+    for (int bb = 0; bb < nib; ++bb) {
+        const double am = __shfl_sync(L0S_FULL, amx, bb), bk = __shfl_sync(L0S_FULL, bkx, bb);
+        const double cm = __shfl_sync(L0S_FULL, cmx, bb);
+        const double G1 = fma(h.la10, am, bk) * (1.0 + 1e-15);
+        const double c1 = fma(-G1 * G1, h.rd1, fma(-am, am, 1.0 - 1e-14));
+        const double w1 = fma(G1, h.as1, fma(am, h.aw0, cm));
+        bool need = false;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const double bl = __shfl_sync(L0S_FULL, blx[p], bb);
+            if (!((valid >> p) & 1u)) continue;
+            const double G2 = fma(fabs(l21[p]), G1, fma(fabs(l20[p]), am, bl)) * (1.0 + 1e-15);
+            const double db = fma(-G2 * G2, rd2[p], c1);
+            const double wb = fma(G2, as2[p], w1) * (1.0 + 1e-14);
+            const double q = fma(wb, wb, bm[p]);
+            need |= !(db > 1e-6 && fma(kq[p], db, -q) > 0.0);
+        }
+        if (__any_sync(L0S_FULL, need)) word |= 1u << bb;
+    }
+    return word;
+}
+
+#ifndef L0S_TSK4
+#define L0S_TSK4 1
+#endif
+constexpr bool TSK4 = L0S_TSK4;
+// SCR: the screened instantiation (launched first; each CTA runs the one its threshold selects,
+// as in fit3.cu's k_fit3).
+template <int NT, bool SCR>
 __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs a) {
     using C = Cfg4<NT>;
     constexpr int P = C::P, IB = C::IB, TS = C::TS, BS = C::BS, LSPAN = C::LSPAN;
     extern __shared__ __align__(16) double sm[];
     __shared__ int s_unit;
     __shared__ unsigned char s_force[2][IB];
+    __shared__ unsigned s_need;
+    __shared__ int s_use;
+    int t0 = -1;                      // SCR: the screened task slot
+    unsigned long long n_tests = 0;   // SCR: tile tests of this warp (flushed at the end)
+    if constexpr (TSK4) {
+        if (threadIdx.x == 0) {
+            double y2 = 0.0;
+            for (int t = 0; t < a.T; ++t) y2 = fmax(y2, a.G[(int64_t)t * a.mp * a.mp + a.m * a.mp + a.m]);
+            const double th = a.collect == 1 ? a.theta0 : ord_dec(*(volatile unsigned long long*)a.theta_g);
+            int tt = -1;
+            if (a.tmax) {
+                const int64_t nbk = (a.m + IB - 1) / IB;
+                tt = (int)a.tmax[(a.m + 1 + (a.m + 31) / 32) * nbk];
+            }
+            s_use = (a.tmax != nullptr && th < y2 && tt >= 0 && tt < NT) ? tt : -1;
+        }
+        __syncthreads();
+        if ((s_use >= 0) != SCR) return;
+        t0 = s_use;
+    }
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     double* sKraw = sm + 2 * BS + 2 * NW * CAP_WIDE + tid * P;
     const int64_t m = a.m, mp = a.mp;
@@ -161,6 +246,7 @@ __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs
         // ---------------- hoist ----------------
         double L10[NT], rd1[NT], s1[NT], w0[NT];
         double L20[P][NT], L21[P][NT], rd2[P][NT], s2[P][NT], Kq[P], Bm[P];
+        double K0[SCR ? P : 1];  // SCR: slot t0's share of the bound, base_t0 - A_t0
         unsigned valid = 0, bad = 0, forced = 0;
         const int jj = j < m ? j : (int)m - 1;
 #pragma unroll
@@ -187,6 +273,9 @@ __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs
                 rd2[p][t] = h.rd2;
                 s2[p][t] = h.s2;
                 kr += h.base - At;
+                if constexpr (SCR) {
+                    if (t == t0) K0[p] = h.base - At;
+                }
                 bm = fmax(bm, Bt);
                 if (!(h.d1 > 0.0) || !(h.d2 > 0.0) || !(vk * (1.0 + 4.0 * h.tr3) <= FO_LIM)) isbad = true;
                 // dead features (NaN Gram rows) drop the pair; a NaN produced by a near-singular
@@ -210,13 +299,67 @@ __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs
         };
         set_kq();
 
-        // ---------------- sweep i ----------------
+        // ---------------- tile screen (SCR) ----------------
         const int nib = (i_hi - i_lo + IB - 1) / IB;
-        for (int bi = 0; bi < nib; ++bi) {
-            const int buf = bi & 1;
+        unsigned wneed = ~0u, cneed = ~0u;  // this warp's / the CTA's needed tiles
+        if constexpr (SCR) {
+            if (tid == 0) s_need = 0u;
+            __syncthreads();
+            if (nib <= 32) {
+                Slot4 h4;
+                double l20[P], l21[P], r2[P], a2[P], kq[P];
+                unsigned cand = 0u;
+#pragma unroll
+                for (int t = 0; t < NT; ++t)
+                    if (t == t0) {
+                        h4.la10 = fabs(L10[t]);
+                        h4.rd1 = rd1[t] * (1.0 + 2e-14);
+                        h4.as1 = fabs(s1[t]);
+                        h4.aw0 = fabs(w0[t]);
+#pragma unroll
+                        for (int p = 0; p < P; ++p) {
+                            l20[p] = L20[p][t];
+                            l21[p] = L21[p][t];
+                            r2[p] = rd2[p][t] * (1.0 + 2e-14);
+                            a2[p] = fabs(s2[p][t]);
+                        }
+                    }
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const double x = (NT == 1) ? Kq[p] : (K0[p] - wc.theta) * shrink;
+                    kq[p] = x * (1.0 / ((1.0 + 4.0 * kRcpRel) * (1.0 + 1e-12)));
+                    if (!((forced >> p) & 1u) && kq[p] > 0.0) cand |= 1u << p;
+                }
+                wneed = tile_screen4<P, IB>(a, h4, l20, l21, r2, a2, kq, Bm, valid, cand, lane, U.x & 0xffff, k,
+                                            lbase, i_lo, i_hi, nib);
+                n_tests += (unsigned long long)nib;
+            }
+            if (lane == 0) atomicOr(&s_need, wneed);
+            __syncthreads();
+            cneed = __reduce_or_sync(L0S_FULL, s_need);  // (warp-uniform for the compiler)
+        }
+        // needed tiles in order; tile 0 was staged before the hoist
+        auto next_tile = [&](int b) -> int {
+            if constexpr (SCR) {
+                const unsigned mk = b >= 32 ? 0u : (cneed & (~0u << b));
+                return (b < 32 && mk) ? (__ffs(mk) - 1) : nib;
+            } else {
+                return b;
+            }
+        };
+        int bi = next_tile(0);
+        if (SCR && bi != 0) {
+            cp_async_wait<0>();  // tile 0's copies land before buffer 0 is refilled
+            __syncthreads();
+            if (bi < nib) load_tiles(0, i_lo + bi * IB, j0, k, l0);
+        }
+
+        // ---------------- sweep i ----------------
+        for (int buf = 0; bi < nib; buf ^= 1) {
             const int ib0 = i_lo + bi * IB;
-            if (bi + 1 < nib) {
-                load_tiles(buf ^ 1, ib0 + IB, j0, k, l0);
+            const int bn = next_tile(bi + 1);
+            if (bn < nib) {
+                load_tiles(buf ^ 1, i_lo + bn * IB, j0, k, l0);
                 cp_async_wait<1>();
             } else {
                 cp_async_wait<0>();
@@ -226,11 +369,12 @@ __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs
             constexpr int NPW = (IB * P + 31) / 32;
             constexpr int IPW = 32 / P;
             unsigned pend[NPW];
+            const bool wn = !SCR || __any_sync(L0S_FULL, (wneed >> (bi & 31)) & 1u);
 #pragma unroll
             for (int pw = 0; pw < NPW; ++pw) {
                 unsigned word = 0u;
 #pragma unroll 1
-                for (int iw = 0; iw < IPW; ++iw) {
+                for (int iw = 0; iw < (wn ? IPW : 0); ++iw) {
                     const int ii = pw * IPW + iw;
                     const int i = ib0 + ii;
                     double acc[P];
@@ -292,8 +436,10 @@ __global__ void __launch_bounds__(256, 1) k_fit4(const __grid_constant__ FitArgs
                 },
                 set_kq);
             __syncthreads();
+            bi = bn;
         }
     }
+    if (SCR && lane == 0 && n_tests && a.n_screen) atomicAdd(a.n_screen, n_tests);
     flush_warp(a, wc, blockIdx.x * NW + warp, lane);
 }
 
@@ -309,9 +455,10 @@ __global__ void k_screen4(const __grid_constant__ FitArgs a, const int64_t* __re
 template <int NT>
 int occupancy4(int nsm) {
     using C = Cfg4<NT>;
-    cudaFuncSetAttribute(k_fit4<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes);
+    cudaFuncSetAttribute(k_fit4<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes);
+    cudaFuncSetAttribute(k_fit4<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit4<NT>, 256, C::smem_bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fit4<NT, false>, 256, C::smem_bytes);
     return nsm * (per_sm < 1 ? 1 : per_sm);
 }
 
@@ -327,7 +474,12 @@ template <int NT>
 int launch4(const FitArgs& a, int nsm, cudaStream_t st) {
     const int grid = occupancy4<NT>(nsm);
     if (a.collect != 1) seed_launch<4, 12>(k_seed_eval4, a, st);
-    k_fit4<NT><<<grid, 256, Cfg4<NT>::smem_bytes, st>>>(a);
+    if (TSK4 && a.tmax) {
+        k_tile_max<Cfg4<NT>::IB><<<dim3((unsigned)((a.m + 256) / 256), (unsigned)((a.m + Cfg4<NT>::IB - 1) / Cfg4<NT>::IB)),
+                                    256, 0, st>>>(a.G, a.iforce, a.m, a.mp, a.T, a.tmax);
+        k_fit4<NT, true><<<grid, 256, Cfg4<NT>::smem_bytes, st>>>(a);
+    }
+    k_fit4<NT, false><<<grid, 256, Cfg4<NT>::smem_bytes, st>>>(a);
     return grid;
 }
 

@@ -449,6 +449,52 @@ __device__ __forceinline__ bool seed_tuple(const FitArgs& a, const SeedSmem& S, 
 }
 
 namespace {
+// Row-block maxima for the tile screen (TSK), blocks of IB rows (the sweep's tile height,
+// aligned at row 0) of the first task slot (the task of largest |y_c|^2, first on ties, as k_fit3
+// orders them; k_fit4 screens the same task): [col][block] max |C[i, col]| over i != col for col <= m (col = m: max |c_i|;
+// the diagonal is left out -- every tile that reaches a lane's own j or k would fail), then
+// [j-block][block] the maximum over the j-block's 32 columns, then the slot's task index.  +inf
+// where a row is iforce-flagged (column m) or an entry is NaN.  One read of one task's Gram.
+template <int IB>
+__global__ void __launch_bounds__(256) k_tile_max(const double* __restrict__ G, const unsigned char* __restrict__ iforce,
+                                                  int64_t m, int64_t mp, int T, double* __restrict__ out) {
+    __shared__ int s_t0;
+    const int64_t nbk = (m + IB - 1) / IB, nJ = (m + 31) / 32;
+    if (threadIdx.x == 0) {
+        int best = 0;
+        double bv = G[m * mp + m];
+        for (int t = 1; t < T; ++t) {
+            const double v = G[(int64_t)t * mp * mp + m * mp + m];
+            if (v > bv) {
+                bv = v;
+                best = t;
+            }
+        }
+        s_t0 = best;
+        if (blockIdx.x == 0 && blockIdx.y == 0) out[(m + 1 + nJ) * nbk] = (double)best;
+    }
+    __syncthreads();
+    const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t b = blockIdx.y;
+    const double* Gt = G + (int64_t)s_t0 * mp * mp;
+    double mx = 0.0;
+    if (col <= m) {
+        bool bad = false;
+        for (int64_t i = b * IB; i < min(b * IB + IB, m); ++i) {
+            if (i == col) continue;  // C_jj = 1: a tuple never repeats a feature (i < j < k ...)
+            const double v = Gt[i * mp + col];
+            bad |= (v != v) || (col == m && iforce[i]);
+            mx = fmax(mx, fabs(v));
+        }
+        if (bad) mx = INFINITY;
+        out[col * nbk + b] = mx;
+    }
+    double jm = col < m ? mx : 0.0;  // warps cover whole j-blocks (blockDim and the x offset are multiples of 32)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) jm = fmax(jm, __shfl_xor_sync(L0S_FULL, jm, o));
+    if ((threadIdx.x & 31) == 0 && col < m) out[(m + 1) * nbk + (col >> 5) * nbk + b] = jm;
+}
+
 // Seed phase 1 (one CTA of 512): the subsets, written to a.seed_tup (-1: outside the rank range).
 template <int N, int F>
 __global__ void __launch_bounds__(512, 1) k_seed_select(const __grid_constant__ FitArgs a) {
