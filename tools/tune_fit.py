@@ -22,8 +22,9 @@ VDIR = os.path.join(ROOT, "paper_2502_20072_b200", "variants")
 
 VARIANTS = {
     "base": (),
-    "warp_only": ("L0S_TSK_CTA=0",),
-    "no_tile_screen": ("L0S_TSKIP=0",),
+    "ich256": ("L0S_ICH4=256",),
+    "ich512": ("L0S_ICH4=512",),
+    "ich1024": ("L0S_ICH4=1024",),
 }
 if os.environ.get("L0S_TUNE_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["L0S_TUNE_ONLY"].split(",")}
