@@ -52,14 +52,32 @@ __device__ __forceinline__ double warp_sum(double v) {
 // p2 = 2^(7 OZ_DIGITS - e) (an exact scaling; |t| < 2^28) and integer field extraction.
 __device__ __forceinline__ unsigned oz_digits(double z, double p2) {
     const int q = __double2int_rz(z * p2);
-    const unsigned au = (unsigned)(q < 0 ? -q : q), neg = q < 0 ? 0xffu : 0u;
-    unsigned w = 0u;
+    const unsigned au = (unsigned)(q < 0 ? -q : q);
+    if constexpr (OZ_DIGITS == 4) {
+        // byte a = 7-bit digit a (most significant first); negative: every byte negated mod 256
+        const unsigned w = ((au >> 21) & 127u) | (((au >> 14) & 127u) << 8) | (((au >> 7) & 127u) << 16) |
+                           ((au & 127u) << 24);
+        return q < 0 ? __vsub4(0u, w) : w;
+    } else {
+        const unsigned neg = q < 0 ? 0xffu : 0u;
+        unsigned w = 0u;
 #pragma unroll
-    for (int a = 0; a < OZ_DIGITS; ++a) {
-        const unsigned d = (au >> (7 * (OZ_DIGITS - 1 - a))) & 127u;
-        w |= (((d ^ neg) + (neg & 1u)) & 0xffu) << (8 * a);  // two's complement byte of -d when negative
+        for (int a = 0; a < OZ_DIGITS; ++a) {
+            const unsigned d = (au >> (7 * (OZ_DIGITS - 1 - a))) & 127u;
+            w |= (((d ^ neg) + (neg & 1u)) & 0xffu) << (8 * a);  // two's complement byte of -d when negative
+        }
+        return w;
     }
-    return w;
+}
+
+// pk[a] = byte a of w[0..3] (a 4 x 4 byte transpose in 8 PRMTs)
+__device__ __forceinline__ void oz_transpose4(const unsigned (&w)[4], unsigned (&pk)[4]) {
+    const unsigned t0 = __byte_perm(w[0], w[1], 0x5140), t1 = __byte_perm(w[0], w[1], 0x7362);
+    const unsigned u0 = __byte_perm(w[2], w[3], 0x5140), u1 = __byte_perm(w[2], w[3], 0x7362);
+    pk[0] = __byte_perm(t0, u0, 0x5410);
+    pk[1] = __byte_perm(t0, u0, 0x7632);
+    pk[2] = __byte_perm(t1, u1, 0x5410);
+    pk[3] = __byte_perm(t1, u1, 0x7632);
 }
 
 // One warp per (row, task) of rows [f0, f1); row m is the property.
@@ -264,13 +282,32 @@ __global__ void __launch_bounds__(SR_THREADS) k_stage_rows(const double* __restr
         const double p2 = finite ? ldexp(1.0, 7 * OZ_DIGITS - e) : 0.0;
         for (int64_t i0 = 4 * (int64_t)tid; i0 < klen; i0 += 4 * SR_THREADS) {
             unsigned pk[OZ_DIGITS] = {};
+            if constexpr (OZ_DIGITS == 4) {
+                // the four segment values as two 16-byte loads (no bank conflicts), digits packed
+                // by a byte transpose
+                double z[4];
+                if (i0 + 3 < r) {
+                    const double2 a01 = *reinterpret_cast<const double2*>(seg + i0);
+                    const double2 a23 = *reinterpret_cast<const double2*>(seg + i0 + 2);
+                    z[0] = (a01.x - mean) * scale, z[1] = (a01.y - mean) * scale;
+                    z[2] = (a23.x - mean) * scale, z[3] = (a23.y - mean) * scale;
+                } else {
 #pragma unroll
-            for (int e4 = 0; e4 < 4; ++e4) {
-                const int64_t i = i0 + e4;
-                const double z = (i < r) ? (seg[i] - mean) * scale : 0.0;
-                const unsigned w = oz_digits(z, p2);
+                    for (int e4 = 0; e4 < 4; ++e4) z[e4] = i0 + e4 < r ? (seg[i0 + e4] - mean) * scale : 0.0;
+                }
+                unsigned w[4];
 #pragma unroll
-                for (int a = 0; a < OZ_DIGITS; ++a) pk[a] |= ((w >> (8 * a)) & 0xffu) << (8 * e4);
+                for (int e4 = 0; e4 < 4; ++e4) w[e4] = oz_digits(z[e4], p2);
+                oz_transpose4(w, pk);
+            } else {
+#pragma unroll
+                for (int e4 = 0; e4 < 4; ++e4) {
+                    const int64_t i = i0 + e4;
+                    const double z = (i < r) ? (seg[i] - mean) * scale : 0.0;
+                    const unsigned w = oz_digits(z, p2);
+#pragma unroll
+                    for (int a = 0; a < OZ_DIGITS; ++a) pk[a] |= ((w >> (8 * a)) & 0xffu) << (8 * e4);
+                }
             }
 #pragma unroll
             for (int a = 0; a < OZ_DIGITS; ++a)
