@@ -1,7 +1,8 @@
 """A small workload touching every kernel family once, for compute-sanitizer (racecheck /
 synccheck / memcheck): screened n = 2, 3, 4 searches (TMA + mbarrier sweeps, seeds, merge),
 the INT8 Ozaki Gram (tcgen05 + TMEM + TMA), the QR screen, the exact kernels, SIS scores and
-the final-rung evaluator, the INT8 Gram fix-up rows and the double-double ill-tuple screen.
+the final-rung evaluator, the INT8 Gram fix-up rows, the double-double ill-tuple screen and
+the tile-screened dim-3 / dim-4 sweeps.
 Checks every result against the oracle."""
 import os
 import sys
@@ -58,6 +59,17 @@ def main():
     got = l0_search(v2, y2, None, L0Config(dimension=4), mode="fast")
     check(got, orc.l0_search(v2, y2, None, 4, 10, "fp64", threads=16))
     del os.environ["L0S_QR_SCREEN"]
+    # the tile-screened sweeps (k_tile_max + k_fit3<.., true>, fit4's screened kernel) on planted
+    # properties, one task (the screen engages: n_screen counts the tile tests)
+    for n, m3, seed in ((3, 200, 31), (4, 100, 32)):
+        r3 = np.random.default_rng(seed)
+        v3 = r3.uniform(0.5, 2.0, size=(m3, 1000))
+        y3 = 2.0 * v3[3] - v3[m3 // 2] + 0.5 * v3[m3 - 9] + (0.3 * v3[m3 // 3] if n == 4 else 0.0) \
+            + 0.01 * r3.standard_normal(1000)
+        st3 = SearchStats()
+        got = l0_search(v3, y3, None, L0Config(dimension=n), stats=st3, mode="fast")
+        check(got, orc.l0_search(v3, y3, None, n, 10, "fp64", threads=16))
+        print(f"tile screen n={n}: n_screen {st3.device.get('n_screen')}", flush=True)
     # SIS scores
     eng = _lib.engine(0)
     eng.sis_prepare(np.stack([y, y ** 2]), np.concatenate(sl), np.array([0, 200, 400]))
