@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(SR_THREADS) k_stage_rows(const double* __restr
     W* dx = f < m ? Xp + f * s + lo : yp + lo;
     // gather (+ the working dtype's rounding, numpy astype) and the first sum
     // (batches of SR_B indices, then SR_B value loads in flight per thread)
-    constexpr int SR_B = 8;
+    constexpr int SR_B = 16;
     double sum = 0.0;
     for (int64_t i0 = tid; i0 < r; i0 += SR_B * SR_THREADS) {
         int64_t src[SR_B];
